@@ -1,0 +1,16 @@
+"""paper_2601_12713_b200 -- B200-native engine for the OMPDataPerf hot path
+(content hashing of mapped buffers + offline trace analysis), a drop-in
+behind the reference analyzer's Python API (dmlens).  See DESIGN.md."""
+from __future__ import annotations
+
+__version__ = "0.1.0"
+
+from .errors import (DeviceOutOfRange, EmptyPayload, EngineError, EngineUnavailable,
+                     FindingsTraceMismatch, InvalidTrace)
+from .hashing import HashFn, hash_batch, hash_bytes, hash_device, hash_tensors, make_hasher
+
+__all__ = [
+    "DeviceOutOfRange", "EmptyPayload", "EngineError", "EngineUnavailable",
+    "FindingsTraceMismatch", "InvalidTrace", "HashFn", "hash_batch", "hash_bytes",
+    "hash_device", "hash_tensors", "make_hasher",
+]

@@ -1,0 +1,242 @@
+// C ABI of libb2l (declared in include/b2l.h): error plumbing, device info,
+// hashing entry points and the host-buffer (end-to-end) hashing pipeline.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "b2l_common.cuh"
+
+namespace b2l {
+
+static thread_local std::string t_last_error;
+
+void set_error(const std::string &msg) { t_last_error = msg; }
+int fail(int code, const std::string &msg) {
+    t_last_error = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char *what) {
+    t_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    return e == cudaErrorMemoryAllocation ? B2L_E_OOM : B2L_E_CUDA;
+}
+
+int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (!cached[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = v > 0 ? v : 148;
+    }
+    return cached[dev];
+}
+
+// defined in b2l_hash.cu
+int hash_batch_launch(const uint64_t *, const uint64_t *, uint64_t, uint64_t *, const uint32_t *, cudaStream_t);
+int hash_launch_info(uint64_t, int *, int *, int *);
+int fill_payloads_launch(uint8_t *, const uint64_t *, const uint64_t *, const uint64_t *, uint64_t, uint64_t,
+                         cudaStream_t);
+
+// ------------------------------------------------------------------ host pipeline
+// Double-buffered device ring: batch b's host->device copy (side stream) overlaps
+// batch b-1's hashing (compute stream).  Contiguous host buffers are merged into
+// one DMA.  One pipeline per device, serialized by a mutex.
+namespace {
+
+constexpr uint64_t RING_SLOT_BYTES = 512ull << 20;
+
+struct Slot {
+    uint8_t *d_data = nullptr;
+    uint64_t cap = 0;
+    uint64_t *h_meta = nullptr;  // pinned: [ptrs | lens] for the batch
+    uint32_t *h_order = nullptr;
+    uint64_t *d_meta = nullptr;
+    uint32_t *d_order = nullptr;
+    uint64_t meta_cap = 0;
+    cudaEvent_t copied = nullptr, hashed = nullptr;
+    bool used = false;
+};
+
+struct HostPipe {
+    int device = -1;
+    cudaStream_t copy = nullptr, comp = nullptr;
+    Slot slot[2];
+    uint64_t *d_digests = nullptr;
+    uint64_t dig_cap = 0;
+};
+
+std::mutex g_pipe_mu;
+HostPipe g_pipes[64];
+
+int ensure_slot(Slot &s, uint64_t data_bytes, uint64_t nbuf) {
+    if (!s.copied) {
+        B2L_CUDA(cudaEventCreateWithFlags(&s.copied, cudaEventDisableTiming));
+        B2L_CUDA(cudaEventCreateWithFlags(&s.hashed, cudaEventDisableTiming));
+    }
+    if (s.cap < data_bytes) {
+        if (s.used) B2L_CUDA(cudaEventSynchronize(s.hashed));
+        if (s.d_data) cudaFree(s.d_data);
+        s.d_data = nullptr;
+        s.cap = 0;
+        B2L_CUDA(cudaMalloc(&s.d_data, data_bytes));
+        s.cap = data_bytes;
+    }
+    if (s.meta_cap < nbuf) {
+        if (s.used) B2L_CUDA(cudaEventSynchronize(s.hashed));
+        if (s.h_meta) cudaFreeHost(s.h_meta);
+        if (s.h_order) cudaFreeHost(s.h_order);
+        if (s.d_meta) cudaFree(s.d_meta);
+        if (s.d_order) cudaFree(s.d_order);
+        s.h_meta = nullptr;
+        s.h_order = nullptr;
+        s.d_meta = nullptr;
+        s.d_order = nullptr;
+        s.meta_cap = 0;
+        uint64_t cap = std::max<uint64_t>(nbuf, 4096);
+        B2L_CUDA(cudaMallocHost(&s.h_meta, 2 * cap * sizeof(uint64_t)));
+        B2L_CUDA(cudaMallocHost(&s.h_order, cap * sizeof(uint32_t)));
+        B2L_CUDA(cudaMalloc(&s.d_meta, 2 * cap * sizeof(uint64_t)));
+        B2L_CUDA(cudaMalloc(&s.d_order, cap * sizeof(uint32_t)));
+        s.meta_cap = cap;
+    }
+    return B2L_OK;
+}
+
+inline uint64_t span_bytes(uint64_t start, uint64_t len) { return len + (start & 15) + 16; }
+
+}  // namespace
+
+int hash_host_impl(const void *const *h_bufs, const uint64_t *h_lens, uint64_t n, uint64_t *h_digests) {
+    if (n == 0) return B2L_OK;
+    if (!h_bufs || !h_lens || !h_digests) return fail(B2L_E_INVALID_ARG, "b2l_hash_host: null array");
+    int dev = 0;
+    B2L_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return fail(B2L_E_INVALID_ARG, "device ordinal out of range");
+    std::lock_guard<std::mutex> lock(g_pipe_mu);
+    HostPipe &P = g_pipes[dev];
+    if (!P.copy) {
+        B2L_CUDA(cudaStreamCreateWithFlags(&P.copy, cudaStreamNonBlocking));
+        B2L_CUDA(cudaStreamCreateWithFlags(&P.comp, cudaStreamNonBlocking));
+        P.device = dev;
+    }
+    if (P.dig_cap < n) {
+        if (P.d_digests) cudaFree(P.d_digests);
+        P.d_digests = nullptr;
+        P.dig_cap = 0;
+        B2L_CUDA(cudaMalloc(&P.d_digests, n * sizeof(uint64_t)));
+        P.dig_cap = n;
+    }
+    bool any_empty = false;
+    uint64_t i0 = 0;
+    int cur = 0;
+    while (i0 < n) {
+        // ---- form batch [i0, i1): fits one ring slot (a single oversized buffer gets its own, grown slot)
+        uint64_t i1 = i0, bytes = 0;
+        while (i1 < n) {
+            uint64_t sb = span_bytes((uint64_t)h_bufs[i1], h_lens[i1]);
+            if (i1 > i0 && bytes + sb > RING_SLOT_BYTES) break;
+            bytes += sb;
+            ++i1;
+        }
+        const uint64_t nb = i1 - i0;
+        Slot &S = P.slot[cur];
+        int rc = ensure_slot(S, std::max(bytes, RING_SLOT_BYTES), nb);
+        if (rc) return rc;
+        if (S.used) B2L_CUDA(cudaEventSynchronize(S.hashed));  // ring slot + pinned meta free again
+        // ---- copy plan: merge host-contiguous runs into one DMA, keep (addr mod 16) in the ring
+        uint64_t *mp = S.h_meta, *ml = S.h_meta + nb;
+        uint64_t off = 0;
+        bool uniform = true;
+        for (uint64_t k = i0; k < i1;) {
+            uint64_t run_start = (uint64_t)h_bufs[k];
+            uint64_t run_end = run_start + h_lens[k];
+            uint64_t e = k + 1;
+            while (e < i1 && (uint64_t)h_bufs[e] == run_end) run_end += h_lens[e++];
+            off = ((off + 15) & ~15ull) + (run_start & 15);
+            uint8_t *dst = S.d_data + off;
+            if (run_end > run_start)
+                B2L_CUDA(cudaMemcpyAsync(dst, (const void *)run_start, run_end - run_start, cudaMemcpyHostToDevice,
+                                         P.copy));
+            for (uint64_t j = k; j < e; ++j) {
+                mp[j - i0] = (uint64_t)dst + ((uint64_t)h_bufs[j] - run_start);
+                ml[j - i0] = h_lens[j];
+                if (h_lens[j] == 0) any_empty = true;
+                if (h_lens[j] != h_lens[i0]) uniform = false;
+            }
+            off += run_end - run_start;
+            k = e;
+        }
+        const uint32_t *d_order = nullptr;
+        if (!uniform) {  // longest-first processing order (static LPT over lanes)
+            std::iota(S.h_order, S.h_order + nb, 0u);
+            std::stable_sort(S.h_order, S.h_order + nb, [&](uint32_t a, uint32_t b) { return ml[a] > ml[b]; });
+            B2L_CUDA(cudaMemcpyAsync(S.d_order, S.h_order, nb * sizeof(uint32_t), cudaMemcpyHostToDevice, P.copy));
+            d_order = S.d_order;
+        }
+        B2L_CUDA(cudaMemcpyAsync(S.d_meta, S.h_meta, 2 * nb * sizeof(uint64_t), cudaMemcpyHostToDevice, P.copy));
+        B2L_CUDA(cudaEventRecord(S.copied, P.copy));
+        B2L_CUDA(cudaStreamWaitEvent(P.comp, S.copied, 0));
+        rc = hash_batch_launch(S.d_meta, S.d_meta + nb, nb, P.d_digests + i0, d_order, P.comp);
+        if (rc) return rc;
+        B2L_CUDA(cudaEventRecord(S.hashed, P.comp));
+        S.used = true;
+        i0 = i1;
+        cur ^= 1;
+    }
+    B2L_CUDA(cudaMemcpyAsync(h_digests, P.d_digests, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, P.comp));
+    B2L_CUDA(cudaStreamSynchronize(P.comp));
+    if (any_empty) return fail(B2L_E_EMPTY_PAYLOAD, "cannot hash a zero-byte payload");
+    return B2L_OK;
+}
+
+}  // namespace b2l
+
+// =================================================================== extern "C"
+extern "C" {
+
+int b2l_abi_version(void) { return B2L_ABI_VERSION; }
+
+const char *b2l_last_error(void) { return b2l::t_last_error.c_str(); }
+
+int b2l_device_count(int *count) {
+    if (!count) return b2l::fail(B2L_E_INVALID_ARG, "null count");
+    cudaError_t e = cudaGetDeviceCount(count);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return b2l::cuda_fail(e, "cudaGetDeviceCount");
+    }
+    return B2L_OK;
+}
+
+int b2l_hash_batch(const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n, uint64_t *d_digests,
+                   const uint32_t *d_order, void *stream) {
+    return b2l::hash_batch_launch(d_ptrs, d_lens, n, d_digests, d_order, (cudaStream_t)stream);
+}
+
+int b2l_hash_host(const void *const *h_bufs, const uint64_t *h_lens, uint64_t n, uint64_t *h_digests) {
+    return b2l::hash_host_impl(h_bufs, h_lens, n, h_digests);
+}
+
+int b2l_hash_bytes(const void *h_buf, uint64_t len, uint64_t *digest) {
+    if (!digest) return b2l::fail(B2L_E_INVALID_ARG, "null digest");
+    if (len == 0) return b2l::fail(B2L_E_EMPTY_PAYLOAD, "cannot hash a zero-byte payload");
+    if (!h_buf) return b2l::fail(B2L_E_INVALID_ARG, "null payload");
+    const void *bufs[1] = {h_buf};
+    return b2l::hash_host_impl(bufs, &len, 1, digest);
+}
+
+int b2l_fill_payloads(uint8_t *d_base, const uint64_t *d_offsets, const uint64_t *d_lens,
+                      const uint64_t *d_content_ids, uint64_t n, uint64_t seed, void *stream) {
+    if (!d_base || !d_offsets || !d_lens || !d_content_ids) return b2l::fail(B2L_E_INVALID_ARG, "null array");
+    return b2l::fill_payloads_launch(d_base, d_offsets, d_lens, d_content_ids, n, seed, (cudaStream_t)stream);
+}
+
+int b2l_hash_launch_info(uint64_t n, int *grid, int *block, int *smem_bytes) {
+    return b2l::hash_launch_info(n, grid, block, smem_bytes);
+}
+
+}  // extern "C"
