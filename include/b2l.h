@@ -78,6 +78,11 @@ int b2l_hash_bytes(const void *h_buf, uint64_t len, uint64_t *digest);
 int b2l_fill_payloads(uint8_t *d_base, const uint64_t *d_offsets, const uint64_t *d_lens,
                       const uint64_t *d_content_ids, uint64_t n, uint64_t seed, void *stream);
 
+/* Kernel variant selection (tuning / tests): variant -1 only reports the
+ * number of variants in *count, -2 restores the default (the tuned variant,
+ * DESIGN.md K1).  Process-wide. */
+int b2l_hash_select_variant(int variant, int *count);
+
 /* Device-side occupancy/launch info of the hash kernel (diagnostics). */
 int b2l_hash_launch_info(uint64_t n, int *grid, int *block, int *smem_bytes);
 

@@ -38,6 +38,7 @@ int sm_count() {
 // defined in b2l_hash.cu
 int hash_batch_launch(const uint64_t *, const uint64_t *, uint64_t, uint64_t *, const uint32_t *, cudaStream_t);
 int hash_launch_info(uint64_t, int *, int *, int *);
+int hash_select_variant(int, int *);
 int fill_payloads_launch(uint8_t *, const uint64_t *, const uint64_t *, const uint64_t *, uint64_t, uint64_t,
                          cudaStream_t);
 
@@ -234,6 +235,8 @@ int b2l_fill_payloads(uint8_t *d_base, const uint64_t *d_offsets, const uint64_t
     if (!d_base || !d_offsets || !d_lens || !d_content_ids) return b2l::fail(B2L_E_INVALID_ARG, "null array");
     return b2l::fill_payloads_launch(d_base, d_offsets, d_lens, d_content_ids, n, seed, (cudaStream_t)stream);
 }
+
+int b2l_hash_select_variant(int variant, int *count) { return b2l::hash_select_variant(variant, count); }
 
 int b2l_hash_launch_info(uint64_t n, int *grid, int *block, int *smem_bytes) {
     return b2l::hash_launch_info(n, grid, block, smem_bytes);

@@ -79,6 +79,17 @@ __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t h) {
     return h;
 }
 __host__ __device__ __forceinline__ uint64_t fnv_step(uint64_t h, uint64_t w) { return (h ^ w) * FNV_PRIME; }
+// One FNV step on 32-bit halves.  P = 2^40 + 435, so
+//   lo' = lo32(xl*435),  hi' = xh*435 + hi32(xl*435) + (xl << 8)
+// and the hi recurrence is one IMAD (xh*435 + c) whose addend c comes off the lo chain.
+__device__ __forceinline__ void fnv_step32(uint32_t &hl, uint32_t &hh, uint32_t wl, uint32_t wh) {
+    const uint32_t xl = hl ^ wl, xh = hh ^ wh;
+    const uint64_t p = (uint64_t)xl * 435u;
+    const uint32_t c = (uint32_t)(p >> 32) + (xl << 8);
+    hl = (uint32_t)p;
+    // keep the hi recurrence a single IMAD on the critical path (stop re-association)
+    asm("mad.lo.u32 %0, %1, 435, %2;" : "=r"(hh) : "r"(xh), "r"(c));
+}
 __host__ __device__ __forceinline__ uint64_t finish_digest(uint64_t h, uint64_t n) {
     h = fmix64(h ^ n);
     return h ? h : 1ull;

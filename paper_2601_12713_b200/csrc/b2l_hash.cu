@@ -15,13 +15,14 @@
 // shift when start % 8 != 0.  Reads never leave the 16-B aligned segments
 // that contain buffer bytes, so they never cross a page the buffer does not
 // touch.
+#include <cstdlib>
+
 #include "b2l_common.cuh"
 
 namespace b2l {
 
 namespace {
 
-constexpr int HASH_THREADS = 128;
 
 struct BufCursor {
     uint64_t idx;    // buffer index (for digests) ; UINT64_MAX = exhausted
@@ -50,60 +51,120 @@ __device__ __forceinline__ void cursor_load(BufCursor &c, const uint64_t *__rest
     c.pos = 0;
 }
 
-template <int CH, int S>
+// Hash one staged chunk (`bytes` stream bytes starting at stream offset cs.pos) into (h, prev).
+// Word j of the payload is stream u64 q = q0 + j, or -- when start % 8 != 0 -- the funnel of
+// stream u64s (q0+j, q0+j+1), emitted at q0+j+1.
+template <int CH>
+__device__ __forceinline__ void consume_chunk(const BufCursor &cs, uint32_t bytes, const uint4 *__restrict__ src,
+                                              uint64_t &h, uint64_t &prev) {
+    const uint32_t r = cs.m & 7u;
+    const uint64_t qb = (cs.m >> 3) + (r ? 1 : 0);
+    const uint64_t nw = (cs.n + 7) >> 3;
+    const uint64_t qe = qb + nw;  // exclusive
+    const uint64_t qc = cs.pos >> 3;
+    const uint32_t nu = bytes >> 3;
+    const bool interior = qc >= qb && qc + nu < qe && cs.pos + bytes < cs.L;  // full, not the last chunk
+    if (r == 0 && interior) {
+        uint32_t hl = (uint32_t)h, hh = (uint32_t)(h >> 32);
+#pragma unroll 8
+        for (uint32_t i = 0; i < (uint32_t)CH / 16; ++i) {
+            uint4 v = src[i];
+            fnv_step32(hl, hh, v.x, v.y);
+            fnv_step32(hl, hh, v.z, v.w);
+        }
+        h = ((uint64_t)hh << 32) | hl;
+    } else if (r != 0 && interior) {
+        const uint32_t sh = r * 8;
+        uint32_t hl = (uint32_t)h, hh = (uint32_t)(h >> 32);
+#pragma unroll 4
+        for (uint32_t i = 0; i < (uint32_t)CH / 16; ++i) {
+            uint4 v = src[i];
+            uint64_t u0 = ((uint64_t)v.y << 32) | v.x, u1 = ((uint64_t)v.w << 32) | v.z;
+            uint64_t w0 = (prev >> sh) | (u0 << (64 - sh));
+            uint64_t w1 = (u0 >> sh) | (u1 << (64 - sh));
+            fnv_step32(hl, hh, (uint32_t)w0, (uint32_t)(w0 >> 32));
+            fnv_step32(hl, hh, (uint32_t)w1, (uint32_t)(w1 >> 32));
+            prev = u1;
+        }
+        h = ((uint64_t)hh << 32) | hl;
+    } else {
+        const uint32_t sh = r * 8;
+        const uint32_t tailb = (uint32_t)(cs.n & 7);
+        for (uint32_t i = 0; i < nu; ++i) {
+            const uint32_t *p32 = reinterpret_cast<const uint32_t *>(src) + 2 * i;
+            uint64_t u = ((uint64_t)p32[1] << 32) | p32[0];
+            uint64_t q = qc + i;
+            if (q >= qb && q < qe) {
+                uint64_t w = r ? ((prev >> sh) | (u << (64 - sh))) : u;
+                if (q == qe - 1 && tailb) w &= (1ull << (8 * tailb)) - 1;
+                h = fnv_step(h, w);
+            }
+            prev = u;
+        }
+        // misaligned payload whose last (partial) word lies wholly inside the final stream
+        // u64: the stream ends before that word's emission point -- emit it here.
+        if (r && qc + nu == (cs.L >> 3) && qe > (cs.L >> 3))
+            h = fnv_step(h, (prev >> sh) & ((1ull << (8 * tailb)) - 1));
+    }
+}
+
+__device__ __forceinline__ uint32_t chunk_bytes(const BufCursor &c, int ch) {
+    uint64_t rem = c.L - c.pos;
+    return rem < (uint64_t)ch ? (uint32_t)rem : (uint32_t)ch;
+}
+
+// ============================================================================ variant A
+// Per-lane TMA ring: each lane issues its own cp.async.bulk per chunk (ptxas serialises the
+// 32 lanes' bulk copies in a uniform-register loop), completion on a per-lane mbarrier.
+template <int NT, int CH, int S>
 struct HashSmem {
     static constexpr int SLOT = CH + 16;  // stride == 16 mod 128: conflict-free LDS.128 across 8 lanes
-    static constexpr size_t data_bytes = (size_t)S * HASH_THREADS * SLOT;
-    static constexpr size_t bytes = data_bytes + (size_t)S * HASH_THREADS * sizeof(uint64_t);
+    static constexpr size_t data_bytes = (size_t)S * NT * SLOT;
+    static constexpr size_t bytes = data_bytes + (size_t)S * NT * sizeof(uint64_t);
 };
 
-template <int CH, int S>
-__global__ void __launch_bounds__(HASH_THREADS) k_hash_seq(const uint64_t *__restrict__ ptrs,
-                                                           const uint64_t *__restrict__ lens,
-                                                           const uint32_t *__restrict__ order, uint64_t n_bufs,
-                                                           uint64_t *__restrict__ digests) {
-    using SM = HashSmem<CH, S>;
+template <int NT, int CH, int S>
+__global__ void __launch_bounds__(NT) k_hash_seq(const uint64_t *__restrict__ ptrs, const uint64_t *__restrict__ lens,
+                                                 const uint32_t *__restrict__ order, uint64_t n_bufs,
+                                                 uint64_t *__restrict__ digests) {
+    using SM = HashSmem<NT, CH, S>;
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + SM::data_bytes);
     const int tid = threadIdx.x;
-    const uint64_t T = (uint64_t)gridDim.x * HASH_THREADS;
-    const uint64_t g = (uint64_t)blockIdx.x * HASH_THREADS + tid;
+    const uint64_t T = (uint64_t)gridDim.x * NT;
+    const uint64_t g = (uint64_t)blockIdx.x * NT + tid;
 
 #pragma unroll
-    for (int s = 0; s < S; ++s) mbar_init(&bars[s * HASH_THREADS + tid], 1);
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s * NT + tid], 1);
     fence_mbar_init();
     __syncthreads();
 
     const uint64_t policy = l2_policy_evict_first();
-    auto slot_ptr = [&](int s) { return smem + ((size_t)s * HASH_THREADS + tid) * SM::SLOT; };
+    auto slot_ptr = [&](int s) { return smem + ((size_t)s * NT + tid) * SM::SLOT; };
 
-    // ---------------- loader (runs S chunks ahead of the consumer)
-    BufCursor ld;
+    BufCursor ld;  // loader: S chunks ahead of the consumer
     uint64_t ld_k = g;
     cursor_load(ld, ptrs, lens, order, ld_k, n_bufs);
     auto issue = [&](int s) {
-        while (ld.idx != ~0ull && ld.pos >= ld.L) {  // finished or empty buffer: advance
+        while (ld.idx != ~0ull && ld.pos >= ld.L) {
             ld_k += T;
             cursor_load(ld, ptrs, lens, order, ld_k, n_bufs);
         }
         if (ld.idx == ~0ull) return;
-        uint64_t rem = ld.L - ld.pos;
-        uint32_t bytes = rem < (uint64_t)CH ? (uint32_t)rem : (uint32_t)CH;
-        uint64_t *bar = &bars[s * HASH_THREADS + tid];
+        const uint32_t bytes = chunk_bytes(ld, CH);
+        uint64_t *bar = &bars[s * NT + tid];
         mbar_expect_tx(bar, bytes);
         bulk_g2s(slot_ptr(s), reinterpret_cast<const void *>(ld.a0 + ld.pos), bytes, bar, policy);
         ld.pos += bytes;
     };
-
 #pragma unroll
     for (int s = 0; s < S; ++s) issue(s);
 
-    // ---------------- consumer
     BufCursor cs;
     uint64_t cs_k = g;
     cursor_load(cs, ptrs, lens, order, cs_k, n_bufs);
     uint64_t h = FNV_OFFSET, prev = 0;
-    uint32_t phase_bits = 0;  // bit s = parity to wait for on slot s
+    uint32_t phase_bits = 0;
     int s = 0;
     while (cs.idx != ~0ull) {
         if (cs.L == 0) {  // zero-length payload: reserved digest 0 (host raises EmptyPayload)
@@ -112,45 +173,11 @@ __global__ void __launch_bounds__(HASH_THREADS) k_hash_seq(const uint64_t *__res
             cursor_load(cs, ptrs, lens, order, cs_k, n_bufs);
             continue;
         }
-        uint64_t rem = cs.L - cs.pos;
-        const uint32_t bytes = rem < (uint64_t)CH ? (uint32_t)rem : (uint32_t)CH;
-        mbar_wait(&bars[s * HASH_THREADS + tid], (phase_bits >> s) & 1u);
+        const uint32_t bytes = chunk_bytes(cs, CH);
+        mbar_wait(&bars[s * NT + tid], (phase_bits >> s) & 1u);
         phase_bits ^= 1u << s;
-
-        // word j of the payload lives at stream u64 q = q0 + j (+1 when misaligned, via funnel)
-        const uint32_t r = cs.m & 7u;
-        const uint64_t qb = (cs.m >> 3) + (r ? 1 : 0);
-        const uint64_t nw = (cs.n + 7) >> 3;
-        const uint64_t qe = qb + nw;  // exclusive
-        const uint64_t qc = cs.pos >> 3;  // first stream u64 of this chunk
-        const uint32_t nu = bytes >> 3;
-        const uint4 *src = reinterpret_cast<const uint4 *>(slot_ptr(s));
-        if (r == 0 && qc >= qb && qc + nu < qe) {
-            // interior chunk, aligned: every u64 is a full payload word
-#pragma unroll 8
-            for (uint32_t i = 0; i < (uint32_t)CH / 16; ++i) {  // interior chunks are always full
-                uint4 v = src[i];
-                h = fnv_step(h, ((uint64_t)v.y << 32) | v.x);
-                h = fnv_step(h, ((uint64_t)v.w << 32) | v.z);
-            }
-            prev = 0;
-        } else {
-            const uint32_t sh = r * 8;
-            const uint32_t tailb = (uint32_t)(cs.n & 7);
-            for (uint32_t i = 0; i < nu; ++i) {
-                const uint32_t *p32 = reinterpret_cast<const uint32_t *>(src) + 2 * i;
-                uint64_t u = ((uint64_t)p32[1] << 32) | p32[0];
-                uint64_t q = qc + i;
-                if (q >= qb && q < qe) {
-                    uint64_t w = r ? ((prev >> sh) | (u << (64 - sh))) : u;
-                    if (q == qe - 1 && tailb) w &= (1ull << (8 * tailb)) - 1;
-                    h = fnv_step(h, w);
-                }
-                prev = u;
-            }
-        }
+        consume_chunk<CH>(cs, bytes, reinterpret_cast<const uint4 *>(slot_ptr(s)), h, prev);
         cs.pos += bytes;
-        // refill this slot before finishing the buffer so the copy is in flight during the epilogue
         issue(s);
         s = (s + 1 == S) ? 0 : s + 1;
         if (cs.pos >= cs.L) {
@@ -163,33 +190,169 @@ __global__ void __launch_bounds__(HASH_THREADS) k_hash_seq(const uint64_t *__res
     }
 }
 
-// Chosen configuration: 128 lanes per CTA, 256-B chunks, 4-deep ring.
-constexpr int CFG_CH = 256;
-constexpr int CFG_S = 4;
-using CfgSmem = HashSmem<CFG_CH, CFG_S>;
+// ============================================================================ variant B
+// Warp-cooperative ring: a warp moves the 32 lanes' next chunks with coalesced 16-B
+// cp.async (LDGSTS, L1 bypass) -- each warp instruction covers 512 contiguous-per-buffer
+// bytes of 32*16/CH buffers -- S-1 rounds ahead of the round being hashed.  No per-lane
+// copy descriptors, so many more chains fit per SM than in variant A.
+template <int WARPS, int CH, int S>
+struct CoopSmem {
+    static constexpr int SLOT = CH + 16;
+    static constexpr size_t warp_bytes = (size_t)S * 32 * SLOT;
+    static constexpr size_t bytes = warp_bytes * WARPS;
+};
 
-int g_hash_ctas_per_sm = -1;
-
-int hash_ctas_per_sm() {
-    if (g_hash_ctas_per_sm < 0) {
-        auto kern = k_hash_seq<CFG_CH, CFG_S>;
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CfgSmem::bytes) !=
-            cudaSuccess)
-            return -1;
-        int nb = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, HASH_THREADS, CfgSmem::bytes) != cudaSuccess)
-            return -1;
-        g_hash_ctas_per_sm = nb > 0 ? nb : 1;
-    }
-    return g_hash_ctas_per_sm;
+__device__ __forceinline__ void cp_async16(uint32_t dst, uint64_t src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-void hash_grid(uint64_t n, int &grid) {
-    int per_sm = hash_ctas_per_sm();
-    uint64_t max_ctas = (uint64_t)sm_count() * (uint64_t)(per_sm > 0 ? per_sm : 1);
-    uint64_t need = (n + HASH_THREADS - 1) / HASH_THREADS;
-    grid = (int)(need < max_ctas ? need : max_ctas);
-    if (grid < 1) grid = 1;
+template <int WARPS, int CH, int S>
+__global__ void __launch_bounds__(WARPS * 32) k_hash_coop(const uint64_t *__restrict__ ptrs,
+                                                          const uint64_t *__restrict__ lens,
+                                                          const uint32_t *__restrict__ order, uint64_t n_bufs,
+                                                          uint64_t *__restrict__ digests) {
+    static_assert(CH % 128 == 0 && CH <= 512 && S >= 2, "chunk must be 128..512 B");
+    using SM = CoopSmem<WARPS, CH, S>;
+    constexpr int PIECES = CH / 16;            // 16-B pieces per chunk
+    constexpr int PER_INSTR = 32 / PIECES;     // chunks moved per warp instruction
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t T = (uint64_t)gridDim.x * WARPS * 32;
+    const uint64_t g = ((uint64_t)blockIdx.x * WARPS + warp) * 32 + lane;
+    uint8_t *wbase = smem + warp * SM::warp_bytes;
+    const uint32_t wbase_s = smem_u32(wbase);
+
+    BufCursor ld;
+    uint64_t ld_k = g;
+    cursor_load(ld, ptrs, lens, order, ld_k, n_bufs);
+    auto issue_round = [&](int stage) {
+        while (ld.idx != ~0ull && ld.pos >= ld.L) {
+            ld_k += T;
+            cursor_load(ld, ptrs, lens, order, ld_k, n_bufs);
+        }
+        uint64_t my_addr = 0;
+        uint32_t my_bytes = 0;
+        if (ld.idx != ~0ull) {
+            my_bytes = chunk_bytes(ld, CH);
+            my_addr = ld.a0 + ld.pos;
+            ld.pos += my_bytes;
+        }
+        const int p = lane % PIECES;
+#pragma unroll
+        for (int i = 0; i < PIECES; ++i) {
+            const int j = i * PER_INSTR + lane / PIECES;
+            const uint64_t a = __shfl_sync(0xffffffffu, my_addr, j);
+            const uint32_t b = __shfl_sync(0xffffffffu, my_bytes, j);
+            if ((uint32_t)(16 * p) < b)
+                cp_async16(wbase_s + (uint32_t)((stage * 32 + j) * SM::SLOT + 16 * p), a + 16 * p);
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) issue_round(s);
+
+    BufCursor cs;
+    uint64_t cs_k = g;
+    cursor_load(cs, ptrs, lens, order, cs_k, n_bufs);
+    uint64_t h = FNV_OFFSET, prev = 0;
+    int stage = 0;
+    for (;;) {
+        while (cs.idx != ~0ull && cs.L == 0) {  // zero-length payloads take no round
+            digests[cs.idx] = 0;
+            cs_k += T;
+            cursor_load(cs, ptrs, lens, order, cs_k, n_bufs);
+        }
+        if (!__any_sync(0xffffffffu, cs.idx != ~0ull)) break;
+        cp_async_wait<S - 2>();
+        __syncwarp();
+        issue_round(stage == 0 ? S - 1 : stage - 1);
+        if (cs.idx != ~0ull) {
+            const uint32_t bytes = chunk_bytes(cs, CH);
+            consume_chunk<CH>(cs, bytes, reinterpret_cast<const uint4 *>(wbase + (stage * 32 + lane) * SM::SLOT), h,
+                              prev);
+            cs.pos += bytes;
+            if (cs.pos >= cs.L) {
+                digests[cs.idx] = finish_digest(h, cs.n);
+                h = FNV_OFFSET;
+                prev = 0;
+                cs_k += T;
+                cursor_load(cs, ptrs, lens, order, cs_k, n_bufs);
+            }
+        }
+        stage = (stage + 1 == S) ? 0 : stage + 1;
+    }
+    cp_async_wait<0>();
+}
+
+// Launch configurations (lanes per CTA, chunk bytes, ring depth).  Selected at
+// first use; B2L_HASH_CFG=<i> overrides (used by the tuning sweep).
+struct HashCfg {
+    int nt, ch, s;
+    size_t smem;
+    const void *fn;
+};
+template <int NT, int CH, int S>
+HashCfg make_tma() {
+    return HashCfg{NT, CH, S, HashSmem<NT, CH, S>::bytes, (const void *)k_hash_seq<NT, CH, S>};
+}
+template <int W, int CH, int S>
+HashCfg make_coop() {
+    return HashCfg{W * 32, CH, S, CoopSmem<W, CH, S>::bytes, (const void *)k_hash_coop<W, CH, S>};
+}
+const HashCfg *cfg_table(int &count) {
+    static const HashCfg tab[] = {
+        make_coop<4, 128, 3>(),  make_coop<4, 256, 2>(), make_coop<4, 128, 4>(), make_coop<2, 256, 3>(),
+        make_coop<8, 128, 3>(),  make_coop<4, 256, 3>(), make_coop<2, 512, 2>(), make_coop<1, 128, 3>(),
+        make_tma<128, 384, 3>(), make_tma<128, 256, 4>(), make_tma<96, 512, 3>(),
+    };
+    count = (int)(sizeof(tab) / sizeof(tab[0]));
+    return tab;
+}
+constexpr int DEFAULT_CFG = 6;  // coop<2 warps, 512 B, 2 stages>: 96.5% of measured HBM on C2 (r01 sweep)
+
+struct HashLaunch {
+    int cfg = -1;
+    int ctas_per_sm = 0;
+};
+HashLaunch g_launch[64];
+int setenv_variant = -1;  // b2l_hash_select_variant override
+
+const HashCfg *active_cfg(int &ctas_per_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    HashLaunch &L = g_launch[dev & 63];
+    int count;
+    const HashCfg *tab = cfg_table(count);
+    if (L.cfg < 0) {
+        int c = DEFAULT_CFG;
+        if (const char *e = getenv("B2L_HASH_CFG")) {
+            int v = atoi(e);
+            if (v >= 0 && v < count) c = v;
+        }
+        if (setenv_variant >= 0) c = setenv_variant;
+        if (cudaFuncSetAttribute(tab[c].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab[c].smem) !=
+            cudaSuccess)
+            return nullptr;
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tab[c].fn, tab[c].nt, tab[c].smem) != cudaSuccess)
+            return nullptr;
+        L.ctas_per_sm = nb > 0 ? nb : 1;
+        L.cfg = c;
+    }
+    ctas_per_sm = L.ctas_per_sm;
+    return &tab[L.cfg];
+}
+
+int hash_grid(const HashCfg &c, int per_sm, uint64_t n) {
+    uint64_t max_ctas = (uint64_t)sm_count() * (uint64_t)per_sm;
+    uint64_t need = (n + c.nt - 1) / c.nt;
+    uint64_t g = need < max_ctas ? need : max_ctas;
+    return g < 1 ? 1 : (int)g;
 }
 
 // ---------------------------------------------------------------- synthetic payloads
@@ -234,22 +397,33 @@ int hash_batch_launch(const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n
                       const uint32_t *d_order, cudaStream_t stream) {
     if (n == 0) return B2L_OK;
     if (!d_ptrs || !d_lens || !d_digests) return fail(B2L_E_INVALID_ARG, "b2l_hash_batch: null array");
-    if (hash_ctas_per_sm() < 0) return fail(B2L_E_CUDA, "b2l_hash_batch: cannot configure hash kernel");
-    int grid;
-    hash_grid(n, grid);
-    k_hash_seq<CFG_CH, CFG_S><<<grid, HASH_THREADS, CfgSmem::bytes, stream>>>(d_ptrs, d_lens, d_order, n,
-                                                                               d_digests);
-    B2L_CHECK_LAUNCH("k_hash_seq launch");
+    int per_sm = 0;
+    const HashCfg *c = active_cfg(per_sm);
+    if (!c) return fail(B2L_E_CUDA, "b2l_hash_batch: cannot configure hash kernel");
+    int grid = hash_grid(*c, per_sm, n);
+    void *args[] = {(void *)&d_ptrs, (void *)&d_lens, (void *)&d_order, (void *)&n, (void *)&d_digests};
+    B2L_CUDA(cudaLaunchKernel(c->fn, dim3(grid), dim3(c->nt), args, c->smem, stream));
+    return B2L_OK;
+}
+
+int hash_select_variant(int v, int *count) {
+    int n;
+    cfg_table(n);
+    if (count) *count = n;
+    if (v == -1) return B2L_OK;  // query only
+    if (v >= n || v < -2) return fail(B2L_E_INVALID_ARG, "hash variant out of range");
+    for (auto &L : g_launch) L.cfg = -1;
+    setenv_variant = v == -2 ? -1 : v;  // -2: back to the default
     return B2L_OK;
 }
 
 int hash_launch_info(uint64_t n, int *grid, int *block, int *smem) {
-    if (hash_ctas_per_sm() < 0) return fail(B2L_E_CUDA, "hash kernel configuration failed");
-    int gr;
-    hash_grid(n, gr);
-    if (grid) *grid = gr;
-    if (block) *block = HASH_THREADS;
-    if (smem) *smem = (int)CfgSmem::bytes;
+    int per_sm = 0;
+    const HashCfg *c = active_cfg(per_sm);
+    if (!c) return fail(B2L_E_CUDA, "hash kernel configuration failed");
+    if (grid) *grid = hash_grid(*c, per_sm, n);
+    if (block) *block = c->nt;
+    if (smem) *smem = (int)c->smem;
     return B2L_OK;
 }
 

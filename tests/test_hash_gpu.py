@@ -63,6 +63,40 @@ def test_every_length_1_to_4096_device_and_host(cuda):
     assert hash_batch(payloads) == want
 
 
+def _variants():
+    import ctypes
+    from paper_2601_12713_b200 import _lib
+    n = ctypes.c_int(0)
+    _lib.check(_lib.lib().b2l_hash_select_variant(-1, ctypes.byref(n)))
+    return list(range(n.value))
+
+
+@pytest.fixture(params=range(16))
+def variant(request, cuda):
+    from paper_2601_12713_b200 import _lib
+    if request.param >= len(_variants()):
+        pytest.skip("no such variant")
+    _lib.check(_lib.lib().b2l_hash_select_variant(request.param, None))
+    yield request.param
+    _lib.check(_lib.lib().b2l_hash_select_variant(-2, None))
+
+
+def test_all_variants_misaligned_ragged(variant):
+    import torch
+    cuda = torch.device("cuda:0")
+    rng = np.random.default_rng(10 + variant)
+    lens = [int(x) for x in rng.integers(1, 5000, size=200)] + [1, 7, 8, 9, 15, 16, 17, 127, 128, 129, 383, 384,
+                                                                  385, 511, 512, 513, 1023, 1024, 1025, 2047]
+    offs = [int(x) for x in rng.integers(0, 16, size=len(lens))]
+    payloads = [hash_ref.payload(n, 21, i) for i, n in enumerate(lens)]
+    want = [hash_ref.fold64_c(p) for p in payloads]
+    assert _device_digests(cuda, payloads, offsets=offs) == want
+    order = list(np.argsort(-np.array(lens), kind="stable"))
+    assert _device_digests(cuda, payloads, offsets=offs, order=order) == want
+    z = _device_digests(cuda, [b"ab", b"", b"c" * 1000, b""])
+    assert z[1] == 0 and z[3] == 0 and z[0] == hash_ref.fold64_c(b"ab")
+
+
 def test_misaligned_starts_0_to_15(cuda):
     rng = np.random.default_rng(1)
     for off in range(16):
