@@ -37,7 +37,7 @@ METRIC = "GB/s of mapped bytes hashed; M trace events/s analysed"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n-bufs", type=int, default=N_BUFS)
@@ -260,7 +260,7 @@ def run_ours(args, rank, world, local):
                    "l2": "inputs (16 GB) larger than the 126 MB L2, no flush", "parallelism": f"shard{world}"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "k_hash_seq", "algorithmic_bytes_per_launch": total},
+                     "kernel": "k_hash_coop<2,512,2> (b2l_hash_batch default variant)", "algorithmic_bytes_per_launch": total},
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": args.steps, "verified": bool(verified),
         "clocks": clk.summary(), "impl": "ours",
     }
