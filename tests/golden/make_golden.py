@@ -50,7 +50,105 @@ def hash_fixture():
     return out
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--analysis" not in sys.argv:
     with open(os.path.join(HERE, "hash_vectors.json"), "w") as f:
         json.dump(hash_fixture(), f, indent=0)
     print("wrote hash_vectors.json")
+
+
+# ----------------------------------------------------------------------------- analysis
+def _trace_json(tr):
+    return {"version": tr.version, "num_devices_total": tr.num_devices_total, "host_device": tr.host_device,
+            "wall_time_ns": tr.wall_time_ns,
+            "events": [[e.seq, e.kind.value, e.start_ns, e.end_ns, e.src_device, e.dst_device, e.src_addr,
+                        e.dst_addr, e.bytes, str(e.hash), e.loc.codeptr, e.loc.file, e.loc.line]
+                       for e in tr.events]}
+
+
+def _pair_json(p):
+    return [p.alloc_event.seq, p.delete_event.seq, p.synthetic_delete]
+
+
+def _findings_json(f):
+    return {
+        "dd": [[str(g.hash), g.dest_device, [e.seq for e in g.events]] for g in f.duplicates],
+        "rt": [[str(g.hash), g.src_device, g.dest_device, [[a.seq, b.seq] for a, b in g.trips]]
+               for g in f.round_trips],
+        "ra": [[g.host_addr, g.tgt_device, g.bytes, [_pair_json(p) for p in g.pairs]] for g in f.repeated_allocs],
+        "ua": [_pair_json(p) for p in f.unused_allocs],
+        "ut": [e.seq for e in f.unused_transfers],
+    }
+
+
+def _case(name, tr):
+    from dmlens import analyze, attribute, estimate
+    from dmlens.detectors import InvalidTrace
+    from dmlens.prep import get_alloc_delete_pairs
+    from dmlens.model import EventKind
+    case = {"name": name, "trace": _trace_json(tr)}
+    try:
+        warns = []
+        f = analyze(tr, warn=warns.append)
+    except InvalidTrace as exc:
+        case["violations"] = [[v.rule, v.message, v.seq] for v in exc.violations]
+        return case
+    case["warnings"] = [[w.seq, w.reason] for w in warns]
+    case["findings"] = _findings_json(f)
+    case["findings_strict"] = _findings_json(analyze(tr, strict_pseudocode=True))
+    data_ops = [e for e in tr.events if e.kind is not EventKind.KERNEL]
+    case["pairs"] = [_pair_json(p) for p in get_alloc_delete_pairs(data_ops)]
+    s = estimate(tr, f)
+    case["estimate"] = {"per_category_ns": s.per_category_ns, "union_ns": s.union_ns,
+                        "wall_time_ns": s.wall_time_ns, "predicted_speedup": repr(s.predicted_speedup),
+                        "eliminable_seqs": sorted(s.eliminable_seqs), "warnings": list(s.warnings)}
+    case["attribute"] = [[r.category, [r.location.codeptr, r.location.file, r.location.line], r.occurrence_count,
+                          r.total_ns, r.total_bytes, repr(r.pct_of_wall)] for r in attribute(tr, f)]
+    return case
+
+
+def analysis_fixture():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("ref_conftest", os.path.join(os.path.dirname(REF), "tests",
+                                                                               "conftest.py"))
+    conf = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(conf)
+    from dmlens.synth import PATTERNS, PatternSpec, generate, generate_scale
+    from dmlens.model import CodeLocation, EventKind, Trace, TraceEvent
+    cases = []
+    for seed in range(300):
+        cases.append(_case(f"random_trace({seed})", conf.random_trace(seed)))
+    for seed in range(1000, 1012):
+        cases.append(_case(f"random_trace({seed}, 2000, 6)", conf.random_trace(seed, max_events=2000,
+                                                                                 max_devices=6)))
+    for pat in PATTERNS:
+        for n, nd in ((1, 2), (3, 3), (5, 4)):
+            tr, _ = generate(PatternSpec(pattern=pat, n_iterations=n, n_devices=nd, seed=n * 7 + nd))
+            cases.append(_case(f"synth({pat},{n},{nd})", tr))
+    cases.append(_case("generate_scale(20000,1,3)", generate_scale(20000, seed=1, n_devices=3)))
+    # invalid traces (model.py:125-200 messages)
+    mk = conf.make_event
+    bad = [
+        ("inverted", [mk(0, EventKind.TRANSFER, 10, 5, hash=1, nbytes=8)]),
+        ("hashless", [mk(0, EventKind.TRANSFER, 0, 5, nbytes=8, hash=0)]),
+        ("alloc0", [mk(0, EventKind.ALLOC, 0, 5, nbytes=0, dst_addr=0)]),
+        ("delete0", [mk(0, EventKind.DELETE, 0, 5, dst_addr=0)]),
+        ("kernel", [mk(0, EventKind.KERNEL, 0, 5, src=0, dst=1)]),
+        ("device", [mk(0, EventKind.TRANSFER, 0, 5, src=7, dst=-1, nbytes=0)]),
+        ("unsorted", [mk(0, EventKind.KERNEL, 10, 15, src=1, dst=1), mk(1, EventKind.KERNEL, 5, 6, src=1, dst=1)]),
+        ("seqdup", [mk(3, EventKind.KERNEL, 0, 1, src=1, dst=1), mk(3, EventKind.KERNEL, 0, 1, src=1, dst=1),
+                    mk(2, EventKind.KERNEL, 0, 1, src=1, dst=1)]),
+        ("loc", [mk(0, EventKind.KERNEL, 0, 1, src=1, dst=1, file="a.c"),
+                 mk(1, EventKind.KERNEL, 0, 1, src=1, dst=1, codeptr=5, file="b.c", line=0),
+                 mk(2, EventKind.KERNEL, 0, 1, src=1, dst=1, line=-3)]),
+    ]
+    for name, evs in bad:
+        cases.append(_case("invalid:" + name, Trace(1, 2, 0, None, evs)))
+    cases.append(_case("invalid:header", Trace(1, 0, 3, None, [])))
+    return cases
+
+
+if __name__ == "__main__" and "--analysis" in sys.argv:
+    import gzip
+    with gzip.open(os.path.join(HERE, "analysis_cases.json.gz"), "wt") as f:
+        json.dump(analysis_fixture(), f)
+    print("wrote analysis_cases.json.gz")
