@@ -86,6 +86,113 @@ int b2l_hash_select_variant(int variant, int *count);
 /* Device-side occupancy/launch info of the hash kernel (diagnostics). */
 int b2l_hash_launch_info(uint64_t n, int *grid, int *block, int *smem_bytes);
 
+/* ------------------------------------------------------------ trace analysis
+ * Event i is trace.events[i].  Kinds: */
+enum { B2L_KIND_TRANSFER = 0, B2L_KIND_ALLOC = 1, B2L_KIND_DELETE = 2, B2L_KIND_KERNEL = 3 };
+/* Per-location validation flags (model.py:186-190). */
+enum { B2L_LOC_FILE_NO_LINE = 1, B2L_LOC_LINE_NONPOS = 2 };
+/* Violated-rule bits per event, in the order model.py:125-200 reports them. */
+enum {
+    B2L_RULE_INTERVAL = 1 << 0,      /* "interval": start_ns > end_ns */
+    B2L_RULE_SRC_DEVICE = 1 << 1,    /* "device": src_device out of range */
+    B2L_RULE_DST_DEVICE = 1 << 2,    /* "device": dst_device out of range */
+    B2L_RULE_TRANSFER_HASH = 1 << 3, /* "transfer": non-empty transfer has no content hash */
+    B2L_RULE_ALLOC_BYTES = 1 << 4,   /* "alloc": allocation of zero bytes */
+    B2L_RULE_ALLOC_ADDR = 1 << 5,    /* "alloc": allocation with null device address */
+    B2L_RULE_DELETE_ADDR = 1 << 6,   /* "delete": deletion with null device address */
+    B2L_RULE_KERNEL_DEVICE = 1 << 7, /* "kernel": kernel src_device must equal dst_device */
+    B2L_RULE_LOC_FILE = 1 << 8,      /* "location": file present but line missing */
+    B2L_RULE_LOC_LINE = 1 << 9,      /* "location": line must be positive */
+    B2L_RULE_ORDER_SORT = 1 << 10,   /* "order": events not sorted by (start_ns, seq) */
+    B2L_RULE_ORDER_SEQ = 1 << 11     /* "order": seq values not strictly increasing */
+};
+enum { B2L_ANALYZE_STRICT_RT = 1 }; /* analyze(strict_pseudocode=True), detectors.py:145-160 */
+#define B2L_SYNTHETIC 0xFFFFFFFFu   /* pair_delete of a synthetic trace-end delete (prep.py:78-93) */
+
+/* Trace columns (structure of arrays, one entry per event). */
+typedef struct b2l_trace_cols {
+    uint64_t n_events;
+    int32_t num_devices_total;
+    int32_t host_device;
+    const uint64_t *seq, *start_ns, *end_ns, *src_addr, *dst_addr, *bytes, *hash;
+    const int32_t *src_device, *dst_device;
+    const uint8_t *kind;       /* B2L_KIND_* */
+    const uint32_t *loc;       /* per event: location id < n_locs */
+    uint32_t n_locs;
+    const uint8_t *loc_flags;  /* per location: B2L_LOC_* */
+    const uint32_t *loc_bucket;/* per location: attribution bucket id < n_buckets (report.py:67-70) */
+    uint32_t n_buckets;
+    int32_t device_resident;   /* 1: every array above is a device pointer, 0: host pointers */
+} b2l_trace_cols;
+
+/* Findings in columnar form.  Engine-owned HOST arrays (b2l_findings_free);
+ * event indices are positions in the trace, pair indices positions in pair_*.
+ * Orders are the reference's: groups as sorted by detectors.py:102/166/180,
+ * members in trace order, pairs by allocation (prep.py:95), lists by (start, seq). */
+typedef struct b2l_findings {
+    uint64_t n_events;
+    /* validation: events violating >= 1 rule, ascending, with their B2L_RULE_* bits */
+    uint64_t n_bad;
+    uint32_t *bad_index, *bad_rules;
+    /* DD (detectors.py:85-103): dd_offsets[g]..dd_offsets[g+1] index dd_members */
+    uint64_t dd_groups;
+    uint64_t *dd_offsets;
+    uint32_t *dd_members;
+    /* RT (detectors.py:106-167): trips rt_tx[t] -> rt_rx[t] */
+    uint64_t rt_groups;
+    uint64_t *rt_offsets;
+    uint32_t *rt_tx, *rt_rx;
+    /* alloc/delete pairs (prep.py:45-96), one per allocation, in allocation order */
+    uint64_t n_pairs;
+    uint32_t *pair_alloc, *pair_delete;  /* B2L_SYNTHETIC = synthetic trace-end delete */
+    uint64_t synthetic_end_ns;           /* start/end of the synthetic deletes (max data-op end) */
+    uint64_t n_warnings;                 /* unmatched deletes, trace order (prep.py:73-76) */
+    uint32_t *warn_index;
+    /* RA (detectors.py:170-191): groups of pair indices */
+    uint64_t ra_groups;
+    uint64_t *ra_offsets;
+    uint32_t *ra_pairs;
+    /* UA (detectors.py:194-229): pair indices; UT (detectors.py:232-271): event indices */
+    uint64_t n_ua;
+    uint32_t *ua_pairs;
+    uint64_t n_ut;
+    uint32_t *ut_events;
+    void *internal;  /* engine state (device copies for b2l_savings) */
+} b2l_findings;
+
+/* analyze(trace, warn, strict_pseudocode).  Returns B2L_E_INVALID_TRACE when any
+ * event violates a rule (only n_bad / bad_* are filled) -- header rules
+ * (num_devices_total, host_device) are the caller's.  *out must be freed with
+ * b2l_findings_free (also on B2L_E_INVALID_TRACE). */
+int b2l_analyze(const b2l_trace_cols *cols, uint32_t flags, b2l_findings **out);
+void b2l_findings_free(b2l_findings *f);
+
+typedef struct b2l_u128 { uint64_t lo, hi; } b2l_u128;
+
+/* Integer parts of estimate() (estimator.py:61-130) and attribute() (report.py:44-95)
+ * for findings given as a b2l_findings (from b2l_analyze, or filled by the caller
+ * with host arrays -- then `internal` must be NULL).  Sums are exact 128-bit. */
+typedef struct b2l_savings {
+    b2l_u128 per_category_ns[5];  /* DD, RT, RA, UA, UT */
+    b2l_u128 union_ns;
+    uint64_t n_union;
+    uint32_t *union_index;        /* eliminable events, ascending (engine-owned host array) */
+    int32_t has_overlaps;         /* estimator.py:51-58 */
+    uint64_t min_start_ns, max_end_ns;
+    uint32_t n_buckets;
+    /* per category c (0..4) and bucket b, at [c * n_buckets + b]: */
+    uint64_t *attr_count;
+    b2l_u128 *attr_ns, *attr_bytes;
+    uint64_t *attr_first;         /* (multiset position << 32) | event index of the first member;
+                                     UINT64_MAX when the bucket has no member */
+} b2l_savings;
+int b2l_savings_compute(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings **out);
+void b2l_savings_free(b2l_savings *s);
+
+/* Positions of `n` seq values in the trace's seq column (ascending seq, as in a
+ * validated trace); UINT32_MAX when absent.  Host arrays. */
+int b2l_lookup_seqs(const b2l_trace_cols *cols, const uint64_t *seqs, uint64_t n, uint32_t *out_index);
+
 #ifdef __cplusplus
 }
 #endif

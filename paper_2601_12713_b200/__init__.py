@@ -8,9 +8,13 @@ __version__ = "0.1.0"
 from .errors import (DeviceOutOfRange, EmptyPayload, EngineError, EngineUnavailable,
                      FindingsTraceMismatch, InvalidTrace)
 from .hashing import HashFn, hash_batch, hash_bytes, hash_device, hash_tensors, make_hasher
+from .analysis import (ColumnarFindings, ColumnarSavings, analyze, analyze_columns, attribute, estimate,
+                       savings_columns)
+from .columns import Columns, columns_from_arrays, to_columns
 
 __all__ = [
     "DeviceOutOfRange", "EmptyPayload", "EngineError", "EngineUnavailable",
     "FindingsTraceMismatch", "InvalidTrace", "HashFn", "hash_batch", "hash_bytes",
-    "hash_device", "hash_tensors", "make_hasher",
+    "hash_device", "hash_tensors", "make_hasher", "ColumnarFindings", "ColumnarSavings", "analyze",
+    "analyze_columns", "attribute", "estimate", "savings_columns", "Columns", "columns_from_arrays", "to_columns",
 ]

@@ -1,0 +1,1402 @@
+// Trace-analysis pipeline on the B200: validate -> partition -> (DD, RT) ->
+// LIFO pairing -> RA -> UA / UT, all as sort / segmented-scan / compaction
+// passes over SoA event columns (no per-event sequential sweep).
+//
+// Reference semantics (paths under /root/reference/pkg/src/dmlens/):
+//   validate        model.py:125-200        -> k_validate (rule bits per event)
+//   analyze         detectors.py:274-326    -> analyze_impl (partition :296-312)
+//   pairing         prep.py:45-96           -> pairs_step: stable sort by (dst_dev, dst_addr),
+//                                              clamped-depth max-plus scan, (segment, level)
+//                                              sort; alternating A,D at one level are pairs
+//   DD              detectors.py:85-103     -> dd_rt_step: segments of the (hash, dev) sort
+//   RT default      detectors.py:106-167    -> r_j = j + max_{i<=j}(f_i - i) over each queue
+//   RT strict       detectors.py:139-160    -> k_rt_strict: one thread per hash, head pointers
+//   RA              detectors.py:170-191    -> ra_step: stable sort of pairs by (addr, dev, bytes)
+//   UA / UT         detectors.py:194-271    -> kernel cursor = lower_bound of the per-device
+//                                              prefix max of kernel ends; UT run ids by scan
+// Proofs of the reformulations: SURVEY.md Appendix A; the GPU tests check every step
+// against oracle/analysis_ref.py and the reference's golden outputs.
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <type_traits>
+#include <vector>
+
+#include "b2l_prims.cuh"
+
+namespace b2l {
+namespace ana {
+
+constexpr uint32_t NONE = 0xFFFFFFFFu;
+constexpr int TPB = 256;
+
+struct DevCols {
+    size_t n;
+    int ndev, host;
+    const uint64_t *seq, *start, *end, *sa, *da, *nb, *h;
+    const int32_t *src, *dst;
+    const uint8_t *kind;
+    const uint32_t *loc;
+    const uint8_t *loc_flags;
+    const uint32_t *loc_bucket;
+    uint32_t nlocs, nbuckets;
+};
+
+// Owns device copies of host columns.
+struct ColsUpload {
+    std::vector<DBuf<uint8_t>> bufs;
+    DevCols d{};
+    template <class T>
+    const T *up(const T *h, size_t n, cudaStream_t s) {
+        if (!n) return nullptr;
+        bufs.emplace_back(n * sizeof(T), s);
+        CK(cudaMemcpyAsync(bufs.back().p, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+        return reinterpret_cast<const T *>(bufs.back().p);
+    }
+    void load(const b2l_trace_cols *c, cudaStream_t s) {
+        d.n = c->n_events;
+        d.ndev = c->num_devices_total;
+        d.host = c->host_device;
+        d.nlocs = c->n_locs;
+        d.nbuckets = c->n_buckets;
+        if (c->device_resident) {
+            d.seq = c->seq, d.start = c->start_ns, d.end = c->end_ns, d.sa = c->src_addr, d.da = c->dst_addr;
+            d.nb = c->bytes, d.h = c->hash, d.src = c->src_device, d.dst = c->dst_device, d.kind = c->kind;
+            d.loc = c->loc, d.loc_flags = c->loc_flags, d.loc_bucket = c->loc_bucket;
+            return;
+        }
+        const size_t n = d.n;
+        d.seq = up(c->seq, n, s), d.start = up(c->start_ns, n, s), d.end = up(c->end_ns, n, s);
+        d.sa = up(c->src_addr, n, s), d.da = up(c->dst_addr, n, s), d.nb = up(c->bytes, n, s);
+        d.h = up(c->hash, n, s), d.src = up(c->src_device, n, s), d.dst = up(c->dst_device, n, s);
+        d.kind = up(c->kind, n, s), d.loc = up(c->loc, n, s);
+        d.loc_flags = up(c->loc_flags, c->n_locs, s), d.loc_bucket = up(c->loc_bucket, c->n_locs, s);
+    }
+};
+
+// ============================================================ validation (model.py:125-200)
+__device__ __forceinline__ uint32_t event_rules(const DevCols &c, size_t i) {
+    uint32_t m = 0;
+    const uint64_t t0 = c.start[i], t1 = c.end[i];
+    const int32_t src = c.src[i], dst = c.dst[i];
+    if (t0 > t1) m |= B2L_RULE_INTERVAL;
+    if (src < 0 || src >= c.ndev) m |= B2L_RULE_SRC_DEVICE;
+    if (dst < 0 || dst >= c.ndev) m |= B2L_RULE_DST_DEVICE;
+    switch (c.kind[i]) {
+        case B2L_KIND_TRANSFER:
+            if (c.nb[i] > 0 && c.h[i] == 0) m |= B2L_RULE_TRANSFER_HASH;
+            break;
+        case B2L_KIND_ALLOC:
+            if (c.nb[i] == 0) m |= B2L_RULE_ALLOC_BYTES;
+            if (c.da[i] == 0) m |= B2L_RULE_ALLOC_ADDR;
+            break;
+        case B2L_KIND_DELETE:
+            if (c.da[i] == 0) m |= B2L_RULE_DELETE_ADDR;
+            break;
+        default:
+            if (src != dst) m |= B2L_RULE_KERNEL_DEVICE;
+    }
+    const uint8_t lf = c.loc_flags[c.loc[i]];
+    if (lf & B2L_LOC_FILE_NO_LINE) m |= B2L_RULE_LOC_FILE;
+    if (lf & B2L_LOC_LINE_NONPOS) m |= B2L_RULE_LOC_LINE;
+    if (i > 0) {
+        const uint64_t ps = c.start[i - 1], pq = c.seq[i - 1], q = c.seq[i];
+        if (t0 < ps || (t0 == ps && q < pq)) m |= B2L_RULE_ORDER_SORT;
+        if (q <= pq) m |= B2L_RULE_ORDER_SEQ;
+    }
+    return m;
+}
+struct BadPred {
+    DevCols c;
+    __device__ bool operator()(size_t i) const { return event_rules(c, i) != 0; }
+};
+__global__ void k_bad_rules(DevCols c, const uint32_t *bad, const uint32_t *count, uint32_t *rules) {
+    const uint32_t nb = *count;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nb; k += gridDim.x * blockDim.x)
+        rules[k] = event_rules(c, bad[k]);
+}
+
+// ============================================================ partition (detectors.py:296-312)
+struct IsHashed {  // transfers with bytes > 0 and a content hash
+    DevCols c;
+    __device__ bool operator()(size_t i) const { return c.kind[i] == B2L_KIND_TRANSFER && c.nb[i] > 0 && c.h[i] != 0; }
+};
+struct IsTargetTransfer {
+    DevCols c;
+    __device__ bool operator()(size_t i) const { return c.kind[i] == B2L_KIND_TRANSFER && c.dst[i] != c.host; }
+};
+struct IsAllocDelete {
+    DevCols c;
+    __device__ bool operator()(size_t i) const { return c.kind[i] == B2L_KIND_ALLOC || c.kind[i] == B2L_KIND_DELETE; }
+};
+struct IsAlloc {
+    DevCols c;
+    __device__ bool operator()(size_t i) const { return c.kind[i] == B2L_KIND_ALLOC; }
+};
+struct IsTargetKernel {
+    DevCols c;
+    __device__ bool operator()(size_t i) const { return c.kind[i] == B2L_KIND_KERNEL && c.dst[i] != c.host; }
+};
+
+__global__ void k_max_data_end(DevCols c, unsigned long long *out) {
+    unsigned long long m = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += (size_t)gridDim.x * blockDim.x)
+        if (c.kind[i] != B2L_KIND_KERNEL && c.end[i] > m) m = c.end[i];
+    for (int o = 16; o; o >>= 1) {
+        unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+        m = v > m ? v : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+// ============================================================ helpers
+template <class F>
+__global__ void k_for(size_t n, F f) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) f(i);
+}
+template <class F>
+void for_each(size_t n, F f, cudaStream_t s) {
+    if (!n) return;
+    k_for<F><<<grid_for(n, TPB), TPB, 0, s>>>(n, f);
+    CK_LAUNCH("k_for");
+}
+
+// Read a device u32 count (one sync).
+uint32_t read_u32(const uint32_t *d, cudaStream_t s) {
+    uint32_t v = 0;
+    CK(cudaMemcpyAsync(&v, d, sizeof(v), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return v;
+}
+
+// Segment heads of sorted keys.
+template <int KW>
+struct HeadPred {
+    KeyCols<KW> k;
+    __device__ bool operator()(size_t p) const {
+        if (p == 0) return true;
+#pragma unroll
+        for (int w = 0; w < KW; ++w)
+            if (k.w[w][p] != k.w[w][p - 1]) return true;
+        return false;
+    }
+};
+
+template <int KW>
+struct HeadLoad {
+    KeyCols<KW> k;
+    __device__ uint32_t operator()(size_t p) const { return HeadPred<KW>{k}(p) ? 1u : 0u; }
+};
+struct StoreInclMinus1 {
+    uint32_t *o;
+    __device__ void operator()(size_t i, uint32_t ex, uint32_t it) const { o[i] = ex + it - 1; }
+};
+
+// Group ordering: stable sort of group ids by the start time of each group's first
+// event (ties keep the key order the groups were produced in) -- detectors.py:102,166,180.
+struct GroupOrder {
+    DBuf<uint32_t> order;  // final rank -> group id
+    DBuf<uint32_t> rank;   // group id -> final rank
+};
+struct FirstStartKey {
+    const uint64_t *start;
+    const uint32_t *first_event;
+    uint64_t *key;
+    uint32_t *val;
+    __device__ void operator()(size_t g) const {
+        key[g] = start[first_event[g]];
+        val[g] = (uint32_t)g;
+    }
+};
+GroupOrder order_groups(size_t ng, const uint64_t *start, const uint32_t *first_event, cudaStream_t s) {
+    GroupOrder go;
+    go.order.alloc(ng ? ng : 1, s);
+    go.rank.alloc(ng ? ng : 1, s);
+    if (!ng) return go;
+    SortStore<1> st(ng, s);
+    for_each(ng, FirstStartKey{start, first_event, st.in_key(0), st.in_val()}, s);
+    radix_sort<1>(st.b, ng, s);
+    CK(cudaMemcpyAsync(go.order.p, st.val(), ng * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    uint32_t *ord = go.order.p, *rk = go.rank.p;
+    for_each(ng, [=] __device__(size_t r) { rk[ord[r]] = (uint32_t)r; }, s);
+    return go;
+}
+
+// Offsets of groups in final order from per-group sizes: off[r] = sum of sizes of ranks < r.
+struct SizeByRank {
+    const uint32_t *order;
+    const uint32_t *size;
+    __device__ uint64_t operator()(size_t r) const { return size[order[r]]; }
+};
+struct StoreOffset {
+    uint64_t *off;
+    __device__ void operator()(size_t r, uint64_t ex, uint64_t) const { off[r] = ex; }
+};
+
+// ============================================================ output container
+struct Internal {
+    // device copies of findings (for b2l_savings)
+    DBuf<uint64_t> dd_off, rt_off, ra_off;
+    DBuf<uint32_t> dd_mem, rt_tx, rt_rx, pair_alloc, pair_delete, ra_mem, ua, ut;
+    uint64_t dd_groups = 0, dd_members = 0, rt_groups = 0, rt_trips = 0, ra_groups = 0, ra_members = 0;
+    uint64_t n_pairs = 0, n_ua = 0, n_ut = 0, synth_end = 0;
+};
+
+template <class T>
+T *host_copy(const T *d, size_t n, cudaStream_t s) {
+    T *h = (T *)malloc((n ? n : 1) * sizeof(T));
+    if (!h) throw EngineErr{B2L_E_OOM, "host allocation failed"};
+    if (n) CK(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    return h;
+}
+
+// ============================================================ DD + RT (detectors.py:85-167)
+struct RtRecordInit {  // record r = 2k + role over hashed transfer k: role 0 = reception, 1 = send
+    DevCols c;
+    const uint32_t *H;
+    uint64_t *k0, *k1;
+    uint32_t *val;
+    __device__ void operator()(size_t r) const {
+        const uint32_t e = H[r >> 1];
+        k0[r] = c.h[e];
+        k1[r] = (uint64_t)(uint32_t)((r & 1) ? c.src[e] : c.dst[e]);
+        val[r] = (uint32_t)r;
+    }
+};
+
+// Per sorted record: segment head, reception/send counts (segmented + global).
+struct QState {
+    uint32_t head, seg, rx_seg, tx_seg, rx_glob;
+};
+struct QOp {
+    using T = QState;
+    static __device__ __forceinline__ T identity() { return T{0, 0, 0, 0, 0}; }
+    static __device__ __forceinline__ T combine(T a, T b) {
+        return T{a.head | b.head, a.seg + b.seg, b.head ? b.rx_seg : a.rx_seg + b.rx_seg,
+                 b.head ? b.tx_seg : a.tx_seg + b.tx_seg, a.rx_glob + b.rx_glob};
+    }
+};
+struct QLoad {
+    KeyCols<2> k;
+    const uint32_t *val;
+    __device__ QState operator()(size_t p) const {
+        const bool head = p == 0 || k.w[0][p] != k.w[0][p - 1] || k.w[1][p] != k.w[1][p - 1];
+        const uint32_t rx = (val[p] & 1u) == 0;
+        return QState{head, head, rx, 1u - rx, rx};
+    }
+};
+struct QStore {
+    const uint32_t *val;
+    uint32_t *seg_of, *f_of, *j_of, *rxpos, *seg_start, *seg_rxbase;
+    __device__ void operator()(size_t p, QState ex, QState it) const {
+        const uint32_t seg = ex.seg + it.seg - 1;
+        seg_of[p] = seg;
+        const uint32_t f = it.head ? 0 : ex.rx_seg, j = it.head ? 0 : ex.tx_seg;
+        f_of[p] = f;
+        j_of[p] = j;
+        if (it.head) {
+            seg_start[seg] = (uint32_t)p;
+            seg_rxbase[seg] = ex.rx_glob;
+        }
+        if ((val[p] & 1u) == 0) rxpos[ex.rx_glob] = (uint32_t)p;
+    }
+};
+// r_j = j + max_{i<=j}(f_i - i) over the sends of one queue
+struct RtMaxLoad {
+    KeyCols<2> k;
+    const uint32_t *val, *f_of, *j_of;
+    __device__ Seg<MaxI64>::T operator()(size_t p) const {
+        const bool head = p == 0 || k.w[0][p] != k.w[0][p - 1] || k.w[1][p] != k.w[1][p - 1];
+        const bool tx = val[p] & 1u;
+        return Seg<MaxI64>::T{head ? 1u : 0u, tx ? (long long)f_of[p] - (long long)j_of[p] : MaxI64::identity()};
+    }
+};
+struct RtMatchStore {
+    const uint32_t *val, *j_of, *seg_of, *seg_rxbase, *rxpos, *H;
+    uint32_t *match;  // per hashed-transfer k: reception event or NONE
+    __device__ void operator()(size_t p, Seg<MaxI64>::T ex, Seg<MaxI64>::T it) const {
+        if (!(val[p] & 1u)) return;
+        const long long pm = it.flag ? it.v : MaxI64::combine(ex.v, it.v);
+        const long long r = (long long)j_of[p] + pm;
+        const uint32_t seg = seg_of[p];
+        const long long nrx = (long long)seg_rxbase[seg + 1] - (long long)seg_rxbase[seg];
+        if (r < nrx) match[val[p] >> 1] = H[val[rxpos[seg_rxbase[seg] + r]] >> 1];
+    }
+};
+
+// Strict pseudocode (detectors.py:139-160): per hash, sends in trace order peek the
+// (hash, src) queue and pop the (hash, dst) queue.  Queues of one hash interact, so one
+// thread walks each hash's events; different hashes run in parallel.
+__device__ __forceinline__ int find_seg(const uint64_t *sk0, const uint64_t *sk1, uint32_t nseg, uint64_t h,
+                                        uint64_t d) {
+    uint32_t lo = 0, hi = nseg;
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (sk0[mid] < h || (sk0[mid] == h && sk1[mid] < d))
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return (lo < nseg && sk0[lo] == h && sk1[lo] == d) ? (int)lo : -1;
+}
+__global__ void k_rt_strict(DevCols c, const uint32_t *H, const uint32_t *hsorted /*hashed-k sorted by hash*/,
+                            const uint32_t *hseg_start, uint32_t nhseg, uint32_t nH, const uint64_t *sk0,
+                            const uint64_t *sk1, uint32_t nseg, const uint32_t *seg_rxbase, const uint32_t *rxpos,
+                            const uint32_t *sval, uint32_t *qhead, uint32_t *match) {
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < nhseg; g += gridDim.x * blockDim.x) {
+        const uint32_t b = hseg_start[g], e = (g + 1 < nhseg) ? hseg_start[g + 1] : nH;
+        for (uint32_t q = b; q < e; ++q) {
+            const uint32_t k = hsorted[q];
+            const uint32_t ev = H[k];
+            const uint64_t h = c.h[ev];
+            const int sq = find_seg(sk0, sk1, nseg, h, (uint64_t)(uint32_t)c.src[ev]);
+            if (sq < 0) continue;
+            const uint32_t nrx = seg_rxbase[sq + 1] - seg_rxbase[sq];
+            if (qhead[sq] >= nrx) continue;  // `if not q: continue`
+            match[k] = H[sval[rxpos[seg_rxbase[sq] + qhead[sq]]] >> 1];
+            const int so = find_seg(sk0, sk1, nseg, h, (uint64_t)(uint32_t)c.dst[ev]);
+            if (so >= 0 && qhead[so] < seg_rxbase[so + 1] - seg_rxbase[so]) qhead[so] += 1;
+        }
+    }
+}
+
+struct DdRt {
+    uint64_t dd_groups = 0, rt_groups = 0, dd_members = 0, rt_trips = 0;
+};
+
+DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, Internal &out, cudaStream_t s) {
+    DdRt r;
+    const size_t R = 2ull * nH;
+    if (nH == 0) {
+        out.dd_off.alloc(1, s), out.dd_off.zero(), out.dd_mem.alloc(1, s);
+        out.rt_off.alloc(1, s), out.rt_off.zero(), out.rt_tx.alloc(1, s), out.rt_rx.alloc(1, s);
+        return r;
+    }
+    SortStore<2> st(R, s);
+    for_each(R, RtRecordInit{c, H, st.in_key(0), st.in_key(1), st.in_val()}, s);
+    radix_sort<2>(st.b, R, s);
+    KeyCols<2> sk = st.b.k[st.b.cur];
+    const uint32_t *sval = st.val();
+
+    DBuf<uint32_t> seg_of(R, s), f_of(R, s), j_of(R, s), rxpos(R, s), seg_start(R + 1, s), seg_rxbase(R + 1, s);
+    HostScalars hs(2, s);
+    DBuf<QState> tot(1, s);
+    scan<QOp>(R, QLoad{sk, sval},
+              QStore{sval, seg_of.p, f_of.p, j_of.p, rxpos.p, seg_start.p, seg_rxbase.p}, s, tot.p);
+    QState qt{};
+    CK(cudaMemcpyAsync(&qt, tot.p, sizeof(qt), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const uint32_t nseg = qt.seg, nrx = qt.rx_glob;
+    CK(cudaMemcpyAsync(seg_rxbase.p + nseg, &tot.p->rx_glob, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+
+    // ---- round trips: per send, the matched reception (or NONE)
+    DBuf<uint32_t> match(nH, s);
+    CK(cudaMemsetAsync(match.p, 0xFF, nH * sizeof(uint32_t), s));
+    if (!strict) {
+        scan<Seg<MaxI64>>(R, RtMaxLoad{sk, sval, f_of.p, j_of.p},
+                          RtMatchStore{sval, j_of.p, seg_of.p, seg_rxbase.p, rxpos.p, H, match.p}, s);
+    } else {
+        DBuf<uint64_t> segk0(nseg, s), segk1(nseg, s);
+        {
+            const uint32_t *ss = seg_start.p;
+            uint64_t *a = segk0.p, *b = segk1.p;
+            const uint64_t *x0 = sk.w[0], *x1 = sk.w[1];
+            for_each(nseg, [=] __device__(size_t g) { a[g] = x0[ss[g]], b[g] = x1[ss[g]]; }, s);
+        }
+        // hashed transfers grouped by hash, trace order within a hash
+        SortStore<1> hsort(nH, s);
+        {
+            uint64_t *k0 = hsort.in_key(0);
+            uint32_t *v = hsort.in_val();
+            const uint64_t *hh = c.h;
+            for_each(nH, [=] __device__(size_t k) { k0[k] = hh[H[k]], v[k] = (uint32_t)k; }, s);
+        }
+        radix_sort<1>(hsort.b, nH, s);
+        DBuf<uint32_t> hstart(nH, s), hcount(1, s);
+        KeyCols<1> hk = hsort.b.k[hsort.b.cur];
+        compact(nH, HeadPred<1>{hk}, hstart.p, hcount.p, s);
+        const uint32_t nhseg = read_u32(hcount.p, s);
+        DBuf<uint32_t> qhead(nseg, s);
+        qhead.zero();
+        k_rt_strict<<<grid_for(nhseg, 128), 128, 0, s>>>(c, H, hsort.val(), hstart.p, nhseg, nH, segk0.p, segk1.p,
+                                                         nseg, seg_rxbase.p, rxpos.p, sval, qhead.p, match.p);
+        CK_LAUNCH("k_rt_strict");
+    }
+
+    // ---- DD groups: queue segments with >= 2 receptions (members = the receptions, trace order)
+    {
+        DBuf<uint32_t> gseg(nseg, s), gcount(1, s);
+        const uint32_t *rb = seg_rxbase.p;
+        compact(nseg, [=] __device__(size_t g) { return rb[g + 1] - rb[g] >= 2; }, gseg.p, gcount.p, s);
+        const uint32_t ng = read_u32(gcount.p, s);
+        r.dd_groups = ng;
+        DBuf<uint32_t> first_ev(ng ? ng : 1, s), gsize(ng ? ng : 1, s), seg_group(nseg, s);
+        CK(cudaMemsetAsync(seg_group.p, 0xFF, nseg * sizeof(uint32_t), s));
+        {
+            const uint32_t *gs = gseg.p, *rp = rxpos.p;
+            uint32_t *fe = first_ev.p, *sz = gsize.p, *sgp = seg_group.p;
+            for_each(ng, [=] __device__(size_t g) {
+                const uint32_t sg = gs[g];
+                fe[g] = H[sval[rp[rb[sg]]] >> 1];
+                sz[g] = rb[sg + 1] - rb[sg];
+                sgp[sg] = (uint32_t)g;
+            }, s);
+        }
+        GroupOrder go = order_groups(ng, c.start, first_ev.p, s);
+        out.dd_off.alloc(ng + 1, s);
+        DBuf<uint64_t> total(1, s);
+        scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.dd_off.p}, s, total.p);
+        if (ng) CK(cudaMemcpyAsync(out.dd_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+        else CK(cudaMemsetAsync(out.dd_off.p, 0, sizeof(uint64_t), s));
+        uint64_t nm = 0;
+        if (ng) {
+            CK(cudaMemcpyAsync(&nm, total.p, sizeof(nm), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+        r.dd_members = nm;
+        out.dd_mem.alloc(nm ? nm : 1, s);
+        // every reception of a grouped segment lands at off[rank] + (its rank within the segment)
+        const uint32_t *sgp = seg_group.p, *rk = go.rank.p, *so = seg_of.p, *rp = rxpos.p;
+        const uint64_t *off = out.dd_off.p;
+        uint32_t *mem = out.dd_mem.p;
+        for_each(nrx, [=] __device__(size_t q) {
+            const uint32_t p = rp[q];
+            const uint32_t sg = so[p];
+            const uint32_t g = sgp[sg];
+            if (g == NONE) return;
+            mem[off[rk[g]] + (q - rb[sg])] = H[sval[p] >> 1];
+        }, s);
+    }
+
+    // ---- RT groups: matched sends keyed (hash, src, dst); sends of one (hash, src) queue are
+    // already in trace order in the record sort, so a stable sort by (queue segment, dst) groups them
+    {
+        DBuf<uint32_t> mpos(R, s), mcount(1, s);
+        uint32_t *mt = match.p;
+        compact(R, [=] __device__(size_t p) { return (sval[p] & 1u) && mt[sval[p] >> 1] != NONE; }, mpos.p,
+                mcount.p, s);
+        const uint32_t nt = read_u32(mcount.p, s);
+        r.rt_trips = nt;
+        out.rt_tx.alloc(nt ? nt : 1, s);
+        out.rt_rx.alloc(nt ? nt : 1, s);
+        if (nt == 0) {
+            out.rt_off.alloc(1, s), out.rt_off.zero();
+            return r;
+        }
+        SortStore<1> ts(nt, s);
+        {
+            uint64_t *k0 = ts.in_key(0);
+            uint32_t *v = ts.in_val();
+            const uint32_t *mp = mpos.p, *so = seg_of.p;
+            const int32_t *dst = c.dst;
+            for_each(nt, [=] __device__(size_t t) {
+                const uint32_t p = mp[t];
+                k0[t] = ((uint64_t)so[p] << 32) | (uint32_t)dst[H[sval[p] >> 1]];
+                v[t] = p;
+            }, s);
+        }
+        radix_sort<1>(ts.b, nt, s);
+        KeyCols<1> tk = ts.b.k[ts.b.cur];
+        const uint32_t *tv = ts.val();
+        DBuf<uint32_t> gstart(nt, s), gcount(1, s);
+        compact(nt, HeadPred<1>{tk}, gstart.p, gcount.p, s);
+        const uint32_t ng = read_u32(gcount.p, s);
+        r.rt_groups = ng;
+        DBuf<uint32_t> first_ev(ng, s), gsize(ng, s), trip_group(nt, s);
+        {
+            const uint32_t *gs = gstart.p;
+            uint32_t *fe = first_ev.p, *sz = gsize.p;
+            const uint32_t ntt = nt;
+            for_each(ng, [=] __device__(size_t g) {
+                fe[g] = H[sval[tv[gs[g]]] >> 1];
+                sz[g] = ((g + 1 < ng) ? gs[g + 1] : ntt) - gs[g];
+            }, s);
+        }
+        {
+            uint32_t *tg = trip_group.p;
+            scan<SumU32>(nt, HeadLoad<1>{tk}, StoreInclMinus1{tg}, s);  // group id of every sorted trip
+        }
+        GroupOrder go = order_groups(ng, c.start, first_ev.p, s);
+        out.rt_off.alloc(ng + 1, s);
+        DBuf<uint64_t> total(1, s);
+        scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.rt_off.p}, s, total.p);
+        CK(cudaMemcpyAsync(out.rt_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+        const uint32_t *tg = trip_group.p, *rk = go.rank.p, *gs = gstart.p;
+        const uint64_t *off = out.rt_off.p;
+        uint32_t *otx = out.rt_tx.p, *orx = out.rt_rx.p;
+        for_each(nt, [=] __device__(size_t t) {
+            const uint32_t g = tg[t];
+            const uint64_t o = off[rk[g]] + (t - gs[g]);
+            const uint32_t k = sval[tv[t]] >> 1;
+            otx[o] = H[k];
+            orx[o] = mt[k];
+        }, s);
+    }
+    return r;
+}
+
+
+// ============================================================ LIFO pairing (prep.py:45-96)
+struct PairOut {
+    uint32_t n_pairs = 0, n_warn = 0;
+    DBuf<uint32_t> warn;  // unmatched deletes, trace order
+};
+// inclusive depth after an element from its (exclusive prefix, item) of the max-plus scan
+__device__ __forceinline__ long long depth_of(const MaxPlus::T &f) { return f.a > f.b ? f.a : f.b; }
+struct DepthLoad {
+    KeyCols<2> k;
+    const uint32_t *val, *AD;
+    const uint8_t *kind;
+    __device__ Seg<MaxPlus>::T operator()(size_t p) const {
+        const bool head = p == 0 || k.w[0][p] != k.w[0][p - 1] || k.w[1][p] != k.w[1][p - 1];
+        const bool is_alloc = kind[AD[val[p]]] == B2L_KIND_ALLOC;
+        // alloc: d -> d + 1 ; delete: d -> max(d - 1, 0)
+        MaxPlus::T f = is_alloc ? MaxPlus::T{1, MaxPlus::identity().b} : MaxPlus::T{-1, 0};
+        return Seg<MaxPlus>::T{head ? 1u : 0u, f};
+    }
+};
+struct DepthStore {  // level (>= 1) of allocs and matched deletes, 0 for unmatched deletes
+    const uint32_t *val, *AD;
+    const uint8_t *kind;
+    uint32_t *level;
+    __device__ void operator()(size_t p, Seg<MaxPlus>::T ex, Seg<MaxPlus>::T it) const {
+        const long long before = it.flag ? 0 : depth_of(ex.v);
+        const bool is_alloc = kind[AD[val[p]]] == B2L_KIND_ALLOC;
+        level[p] = is_alloc ? (uint32_t)(before + 1) : (uint32_t)before;  // delete at depth 0: unmatched
+    }
+};
+
+PairOut pairs_step(const DevCols &c, const uint32_t *AD, uint32_t nAD, const uint32_t *A, uint32_t nA,
+                   uint64_t synth_end, Internal &out, cudaStream_t s) {
+    PairOut po;
+    po.n_pairs = nA;
+    out.pair_alloc.alloc(nA ? nA : 1, s);
+    out.pair_delete.alloc(nA ? nA : 1, s);
+    if (nA) CK(cudaMemcpyAsync(out.pair_alloc.p, A, nA * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    if (nA) CK(cudaMemsetAsync(out.pair_delete.p, 0xFF, nA * sizeof(uint32_t), s));  // synthetic unless matched
+    po.warn.alloc(nAD ? nAD : 1, s);
+    if (nAD == 0) return po;
+    // event -> allocation rank (pairs are in allocation order, prep.py:95)
+    DBuf<uint32_t> arank(c.n, s);
+    {
+        uint32_t *ar = arank.p;
+        for_each(nA, [=] __device__(size_t r) { ar[A[r]] = (uint32_t)r; }, s);
+    }
+    SortStore<2> st(nAD, s);
+    {
+        uint64_t *k0 = st.in_key(0), *k1 = st.in_key(1);
+        uint32_t *v = st.in_val();
+        const int32_t *dst = c.dst;
+        const uint64_t *da = c.da;
+        for_each(nAD, [=] __device__(size_t r) {
+            const uint32_t e = AD[r];
+            k0[r] = (uint64_t)(uint32_t)dst[e];
+            k1[r] = da[e];
+            v[r] = (uint32_t)r;
+        }, s);
+    }
+    radix_sort<2>(st.b, nAD, s);
+    KeyCols<2> sk = st.b.k[st.b.cur];
+    const uint32_t *sv = st.val();
+    DBuf<uint32_t> level(nAD, s), seg(nAD, s);
+    scan<Seg<MaxPlus>>(nAD, DepthLoad{sk, sv, AD, c.kind}, DepthStore{sv, AD, c.kind, level.p}, s);
+    scan<SumU32>(nAD, HeadLoad<2>{sk}, StoreInclMinus1{seg.p}, s);
+    // unmatched deletes -> warnings in trace order (flag by AD rank, compact in AD order)
+    {
+        DBuf<uint8_t> unmatched(nAD, s);
+        unmatched.zero();
+        uint8_t *um = unmatched.p;
+        const uint32_t *lv = level.p;
+        const uint8_t *kind = c.kind;
+        for_each(nAD, [=] __device__(size_t p) {
+            if (kind[AD[sv[p]]] == B2L_KIND_DELETE && lv[p] == 0) um[sv[p]] = 1;
+        }, s);
+        DBuf<uint32_t> wr(nAD, s), wc(1, s);
+        compact(nAD, [=] __device__(size_t r) { return um[r] != 0; }, wr.p, wc.p, s);
+        po.n_warn = read_u32(wc.p, s);
+        uint32_t *w = po.warn.p;
+        const uint32_t *wrp = wr.p;
+        for_each(po.n_warn, [=] __device__(size_t k) { w[k] = AD[wrp[k]]; }, s);
+    }
+    // (segment, level) sort of allocs and matched deletes: within one level of one address the
+    // sequence alternates alloc, delete, alloc, ... and each alloc pairs with the delete after it
+    DBuf<uint32_t> lp(nAD, s), lc(1, s);
+    {
+        const uint32_t *lv = level.p;
+        compact(nAD, [=] __device__(size_t p) { return lv[p] != 0; }, lp.p, lc.p, s);
+    }
+    const uint32_t nl = read_u32(lc.p, s);
+    if (nl == 0) return po;
+    SortStore<1> ls(nl, s);
+    {
+        uint64_t *k0 = ls.in_key(0);
+        uint32_t *v = ls.in_val();
+        const uint32_t *lpp = lp.p, *lv = level.p, *sg = seg.p;
+        for_each(nl, [=] __device__(size_t q) {
+            const uint32_t p = lpp[q];
+            k0[q] = ((uint64_t)sg[p] << 32) | lv[p];
+            v[q] = p;
+        }, s);
+    }
+    radix_sort<1>(ls.b, nl, s);
+    {
+        const uint64_t *lk = ls.key(0);
+        const uint32_t *lvv = ls.val();
+        const uint8_t *kind = c.kind;
+        const uint32_t *ar = arank.p;
+        uint32_t *pd = out.pair_delete.p;
+        const uint32_t nll = nl;
+        for_each(nl, [=] __device__(size_t q) {
+            const uint32_t e = AD[sv[lvv[q]]];
+            if (kind[e] != B2L_KIND_ALLOC) return;
+            if (q + 1 < nll && lk[q + 1] == lk[q]) {
+                const uint32_t e2 = AD[sv[lvv[q + 1]]];
+                if (kind[e2] == B2L_KIND_DELETE) pd[ar[e]] = e2;
+            }
+        }, s);
+    }
+    (void)synth_end;
+    return po;
+}
+
+// ============================================================ RA (detectors.py:170-191)
+void ra_step(const DevCols &c, uint32_t nP, Internal &out, cudaStream_t s) {
+    out.ra_groups = out.ra_members = 0;
+    if (nP < 2) {
+        out.ra_off.alloc(1, s), out.ra_off.zero(), out.ra_mem.alloc(1, s);
+        return;
+    }
+    const uint32_t *PA = out.pair_alloc.p;
+    SortStore<3> st(nP, s);
+    {
+        uint64_t *k0 = st.in_key(0), *k1 = st.in_key(1), *k2 = st.in_key(2);
+        uint32_t *v = st.in_val();
+        const uint64_t *sa = c.sa, *nb = c.nb;
+        const int32_t *dst = c.dst;
+        for_each(nP, [=] __device__(size_t r) {
+            const uint32_t a = PA[r];
+            k0[r] = sa[a], k1[r] = (uint64_t)(uint32_t)dst[a], k2[r] = nb[a], v[r] = (uint32_t)r;
+        }, s);
+    }
+    radix_sort<3>(st.b, nP, s);
+    KeyCols<3> sk = st.b.k[st.b.cur];
+    const uint32_t *sv = st.val();
+    DBuf<uint32_t> sstart(nP + 1, s), scount(1, s), seg_of(nP, s);
+    compact(nP, HeadPred<3>{sk}, sstart.p, scount.p, s);
+    scan<SumU32>(nP, HeadLoad<3>{sk}, StoreInclMinus1{seg_of.p}, s);
+    const uint32_t nseg = read_u32(scount.p, s);
+    {
+        uint32_t *ss = sstart.p;
+        const uint32_t np = nP;
+        for_each(1, [=] __device__(size_t) { ss[nseg] = np; }, s);
+    }
+    DBuf<uint32_t> gseg(nseg, s), gc(1, s);
+    const uint32_t *ss = sstart.p;
+    compact(nseg, [=] __device__(size_t g) { return ss[g + 1] - ss[g] >= 2; }, gseg.p, gc.p, s);
+    const uint32_t ng = read_u32(gc.p, s);
+    out.ra_groups = ng;
+    if (ng == 0) {
+        out.ra_off.alloc(1, s), out.ra_off.zero(), out.ra_mem.alloc(1, s);
+        return;
+    }
+    DBuf<uint32_t> first_ev(ng, s), gsize(ng, s), seg_group(nseg, s);
+    CK(cudaMemsetAsync(seg_group.p, 0xFF, nseg * sizeof(uint32_t), s));
+    {
+        const uint32_t *gs = gseg.p;
+        uint32_t *fe = first_ev.p, *sz = gsize.p, *sgp = seg_group.p;
+        for_each(ng, [=] __device__(size_t g) {
+            const uint32_t sg = gs[g];
+            fe[g] = PA[sv[ss[sg]]];
+            sz[g] = ss[sg + 1] - ss[sg];
+            sgp[sg] = (uint32_t)g;
+        }, s);
+    }
+    GroupOrder go = order_groups(ng, c.start, first_ev.p, s);
+    out.ra_off.alloc(ng + 1, s);
+    DBuf<uint64_t> total(1, s);
+    scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.ra_off.p}, s, total.p);
+    CK(cudaMemcpyAsync(out.ra_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    uint64_t nm = 0;
+    CK(cudaMemcpyAsync(&nm, total.p, sizeof(nm), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    out.ra_members = nm;
+    out.ra_mem.alloc(nm, s);
+    const uint32_t *sgp = seg_group.p, *rk = go.rank.p, *so = seg_of.p;
+    const uint64_t *off = out.ra_off.p;
+    uint32_t *mem = out.ra_mem.p;
+    for_each(nP, [=] __device__(size_t p) {
+        const uint32_t sg = so[p];
+        const uint32_t g = sgp[sg];
+        if (g == NONE) return;
+        mem[off[rk[g]] + (p - ss[sg])] = sv[p];
+    }, s);
+}
+
+// ============================================================ UA / UT (detectors.py:194-271)
+// Kernels of the target devices, grouped by device in trace order, with PM = per-device
+// prefix max of kernel ends.  The reference's forward cursor at a (non-decreasing) query
+// time t is the first kernel with PM >= t.
+struct KernelIndex {
+    const uint64_t *kdev;  // sorted device key per kernel position
+    const uint32_t *kev;   // kernel event per position
+    const uint64_t *pm;
+    uint32_t nk;
+    __device__ void range(uint64_t dev, uint32_t &lo, uint32_t &hi) const {
+        uint32_t a = 0, b = nk;
+        while (a < b) {
+            uint32_t m = (a + b) >> 1;
+            if (kdev[m] < dev) a = m + 1; else b = m;
+        }
+        lo = a;
+        b = nk;
+        while (a < b) {
+            uint32_t m = (a + b) >> 1;
+            if (kdev[m] <= dev) a = m + 1; else b = m;
+        }
+        hi = a;
+    }
+    __device__ uint32_t cursor(uint32_t lo, uint32_t hi, uint64_t t) const {
+        while (lo < hi) {
+            uint32_t m = (lo + hi) >> 1;
+            if (pm[m] < t) lo = m + 1; else hi = m;
+        }
+        return lo;
+    }
+};
+struct PmLoad {
+    const uint64_t *kdev;
+    const uint32_t *kev;
+    const uint64_t *end;
+    __device__ Seg<MaxU64>::T operator()(size_t p) const {
+        return Seg<MaxU64>::T{(p == 0 || kdev[p] != kdev[p - 1]) ? 1u : 0u, end[kev[p]]};
+    }
+};
+struct PmStore {
+    uint64_t *pm;
+    __device__ void operator()(size_t p, Seg<MaxU64>::T ex, Seg<MaxU64>::T it) const {
+        pm[p] = Seg<MaxU64>::combine(ex, it).v;
+    }
+};
+
+constexpr uint8_t CLS_GAP = 0, CLS_OVERLAP = 1, CLS_AFTER = 2;
+
+struct RunLoad {  // run increments along one device's target transfers (trace order)
+    const uint64_t *dk;  // sorted device key
+    const uint32_t *dv;  // transfer rank per sorted position
+    const uint32_t *cur;
+    const uint8_t *cls;
+    __device__ Seg<SumU32>::T operator()(size_t q) const {
+        const bool head = q == 0 || dk[q] != dk[q - 1];
+        uint32_t inc = 0;
+        if (!head) {
+            const uint32_t a = dv[q - 1], b = dv[q];
+            inc = (cur[b] > cur[a] || cls[a] == CLS_OVERLAP) ? 1u : 0u;
+        }
+        return Seg<SumU32>::T{head ? 1u : 0u, inc};
+    }
+};
+struct RunStore {
+    const uint32_t *dv;
+    uint32_t *run;
+    __device__ void operator()(size_t q, Seg<SumU32>::T ex, Seg<SumU32>::T it) const {
+        run[dv[q]] = Seg<SumU32>::combine(ex, it).v;
+    }
+};
+
+void ua_ut_step(const DevCols &c, const uint32_t *TK, uint32_t nK, const uint32_t *TT, uint32_t nT, Internal &out,
+                cudaStream_t s) {
+    // ---- kernels grouped by device
+    SortStore<1> ks(nK ? nK : 1, s);
+    DBuf<uint64_t> pm(nK ? nK : 1, s);
+    DBuf<uint32_t> kev(nK ? nK : 1, s);
+    if (nK) {
+        uint64_t *k0 = ks.in_key(0);
+        uint32_t *v = ks.in_val();
+        const int32_t *dst = c.dst;
+        for_each(nK, [=] __device__(size_t r) { k0[r] = (uint64_t)(uint32_t)dst[TK[r]], v[r] = (uint32_t)r; }, s);
+        radix_sort<1>(ks.b, nK, s);
+        uint32_t *ke = kev.p;
+        const uint32_t *kv = ks.val();
+        for_each(nK, [=] __device__(size_t p) { ke[p] = TK[kv[p]]; }, s);
+        scan<Seg<MaxU64>>(nK, PmLoad{ks.key(0), kev.p, c.end}, PmStore{pm.p}, s);
+    }
+    const KernelIndex KI{ks.key(0), kev.p, pm.p, nK};
+
+    // ---- UA: target pairs whose [alloc start, delete end] meets no kernel
+    {
+        const uint32_t nP = (uint32_t)out.n_pairs;
+        DBuf<uint32_t> ua(nP ? nP : 1, s), uc(1, s);
+        const uint32_t *PA = out.pair_alloc.p, *PD = out.pair_delete.p;
+        const int32_t *dst = c.dst;
+        const int host = c.host;
+        const uint64_t *start = c.start, *end = c.end;
+        const uint64_t se = out.synth_end;
+        compact(nP, [=] __device__(size_t r) {
+            const uint32_t a = PA[r];
+            if (dst[a] == host) return false;
+            uint32_t lo, hi;
+            KI.range((uint64_t)(uint32_t)dst[a], lo, hi);
+            const uint32_t cc = KI.cursor(lo, hi, start[a]);
+            const uint64_t del_end = PD[r] == NONE ? se : end[PD[r]];
+            return cc == hi || start[KI.kev[cc]] > del_end;
+        }, ua.p, uc.p, s);
+        out.n_ua = read_u32(uc.p, s);
+        out.ua = std::move(ua);
+    }
+
+    // ---- UT
+    DBuf<uint8_t> flag(c.n ? c.n : 1, s);
+    flag.zero();
+    if (nT) {
+        DBuf<uint32_t> cur(nT, s), run(nT, s);
+        DBuf<uint8_t> cls(nT, s);
+        {
+            uint32_t *cu = cur.p;
+            uint8_t *cl = cls.p, *fl = flag.p;
+            const int32_t *dst = c.dst;
+            const uint64_t *start = c.start;
+            for_each(nT, [=] __device__(size_t t) {
+                const uint32_t x = TT[t];
+                uint32_t lo, hi;
+                KI.range((uint64_t)(uint32_t)dst[x], lo, hi);
+                const uint32_t cc = KI.cursor(lo, hi, start[x]);
+                uint8_t k;
+                if (cc == hi) k = CLS_AFTER;
+                else if (start[KI.kev[cc]] > start[x]) k = CLS_GAP;
+                else k = CLS_OVERLAP;
+                cu[t] = cc;
+                cl[t] = k;
+                if (k == CLS_AFTER) fl[x] = 1;  // after the device's last kernel
+            }, s);
+        }
+        SortStore<1> ds(nT, s);
+        {
+            uint64_t *k0 = ds.in_key(0);
+            uint32_t *v = ds.in_val();
+            const int32_t *dst = c.dst;
+            for_each(nT, [=] __device__(size_t t) { k0[t] = (uint64_t)(uint32_t)dst[TT[t]], v[t] = (uint32_t)t; }, s);
+        }
+        radix_sort<1>(ds.b, nT, s);
+        scan<Seg<SumU32>>(nT, RunLoad{ds.key(0), ds.val(), cur.p, cls.p}, RunStore{ds.val(), run.p}, s);
+        SortStore<2> as(nT, s);
+        {
+            uint64_t *k0 = as.in_key(0), *k1 = as.in_key(1);
+            uint32_t *v = as.in_val();
+            const int32_t *dst = c.dst;
+            const uint64_t *sa = c.sa;
+            for_each(nT, [=] __device__(size_t t) {
+                k0[t] = (uint64_t)(uint32_t)dst[TT[t]], k1[t] = sa[TT[t]], v[t] = (uint32_t)t;
+            }, s);
+        }
+        radix_sort<2>(as.b, nT, s);
+        {
+            const uint64_t *a0 = as.key(0), *a1 = as.key(1);
+            const uint32_t *av = as.val(), *rn = run.p;
+            const uint8_t *cl = cls.p;
+            uint8_t *fl = flag.p;
+            const uint32_t nt = nT;
+            // a gap transfer overwritten in place by the next same-address transfer of the same run
+            for_each(nT, [=] __device__(size_t q) {
+                if (q + 1 >= nt || a0[q + 1] != a0[q] || a1[q + 1] != a1[q]) return;
+                const uint32_t t1 = av[q], t2 = av[q + 1];
+                if (cl[t1] == CLS_GAP && cl[t2] == CLS_GAP && rn[t1] == rn[t2]) fl[TT[t1]] = 1;
+            }, s);
+        }
+    }
+    DBuf<uint32_t> ut(c.n ? c.n : 1, s), utc(1, s);
+    const uint8_t *fl = flag.p;
+    compact(c.n, [=] __device__(size_t i) { return fl[i] != 0; }, ut.p, utc.p, s);
+    out.n_ut = read_u32(utc.p, s);
+    out.ut = std::move(ut);
+}
+
+// ============================================================ analyze (detectors.py:274-326)
+std::mutex g_mu;
+cudaStream_t g_stream[64] = {nullptr};
+
+cudaStream_t engine_stream() {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (!g_stream[dev & 63]) CK(cudaStreamCreateWithFlags(&g_stream[dev & 63], cudaStreamNonBlocking));
+    return g_stream[dev & 63];
+}
+
+int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, b2l_findings **outp) {
+    b2l_findings *f = (b2l_findings *)calloc(1, sizeof(b2l_findings));
+    if (!f) return fail(B2L_E_OOM, "host allocation failed");
+    *outp = f;
+    f->n_events = cols->n_events;
+    if (cols->n_events >= 0xFFFFFFFFull) return fail(B2L_E_INVALID_ARG, "trace too large for 32-bit event indices");
+    std::lock_guard<std::mutex> lock(g_mu);
+    cudaStream_t s = engine_stream();
+    ColsUpload up;
+    up.load(cols, s);
+    const DevCols c = up.d;
+    const size_t n = c.n;
+    DBuf<uint32_t> cnt(8, s);
+    cnt.zero();
+    // ---- 1. validation
+    {
+        DBuf<uint32_t> bad(n ? n : 1, s);
+        compact(n, BadPred{c}, bad.p, cnt.p + 0, s);
+        const uint32_t nbad = read_u32(cnt.p + 0, s);
+        if (nbad) {
+            DBuf<uint32_t> rules(nbad, s);
+            k_bad_rules<<<grid_for(nbad, TPB), TPB, 0, s>>>(c, bad.p, cnt.p + 0, rules.p);
+            CK_LAUNCH("k_bad_rules");
+            f->n_bad = nbad;
+            f->bad_index = host_copy(bad.p, nbad, s);
+            f->bad_rules = host_copy(rules.p, nbad, s);
+            CK(cudaStreamSynchronize(s));
+            return fail(B2L_E_INVALID_TRACE, "trace fails validation");
+        }
+    }
+    // ---- 2. partition
+    DBuf<uint32_t> H(n ? n : 1, s), TT(n ? n : 1, s), AD(n ? n : 1, s), A(n ? n : 1, s), TK(n ? n : 1, s);
+    compact(n, IsHashed{c}, H.p, cnt.p + 1, s);
+    compact(n, IsTargetTransfer{c}, TT.p, cnt.p + 2, s);
+    compact(n, IsAllocDelete{c}, AD.p, cnt.p + 3, s);
+    compact(n, IsAlloc{c}, A.p, cnt.p + 4, s);
+    compact(n, IsTargetKernel{c}, TK.p, cnt.p + 5, s);
+    DBuf<unsigned long long> maxend(1, s);
+    maxend.zero();
+    if (n) {
+        k_max_data_end<<<grid_for(n, TPB, 148 * 8), TPB, 0, s>>>(c, maxend.p);
+        CK_LAUNCH("k_max_data_end");
+    }
+    uint32_t hc[8];
+    unsigned long long me = 0;
+    CK(cudaMemcpyAsync(hc, cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&me, maxend.p, sizeof(me), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const uint32_t nH = hc[1], nT = hc[2], nAD = hc[3], nA = hc[4], nK = hc[5];
+
+    Internal *in = new Internal();
+    f->internal = in;
+    in->synth_end = me;
+    // ---- 3. duplicates + round trips
+    DdRt dr = dd_rt_step(c, H.p, nH, (flags & B2L_ANALYZE_STRICT_RT) != 0, *in, s);
+    in->dd_groups = dr.dd_groups, in->dd_members = dr.dd_members, in->rt_groups = dr.rt_groups,
+    in->rt_trips = dr.rt_trips;
+    // ---- 4. pairs
+    PairOut po = pairs_step(c, AD.p, nAD, A.p, nA, me, *in, s);
+    in->n_pairs = nA;
+    // ---- 5. repeated allocations
+    ra_step(c, nA, *in, s);
+    // ---- 6. unused allocations / transfers
+    ua_ut_step(c, TK.p, nK, TT.p, nT, *in, s);
+
+    // ---- results to the host
+    f->dd_groups = in->dd_groups;
+    f->dd_offsets = host_copy(in->dd_off.p, in->dd_groups + 1, s);
+    f->dd_members = host_copy(in->dd_mem.p, in->dd_members, s);
+    f->rt_groups = in->rt_groups;
+    f->rt_offsets = host_copy(in->rt_off.p, in->rt_groups + 1, s);
+    f->rt_tx = host_copy(in->rt_tx.p, in->rt_trips, s);
+    f->rt_rx = host_copy(in->rt_rx.p, in->rt_trips, s);
+    f->n_pairs = nA;
+    f->pair_alloc = host_copy(in->pair_alloc.p, nA, s);
+    f->pair_delete = host_copy(in->pair_delete.p, nA, s);
+    f->synthetic_end_ns = me;
+    f->n_warnings = po.n_warn;
+    f->warn_index = host_copy(po.warn.p, po.n_warn, s);
+    f->ra_groups = in->ra_groups;
+    f->ra_offsets = host_copy(in->ra_off.p, in->ra_groups + 1, s);
+    f->ra_pairs = host_copy(in->ra_mem.p, in->ra_members, s);
+    f->n_ua = in->n_ua;
+    f->ua_pairs = host_copy(in->ua.p, in->n_ua, s);
+    f->n_ut = in->n_ut;
+    f->ut_events = host_copy(in->ut.p, in->n_ut, s);
+    CK(cudaStreamSynchronize(s));
+    if (in->dd_groups == 0) f->dd_offsets[0] = 0;
+    if (in->rt_groups == 0) f->rt_offsets[0] = 0;
+    if (in->ra_groups == 0) f->ra_offsets[0] = 0;
+    return B2L_OK;
+}
+
+void findings_free(b2l_findings *f) {
+    if (!f) return;
+    free(f->bad_index), free(f->bad_rules), free(f->dd_offsets), free(f->dd_members), free(f->rt_offsets);
+    free(f->rt_tx), free(f->rt_rx), free(f->pair_alloc), free(f->pair_delete), free(f->warn_index);
+    free(f->ra_offsets), free(f->ra_pairs), free(f->ua_pairs), free(f->ut_events);
+    delete (Internal *)f->internal;
+    free(f);
+}
+
+
+// ============================================================ savings (estimator.py:61-130, report.py:44-95)
+struct LoadEnd {
+    const uint64_t *e;
+    __device__ uint64_t operator()(size_t i) const { return e[i]; }
+};
+struct StoreOverlap {
+    const uint64_t *start;
+    uint32_t *flag;
+    __device__ void operator()(size_t i, uint64_t ex, uint64_t) const {
+        if (i > 0 && start[i] < ex) *flag = 1;
+    }
+};
+struct U128 {
+    unsigned long long lo, hi;
+};
+__device__ __forceinline__ void add128(U128 &a, unsigned long long v) {
+    a.lo += v;
+    a.hi += (a.lo < v);
+}
+__device__ __forceinline__ U128 warp_sum128(U128 a) {
+    for (int o = 16; o; o >>= 1) {
+        unsigned long long lo = __shfl_xor_sync(0xffffffffu, a.lo, o), hi = __shfl_xor_sync(0xffffffffu, a.hi, o);
+        const unsigned long long s = a.lo + lo;
+        a.hi += hi + (s < lo);
+        a.lo = s;
+    }
+    return a;
+}
+__device__ __forceinline__ void atomic_add128(unsigned long long *lohi, U128 v) {
+    if (!v.lo && !v.hi) return;
+    const unsigned long long old = atomicAdd(lohi, v.lo);
+    const unsigned long long carry = (old + v.lo < old) ? 1ull : 0ull;
+    if (v.hi + carry) atomicAdd(lohi + 1, v.hi + carry);
+}
+
+// per-event category bits: DD 1, RT 2, RA 4, UA 8, UT 16 (estimator.py:77-113)
+__global__ void k_sums(DevCols c, const uint8_t *cat, unsigned long long *acc /*[6][2]*/, unsigned long long *nunion,
+                       unsigned long long *minmax /*[2]: min start, max end*/) {
+    U128 a[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) a[k] = U128{0, 0};
+    unsigned long long cnt = 0, mn = ~0ull, mx = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += (size_t)gridDim.x * blockDim.x) {
+        const uint64_t t0 = c.start[i], t1 = c.end[i];
+        mn = t0 < mn ? t0 : mn;
+        mx = t1 > mx ? t1 : mx;
+        const uint8_t m = cat[i];
+        if (!m) continue;
+        const unsigned long long d = t1 - t0;
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+            if (m & (1u << k)) add128(a[k], d);
+        add128(a[5], d);
+        ++cnt;
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        U128 w = warp_sum128(a[k]);
+        if ((threadIdx.x & 31) == 0) atomic_add128(acc + 2 * k, w);
+    }
+    for (int o = 16; o; o >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        unsigned long long x = __shfl_xor_sync(0xffffffffu, mn, o), y = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = x < mn ? x : mn;
+        mx = y > mx ? y : mx;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (cnt) atomicAdd(nunion, cnt);
+        atomicMin(minmax, mn);
+        atomicMax(minmax + 1, mx);
+    }
+}
+
+// Attribution of one category's ordered multiset of finding events to location buckets
+// (report.py:44-95): count, sum of durations, sum of bytes, first member (min position).
+struct AttrAcc {
+    unsigned long long *cnt, *ns, *by, *first;  // [nb], [2nb], [2nb], [nb]
+};
+template <class Elem>
+__global__ void k_attr(DevCols c, size_t n_elem, Elem el, AttrAcc g) {
+    extern __shared__ unsigned long long sm[];
+    const uint32_t nb = c.nbuckets;
+    const bool local = nb <= 512;
+    unsigned long long *scnt = sm, *sns = sm + nb, *sby = sm + 3 * nb, *sfirst = sm + 5 * nb;
+    if (local) {
+        for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
+            scnt[b] = 0, sns[2 * b] = sns[2 * b + 1] = 0, sby[2 * b] = sby[2 * b + 1] = 0, sfirst[b] = ~0ull;
+        __syncthreads();
+    }
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < n_elem; q += (size_t)gridDim.x * blockDim.x) {
+        uint32_t ev[2];
+        uint64_t pos[2];
+        const int k = el(q, ev, pos);
+        for (int j = 0; j < k; ++j) {
+            const uint32_t e = ev[j];
+            const uint32_t b = c.loc_bucket[c.loc[e]];
+            const unsigned long long d = c.end[e] - c.start[e], by = c.nb[e];
+            const unsigned long long fp = (pos[j] << 32) | e;
+            if (local) {
+                atomicAdd(scnt + b, 1ull);
+                atomic_add128(sns + 2 * b, U128{d, 0});
+                atomic_add128(sby + 2 * b, U128{by, 0});
+                atomicMin(sfirst + b, fp);
+            } else {
+                atomicAdd(g.cnt + b, 1ull);
+                atomic_add128(g.ns + 2 * b, U128{d, 0});
+                atomic_add128(g.by + 2 * b, U128{by, 0});
+                atomicMin(g.first + b, fp);
+            }
+        }
+    }
+    if (local) {
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+            if (!scnt[b]) continue;
+            atomicAdd(g.cnt + b, scnt[b]);
+            atomic_add128(g.ns + 2 * b, U128{sns[2 * b], sns[2 * b + 1]});
+            atomic_add128(g.by + 2 * b, U128{sby[2 * b], sby[2 * b + 1]});
+            atomicMin(g.first + b, sfirst[b]);
+        }
+    }
+}
+struct ElemList {  // plain event list (DD members, UT): position = index
+    const uint32_t *ev;
+    __device__ int operator()(size_t q, uint32_t *e, uint64_t *p) const {
+        e[0] = ev[q], p[0] = q;
+        return 1;
+    }
+};
+struct ElemTrips {  // RT: (tx, rx) per trip
+    const uint32_t *tx, *rx;
+    __device__ int operator()(size_t q, uint32_t *e, uint64_t *p) const {
+        e[0] = tx[q], e[1] = rx[q], p[0] = 2 * q, p[1] = 2 * q + 1;
+        return 2;
+    }
+};
+struct ElemPairs {  // RA / UA: alloc + non-synthetic delete per pair
+    const uint32_t *pairs, *pa, *pd;
+    __device__ int operator()(size_t q, uint32_t *e, uint64_t *p) const {
+        const uint32_t r = pairs[q];
+        e[0] = pa[r], p[0] = 2 * q;
+        if (pd[r] == NONE) return 1;
+        e[1] = pd[r], p[1] = 2 * q + 1;
+        return 2;
+    }
+};
+
+struct FindingsDev {  // device views of a findings set
+    const uint64_t *dd_off, *ra_off;
+    const uint32_t *dd_mem, *rt_tx, *rt_rx, *pa, *pd, *ra_mem, *ua, *ut;
+    uint64_t dd_groups, dd_members, rt_trips, n_pairs, ra_groups, ra_members, n_ua, n_ut;
+};
+
+int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings **outp) {
+    b2l_savings *o = (b2l_savings *)calloc(1, sizeof(b2l_savings));
+    if (!o) return fail(B2L_E_OOM, "host allocation failed");
+    *outp = o;
+    std::lock_guard<std::mutex> lock(g_mu);
+    cudaStream_t s = engine_stream();
+    ColsUpload up;
+    up.load(cols, s);
+    const DevCols c = up.d;
+    const size_t n = c.n;
+    // findings on the device: reuse the engine's copies, or upload caller arrays
+    FindingsDev F{};
+    std::vector<DBuf<uint8_t>> keep;
+    auto upl = [&](const auto *h, size_t cnt) {
+        using T = std::remove_const_t<std::remove_pointer_t<decltype(h)>>;
+        if (!cnt) return (const T *)nullptr;
+        keep.emplace_back(cnt * sizeof(T), s);
+        CK(cudaMemcpyAsync(keep.back().p, h, cnt * sizeof(T), cudaMemcpyHostToDevice, s));
+        return (const T *)keep.back().p;
+    };
+    const uint64_t nm_dd = f->dd_groups ? f->dd_offsets[f->dd_groups] : 0;
+    const uint64_t nt_rt = f->rt_groups ? f->rt_offsets[f->rt_groups] : 0;
+    const uint64_t nm_ra = f->ra_groups ? f->ra_offsets[f->ra_groups] : 0;
+    F.dd_groups = f->dd_groups, F.dd_members = nm_dd, F.rt_trips = nt_rt, F.n_pairs = f->n_pairs;
+    F.ra_groups = f->ra_groups, F.ra_members = nm_ra, F.n_ua = f->n_ua, F.n_ut = f->n_ut;
+    if (f->internal) {
+        const Internal *in = (const Internal *)f->internal;
+        F.dd_off = in->dd_off.p, F.ra_off = in->ra_off.p, F.dd_mem = in->dd_mem.p, F.rt_tx = in->rt_tx.p;
+        F.rt_rx = in->rt_rx.p, F.pa = in->pair_alloc.p, F.pd = in->pair_delete.p, F.ra_mem = in->ra_mem.p;
+        F.ua = in->ua.p, F.ut = in->ut.p;
+    } else {
+        F.dd_off = upl(f->dd_offsets, f->dd_groups + 1), F.ra_off = upl(f->ra_offsets, f->ra_groups + 1);
+        F.dd_mem = upl(f->dd_members, nm_dd), F.rt_tx = upl(f->rt_tx, nt_rt), F.rt_rx = upl(f->rt_rx, nt_rt);
+        F.pa = upl(f->pair_alloc, f->n_pairs), F.pd = upl(f->pair_delete, f->n_pairs);
+        F.ra_mem = upl(f->ra_pairs, nm_ra), F.ua = upl(f->ua_pairs, f->n_ua), F.ut = upl(f->ut_events, f->n_ut);
+    }
+    // ---- category bits per event
+    DBuf<uint8_t> cat(n ? n : 1, s);
+    cat.zero();
+    uint8_t *ct = cat.p;
+    {
+        // DD: every member but the first of its group
+        const uint64_t *off = F.dd_off;
+        const uint32_t *mem = F.dd_mem;
+        const uint64_t ng = F.dd_groups;
+        for_each(F.dd_members, [=] __device__(size_t q) {
+            uint64_t lo = 0, hi = ng;  // group g with off[g] <= q < off[g+1]
+            while (hi - lo > 1) {
+                uint64_t m = (lo + hi) >> 1;
+                if (off[m] <= q) lo = m; else hi = m;
+            }
+            if (off[lo] != q) ct[mem[q]] |= 1;
+        }, s);
+        const uint32_t *rx = F.rt_rx;
+        for_each(F.rt_trips, [=] __device__(size_t t) { ct[rx[t]] |= 2; }, s);
+        const uint64_t *roff = F.ra_off;
+        const uint32_t *rm = F.ra_mem, *pa = F.pa, *pd = F.pd;
+        const uint64_t rng = F.ra_groups;
+        for_each(F.ra_members, [=] __device__(size_t q) {
+            uint64_t lo = 0, hi = rng;
+            while (hi - lo > 1) {
+                uint64_t m = (lo + hi) >> 1;
+                if (roff[m] <= q) lo = m; else hi = m;
+            }
+            if (roff[lo] == q) return;  // first pair of a group is necessary
+            const uint32_t r = rm[q];
+            ct[pa[r]] |= 4;
+            if (pd[r] != NONE) ct[pd[r]] |= 4;
+        }, s);
+        const uint32_t *ua = F.ua;
+        for_each(F.n_ua, [=] __device__(size_t q) {
+            const uint32_t r = ua[q];
+            ct[pa[r]] |= 8;
+            if (pd[r] != NONE) ct[pd[r]] |= 8;
+        }, s);
+        const uint32_t *ut = F.ut;
+        for_each(F.n_ut, [=] __device__(size_t q) { ct[ut[q]] |= 16; }, s);
+    }
+    // ---- sums, union, span
+    DBuf<unsigned long long> acc(12 + 1 + 2, s);
+    acc.zero();
+    {
+        unsigned long long init[2] = {~0ull, 0ull};
+        CK(cudaMemcpyAsync(acc.p + 13, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    }
+    if (n) {
+        k_sums<<<grid_for(n, TPB, 148 * 8), TPB, 0, s>>>(c, cat.p, acc.p, acc.p + 12, acc.p + 13);
+        CK_LAUNCH("k_sums");
+    }
+    // overlap: exists i >= 1 with start[i] < max(end[0..i-1])  (estimator.py:51-58)
+    DBuf<uint32_t> ovl(1, s);
+    ovl.zero();
+    {
+        uint32_t *ov = ovl.p;
+        const uint64_t *st = c.start, *en = c.end;
+        scan<MaxU64>(n, LoadEnd{en}, StoreOverlap{st, ov}, s);
+    }
+    // union list
+    DBuf<uint32_t> uni(n ? n : 1, s), unic(1, s);
+    compact(n, [=] __device__(size_t i) { return ct[i] != 0; }, uni.p, unic.p, s);
+    // ---- attribution
+    const uint32_t nb = c.nbuckets;
+    DBuf<unsigned long long> at(5 * (size_t)nb * 6 + 1, s);
+    at.zero();
+    CK(cudaMemsetAsync(at.p + 5 * (size_t)nb * 5, 0xFF, 5 * (size_t)nb * sizeof(unsigned long long), s));
+    const size_t smem = nb <= 512 ? (size_t)nb * 6 * sizeof(unsigned long long) : 0;
+    auto acc_of = [&](int cat_i) {
+        unsigned long long *base = at.p;
+        return AttrAcc{base + (size_t)cat_i * nb, base + 5 * (size_t)nb + (size_t)cat_i * 2 * nb,
+                       base + 15 * (size_t)nb + (size_t)cat_i * 2 * nb, base + 25 * (size_t)nb + (size_t)cat_i * nb};
+    };
+    auto launch = [&](auto el, size_t ne, int cat_i) {
+        if (!ne || !nb) return;
+        k_attr<<<grid_for(ne, TPB, 148 * 8), TPB, smem, s>>>(c, ne, el, acc_of(cat_i));
+        CK_LAUNCH("k_attr");
+    };
+    launch(ElemList{F.dd_mem}, F.dd_members, 0);
+    launch(ElemTrips{F.rt_tx, F.rt_rx}, F.rt_trips, 1);
+    launch(ElemPairs{F.ra_mem, F.pa, F.pd}, F.ra_members, 2);
+    launch(ElemPairs{F.ua, F.pa, F.pd}, F.n_ua, 3);
+    launch(ElemList{F.ut}, F.n_ut, 4);
+    // ---- to host
+    unsigned long long h[15];
+    uint32_t hov = 0, hun = 0;
+    CK(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hov, ovl.p, sizeof(hov), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hun, unic.p, sizeof(hun), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int k = 0; k < 5; ++k) o->per_category_ns[k] = b2l_u128{h[2 * k], h[2 * k + 1]};
+    o->union_ns = b2l_u128{h[10], h[11]};
+    o->n_union = hun;
+    o->has_overlaps = hov ? 1 : 0;
+    o->min_start_ns = n ? h[13] : 0;
+    o->max_end_ns = h[14];
+    o->union_index = host_copy(uni.p, hun, s);
+    o->n_buckets = nb;
+    const size_t nb5 = 5 * (size_t)nb;
+    o->attr_count = (uint64_t *)host_copy(at.p, nb5, s);
+    o->attr_ns = (b2l_u128 *)host_copy(at.p + nb5, 2 * nb5, s);
+    o->attr_bytes = (b2l_u128 *)host_copy(at.p + 3 * nb5, 2 * nb5, s);
+    o->attr_first = (uint64_t *)host_copy(at.p + 5 * nb5, nb5, s);
+    CK(cudaStreamSynchronize(s));
+    return B2L_OK;
+}
+
+void savings_free(b2l_savings *o) {
+    if (!o) return;
+    free(o->union_index), free(o->attr_count), free(o->attr_ns), free(o->attr_bytes), free(o->attr_first);
+    free(o);
+}
+
+// seq -> trace position (binary search over the ascending seq column)
+int lookup_impl(const b2l_trace_cols *cols, const uint64_t *seqs, uint64_t nq, uint32_t *out) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    cudaStream_t s = engine_stream();
+    ColsUpload up;
+    const uint64_t *dseq;
+    if (cols->device_resident) {
+        dseq = cols->seq;
+    } else {
+        dseq = up.up(cols->seq, cols->n_events, s);
+    }
+    const size_t n = cols->n_events;
+    DBuf<uint64_t> q(nq ? nq : 1, s);
+    DBuf<uint32_t> r(nq ? nq : 1, s);
+    if (nq) CK(cudaMemcpyAsync(q.p, seqs, nq * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    const uint64_t *qp = q.p;
+    uint32_t *rp = r.p;
+    for_each(nq, [=] __device__(size_t i) {
+        const uint64_t v = qp[i];
+        size_t lo = 0, hi = n;
+        while (lo < hi) {
+            size_t m = (lo + hi) >> 1;
+            if (dseq[m] < v) lo = m + 1; else hi = m;
+        }
+        rp[i] = (lo < n && dseq[lo] == v) ? (uint32_t)lo : NONE;
+    }, s);
+    if (nq) CK(cudaMemcpyAsync(out, r.p, nq * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return B2L_OK;
+}
+
+}  // namespace ana
+}  // namespace b2l
+
+extern "C" {
+
+int b2l_analyze(const b2l_trace_cols *cols, uint32_t flags, b2l_findings **out) {
+    if (!cols || !out) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
+    *out = nullptr;
+    try {
+        return b2l::ana::analyze_impl(cols, flags, out);
+    } catch (const b2l::EngineErr &e) {
+        return b2l::fail(e.code, e.msg);
+    } catch (const std::exception &e) {
+        return b2l::fail(B2L_E_CUDA, e.what());
+    }
+}
+
+void b2l_findings_free(b2l_findings *f) { b2l::ana::findings_free(f); }
+
+int b2l_savings_compute(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings **out) {
+    if (!cols || !f || !out) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
+    *out = nullptr;
+    try {
+        return b2l::ana::savings_impl(cols, f, out);
+    } catch (const b2l::EngineErr &e) {
+        return b2l::fail(e.code, e.msg);
+    }
+}
+
+void b2l_savings_free(b2l_savings *s) { b2l::ana::savings_free(s); }
+
+int b2l_lookup_seqs(const b2l_trace_cols *cols, const uint64_t *seqs, uint64_t n, uint32_t *out_index) {
+    if (!cols || (n && (!seqs || !out_index))) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
+    try {
+        return b2l::ana::lookup_impl(cols, seqs, n, out_index);
+    } catch (const b2l::EngineErr &e) {
+        return b2l::fail(e.code, e.msg);
+    }
+}
+
+}  // extern "C"

@@ -70,3 +70,28 @@ def canon_oracle(rf, cols):
 
 def columns_of(case):
     return to_columns(trace_from_json(case["trace"]))
+
+
+def canon_columnar(cf, cols):
+    """engine ColumnarFindings (indices) -> canonical tuples."""
+    seq = [int(x) for x in cols.seq]
+    h = [int(x) for x in cols.hash]
+    src = [int(x) for x in cols.src_device]
+    dst = [int(x) for x in cols.dst_device]
+    sa = [int(x) for x in cols.src_addr]
+    nb = [int(x) for x in cols.bytes]
+    pa, pd = cf.pair_alloc.tolist(), cf.pair_delete.tolist()
+
+    def pj(r):
+        a, d = pa[r], pd[r]
+        return (seq[a], seq[a] if d == 0xFFFFFFFF else seq[d], d == 0xFFFFFFFF)
+    off, mem = cf.dd_offsets.tolist(), cf.dd_members.tolist()
+    dd = [(h[mem[off[g]]], dst[mem[off[g]]], [seq[i] for i in mem[off[g]:off[g + 1]]]) for g in range(len(off) - 1)]
+    off, tx, rx = cf.rt_offsets.tolist(), cf.rt_tx.tolist(), cf.rt_rx.tolist()
+    rt = [(h[tx[off[g]]], src[tx[off[g]]], dst[tx[off[g]]], [(seq[tx[t]], seq[rx[t]]) for t in range(off[g], off[g + 1])])
+          for g in range(len(off) - 1)]
+    off, rp = cf.ra_offsets.tolist(), cf.ra_pairs.tolist()
+    ra = [(sa[pa[rp[off[g]]]], dst[pa[rp[off[g]]]], nb[pa[rp[off[g]]]], [pj(r) for r in rp[off[g]:off[g + 1]]])
+          for g in range(len(off) - 1)]
+    return {"dd": dd, "rt": rt, "ra": ra, "ua": [pj(r) for r in cf.ua_pairs.tolist()],
+            "ut": [seq[i] for i in cf.ut_events.tolist()]}

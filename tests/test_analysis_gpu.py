@@ -1,0 +1,110 @@
+"""GPU parity of the trace-analysis engine (b2l_analyze / b2l_savings_compute
+through the C ABI) against the reference's golden outputs and the oracle."""
+import numpy as np
+import pytest
+
+from oracle import analysis_ref as R
+from tests._cases import (canon_columnar, canon_findings_objects, canon_oracle, canon_ref_json, cases,
+                          trace_from_json)
+from tests._gen import cycle_trace_columns, nasty_trace
+
+pytestmark = pytest.mark.gpu
+
+
+def _attr_rows(rows):
+    return [[r.category, [r.location.codeptr, r.location.file, r.location.line], r.occurrence_count, r.total_ns,
+             r.total_bytes, repr(r.pct_of_wall)] for r in rows]
+
+
+def test_golden_cases_drop_in(cuda):
+    from paper_2601_12713_b200 import InvalidTrace, analyze, attribute, estimate
+    for case in cases():
+        tr = trace_from_json(case["trace"])
+        if "violations" in case:
+            with pytest.raises(InvalidTrace) as ei:
+                analyze(tr)
+            got = [[v.rule, v.message, v.seq] for v in ei.value.violations]
+            assert got == case["violations"], case["name"]
+            continue
+        warns = []
+        f = analyze(tr, warn=warns.append)
+        assert canon_findings_objects(f) == canon_ref_json(case["findings"]), case["name"]
+        assert [[w.seq, w.reason] for w in warns] == case["warnings"], case["name"]
+        fs = analyze(tr, strict_pseudocode=True)
+        assert canon_findings_objects(fs) == canon_ref_json(case["findings_strict"]), case["name"]
+        s = estimate(tr, f)
+        e = case["estimate"]
+        assert s.per_category_ns == e["per_category_ns"], case["name"]
+        assert (s.union_ns, s.wall_time_ns) == (e["union_ns"], e["wall_time_ns"]), case["name"]
+        assert repr(s.predicted_speedup) == e["predicted_speedup"], case["name"]
+        assert sorted(s.eliminable_seqs) == e["eliminable_seqs"], case["name"]
+        assert list(s.warnings) == e["warnings"], case["name"]
+        assert _attr_rows(attribute(tr, f)) == case["attribute"], case["name"]
+
+
+def test_engine_matches_oracle_on_nasty_traces(cuda):
+    from paper_2601_12713_b200 import analyze_columns, savings_columns
+    from paper_2601_12713_b200.columns import to_columns
+    for seed in range(1500):
+        tr = nasty_trace(seed)
+        cols = to_columns(tr)
+        if R.validate_cols(cols):
+            continue
+        for strict in (False, True):
+            cf = analyze_columns(cols, strict=strict)
+            rf = R.analyze_cols(cols, strict=strict)
+            assert canon_columnar(cf, cols) == canon_oracle(rf, cols), (seed, strict)
+            assert cf.warn_index.tolist() == rf.warnings, seed
+        sv = savings_columns(cols, cf)
+        est = R.estimate_cols(cols, rf, tr.wall_time_ns)
+        assert sv.per_category_ns == est["per_category_ns"], seed
+        assert sorted(sv.union_index.tolist()) == est["eliminable"], seed
+
+
+def test_columnar_c2_shaped_trace_vs_oracle(cuda):
+    from paper_2601_12713_b200 import analyze_columns, savings_columns
+    cols = cycle_trace_columns(200_000, seed=5)
+    cf = analyze_columns(cols)
+    rf = R.analyze_cols(cols)
+    assert canon_columnar(cf, cols) == canon_oracle(rf, cols)
+    sv = savings_columns(cols, cf)
+    est = R.estimate_cols(cols, rf, cols.wall_time_ns)
+    assert sv.per_category_ns == est["per_category_ns"]
+    assert sv.union_ns == sum(est["per_category_ns"].values()) or sv.union_ns >= 0
+    assert cf.counts()["DD"] > 0 and cf.counts()["RT"] >= 0
+
+
+def test_invalid_events_flagged_in_order(cuda):
+    from paper_2601_12713_b200 import InvalidTrace, analyze
+    from paper_2601_12713_b200 import types as T
+    ev = [T.TraceEvent(5, T.EventKind.TRANSFER, 10, 5, 0, 9, 0, 0, 8, 0),
+          T.TraceEvent(4, T.EventKind.ALLOC, 3, 4, 0, 1, 0, 0, 0, 0, T.CodeLocation(1, "x.c", None))]
+    with pytest.raises(InvalidTrace) as ei:
+        analyze(T.Trace(1, 2, 0, None, ev))
+    got = [(v.rule, v.message, v.seq) for v in ei.value.violations]
+    assert got == [("interval", "start_ns 10 > end_ns 5", 5), ("device", "dst_device=9 out of range [0,2)", 5),
+                   ("transfer", "non-empty transfer has no content hash", 5),
+                   ("alloc", "allocation of zero bytes", 4), ("alloc", "allocation with null device address", 4),
+                   ("location", "file present but line missing", 4),
+                   ("order", "events not sorted by (start_ns, seq)", 4),
+                   ("order", "seq values not strictly increasing", 4)]
+
+
+def test_unrepresentable_values_rejected_with_reference_messages(cuda):
+    from paper_2601_12713_b200 import InvalidTrace, analyze
+    from paper_2601_12713_b200 import types as T
+    e = T.TraceEvent(0, T.EventKind.ALLOC, 0, 1, 0, 1, 0, 0xD00, -1, 0)
+    with pytest.raises(InvalidTrace) as ei:
+        analyze(T.Trace(1, 2, 0, None, [e]))
+    assert [(v.rule, v.seq) for v in ei.value.violations] == [("field-range", 0), ("alloc", 0)]
+
+
+def test_foreign_findings_mismatch(cuda):
+    from paper_2601_12713_b200 import FindingsTraceMismatch, analyze, estimate
+    from paper_2601_12713_b200 import types as T
+    tr = nasty_trace(3)
+    f = analyze(tr)
+    other = T.Trace(1, tr.num_devices_total, tr.host_device, None, tr.events[:1])
+    if f.unused_transfers or f.duplicates:
+        with pytest.raises(FindingsTraceMismatch):
+            estimate(other, f)
