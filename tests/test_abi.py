@@ -9,7 +9,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "b2l.h")).read()
-    return sorted(set(re.findall(r"\b(b2l_[a-z0-9_]+)\s*\(", src)))
+    # function declarations: "<type> [*]b2l_name(" at the start of a line
+    return sorted(set(re.findall(r"^(?:int|void|const char \*)\s*\*?(b2l_[a-z0-9_]+)\(", src, re.M)))
 
 
 def test_library_exports_header_symbols():
