@@ -61,7 +61,7 @@ def cycle_trace_columns(n_events, n_targets=8, seed=2, dup_frac=0.25, n_host_add
     start[1:] = np.cumsum(dur)[:-1]
     end = start + dur
     d = np.repeat(dev, 5)
-    src = np.where((state == 3), d, 0).astype(np.int32)
+    src = np.where((state == 3) | (state == 2), d, 0).astype(np.int32)
     dst = np.where((state == 3), 0, d).astype(np.int32)
     haddr = (0x7F0000000000 + (rng.integers(0, n_host_addrs, ncyc) * 0x100000)).astype(np.uint64)
     daddr = (0xD00000000000 + dev.astype(np.uint64) * 0x1000000).astype(np.uint64)
@@ -79,7 +79,8 @@ def cycle_trace_columns(n_events, n_targets=8, seed=2, dup_frac=0.25, n_host_add
     back = (np.arange(ncyc, dtype=np.uint64) + np.uint64(1 << 40)) * np.uint64(0xBF58476D1CE4E5B9) | np.uint64(1)
     hashv = np.zeros(n, dtype=np.uint64)
     hashv[state == 1] = hh
-    hashv[state == 3] = back
+    unmodified = rng.random(ncyc) < 0.3  # kernel left the array unchanged: D2H returns the H2D content
+    hashv[state == 3] = np.where(unmodified, hh, back)
     seq = np.arange(n, dtype=np.uint64)
     return columns_from_arrays(n_targets + 1, 0, seq, start, end, src, dst, kind, src_addr, dst_addr, nbytes, hashv,
                                wall_time_ns=int(end[-1]) if n else 0)
