@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--n-events", type=int, default=N_EVENTS)
+    ap.add_argument("--no-analysis", action="store_true")
     return ap.parse_args()
 
 
@@ -267,6 +269,97 @@ def run_ours(args, rank, world, local):
     return rec
 
 
+# ----------------------------------------------------------------------------- analysis (C2 1M-event trace)
+N_EVENTS = 1_000_000
+EVENT_BYTES = 64  # algorithmic bytes per event: one read of the packed row
+
+
+def run_analysis_ours(args, rank, world, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_12713_b200.analysis import DeviceColumns, analyze_columns, savings_columns
+    from paper_2601_12713_b200.synth import c2_trace
+
+    dev = torch.device("cuda", local)
+    cols = c2_trace(args.n_events, seed=SEED + rank)
+    dcols = DeviceColumns(cols, dev)
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        cf = analyze_columns(dcols)
+        savings_columns(dcols, cf)
+    verified = None
+    if rank == 0 and not args.no_cpu:
+        from oracle import analysis_ref as R  # checker only
+        t0 = time.perf_counter()
+        rf = R.analyze_cols(cols)
+        cpu_dt = time.perf_counter() - t0
+        est = R.estimate_cols(cols, rf, cols.wall_time_ns)
+        sv = savings_columns(dcols, cf)
+        verified = bool(
+            [len(rf.dd), len(rf.rt), len(rf.ra), len(rf.ua), len(rf.ut)] == list(cf.counts().values())
+            and [i for g in rf.dd for i in g[2]] == cf.dd_members.tolist()
+            and [t for g in rf.rt for t, _ in g[3]] == cf.rt_tx.tolist()
+            and [r for g in rf.rt for _, r in g[3]] == cf.rt_rx.tolist()
+            and [p for g in rf.ra for p in g[3]] == cf.ra_pairs.tolist()
+            and sv.per_category_ns == est["per_category_ns"])
+    else:
+        cpu_dt = None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cf = analyze_columns(dcols)
+        savings_columns(dcols, cf)
+    torch.cuda.synchronize()
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    step_s = float(dt.item()) / args.steps
+    value = world * cols.n / step_s / 1e6
+    # e2e: host columns in, host findings + sums out
+    e2e_steps = max(1, min(args.steps, 10))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        cfh = analyze_columns(cols)
+        savings_columns(cols, cfh)
+    torch.cuda.synchronize()
+    de = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(de, op=dist.ReduceOp.MAX)
+    h2d = sum(getattr(cols, f).nbytes for f in DeviceColumns.FIELDS)
+    d2h = sum(a.nbytes for a in (cfh.dd_offsets, cfh.dd_members, cfh.rt_offsets, cfh.rt_tx, cfh.rt_rx,
+                                 cfh.pair_alloc, cfh.pair_delete, cfh.warn_index, cfh.ra_offsets, cfh.ra_pairs,
+                                 cfh.ua_pairs, cfh.ut_events))
+    peak, peak_src = peaks()
+    achieved = cols.n * EVENT_BYTES / step_s / 1e9
+    out = {
+        "metric": "M trace events/s analysed", "value": round(value, 3), "unit": "M events/s",
+        "ms_per_step": round(step_s * 1e3, 3), "steps": args.steps,
+        "config": {"workload": f"C2 trace: {cols.n} events ([ALLOC,H2D,KERNEL,D2H,DELETE] x 8 target devices, "
+                               f"25% duplicate H2D content, 30% unmodified D2H), validate + 5 detectors + "
+                               f"estimate/attribute sums, columns resident in HBM", "events_per_gpu": cols.n},
+        "counts": cf.counts(),
+        "timing": "host-synchronous C-ABI call (b2l_analyze + b2l_savings_compute), perf_counter bracketed by "
+                  "cuda synchronize, max over ranks",
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 5), "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_step": cols.n * EVENT_BYTES},
+        "e2e": {"value": round(world * cols.n * e2e_steps / float(de.item()) / 1e6, 3), "unit": "M events/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "b2l_analyze + b2l_savings_compute on host numpy columns"},
+        "verified": verified,
+    }
+    if cpu_dt is not None:
+        out["cpu_baseline"] = {"value": round(cols.n / cpu_dt / 1e6, 4), "unit": "M events/s", "cores": 1,
+                               "kind": "port", "sample": f"the full {cols.n}-event C2 trace through "
+                                                         f"oracle/analysis_ref.analyze_cols (1 thread)"}
+    return out
+
+
 # ----------------------------------------------------------------------------- reference arm
 _REF_STATE = {}
 
@@ -309,6 +402,7 @@ def run_reference(args, rank, world):
             total += sum(b for _, b in res)
         dt = time.perf_counter() - t0
     value = total / dt / 1e9
+    analysis = None if args.no_analysis else run_analysis_reference(args, ref_path)
     sample = (f"each step: {cores} processes x {per_worker} C2 buffers of {BUF_BYTES} B "
               f"({cores * per_worker * BUF_BYTES / 1e9:.2f} GB) through dmlens.hashing.hash_bytes "
               f"(unmodified reference from baseline/_ref)")
@@ -321,8 +415,39 @@ def run_reference(args, rank, world):
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "gpu_launches": 0,
+        "gpu_launches": 0, "analysis": analysis,
     }
+
+
+def run_analysis_reference(args, ref_path, sample_events=200_000):
+    """dmlens.analyze + estimate + attribute (unmodified reference) on a bounded sample of the C2 trace."""
+    sys.path.insert(0, ref_path)
+    from dmlens import analyze, attribute, estimate
+    from dmlens.model import CodeLocation, EventKind, Trace, TraceEvent
+
+    from paper_2601_12713_b200.synth import c2_trace  # input generation only (not timed)
+    cols = c2_trace(min(args.n_events, sample_events), seed=SEED)
+    kinds = [EventKind.TRANSFER, EventKind.ALLOC, EventKind.DELETE, EventKind.KERNEL]
+    loc = CodeLocation()
+    L = lambda a: a.tolist()  # noqa: E731
+    ev = [TraceEvent(q, kinds[k], a, b, s_, d, sa, da, nb, h, loc) for q, k, a, b, s_, d, sa, da, nb, h in zip(
+        L(cols.seq), L(cols.kind), L(cols.start_ns), L(cols.end_ns), L(cols.src_device), L(cols.dst_device),
+        L(cols.src_addr), L(cols.dst_addr), L(cols.bytes), L(cols.hash))]
+    tr = Trace(1, cols.num_devices_total, cols.host_device, cols.wall_time_ns, ev)
+    steps = max(1, min(args.steps, 3))
+    f = analyze(tr)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        f = analyze(tr)
+        estimate(tr, f)
+        attribute(tr, f)
+    dt = (time.perf_counter() - t0) / steps
+    v = round(cols.n / dt / 1e6, 4)
+    return {"metric": "M trace events/s analysed", "value": v, "unit": "M events/s", "ms_per_step": round(dt * 1e3, 1),
+            "cpu_baseline": {"value": v, "unit": "M events/s", "cores": 1, "kind": "reference",
+                             "sample": f"first {cols.n} events of the C2 trace as dmlens objects; analyze + "
+                                       f"estimate + attribute, {steps} steps (single-threaded by design)"},
+            "e2e": {"value": v, "unit": "M events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 def main():
@@ -339,6 +464,8 @@ def main():
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rec = run_ours(args, rank, world, local)
+    if not args.no_analysis:
+        rec["analysis"] = run_analysis_ours(args, rank, world, local)
     if rank == 0:
         print(json.dumps(rec), flush=True)
     if world > 1:

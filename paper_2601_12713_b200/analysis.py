@@ -104,6 +104,37 @@ def _cols_struct(c: Columns):
     return s, keep
 
 
+class DeviceColumns:
+    """Columns resident in device memory (torch tensors used only as buffers);
+    b2l_analyze reads them in place (device_resident = 1)."""
+
+    FIELDS = ("seq", "start_ns", "end_ns", "src_addr", "dst_addr", "bytes", "hash", "src_device", "dst_device",
+              "kind", "loc", "loc_flags", "loc_bucket")
+
+    def __init__(self, cols: Columns, device="cuda"):
+        import torch
+        self.host = cols
+        self.t = {}
+        for f in self.FIELDS:
+            a = getattr(cols, f)
+            if a.dtype == np.uint64:
+                a = a.view(np.int64)
+            elif a.dtype == np.uint32:
+                a = a.view(np.int32)
+            self.t[f] = torch.from_numpy(np.ascontiguousarray(a)).to(device)
+        ptr = lambda f: self.t[f].data_ptr() if self.t[f].numel() else None  # noqa: E731
+        self.struct = _Cols(n_events=cols.n, num_devices_total=cols.num_devices_total, host_device=cols.host_device,
+                            seq=ptr("seq"), start_ns=ptr("start_ns"), end_ns=ptr("end_ns"), src_addr=ptr("src_addr"),
+                            dst_addr=ptr("dst_addr"), bytes=ptr("bytes"), hash=ptr("hash"),
+                            src_device=ptr("src_device"), dst_device=ptr("dst_device"), kind=ptr("kind"),
+                            loc=ptr("loc"), n_locs=int(cols.loc_flags.size), loc_flags=ptr("loc_flags"),
+                            loc_bucket=ptr("loc_bucket"), n_buckets=cols.n_buckets, device_resident=1)
+
+    @property
+    def n(self):
+        return self.host.n
+
+
 def _arr(ptr, n, dtype):
     if not n or not ptr:
         return np.zeros(0, dtype=dtype)
@@ -163,7 +194,10 @@ def analyze_columns(cols: Columns, strict: bool = False) -> ColumnarFindings:
     """Run the whole detection pipeline on the device.  Raises EngineInvalid with
     the flagged events / rule bits when the trace fails validation."""
     L = _L()
-    cs, keep = _cols_struct(cols)
+    if isinstance(cols, DeviceColumns):
+        cs, keep = cols.struct, None
+    else:
+        cs, keep = _cols_struct(cols)
     fp = ctypes.POINTER(_Findings)()
     rc = L.b2l_analyze(ctypes.byref(cs), 1 if strict else 0, ctypes.byref(fp))
     handle = _Handle(fp if fp else None)
@@ -242,7 +276,10 @@ def _findings_struct(cf: ColumnarFindings):
 def savings_columns(cols: Columns, cf: ColumnarFindings) -> ColumnarSavings:
     """Exact integer estimate/attribute aggregates on the device."""
     L = _L()
-    cs, keep_c = _cols_struct(cols)
+    if isinstance(cols, DeviceColumns):
+        cs, keep_c = cols.struct, None
+    else:
+        cs, keep_c = _cols_struct(cols)
     if cf._handle is not None and cf._handle.ptr:
         fptr = cf._handle.ptr
         keep_f = None

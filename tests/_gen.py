@@ -46,41 +46,6 @@ def nasty_trace(seed, max_events=300, max_devices=5):
     return T.Trace(version=1, num_devices_total=ndev, host_device=host, wall_time_ns=wall, events=evs)
 
 
-def cycle_trace_columns(n_events, n_targets=8, seed=2, dup_frac=0.25, n_host_addrs=4096, payload=40000):
-    """C2-shaped columnar trace: [ALLOC, H2D, KERNEL, D2H, DELETE] cycles rotating over the
-    target devices (device 0 = host), H2D content repeated with probability dup_frac."""
-    rng = np.random.default_rng(seed)
-    ncyc = n_events // 5
-    n = ncyc * 5
-    cyc = np.arange(ncyc)
-    dev = (cyc % n_targets + 1).astype(np.int32)
-    state = np.tile(np.arange(5), ncyc)
-    kind = np.array([1, 0, 3, 0, 2], dtype=np.uint8)[state]
-    dur = np.array([300, 2 * payload, 10000, 2 * payload, 300], dtype=np.uint64)[state]
-    start = np.zeros(n, dtype=np.uint64)
-    start[1:] = np.cumsum(dur)[:-1]
-    end = start + dur
-    d = np.repeat(dev, 5)
-    src = np.where((state == 3) | (state == 2), d, 0).astype(np.int32)
-    dst = np.where((state == 3), 0, d).astype(np.int32)
-    haddr = (0x7F0000000000 + (rng.integers(0, n_host_addrs, ncyc) * 0x100000)).astype(np.uint64)
-    daddr = (0xD00000000000 + dev.astype(np.uint64) * 0x1000000).astype(np.uint64)
-    h = np.repeat(haddr, 5)
-    dv = np.repeat(daddr, 5)
-    src_addr = np.where(state == 0, h, np.where(state == 1, h, np.where(state == 3, dv, 0))).astype(np.uint64)
-    dst_addr = np.where(state == 3, h, np.where(state == 2, 0, dv)).astype(np.uint64)
-    nbytes = np.where((state <= 1) | (state == 3), payload, 0).astype(np.uint64)
-    content = np.arange(ncyc, dtype=np.uint64) + 1
-    dup = rng.random(ncyc) < dup_frac
-    dup[0] = False
-    idx = np.nonzero(dup)[0]
-    content[idx] = content[(rng.random(idx.size) * idx).astype(np.int64)]
-    hh = (content * np.uint64(0x9E3779B97F4A7C15)) | np.uint64(1)
-    back = (np.arange(ncyc, dtype=np.uint64) + np.uint64(1 << 40)) * np.uint64(0xBF58476D1CE4E5B9) | np.uint64(1)
-    hashv = np.zeros(n, dtype=np.uint64)
-    hashv[state == 1] = hh
-    unmodified = rng.random(ncyc) < 0.3  # kernel left the array unchanged: D2H returns the H2D content
-    hashv[state == 3] = np.where(unmodified, hh, back)
-    seq = np.arange(n, dtype=np.uint64)
-    return columns_from_arrays(n_targets + 1, 0, seq, start, end, src, dst, kind, src_addr, dst_addr, nbytes, hashv,
-                               wall_time_ns=int(end[-1]) if n else 0)
+def cycle_trace_columns(n_events, seed=2, **kw):
+    from paper_2601_12713_b200.synth import c2_trace
+    return c2_trace(n_events, seed=seed, **kw)
