@@ -1,8 +1,27 @@
-import sys, time
-sys.path.insert(0, '.')
-from tests._gen import cycle_trace_columns
-from paper_2601_12713_b200 import analyze_columns, savings_columns
-c = cycle_trace_columns(1_000_000, seed=2)
-for i in range(4):
-    t = time.perf_counter(); cf = analyze_columns(c); t1 = time.perf_counter(); sv = savings_columns(c, cf); t2 = time.perf_counter()
-    print(f"analyze {1e3*(t1-t):.2f} ms  savings {1e3*(t2-t1):.2f} ms", cf.counts())
+"""Times the analysis pipeline on synthetic configs (used under ncu for launch lists)."""
+import argparse
+import sys
+import time
+
+sys.path.insert(0, ".")
+from paper_2601_12713_b200 import analyze_columns, savings_columns  # noqa: E402
+from paper_2601_12713_b200.analysis import DeviceColumns  # noqa: E402
+from paper_2601_12713_b200.synth import c2_trace, c3_trace, c4_trace  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--n", type=int, default=1_000_000)
+ap.add_argument("--iters", type=int, default=4)
+ap.add_argument("--device", action="store_true")
+a = ap.parse_args()
+gen = {"c2": lambda: c2_trace(a.n), "c3": lambda: c3_trace(max(1, a.n // 3)), "c4": lambda: c4_trace(a.n)}[a.config]
+c = gen()
+cols = DeviceColumns(c) if a.device else c
+for i in range(a.iters):
+    t = time.perf_counter()
+    cf = analyze_columns(cols)
+    t1 = time.perf_counter()
+    sv = savings_columns(cols, cf)
+    t2 = time.perf_counter()
+    print(f"{a.config} n={c.n} analyze {1e3*(t1-t):.2f} ms  savings {1e3*(t2-t1):.2f} ms  "
+          f"{c.n/(t2-t)/1e6:.1f} M ev/s", cf.counts())
