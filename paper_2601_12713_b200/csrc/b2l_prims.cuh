@@ -298,60 +298,74 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
+// Histograms of every digit position of every key word in one read of the keys:
+// hist[(w * 8 + byte) * 256 + digit].  Warp-aggregated (match_any) shared-memory counts.
 template <int KW>
-__global__ void k_key_vary(KeyCols<KW> k, size_t n, unsigned long long *vary) {
-    unsigned long long acc[KW];
-    uint64_t first[KW];
-#pragma unroll
-    for (int w = 0; w < KW; ++w) acc[w] = 0, first[w] = k.w[w][0];
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-#pragma unroll
-        for (int w = 0; w < KW; ++w) acc[w] |= k.w[w][i] ^ first[w];
-#pragma unroll
-    for (int w = 0; w < KW; ++w) {
-        unsigned long long v = acc[w];
-        for (int o = 16; o; o >>= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
-        if ((threadIdx.x & 31) == 0 && v) atomicOr(vary + w, v);
-    }
-}
-
-__global__ void __launch_bounds__(RS_THREADS) k_radix_hist(const uint64_t *__restrict__ key, size_t n, int shift,
-                                                           uint32_t *__restrict__ counts, unsigned ntiles) {
-    __shared__ uint32_t hist[256];
-    hist[threadIdx.x] = 0;
+__global__ void __launch_bounds__(RS_THREADS) k_radix_hist_all(KeyCols<KW> k, size_t n, uint32_t *__restrict__ hist) {
+    __shared__ uint32_t sh[KW * 8][256];
+    for (int i = threadIdx.x; i < KW * 8 * 256; i += RS_THREADS) (&sh[0][0])[i] = 0;
     __syncthreads();
-    const size_t base = (size_t)blockIdx.x * RS_TILE;
     const int lane = threadIdx.x & 31;
-#pragma unroll 4
-    for (int r = 0; r < RS_ROUNDS; ++r) {
-        const size_t pos = base + (size_t)r * RS_THREADS + threadIdx.x;
-        const bool valid = pos < n;
-        const uint32_t d = valid ? (uint32_t)(key[pos] >> shift) & 255u : 256u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        if (valid && lane == __ffs(peers) - 1) atomicAdd(&hist[d], (uint32_t)__popc(peers));
+    const size_t stride = (size_t)gridDim.x * RS_THREADS;
+    for (size_t base = (size_t)blockIdx.x * RS_THREADS; base < n; base += stride) {
+        const size_t i = base + threadIdx.x;
+        const bool valid = i < n;
+#pragma unroll
+        for (int w = 0; w < KW; ++w) {
+            const uint64_t key = valid ? k.w[w][i] : 0;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const uint32_t d = valid ? (uint32_t)(key >> (8 * b)) & 255u : 256u;
+                const uint32_t peers = __match_any_sync(0xffffffffu, d);
+                if (valid && lane == __ffs(peers) - 1) atomicAdd(&sh[w * 8 + b][d], (uint32_t)__popc(peers));
+            }
+        }
     }
     __syncthreads();
-    counts[(size_t)threadIdx.x * ntiles + blockIdx.x] = hist[threadIdx.x];
+    for (int i = threadIdx.x; i < KW * 8 * 256; i += RS_THREADS) {
+        const uint32_t v = (&sh[0][0])[i];
+        if (v) atomicAdd(hist + i, v);
+    }
 }
 
+// One LSD pass, Onesweep style: tiles take ids in launch order, rank their keys stably
+// (warp multisplit), publish per-digit tile counts, and resolve the exclusive prefix of
+// every digit across preceding tiles by decoupled look-back -- one launch per pass.
+constexpr uint32_t LB_AGG = 1u << 30, LB_INC = 2u << 30, LB_VAL = (1u << 30) - 1;
+
 template <int KW>
-__global__ void __launch_bounds__(RS_THREADS) k_radix_scatter(KeyCols<KW> in, const uint32_t *__restrict__ vin,
-                                                              KeyCols<KW> out, uint32_t *__restrict__ vout, size_t n,
-                                                              int word, int shift,
-                                                              const uint32_t *__restrict__ offs, unsigned ntiles) {
-    __shared__ uint32_t base_off[256];
+__global__ void __launch_bounds__(RS_THREADS) k_onesweep(KeyCols<KW> in, const uint32_t *__restrict__ vin,
+                                                         KeyCols<KW> out, uint32_t *__restrict__ vout, size_t n,
+                                                         int word, int shift, const uint32_t *__restrict__ hist,
+                                                         uint32_t *status, uint32_t *tile_counter) {
+    __shared__ uint32_t tile_s;
+    __shared__ uint32_t base_s[256];
     __shared__ uint32_t running[256];
     __shared__ uint32_t wcnt[RS_THREADS / 32][256];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    base_off[t] = offs[(size_t)t * ntiles + blockIdx.x];
+    if (t == 0) tile_s = atomicAdd(tile_counter, 1u);
+    // exclusive scan of the global digit histogram (digit bases)
+    base_s[t] = hist[t];
     running[t] = 0;
-    const size_t base = (size_t)blockIdx.x * RS_TILE;
+    __syncthreads();
+#pragma unroll 1
+    for (int off = 1; off < 256; off <<= 1) {
+        const uint32_t x = t >= off ? base_s[t - off] : 0;
+        __syncthreads();
+        base_s[t] += x;
+        __syncthreads();
+    }
+    const uint32_t my_base = base_s[t] - hist[t];
+    const uint32_t tile = tile_s;
+    const size_t tbase = (size_t)tile * RS_TILE;
     const uint64_t *kd = in.w[word];
+    uint32_t packed[RS_ROUNDS];
+#pragma unroll
     for (int r = 0; r < RS_ROUNDS; ++r) {
 #pragma unroll
         for (int w = 0; w < RS_THREADS / 32; ++w) wcnt[w][t] = 0;
         __syncthreads();
-        const size_t pos = base + (size_t)r * RS_THREADS + t;
+        const size_t pos = tbase + (size_t)r * RS_THREADS + t;
         const bool valid = pos < n;
         const uint32_t d = valid ? (uint32_t)(kd[pos] >> shift) & 255u : 256u;
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
@@ -361,21 +375,45 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_scatter(KeyCols<KW> in, co
         uint32_t run = running[t];
 #pragma unroll
         for (int w = 0; w < RS_THREADS / 32; ++w) {
-            uint32_t c = wcnt[w][t];
+            const uint32_t c = wcnt[w][t];
             wcnt[w][t] = run;
             run += c;
         }
         running[t] = run;
         __syncthreads();
-        if (valid) {
-            const uint32_t dst = base_off[d] + wcnt[warp][d] + wrank;
-#pragma unroll
-            for (int w = 0; w < KW; ++w) out.w[w][dst] = in.w[w][pos];
-            vout[dst] = vin[pos];
-        }
-        __syncthreads();
+        packed[r] = valid ? ((d << 16) | (wcnt[warp][d] + wrank)) : 0xFFFFFFFFu;
+        __syncthreads();  // wcnt is re-zeroed by the next round
     }
-    (void)running;
+    __syncthreads();
+    // decoupled look-back for digit t
+    const uint32_t cnt = running[t];
+    volatile uint32_t *st = status;
+    uint32_t excl = 0;
+    if (tile == 0) {
+        st[t] = LB_INC | cnt;
+    } else {
+        st[(size_t)tile * 256 + t] = LB_AGG | cnt;
+        for (int64_t j = (int64_t)tile - 1; j >= 0; --j) {
+            uint32_t v;
+            do {
+                v = st[(size_t)j * 256 + t];
+            } while ((v & (LB_AGG | LB_INC)) == 0);
+            excl += v & LB_VAL;
+            if (v & LB_INC) break;
+        }
+        st[(size_t)tile * 256 + t] = LB_INC | (excl + cnt);
+    }
+    base_s[t] = my_base + excl;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RS_ROUNDS; ++r) {
+        if (packed[r] == 0xFFFFFFFFu) continue;
+        const size_t pos = tbase + (size_t)r * RS_THREADS + t;
+        const uint32_t dst = base_s[packed[r] >> 16] + (packed[r] & 0xFFFFu);
+#pragma unroll
+        for (int w = 0; w < KW; ++w) out.w[w][dst] = in.w[w][pos];
+        vout[dst] = vin[pos];
+    }
 }
 
 template <int KW>
@@ -386,30 +424,35 @@ struct SortBufs {
 };
 
 // Stable sort of n records (keys KW words, value u32) held in side `b.cur`; on return b.cur names
-// the side holding the sorted records.  One host sync (pass planning).
+// the side holding the sorted records.  One histogram read + one host sync (pass planning:
+// a digit position is skipped when one bin holds all n keys), then one launch per live pass.
 template <int KW>
 void radix_sort(SortBufs<KW> &b, size_t n, cudaStream_t s) {
     if (n <= 1) return;
-    DBuf<unsigned long long> vary(KW, s);
-    vary.zero();
-    k_key_vary<KW><<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(b.k[b.cur], n, vary.p);
-    CK_LAUNCH("k_key_vary");
-    unsigned long long hv[KW];
-    CK(cudaMemcpyAsync(hv, vary.p, sizeof(hv), cudaMemcpyDeviceToHost, s));
+    if (n >= (size_t)LB_VAL) throw EngineErr{B2L_E_INVALID_ARG, "radix_sort: too many records"};
+    constexpr int NPOS = KW * 8;
+    DBuf<uint32_t> hist((size_t)NPOS * 256, s);
+    hist.zero();
+    k_radix_hist_all<KW><<<grid_for(n, RS_THREADS, 148 * 4), RS_THREADS, 0, s>>>(b.k[b.cur], n, hist.p);
+    CK_LAUNCH("k_radix_hist_all");
+    static thread_local uint32_t *h_hist = nullptr;
+    if (!h_hist) CK(cudaMallocHost(&h_hist, 3 * 8 * 256 * sizeof(uint32_t)));
+    CK(cudaMemcpyAsync(h_hist, hist.p, (size_t)NPOS * 256 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const unsigned ntiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
-    DBuf<uint32_t> counts((size_t)256 * ntiles, s);
+    DBuf<uint32_t> status((size_t)ntiles * 256 + 1, s);
     for (int w = KW - 1; w >= 0; --w) {
         for (int byte = 0; byte < 8; ++byte) {
-            if (((hv[w] >> (8 * byte)) & 255ull) == 0) continue;  // digit constant over all keys: identity pass
-            const int shift = 8 * byte;
-            k_radix_hist<<<ntiles, RS_THREADS, 0, s>>>(b.k[b.cur].w[w], n, shift, counts.p, ntiles);
-            CK_LAUNCH("k_radix_hist");
-            uint32_t *cp = counts.p;
-            scan<SumU32>((size_t)256 * ntiles, LoadU32{cp}, StoreExclU32{cp}, s);
-            k_radix_scatter<KW><<<ntiles, RS_THREADS, 0, s>>>(b.k[b.cur], b.v[b.cur], b.k[b.cur ^ 1], b.v[b.cur ^ 1],
-                                                              n, w, shift, counts.p, ntiles);
-            CK_LAUNCH("k_radix_scatter");
+            const uint32_t *hp = h_hist + (size_t)(w * 8 + byte) * 256;
+            bool trivial = false;
+            for (int d = 0; d < 256; ++d)
+                if (hp[d] == n) trivial = true;
+            if (trivial) continue;  // digit constant over all keys: identity pass
+            CK(cudaMemsetAsync(status.p, 0, status.n * sizeof(uint32_t), s));
+            k_onesweep<KW><<<ntiles, RS_THREADS, 0, s>>>(b.k[b.cur], b.v[b.cur], b.k[b.cur ^ 1], b.v[b.cur ^ 1], n, w,
+                                                         8 * byte, hist.p + (size_t)(w * 8 + byte) * 256, status.p,
+                                                         status.p + (size_t)ntiles * 256);
+            CK_LAUNCH("k_onesweep");
             b.cur ^= 1;
         }
     }
