@@ -16,6 +16,8 @@
 //                                              prefix max of kernel ends; UT run ids by scan
 // Proofs of the reformulations: SURVEY.md Appendix A; the GPU tests check every step
 // against oracle/analysis_ref.py and the reference's golden outputs.
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -41,6 +43,14 @@ struct DevCols {
     const uint32_t *loc_bucket;
     uint32_t nlocs, nbuckets;
 };
+
+// Which key bytes can vary (OR over events of x ^ x[0] per column) and value-range masks;
+// computed once per trace so no sort needs a host round trip for pass planning.
+struct Masks {
+    uint8_t hash = 0xFF, sa = 0xFF, da = 0xFF, nb = 0xFF, sa_tt = 0xFF, dev = 0xFF, idx = 0xFF;
+    const uint32_t *srank = nullptr;  // srank[i] = first index with start == start[i]
+};
+thread_local Masks g_masks;
 
 // Owns device copies of host columns.
 struct ColsUpload {
@@ -149,6 +159,39 @@ __global__ void k_max_data_end(DevCols c, unsigned long long *out) {
     if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
 
+// Bits that vary inside each key subset (OR ^ AND over the subset): hash over hashed transfers,
+// dst_addr over allocs/deletes, src_addr and bytes over allocs, src_addr over target transfers.
+__global__ void k_col_vary(DevCols c, unsigned long long *out /*[5] OR, [5] AND*/) {
+    unsigned long long o[5] = {0, 0, 0, 0, 0}, a[5] = {~0ull, ~0ull, ~0ull, ~0ull, ~0ull};
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += (size_t)gridDim.x * blockDim.x) {
+        const uint8_t k = c.kind[i];
+        if (k == B2L_KIND_TRANSFER && c.nb[i] > 0 && c.h[i] != 0) o[0] |= c.h[i], a[0] &= c.h[i];
+        if (k == B2L_KIND_ALLOC || k == B2L_KIND_DELETE) o[1] |= c.da[i], a[1] &= c.da[i];
+        if (k == B2L_KIND_ALLOC) o[2] |= c.sa[i], a[2] &= c.sa[i], o[3] |= c.nb[i], a[3] &= c.nb[i];
+        if (k == B2L_KIND_TRANSFER && c.dst[i] != c.host) o[4] |= c.sa[i], a[4] &= c.sa[i];
+    }
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        unsigned long long vo = o[q], va = a[q];
+        for (int off = 16; off; off >>= 1) {
+            vo |= __shfl_xor_sync(0xffffffffu, vo, off);
+            va &= __shfl_xor_sync(0xffffffffu, va, off);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (vo) atomicOr(out + q, vo);
+            if (~va) atomicAnd(out + 5 + q, va);
+        }
+    }
+}
+struct SrankLoad {
+    const uint64_t *start;
+    __device__ uint64_t operator()(size_t i) const { return (i == 0 || start[i] != start[i - 1]) ? i : 0; }
+};
+struct SrankStore {
+    uint32_t *srank;
+    __device__ void operator()(size_t i, uint64_t ex, uint64_t it) const { srank[i] = (uint32_t)(ex > it ? ex : it); }
+};
+
 // ============================================================ helpers
 template <class F>
 __global__ void k_for(size_t n, F f) {
@@ -164,8 +207,7 @@ void for_each(size_t n, F f, cudaStream_t s) {
 // Read a device u32 count (one sync).
 uint32_t read_u32(const uint32_t *d, cudaStream_t s) {
     uint32_t v = 0;
-    CK(cudaMemcpyAsync(&v, d, sizeof(v), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    read_back(&v, d, sizeof(v), s);
     return v;
 }
 
@@ -199,23 +241,26 @@ struct GroupOrder {
     DBuf<uint32_t> rank;   // group id -> final rank
 };
 struct FirstStartKey {
-    const uint64_t *start;
+    const uint32_t *srank;
     const uint32_t *first_event;
     uint64_t *key;
     uint32_t *val;
     __device__ void operator()(size_t g) const {
-        key[g] = start[first_event[g]];
+        key[g] = srank[first_event[g]];
         val[g] = (uint32_t)g;
     }
 };
+// Groups arrive in key order; a stable sort by the start of their first event (as the rank of the
+// first event with that start -- equal starts, equal ranks) gives the reference's (start, key...) order.
 GroupOrder order_groups(size_t ng, const uint64_t *start, const uint32_t *first_event, cudaStream_t s) {
+    (void)start;
     GroupOrder go;
     go.order.alloc(ng ? ng : 1, s);
     go.rank.alloc(ng ? ng : 1, s);
     if (!ng) return go;
     SortStore<1> st(ng, s);
-    for_each(ng, FirstStartKey{start, first_event, st.in_key(0), st.in_val()}, s);
-    radix_sort<1>(st.b, ng, s);
+    for_each(ng, FirstStartKey{g_masks.srank, first_event, st.in_key(0), st.in_val()}, s);
+    radix_sort<1>(st.b, ng, LiveBytes<1>{{g_masks.idx}}, s);
     CK(cudaMemcpyAsync(go.order.p, st.val(), ng * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     uint32_t *ord = go.order.p, *rk = go.rank.p;
     for_each(ng, [=] __device__(size_t r) { rk[ord[r]] = (uint32_t)r; }, s);
@@ -235,6 +280,10 @@ struct StoreOffset {
 
 // ============================================================ output container
 struct Internal {
+    // device copies of the trace columns (when they were uploaded from host) and their identity
+    ColsUpload cols;
+    const void *cols_key[3] = {nullptr, nullptr, nullptr};
+    uint64_t cols_n = 0;
     // device copies of findings (for b2l_savings)
     DBuf<uint64_t> dd_off, rt_off, ra_off;
     DBuf<uint32_t> dd_mem, rt_tx, rt_rx, pair_alloc, pair_delete, ra_mem, ua, ut;
@@ -246,9 +295,57 @@ template <class T>
 T *host_copy(const T *d, size_t n, cudaStream_t s) {
     T *h = (T *)malloc((n ? n : 1) * sizeof(T));
     if (!h) throw EngineErr{B2L_E_OOM, "host allocation failed"};
-    if (n) CK(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    if (n) read_back(h, d, n * sizeof(T), s);
     return h;
 }
+// Many device->host result copies through the pinned stage with a single synchronisation.
+struct HostBatch {
+    struct Item {
+        void *dst;
+        const void *src;
+        size_t bytes;
+    };
+    std::vector<Item> items;
+    template <class T>
+    T *add(const T *d, size_t n) {
+        T *h = (T *)malloc((n ? n : 1) * sizeof(T));
+        if (!h) throw EngineErr{B2L_E_OOM, "host allocation failed"};
+        if (n) items.push_back(Item{h, d, n * sizeof(T)});
+        return h;
+    }
+    void flush(cudaStream_t s) {
+        size_t total = 0;
+        for (auto &it : items) total += (it.bytes + 15) & ~size_t(15);
+        uint8_t *st = pinned().reserve(total ? total : 16);
+        size_t off = 0;
+        for (auto &it : items) {
+            CK(cudaMemcpyAsync(st + off, it.src, it.bytes, cudaMemcpyDeviceToHost, s));
+            off += (it.bytes + 15) & ~size_t(15);
+        }
+        CK(cudaStreamSynchronize(s));
+        off = 0;
+        for (auto &it : items) {
+            memcpy(it.dst, st + off, it.bytes);
+            off += (it.bytes + 15) & ~size_t(15);
+        }
+        items.clear();
+    }
+};
+
+// B2L_TRACE=1: synchronise after each phase and print its wall time (diagnostics only).
+struct PhaseClock {
+    bool on;
+    cudaStream_t s;
+    std::chrono::steady_clock::time_point t;
+    explicit PhaseClock(cudaStream_t st) : on(getenv("B2L_TRACE") != nullptr), s(st), t(std::chrono::steady_clock::now()) {}
+    void mark(const char *name) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[b2l] %-12s %8.3f ms\n", name, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
 
 // ============================================================ DD + RT (detectors.py:85-167)
 struct RtRecordInit {  // record r = 2k + role over hashed transfer k: role 0 = reception, 1 = send
@@ -372,23 +469,25 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
         out.rt_off.alloc(1, s), out.rt_off.zero(), out.rt_tx.alloc(1, s), out.rt_rx.alloc(1, s);
         return r;
     }
+    PhaseClock pc(s);
     SortStore<2> st(R, s);
     for_each(R, RtRecordInit{c, H, st.in_key(0), st.in_key(1), st.in_val()}, s);
-    radix_sort<2>(st.b, R, s);
+    pc.mark(" rt-init");
+    radix_sort<2>(st.b, R, LiveBytes<2>{{g_masks.hash, g_masks.dev}}, s);
+    pc.mark(" rt-sort");
     KeyCols<2> sk = st.b.k[st.b.cur];
     const uint32_t *sval = st.val();
 
     DBuf<uint32_t> seg_of(R, s), f_of(R, s), j_of(R, s), rxpos(R, s), seg_start(R + 1, s), seg_rxbase(R + 1, s);
-    HostScalars hs(2, s);
     DBuf<QState> tot(1, s);
     scan<QOp>(R, QLoad{sk, sval},
               QStore{sval, seg_of.p, f_of.p, j_of.p, rxpos.p, seg_start.p, seg_rxbase.p}, s, tot.p);
     QState qt{};
-    CK(cudaMemcpyAsync(&qt, tot.p, sizeof(qt), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    read_back(&qt, tot.p, sizeof(qt), s);
     const uint32_t nseg = qt.seg, nrx = qt.rx_glob;
     CK(cudaMemcpyAsync(seg_rxbase.p + nseg, &tot.p->rx_glob, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
 
+    pc.mark(" q-scan");
     // ---- round trips: per send, the matched reception (or NONE)
     DBuf<uint32_t> match(nH, s);
     CK(cudaMemsetAsync(match.p, 0xFF, nH * sizeof(uint32_t), s));
@@ -411,7 +510,7 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
             const uint64_t *hh = c.h;
             for_each(nH, [=] __device__(size_t k) { k0[k] = hh[H[k]], v[k] = (uint32_t)k; }, s);
         }
-        radix_sort<1>(hsort.b, nH, s);
+        radix_sort<1>(hsort.b, nH, LiveBytes<1>{{g_masks.hash}}, s);
         DBuf<uint32_t> hstart(nH, s), hcount(1, s);
         KeyCols<1> hk = hsort.b.k[hsort.b.cur];
         compact(nH, HeadPred<1>{hk}, hstart.p, hcount.p, s);
@@ -423,6 +522,7 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
         CK_LAUNCH("k_rt_strict");
     }
 
+    pc.mark(" rt-match");
     // ---- DD groups: queue segments with >= 2 receptions (members = the receptions, trace order)
     {
         DBuf<uint32_t> gseg(nseg, s), gcount(1, s);
@@ -450,8 +550,7 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
         else CK(cudaMemsetAsync(out.dd_off.p, 0, sizeof(uint64_t), s));
         uint64_t nm = 0;
         if (ng) {
-            CK(cudaMemcpyAsync(&nm, total.p, sizeof(nm), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
+            read_back(&nm, total.p, sizeof(nm), s);
         }
         r.dd_members = nm;
         out.dd_mem.alloc(nm ? nm : 1, s);
@@ -468,6 +567,7 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
         }, s);
     }
 
+    pc.mark(" dd-groups");
     // ---- RT groups: matched sends keyed (hash, src, dst); sends of one (hash, src) queue are
     // already in trace order in the record sort, so a stable sort by (queue segment, dst) groups them
     {
@@ -495,7 +595,7 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
                 v[t] = p;
             }, s);
         }
-        radix_sort<1>(ts.b, nt, s);
+        radix_sort<1>(ts.b, nt, LiveBytes<1>{{(uint8_t)(g_masks.dev | (live_range(nseg) << 4))}}, s);
         KeyCols<1> tk = ts.b.k[ts.b.cur];
         const uint32_t *tv = ts.val();
         DBuf<uint32_t> gstart(nt, s), gcount(1, s);
@@ -595,7 +695,7 @@ PairOut pairs_step(const DevCols &c, const uint32_t *AD, uint32_t nAD, const uin
             v[r] = (uint32_t)r;
         }, s);
     }
-    radix_sort<2>(st.b, nAD, s);
+    radix_sort<2>(st.b, nAD, LiveBytes<2>{{g_masks.dev, g_masks.da}}, s);
     KeyCols<2> sk = st.b.k[st.b.cur];
     const uint32_t *sv = st.val();
     DBuf<uint32_t> level(nAD, s), seg(nAD, s);
@@ -638,7 +738,7 @@ PairOut pairs_step(const DevCols &c, const uint32_t *AD, uint32_t nAD, const uin
             v[q] = p;
         }, s);
     }
-    radix_sort<1>(ls.b, nl, s);
+    radix_sort<1>(ls.b, nl, LiveBytes<1>{{(uint8_t)(live_range(nAD + 1) | (live_range(nAD + 1) << 4))}}, s);
     {
         const uint64_t *lk = ls.key(0);
         const uint32_t *lvv = ls.val();
@@ -678,7 +778,7 @@ void ra_step(const DevCols &c, uint32_t nP, Internal &out, cudaStream_t s) {
             k0[r] = sa[a], k1[r] = (uint64_t)(uint32_t)dst[a], k2[r] = nb[a], v[r] = (uint32_t)r;
         }, s);
     }
-    radix_sort<3>(st.b, nP, s);
+    radix_sort<3>(st.b, nP, LiveBytes<3>{{g_masks.sa, g_masks.dev, g_masks.nb}}, s);
     KeyCols<3> sk = st.b.k[st.b.cur];
     const uint32_t *sv = st.val();
     DBuf<uint32_t> sstart(nP + 1, s), scount(1, s), seg_of(nP, s);
@@ -717,8 +817,7 @@ void ra_step(const DevCols &c, uint32_t nP, Internal &out, cudaStream_t s) {
     scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.ra_off.p}, s, total.p);
     CK(cudaMemcpyAsync(out.ra_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
     uint64_t nm = 0;
-    CK(cudaMemcpyAsync(&nm, total.p, sizeof(nm), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    read_back(&nm, total.p, sizeof(nm), s);
     out.ra_members = nm;
     out.ra_mem.alloc(nm, s);
     const uint32_t *sgp = seg_group.p, *rk = go.rank.p, *so = seg_of.p;
@@ -741,7 +840,12 @@ struct KernelIndex {
     const uint32_t *kev;   // kernel event per position
     const uint64_t *pm;
     uint32_t nk;
+    const uint32_t *dlo, *dhi;  // per-device [lo, hi) when the device count is small, else null
     __device__ void range(uint64_t dev, uint32_t &lo, uint32_t &hi) const {
+        if (dlo) {
+            lo = dlo[dev], hi = dhi[dev];
+            return;
+        }
         uint32_t a = 0, b = nk;
         while (a < b) {
             uint32_t m = (a + b) >> 1;
@@ -814,13 +918,26 @@ void ua_ut_step(const DevCols &c, const uint32_t *TK, uint32_t nK, const uint32_
         uint32_t *v = ks.in_val();
         const int32_t *dst = c.dst;
         for_each(nK, [=] __device__(size_t r) { k0[r] = (uint64_t)(uint32_t)dst[TK[r]], v[r] = (uint32_t)r; }, s);
-        radix_sort<1>(ks.b, nK, s);
+        radix_sort<1>(ks.b, nK, LiveBytes<1>{{g_masks.dev}}, s);
         uint32_t *ke = kev.p;
         const uint32_t *kv = ks.val();
         for_each(nK, [=] __device__(size_t p) { ke[p] = TK[kv[p]]; }, s);
         scan<Seg<MaxU64>>(nK, PmLoad{ks.key(0), kev.p, c.end}, PmStore{pm.p}, s);
     }
-    const KernelIndex KI{ks.key(0), kev.p, pm.p, nK};
+    // per-device kernel ranges (one lookup instead of two binary searches per query)
+    const bool small_ndev = c.ndev > 0 && c.ndev <= (1 << 16);
+    DBuf<uint32_t> dlo(small_ndev ? c.ndev : 1, s), dhi(small_ndev ? c.ndev : 1, s);
+    if (small_ndev) {
+        dlo.zero(), dhi.zero();
+        uint32_t *lo = dlo.p, *hi = dhi.p;
+        const uint64_t *kd = ks.key(0);
+        const uint32_t nk = nK;
+        for_each(nK, [=] __device__(size_t p) {
+            if (p == 0 || kd[p] != kd[p - 1]) lo[kd[p]] = (uint32_t)p;
+            if (p + 1 == nk || kd[p + 1] != kd[p]) hi[kd[p]] = (uint32_t)p + 1;
+        }, s);
+    }
+    const KernelIndex KI{ks.key(0), kev.p, pm.p, nK, small_ndev ? dlo.p : nullptr, small_ndev ? dhi.p : nullptr};
 
     // ---- UA: target pairs whose [alloc start, delete end] meets no kernel
     {
@@ -831,15 +948,21 @@ void ua_ut_step(const DevCols &c, const uint32_t *TK, uint32_t nK, const uint32_
         const int host = c.host;
         const uint64_t *start = c.start, *end = c.end;
         const uint64_t se = out.synth_end;
-        compact(nP, [=] __device__(size_t r) {
+        DBuf<uint8_t> uflag(nP ? nP : 1, s);
+        uint8_t *uf = uflag.p;
+        for_each(nP, [=] __device__(size_t r) {
             const uint32_t a = PA[r];
-            if (dst[a] == host) return false;
-            uint32_t lo, hi;
-            KI.range((uint64_t)(uint32_t)dst[a], lo, hi);
-            const uint32_t cc = KI.cursor(lo, hi, start[a]);
-            const uint64_t del_end = PD[r] == NONE ? se : end[PD[r]];
-            return cc == hi || start[KI.kev[cc]] > del_end;
-        }, ua.p, uc.p, s);
+            uint8_t f = 0;
+            if (dst[a] != host) {
+                uint32_t lo, hi;
+                KI.range((uint64_t)(uint32_t)dst[a], lo, hi);
+                const uint32_t cc = KI.cursor(lo, hi, start[a]);
+                const uint64_t del_end = PD[r] == NONE ? se : end[PD[r]];
+                f = (cc == hi || start[KI.kev[cc]] > del_end) ? 1 : 0;
+            }
+            uf[r] = f;
+        }, s);
+        compact(nP, [=] __device__(size_t r) { return uf[r] != 0; }, ua.p, uc.p, s);
         out.n_ua = read_u32(uc.p, s);
         out.ua = std::move(ua);
     }
@@ -876,7 +999,7 @@ void ua_ut_step(const DevCols &c, const uint32_t *TK, uint32_t nK, const uint32_
             const int32_t *dst = c.dst;
             for_each(nT, [=] __device__(size_t t) { k0[t] = (uint64_t)(uint32_t)dst[TT[t]], v[t] = (uint32_t)t; }, s);
         }
-        radix_sort<1>(ds.b, nT, s);
+        radix_sort<1>(ds.b, nT, LiveBytes<1>{{g_masks.dev}}, s);
         scan<Seg<SumU32>>(nT, RunLoad{ds.key(0), ds.val(), cur.p, cls.p}, RunStore{ds.val(), run.p}, s);
         SortStore<2> as(nT, s);
         {
@@ -888,7 +1011,7 @@ void ua_ut_step(const DevCols &c, const uint32_t *TK, uint32_t nK, const uint32_
                 k0[t] = (uint64_t)(uint32_t)dst[TT[t]], k1[t] = sa[TT[t]], v[t] = (uint32_t)t;
             }, s);
         }
-        radix_sort<2>(as.b, nT, s);
+        radix_sort<2>(as.b, nT, LiveBytes<2>{{g_masks.dev, g_masks.sa_tt}}, s);
         {
             const uint64_t *a0 = as.key(0), *a1 = as.key(1);
             const uint32_t *av = as.val(), *rn = run.p;
@@ -917,7 +1040,14 @@ cudaStream_t g_stream[64] = {nullptr};
 cudaStream_t engine_stream() {
     int dev = 0;
     CK(cudaGetDevice(&dev));
-    if (!g_stream[dev & 63]) CK(cudaStreamCreateWithFlags(&g_stream[dev & 63], cudaStreamNonBlocking));
+    if (!g_stream[dev & 63]) {
+        CK(cudaStreamCreateWithFlags(&g_stream[dev & 63], cudaStreamNonBlocking));
+        // keep freed scratch cached in the stream-ordered pool across calls (no re-mapping)
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t keep = ~0ull;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     return g_stream[dev & 63];
 }
 
@@ -929,10 +1059,18 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, b2l_findings **outp
     if (cols->n_events >= 0xFFFFFFFFull) return fail(B2L_E_INVALID_ARG, "trace too large for 32-bit event indices");
     std::lock_guard<std::mutex> lock(g_mu);
     cudaStream_t s = engine_stream();
-    ColsUpload up;
+    PhaseClock pc(s);
+    Internal *in = new Internal();
+    f->internal = in;
+    ColsUpload &up = in->cols;
     up.load(cols, s);
+    if (!cols->device_resident) {
+        in->cols_key[0] = cols->seq, in->cols_key[1] = cols->start_ns, in->cols_key[2] = cols->hash;
+        in->cols_n = cols->n_events;
+    }
     const DevCols c = up.d;
     const size_t n = c.n;
+    pc.mark("upload");
     DBuf<uint32_t> cnt(8, s);
     cnt.zero();
     // ---- 1. validation
@@ -951,6 +1089,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, b2l_findings **outp
             return fail(B2L_E_INVALID_TRACE, "trace fails validation");
         }
     }
+    pc.mark("validate");
     // ---- 2. partition
     DBuf<uint32_t> H(n ? n : 1, s), TT(n ? n : 1, s), AD(n ? n : 1, s), A(n ? n : 1, s), TK(n ? n : 1, s);
     compact(n, IsHashed{c}, H.p, cnt.p + 1, s);
@@ -958,56 +1097,72 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, b2l_findings **outp
     compact(n, IsAllocDelete{c}, AD.p, cnt.p + 3, s);
     compact(n, IsAlloc{c}, A.p, cnt.p + 4, s);
     compact(n, IsTargetKernel{c}, TK.p, cnt.p + 5, s);
-    DBuf<unsigned long long> maxend(1, s);
+    DBuf<unsigned long long> maxend(11, s);  // [0] max data-op end, [1..5] subset OR, [6..10] subset AND
     maxend.zero();
+    CK(cudaMemsetAsync(maxend.p + 6, 0xFF, 5 * sizeof(unsigned long long), s));
+    DBuf<uint32_t> srank(n ? n : 1, s);
     if (n) {
         k_max_data_end<<<grid_for(n, TPB, 148 * 8), TPB, 0, s>>>(c, maxend.p);
         CK_LAUNCH("k_max_data_end");
+        k_col_vary<<<grid_for(n, TPB, 148 * 8), TPB, 0, s>>>(c, maxend.p + 1);
+        CK_LAUNCH("k_col_vary");
+        scan<MaxU64>(n, SrankLoad{c.start}, SrankStore{srank.p}, s);
     }
     uint32_t hc[8];
-    unsigned long long me = 0;
-    CK(cudaMemcpyAsync(hc, cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&me, maxend.p, sizeof(me), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    unsigned long long hm[11];
+    read_back(hc, cnt.p, sizeof(hc), s);
+    read_back(hm, maxend.p, sizeof(hm), s);
+    const unsigned long long me = hm[0];
     const uint32_t nH = hc[1], nT = hc[2], nAD = hc[3], nA = hc[4], nK = hc[5];
+    g_masks.hash = live_mask(hm[1] ^ hm[6]), g_masks.da = live_mask(hm[2] ^ hm[7]);
+    g_masks.sa = live_mask(hm[3] ^ hm[8]), g_masks.nb = live_mask(hm[4] ^ hm[9]);
+    g_masks.sa_tt = live_mask(hm[5] ^ hm[10]);
+    g_masks.dev = live_range((uint64_t)(c.ndev > 0 ? c.ndev : 1));
+    g_masks.idx = live_range(n);
+    g_masks.srank = srank.p;
 
-    Internal *in = new Internal();
-    f->internal = in;
+    pc.mark("partition");
     in->synth_end = me;
     // ---- 3. duplicates + round trips
     DdRt dr = dd_rt_step(c, H.p, nH, (flags & B2L_ANALYZE_STRICT_RT) != 0, *in, s);
     in->dd_groups = dr.dd_groups, in->dd_members = dr.dd_members, in->rt_groups = dr.rt_groups,
     in->rt_trips = dr.rt_trips;
+    pc.mark("dd_rt");
     // ---- 4. pairs
     PairOut po = pairs_step(c, AD.p, nAD, A.p, nA, me, *in, s);
     in->n_pairs = nA;
+    pc.mark("pairs");
     // ---- 5. repeated allocations
     ra_step(c, nA, *in, s);
+    pc.mark("ra");
     // ---- 6. unused allocations / transfers
     ua_ut_step(c, TK.p, nK, TT.p, nT, *in, s);
+    pc.mark("ua_ut");
 
-    // ---- results to the host
+    // ---- results to the host (one pinned staging pass)
+    HostBatch hb;
     f->dd_groups = in->dd_groups;
-    f->dd_offsets = host_copy(in->dd_off.p, in->dd_groups + 1, s);
-    f->dd_members = host_copy(in->dd_mem.p, in->dd_members, s);
+    f->dd_offsets = hb.add(in->dd_off.p, in->dd_groups + 1);
+    f->dd_members = hb.add(in->dd_mem.p, in->dd_members);
     f->rt_groups = in->rt_groups;
-    f->rt_offsets = host_copy(in->rt_off.p, in->rt_groups + 1, s);
-    f->rt_tx = host_copy(in->rt_tx.p, in->rt_trips, s);
-    f->rt_rx = host_copy(in->rt_rx.p, in->rt_trips, s);
+    f->rt_offsets = hb.add(in->rt_off.p, in->rt_groups + 1);
+    f->rt_tx = hb.add(in->rt_tx.p, in->rt_trips);
+    f->rt_rx = hb.add(in->rt_rx.p, in->rt_trips);
     f->n_pairs = nA;
-    f->pair_alloc = host_copy(in->pair_alloc.p, nA, s);
-    f->pair_delete = host_copy(in->pair_delete.p, nA, s);
+    f->pair_alloc = hb.add(in->pair_alloc.p, nA);
+    f->pair_delete = hb.add(in->pair_delete.p, nA);
     f->synthetic_end_ns = me;
     f->n_warnings = po.n_warn;
-    f->warn_index = host_copy(po.warn.p, po.n_warn, s);
+    f->warn_index = hb.add(po.warn.p, po.n_warn);
     f->ra_groups = in->ra_groups;
-    f->ra_offsets = host_copy(in->ra_off.p, in->ra_groups + 1, s);
-    f->ra_pairs = host_copy(in->ra_mem.p, in->ra_members, s);
+    f->ra_offsets = hb.add(in->ra_off.p, in->ra_groups + 1);
+    f->ra_pairs = hb.add(in->ra_mem.p, in->ra_members);
     f->n_ua = in->n_ua;
-    f->ua_pairs = host_copy(in->ua.p, in->n_ua, s);
+    f->ua_pairs = hb.add(in->ua.p, in->n_ua);
     f->n_ut = in->n_ut;
-    f->ut_events = host_copy(in->ut.p, in->n_ut, s);
-    CK(cudaStreamSynchronize(s));
+    f->ut_events = hb.add(in->ut.p, in->n_ut);
+    hb.flush(s);
+    pc.mark("d2h");
     if (in->dd_groups == 0) f->dd_offsets[0] = 0;
     if (in->rt_groups == 0) f->rt_offsets[0] = 0;
     if (in->ra_groups == 0) f->ra_offsets[0] = 0;
@@ -1184,8 +1339,16 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     std::lock_guard<std::mutex> lock(g_mu);
     cudaStream_t s = engine_stream();
     ColsUpload up;
-    up.load(cols, s);
-    const DevCols c = up.d;
+    const Internal *fin = (const Internal *)f->internal;
+    DevCols c;
+    if (fin && !cols->device_resident && fin->cols_n == cols->n_events && fin->cols_key[0] == (const void *)cols->seq &&
+        fin->cols_key[1] == (const void *)cols->start_ns && fin->cols_key[2] == (const void *)cols->hash) {
+        c = fin->cols.d;  // the same host columns analyze() uploaded: reuse the device copy
+        c.nlocs = cols->n_locs, c.nbuckets = cols->n_buckets;
+    } else {
+        up.load(cols, s);
+        c = up.d;
+    }
     const size_t n = c.n;
     // findings on the device: reuse the engine's copies, or upload caller arrays
     FindingsDev F{};
@@ -1301,24 +1464,24 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     // ---- to host
     unsigned long long h[15];
     uint32_t hov = 0, hun = 0;
-    CK(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&hov, ovl.p, sizeof(hov), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&hun, unic.p, sizeof(hun), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    read_back(h, acc.p, sizeof(h), s);
+    read_back(&hov, ovl.p, sizeof(hov), s);
+    read_back(&hun, unic.p, sizeof(hun), s);
     for (int k = 0; k < 5; ++k) o->per_category_ns[k] = b2l_u128{h[2 * k], h[2 * k + 1]};
     o->union_ns = b2l_u128{h[10], h[11]};
     o->n_union = hun;
     o->has_overlaps = hov ? 1 : 0;
     o->min_start_ns = n ? h[13] : 0;
     o->max_end_ns = h[14];
-    o->union_index = host_copy(uni.p, hun, s);
+    HostBatch hb;
+    o->union_index = hb.add(uni.p, hun);
     o->n_buckets = nb;
     const size_t nb5 = 5 * (size_t)nb;
-    o->attr_count = (uint64_t *)host_copy(at.p, nb5, s);
-    o->attr_ns = (b2l_u128 *)host_copy(at.p + nb5, 2 * nb5, s);
-    o->attr_bytes = (b2l_u128 *)host_copy(at.p + 3 * nb5, 2 * nb5, s);
-    o->attr_first = (uint64_t *)host_copy(at.p + 5 * nb5, nb5, s);
-    CK(cudaStreamSynchronize(s));
+    o->attr_count = (uint64_t *)hb.add(at.p, nb5);
+    o->attr_ns = (b2l_u128 *)hb.add(at.p + nb5, 2 * nb5);
+    o->attr_bytes = (b2l_u128 *)hb.add(at.p + 3 * nb5, 2 * nb5);
+    o->attr_first = (uint64_t *)hb.add(at.p + 5 * nb5, nb5);
+    hb.flush(s);
     return B2L_OK;
 }
 

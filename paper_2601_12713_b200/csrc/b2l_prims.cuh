@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -225,28 +226,35 @@ void scan(size_t n, Load ld, Store st, cudaStream_t s, typename Op::T *d_total =
     CK_LAUNCH("k_scan_apply");
 }
 
-// ---------------------------------------------------------------- pinned scalar readback
-struct HostScalars {
-    uint64_t *h = nullptr;
-    uint64_t *d = nullptr;
-    int cap = 0;
-    cudaStream_t s = nullptr;
-    HostScalars(int n, cudaStream_t st) : cap(n), s(st) {
-        CK(cudaMallocHost(&h, n * sizeof(uint64_t)));
-        CK(cudaMallocAsync((void **)&d, n * sizeof(uint64_t), st));
-        CK(cudaMemsetAsync(d, 0, n * sizeof(uint64_t), st));
-    }
-    ~HostScalars() {
-        if (d) cudaFreeAsync(d, s);
-        if (h) cudaFreeHost(h);
-    }
-    uint64_t *dev(int i) { return d + i; }
-    // copy slots [0, k) back and wait
-    void fetch(int k) {
-        CK(cudaMemcpyAsync(h, d, k * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+// ---------------------------------------------------------------- pinned readback staging
+// A per-thread pinned buffer (grown, never per call): small device->host reads and the result
+// arrays go through it, so no call pays cudaMallocHost / pageable-copy costs.
+struct Pinned {
+    uint8_t *p = nullptr;
+    size_t cap = 0;
+    uint8_t *reserve(size_t bytes) {
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            size_t c = bytes < (1u << 20) ? (1u << 20) : bytes + bytes / 2;
+            CK(cudaMallocHost(&p, c));
+            cap = c;
+        }
+        return p;
     }
 };
+inline Pinned &pinned() {
+    static thread_local Pinned pn;
+    return pn;
+}
+// Read `bytes` from device memory into host `dst` (synchronous).
+inline void read_back(void *dst, const void *d_src, size_t bytes, cudaStream_t s) {
+    uint8_t *st = pinned().reserve(bytes);
+    CK(cudaMemcpyAsync(st, d_src, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    memcpy(dst, st, bytes);
+}
 
 // ---------------------------------------------------------------- compaction
 template <class Pred>
@@ -284,7 +292,7 @@ struct StoreExclU32 {
 
 // ---------------------------------------------------------------- radix sort
 constexpr int RS_THREADS = 256;
-constexpr int RS_ROUNDS = 16;
+constexpr int RS_ROUNDS = 8;
 constexpr int RS_TILE = RS_THREADS * RS_ROUNDS;
 
 template <int KW>
@@ -301,7 +309,13 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // Histograms of every digit position of every key word in one read of the keys:
 // hist[(w * 8 + byte) * 256 + digit].  Warp-aggregated (match_any) shared-memory counts.
 template <int KW>
-__global__ void __launch_bounds__(RS_THREADS) k_radix_hist_all(KeyCols<KW> k, size_t n, uint32_t *__restrict__ hist) {
+struct LiveBytes {
+    uint8_t m[KW];  // bit b set: byte b of word w may differ between keys
+};
+
+template <int KW>
+__global__ void __launch_bounds__(RS_THREADS) k_radix_hist_all(KeyCols<KW> k, size_t n, LiveBytes<KW> live,
+                                                               uint32_t *__restrict__ hist) {
     __shared__ uint32_t sh[KW * 8][256];
     for (int i = threadIdx.x; i < KW * 8 * 256; i += RS_THREADS) (&sh[0][0])[i] = 0;
     __syncthreads();
@@ -315,6 +329,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_hist_all(KeyCols<KW> k, si
             const uint64_t key = valid ? k.w[w][i] : 0;
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
+                if (!((live.m[w] >> b) & 1)) continue;
                 const uint32_t d = valid ? (uint32_t)(key >> (8 * b)) & 255u : 256u;
                 const uint32_t peers = __match_any_sync(0xffffffffu, d);
                 if (valid && lane == __ffs(peers) - 1) atomicAdd(&sh[w * 8 + b][d], (uint32_t)__popc(peers));
@@ -424,38 +439,53 @@ struct SortBufs {
 };
 
 // Stable sort of n records (keys KW words, value u32) held in side `b.cur`; on return b.cur names
-// the side holding the sorted records.  One histogram read + one host sync (pass planning:
-// a digit position is skipped when one bin holds all n keys), then one launch per live pass.
+// the side holding the sorted records.  `live` names the key bytes that may vary (callers derive it
+// from column-wide OR-of-XOR masks and known value ranges), so there is no host round trip: one
+// histogram read of the keys, then one Onesweep launch per live digit position.
 template <int KW>
-void radix_sort(SortBufs<KW> &b, size_t n, cudaStream_t s) {
+void radix_sort(SortBufs<KW> &b, size_t n, LiveBytes<KW> live, cudaStream_t s) {
     if (n <= 1) return;
     if (n >= (size_t)LB_VAL) throw EngineErr{B2L_E_INVALID_ARG, "radix_sort: too many records"};
+    int npass = 0;
+    for (int w = 0; w < KW; ++w) npass += __builtin_popcount(live.m[w]);
+    if (npass == 0) return;
     constexpr int NPOS = KW * 8;
     DBuf<uint32_t> hist((size_t)NPOS * 256, s);
     hist.zero();
-    k_radix_hist_all<KW><<<grid_for(n, RS_THREADS, 148 * 4), RS_THREADS, 0, s>>>(b.k[b.cur], n, hist.p);
+    k_radix_hist_all<KW><<<grid_for(n, RS_THREADS, 148 * 4), RS_THREADS, 0, s>>>(b.k[b.cur], n, live, hist.p);
     CK_LAUNCH("k_radix_hist_all");
-    static thread_local uint32_t *h_hist = nullptr;
-    if (!h_hist) CK(cudaMallocHost(&h_hist, 3 * 8 * 256 * sizeof(uint32_t)));
-    CK(cudaMemcpyAsync(h_hist, hist.p, (size_t)NPOS * 256 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
     const unsigned ntiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
-    DBuf<uint32_t> status((size_t)ntiles * 256 + 1, s);
+    const size_t stride = (size_t)ntiles * 256 + 32;  // status words + tile counter per pass
+    DBuf<uint32_t> status(stride * npass, s);
+    status.zero();
+    int p = 0;
     for (int w = KW - 1; w >= 0; --w) {
         for (int byte = 0; byte < 8; ++byte) {
-            const uint32_t *hp = h_hist + (size_t)(w * 8 + byte) * 256;
-            bool trivial = false;
-            for (int d = 0; d < 256; ++d)
-                if (hp[d] == n) trivial = true;
-            if (trivial) continue;  // digit constant over all keys: identity pass
-            CK(cudaMemsetAsync(status.p, 0, status.n * sizeof(uint32_t), s));
+            if (!((live.m[w] >> byte) & 1)) continue;
+            uint32_t *stp = status.p + stride * p++;
             k_onesweep<KW><<<ntiles, RS_THREADS, 0, s>>>(b.k[b.cur], b.v[b.cur], b.k[b.cur ^ 1], b.v[b.cur ^ 1], n, w,
-                                                         8 * byte, hist.p + (size_t)(w * 8 + byte) * 256, status.p,
-                                                         status.p + (size_t)ntiles * 256);
+                                                         8 * byte, hist.p + (size_t)(w * 8 + byte) * 256, stp,
+                                                         stp + (size_t)ntiles * 256);
             CK_LAUNCH("k_onesweep");
             b.cur ^= 1;
         }
     }
+}
+
+// Live-byte mask of a value range [0, v): the low bytes needed to represent v - 1.
+inline uint8_t live_range(uint64_t v) {
+    if (v <= 1) return 0;
+    uint64_t x = v - 1;
+    uint8_t m = 0;
+    for (int b = 0; b < 8 && x; ++b, x >>= 8) m |= (uint8_t)(1u << b);
+    return m;
+}
+// Live-byte mask from an OR-of-XOR column mask.
+inline uint8_t live_mask(uint64_t vary) {
+    uint8_t m = 0;
+    for (int b = 0; b < 8; ++b)
+        if ((vary >> (8 * b)) & 255ull) m |= (uint8_t)(1u << b);
+    return m;
 }
 
 // Owning storage for a sort of n records.
