@@ -106,7 +106,14 @@ enum {
     B2L_RULE_ORDER_SORT = 1 << 10,   /* "order": events not sorted by (start_ns, seq) */
     B2L_RULE_ORDER_SEQ = 1 << 11     /* "order": seq values not strictly increasing */
 };
-enum { B2L_ANALYZE_STRICT_RT = 1 }; /* analyze(strict_pseudocode=True), detectors.py:145-160 */
+enum {
+    B2L_ANALYZE_STRICT_RT = 1,      /* analyze(strict_pseudocode=True), detectors.py:145-160 */
+    B2L_ANALYZE_VALIDATE_ONLY = 2,  /* stop after validation (sharded analysis validates shards) */
+    B2L_ANALYZE_SYNTH_END = 4,      /* b2l_analyze_ex: use the given synthetic-delete time (prep.py:61-62
+                                       max end over ALL data ops -- a trace-wide value for a shard) */
+    B2L_ANALYZE_SKIP_DDRT = 8,      /* shard holds no hash-keyed work: skip DD / RT */
+    B2L_ANALYZE_SKIP_ALLOC = 16     /* shard holds no device-keyed work: skip pairs / RA / UA / UT */
+};
 #define B2L_SYNTHETIC 0xFFFFFFFFu   /* pair_delete of a synthetic trace-end delete (prep.py:78-93) */
 
 /* Trace columns (structure of arrays, one entry per event). */
@@ -165,6 +172,8 @@ typedef struct b2l_findings {
  * (num_devices_total, host_device) are the caller's.  *out must be freed with
  * b2l_findings_free (also on B2L_E_INVALID_TRACE). */
 int b2l_analyze(const b2l_trace_cols *cols, uint32_t flags, b2l_findings **out);
+/* Shard form used by the multi-GPU analysis (paper_2601_12713_b200/sharded.py). */
+int b2l_analyze_ex(const b2l_trace_cols *cols, uint32_t flags, uint64_t synthetic_end_ns, b2l_findings **out);
 void b2l_findings_free(b2l_findings *f);
 
 typedef struct b2l_u128 { uint64_t lo, hi; } b2l_u128;

@@ -211,8 +211,9 @@ def _ut(d, kernels, tt, ndev):
     return unused
 
 
-def analyze_cols(c, strict=False) -> RefFindings:
-    """detectors.py:274-326 over columns (assumes validate_cols() was empty)."""
+def analyze_cols(c, strict=False, synth_end=None) -> RefFindings:
+    """detectors.py:274-326 over columns (assumes validate_cols() was empty).  ``synth_end``
+    overrides the synthetic-delete time (prep.py:61-62) -- used for shards of a trace."""
     d = _ints(c)
     host, ndev = c.host_device, c.num_devices_total
     hashed, tt, data_ops, tk = [], [], [], []
@@ -228,7 +229,9 @@ def analyze_cols(c, strict=False) -> RefFindings:
             data_ops.append(i)
         elif k == KERNEL and d["dst"][i] != host:
             tk.append(i)
-    pairs, warns, synth_end = _pairs(d, data_ops)
+    pairs, warns, local_end = _pairs(d, data_ops)
+    if synth_end is None:
+        synth_end = local_end
     target_pairs = [pi for pi, (a, _) in enumerate(pairs) if d["dst"][a] != host]
     return RefFindings(dd=_dd(d, hashed), rt=_rt(d, hashed, strict), pairs=pairs, synthetic_end=synth_end,
                        warnings=warns, ra=_ra(d, pairs), ua=_ua(d, tk, pairs, target_pairs, ndev, synth_end),

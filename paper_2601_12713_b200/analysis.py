@@ -78,6 +78,8 @@ def _L():
     if not _declared:
         L.b2l_analyze.argtypes = [ctypes.POINTER(_Cols), _u32, ctypes.POINTER(ctypes.POINTER(_Findings))]
         L.b2l_analyze.restype = ctypes.c_int
+        L.b2l_analyze_ex.argtypes = [ctypes.POINTER(_Cols), _u32, _u64, ctypes.POINTER(ctypes.POINTER(_Findings))]
+        L.b2l_analyze_ex.restype = ctypes.c_int
         L.b2l_findings_free.argtypes = [ctypes.POINTER(_Findings)]
         L.b2l_findings_free.restype = None
         L.b2l_savings_compute.argtypes = [ctypes.POINTER(_Cols), ctypes.POINTER(_Findings),
@@ -190,16 +192,24 @@ class EngineInvalid(Exception):
         self.bad_rules = bad_rules
 
 
-def analyze_columns(cols: Columns, strict: bool = False) -> ColumnarFindings:
+FLAG_STRICT_RT, FLAG_VALIDATE_ONLY, FLAG_SYNTH_END, FLAG_SKIP_DDRT, FLAG_SKIP_ALLOC = 1, 2, 4, 8, 16
+
+
+def analyze_columns(cols: Columns, strict: bool = False, flags: int = 0,
+                    synthetic_end_ns: Optional[int] = None) -> ColumnarFindings:
     """Run the whole detection pipeline on the device.  Raises EngineInvalid with
-    the flagged events / rule bits when the trace fails validation."""
+    the flagged events / rule bits when the trace fails validation.  ``flags`` /
+    ``synthetic_end_ns`` are the shard controls of b2l_analyze_ex (sharded.py)."""
     L = _L()
     if isinstance(cols, DeviceColumns):
         cs, keep = cols.struct, None
     else:
         cs, keep = _cols_struct(cols)
     fp = ctypes.POINTER(_Findings)()
-    rc = L.b2l_analyze(ctypes.byref(cs), 1 if strict else 0, ctypes.byref(fp))
+    fl = flags | (FLAG_STRICT_RT if strict else 0)
+    if synthetic_end_ns is not None:
+        fl |= FLAG_SYNTH_END
+    rc = L.b2l_analyze_ex(ctypes.byref(cs), fl, int(synthetic_end_ns or 0), ctypes.byref(fp))
     handle = _Handle(fp if fp else None)
     del keep
     if rc == _lib.B2L_E_INVALID_TRACE:
@@ -207,6 +217,8 @@ def analyze_columns(cols: Columns, strict: bool = False) -> ColumnarFindings:
         raise EngineInvalid(_arr(f.bad_index, f.n_bad, np.uint32), _arr(f.bad_rules, f.n_bad, np.uint32))
     _lib.check(rc, "b2l_analyze")
     f = fp.contents
+    if flags & FLAG_VALIDATE_ONLY:
+        return None
     return ColumnarFindings(
         n_events=f.n_events,
         dd_offsets=_arr(f.dd_offsets, f.dd_groups + 1, np.uint64), dd_members=None,

@@ -1051,7 +1051,7 @@ cudaStream_t engine_stream() {
     return g_stream[dev & 63];
 }
 
-int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, b2l_findings **outp) {
+int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_override, b2l_findings **outp) {
     b2l_findings *f = (b2l_findings *)calloc(1, sizeof(b2l_findings));
     if (!f) return fail(B2L_E_OOM, "host allocation failed");
     *outp = f;
@@ -1090,6 +1090,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, b2l_findings **outp
         }
     }
     pc.mark("validate");
+    if (flags & B2L_ANALYZE_VALIDATE_ONLY) return B2L_OK;
     // ---- 2. partition
     DBuf<uint32_t> H(n ? n : 1, s), TT(n ? n : 1, s), AD(n ? n : 1, s), A(n ? n : 1, s), TK(n ? n : 1, s);
     compact(n, IsHashed{c}, H.p, cnt.p + 1, s);
@@ -1112,8 +1113,10 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, b2l_findings **outp
     unsigned long long hm[11];
     read_back(hc, cnt.p, sizeof(hc), s);
     read_back(hm, maxend.p, sizeof(hm), s);
-    const unsigned long long me = hm[0];
-    const uint32_t nH = hc[1], nT = hc[2], nAD = hc[3], nA = hc[4], nK = hc[5];
+    const unsigned long long me = (flags & B2L_ANALYZE_SYNTH_END) ? synth_end_override : hm[0];
+    const bool ddrt = !(flags & B2L_ANALYZE_SKIP_DDRT), alloc = !(flags & B2L_ANALYZE_SKIP_ALLOC);
+    const uint32_t nH = ddrt ? hc[1] : 0, nT = alloc ? hc[2] : 0, nAD = alloc ? hc[3] : 0, nA = alloc ? hc[4] : 0,
+                   nK = alloc ? hc[5] : 0;
     g_masks.hash = live_mask(hm[1] ^ hm[6]), g_masks.da = live_mask(hm[2] ^ hm[7]);
     g_masks.sa = live_mask(hm[3] ^ hm[8]), g_masks.nb = live_mask(hm[4] ^ hm[9]);
     g_masks.sa_tt = live_mask(hm[5] ^ hm[10]);
@@ -1531,7 +1534,19 @@ int b2l_analyze(const b2l_trace_cols *cols, uint32_t flags, b2l_findings **out) 
     if (!cols || !out) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
     *out = nullptr;
     try {
-        return b2l::ana::analyze_impl(cols, flags, out);
+        return b2l::ana::analyze_impl(cols, flags, 0, out);
+    } catch (const b2l::EngineErr &e) {
+        return b2l::fail(e.code, e.msg);
+    } catch (const std::exception &e) {
+        return b2l::fail(B2L_E_CUDA, e.what());
+    }
+}
+
+int b2l_analyze_ex(const b2l_trace_cols *cols, uint32_t flags, uint64_t synthetic_end_ns, b2l_findings **out) {
+    if (!cols || !out) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
+    *out = nullptr;
+    try {
+        return b2l::ana::analyze_impl(cols, flags, synthetic_end_ns, out);
     } catch (const b2l::EngineErr &e) {
         return b2l::fail(e.code, e.msg);
     } catch (const std::exception &e) {

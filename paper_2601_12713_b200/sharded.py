@@ -1,0 +1,361 @@
+"""Key-range sharded trace analysis across G ranks.
+
+Input: rank r holds a seq-range shard of the trace (contiguous events
+[base_r, base_r + n_r)).  The detectors split along two keys:
+
+  * hash-keyed work -- DD and RT (detectors.py:85-167) only ever relate
+    transfers with the same content hash, so hashed transfers go to the rank
+    owning their hash range ((hash * G) >> 64);
+  * device-keyed work -- LIFO pairing (prep.py:45-96, key (dst_dev, dst_addr)),
+    RA (key (src_addr, dst_dev, bytes)), UA and UT (per target device sweeps,
+    detectors.py:194-271) never cross a device, so allocs/deletes, target
+    kernels and target transfers go to the rank owning their device (dev % G).
+
+One all-to-all redistributes the events (both key spaces in one exchange);
+each rank runs the single-GPU engine on its two sub-traces (a sub-trace keeps
+global trace order, so every detector is exact on it; the synthetic-delete
+time, a trace-wide max, comes from one all-reduce); a final gather brings the
+findings to rank 0, which merges them into the reference's global orders
+(groups by (first start, key...), pairs by allocation, lists by position).
+
+The exchange goes through a small communicator interface: ``TorchComm``
+(torch.distributed: NCCL on GPUs, gloo on CPU) or ``LocalComm`` (G ranks as
+threads of one process -- used to check G-way parity on a single GPU).
+"""
+from __future__ import annotations
+
+import threading
+from typing import Callable, List, Optional
+
+import numpy as np
+
+from .analysis import FLAG_SKIP_ALLOC, FLAG_SKIP_DDRT, FLAG_VALIDATE_ONLY, ColumnarFindings, EngineInvalid
+from .columns import Columns
+
+FIELDS = ("seq", "start_ns", "end_ns", "src_addr", "dst_addr", "bytes", "hash", "src_device", "dst_device",
+          "kind", "loc")
+ROW = 1 + len(FIELDS)  # global index + fields, one u64 each
+SYN = np.uint32(0xFFFFFFFF)
+TRANSFER, ALLOC, DELETE, KERNEL = 0, 1, 2, 3
+
+
+# ------------------------------------------------------------------------ communicators
+class LocalComm:
+    """G ranks as threads of one process (shared slots + a barrier)."""
+
+    class _Shared:
+        def __init__(self, g):
+            self.g = g
+            self.barrier = threading.Barrier(g)
+            self.slots = [None] * g
+
+    def __init__(self, shared, rank):
+        self.s, self.rank, self.size = shared, rank, shared.g
+
+    @classmethod
+    def group(cls, g):
+        sh = cls._Shared(g)
+        return [cls(sh, r) for r in range(g)]
+
+    def _exchange(self, obj):
+        self.s.barrier.wait()
+        self.s.slots[self.rank] = obj
+        self.s.barrier.wait()
+        out = list(self.s.slots)
+        self.s.barrier.wait()
+        return out
+
+    def alltoall(self, parts: List[np.ndarray]) -> List[np.ndarray]:
+        allp = self._exchange(parts)
+        return [allp[src][self.rank] for src in range(self.size)]
+
+    def allreduce_max(self, v: int) -> int:
+        return max(self._exchange(int(v)))
+
+    def allgather(self, obj):
+        return self._exchange(obj)
+
+    def gather0(self, obj):
+        out = self._exchange(obj)
+        return out if self.rank == 0 else None
+
+
+class TorchComm:
+    """torch.distributed communicator (NCCL for CUDA tensors, gloo on CPU)."""
+
+    def __init__(self, device=None):
+        import torch
+        import torch.distributed as dist
+        self.dist, self.torch = dist, torch
+        self.rank, self.size = dist.get_rank(), dist.get_world_size()
+        self.device = device if device is not None else (
+            torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu"))
+
+    def alltoall(self, parts: List[np.ndarray]) -> List[np.ndarray]:
+        torch = self.torch
+        sizes = torch.tensor([p.shape[0] for p in parts], dtype=torch.int64, device=self.device)
+        rsizes = torch.empty_like(sizes)
+        self.dist.all_to_all_single(rsizes, sizes)
+        rs = rsizes.cpu().tolist()
+        send = np.concatenate([p.reshape(-1, ROW) for p in parts]).view(np.int64) if parts else np.zeros((0, ROW))
+        st = torch.from_numpy(np.ascontiguousarray(send).reshape(-1)).to(self.device)
+        rt = torch.empty(sum(rs) * ROW, dtype=torch.int64, device=self.device)
+        self.dist.all_to_all_single(rt, st, [r * ROW for r in rs], [p.shape[0] * ROW for p in parts])
+        flat = rt.cpu().numpy().view(np.uint64).reshape(-1, ROW)
+        out, o = [], 0
+        for r in rs:
+            out.append(flat[o:o + r])
+            o += r
+        return out
+
+    def allreduce_max(self, v: int) -> int:
+        """Max of a u64 over ranks, as (hi, lo) 32-bit halves (exact for any u64)."""
+        torch, dist = self.torch, self.dist
+        hi = torch.tensor([int(v) >> 32], dtype=torch.int64, device=self.device)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        mine = (int(v) & 0xFFFFFFFF) if (int(v) >> 32) == int(hi.item()) else 0
+        lo = torch.tensor([mine], dtype=torch.int64, device=self.device)
+        dist.all_reduce(lo, op=dist.ReduceOp.MAX)
+        return (int(hi.item()) << 32) | int(lo.item())
+
+    def allgather(self, obj):
+        out = [None] * self.size
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def gather0(self, obj):
+        out = [None] * self.size if self.rank == 0 else None
+        self.dist.gather_object(obj, out, dst=0)
+        return out
+
+
+# ------------------------------------------------------------------------ packing
+def _rows(cols: Columns, idx: np.ndarray, base: int) -> np.ndarray:
+    r = np.empty((idx.size, ROW), dtype=np.uint64)
+    r[:, 0] = idx.astype(np.uint64) + np.uint64(base)
+    for k, f in enumerate(FIELDS):
+        a = getattr(cols, f)[idx]
+        r[:, k + 1] = a.astype(np.int64).view(np.uint64) if a.dtype == np.int32 else a.astype(np.uint64)
+    return r
+
+
+def _subtrace(rows: np.ndarray, like: Columns):
+    g = rows[:, 0].astype(np.int64)
+    order = np.argsort(g, kind="stable")  # concatenation of rank-ordered runs is already sorted; be safe
+    rows = rows[order]
+    col = {}
+    for k, f in enumerate(FIELDS):
+        v = rows[:, k + 1]
+        col[f] = v.view(np.int64).astype(np.int32) if f in ("src_device", "dst_device") else (
+            v.astype(np.uint8) if f == "kind" else (v.astype(np.uint32) if f == "loc" else v.copy()))
+    sub = Columns(n=rows.shape[0], num_devices_total=like.num_devices_total, host_device=like.host_device,
+                  seq=col["seq"], start_ns=col["start_ns"], end_ns=col["end_ns"], src_addr=col["src_addr"],
+                  dst_addr=col["dst_addr"], bytes=col["bytes"], hash=col["hash"], src_device=col["src_device"],
+                  dst_device=col["dst_device"], kind=col["kind"], loc=col["loc"], loc_flags=like.loc_flags,
+                  loc_bucket=like.loc_bucket, n_buckets=like.n_buckets, bucket_keys=like.bucket_keys,
+                  wall_time_ns=like.wall_time_ns, locs=like.locs)
+    return sub, rows[:, 0].astype(np.int64)
+
+
+def hash_owner(h: np.ndarray, g: int) -> np.ndarray:
+    return (((h >> np.uint64(32)) * np.uint64(g)) >> np.uint64(32)).astype(np.int64)
+
+
+# ------------------------------------------------------------------------ the sharded pipeline
+def engine_analyzer(cols, flags=0, synthetic_end_ns=None, strict=False):
+    from .analysis import analyze_columns
+    return analyze_columns(cols, strict=strict, flags=flags, synthetic_end_ns=synthetic_end_ns)
+
+
+def analyze_sharded(shard: Columns, base: int, comm, strict: bool = False,
+                    analyzer: Callable = engine_analyzer) -> Optional[ColumnarFindings]:
+    """Findings of the whole trace (global event indices) on rank 0, None elsewhere.
+    Raises EngineInvalid (global indices) on every rank if any shard fails validation."""
+    G = comm.size
+    # ---- 1. validation of every shard + the order rule across shard boundaries (model.py:193-196)
+    bad_i, bad_r = np.zeros(0, np.int64), np.zeros(0, np.uint32)
+    try:
+        analyzer(shard, flags=FLAG_VALIDATE_ONLY)
+    except EngineInvalid as exc:
+        bad_i, bad_r = exc.bad_index.astype(np.int64), exc.bad_rules.astype(np.uint32)
+    edge = (int(shard.start_ns[0]), int(shard.seq[0]), int(shard.start_ns[-1]), int(shard.seq[-1])) \
+        if shard.n else None
+    edges = comm.allgather(edge)
+    prev = None
+    for r in range(comm.rank):
+        if edges[r] is not None:
+            prev = edges[r]
+    if prev is not None and shard.n:
+        s0, q0 = int(shard.start_ns[0]), int(shard.seq[0])
+        m = 0
+        if s0 < prev[2] or (s0 == prev[2] and q0 < prev[3]):
+            m |= 1 << 10
+        if q0 <= prev[3]:
+            m |= 1 << 11
+        if m:
+            k = np.nonzero(bad_i == 0)[0]
+            if k.size:
+                bad_r[k[0]] |= m
+            else:
+                bad_i, bad_r = np.concatenate([[0], bad_i]), np.concatenate([[m], bad_r]).astype(np.uint32)
+    all_bad = comm.allgather((bad_i + base, bad_r))
+    gi = np.concatenate([b[0] for b in all_bad])
+    if gi.size:
+        raise EngineInvalid(gi.astype(np.uint32), np.concatenate([b[1] for b in all_bad]).astype(np.uint32))
+
+    # ---- 2. one all-to-all: hashed transfers by hash range, device work by device
+    kind, nb, h, dst = shard.kind, shard.bytes, shard.hash, shard.dst_device.astype(np.int64)
+    is_h = (kind == TRANSFER) & (nb > 0) & (h != 0)
+    is_d = (kind == ALLOC) | (kind == DELETE) | (((kind == KERNEL) | (kind == TRANSFER)) & (dst != shard.host_device))
+    dmax = int(shard.end_ns[kind != KERNEL].max()) if np.any(kind != KERNEL) else 0
+    ih, idv = np.nonzero(is_h)[0], np.nonzero(is_d)[0]
+    oh, od = hash_owner(h[ih], G), dst[idv] % G
+    rows_h, rows_d = _rows(shard, ih, base), _rows(shard, idv, base)
+    parts = []
+    for r in range(G):
+        a, b = rows_h[oh == r], rows_d[od == r]
+        tag = np.zeros((a.shape[0] + b.shape[0], 1), dtype=np.uint64)
+        tag[a.shape[0]:] = 1
+        # the tag (key space) travels in the top bit of the global index column
+        both = np.concatenate([a, b])
+        both[:, 0] |= tag[:, 0] << np.uint64(63)
+        parts.append(both)
+    got = comm.alltoall(parts)
+    synth_end = comm.allreduce_max(dmax)
+    rec = np.concatenate(got) if got else np.zeros((0, ROW), np.uint64)
+    space = rec[:, 0] >> np.uint64(63)
+    rec = rec.copy()
+    rec[:, 0] &= np.uint64((1 << 63) - 1)
+    sub_h, gid_h = _subtrace(rec[space == 0], shard)
+    sub_d, gid_d = _subtrace(rec[space == 1], shard)
+
+    # ---- 3. per-rank engine runs on the two sub-traces
+    out = {}
+    if sub_h.n:
+        f = analyzer(sub_h, flags=FLAG_SKIP_ALLOC, strict=strict)
+        G_ = gid_h
+        off = f.dd_offsets.astype(np.int64)
+        mem = G_[f.dd_members.astype(np.int64)]
+        first = mem[off[:-1]] if off.size > 1 else np.zeros(0, np.int64)
+        out["dd"] = (off, mem, sub_h.start_ns[f.dd_members[off[:-1]]] if off.size > 1 else np.zeros(0, np.uint64),
+                     sub_h.hash[f.dd_members[off[:-1]]] if off.size > 1 else np.zeros(0, np.uint64),
+                     sub_h.dst_device[f.dd_members[off[:-1]]] if off.size > 1 else np.zeros(0, np.int32), first)
+        off = f.rt_offsets.astype(np.int64)
+        tx, rx = f.rt_tx.astype(np.int64), f.rt_rx.astype(np.int64)
+        ft = tx[off[:-1]] if off.size > 1 else np.zeros(0, np.int64)
+        out["rt"] = (off, G_[tx], G_[rx], sub_h.start_ns[ft], sub_h.hash[ft], sub_h.src_device[ft],
+                     sub_h.dst_device[ft])
+    if sub_d.n:
+        f = analyzer(sub_d, flags=FLAG_SKIP_DDRT, synthetic_end_ns=synth_end)
+        G_ = gid_d
+        pa = f.pair_alloc.astype(np.int64)
+        pd = f.pair_delete
+        out["pairs"] = (G_[pa], np.where(pd == SYN, -1, G_[np.where(pd == SYN, 0, pd).astype(np.int64)]))
+        out["warn"] = G_[f.warn_index.astype(np.int64)]
+        off = f.ra_offsets.astype(np.int64)
+        ra_alloc = G_[pa[f.ra_pairs.astype(np.int64)]]
+        fa = pa[f.ra_pairs[off[:-1]].astype(np.int64)] if off.size > 1 else np.zeros(0, np.int64)
+        out["ra"] = (off, ra_alloc, sub_d.start_ns[fa], sub_d.src_addr[fa], sub_d.dst_device[fa], sub_d.bytes[fa])
+        out["ua"] = G_[pa[f.ua_pairs.astype(np.int64)]]
+        out["ut"] = G_[f.ut_events.astype(np.int64)]
+    parts = comm.gather0(out)
+    if comm.rank != 0:
+        return None
+    return _merge(parts, synth_end, total_events=None)
+
+
+def _cat(parts, key, k, dtype):
+    arrs = [p[key][k] for p in parts if key in p]
+    return np.concatenate(arrs).astype(dtype) if arrs else np.zeros(0, dtype)
+
+
+def _merge_groups(parts, key, member_cols, sort_cols):
+    """Concatenate per-rank groups and order them by the given key columns (lexicographic)."""
+    offs, mems, keys = [], [[] for _ in member_cols], [[] for _ in sort_cols]
+    for p in parts:
+        if key not in p:
+            continue
+        t = p[key]
+        offs.append(t[0])
+        for j, c in enumerate(member_cols):
+            mems[j].append(t[c])
+        for j, c in enumerate(sort_cols):
+            keys[j].append(np.asarray(t[c]).astype(np.int64).astype(np.uint64) if np.asarray(t[c]).dtype == np.int32
+                           else np.asarray(t[c]).astype(np.uint64))
+    sizes = [np.diff(o) for o in offs]
+    if not sizes or sum(s.size for s in sizes) == 0:
+        return np.zeros(1, np.uint64), [np.zeros(0, np.int64) for _ in member_cols]
+    size = np.concatenate(sizes)
+    starts = np.concatenate([o[:-1] + sum(len(m) for m in mems[0][:i]) for i, o in enumerate(offs)])
+    kcols = [np.concatenate(k) for k in keys]
+    order = np.lexsort(tuple(reversed(kcols)))  # first sort column is the primary key
+    flat = [np.concatenate(m) for m in mems]
+    new_off = np.zeros(size.size + 1, np.uint64)
+    new_off[1:] = np.cumsum(size[order])
+    idx = np.concatenate([np.arange(starts[g], starts[g] + size[g]) for g in order]) if order.size else \
+        np.zeros(0, np.int64)
+    return new_off, [f[idx] for f in flat]
+
+
+def _merge(parts, synth_end, total_events=None) -> ColumnarFindings:
+    dd_off, (dd_mem,) = _merge_groups(parts, "dd", [1], [2, 3, 4])
+    rt_off, (rt_tx, rt_rx) = _merge_groups(parts, "rt", [1, 2], [3, 4, 5, 6])
+    pa = _cat(parts, "pairs", 0, np.int64)
+    pdl = _cat(parts, "pairs", 1, np.int64)
+    o = np.argsort(pa, kind="stable")
+    pa, pdl = pa[o], pdl[o]
+    ra_off, (ra_alloc,) = _merge_groups(parts, "ra", [1], [2, 3, 4, 5])
+    ra_pairs = np.searchsorted(pa, ra_alloc)
+    ua = np.sort(np.searchsorted(pa, np.concatenate([p["ua"] for p in parts if "ua" in p]) if any(
+        "ua" in p for p in parts) else np.zeros(0, np.int64)))
+    ut = np.sort(np.concatenate([p["ut"] for p in parts if "ut" in p])) if any("ut" in p for p in parts) else \
+        np.zeros(0, np.int64)
+    warn = np.sort(np.concatenate([p["warn"] for p in parts if "warn" in p])) if any(
+        "warn" in p for p in parts) else np.zeros(0, np.int64)
+    u32 = lambda a: np.asarray(a).astype(np.uint32)  # noqa: E731
+    return ColumnarFindings(
+        n_events=total_events or 0, dd_offsets=dd_off.astype(np.uint64), dd_members=u32(dd_mem),
+        rt_offsets=rt_off.astype(np.uint64), rt_tx=u32(rt_tx), rt_rx=u32(rt_rx), pair_alloc=u32(pa),
+        pair_delete=np.where(pdl < 0, SYN, pdl).astype(np.uint32), synthetic_end_ns=int(synth_end),
+        warn_index=u32(warn), ra_offsets=ra_off.astype(np.uint64), ra_pairs=u32(ra_pairs), ua_pairs=u32(ua),
+        ut_events=u32(ut))
+
+
+def split(cols: Columns, g: int):
+    """Seq-range shards of a trace: [(shard Columns, base index)] for ranks 0..g-1."""
+    out = []
+    bounds = [cols.n * r // g for r in range(g + 1)]
+    for r in range(g):
+        a, b = bounds[r], bounds[r + 1]
+        sl = slice(a, b)
+        out.append((Columns(n=b - a, num_devices_total=cols.num_devices_total, host_device=cols.host_device,
+                            seq=cols.seq[sl], start_ns=cols.start_ns[sl], end_ns=cols.end_ns[sl],
+                            src_addr=cols.src_addr[sl], dst_addr=cols.dst_addr[sl], bytes=cols.bytes[sl],
+                            hash=cols.hash[sl], src_device=cols.src_device[sl], dst_device=cols.dst_device[sl],
+                            kind=cols.kind[sl], loc=cols.loc[sl], loc_flags=cols.loc_flags,
+                            loc_bucket=cols.loc_bucket, n_buckets=cols.n_buckets, bucket_keys=cols.bucket_keys,
+                            wall_time_ns=cols.wall_time_ns, locs=cols.locs), a))
+    return out
+
+
+def run_local(cols: Columns, g: int, strict: bool = False, analyzer: Callable = engine_analyzer):
+    """Simulate G ranks as threads (one process, one device): returns rank 0's merged findings."""
+    comms = LocalComm.group(g)
+    shards = split(cols, g)
+    res, errs = [None] * g, [None] * g
+
+    def work(r):
+        try:
+            res[r] = analyze_sharded(shards[r][0], shards[r][1], comms[r], strict=strict, analyzer=analyzer)
+        except BaseException as exc:  # surfaced below
+            errs[r] = exc
+            comms[r].s.barrier.abort()
+    th = [threading.Thread(target=work, args=(r,)) for r in range(g)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in errs:
+        if e is not None and not isinstance(e, threading.BrokenBarrierError):
+            raise e
+    return res[0]

@@ -1,0 +1,93 @@
+"""Multi-rank (key-range sharded) analysis: G-way results must equal the
+single-shard results exactly.  CPU: ranks as threads and as gloo processes
+(world_size 2) with the oracle as the per-shard analyzer; GPU: ranks as
+threads sharing one B200 with the engine."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import analysis_ref as R
+from paper_2601_12713_b200 import sharded
+from paper_2601_12713_b200.columns import to_columns
+from tests._cases import canon_columnar, canon_oracle
+from tests._gen import nasty_trace
+from tests._oracle_analyzer import oracle_analyzer
+
+
+def _valid_traces(k, seed0=0):
+    out, s = [], seed0
+    while len(out) < k:
+        c = to_columns(nasty_trace(s, max_events=120))
+        s += 1
+        if c.n and not R.validate_cols(c):
+            out.append(c)
+    return out
+
+
+@pytest.mark.parametrize("g", [2, 3, 4])
+def test_local_ranks_with_oracle_match_single(g):
+    for c in _valid_traces(60, seed0=g * 1000):
+        for strict in (False, True):
+            got = sharded.run_local(c, g, strict=strict, analyzer=oracle_analyzer)
+            want = R.analyze_cols(c, strict=strict)
+            assert canon_columnar(got, c) == canon_oracle(want, c)
+            assert got.warn_index.tolist() == want.warnings
+            assert got.synthetic_end_ns == want.synthetic_end
+
+
+def test_local_ranks_report_invalid_shard():
+    c = _valid_traces(1, seed0=77)[0]
+    c.start_ns = c.start_ns.copy()
+    c.start_ns[c.n // 2] = 0 if c.start_ns[c.n // 2 - 1] > 0 else c.start_ns[c.n // 2]
+    if not R.validate_cols(c):
+        pytest.skip("mutation kept the trace valid")
+    with pytest.raises(sharded.EngineInvalid):
+        sharded.run_local(c, 2, analyzer=oracle_analyzer)
+
+
+def _gloo_worker(rank, world, port, result_path):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = sharded.TorchComm()
+        ok = True
+        for c in _valid_traces(25, seed0=500):
+            shard, base = sharded.split(c, world)[rank]
+            got = sharded.analyze_sharded(shard, base, comm, analyzer=oracle_analyzer)
+            if rank == 0:
+                ok &= canon_columnar(got, c) == canon_oracle(R.analyze_cols(c), c)
+        if rank == 0:
+            with open(result_path, "w") as f:
+                f.write("ok" if ok else "mismatch")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world_size_2(tmp_path):
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = tmp_path / "result.txt"
+    mp.spawn(_gloo_worker, args=(2, port, str(out)), nprocs=2, join=True)
+    assert out.read_text() == "ok"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("g", [2, 4])
+def test_local_ranks_engine_on_gpu(cuda, g):
+    from paper_2601_12713_b200 import analyze_columns
+    from paper_2601_12713_b200.synth import c2_trace, c4_trace
+    cases = _valid_traces(40, seed0=9000 + g) + [c2_trace(100_000, seed=3), c4_trace(100_000, seed=5)]
+    for c in cases:
+        for strict in (False, True):
+            got = sharded.run_local(c, g, strict=strict)
+            want = analyze_columns(c, strict=strict)
+            assert canon_columnar(got, c) == canon_columnar(want, c)
+            assert got.warn_index.tolist() == want.warn_index.tolist()
