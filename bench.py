@@ -284,6 +284,8 @@ def run_analysis_ours(args, rank, world, local):
     from paper_2601_12713_b200.synth import c2_trace
 
     dev = torch.device("cuda", local)
+    if world > 1:
+        return run_analysis_sharded(args, rank, world, local)
     cols = c2_trace(args.n_events, seed=SEED + rank)
     dcols = DeviceColumns(cols, dev)
     torch.cuda.synchronize()
@@ -358,6 +360,41 @@ def run_analysis_ours(args, rank, world, local):
         out["cpu_baseline"] = {"value": round(cols.n / cpu_dt / 1e6, 4), "unit": "M events/s", "cores": 1,
                                "kind": "port", "sample": f"the full {cols.n}-event C2 trace through "
                                                          f"oracle/analysis_ref.analyze_cols (1 thread)"}
+    return out
+
+
+def run_analysis_sharded(args, rank, world, local):
+    """N>1: one global C2 trace of world x n_events events, seq-range sharded over the ranks,
+    analysed with the key-range sharded pipeline (one NCCL all-to-all + final gather)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_12713_b200 import sharded
+    from paper_2601_12713_b200.synth import c2_trace
+
+    cols = c2_trace(args.n_events * world, seed=SEED)
+    shard, base = sharded.split(cols, world)[rank]
+    comm = sharded.TorchComm()
+    for _ in range(args.warmup):
+        sharded.analyze_sharded(shard, base, comm)
+    steps = max(1, min(args.steps, 10))
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = sharded.analyze_sharded(shard, base, comm)
+    torch.cuda.synchronize()
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=torch.device("cuda", local))
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    step_s = float(dt.item()) / steps
+    out = {"metric": "M trace events/s analysed", "value": round(cols.n / step_s / 1e6, 3), "unit": "M events/s",
+           "ms_per_step": round(step_s * 1e3, 3), "steps": steps,
+           "config": {"workload": f"C2 trace of {cols.n} events ({args.n_events} per GPU), seq-range shards, "
+                                  f"key-range sharded analysis (hash range / device owner), NCCL all-to-all",
+                      "events_total": cols.n},
+           "timing": "wall clock around analyze_sharded, max over ranks"}
+    if rank == 0 and res is not None:
+        out["counts"] = res.counts()
     return out
 
 

@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <type_traits>
 #include <vector>
 
@@ -316,7 +317,7 @@ struct HostBatch {
     void flush(cudaStream_t s) {
         size_t total = 0;
         for (auto &it : items) total += (it.bytes + 15) & ~size_t(15);
-        uint8_t *st = pinned().reserve(total ? total : 16);
+        uint8_t *st = pinned(s).reserve(total ? total : 16);
         size_t off = 0;
         for (auto &it : items) {
             CK(cudaMemcpyAsync(st + off, it.src, it.bytes, cudaMemcpyDeviceToHost, s));
@@ -1050,6 +1051,13 @@ cudaStream_t engine_stream() {
     }
     return g_stream[dev & 63];
 }
+cudaStream_t g_stream2[64] = {nullptr};
+cudaStream_t engine_stream2() {  // second stream: the device-keyed steps run beside DD/RT
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (!g_stream2[dev & 63]) CK(cudaStreamCreateWithFlags(&g_stream2[dev & 63], cudaStreamNonBlocking));
+    return g_stream2[dev & 63];
+}
 
 int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_override, b2l_findings **outp) {
     b2l_findings *f = (b2l_findings *)calloc(1, sizeof(b2l_findings));
@@ -1126,21 +1134,51 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
 
     pc.mark("partition");
     in->synth_end = me;
-    // ---- 3. duplicates + round trips
-    DdRt dr = dd_rt_step(c, H.p, nH, (flags & B2L_ANALYZE_STRICT_RT) != 0, *in, s);
-    in->dd_groups = dr.dd_groups, in->dd_members = dr.dd_members, in->rt_groups = dr.rt_groups,
-    in->rt_trips = dr.rt_trips;
-    pc.mark("dd_rt");
-    // ---- 4. pairs
-    PairOut po = pairs_step(c, AD.p, nAD, A.p, nA, me, *in, s);
     in->n_pairs = nA;
-    pc.mark("pairs");
-    // ---- 5. repeated allocations
-    ra_step(c, nA, *in, s);
-    pc.mark("ra");
-    // ---- 6. unused allocations / transfers
-    ua_ut_step(c, TK.p, nK, TT.p, nT, *in, s);
-    pc.mark("ua_ut");
+    // ---- 3-6.  Hash-keyed (DD, RT) and device-keyed (pairs, RA, UA, UT) work are independent:
+    // run them on two streams from two host threads (each keeps its own syncs and staging).
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaStream_t s2 = engine_stream2();
+    const Masks masks = g_masks;
+    PairOut po;
+    EngineErr err2{0, ""};
+    bool failed2 = false;
+    // Overlap pays while the steps are latency/launch bound (small traces); large traces are
+    // bandwidth bound and run the two halves back to back on one stream.
+    const bool overlap = n <= (size_t(4) << 20);
+    if (!overlap) s2 = s;
+    auto device_keyed = [&] {
+        try {
+            CK(cudaSetDevice(dev));
+            g_masks = masks;
+            PhaseClock pc2(s2);
+            po = pairs_step(c, AD.p, nAD, A.p, nA, me, *in, s2);
+            pc2.mark("pairs");
+            ra_step(c, nA, *in, s2);
+            pc2.mark("ra");
+            ua_ut_step(c, TK.p, nK, TT.p, nT, *in, s2);
+            pc2.mark("ua_ut");
+            CK(cudaStreamSynchronize(s2));
+        } catch (const EngineErr &e) {
+            err2 = e;
+            failed2 = true;
+        }
+    };
+    std::thread side;
+    if (overlap) side = std::thread(device_keyed);
+    else device_keyed();
+    try {
+        DdRt dr = dd_rt_step(c, H.p, nH, (flags & B2L_ANALYZE_STRICT_RT) != 0, *in, s);
+        in->dd_groups = dr.dd_groups, in->dd_members = dr.dd_members, in->rt_groups = dr.rt_groups,
+        in->rt_trips = dr.rt_trips;
+    } catch (...) {
+        if (side.joinable()) side.join();
+        throw;
+    }
+    if (side.joinable()) side.join();
+    if (failed2) throw err2;
+    pc.mark("detectors");
 
     // ---- results to the host (one pinned staging pass)
     HostBatch hb;

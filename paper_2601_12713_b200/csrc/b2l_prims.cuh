@@ -13,6 +13,8 @@
 #include <stdint.h>
 
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -244,13 +246,17 @@ struct Pinned {
         return p;
     }
 };
-inline Pinned &pinned() {
-    static thread_local Pinned pn;
-    return pn;
+// One staging buffer per stream (a stream is driven by one host thread at a time), kept for the
+// life of the process -- never allocated per call.
+inline Pinned &pinned(cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<cudaStream_t, Pinned> by_stream;
+    std::lock_guard<std::mutex> lock(mu);
+    return by_stream[s];
 }
 // Read `bytes` from device memory into host `dst` (synchronous).
 inline void read_back(void *dst, const void *d_src, size_t bytes, cudaStream_t s) {
-    uint8_t *st = pinned().reserve(bytes);
+    uint8_t *st = pinned(s).reserve(bytes);
     CK(cudaMemcpyAsync(st, d_src, bytes, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     memcpy(dst, st, bytes);
