@@ -68,6 +68,11 @@ int b2l_hash_batch(const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n,
 int b2l_hash_host(const void *const *h_bufs, const uint64_t *h_lens, uint64_t n,
                   uint64_t *h_digests);
 
+/* One DEVICE buffer hashed by the whole GPU (K2: exact 4-bit-group decomposition of the
+ * serial fold, cooperative launch).  For buffers whose serial chain would dominate a batch
+ * (b2l_hash_host routes buffers >= 32 MiB here automatically).  Asynchronous. */
+int b2l_hash_large(const void *d_buf, uint64_t len, uint64_t *d_digest, void *stream);
+
 /* One host payload (the HashFn drop-in). */
 int b2l_hash_bytes(const void *h_buf, uint64_t len, uint64_t *digest);
 

@@ -1309,24 +1309,42 @@ __global__ void k_attr(DevCols c, size_t n_elem, Elem el, AttrAcc g) {
             scnt[b] = 0, sns[2 * b] = sns[2 * b + 1] = 0, sby[2 * b] = sby[2 * b + 1] = 0, sfirst[b] = ~0ull;
         __syncthreads();
     }
-    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < n_elem; q += (size_t)gridDim.x * blockDim.x) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    // warp-uniform trip count so every lane reaches the warp collectives below
+    for (size_t base = (size_t)blockIdx.x * blockDim.x; base < n_elem; base += stride) {
+        const size_t q = base + threadIdx.x;
         uint32_t ev[2];
         uint64_t pos[2];
-        const int k = el(q, ev, pos);
-        for (int j = 0; j < k; ++j) {
-            const uint32_t e = ev[j];
-            const uint32_t b = c.loc_bucket[c.loc[e]];
-            const unsigned long long d = c.end[e] - c.start[e], by = c.nb[e];
-            const unsigned long long fp = (pos[j] << 32) | e;
+        const int k = q < n_elem ? el(q, ev, pos) : 0;
+        for (int j = 0; j < 2; ++j) {
+            const bool have = j < k;
+            const uint32_t e = have ? ev[j] : 0;
+            const uint32_t b = have ? c.loc_bucket[c.loc[e]] : 0xFFFFFFFFu;
+            unsigned long long d = have ? c.end[e] - c.start[e] : 0, by = have ? c.nb[e] : 0;
+            unsigned long long fp = have ? ((pos[j] << 32) | e) : ~0ull, cnt = have ? 1 : 0;
+            const uint32_t peers = __match_any_sync(0xffffffffu, b);
+            U128 sd{d, 0}, sb{by, 0};
+            if (peers == 0xffffffffu) {
+                // the whole warp hit one bucket (the common case: few code locations): reduce first
+                sd = warp_sum128(sd);
+                sb = warp_sum128(sb);
+                for (int o = 16; o; o >>= 1) {
+                    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+                    const unsigned long long x = __shfl_xor_sync(0xffffffffu, fp, o);
+                    fp = x < fp ? x : fp;
+                }
+                if ((threadIdx.x & 31) != 0) continue;
+            }
+            if (b == 0xFFFFFFFFu) continue;
             if (local) {
-                atomicAdd(scnt + b, 1ull);
-                atomic_add128(sns + 2 * b, U128{d, 0});
-                atomic_add128(sby + 2 * b, U128{by, 0});
+                atomicAdd(scnt + b, cnt);
+                atomic_add128(sns + 2 * b, sd);
+                atomic_add128(sby + 2 * b, sb);
                 atomicMin(sfirst + b, fp);
             } else {
-                atomicAdd(g.cnt + b, 1ull);
-                atomic_add128(g.ns + 2 * b, U128{d, 0});
-                atomic_add128(g.by + 2 * b, U128{by, 0});
+                atomicAdd(g.cnt + b, cnt);
+                atomic_add128(g.ns + 2 * b, sd);
+                atomic_add128(g.by + 2 * b, sb);
                 atomicMin(g.first + b, fp);
             }
         }

@@ -39,6 +39,8 @@ int sm_count() {
 int hash_batch_launch(const uint64_t *, const uint64_t *, uint64_t, uint64_t *, const uint32_t *, cudaStream_t);
 int hash_launch_info(uint64_t, int *, int *, int *);
 int hash_select_variant(int, int *);
+int hash_planes_launch(const void *, uint64_t, uint64_t *, cudaStream_t);
+constexpr uint64_t K2_MIN_BYTES = 32ull << 20;  // serial chain >= ~20 ms: the whole-GPU fold wins
 int fill_payloads_launch(uint8_t *, const uint64_t *, const uint64_t *, const uint64_t *, uint64_t, uint64_t,
                          cudaStream_t);
 
@@ -139,7 +141,12 @@ int hash_host_impl(const void *const *h_bufs, const uint64_t *h_lens, uint64_t n
         uint64_t i1 = i0, bytes = 0;
         while (i1 < n) {
             uint64_t sb = span_bytes((uint64_t)h_bufs[i1], h_lens[i1]);
-            if (i1 > i0 && bytes + sb > RING_SLOT_BYTES) break;
+            if (i1 > i0 && (bytes + sb > RING_SLOT_BYTES || h_lens[i1] >= K2_MIN_BYTES)) break;
+            if (h_lens[i1] >= K2_MIN_BYTES) {  // huge buffers are hashed alone by K2
+                bytes += sb;
+                ++i1;
+                break;
+            }
             bytes += sb;
             ++i1;
         }
@@ -181,7 +188,10 @@ int hash_host_impl(const void *const *h_bufs, const uint64_t *h_lens, uint64_t n
         B2L_CUDA(cudaMemcpyAsync(S.d_meta, S.h_meta, 2 * nb * sizeof(uint64_t), cudaMemcpyHostToDevice, P.copy));
         B2L_CUDA(cudaEventRecord(S.copied, P.copy));
         B2L_CUDA(cudaStreamWaitEvent(P.comp, S.copied, 0));
-        rc = hash_batch_launch(S.d_meta, S.d_meta + nb, nb, P.d_digests + i0, d_order, P.comp);
+        if (nb == 1 && h_lens[i0] >= K2_MIN_BYTES)  // one huge buffer: exact whole-GPU fold (K2)
+            rc = hash_planes_launch((const void *)mp[0], h_lens[i0], P.d_digests + i0, P.comp);
+        else
+            rc = hash_batch_launch(S.d_meta, S.d_meta + nb, nb, P.d_digests + i0, d_order, P.comp);
         if (rc) return rc;
         B2L_CUDA(cudaEventRecord(S.hashed, P.comp));
         S.used = true;
@@ -220,6 +230,12 @@ int b2l_hash_batch(const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n, u
 
 int b2l_hash_host(const void *const *h_bufs, const uint64_t *h_lens, uint64_t n, uint64_t *h_digests) {
     return b2l::hash_host_impl(h_bufs, h_lens, n, h_digests);
+}
+
+int b2l_hash_large(const void *d_buf, uint64_t len, uint64_t *d_digest, void *stream) {
+    if (!d_buf || !d_digest) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
+    if (len == 0) return b2l::fail(B2L_E_EMPTY_PAYLOAD, "cannot hash a zero-byte payload");
+    return b2l::hash_planes_launch(d_buf, len, d_digest, (cudaStream_t)stream);
 }
 
 int b2l_hash_bytes(const void *h_buf, uint64_t len, uint64_t *digest) {

@@ -1,0 +1,262 @@
+// K2 hash_planes: the reference's serial FNV fold of ONE huge buffer, parallelised exactly
+// across the whole GPU (in 4-bit groups instead of single bit planes).
+//
+// f_w(h) = (h ^ w) * P is a T-function: bits [k, k+4) of the output depend only on bits < k+4
+// of the inputs.  Processing the 64-bit state in 16 groups of 4 bits, once bits < k of every
+// intermediate state are known (kept as R_i = (x_i mod 2^k) * P per word, x_i = h_i ^ w_i),
+// the 4-bit group of the chain obeys
+//     h4_{i+1} = ((R_i >> k) + 3 * (h4_i ^ w4_i)) mod 16        (P = 2^40 + 435 = 3 mod 16)
+// so every run of words is a map {0..15} -> {0..15}: a 16-nibble table, built for all 16
+// inputs at once with SWAR nibble arithmetic in one u64.  Tables compose associatively, so a
+// group resolves by a prefix composition across threads (warp shuffles), warps and CTAs
+// (decoupled look-back); a second pass with the actual input state advances R_i by
+// (x4_i << k) * P.  The buffer is read from HBM once: each CTA keeps its 32 KiB chunk in
+// registers for all 16 groups; chunks beyond the co-resident grid are processed in rounds
+// chained through a per-group carry.  Verified bit-exact against the serial fold (tests).
+#include <cooperative_groups.h>
+
+#include "b2l_common.cuh"
+
+namespace b2l {
+namespace k2 {
+
+constexpr int THREADS = 256;
+constexpr int WPT = 16;                   // words per thread
+constexpr int CHUNK = THREADS * WPT;      // words per CTA per round
+constexpr unsigned long long ID = 0xFEDCBA9876543210ull;
+constexpr unsigned long long ONES = 0x1111111111111111ull;
+
+struct Status {
+    unsigned long long flag;   // 0 empty, 1 aggregate, 2 inclusive prefix
+    unsigned long long table;
+};
+
+__device__ __forceinline__ unsigned long long nadd(unsigned long long a, unsigned long long b) {
+    return ((a & 0x7777777777777777ull) + (b & 0x7777777777777777ull)) ^ ((a ^ b) & 0x8888888888888888ull);
+}
+// one word through all 16 candidate states
+__device__ __forceinline__ unsigned long long step_table(unsigned long long T, uint32_t w4, uint32_t r4) {
+    const unsigned long long X = T ^ (ONES * w4);
+    return nadd(nadd(nadd(X, X), X), ONES * r4);
+}
+// (first A, then B): out[j] = B[A[j]]
+__device__ __forceinline__ unsigned long long compose(unsigned long long A, unsigned long long B) {
+    unsigned long long out = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const uint32_t a = (uint32_t)(A >> (4 * j)) & 15u;
+        out |= ((B >> (4 * a)) & 15ull) << (4 * j);
+    }
+    return out;
+}
+__device__ __forceinline__ uint32_t apply(unsigned long long T, uint32_t s) { return (uint32_t)(T >> (4 * s)) & 15u; }
+
+__device__ __forceinline__ uint64_t load_word(const uint8_t *buf, uint64_t n, uint64_t i) {
+    const uint64_t start = (uint64_t)buf, a = start + 8 * i;
+    const uint64_t end = start + n;  // exclusive
+    uint64_t w;
+    const uint32_t r = (uint32_t)(a & 7);
+    const uint64_t lo = a - r;
+    if (r == 0) {
+        w = __ldg(reinterpret_cast<const unsigned long long *>(lo));
+    } else {
+        const uint64_t u0 = __ldg(reinterpret_cast<const unsigned long long *>(lo));
+        const uint64_t u1 = (lo + 8 < end) ? __ldg(reinterpret_cast<const unsigned long long *>(lo + 8)) : 0ull;
+        w = (u0 >> (8 * r)) | (u1 << (64 - 8 * r));
+    }
+    if (a + 8 > end) {  // zero-extended tail word
+        const uint32_t valid = (uint32_t)(end - a);
+        w &= (1ull << (8 * valid)) - 1;
+    }
+    return w;
+}
+
+__global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__restrict__ buf, uint64_t nbytes,
+                                                            Status *status, unsigned long long *carry,
+                                                            uint64_t *digest) {
+    __shared__ uint64_t stage[THREADS * (WPT + 1)];
+    __shared__ unsigned long long warp_tab[THREADS / 32];
+    __shared__ uint32_t warp_in[THREADS / 32];
+    __shared__ uint32_t cta_in;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t G = gridDim.x, c = blockIdx.x;
+    const uint64_t nw = (nbytes + 7) >> 3;
+    const uint64_t nchunks = (nw + CHUNK - 1) / CHUNK;
+    const uint64_t rounds = (nchunks + G - 1) / G;
+    volatile Status *vst = status;
+    volatile unsigned long long *vcarry = carry;
+
+    for (uint64_t r = 0; r < rounds; ++r) {
+        const uint64_t q = r * G + c;
+        const bool active = q < nchunks;
+        const uint64_t last_in_round = (nchunks - r * G < G ? nchunks - r * G : G) - 1;
+        uint64_t w[WPT], R[WPT];
+        int nv = 0;
+        if (active) {
+            // coalesced load into padded smem, then each thread takes its 16 consecutive words
+            const uint64_t base = q * CHUNK;
+            for (int idx = t; idx < CHUNK; idx += THREADS) {
+                const uint64_t i = base + idx;
+                stage[(idx / WPT) * (WPT + 1) + idx % WPT] = i < nw ? load_word(buf, nbytes, i) : 0ull;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < WPT; ++j) w[j] = stage[t * (WPT + 1) + j], R[j] = 0;
+            const int64_t left = (int64_t)nw - (int64_t)(base + (uint64_t)t * WPT);
+            nv = left <= 0 ? 0 : (left >= WPT ? WPT : (int)left);
+            __syncthreads();
+        }
+        for (int g = 0; g < 16; ++g) {
+            const int k = 4 * g;
+            const uint64_t slot = r * 16 + g;
+            if (active) {
+                // ---- pass A: this thread's map
+                unsigned long long T = ID;
+#pragma unroll
+                for (int j = 0; j < WPT; ++j)
+                    if (j < nv) T = step_table(T, (uint32_t)(w[j] >> k) & 15u, (uint32_t)(R[j] >> k) & 15u);
+                // ---- inclusive prefix composition across the warp (lane order)
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const unsigned long long o = __shfl_up_sync(0xffffffffu, T, d);
+                    if (lane >= d) T = compose(o, T);
+                }
+                const unsigned long long excl_lane = __shfl_up_sync(0xffffffffu, T, 1);
+                if (lane == 31) warp_tab[warp] = T;
+                __syncthreads();
+                if (t == 0) {
+                    unsigned long long agg = ID;
+                    for (int i = 0; i < THREADS / 32; ++i) agg = compose(agg, warp_tab[i]);
+                    // publish the CTA aggregate, look back for the round prefix, publish inclusive
+                    Status *me = status + slot * G + c;
+                    unsigned long long prefix = ID;
+                    if (c > 0) {
+                        me->table = agg;
+                        __threadfence();
+                        atomicExch(&me->flag, 1ull);
+                        for (int64_t j = (int64_t)c - 1; j >= 0; --j) {
+                            unsigned long long f;
+                            do {
+                                f = vst[slot * G + j].flag;
+                            } while (f == 0);
+                            __threadfence();
+                            prefix = compose(vst[slot * G + j].table, prefix);
+                            if (f == 2) break;
+                        }
+                    }
+                    me->table = compose(prefix, agg);
+                    __threadfence();
+                    atomicExch(&me->flag, 2ull);
+                    // the group's state entering this round
+                    uint32_t s_round;
+                    if (r == 0) {
+                        s_round = (uint32_t)(FNV_OFFSET >> k) & 15u;
+                    } else {
+                        unsigned long long v;
+                        do {
+                            v = vcarry[slot - 16];
+                        } while (v == 0);
+                        s_round = (uint32_t)v & 15u;
+                    }
+                    uint32_t s = apply(prefix, s_round);
+                    cta_in = s;
+                    for (int i = 0; i < THREADS / 32; ++i) {
+                        warp_in[i] = s;
+                        s = apply(warp_tab[i], s);
+                    }
+                    if (q == r * G + last_in_round) {  // last chunk of the round: carry its output state
+                        __threadfence();
+                        atomicExch(&carry[slot], 0x100ull | s);
+                    }
+                }
+                __syncthreads();
+                // ---- pass B with the actual input state
+                uint32_t s = lane == 0 ? warp_in[warp] : apply(excl_lane, warp_in[warp]);
+#pragma unroll
+                for (int j = 0; j < WPT; ++j) {
+                    if (j < nv) {
+                        const uint32_t x4 = s ^ ((uint32_t)(w[j] >> k) & 15u);
+                        s = (((uint32_t)(R[j] >> k) & 15u) + 3u * x4) & 15u;
+                        R[j] += ((uint64_t)x4 << k) * FNV_PRIME;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    // the final state is the carry of the last round; CTA 0 finishes the digest
+    if (c == 0 && threadIdx.x == 0) {
+        uint64_t h = 0;
+        const uint64_t last = rounds - 1;
+        for (int g = 0; g < 16; ++g) {
+            unsigned long long v;
+            do {
+                v = vcarry[last * 16 + g];
+            } while (v == 0);
+            h |= (uint64_t)(v & 15ull) << (4 * g);
+        }
+        *digest = finish_digest(h, nbytes);
+    }
+}
+
+struct Ctx {
+    int grid = 0;
+    Status *status = nullptr;
+    unsigned long long *carry = nullptr;
+    size_t status_cap = 0, carry_cap = 0;
+};
+Ctx g_ctx[64];
+
+}  // namespace k2
+
+int k2_grid() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    k2::Ctx &C = k2::g_ctx[dev & 63];
+    if (!C.grid) {
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k2::k_hash_planes, k2::THREADS, 0) != cudaSuccess ||
+            nb < 1)
+            return -1;
+        C.grid = nb * sm_count();
+    }
+    return C.grid;
+}
+
+// Digest of one device buffer with the whole GPU (cooperative launch: every CTA co-resident).
+int hash_planes_launch(const void *d_buf, uint64_t nbytes, uint64_t *d_digest, cudaStream_t stream) {
+    if (nbytes == 0) return B2L_OK;
+    int dev = 0;
+    B2L_CUDA(cudaGetDevice(&dev));
+    k2::Ctx &C = k2::g_ctx[dev & 63];
+    const int grid = k2_grid();
+    if (grid < 1) return fail(B2L_E_CUDA, "k_hash_planes: no occupancy");
+    const uint64_t nw = (nbytes + 7) >> 3;
+    const uint64_t nchunks = (nw + k2::CHUNK - 1) / k2::CHUNK;
+    const uint64_t g = nchunks < (uint64_t)grid ? nchunks : (uint64_t)grid;
+    const uint64_t rounds = (nchunks + g - 1) / g;
+    const size_t need_st = rounds * 16 * g, need_c = rounds * 16;
+    if (C.status_cap < need_st) {
+        if (C.status) cudaFree(C.status);
+        C.status = nullptr;
+        C.status_cap = 0;
+        B2L_CUDA(cudaMalloc(&C.status, need_st * sizeof(k2::Status)));
+        C.status_cap = need_st;
+    }
+    if (C.carry_cap < need_c) {
+        if (C.carry) cudaFree(C.carry);
+        C.carry = nullptr;
+        C.carry_cap = 0;
+        B2L_CUDA(cudaMalloc(&C.carry, need_c * sizeof(unsigned long long)));
+        C.carry_cap = need_c;
+    }
+    B2L_CUDA(cudaMemsetAsync(C.status, 0, need_st * sizeof(k2::Status), stream));
+    B2L_CUDA(cudaMemsetAsync(C.carry, 0, need_c * sizeof(unsigned long long), stream));
+    const uint8_t *b = (const uint8_t *)d_buf;
+    void *args[] = {(void *)&b, (void *)&nbytes, (void *)&C.status, (void *)&C.carry, (void *)&d_digest};
+    B2L_CUDA(cudaLaunchCooperativeKernel((const void *)k2::k_hash_planes, dim3((unsigned)g), dim3(k2::THREADS), args, 0,
+                                         stream));
+    return B2L_OK;
+}
+
+}  // namespace b2l

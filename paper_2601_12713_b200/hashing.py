@@ -109,6 +109,21 @@ def hash_device(ptrs, lens, out, order=None, stream=None) -> None:
     _lib.check(rc, "b2l_hash_batch")
 
 
+K2_MIN_BYTES = 32 << 20  # buffers whose serial chain would dominate: hashed by the whole GPU (K2)
+
+
+def hash_large(ptr: int, nbytes: int, out_ptr: int, stream=None) -> None:
+    """One device buffer (address, length) with the whole GPU -- b2l_hash_large (K2).
+    Writes the u64 digest to device address ``out_ptr``.  Asynchronous."""
+    import torch
+    if nbytes == 0:
+        raise EmptyPayload()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    _lib.check(_lib.lib().b2l_hash_large(ptr, nbytes, out_ptr, sp), "b2l_hash_large")
+
+
 def hash_tensors(tensors: Sequence, stream=None):
     """Digests of device-resident tensors' bytes, as an int64 CUDA tensor
     holding the u64 bit patterns (``to_u64_list`` converts).  Ragged batches
@@ -124,13 +139,22 @@ def hash_tensors(tensors: Sequence, stream=None):
     for t in tensors:
         if not t.is_contiguous() or t.device != dev:
             raise ValueError("hash_tensors needs contiguous tensors on one CUDA device")
+    out = torch.empty(len(tensors), dtype=torch.int64, device=dev)
+    big = [i for i, n in enumerate(lens_h) if n >= K2_MIN_BYTES]
+    for i in big:  # each huge buffer with the whole GPU, then the rest as one batch
+        hash_large(tensors[i].data_ptr(), lens_h[i], out.data_ptr() + 8 * i, stream)
+    if big:
+        small = [i for i in range(len(tensors)) if lens_h[i] < K2_MIN_BYTES]
+        if small:
+            sub = hash_tensors([tensors[i] for i in small], stream=stream)
+            out[torch.tensor(small, device=dev)] = sub
+        return out
     meta = torch.tensor([[t.data_ptr() for t in tensors], lens_h], dtype=torch.int64)
     order = None
     if len(set(lens_h)) > 1:
         order = torch.from_numpy(np.argsort(-np.asarray(lens_h, dtype=np.int64), kind="stable")
                                  .astype(np.int32)).to(dev, non_blocking=True)
     meta_d = meta.to(dev, non_blocking=True)
-    out = torch.empty(len(tensors), dtype=torch.int64, device=dev)
     hash_device(meta_d[0], meta_d[1], out, order=order, stream=stream)
     return out
 

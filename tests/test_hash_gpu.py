@@ -201,3 +201,49 @@ def test_buffer_larger_than_4GiB(cuda):
     want = hash_ref.fold64_c_batch(np.array([host.ctypes.data], dtype=np.uint64),
                                    np.array([size], dtype=np.uint64))
     assert to_u64_list(out)[0] == int(want[0])
+
+
+# ----------------------------------------------------------------------------- K2 (whole-GPU fold)
+def _k2_digest(cuda, slab, off, n):
+    import torch
+    from paper_2601_12713_b200.hashing import hash_large, to_u64_list
+    out = torch.zeros(1, dtype=torch.int64, device=cuda)
+    hash_large(slab.data_ptr() + off, n, out.data_ptr())
+    torch.cuda.synchronize()
+    return to_u64_list(out)[0]
+
+
+def test_k2_small_lengths_and_offsets(cuda):
+    import torch
+    rng = np.random.default_rng(31)
+    host = np.frombuffer(hash_ref.payload(1 << 20, 5, 1), dtype=np.uint8)
+    slab = torch.from_numpy(host.copy()).to(cuda)
+    cases = [(o, n) for o in range(16) for n in (1, 2, 7, 8, 9, 15, 16, 17, 63, 64, 65, 255)]
+    cases += [(int(rng.integers(0, 64)), int(rng.integers(1, 200_000))) for _ in range(40)]
+    cases += [(3, 32768 * 8 - 5), (0, 32768 * 8), (8, 32768 * 8 + 8), (5, (1 << 20) - 64)]
+    for off, n in cases:
+        assert _k2_digest(cuda, slab, off, n) == hash_ref.fold64_c(host[off:off + n].tobytes()), (off, n)
+
+
+def test_k2_multi_round_buffer_and_routing(cuda):
+    """256 MiB + 3 bytes (C3-sized, many rounds of the co-resident grid), misaligned."""
+    import torch
+    from paper_2601_12713_b200 import _lib, hash_tensors
+    from paper_2601_12713_b200.hashing import to_u64_list
+    size = (256 << 20) + 3
+    slab = torch.empty(size + 16, dtype=torch.uint8, device=cuda)
+    z = torch.zeros(1, dtype=torch.int64, device=cuda)
+    ln = torch.tensor([size + 16], dtype=torch.int64, device=cuda)
+    cid = torch.tensor([4242], dtype=torch.int64, device=cuda)
+    _lib.check(_lib.lib().b2l_fill_payloads(slab.data_ptr(), z.data_ptr(), ln.data_ptr(), cid.data_ptr(), 1, 3,
+                                            torch.cuda.current_stream().cuda_stream))
+    host = slab.cpu().numpy()
+    for off in (0, 5):
+        want = hash_ref.fold64_c_batch(np.array([host.ctypes.data + off], dtype=np.uint64),
+                                       np.array([size], dtype=np.uint64))[0]
+        assert _k2_digest(cuda, slab, off, size) == int(want), off
+    # hash_tensors routes >= 32 MiB buffers to K2 and the rest to the batch kernel
+    ts = [slab[:size], slab[1:1001], slab[:40 << 20]]
+    got = to_u64_list(hash_tensors(ts))
+    want = [hash_ref.fold64_c(t.cpu().numpy().tobytes()) for t in ts]
+    assert got == want
