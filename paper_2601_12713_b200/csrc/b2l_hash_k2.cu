@@ -27,8 +27,9 @@ constexpr unsigned long long ID = 0xFEDCBA9876543210ull;
 constexpr unsigned long long ONES = 0x1111111111111111ull;
 
 struct Status {
-    unsigned long long flag;   // 0 empty, 1 aggregate, 2 inclusive prefix
-    unsigned long long table;
+    unsigned long long flag;   // 0 empty, 1 aggregate published, 2 inclusive prefix published
+    unsigned long long agg;    // this CTA's map (never changes once flag >= 1)
+    unsigned long long incl;   // maps of CTAs 0..c of the round (valid once flag == 2)
 };
 
 __device__ __forceinline__ unsigned long long nadd(unsigned long long a, unsigned long long b) {
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__res
                     Status *me = status + slot * G + c;
                     unsigned long long prefix = ID;
                     if (c > 0) {
-                        me->table = agg;
+                        me->agg = agg;
                         __threadfence();
                         atomicExch(&me->flag, 1ull);
                         for (int64_t j = (int64_t)c - 1; j >= 0; --j) {
@@ -140,11 +141,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__res
                                 f = vst[slot * G + j].flag;
                             } while (f == 0);
                             __threadfence();
-                            prefix = compose(vst[slot * G + j].table, prefix);
-                            if (f == 2) break;
+                            if (f == 2) {
+                                prefix = compose(vst[slot * G + j].incl, prefix);
+                                break;
+                            }
+                            prefix = compose(vst[slot * G + j].agg, prefix);
                         }
                     }
-                    me->table = compose(prefix, agg);
+                    me->incl = compose(prefix, agg);
                     __threadfence();
                     atomicExch(&me->flag, 2ull);
                     // the group's state entering this round
