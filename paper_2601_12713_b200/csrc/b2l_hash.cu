@@ -309,11 +309,15 @@ const HashCfg *cfg_table(int &count) {
         make_coop<4, 128, 3>(),  make_coop<4, 256, 2>(), make_coop<4, 128, 4>(), make_coop<2, 256, 3>(),
         make_coop<8, 128, 3>(),  make_coop<4, 256, 3>(), make_coop<2, 512, 2>(), make_coop<1, 128, 3>(),
         make_tma<128, 384, 3>(), make_tma<128, 256, 4>(), make_tma<96, 512, 3>(),
+        // deep rings for few, long chains (latency-bound batches): 5-7 chunks in flight per lane
+        make_coop<1, 512, 6>(),  make_coop<1, 512, 8>(),  make_coop<1, 256, 8>(),
     };
     count = (int)(sizeof(tab) / sizeof(tab[0]));
     return tab;
 }
 constexpr int DEFAULT_CFG = 6;  // coop<2 warps, 512 B, 2 stages>: 96.5% of measured HBM on C2 (r01 sweep)
+constexpr int LATENCY_CFG = 11;   // coop<1 warp, 512 B, 6 stages>: batches too small to fill the GPU
+constexpr uint64_t LATENCY_MAX_BUFS = 148ull * 2 * 32;  // one lane per buffer fits the deep variant
 
 struct HashLaunch {
     int cfg = -1;
@@ -400,6 +404,24 @@ int hash_batch_launch(const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n
     int per_sm = 0;
     const HashCfg *c = active_cfg(per_sm);
     if (!c) return fail(B2L_E_CUDA, "b2l_hash_batch: cannot configure hash kernel");
+    if (setenv_variant < 0 && !getenv("B2L_HASH_CFG") && n <= LATENCY_MAX_BUFS) {
+        // few buffers: every chain runs alone, so what matters is bytes in flight per lane
+        int count;
+        const HashCfg *tab = cfg_table(count);
+        static int lat_per_sm[64] = {0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!lat_per_sm[dev & 63]) {
+            int nb = 0;
+            B2L_CUDA(cudaFuncSetAttribute(tab[LATENCY_CFG].fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)tab[LATENCY_CFG].smem));
+            B2L_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tab[LATENCY_CFG].fn, tab[LATENCY_CFG].nt,
+                                                                   tab[LATENCY_CFG].smem));
+            lat_per_sm[dev & 63] = nb > 0 ? nb : 1;
+        }
+        c = &tab[LATENCY_CFG];
+        per_sm = lat_per_sm[dev & 63];
+    }
     int grid = hash_grid(*c, per_sm, n);
     void *args[] = {(void *)&d_ptrs, (void *)&d_lens, (void *)&d_order, (void *)&n, (void *)&d_digests};
     B2L_CUDA(cudaLaunchKernel(c->fn, dim3(grid), dim3(c->nt), args, c->smem, stream));

@@ -21,36 +21,55 @@ namespace b2l {
 namespace k2 {
 
 constexpr int THREADS = 256;
-constexpr int WPT = 16;                   // words per thread
+constexpr int WPT = 32;                   // words per thread (kept in registers for all 16 groups)
 constexpr int CHUNK = THREADS * WPT;      // words per CTA per round
-constexpr unsigned long long ID = 0xFEDCBA9876543210ull;
-constexpr unsigned long long ONES = 0x1111111111111111ull;
+constexpr size_t SMEM = (size_t)THREADS * (WPT + 1) * sizeof(uint64_t);
 
 struct Status {
-    unsigned long long flag;   // 0 empty, 1 aggregate published, 2 inclusive prefix published
-    unsigned long long agg;    // this CTA's map (never changes once flag >= 1)
-    unsigned long long incl;   // maps of CTAs 0..c of the round (valid once flag == 2)
+    unsigned long long flag;  // 0 empty, 1 aggregate published, 2 inclusive prefix published
+    uint4 agg;                // this CTA's map (never changes once flag >= 1)
+    uint4 incl;               // maps of CTAs 0..c of the round (valid once flag == 2)
 };
 
-__device__ __forceinline__ unsigned long long nadd(unsigned long long a, unsigned long long b) {
-    return ((a & 0x7777777777777777ull) + (b & 0x7777777777777777ull)) ^ ((a ^ b) & 0x8888888888888888ull);
-}
-// one word through all 16 candidate states
-__device__ __forceinline__ unsigned long long step_table(unsigned long long T, uint32_t w4, uint32_t r4) {
-    const unsigned long long X = T ^ (ONES * w4);
-    return nadd(nadd(nadd(X, X), X), ONES * r4);
+// A map {0..15} -> {0..15} as 16 bytes (entry j = byte j): byte-parallel arithmetic never
+// carries across bytes here, and composition is a byte gather done with PRMT.
+struct Tab {
+    uint32_t r[4];
+};
+__device__ __forceinline__ Tab tab_id() { return Tab{{0x03020100u, 0x07060504u, 0x0B0A0908u, 0x0F0E0D0Cu}}; }
+// one word through all 16 candidate states: t -> ((R>>k)&15) + 3 * (t ^ w4)  (mod 16)
+__device__ __forceinline__ void tab_step(Tab &T, uint32_t w4, uint32_t r4) {
+    const uint32_t wb = w4 * 0x01010101u, rb = r4 * 0x01010101u;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) T.r[m] = ((T.r[m] ^ wb) * 3u + rb) & 0x0F0F0F0Fu;
 }
 // (first A, then B): out[j] = B[A[j]]
-__device__ __forceinline__ unsigned long long compose(unsigned long long A, unsigned long long B) {
-    unsigned long long out = 0;
+__device__ __forceinline__ Tab tab_compose(const Tab &A, const Tab &B) {
+    Tab o;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        const uint32_t a = (uint32_t)(A >> (4 * j)) & 15u;
-        out |= ((B >> (4 * a)) & 15ull) << (4 * j);
+    for (int m = 0; m < 4; ++m) {
+        const uint32_t a = A.r[m];
+        const uint32_t x = a & 0x07070707u;
+        const uint32_t sx = x | (x >> 4);
+        const uint32_t sel = (sx & 0xFFu) | ((sx >> 8) & 0xFF00u);
+        const uint32_t lo = __byte_perm(B.r[0], B.r[1], sel), hi = __byte_perm(B.r[2], B.r[3], sel);
+        const uint32_t mask = ((a >> 3) & 0x01010101u) * 0xFFu;
+        o.r[m] = (lo & ~mask) | (hi & mask);
     }
-    return out;
+    return o;
 }
-__device__ __forceinline__ uint32_t apply(unsigned long long T, uint32_t s) { return (uint32_t)(T >> (4 * s)) & 15u; }
+__device__ __forceinline__ uint32_t tab_apply(const Tab &T, uint32_t s) {
+    const uint32_t v = (s & 8) ? ((s & 4) ? T.r[3] : T.r[2]) : ((s & 4) ? T.r[1] : T.r[0]);
+    return (v >> (8 * (s & 3))) & 15u;
+}
+__device__ __forceinline__ Tab tab_shfl_up(const Tab &T, int d) {
+    Tab o;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) o.r[m] = __shfl_up_sync(0xffffffffu, T.r[m], d);
+    return o;
+}
+__device__ __forceinline__ uint4 tab_pack(const Tab &T) { return make_uint4(T.r[0], T.r[1], T.r[2], T.r[3]); }
+__device__ __forceinline__ Tab tab_unpack(uint4 v) { return Tab{{v.x, v.y, v.z, v.w}}; }
 
 __device__ __forceinline__ uint64_t load_word(const uint8_t *buf, uint64_t n, uint64_t i) {
     const uint64_t start = (uint64_t)buf, a = start + 8 * i;
@@ -75,10 +94,9 @@ __device__ __forceinline__ uint64_t load_word(const uint8_t *buf, uint64_t n, ui
 __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__restrict__ buf, uint64_t nbytes,
                                                             Status *status, unsigned long long *carry,
                                                             uint64_t *digest) {
-    __shared__ uint64_t stage[THREADS * (WPT + 1)];
-    __shared__ unsigned long long warp_tab[THREADS / 32];
+    extern __shared__ uint64_t stage[];  // THREADS x (WPT + 1) words, padded: conflict-free row reads
+    __shared__ uint4 warp_tab[THREADS / 32];
     __shared__ uint32_t warp_in[THREADS / 32];
-    __shared__ uint32_t cta_in;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint32_t G = gridDim.x, c = blockIdx.x;
     const uint64_t nw = (nbytes + 7) >> 3;
@@ -89,50 +107,56 @@ __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__res
 
     for (uint64_t r = 0; r < rounds; ++r) {
         const uint64_t q = r * G + c;
-        const bool active = q < nchunks;
+        if (q >= nchunks) break;  // only the last round has idle CTAs, and nobody waits on them
         const uint64_t last_in_round = (nchunks - r * G < G ? nchunks - r * G : G) - 1;
         uint64_t w[WPT], R[WPT];
-        int nv = 0;
-        if (active) {
-            // coalesced load into padded smem, then each thread takes its 16 consecutive words
-            const uint64_t base = q * CHUNK;
-            for (int idx = t; idx < CHUNK; idx += THREADS) {
-                const uint64_t i = base + idx;
-                stage[(idx / WPT) * (WPT + 1) + idx % WPT] = i < nw ? load_word(buf, nbytes, i) : 0ull;
-            }
-            __syncthreads();
-#pragma unroll
-            for (int j = 0; j < WPT; ++j) w[j] = stage[t * (WPT + 1) + j], R[j] = 0;
-            const int64_t left = (int64_t)nw - (int64_t)(base + (uint64_t)t * WPT);
-            nv = left <= 0 ? 0 : (left >= WPT ? WPT : (int)left);
-            __syncthreads();
+        const uint64_t base = q * CHUNK;
+        for (int idx = t; idx < CHUNK; idx += THREADS) {
+            const uint64_t i = base + idx;
+            stage[(idx / WPT) * (WPT + 1) + idx % WPT] = i < nw ? load_word(buf, nbytes, i) : 0ull;
         }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < WPT; ++j) w[j] = stage[t * (WPT + 1) + j], R[j] = 0;
+        const int64_t left = (int64_t)nw - (int64_t)(base + (uint64_t)t * WPT);
+        const int nv = left <= 0 ? 0 : (left >= WPT ? WPT : (int)left);
+        __syncthreads();
         for (int g = 0; g < 16; ++g) {
             const int k = 4 * g;
             const uint64_t slot = r * 16 + g;
-            if (active) {
-                // ---- pass A: this thread's map
-                unsigned long long T = ID;
+            // ---- pass A: this thread's map over its words
+            Tab T = tab_id();
 #pragma unroll
-                for (int j = 0; j < WPT; ++j)
-                    if (j < nv) T = step_table(T, (uint32_t)(w[j] >> k) & 15u, (uint32_t)(R[j] >> k) & 15u);
-                // ---- inclusive prefix composition across the warp (lane order)
+            for (int j = 0; j < WPT; ++j)
+                if (j < nv) tab_step(T, (uint32_t)(w[j] >> k) & 15u, (uint32_t)(R[j] >> k) & 15u);
+            // ---- inclusive prefix composition across the warp (lane order)
 #pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const unsigned long long o = __shfl_up_sync(0xffffffffu, T, d);
-                    if (lane >= d) T = compose(o, T);
+            for (int d = 1; d < 32; d <<= 1) {
+                const Tab o = tab_shfl_up(T, d);
+                if (lane >= d) T = tab_compose(o, T);
+            }
+            const Tab excl_lane = tab_shfl_up(T, 1);
+            if (lane == 31) warp_tab[warp] = tab_pack(T);
+            __syncthreads();
+            if (warp == 0) {
+                // prefix over the 8 warps (lanes 0..7), CTA aggregate in lane 7
+                Tab W = lane < THREADS / 32 ? tab_unpack(warp_tab[lane]) : tab_id();
+#pragma unroll
+                for (int d = 1; d < THREADS / 32; d <<= 1) {
+                    const Tab o = tab_shfl_up(W, d);
+                    if (lane >= d) W = tab_compose(o, W);
                 }
-                const unsigned long long excl_lane = __shfl_up_sync(0xffffffffu, T, 1);
-                if (lane == 31) warp_tab[warp] = T;
-                __syncthreads();
-                if (t == 0) {
-                    unsigned long long agg = ID;
-                    for (int i = 0; i < THREADS / 32; ++i) agg = compose(agg, warp_tab[i]);
-                    // publish the CTA aggregate, look back for the round prefix, publish inclusive
+                const Tab wexcl = tab_shfl_up(W, 1);
+                Tab agg;
+#pragma unroll
+                for (int m = 0; m < 4; ++m) agg.r[m] = __shfl_sync(0xffffffffu, W.r[m], THREADS / 32 - 1);
+                uint32_t s_cta = 0;
+                if (lane == 0) {
+                    // publish the aggregate, look back for the round prefix, publish the inclusive map
                     Status *me = status + slot * G + c;
-                    unsigned long long prefix = ID;
+                    Tab prefix = tab_id();
                     if (c > 0) {
-                        me->agg = agg;
+                        me->agg = tab_pack(agg);
                         __threadfence();
                         atomicExch(&me->flag, 1ull);
                         for (int64_t j = (int64_t)c - 1; j >= 0; --j) {
@@ -141,18 +165,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__res
                                 f = vst[slot * G + j].flag;
                             } while (f == 0);
                             __threadfence();
-                            if (f == 2) {
-                                prefix = compose(vst[slot * G + j].incl, prefix);
-                                break;
-                            }
-                            prefix = compose(vst[slot * G + j].agg, prefix);
+                            volatile uint4 *src = f == 2 ? &vst[slot * G + j].incl : &vst[slot * G + j].agg;
+                            const uint4 v = make_uint4(src->x, src->y, src->z, src->w);
+                            prefix = tab_compose(tab_unpack(v), prefix);
+                            if (f == 2) break;
                         }
                     }
-                    me->incl = compose(prefix, agg);
+                    me->incl = tab_pack(tab_compose(prefix, agg));
                     __threadfence();
                     atomicExch(&me->flag, 2ull);
-                    // the group's state entering this round
-                    uint32_t s_round;
+                    uint32_t s_round;  // the group's state entering this round
                     if (r == 0) {
                         s_round = (uint32_t)(FNV_OFFSET >> k) & 15u;
                     } else {
@@ -162,31 +184,28 @@ __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__res
                         } while (v == 0);
                         s_round = (uint32_t)v & 15u;
                     }
-                    uint32_t s = apply(prefix, s_round);
-                    cta_in = s;
-                    for (int i = 0; i < THREADS / 32; ++i) {
-                        warp_in[i] = s;
-                        s = apply(warp_tab[i], s);
-                    }
+                    s_cta = tab_apply(prefix, s_round);
                     if (q == r * G + last_in_round) {  // last chunk of the round: carry its output state
                         __threadfence();
-                        atomicExch(&carry[slot], 0x100ull | s);
+                        atomicExch(&carry[slot], 0x100ull | tab_apply(agg, s_cta));
                     }
                 }
-                __syncthreads();
-                // ---- pass B with the actual input state
-                uint32_t s = lane == 0 ? warp_in[warp] : apply(excl_lane, warp_in[warp]);
+                s_cta = __shfl_sync(0xffffffffu, s_cta, 0);
+                if (lane < THREADS / 32) warp_in[lane] = lane == 0 ? s_cta : tab_apply(wexcl, s_cta);
+            }
+            __syncthreads();
+            // ---- pass B with the actual input state
+            uint32_t s = lane == 0 ? warp_in[warp] : tab_apply(excl_lane, warp_in[warp]);
 #pragma unroll
-                for (int j = 0; j < WPT; ++j) {
-                    if (j < nv) {
-                        const uint32_t x4 = s ^ ((uint32_t)(w[j] >> k) & 15u);
-                        s = (((uint32_t)(R[j] >> k) & 15u) + 3u * x4) & 15u;
-                        R[j] += ((uint64_t)x4 << k) * FNV_PRIME;
-                    }
+            for (int j = 0; j < WPT; ++j) {
+                if (j < nv) {
+                    const uint32_t x4 = s ^ ((uint32_t)(w[j] >> k) & 15u);
+                    s = (((uint32_t)(R[j] >> k) & 15u) + 3u * x4) & 15u;
+                    R[j] += ((uint64_t)x4 << k) * FNV_PRIME;
                 }
-                __syncthreads();
             }
         }
+        __syncthreads();
     }
     // the final state is the carry of the last round; CTA 0 finishes the digest
     if (c == 0 && threadIdx.x == 0) {
@@ -219,7 +238,11 @@ int k2_grid() {
     k2::Ctx &C = k2::g_ctx[dev & 63];
     if (!C.grid) {
         int nb = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k2::k_hash_planes, k2::THREADS, 0) != cudaSuccess ||
+        if (cudaFuncSetAttribute(k2::k_hash_planes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2::SMEM) !=
+            cudaSuccess)
+            return -1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k2::k_hash_planes, k2::THREADS, k2::SMEM) !=
+                cudaSuccess ||
             nb < 1)
             return -1;
         C.grid = nb * sm_count();
@@ -258,8 +281,8 @@ int hash_planes_launch(const void *d_buf, uint64_t nbytes, uint64_t *d_digest, c
     B2L_CUDA(cudaMemsetAsync(C.carry, 0, need_c * sizeof(unsigned long long), stream));
     const uint8_t *b = (const uint8_t *)d_buf;
     void *args[] = {(void *)&b, (void *)&nbytes, (void *)&C.status, (void *)&C.carry, (void *)&d_digest};
-    B2L_CUDA(cudaLaunchCooperativeKernel((const void *)k2::k_hash_planes, dim3((unsigned)g), dim3(k2::THREADS), args, 0,
-                                         stream));
+    B2L_CUDA(cudaLaunchCooperativeKernel((const void *)k2::k_hash_planes, dim3((unsigned)g), dim3(k2::THREADS), args,
+                                         k2::SMEM, stream));
     return B2L_OK;
 }
 
