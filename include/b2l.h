@@ -117,7 +117,10 @@ enum {
     B2L_ANALYZE_SYNTH_END = 4,      /* b2l_analyze_ex: use the given synthetic-delete time (prep.py:61-62
                                        max end over ALL data ops -- a trace-wide value for a shard) */
     B2L_ANALYZE_SKIP_DDRT = 8,      /* shard holds no hash-keyed work: skip DD / RT */
-    B2L_ANALYZE_SKIP_ALLOC = 16     /* shard holds no device-keyed work: skip pairs / RA / UA / UT */
+    B2L_ANALYZE_SKIP_ALLOC = 16,    /* shard holds no device-keyed work: skip pairs / RA / UA / UT */
+    B2L_ANALYZE_NO_VALIDATE = 32,   /* standalone detectors (find_*) take event lists as given */
+    B2L_ANALYZE_RAW_HASHED = 64     /* DD/RT over every transfer row (find_duplicate_transfers /
+                                       find_round_trips group whatever they are given) */
 };
 #define B2L_SYNTHETIC 0xFFFFFFFFu   /* pair_delete of a synthetic trace-end delete (prep.py:78-93) */
 
@@ -202,6 +205,10 @@ typedef struct b2l_savings {
 } b2l_savings;
 int b2l_savings_compute(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings **out);
 void b2l_savings_free(b2l_savings *s);
+
+/* Stable sort of n u32 keys (host arrays): out_perm[i] = index of the i-th smallest key
+ * (equal keys keep their order) -- sort_by_device (prep.py:99-115). */
+int b2l_stable_sort_u32(const uint32_t *keys, uint64_t n, uint32_t *out_perm);
 
 /* Positions of `n` seq values in the trace's seq column (ascending seq, as in a
  * validated trace); UINT32_MAX when absent.  Host arrays. */

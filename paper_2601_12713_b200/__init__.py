@@ -11,10 +11,14 @@ from .hashing import HashFn, hash_batch, hash_bytes, hash_device, hash_tensors, 
 from .analysis import (ColumnarFindings, ColumnarSavings, analyze, analyze_columns, attribute, estimate,
                        savings_columns)
 from .columns import Columns, columns_from_arrays, to_columns
+from .standalone import (find_duplicate_transfers, find_repeated_allocs, find_round_trips, find_unused_allocs,
+                         find_unused_transfers, get_alloc_delete_pairs, sort_by_device, validate)
 
 __all__ = [
     "DeviceOutOfRange", "EmptyPayload", "EngineError", "EngineUnavailable",
     "FindingsTraceMismatch", "InvalidTrace", "HashFn", "hash_batch", "hash_bytes",
     "hash_device", "hash_tensors", "make_hasher", "ColumnarFindings", "ColumnarSavings", "analyze",
     "analyze_columns", "attribute", "estimate", "savings_columns", "Columns", "columns_from_arrays", "to_columns",
+    "find_duplicate_transfers", "find_repeated_allocs", "find_round_trips", "find_unused_allocs",
+    "find_unused_transfers", "get_alloc_delete_pairs", "sort_by_device", "validate",
 ]

@@ -128,9 +128,12 @@ __global__ void k_bad_rules(DevCols c, const uint32_t *bad, const uint32_t *coun
 }
 
 // ============================================================ partition (detectors.py:296-312)
-struct IsHashed {  // transfers with bytes > 0 and a content hash
+struct IsHashed {  // transfers with bytes > 0 and a content hash (raw: every transfer row)
     DevCols c;
-    __device__ bool operator()(size_t i) const { return c.kind[i] == B2L_KIND_TRANSFER && c.nb[i] > 0 && c.h[i] != 0; }
+    bool raw;
+    __device__ bool operator()(size_t i) const {
+        return c.kind[i] == B2L_KIND_TRANSFER && (raw || (c.nb[i] > 0 && c.h[i] != 0));
+    }
 };
 struct IsTargetTransfer {
     DevCols c;
@@ -166,7 +169,7 @@ __global__ void k_col_vary(DevCols c, unsigned long long *out /*[5] OR, [5] AND*
     unsigned long long o[5] = {0, 0, 0, 0, 0}, a[5] = {~0ull, ~0ull, ~0ull, ~0ull, ~0ull};
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += (size_t)gridDim.x * blockDim.x) {
         const uint8_t k = c.kind[i];
-        if (k == B2L_KIND_TRANSFER && c.nb[i] > 0 && c.h[i] != 0) o[0] |= c.h[i], a[0] &= c.h[i];
+        if (k == B2L_KIND_TRANSFER) o[0] |= c.h[i], a[0] &= c.h[i];  // superset of the hashed subset
         if (k == B2L_KIND_ALLOC || k == B2L_KIND_DELETE) o[1] |= c.da[i], a[1] &= c.da[i];
         if (k == B2L_KIND_ALLOC) o[2] |= c.sa[i], a[2] &= c.sa[i], o[3] |= c.nb[i], a[3] &= c.nb[i];
         if (k == B2L_KIND_TRANSFER && c.dst[i] != c.host) o[4] |= c.sa[i], a[4] &= c.sa[i];
@@ -1081,8 +1084,8 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     pc.mark("upload");
     DBuf<uint32_t> cnt(8, s);
     cnt.zero();
-    // ---- 1. validation
-    {
+    // ---- 1. validation (the standalone detector entry points take unvalidated event lists)
+    if (!(flags & B2L_ANALYZE_NO_VALIDATE)) {
         DBuf<uint32_t> bad(n ? n : 1, s);
         compact(n, BadPred{c}, bad.p, cnt.p + 0, s);
         const uint32_t nbad = read_u32(cnt.p + 0, s);
@@ -1101,7 +1104,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     if (flags & B2L_ANALYZE_VALIDATE_ONLY) return B2L_OK;
     // ---- 2. partition
     DBuf<uint32_t> H(n ? n : 1, s), TT(n ? n : 1, s), AD(n ? n : 1, s), A(n ? n : 1, s), TK(n ? n : 1, s);
-    compact(n, IsHashed{c}, H.p, cnt.p + 1, s);
+    compact(n, IsHashed{c, (flags & B2L_ANALYZE_RAW_HASHED) != 0}, H.p, cnt.p + 1, s);
     compact(n, IsTargetTransfer{c}, TT.p, cnt.p + 2, s);
     compact(n, IsAllocDelete{c}, AD.p, cnt.p + 3, s);
     compact(n, IsAlloc{c}, A.p, cnt.p + 4, s);
@@ -1623,6 +1626,28 @@ int b2l_savings_compute(const b2l_trace_cols *cols, const b2l_findings *f, b2l_s
 }
 
 void b2l_savings_free(b2l_savings *s) { b2l::ana::savings_free(s); }
+
+int b2l_stable_sort_u32(const uint32_t *keys, uint64_t n, uint32_t *out_perm) {
+    if (n && (!keys || !out_perm)) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
+    if (n == 0) return B2L_OK;
+    try {
+        using namespace b2l;
+        std::lock_guard<std::mutex> lock(ana::g_mu);
+        cudaStream_t s = ana::engine_stream();
+        DBuf<uint32_t> k32(n, s);
+        CK(cudaMemcpyAsync(k32.p, keys, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        SortStore<1> st(n, s);
+        uint64_t *k0 = st.in_key(0);
+        uint32_t *v = st.in_val();
+        const uint32_t *kk = k32.p;
+        ana::for_each(n, [=] __device__(size_t i) { k0[i] = kk[i], v[i] = (uint32_t)i; }, s);
+        radix_sort<1>(st.b, n, LiveBytes<1>{{0x0F}}, s);
+        read_back(out_perm, st.val(), n * sizeof(uint32_t), s);
+        return B2L_OK;
+    } catch (const b2l::EngineErr &e) {
+        return b2l::fail(e.code, e.msg);
+    }
+}
 
 int b2l_lookup_seqs(const b2l_trace_cols *cols, const uint64_t *seqs, uint64_t n, uint32_t *out_index) {
     if (!cols || (n && (!seqs || !out_index))) return b2l::fail(B2L_E_INVALID_ARG, "null argument");

@@ -50,7 +50,7 @@ def hash_fixture():
     return out
 
 
-if __name__ == "__main__" and "--analysis" not in sys.argv:
+if __name__ == "__main__" and "--analysis" not in sys.argv and "--standalone" not in sys.argv:
     with open(os.path.join(HERE, "hash_vectors.json"), "w") as f:
         json.dump(hash_fixture(), f, indent=0)
     print("wrote hash_vectors.json")
@@ -152,3 +152,57 @@ if __name__ == "__main__" and "--analysis" in sys.argv:
     with gzip.open(os.path.join(HERE, "analysis_cases.json.gz"), "wt") as f:
         json.dump(analysis_fixture(), f)
     print("wrote analysis_cases.json.gz")
+
+
+# ----------------------------------------------------------------------------- standalone detectors
+def standalone_fixture():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("ref_conftest", os.path.join(os.path.dirname(REF), "tests",
+                                                                               "conftest.py"))
+    conf = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(conf)
+    from dmlens.detectors import (find_duplicate_transfers, find_repeated_allocs, find_round_trips,
+                                  find_unused_allocs, find_unused_transfers)
+    from dmlens.model import EventKind
+    from dmlens.prep import get_alloc_delete_pairs, sort_by_device
+    out = []
+    for seed in range(3000, 3080):
+        tr = conf.random_trace(seed)
+        ev, host, nd = tr.events, tr.host_device, tr.num_devices_total
+        transfers = [e for e in ev if e.kind is EventKind.TRANSFER]
+        data_ops = [e for e in ev if e.kind is not EventKind.KERNEL]
+        kernels = [e for e in ev if e.kind is EventKind.KERNEL]
+        tk = [e for e in kernels if e.dst_device != host]
+        tt = [e for e in transfers if e.dst_device != host]
+        warns = []
+        c = {"seed": seed, "trace": _trace_json(tr),
+             # raw lists: every transfer (hash 0 / zero-byte included), every kernel (host included)
+             "dd_raw": _findings_json_part_dd(find_duplicate_transfers(transfers)),
+             "rt_raw": _findings_json_part_rt(find_round_trips(transfers)),
+             "rt_raw_strict": _findings_json_part_rt(find_round_trips(transfers, strict_pseudocode=True)),
+             "pairs": [_pair_json(p) for p in get_alloc_delete_pairs(data_ops, warn=warns.append)],
+             "ra": [[g.host_addr, g.tgt_device, g.bytes, [_pair_json(p) for p in g.pairs]]
+                    for g in find_repeated_allocs(data_ops)],
+             "ua_all_kernels": [_pair_json(p) for p in find_unused_allocs(kernels, data_ops, nd)],
+             "ut_all": [e.seq for e in find_unused_transfers(kernels, transfers, nd)],
+             "ut_target": [e.seq for e in find_unused_transfers(tk, tt, nd)],
+             "by_device_dst": [[e.seq for e in lst] for lst in sort_by_device(ev, nd, key="dst")],
+             "by_device_src": [[e.seq for e in lst] for lst in sort_by_device(ev, nd, key="src")]}
+        c["warnings"] = [w.seq for w in warns]
+        out.append(c)
+    return out
+
+
+def _findings_json_part_dd(groups):
+    return [[str(g.hash), g.dest_device, [e.seq for e in g.events]] for g in groups]
+
+
+def _findings_json_part_rt(groups):
+    return [[str(g.hash), g.src_device, g.dest_device, [[a.seq, b.seq] for a, b in g.trips]] for g in groups]
+
+
+if __name__ == "__main__" and "--standalone" in sys.argv:
+    import gzip
+    with gzip.open(os.path.join(HERE, "standalone_cases.json.gz"), "wt") as f:
+        json.dump(standalone_fixture(), f)
+    print("wrote standalone_cases.json.gz")
