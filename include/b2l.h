@@ -202,6 +202,7 @@ typedef struct b2l_savings {
     b2l_u128 *attr_ns, *attr_bytes;
     uint64_t *attr_first;         /* (multiset position << 32) | event index of the first member;
                                      UINT64_MAX when the bucket has no member */
+    void *internal;               /* engine-owned pinned memory behind the arrays above */
 } b2l_savings;
 int b2l_savings_compute(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings **out);
 void b2l_savings_free(b2l_savings *s);

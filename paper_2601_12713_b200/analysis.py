@@ -66,7 +66,7 @@ class _U128(ctypes.Structure):
 class _Savings(ctypes.Structure):
     _fields_ = [("per_category_ns", _U128 * 5), ("union_ns", _U128), ("n_union", _u64), ("union_index", _P),
                 ("has_overlaps", _i32), ("min_start_ns", _u64), ("max_end_ns", _u64), ("n_buckets", _u32),
-                ("attr_count", _P), ("attr_ns", _P), ("attr_bytes", _P), ("attr_first", _P)]
+                ("attr_count", _P), ("attr_ns", _P), ("attr_bytes", _P), ("attr_first", _P), ("internal", _P)]
 
 
 _declared = False
@@ -135,6 +135,15 @@ class DeviceColumns:
     @property
     def n(self):
         return self.host.n
+
+
+def _view(ptr, n, dtype, owner):
+    """Zero-copy numpy view of engine-owned (pinned) memory; the view keeps `owner` alive."""
+    if not n or not ptr:
+        return np.zeros(0, dtype=dtype)
+    buf = (ctypes.c_char * (int(n) * np.dtype(dtype).itemsize)).from_address(ptr)
+    buf._owner = owner
+    return np.frombuffer(buf, dtype=dtype)
 
 
 def _arr(ptr, n, dtype):
@@ -219,30 +228,19 @@ def analyze_columns(cols: Columns, strict: bool = False, flags: int = 0,
     f = fp.contents
     if flags & FLAG_VALIDATE_ONLY:
         return None
+    V = lambda ptr, n, dt: _view(ptr, n, dt, handle)  # noqa: E731
+    dd_off = V(f.dd_offsets, f.dd_groups + 1, np.uint64)
+    rt_off = V(f.rt_offsets, f.rt_groups + 1, np.uint64)
+    ra_off = V(f.ra_offsets, f.ra_groups + 1, np.uint64)
+    nm, nt, nr = (int(o[-1]) if len(o) else 0 for o in (dd_off, rt_off, ra_off))
     return ColumnarFindings(
-        n_events=f.n_events,
-        dd_offsets=_arr(f.dd_offsets, f.dd_groups + 1, np.uint64), dd_members=None,
-        rt_offsets=_arr(f.rt_offsets, f.rt_groups + 1, np.uint64), rt_tx=None, rt_rx=None,
-        pair_alloc=_arr(f.pair_alloc, f.n_pairs, np.uint32), pair_delete=_arr(f.pair_delete, f.n_pairs, np.uint32),
-        synthetic_end_ns=int(f.synthetic_end_ns), warn_index=_arr(f.warn_index, f.n_warnings, np.uint32),
-        ra_offsets=_arr(f.ra_offsets, f.ra_groups + 1, np.uint64), ra_pairs=None,
-        ua_pairs=_arr(f.ua_pairs, f.n_ua, np.uint32), ut_events=_arr(f.ut_events, f.n_ut, np.uint32),
-        _handle=handle,
-    )._fill(f)
-
-
-def _fill(self, f):
-    nm = int(self.dd_offsets[-1]) if len(self.dd_offsets) else 0
-    nt = int(self.rt_offsets[-1]) if len(self.rt_offsets) else 0
-    nr = int(self.ra_offsets[-1]) if len(self.ra_offsets) else 0
-    self.dd_members = _arr(f.dd_members, nm, np.uint32)
-    self.rt_tx = _arr(f.rt_tx, nt, np.uint32)
-    self.rt_rx = _arr(f.rt_rx, nt, np.uint32)
-    self.ra_pairs = _arr(f.ra_pairs, nr, np.uint32)
-    return self
-
-
-ColumnarFindings._fill = _fill
+        n_events=f.n_events, dd_offsets=dd_off, dd_members=V(f.dd_members, nm, np.uint32),
+        rt_offsets=rt_off, rt_tx=V(f.rt_tx, nt, np.uint32), rt_rx=V(f.rt_rx, nt, np.uint32),
+        pair_alloc=V(f.pair_alloc, f.n_pairs, np.uint32), pair_delete=V(f.pair_delete, f.n_pairs, np.uint32),
+        synthetic_end_ns=int(f.synthetic_end_ns), warn_index=V(f.warn_index, f.n_warnings, np.uint32),
+        ra_offsets=ra_off, ra_pairs=V(f.ra_pairs, nr, np.uint32),
+        ua_pairs=V(f.ua_pairs, f.n_ua, np.uint32), ut_events=V(f.ut_events, f.n_ut, np.uint32),
+        _handle=handle)
 
 
 @dataclass

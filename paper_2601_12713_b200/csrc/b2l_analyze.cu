@@ -283,7 +283,9 @@ struct StoreOffset {
 };
 
 // ============================================================ output container
+struct HostSlab;
 struct Internal {
+    HostSlab *slab = nullptr;  // pinned host memory behind the b2l_findings arrays
     // device copies of the trace columns (when they were uploaded from host) and their identity
     ColsUpload cols;
     const void *cols_key[3] = {nullptr, nullptr, nullptr};
@@ -302,36 +304,34 @@ T *host_copy(const T *d, size_t n, cudaStream_t s) {
     if (n) read_back(h, d, n * sizeof(T), s);
     return h;
 }
-// Many device->host result copies through the pinned stage with a single synchronisation.
+// Many device->host result copies straight into one pinned slab with a single synchronisation.
+struct HostSlab {
+    uint8_t *p = nullptr;
+    size_t cap = 0;
+    ~HostSlab() { slab_pool().release(p, cap); }
+};
 struct HostBatch {
     struct Item {
-        void *dst;
+        void **dst;
         const void *src;
         size_t bytes;
     };
     std::vector<Item> items;
     template <class T>
-    T *add(const T *d, size_t n) {
-        T *h = (T *)malloc((n ? n : 1) * sizeof(T));
-        if (!h) throw EngineErr{B2L_E_OOM, "host allocation failed"};
-        if (n) items.push_back(Item{h, d, n * sizeof(T)});
-        return h;
+    void add(T **dst, const T *d, size_t n) {
+        items.push_back(Item{(void **)dst, d, n * sizeof(T)});
     }
-    void flush(cudaStream_t s) {
+    void flush(HostSlab &slab, cudaStream_t s) {
         size_t total = 0;
-        for (auto &it : items) total += (it.bytes + 15) & ~size_t(15);
-        uint8_t *st = pinned(s).reserve(total ? total : 16);
+        for (auto &it : items) total += (it.bytes + 63) & ~size_t(63);
+        slab.p = slab_pool().acquire(total, slab.cap);
         size_t off = 0;
         for (auto &it : items) {
-            CK(cudaMemcpyAsync(st + off, it.src, it.bytes, cudaMemcpyDeviceToHost, s));
-            off += (it.bytes + 15) & ~size_t(15);
+            if (it.bytes) CK(cudaMemcpyAsync(slab.p + off, it.src, it.bytes, cudaMemcpyDeviceToHost, s));
+            *it.dst = slab.p + off;
+            off += (it.bytes + 63) & ~size_t(63);
         }
         CK(cudaStreamSynchronize(s));
-        off = 0;
-        for (auto &it : items) {
-            memcpy(it.dst, st + off, it.bytes);
-            off += (it.bytes + 15) & ~size_t(15);
-        }
         items.clear();
     }
 };
@@ -1094,9 +1094,11 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
             k_bad_rules<<<grid_for(nbad, TPB), TPB, 0, s>>>(c, bad.p, cnt.p + 0, rules.p);
             CK_LAUNCH("k_bad_rules");
             f->n_bad = nbad;
-            f->bad_index = host_copy(bad.p, nbad, s);
-            f->bad_rules = host_copy(rules.p, nbad, s);
-            CK(cudaStreamSynchronize(s));
+            HostBatch hb;
+            hb.add(&f->bad_index, bad.p, nbad);
+            hb.add(&f->bad_rules, rules.p, nbad);
+            in->slab = new HostSlab();
+            hb.flush(*in->slab, s);
             return fail(B2L_E_INVALID_TRACE, "trace fails validation");
         }
     }
@@ -1183,29 +1185,30 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     if (failed2) throw err2;
     pc.mark("detectors");
 
-    // ---- results to the host (one pinned staging pass)
+    // ---- results to the host (one pinned slab, one synchronisation)
     HostBatch hb;
     f->dd_groups = in->dd_groups;
-    f->dd_offsets = hb.add(in->dd_off.p, in->dd_groups + 1);
-    f->dd_members = hb.add(in->dd_mem.p, in->dd_members);
+    hb.add(&f->dd_offsets, in->dd_off.p, in->dd_groups + 1);
+    hb.add(&f->dd_members, in->dd_mem.p, in->dd_members);
     f->rt_groups = in->rt_groups;
-    f->rt_offsets = hb.add(in->rt_off.p, in->rt_groups + 1);
-    f->rt_tx = hb.add(in->rt_tx.p, in->rt_trips);
-    f->rt_rx = hb.add(in->rt_rx.p, in->rt_trips);
+    hb.add(&f->rt_offsets, in->rt_off.p, in->rt_groups + 1);
+    hb.add(&f->rt_tx, in->rt_tx.p, in->rt_trips);
+    hb.add(&f->rt_rx, in->rt_rx.p, in->rt_trips);
     f->n_pairs = nA;
-    f->pair_alloc = hb.add(in->pair_alloc.p, nA);
-    f->pair_delete = hb.add(in->pair_delete.p, nA);
+    hb.add(&f->pair_alloc, in->pair_alloc.p, nA);
+    hb.add(&f->pair_delete, in->pair_delete.p, nA);
     f->synthetic_end_ns = me;
     f->n_warnings = po.n_warn;
-    f->warn_index = hb.add(po.warn.p, po.n_warn);
+    hb.add(&f->warn_index, po.warn.p, po.n_warn);
     f->ra_groups = in->ra_groups;
-    f->ra_offsets = hb.add(in->ra_off.p, in->ra_groups + 1);
-    f->ra_pairs = hb.add(in->ra_mem.p, in->ra_members);
+    hb.add(&f->ra_offsets, in->ra_off.p, in->ra_groups + 1);
+    hb.add(&f->ra_pairs, in->ra_mem.p, in->ra_members);
     f->n_ua = in->n_ua;
-    f->ua_pairs = hb.add(in->ua.p, in->n_ua);
+    hb.add(&f->ua_pairs, in->ua.p, in->n_ua);
     f->n_ut = in->n_ut;
-    f->ut_events = hb.add(in->ut.p, in->n_ut);
-    hb.flush(s);
+    hb.add(&f->ut_events, in->ut.p, in->n_ut);
+    in->slab = new HostSlab();
+    hb.flush(*in->slab, s);
     pc.mark("d2h");
     if (in->dd_groups == 0) f->dd_offsets[0] = 0;
     if (in->rt_groups == 0) f->rt_offsets[0] = 0;
@@ -1215,10 +1218,9 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
 
 void findings_free(b2l_findings *f) {
     if (!f) return;
-    free(f->bad_index), free(f->bad_rules), free(f->dd_offsets), free(f->dd_members), free(f->rt_offsets);
-    free(f->rt_tx), free(f->rt_rx), free(f->pair_alloc), free(f->pair_delete), free(f->warn_index);
-    free(f->ra_offsets), free(f->ra_pairs), free(f->ua_pairs), free(f->ut_events);
-    delete (Internal *)f->internal;
+    Internal *in = (Internal *)f->internal;
+    if (in) delete in->slab;  // arrays live in the slab
+    delete in;
     free(f);
 }
 
@@ -1536,20 +1538,22 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     o->min_start_ns = n ? h[13] : 0;
     o->max_end_ns = h[14];
     HostBatch hb;
-    o->union_index = hb.add(uni.p, hun);
+    hb.add(&o->union_index, uni.p, hun);
     o->n_buckets = nb;
     const size_t nb5 = 5 * (size_t)nb;
-    o->attr_count = (uint64_t *)hb.add(at.p, nb5);
-    o->attr_ns = (b2l_u128 *)hb.add(at.p + nb5, 2 * nb5);
-    o->attr_bytes = (b2l_u128 *)hb.add(at.p + 3 * nb5, 2 * nb5);
-    o->attr_first = (uint64_t *)hb.add(at.p + 5 * nb5, nb5);
-    hb.flush(s);
+    hb.add((unsigned long long **)&o->attr_count, at.p, nb5);
+    hb.add((unsigned long long **)&o->attr_ns, at.p + nb5, 2 * nb5);
+    hb.add((unsigned long long **)&o->attr_bytes, at.p + 3 * nb5, 2 * nb5);
+    hb.add((unsigned long long **)&o->attr_first, at.p + 5 * nb5, nb5);
+    HostSlab *slab = new HostSlab();
+    o->internal = slab;
+    hb.flush(*slab, s);
     return B2L_OK;
 }
 
 void savings_free(b2l_savings *o) {
     if (!o) return;
-    free(o->union_index), free(o->attr_count), free(o->attr_ns), free(o->attr_bytes), free(o->attr_first);
+    delete (HostSlab *)o->internal;
     free(o);
 }
 

@@ -254,6 +254,41 @@ inline Pinned &pinned(cudaStream_t s) {
     std::lock_guard<std::mutex> lock(mu);
     return by_stream[s];
 }
+// Pinned result slabs: findings / sums arrays live in page-locked memory the engine owns and
+// recycles (DMA'd straight into place, no malloc + memcpy; the Python side wraps them zero-copy).
+struct SlabPool {
+    std::mutex mu;
+    std::multimap<size_t, uint8_t *> free_;
+    uint8_t *acquire(size_t bytes, size_t &cap) {
+        bytes = bytes < 4096 ? 4096 : bytes;
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            auto it = free_.lower_bound(bytes);
+            if (it != free_.end() && it->first <= 4 * bytes) {
+                cap = it->first;
+                uint8_t *p = it->second;
+                free_.erase(it);
+                return p;
+            }
+        }
+        size_t c = 4096;
+        while (c < bytes) c <<= 1;
+        uint8_t *p = nullptr;
+        CK(cudaMallocHost(&p, c));
+        cap = c;
+        return p;
+    }
+    void release(uint8_t *p, size_t cap) {
+        if (!p) return;
+        std::lock_guard<std::mutex> lock(mu);
+        free_.emplace(cap, p);
+    }
+};
+inline SlabPool &slab_pool() {
+    static SlabPool pool;
+    return pool;
+}
+
 // Read `bytes` from device memory into host `dst` (synchronous).
 inline void read_back(void *dst, const void *d_src, size_t bytes, cudaStream_t s) {
     uint8_t *st = pinned(s).reserve(bytes);
