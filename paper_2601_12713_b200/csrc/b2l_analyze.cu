@@ -160,7 +160,13 @@ __global__ void k_max_data_end(DevCols c, unsigned long long *out) {
         unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
         m = v > m ? v : m;
     }
-    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+    __shared__ unsigned long long wm[32];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = wm[w] > m ? wm[w] : m;
+        if (m) atomicMax(out, m);
+    }
 }
 
 // Bits that vary inside each key subset (OR ^ AND over the subset): hash over hashed transfers,
@@ -174,6 +180,9 @@ __global__ void k_col_vary(DevCols c, unsigned long long *out /*[5] OR, [5] AND*
         if (k == B2L_KIND_ALLOC) o[2] |= c.sa[i], a[2] &= c.sa[i], o[3] |= c.nb[i], a[3] &= c.nb[i];
         if (k == B2L_KIND_TRANSFER && c.dst[i] != c.host) o[4] |= c.sa[i], a[4] &= c.sa[i];
     }
+    // warp, then block reduction: one pair of atomics per block and column
+    __shared__ unsigned long long so[32][5], sa[32][5];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
         unsigned long long vo = o[q], va = a[q];
@@ -181,10 +190,14 @@ __global__ void k_col_vary(DevCols c, unsigned long long *out /*[5] OR, [5] AND*
             vo |= __shfl_xor_sync(0xffffffffu, vo, off);
             va &= __shfl_xor_sync(0xffffffffu, va, off);
         }
-        if ((threadIdx.x & 31) == 0) {
-            if (vo) atomicOr(out + q, vo);
-            if (~va) atomicAnd(out + 5 + q, va);
-        }
+        if (lane == 0) so[wid][q] = vo, sa[wid][q] = va;
+    }
+    __syncthreads();
+    if (threadIdx.x < 5) {
+        unsigned long long vo = 0, va = ~0ull;
+        for (int w = 0; w < nw; ++w) vo |= so[w][threadIdx.x], va &= sa[w][threadIdx.x];
+        if (vo) atomicOr(out + threadIdx.x, vo);
+        if (~va) atomicAnd(out + 5 + threadIdx.x, va);
     }
 }
 struct SrankLoad {
