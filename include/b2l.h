@@ -83,6 +83,14 @@ int b2l_hash_bytes(const void *h_buf, uint64_t len, uint64_t *digest);
 int b2l_fill_payloads(uint8_t *d_base, const uint64_t *d_offsets, const uint64_t *d_lens,
                       const uint64_t *d_content_ids, uint64_t n, uint64_t seed, void *stream);
 
+/* Collision audit (hashing.py:70-92 CollisionAuditStore.observe over n observations in
+ * order, used by `dmlens audit`, cli.py:206-236): observation i = (d_hashes[i], payload at
+ * d_ptrs[i] of d_lens[i] bytes), device arrays.  *collisions = observations whose payload
+ * differs from the first payload seen with the same hash; *distinct = distinct hashes
+ * (len(store)).  Synchronous. */
+int b2l_audit_batch(const uint64_t *d_hashes, const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n,
+                    uint64_t *collisions, uint64_t *distinct);
+
 /* Kernel variant selection (tuning / tests): variant -1 only reports the
  * number of variants in *count, -2 restores the default (the tuned variant,
  * DESIGN.md K1).  Process-wide. */

@@ -92,3 +92,15 @@ def payload(nbytes: int, seed: int, content_id: int) -> bytes:
     if nbytes:
         lib().orc_fill_payload(buf.ctypes.data, nbytes, seed, content_id)
     return buf.tobytes()
+
+
+def audit_ref(observations):
+    """Restatement of dmlens.hashing.CollisionAuditStore.observe (hashing.py:70-87) over
+    (hash, payload) observations in order -> (collision_count, distinct hashes)."""
+    first, count = {}, 0
+    for h, p in observations:
+        if h not in first:
+            first[h] = bytes(p)
+        elif first[h] != p:
+            count += 1
+    return count, len(first)

@@ -7,7 +7,8 @@ __version__ = "0.1.0"
 
 from .errors import (DeviceOutOfRange, EmptyPayload, EngineError, EngineUnavailable,
                      FindingsTraceMismatch, InvalidTrace)
-from .hashing import HashFn, hash_batch, hash_bytes, hash_device, hash_tensors, make_hasher
+from .hashing import (CollisionAuditStore, HashFn, audit_observe, hash_batch, hash_bytes, hash_device,
+                      hash_tensors, make_hasher)
 from .analysis import (ColumnarFindings, ColumnarSavings, analyze, analyze_columns, attribute, estimate,
                        savings_columns)
 from .columns import Columns, columns_from_arrays, to_columns
@@ -17,7 +18,7 @@ from .standalone import (find_duplicate_transfers, find_repeated_allocs, find_ro
 __all__ = [
     "DeviceOutOfRange", "EmptyPayload", "EngineError", "EngineUnavailable",
     "FindingsTraceMismatch", "InvalidTrace", "HashFn", "hash_batch", "hash_bytes",
-    "hash_device", "hash_tensors", "make_hasher", "ColumnarFindings", "ColumnarSavings", "analyze",
+    "hash_device", "hash_tensors", "make_hasher", "CollisionAuditStore", "audit_observe", "ColumnarFindings", "ColumnarSavings", "analyze",
     "analyze_columns", "attribute", "estimate", "savings_columns", "Columns", "columns_from_arrays", "to_columns",
     "find_duplicate_transfers", "find_repeated_allocs", "find_round_trips", "find_unused_allocs",
     "find_unused_transfers", "get_alloc_delete_pairs", "sort_by_device", "validate",

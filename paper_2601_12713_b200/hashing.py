@@ -163,3 +163,74 @@ def to_u64_list(t) -> list[int]:
     """int64 digest tensor/array -> Python ints in [0, 2**64)."""
     arr = t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t)
     return [int(x) & U64_MASK for x in arr.view(np.uint64)]
+
+
+# ---------------------------------------------------------------------------- collision audit
+class CollisionAuditStore:
+    """Drop-in for dmlens.hashing.CollisionAuditStore (hashing.py:70-87): keeps the first
+    payload per hash, counts byte-unequal repeats.  Observations are buffered and audited on
+    the device in one batch (b2l_audit_batch) when ``collision_count`` or ``len()`` is read;
+    the result equals observing them one by one."""
+
+    def __init__(self) -> None:
+        self._obs: list = []          # (hash, payload bytes) in observation order
+        self._count = 0
+        self._distinct = 0
+        self._clean = True
+
+    def observe(self, hash_value: int, payload: bytes) -> None:
+        self._obs.append((int(hash_value), bytes(payload)))
+        self._clean = False
+
+    def _flush(self):
+        if self._clean:
+            return
+        self._count, self._distinct = audit_payloads([h for h, _ in self._obs], [p for _, p in self._obs])
+        self._clean = True
+
+    @property
+    def collision_count(self) -> int:
+        self._flush()
+        return self._count
+
+    def __len__(self) -> int:
+        self._flush()
+        return self._distinct
+
+
+def audit_observe(store: CollisionAuditStore, hash_value: int, payload: bytes) -> CollisionAuditStore:
+    store.observe(hash_value, payload)
+    return store
+
+
+def audit_payloads(hashes, payloads) -> tuple:
+    """(collision_count, distinct hashes) of observations in order -- host payloads are
+    packed into one device slab and audited by b2l_audit_batch."""
+    import torch
+
+    n = len(hashes)
+    if n == 0:
+        return 0, 0
+    lens = np.array([len(p) for p in payloads], dtype=np.int64)
+    offs = np.zeros(n, dtype=np.int64)
+    if n > 1:
+        offs[1:] = np.cumsum((lens + 15) // 16 * 16)[:-1]
+    total = int(offs[-1] + lens[-1]) + 16
+    host = np.zeros(total, dtype=np.uint8)
+    for o, p in zip(offs.tolist(), payloads):
+        if p:
+            host[o:o + len(p)] = np.frombuffer(p, dtype=np.uint8)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    slab = torch.from_numpy(host).to(dev)
+    return audit_device(torch.tensor(np.array(hashes, dtype=np.uint64).view(np.int64), device=dev),
+                        torch.from_numpy(offs).to(dev) + slab.data_ptr(), torch.from_numpy(lens).to(dev))
+
+
+def audit_device(hashes, ptrs, lens) -> tuple:
+    """Device observations: int64 CUDA tensors of hash bit patterns, device addresses, lengths."""
+    c, d = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    L = _lib.lib()
+    L.b2l_audit_batch.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]
+    _lib.check(L.b2l_audit_batch(hashes.data_ptr(), ptrs.data_ptr(), lens.data_ptr(), hashes.numel(),
+                                 ctypes.byref(c), ctypes.byref(d)), "b2l_audit_batch")
+    return int(c.value), int(d.value)

@@ -247,3 +247,36 @@ def test_k2_multi_round_buffer_and_routing(cuda):
     got = to_u64_list(hash_tensors(ts))
     want = [hash_ref.fold64_c(t.cpu().numpy().tobytes()) for t in ts]
     assert got == want
+
+
+# ----------------------------------------------------------------------------- collision audit
+def test_audit_reference_cases(cuda):
+    from paper_2601_12713_b200 import CollisionAuditStore, audit_observe, hash_bytes
+    store = CollisionAuditStore()
+    h = hash_bytes(b"abcdef")
+    audit_observe(store, h, b"abcdef")
+    audit_observe(store, h, b"abcdef")
+    assert store.collision_count == 0 and len(store) == 1
+    store = CollisionAuditStore()
+    audit_observe(store, 42, b"first")
+    audit_observe(store, 42, b"second")
+    assert store.collision_count == 1
+    audit_observe(store, 42, b"third")
+    assert store.collision_count == 2
+    audit_observe(store, 42, b"first")
+    assert store.collision_count == 2
+
+
+def test_audit_random_vs_oracle(cuda):
+    from paper_2601_12713_b200.hashing import audit_payloads
+    rng = np.random.default_rng(9)
+    for trial in range(20):
+        n = int(rng.integers(1, 400))
+        pool = [hash_ref.payload(int(rng.integers(1, 3000)), 4, i) for i in range(int(rng.integers(1, 30)))]
+        obs = []
+        for _ in range(n):
+            p = pool[int(rng.integers(0, len(pool)))]
+            if rng.random() < 0.1 and len(p) > 1:  # near-miss: one flipped byte / truncated
+                p = p[:-1] if rng.random() < 0.5 else bytes([p[0] ^ 1]) + p[1:]
+            obs.append((int(rng.integers(0, 8)), p))
+        assert audit_payloads([h for h, _ in obs], [p for _, p in obs]) == hash_ref.audit_ref(obs), trial
