@@ -91,6 +91,34 @@ int b2l_fill_payloads(uint8_t *d_base, const uint64_t *d_offsets, const uint64_t
 int b2l_audit_batch(const uint64_t *d_hashes, const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n,
                     uint64_t *collisions, uint64_t *distinct);
 
+/* Native NDJSON ingest (traceio.py:153-191 wire format).  Parses the header and every
+ * event record into columns (input order, not yet sorted or validated) over `threads`
+ * host threads.  If any line is not a record the reference accepts without error,
+ * err_line names the first such line (1-based) and no columns are returned: the caller
+ * reproduces the reference's exception for it.  Free with b2l_ingest_free. */
+typedef struct b2l_ingest {
+    uint64_t err_line;            /* 0 = every line accepted */
+    uint64_t header_line;         /* 0 = no header line found */
+    uint64_t version, num_devices, host_device, wall_time_ns;
+    int32_t has_wall;
+    uint64_t n_events;
+    const uint64_t *seq, *start_ns, *end_ns, *src_device, *dst_device, *src_addr, *dst_addr, *bytes, *hash;
+    const uint8_t *kind;
+    const uint32_t *loc;
+    uint32_t n_locs;
+    const uint64_t *loc_codeptr;
+    const int64_t *loc_line;      /* -1 = None */
+    const uint64_t *loc_file_off; /* into strings; UINT64_MAX = None */
+    const uint32_t *loc_file_len;
+    const char *strings;          /* UTF-8 file names */
+} b2l_ingest;
+int b2l_ingest_ndjson(const char *data, uint64_t len, int threads, b2l_ingest **out);
+void b2l_ingest_free(b2l_ingest *p);
+
+/* Stable sort of n (k0, k1) u64 key pairs (host arrays): out_perm = sorting permutation
+ * (parse_trace's events.sort(key=(start_ns, seq)), traceio.py:183). */
+int b2l_sort_u64_pairs(const uint64_t *k0, const uint64_t *k1, uint64_t n, uint32_t *out_perm);
+
 /* Kernel variant selection (tuning / tests): variant -1 only reports the
  * number of variants in *count, -2 restores the default (the tuned variant,
  * DESIGN.md K1).  Process-wide. */

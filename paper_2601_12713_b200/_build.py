@@ -10,7 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libb2l.so")
-SOURCES = ["b2l_api.cu", "b2l_hash.cu", "b2l_hash_k2.cu", "b2l_analyze.cu", "b2l_audit.cu"]
+SOURCES = ["b2l_api.cu", "b2l_hash.cu", "b2l_hash_k2.cu", "b2l_analyze.cu", "b2l_audit.cu", "b2l_ingest.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

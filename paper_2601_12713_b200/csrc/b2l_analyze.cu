@@ -1666,6 +1666,29 @@ int b2l_stable_sort_u32(const uint32_t *keys, uint64_t n, uint32_t *out_perm) {
     }
 }
 
+int b2l_sort_u64_pairs(const uint64_t *k0, const uint64_t *k1, uint64_t n, uint32_t *out_perm) {
+    if (n && (!k0 || !k1 || !out_perm)) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
+    if (n == 0) return B2L_OK;
+    try {
+        using namespace b2l;
+        std::lock_guard<std::mutex> lock(ana::g_mu);
+        cudaStream_t s = ana::engine_stream();
+        SortStore<2> st(n, s);
+        CK(cudaMemcpyAsync(st.in_key(0), k0, n * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(st.in_key(1), k1, n * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+        uint32_t *v = st.in_val();
+        ana::for_each(n, [=] __device__(size_t i) { v[i] = (uint32_t)i; }, s);
+        // live digit bytes from an OR/AND pass over the (host) keys
+        uint64_t o0 = 0, a0 = ~0ull, o1 = 0, a1 = ~0ull;
+        for (uint64_t i = 0; i < n; ++i) o0 |= k0[i], a0 &= k0[i], o1 |= k1[i], a1 &= k1[i];
+        radix_sort<2>(st.b, n, LiveBytes<2>{{live_mask(o0 ^ a0), live_mask(o1 ^ a1)}}, s);
+        read_back(out_perm, st.val(), n * sizeof(uint32_t), s);
+        return B2L_OK;
+    } catch (const b2l::EngineErr &e) {
+        return b2l::fail(e.code, e.msg);
+    }
+}
+
 int b2l_lookup_seqs(const b2l_trace_cols *cols, const uint64_t *seqs, uint64_t n, uint32_t *out_index) {
     if (!cols || (n && (!seqs || !out_index))) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
     try {

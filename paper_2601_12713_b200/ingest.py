@@ -1,0 +1,335 @@
+"""NDJSON trace ingest -- drop-in for dmlens.traceio.parse_trace / load_trace_file
+(traceio.py:153-191, 240-242) on the native parser (b2l_ingest_ndjson, C++ over host
+threads) plus GPU sorting (b2l_sort_u64_pairs) and GPU validation (b2l_analyze_ex
+VALIDATE_ONLY).
+
+  parse_trace(data, types=None) -> Trace            objects, like the reference
+  parse_trace_columns(data)     -> Columns          no Python objects (large traces)
+
+Error behaviour is the reference's: MissingHeader, UnsupportedVersion,
+MalformedRecord(line_no, reason), InvariantViolation(violations) (classes from
+dmlens.traceio when types="dmlens").  The native parser accepts exactly the records
+the reference accepts without error and names the first line it cannot vouch for;
+that input is then parsed by ``_parse_exact`` (a restatement of traceio.py:87-191),
+which raises the reference's exception for that line -- or, if the line was only
+unusual (e.g. Unicode whitespace the reference strips), parses the whole input.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+from collections import namedtuple
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .analysis import FLAG_VALIDATE_ONLY, EngineInvalid, _RULE_TEXT, analyze_columns
+from .columns import LOC_FILE_NO_LINE, LOC_LINE_NONPOS, Columns, loc_key
+from .types import family
+
+U64_MAX = 2**64 - 1
+I32_MAX = 2**31 - 1
+FORMAT_VERSION = 1
+_KINDS = ("transfer", "alloc", "delete", "kernel")
+_REQUIRED = ("seq", "kind", "t0", "t1", "src_dev", "dst_dev", "src_addr", "dst_addr", "bytes", "hash", "codeptr")
+
+
+# ------------------------------------------------------------------------ error classes (traceio.py:42-75)
+class TraceIOError(Exception):
+    pass
+
+
+class MalformedRecord(TraceIOError):
+    def __init__(self, line_no: int, reason: str):
+        super().__init__(f"line {line_no}: {reason}")
+        self.line_no = line_no
+        self.reason = reason
+
+
+class MissingHeader(TraceIOError):
+    def __init__(self, detail: str = "first non-comment line must be the trace header"):
+        super().__init__(detail)
+
+
+class UnsupportedVersion(TraceIOError):
+    def __init__(self, version):
+        super().__init__(f"unsupported trace format version {version!r} (supported: {FORMAT_VERSION})")
+        self.version = version
+
+
+class InvariantViolation(TraceIOError):
+    def __init__(self, violations):
+        lines = "; ".join(str(v) for v in violations[:10])
+        more = f" (+{len(violations) - 10} more)" if len(violations) > 10 else ""
+        super().__init__(f"trace violates model invariants: {lines}{more}")
+        self.violations = violations
+
+
+def _errors(types):
+    if types is not None and getattr(types, "root", None):
+        import importlib
+        t = importlib.import_module(types.root + ".traceio")
+        return t.MalformedRecord, t.MissingHeader, t.UnsupportedVersion, t.InvariantViolation
+    return MalformedRecord, MissingHeader, UnsupportedVersion, InvariantViolation
+
+
+# ------------------------------------------------------------------------ native path
+class _Ingest(ctypes.Structure):
+    _P = ctypes.c_void_p
+    _fields_ = [("err_line", ctypes.c_uint64), ("header_line", ctypes.c_uint64), ("version", ctypes.c_uint64),
+                ("num_devices", ctypes.c_uint64), ("host_device", ctypes.c_uint64), ("wall_time_ns", ctypes.c_uint64),
+                ("has_wall", ctypes.c_int32), ("n_events", ctypes.c_uint64),
+                ("seq", _P), ("start_ns", _P), ("end_ns", _P), ("src_device", _P), ("dst_device", _P),
+                ("src_addr", _P), ("dst_addr", _P), ("bytes", _P), ("hash", _P), ("kind", _P), ("loc", _P),
+                ("n_locs", ctypes.c_uint32), ("loc_codeptr", _P), ("loc_line", _P), ("loc_file_off", _P),
+                ("loc_file_len", _P), ("strings", _P)]
+
+
+def _as_bytes(data):
+    if hasattr(data, "read"):
+        data = data.read()
+    if isinstance(data, str):
+        return data.encode("utf-8"), data
+    data = bytes(data)
+    return data, None
+
+
+def _copy(ptr, n, dtype):
+    if not n or not ptr:
+        return np.zeros(0, dtype=dtype)
+    buf = (ctypes.c_char * (int(n) * np.dtype(dtype).itemsize)).from_address(ptr)
+    return np.frombuffer(buf, dtype=dtype).copy()
+
+
+def _native(raw: bytes, threads: int):
+    L = _lib.lib()
+    L.b2l_ingest_ndjson.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int,
+                                    ctypes.POINTER(ctypes.POINTER(_Ingest))]
+    L.b2l_ingest_ndjson.restype = ctypes.c_int
+    L.b2l_ingest_free.argtypes = [ctypes.POINTER(_Ingest)]
+    out = ctypes.POINTER(_Ingest)()
+    _lib.check(L.b2l_ingest_ndjson(raw, len(raw), threads, ctypes.byref(out)), "b2l_ingest_ndjson")
+    try:
+        g = out.contents
+        if g.err_line:
+            return None
+        n = int(g.n_events)
+        cols = {f: _copy(getattr(g, f), n, np.uint64) for f in
+                ("seq", "start_ns", "end_ns", "src_device", "dst_device", "src_addr", "dst_addr", "bytes", "hash")}
+        cols["kind"] = _copy(g.kind, n, np.uint8)
+        cols["loc"] = _copy(g.loc, n, np.uint32)
+        nl = int(g.n_locs)
+        cp = _copy(g.loc_codeptr, nl, np.uint64)
+        ln = _copy(g.loc_line, nl, np.int64)
+        off = _copy(g.loc_file_off, nl, np.uint64)
+        flen = _copy(g.loc_file_len, nl, np.uint32)
+        strings = b""
+        total = int(max((int(o) + int(fl) for o, fl in zip(off, flen) if o != U64_MAX), default=0))
+        if total:
+            strings = ctypes.string_at(g.strings, total)
+        locs = []
+        for k in range(nl):
+            f = None if off[k] == U64_MAX else strings[int(off[k]):int(off[k]) + int(flen[k])].decode("utf-8")
+            locs.append((int(cp[k]), f, None if ln[k] < 0 else int(ln[k])))
+        header = (int(g.version), int(g.num_devices), int(g.host_device),
+                  int(g.wall_time_ns) if g.has_wall else None)
+        return header, cols, locs
+    finally:
+        L.b2l_ingest_free(out)
+
+
+def _sort_perm(t0: np.ndarray, seq: np.ndarray) -> Optional[np.ndarray]:
+    """Permutation sorting events by (t0, seq) (traceio.py:183), or None if already sorted."""
+    n = t0.size
+    if n < 2:
+        return None
+    d0 = t0[1:] >= t0[:-1]
+    if np.all(d0 & ((t0[1:] > t0[:-1]) | (seq[1:] >= seq[:-1]))):
+        return None
+    perm = np.zeros(n, dtype=np.uint32)
+    L = _lib.lib()
+    L.b2l_sort_u64_pairs.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_uint64] + [ctypes.c_void_p]
+    L.b2l_sort_u64_pairs.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
+    a, b = np.ascontiguousarray(t0), np.ascontiguousarray(seq)
+    _lib.check(L.b2l_sort_u64_pairs(a.ctypes.data, b.ctypes.data, n, perm.ctypes.data), "b2l_sort_u64_pairs")
+    return perm
+
+
+_Ev = namedtuple("_Ev", "seq start_ns end_ns src_device dst_device loc")
+_Lc = namedtuple("_Lc", "line")
+
+
+def _to_columns(header, cols, locs) -> Columns:
+    version, nd, host, wall = header
+    perm = _sort_perm(cols["start_ns"], cols["seq"])
+    if perm is not None:
+        cols = {k: v[perm] for k, v in cols.items()}
+    n = cols["seq"].size
+    if wall is None:  # derived once at parse time (traceio.py:185-186)
+        wall = int(cols["end_ns"].max() - cols["start_ns"].min()) if n else 0
+    flags, bucket_of, bucket_ids, bucket_keys = [], [], {}, []
+    for cp, f, ln in locs:
+        fl = (LOC_FILE_NO_LINE if (f is not None and ln is None) else 0) | (
+            LOC_LINE_NONPOS if (ln is not None and ln <= 0) else 0)
+        flags.append(fl)
+        bk = loc_key(cp, f, ln)
+        if bk not in bucket_ids:
+            bucket_ids[bk] = len(bucket_keys)
+            bucket_keys.append(bk)
+        bucket_of.append(bucket_ids[bk])
+    return Columns(n=n, num_devices_total=nd, host_device=host, seq=cols["seq"], start_ns=cols["start_ns"],
+                   end_ns=cols["end_ns"], src_addr=cols["src_addr"], dst_addr=cols["dst_addr"], bytes=cols["bytes"],
+                   hash=cols["hash"], src_device=cols["src_device"].astype(np.int32),
+                   dst_device=cols["dst_device"].astype(np.int32), kind=cols["kind"], loc=cols["loc"],
+                   loc_flags=np.array(flags or [0], dtype=np.uint8), loc_bucket=np.array(bucket_of or [0], np.uint32),
+                   n_buckets=max(len(bucket_keys), 1), bucket_keys=bucket_keys or [(1, "", 0)], wall_time_ns=wall,
+                   locs=locs or [(0, None, None)])
+
+
+def _validate_columns(c: Columns, types):
+    """GPU validation of parsed columns -> violations (model.py:125-200 messages)."""
+    T = family(types.root) if types is not None and getattr(types, "root", None) else family(None)
+    V = T.Violation
+    out = []
+    if c.num_devices_total < 1:
+        out.append(V("header", f"num_devices_total={c.num_devices_total} must be positive"))
+    if not 0 <= c.host_device < max(c.num_devices_total, 1):
+        out.append(V("header", f"host_device={c.host_device} out of range"))
+    try:
+        analyze_columns(c, flags=FLAG_VALIDATE_ONLY)
+    except EngineInvalid as exc:
+        for i, m in zip(exc.bad_index.tolist(), exc.bad_rules.tolist()):
+            loc = c.locs[int(c.loc[i])]
+            e = _Ev(int(c.seq[i]), int(c.start_ns[i]), int(c.end_ns[i]), int(c.src_device[i]),
+                    int(c.dst_device[i]), _Lc(loc[2]))
+            for bit, rule, text in _RULE_TEXT:
+                if m & bit:
+                    out.append(V(rule, text(e, c.num_devices_total), e.seq))
+    return out
+
+
+def parse_trace_columns(data, threads: Optional[int] = None, types=None) -> Columns:
+    """Parse + sort + validate into device-ready columns (no per-event Python objects)."""
+    raw, text = _as_bytes(data)
+    if text is None:
+        text = raw.decode("utf-8")  # the reference decodes first (UnicodeDecodeError as it does)
+    threads = threads or min(32, os.cpu_count() or 1)
+    got = _native(raw, threads)
+    header_ok = got is not None and got[0][1] <= I32_MAX and got[0][2] <= I32_MAX
+    if not header_ok or got is None or (got[1]["src_device"].size and (
+            got[1]["src_device"].max() > I32_MAX or got[1]["dst_device"].max() > I32_MAX)):
+        from .columns import to_columns
+        return to_columns(_parse_exact(text, types))
+    c = _to_columns(*got)
+    viol = _validate_columns(c, types)
+    if viol:
+        raise _errors(types)[3](viol)
+    return c
+
+
+def parse_trace(data, types=None, threads: Optional[int] = None):
+    """Drop-in for dmlens.traceio.parse_trace; ``types=family("dmlens")`` returns dmlens objects."""
+    raw, text = _as_bytes(data)
+    if text is None:
+        text = raw.decode("utf-8")
+    T = types or family(None)
+    threads = threads or min(32, os.cpu_count() or 1)
+    got = _native(raw, threads)
+    if got is None or got[0][1] > I32_MAX or got[0][2] > I32_MAX or (got[1]["src_device"].size and (
+            got[1]["src_device"].max() > I32_MAX or got[1]["dst_device"].max() > I32_MAX)):
+        return _parse_exact(text, types)
+    c = _to_columns(*got)
+    viol = _validate_columns(c, types)
+    if viol:
+        raise _errors(types)[3](viol)
+    locs = [T.CodeLocation(codeptr=cp, file=f, line=ln) for cp, f, ln in c.locs]
+    kinds = [T.EventKind(k) for k in _KINDS]
+    L = lambda a: a.tolist()  # noqa: E731
+    ev = [T.TraceEvent(q, kinds[k], a, b, s, d, sa, da, nb, h, locs[lo]) for q, k, a, b, s, d, sa, da, nb, h, lo in zip(
+        L(c.seq), L(c.kind), L(c.start_ns), L(c.end_ns), L(c.src_device), L(c.dst_device), L(c.src_addr),
+        L(c.dst_addr), L(c.bytes), L(c.hash), L(c.loc))]
+    return T.Trace(version=got[0][0], num_devices_total=c.num_devices_total, host_device=c.host_device,
+                   wall_time_ns=c.wall_time_ns, events=ev)
+
+
+def load_trace_file(path, types=None):
+    with open(path, "rb") as fh:
+        return parse_trace(fh.read(), types=types)
+
+
+# ------------------------------------------------------------------------ exact path (traceio.py:78-191)
+def _u64(obj, key, line_no, E):
+    value = obj[key]
+    if isinstance(value, bool) or not isinstance(value, int):
+        raise E(line_no, f'field "{key}" must be an integer, got {value!r}')
+    if not 0 <= value <= U64_MAX:
+        raise E(line_no, f'field "{key}"={value} outside 64-bit unsigned range')
+    return value
+
+
+def _parse_exact(text: str, types=None):
+    """Line-by-line restatement of the reference parser: raises its exact exceptions."""
+    T = types or family(None)
+    Malformed, Missing, Unsupported, Invariant = _errors(types)
+    trace, events, cache = None, [], {}
+    for line_no, raw in enumerate(text.split("\n"), start=1):
+        line = raw.strip()
+        if not line or line.startswith("#"):
+            continue
+        try:
+            obj = json.loads(line)
+        except json.JSONDecodeError as exc:
+            raise Malformed(line_no, f"invalid JSON: {exc.msg}") from exc
+        if not isinstance(obj, dict):
+            raise Malformed(line_no, "record is not a JSON object")
+        if trace is None:
+            if "dmlens" not in obj:
+                raise Missing()
+            version = obj["dmlens"]
+            if version != FORMAT_VERSION:
+                raise Unsupported(version)
+            nd = _u64(obj, "num_devices", line_no, Malformed)
+            host = _u64(obj, "host_device", line_no, Malformed)
+            wall = _u64(obj, "wall_time_ns", line_no, Malformed) if "wall_time_ns" in obj else None
+            trace = T.Trace(version=version, num_devices_total=nd, host_device=host, wall_time_ns=wall, events=[])
+            continue
+        for key in _REQUIRED:
+            if key not in obj:
+                raise Malformed(line_no, f'missing required field "{key}"')
+        kind_str = obj["kind"]
+        if kind_str not in _KINDS or not isinstance(kind_str, str):
+            raise Malformed(line_no, f"unknown event kind {kind_str!r}")
+        t0 = _u64(obj, "t0", line_no, Malformed)
+        t1 = _u64(obj, "t1", line_no, Malformed)
+        if t1 < t0:
+            raise Malformed(line_no, f"event interval inverted (t1 {t1} < t0 {t0})")
+        file, ln = obj.get("file"), obj.get("line")
+        if file is not None and not isinstance(file, str):
+            raise Malformed(line_no, f'field "file" must be a string, got {file!r}')
+        if ln is not None and (isinstance(ln, bool) or not isinstance(ln, int) or ln <= 0):
+            raise Malformed(line_no, f'field "line" must be a positive integer, got {ln!r}')
+        if file is not None and ln is None:
+            raise Malformed(line_no, 'field "file" present without "line"')
+        codeptr = _u64(obj, "codeptr", line_no, Malformed)
+        key = (codeptr, file, ln)
+        loc = cache.get(key)
+        if loc is None:
+            loc = cache[key] = T.CodeLocation(codeptr=codeptr, file=file, line=ln)
+        events.append(T.TraceEvent(
+            seq=_u64(obj, "seq", line_no, Malformed), kind=T.EventKind(kind_str), start_ns=t0, end_ns=t1,
+            src_device=_u64(obj, "src_dev", line_no, Malformed), dst_device=_u64(obj, "dst_dev", line_no, Malformed),
+            src_addr=_u64(obj, "src_addr", line_no, Malformed), dst_addr=_u64(obj, "dst_addr", line_no, Malformed),
+            bytes=_u64(obj, "bytes", line_no, Malformed), hash=_u64(obj, "hash", line_no, Malformed), loc=loc))
+    if trace is None:
+        raise Missing("empty input: no header line found")
+    events.sort(key=lambda e: (e.start_ns, e.seq))
+    trace.events = events
+    if trace.wall_time_ns is None:
+        trace.wall_time_ns = trace.wall_time()
+    from .standalone import validate
+    violations = validate(trace)
+    if violations:
+        raise Invariant(violations)
+    return trace

@@ -163,7 +163,7 @@ _OWN = SimpleNamespace(
     EventKind=EventKind, CodeLocation=CodeLocation, TraceEvent=TraceEvent, Trace=Trace, Violation=Violation,
     AllocPair=AllocPair, PrepWarning=PrepWarning, DuplicateGroup=DuplicateGroup, RoundTripGroup=RoundTripGroup,
     RepeatedAllocGroup=RepeatedAllocGroup, Findings=Findings, SavingsEstimate=SavingsEstimate,
-    AttributedIssue=AttributedIssue, InvalidTrace=None, FindingsTraceMismatch=None)
+    AttributedIssue=AttributedIssue, InvalidTrace=None, FindingsTraceMismatch=None, root=None)
 
 
 def type_family(obj) -> SimpleNamespace:
@@ -172,23 +172,24 @@ def type_family(obj) -> SimpleNamespace:
     isinstance() checks in reference code keep working; ours otherwise."""
     mod = type(obj).__module__
     if mod.startswith("dmlens"):
-        root = mod.split(".")[0]
-        m = sys.modules.get(root + ".model")
-        d = sys.modules.get(root + ".detectors")
-        p = sys.modules.get(root + ".prep")
-        if m is None or d is None or p is None:
-            import importlib
-            m = importlib.import_module(root + ".model")
-            d = importlib.import_module(root + ".detectors")
-            p = importlib.import_module(root + ".prep")
-        import importlib
-        e = importlib.import_module(root + ".estimator")
-        r = importlib.import_module(root + ".report")
-        return SimpleNamespace(
-            EventKind=m.EventKind, CodeLocation=m.CodeLocation, TraceEvent=m.TraceEvent, Trace=m.Trace,
-            Violation=m.Violation, AllocPair=p.AllocPair, PrepWarning=p.PrepWarning,
-            DuplicateGroup=d.DuplicateGroup, RoundTripGroup=d.RoundTripGroup,
-            RepeatedAllocGroup=d.RepeatedAllocGroup, Findings=d.Findings, SavingsEstimate=e.SavingsEstimate,
-            AttributedIssue=r.AttributedIssue, InvalidTrace=d.InvalidTrace,
-            FindingsTraceMismatch=e.FindingsTraceMismatch)
+        return family(mod.split(".")[0])
     return _OWN
+
+
+def family(root: str = None) -> SimpleNamespace:
+    """Class family by package name: None -> ours, "dmlens" -> the reference's."""
+    if root is None:
+        return _OWN
+    import importlib
+    m = importlib.import_module(root + ".model")
+    d = importlib.import_module(root + ".detectors")
+    p = importlib.import_module(root + ".prep")
+    e = importlib.import_module(root + ".estimator")
+    r = importlib.import_module(root + ".report")
+    return SimpleNamespace(
+        EventKind=m.EventKind, CodeLocation=m.CodeLocation, TraceEvent=m.TraceEvent, Trace=m.Trace,
+        Violation=m.Violation, AllocPair=p.AllocPair, PrepWarning=p.PrepWarning,
+        DuplicateGroup=d.DuplicateGroup, RoundTripGroup=d.RoundTripGroup,
+        RepeatedAllocGroup=d.RepeatedAllocGroup, Findings=d.Findings, SavingsEstimate=e.SavingsEstimate,
+        AttributedIssue=r.AttributedIssue, InvalidTrace=d.InvalidTrace,
+        FindingsTraceMismatch=e.FindingsTraceMismatch, root=root)

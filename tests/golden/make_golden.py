@@ -50,7 +50,7 @@ def hash_fixture():
     return out
 
 
-if __name__ == "__main__" and "--analysis" not in sys.argv and "--standalone" not in sys.argv:
+if __name__ == "__main__" and not set(sys.argv) & {"--analysis", "--standalone", "--ingest"}:
     with open(os.path.join(HERE, "hash_vectors.json"), "w") as f:
         json.dump(hash_fixture(), f, indent=0)
     print("wrote hash_vectors.json")
@@ -206,3 +206,81 @@ if __name__ == "__main__" and "--standalone" in sys.argv:
     with gzip.open(os.path.join(HERE, "standalone_cases.json.gz"), "wt") as f:
         json.dump(standalone_fixture(), f)
     print("wrote standalone_cases.json.gz")
+
+
+# ----------------------------------------------------------------------------- NDJSON ingest
+def ingest_fixture():
+    import importlib.util
+    import random as _r
+    spec = importlib.util.spec_from_file_location("ref_conftest", os.path.join(os.path.dirname(REF), "tests",
+                                                                               "conftest.py"))
+    conf = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(conf)
+    from dmlens.traceio import parse_trace, serialize_trace
+    H = '{"dmlens":1,"num_devices":2,"host_device":0,"wall_time_ns":100}'
+    E = ('{"seq":0,"kind":"transfer","t0":0,"t1":10,"src_dev":0,"dst_dev":1,'
+         '"src_addr":1,"dst_addr":2,"bytes":8,"hash":7,"codeptr":0}')
+    texts = []
+    for seed in range(40):
+        tr = conf.random_trace(seed)
+        lines = serialize_trace(tr).decode().split("\n")
+        body = lines[1:-1]
+        _r.Random(seed).shuffle(body)  # any order in the file; parse re-sorts by (t0, seq)
+        texts.append(("random%d" % seed, "\n".join([lines[0]] + body) + "\n"))
+    odd = [
+        ("crlf-comments-blank", "# c\r\n\r\n" + H + "\r\n\r\n# x\r\n" + E + "\r\n"),
+        ("spaces-unicode-escape", H + "\n" + E.replace('"codeptr":0', ' "codeptr" : 0 , "file":"k\\u00e9rnel\\n.c","line":3 ')),
+        ("unknown-nested", H + "\n" + E.replace('"codeptr":0', '"codeptr":0,"extra":{"a":[1,2.5,{"b":null}],"c":"x"}')),
+        ("duplicate-key-last-wins", H + "\n" + E.replace('"hash":7', '"hash":5,"hash":7')),
+        ("minus-zero", H + "\n" + E.replace('"bytes":8', '"bytes":-0')),
+        ("float-in-unknown", H + "\n" + E.replace('"codeptr":0', '"codeptr":0,"ratio":1.5e3')),
+        ("nbsp-stripped", " " + H + "\n" + E),
+        ("line-huge", H + "\n" + E.replace('"codeptr":0', '"codeptr":0,"file":"a.c","line":%d' % (2**70))),
+        ("null-file-line", H + "\n" + E.replace('"codeptr":0', '"codeptr":0,"file":null,"line":null')),
+        ("no-wall", '{"dmlens":1,"num_devices":3,"host_device":1}\n' + E.replace('"dst_dev":1', '"dst_dev":2')),
+        ("header-true-version", '{"dmlens":true,"num_devices":2,"host_device":0}\n'),
+        ("bad-json-trailing", H + "\n" + E + " x\n"),
+        ("bad-leading-zero", H + "\n" + E.replace('"bytes":8', '"bytes":08')),
+        ("nan-value", H + "\n" + E.replace('"hash":7', '"hash":NaN')),
+        ("control-char", H + "\n" + E.replace('"codeptr":0', '"codeptr":0,"file":"a\tb","line":1')),
+        ("kind-escaped", H + "\n" + E.replace('"transfer"', '"transf\\u0065r"')),
+        ("second-header", H + "\n" + H + "\n"),
+        ("array-record", H + "\n[1,2,3]\n"),
+        ("device-huge", H + "\n" + E.replace('"dst_dev":1', '"dst_dev":%d' % (2**40))),
+    ]
+    mut = [
+        ("missing-seq", lambda o: o.pop("seq")), ("kind-warp", lambda o: o.update(kind="warp")),
+        ("inverted", lambda o: o.update(t0=50, t1=5)), ("neg-bytes", lambda o: o.update(bytes=-4)),
+        ("big-bytes", lambda o: o.update(bytes=2**64)), ("str-hash", lambda o: o.update(hash="abc")),
+        ("float-hash", lambda o: o.update(hash=1.5)), ("bool-hash", lambda o: o.update(hash=True)),
+        ("file-no-line", lambda o: o.update(file="a.c")), ("file-int", lambda o: o.update(file=9, line=1)),
+        ("line-zero", lambda o: o.update(file="a.c", line=0)), ("kind-int", lambda o: o.update(kind=3)),
+    ]
+    for name, m in mut:
+        o = json.loads(E)
+        m(o)
+        texts.append(("mut-" + name, H + "\n" + json.dumps(o)))
+    corpus = [
+        ("empty-file", ""), ("comment-only", "# nothing here\n"), ("event-before-header", E + "\n"),
+        ("bad-version", '{"dmlens":3,"num_devices":2,"host_device":0}\n'), ("header-not-json", '{"dmlens":1,,}\n'),
+        ("event-not-json", H + "\n{not json}\n"), ("event-not-object", H + "\n42\n"),
+        ("hashless-transfer", H + "\n" + E.replace('"hash":7', '"hash":0') + "\n"),
+        ("duplicate-seq", H + "\n" + E + "\n" + E.replace('"t0":0,"t1":10', '"t0":20,"t1":30') + "\n"),
+        ("bad-host-device", '{"dmlens":1,"num_devices":2,"host_device":5}\n'),
+    ]
+    out = []
+    for name, text in texts + odd + corpus:
+        rec = {"name": name, "text": text}
+        try:
+            tr = parse_trace(text)
+            rec["trace"] = _trace_json(tr)
+        except Exception as exc:  # noqa: BLE001 - record the reference's exact exception
+            rec["error"] = [type(exc).__name__, str(exc)]
+        out.append(rec)
+    return out
+
+
+if __name__ == "__main__" and "--ingest" in sys.argv:
+    with open(os.path.join(HERE, "ingest_cases.json"), "w") as f:
+        json.dump(ingest_fixture(), f)
+    print("wrote ingest_cases.json")

@@ -1,0 +1,83 @@
+"""Native NDJSON ingest vs the reference's parse_trace outputs (golden).
+CPU: the C++ parser's columns / rejection points and the exact-path errors.
+GPU: the full parse_trace drop-in (GPU sort + validation) on every fixture."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2601_12713_b200 import ingest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CASES = json.load(open(os.path.join(HERE, "golden", "ingest_cases.json")))
+
+
+def _events_json(cols_or_none):
+    return cols_or_none
+
+
+def test_native_parser_columns_match_reference_order_free():
+    accepted = 0
+    for c in CASES:
+        got = ingest._native(c["text"].encode("utf-8"), threads=3)
+        if got is None:
+            continue
+        accepted += 1
+        assert "trace" in c or c["error"][0] == "InvariantViolation", c["name"]
+        if "trace" not in c:
+            continue
+        header, cols, locs = got
+        tj = c["trace"]
+        assert header[1:3] == (tj["num_devices_total"], tj["host_device"]), c["name"]
+        order = np.lexsort((cols["seq"], cols["start_ns"]))
+        rows = []
+        for i in order.tolist():
+            cp, f, ln = locs[int(cols["loc"][i])]
+            rows.append([int(cols["seq"][i]), ingest._KINDS[int(cols["kind"][i])], int(cols["start_ns"][i]),
+                         int(cols["end_ns"][i]), int(cols["src_device"][i]), int(cols["dst_device"][i]),
+                         int(cols["src_addr"][i]), int(cols["dst_addr"][i]), int(cols["bytes"][i]),
+                         str(int(cols["hash"][i])), cp, f, ln])
+        assert rows == tj["events"], c["name"]
+    assert accepted >= 45  # every serialized random trace and the plain odd cases take the native path
+
+
+def test_native_parser_multithreaded_large_input():
+    lines = ['{"dmlens":1,"num_devices":3,"host_device":0}']
+    for i in range(200_000):
+        lines.append('{"seq":%d,"kind":"kernel","t0":%d,"t1":%d,"src_dev":1,"dst_dev":1,"src_addr":0,'
+                     '"dst_addr":0,"bytes":0,"hash":0,"codeptr":%d}' % (i, 10 * i, 10 * i + 5, i % 7))
+    raw = ("\n".join(lines) + "\n").encode()
+    header, cols, locs = ingest._native(raw, threads=8)
+    assert cols["seq"].size == 200_000 and np.array_equal(cols["seq"], np.arange(200_000, dtype=np.uint64))
+    assert len(locs) == 7
+    bad = raw.replace(b'"seq":123456,', b'"seq":123456,,')
+    from paper_2601_12713_b200 import _lib
+    assert ingest._native(bad, threads=8) is None
+    del _lib
+
+
+def test_exact_path_errors_match_reference():
+    for c in CASES:
+        if "error" not in c or c["error"][0] == "InvariantViolation":
+            continue
+        with pytest.raises(ingest.TraceIOError) as ei:
+            ingest._parse_exact(c["text"])
+        assert [type(ei.value).__name__, str(ei.value)] == c["error"], c["name"]
+
+
+@pytest.mark.gpu
+def test_parse_trace_drop_in_matches_reference(cuda):
+    from tests._cases import trace_from_json
+    for c in CASES:
+        if "error" in c:
+            with pytest.raises(ingest.TraceIOError) as ei:
+                ingest.parse_trace(c["text"])
+            assert [type(ei.value).__name__, str(ei.value)] == c["error"], c["name"]
+        else:
+            got = ingest.parse_trace(c["text"])
+            want = trace_from_json(c["trace"])
+            assert got.events == want.events and got.wall_time_ns == want.wall_time_ns, c["name"]
+            assert (got.num_devices_total, got.host_device) == (want.num_devices_total, want.host_device)
+            cols = ingest.parse_trace_columns(c["text"])
+            assert [int(x) for x in cols.seq] == [e.seq for e in want.events], c["name"]

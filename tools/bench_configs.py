@@ -123,11 +123,34 @@ def c5s(args):
     print(json.dumps(analysis_line("C5-single-GPU-slice", c2_trace(args.c5_events, seed=5), iters=2)), flush=True)
 
 
+def ingest_cfg(args):
+    """NDJSON -> validated columns (native parser + GPU sort/validate) on the C2 1M-event trace."""
+    from paper_2601_12713_b200.ingest import parse_trace_columns
+    c = c2_trace(1_000_000, seed=2)
+    kinds = ["transfer", "alloc", "delete", "kernel"]
+    L = lambda a: a.tolist()  # noqa: E731
+    lines = ['{"dmlens":1,"num_devices":%d,"host_device":%d}' % (c.num_devices_total, c.host_device)]
+    for q, k, a, b, s_, d, sa, da, nb, h in zip(L(c.seq), L(c.kind), L(c.start_ns), L(c.end_ns), L(c.src_device),
+                                                 L(c.dst_device), L(c.src_addr), L(c.dst_addr), L(c.bytes),
+                                                 L(c.hash)):
+        lines.append('{"seq":%d,"kind":"%s","t0":%d,"t1":%d,"src_dev":%d,"dst_dev":%d,"src_addr":%d,'
+                     '"dst_addr":%d,"bytes":%d,"hash":%d,"codeptr":0}' % (q, kinds[k], a, b, s_, d, sa, da, nb, h))
+    raw = ("\n".join(lines) + "\n").encode()
+    parse_trace_columns(raw)
+    t = time.perf_counter()
+    for _ in range(3):
+        cols = parse_trace_columns(raw)
+    dt = (time.perf_counter() - t) / 3
+    print(json.dumps({"config": "ingest-C2", "metric": "M events/s parsed (NDJSON -> sorted, validated columns)",
+                      "events": cols.n, "bytes": len(raw), "value": round(cols.n / dt / 1e6, 2),
+                      "ms_per_step": round(dt * 1e3, 1), "threads": min(32, os.cpu_count() or 1)}), flush=True)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="c1,c3,c4,c5s")
+    ap.add_argument("--configs", default="c1,c3,c4,c5s,ingest")
     ap.add_argument("--c3-buffers", type=int, default=8)
     ap.add_argument("--c5-events", type=int, default=100_000_000)
     a = ap.parse_args()
     for c in a.configs.split(","):
-        globals()[c](a)
+        globals()["ingest_cfg" if c == "ingest" else c](a)
