@@ -21,15 +21,33 @@ namespace b2l {
 namespace k2 {
 
 constexpr int THREADS = 256;
-constexpr int WPT = 32;                   // words per thread (kept in registers for all 16 groups)
-constexpr int CHUNK = THREADS * WPT;      // words per CTA per round
+constexpr int WPT = 64;                   // words per thread: payload words in smem, R_i in registers
+constexpr int CHUNK = THREADS * WPT;      // words per CTA per round (128 KiB)
 constexpr size_t SMEM = (size_t)THREADS * (WPT + 1) * sizeof(uint64_t);
 
+// Look-back slots: a map is 16 bytes whose entries use only the low nibble, so the high
+// nibble of byte 0 marks a published slot and map + mark travel in one 16-byte access.
 struct Status {
-    unsigned long long flag;  // 0 empty, 1 aggregate published, 2 inclusive prefix published
-    uint4 agg;                // this CTA's map (never changes once flag >= 1)
-    uint4 incl;               // maps of CTAs 0..c of the round (valid once flag == 2)
+    uint4 agg;   // this CTA's map, marked 0x10 once published
+    uint4 incl;  // maps of CTAs 0..c of the round, marked 0x10 once published
 };
+constexpr uint32_t MARK = 0x10u;
+__device__ __forceinline__ uint4 ld_slot(const uint4 *p) {
+    uint4 v;
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_slot(uint4 *p, uint4 v) {
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x | MARK), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 unmark(uint4 v) {
+    v.x &= 0x0F0F0F0Fu;
+    return v;
+}
 
 // A map {0..15} -> {0..15} as 16 bytes (entry j = byte j): byte-parallel arithmetic never
 // carries across bytes here, and composition is a byte gather done with PRMT.
@@ -102,14 +120,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__res
     const uint64_t nw = (nbytes + 7) >> 3;
     const uint64_t nchunks = (nw + CHUNK - 1) / CHUNK;
     const uint64_t rounds = (nchunks + G - 1) / G;
-    volatile Status *vst = status;
     volatile unsigned long long *vcarry = carry;
 
     for (uint64_t r = 0; r < rounds; ++r) {
         const uint64_t q = r * G + c;
         if (q >= nchunks) break;  // only the last round has idle CTAs, and nobody waits on them
         const uint64_t last_in_round = (nchunks - r * G < G ? nchunks - r * G : G) - 1;
-        uint64_t w[WPT], R[WPT];
+        uint64_t R[WPT];
         const uint64_t base = q * CHUNK;
         for (int idx = t; idx < CHUNK; idx += THREADS) {
             const uint64_t i = base + idx;
@@ -117,18 +134,27 @@ __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__res
         }
         __syncthreads();
 #pragma unroll
-        for (int j = 0; j < WPT; ++j) w[j] = stage[t * (WPT + 1) + j], R[j] = 0;
+        for (int j = 0; j < WPT; ++j) R[j] = 0;
+        const uint64_t *w = stage + t * (WPT + 1);  // this thread's words, resident for the round
         const int64_t left = (int64_t)nw - (int64_t)(base + (uint64_t)t * WPT);
         const int nv = left <= 0 ? 0 : (left >= WPT ? WPT : (int)left);
-        __syncthreads();
         for (int g = 0; g < 16; ++g) {
             const int k = 4 * g;
             const uint64_t slot = r * 16 + g;
-            // ---- pass A: this thread's map over its words
-            Tab T = tab_id();
+            // ---- pass A: this thread's map over its words, as four independent quarter chains (ILP)
+            constexpr int Q = WPT / 4;
+            Tab Tq[4] = {tab_id(), tab_id(), tab_id(), tab_id()};
 #pragma unroll
-            for (int j = 0; j < WPT; ++j)
-                if (j < nv) tab_step(T, (uint32_t)(w[j] >> k) & 15u, (uint32_t)(R[j] >> k) & 15u);
+            for (int j = 0; j < Q; ++j) {
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int jj = h * Q + j;
+                    if (jj < nv) tab_step(Tq[h], (uint32_t)(w[jj] >> k) & 15u, (uint32_t)(R[jj] >> k) & 15u);
+                }
+            }
+            const Tab T01 = tab_compose(Tq[0], Tq[1]);
+            const Tab T012 = tab_compose(T01, Tq[2]);
+            Tab T = tab_compose(T012, Tq[3]);
             // ---- inclusive prefix composition across the warp (lane order)
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
@@ -150,30 +176,30 @@ __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__res
                 Tab agg;
 #pragma unroll
                 for (int m = 0; m < 4; ++m) agg.r[m] = __shfl_sync(0xffffffffu, W.r[m], THREADS / 32 - 1);
-                uint32_t s_cta = 0;
+                // decoupled look-back (lane 0): publish the aggregate, walk back to the nearest
+                // published inclusive prefix, publish our inclusive prefix
+                Tab P = tab_id();
                 if (lane == 0) {
-                    // publish the aggregate, look back for the round prefix, publish the inclusive map
                     Status *me = status + slot * G + c;
-                    Tab prefix = tab_id();
                     if (c > 0) {
-                        me->agg = tab_pack(agg);
-                        __threadfence();
-                        atomicExch(&me->flag, 1ull);
-                        for (int64_t j = (int64_t)c - 1; j >= 0; --j) {
-                            unsigned long long f;
-                            do {
-                                f = vst[slot * G + j].flag;
-                            } while (f == 0);
-                            __threadfence();
-                            volatile uint4 *src = f == 2 ? &vst[slot * G + j].incl : &vst[slot * G + j].agg;
-                            const uint4 v = make_uint4(src->x, src->y, src->z, src->w);
-                            prefix = tab_compose(tab_unpack(v), prefix);
-                            if (f == 2) break;
+                        st_slot(&me->agg, tab_pack(agg));
+                        for (int64_t j = (int64_t)c - 1; j >= 0;) {
+                            const uint4 inc = ld_slot(&status[slot * G + j].incl);
+                            if (inc.x & MARK) {
+                                P = tab_compose(tab_unpack(unmark(inc)), P);
+                                break;
+                            }
+                            const uint4 ag = ld_slot(&status[slot * G + j].agg);
+                            if (ag.x & MARK) {
+                                P = tab_compose(tab_unpack(unmark(ag)), P);
+                                --j;
+                            }
                         }
                     }
-                    me->incl = tab_pack(tab_compose(prefix, agg));
-                    __threadfence();
-                    atomicExch(&me->flag, 2ull);
+                    st_slot(&me->incl, tab_pack(tab_compose(P, agg)));
+                }
+                uint32_t s_cta = 0;
+                if (lane == 0) {
                     uint32_t s_round;  // the group's state entering this round
                     if (r == 0) {
                         s_round = (uint32_t)(FNV_OFFSET >> k) & 15u;
@@ -184,7 +210,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__res
                         } while (v == 0);
                         s_round = (uint32_t)v & 15u;
                     }
-                    s_cta = tab_apply(prefix, s_round);
+                    s_cta = tab_apply(P, s_round);
                     if (q == r * G + last_in_round) {  // last chunk of the round: carry its output state
                         __threadfence();
                         atomicExch(&carry[slot], 0x100ull | tab_apply(agg, s_cta));
@@ -194,14 +220,20 @@ __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__res
                 if (lane < THREADS / 32) warp_in[lane] = lane == 0 ? s_cta : tab_apply(wexcl, s_cta);
             }
             __syncthreads();
-            // ---- pass B with the actual input state
-            uint32_t s = lane == 0 ? warp_in[warp] : tab_apply(excl_lane, warp_in[warp]);
+            // ---- pass B with the actual input state, the four quarters at once (quarter h's
+            // input is the composed map of the quarters before it applied to the thread's input)
+            const uint32_t sin = lane == 0 ? warp_in[warp] : tab_apply(excl_lane, warp_in[warp]);
+            uint32_t sq[4] = {sin, tab_apply(Tq[0], sin), tab_apply(T01, sin), tab_apply(T012, sin)};
 #pragma unroll
-            for (int j = 0; j < WPT; ++j) {
-                if (j < nv) {
-                    const uint32_t x4 = s ^ ((uint32_t)(w[j] >> k) & 15u);
-                    s = (((uint32_t)(R[j] >> k) & 15u) + 3u * x4) & 15u;
-                    R[j] += ((uint64_t)x4 << k) * FNV_PRIME;
+            for (int j = 0; j < Q; ++j) {
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int jj = h * Q + j;
+                    if (jj < nv) {
+                        const uint32_t x4 = sq[h] ^ ((uint32_t)(w[jj] >> k) & 15u);
+                        sq[h] = (((uint32_t)(R[jj] >> k) & 15u) + 3u * x4) & 15u;
+                        R[jj] += ((uint64_t)x4 << k) * FNV_PRIME;
+                    }
                 }
             }
         }
