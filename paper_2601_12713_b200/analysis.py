@@ -298,25 +298,38 @@ def savings_columns(cols: Columns, cf: ColumnarFindings) -> ColumnarSavings:
         fptr = ctypes.pointer(fs)
     sp = ctypes.POINTER(_Savings)()
     rc = L.b2l_savings_compute(ctypes.byref(cs), fptr, ctypes.byref(sp))
-    try:
-        _lib.check(rc, "b2l_savings_compute")
-        s = sp.contents
-        nb = int(s.n_buckets)
-        per = {c: _u128(s.per_category_ns[k]) for k, c in enumerate(CATEGORIES)}
-        ns = _arr(s.attr_ns, 2 * 5 * nb, np.uint64).reshape(5, nb, 2) if nb else np.zeros((5, 0, 2), np.uint64)
-        by = _arr(s.attr_bytes, 2 * 5 * nb, np.uint64).reshape(5, nb, 2) if nb else np.zeros((5, 0, 2), np.uint64)
-        out = ColumnarSavings(
-            per_category_ns=per, union_ns=_u128(s.union_ns), union_index=_arr(s.union_index, s.n_union, np.uint32),
-            has_overlaps=bool(s.has_overlaps), min_start_ns=int(s.min_start_ns), max_end_ns=int(s.max_end_ns),
-            attr_count=_arr(s.attr_count, 5 * nb, np.uint64).reshape(5, nb),
-            attr_ns=[[int(ns[c, b, 0]) | (int(ns[c, b, 1]) << 64) for b in range(nb)] for c in range(5)],
-            attr_bytes=[[int(by[c, b, 0]) | (int(by[c, b, 1]) << 64) for b in range(nb)] for c in range(5)],
-            attr_first=_arr(s.attr_first, 5 * nb, np.uint64).reshape(5, nb))
-    finally:
-        if sp:
-            L.b2l_savings_free(sp)
+    owner = _SavingsHandle(sp if sp else None)
+    _lib.check(rc, "b2l_savings_compute")
+    s = sp.contents
+    nb = int(s.n_buckets)
+    per = {c: _u128(s.per_category_ns[k]) for k, c in enumerate(CATEGORIES)}
+    ns = _arr(s.attr_ns, 2 * 5 * nb, np.uint64).reshape(5, nb, 2) if nb else np.zeros((5, 0, 2), np.uint64)
+    by = _arr(s.attr_bytes, 2 * 5 * nb, np.uint64).reshape(5, nb, 2) if nb else np.zeros((5, 0, 2), np.uint64)
+    out = ColumnarSavings(
+        per_category_ns=per, union_ns=_u128(s.union_ns),
+        union_index=_view(s.union_index, s.n_union, np.uint32, owner),  # zero-copy (pinned)
+        has_overlaps=bool(s.has_overlaps), min_start_ns=int(s.min_start_ns), max_end_ns=int(s.max_end_ns),
+        attr_count=_arr(s.attr_count, 5 * nb, np.uint64).reshape(5, nb),
+        attr_ns=[[int(ns[c, b, 0]) | (int(ns[c, b, 1]) << 64) for b in range(nb)] for c in range(5)],
+        attr_bytes=[[int(by[c, b, 0]) | (int(by[c, b, 1]) << 64) for b in range(nb)] for c in range(5)],
+        attr_first=_arr(s.attr_first, 5 * nb, np.uint64).reshape(5, nb))
     del keep_c, keep_f
     return out
+
+
+class _SavingsHandle:
+    """Owns a b2l_savings* (its pinned arrays back zero-copy views) until garbage-collected."""
+
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                _L().b2l_savings_free(self.ptr)
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+        self.ptr = None
 
 
 def lookup_seqs(cols: Columns, seqs: np.ndarray) -> np.ndarray:

@@ -1453,6 +1453,8 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
         F.pa = upl(f->pair_alloc, f->n_pairs), F.pd = upl(f->pair_delete, f->n_pairs);
         F.ra_mem = upl(f->ra_pairs, nm_ra), F.ua = upl(f->ua_pairs, f->n_ua), F.ut = upl(f->ut_events, f->n_ut);
     }
+    PhaseClock pc(s);
+    pc.mark("sv-setup");
     // ---- category bits per event
     DBuf<uint8_t> cat(n ? n : 1, s);
     cat.zero();
@@ -1495,6 +1497,7 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
         const uint32_t *ut = F.ut;
         for_each(F.n_ut, [=] __device__(size_t q) { ct[ut[q]] |= 16; }, s);
     }
+    pc.mark("sv-catbits");
     // ---- sums, union, span
     DBuf<unsigned long long> acc(12 + 1 + 2, s);
     acc.zero();
@@ -1517,6 +1520,7 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     // union list
     DBuf<uint32_t> uni(n ? n : 1, s), unic(1, s);
     compact(n, [=] __device__(size_t i) { return ct[i] != 0; }, uni.p, unic.p, s);
+    pc.mark("sv-sums");
     // ---- attribution
     const uint32_t nb = c.nbuckets;
     DBuf<unsigned long long> at(5 * (size_t)nb * 6 + 1, s);
@@ -1538,6 +1542,7 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     launch(ElemPairs{F.ra_mem, F.pa, F.pd}, F.ra_members, 2);
     launch(ElemPairs{F.ua, F.pa, F.pd}, F.n_ua, 3);
     launch(ElemList{F.ut}, F.n_ut, 4);
+    pc.mark("sv-attr");
     // ---- to host
     unsigned long long h[15];
     uint32_t hov = 0, hun = 0;
@@ -1561,6 +1566,7 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     HostSlab *slab = new HostSlab();
     o->internal = slab;
     hb.flush(*slab, s);
+    pc.mark("sv-d2h");
     return B2L_OK;
 }
 

@@ -91,3 +91,40 @@ def test_local_ranks_engine_on_gpu(cuda, g):
             want = analyze_columns(c, strict=strict)
             assert canon_columnar(got, c) == canon_columnar(want, c)
             assert got.warn_index.tolist() == want.warn_index.tolist()
+
+
+def _gloo_engine_worker(rank, world, port, result_path):
+    """Two processes on one GPU: TorchComm over gloo for the exchange, the CUDA engine per shard."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2601_12713_b200 import analyze_columns
+        from paper_2601_12713_b200.synth import c2_trace, c4_trace
+        comm = sharded.TorchComm()
+        ok = True
+        for c in _valid_traces(10, seed0=700) + [c2_trace(50_000, seed=7), c4_trace(50_000, seed=8)]:
+            shard, base = sharded.split(c, world)[rank]
+            got = sharded.analyze_sharded(shard, base, comm)
+            if rank == 0:
+                ok &= canon_columnar(got, c) == canon_columnar(analyze_columns(c), c)
+        if rank == 0:
+            with open(result_path, "w") as f:
+                f.write("ok" if ok else "mismatch")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gloo_two_processes_engine_on_gpu(cuda, tmp_path):
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = tmp_path / "result.txt"
+    mp.spawn(_gloo_engine_worker, args=(2, port, str(out)), nprocs=2, join=True)
+    assert out.read_text() == "ok"
