@@ -50,7 +50,7 @@ def hash_fixture():
     return out
 
 
-if __name__ == "__main__" and not set(sys.argv) & {"--analysis", "--standalone", "--ingest"}:
+if __name__ == "__main__" and not set(sys.argv) & {"--analysis", "--standalone", "--ingest", "--reports"}:
     with open(os.path.join(HERE, "hash_vectors.json"), "w") as f:
         json.dump(hash_fixture(), f, indent=0)
     print("wrote hash_vectors.json")
@@ -284,3 +284,41 @@ if __name__ == "__main__" and "--ingest" in sys.argv:
     with open(os.path.join(HERE, "ingest_cases.json"), "w") as f:
         json.dump(ingest_fixture(), f)
     print("wrote ingest_cases.json")
+
+
+# ----------------------------------------------------------------------------- reports (CLI path)
+def report_fixture():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("ref_conftest", os.path.join(os.path.dirname(REF), "tests",
+                                                                               "conftest.py"))
+    conf = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(conf)
+    from dmlens.cli import _filter_min_bytes
+    from dmlens import analyze, attribute, estimate, render_json, render_text
+    from dmlens.synth import PATTERNS, PatternSpec, generate
+    from dmlens.traceio import serialize_trace
+    traces = [("listing1", generate(PatternSpec(pattern="listing1"))[0])]
+    for pat in PATTERNS:
+        traces.append((f"synth-{pat}", generate(PatternSpec(pattern=pat, n_iterations=3, n_devices=3, seed=5))[0]))
+    for seed in range(20):
+        tr = conf.random_trace(seed)
+        if tr.wall_time_ns is None:
+            tr.wall_time_ns = tr.wall_time()
+        traces.append((f"random{seed}", tr))
+    out = []
+    for name, tr in traces:
+        f = analyze(tr)
+        for mb in (0, 64, 4096):
+            rep = _filter_min_bytes(f, mb)
+            s = estimate(tr, rep)
+            iss = attribute(tr, rep)
+            out.append({"name": name, "min_bytes": mb, "ndjson": serialize_trace(tr).decode(),
+                        "text": render_text(tr, rep, s, iss), "json": render_json(tr, rep, s, iss)})
+    return out
+
+
+if __name__ == "__main__" and "--reports" in sys.argv:
+    import gzip
+    with gzip.open(os.path.join(HERE, "report_cases.json.gz"), "wt") as f:
+        json.dump(report_fixture(), f)
+    print("wrote report_cases.json.gz")
