@@ -83,7 +83,6 @@ def validate(trace):
 # ------------------------------------------------------------------------ pairs (prep.py)
 def _pairs_from(data_op_events, T, warn, extra_rows=(), ndev=None, flags=FLAG_SKIP_DDRT):
     rows = [(e, _kind(e) if _kind(e) in (ALLOC, DELETE) else TRANSFER) for e in data_op_events]
-    base = len(rows)
     rows += list(extra_rows)
     order = np.argsort(np.fromiter((e.start_ns for e, _ in rows), dtype=np.uint64, count=len(rows)),
                        kind="stable") if extra_rows else np.arange(len(rows))
@@ -105,7 +104,6 @@ def _pairs_from(data_op_events, T, warn, extra_rows=(), ndev=None, flags=FLAG_SK
             pairs.append(T.AllocPair(al, syn, synthetic_delete=True))
         else:
             pairs.append(T.AllocPair(al, ev[d]))
-    del base
     return cf, ev, pairs
 
 
