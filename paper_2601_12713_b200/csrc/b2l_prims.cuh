@@ -333,8 +333,6 @@ struct StoreExclU32 {
 
 // ---------------------------------------------------------------- radix sort
 constexpr int RS_THREADS = 256;
-constexpr int RS_ROUNDS = 8;
-constexpr int RS_TILE = RS_THREADS * RS_ROUNDS;
 
 template <int KW>
 struct KeyCols {
@@ -387,68 +385,99 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_hist_all(KeyCols<KW> k, si
 // One LSD pass, Onesweep style: tiles take ids in launch order, rank their keys stably
 // (warp multisplit), publish per-digit tile counts, and resolve the exclusive prefix of
 // every digit across preceding tiles by decoupled look-back -- one launch per pass.
+// The tile is then reordered by digit in shared memory and written out run by run, so
+// each warp store covers consecutive addresses of one digit's output range (coalesced),
+// one key word at a time through a 32 KB staging buffer.
 constexpr uint32_t LB_AGG = 1u << 30, LB_INC = 2u << 30, LB_VAL = (1u << 30) - 1;
+constexpr int OS_THREADS = 256;
+constexpr int OS_WARPS = OS_THREADS / 32;
+constexpr int OS_ITEMS = 16;
+constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096 records per tile
+
+// Exclusive scan of one u32 per thread across a 256-thread block (warp shuffles + one
+// cross-warp step).  `wsum` is OS_WARPS words of shared scratch.  Returns the block total.
+__device__ __forceinline__ uint32_t block256_excl(uint32_t v, uint32_t *wsum, uint32_t &total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    uint32_t before = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < OS_WARPS; ++w) {
+        const uint32_t c = wsum[w];
+        before += w < warp ? c : 0u;
+        tot += c;
+    }
+    total = tot;
+    return before + x - v;
+}
 
 template <int KW>
-__global__ void __launch_bounds__(RS_THREADS) k_onesweep(KeyCols<KW> in, const uint32_t *__restrict__ vin,
+__global__ void __launch_bounds__(OS_THREADS) k_onesweep(KeyCols<KW> in, const uint32_t *__restrict__ vin,
                                                          KeyCols<KW> out, uint32_t *__restrict__ vout, size_t n,
                                                          int word, int shift, const uint32_t *__restrict__ hist,
                                                          uint32_t *status, uint32_t *tile_counter) {
     __shared__ uint32_t tile_s;
-    __shared__ uint32_t base_s[256];
-    __shared__ uint32_t running[256];
-    __shared__ uint32_t wcnt[RS_THREADS / 32][256];
+    __shared__ uint32_t wsum[2][OS_WARPS];
+    __shared__ uint32_t wcnt[OS_WARPS][256];  // per-warp digit counts -> tile positions of each warp's run
+    __shared__ uint32_t gofs[256];            // output index of tile position j of digit d = gofs[d] + j
+    __shared__ uint8_t sdig[OS_TILE];         // digit of tile position j
+    __shared__ uint64_t stage[OS_TILE];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     if (t == 0) tile_s = atomicAdd(tile_counter, 1u);
-    // exclusive scan of the global digit histogram (digit bases)
-    base_s[t] = hist[t];
-    running[t] = 0;
+#pragma unroll
+    for (int w = 0; w < OS_WARPS; ++w) wcnt[w][t] = 0;
     __syncthreads();
-#pragma unroll 1
-    for (int off = 1; off < 256; off <<= 1) {
-        const uint32_t x = t >= off ? base_s[t - off] : 0;
-        __syncthreads();
-        base_s[t] += x;
-        __syncthreads();
-    }
-    const uint32_t my_base = base_s[t] - hist[t];
     const uint32_t tile = tile_s;
-    const size_t tbase = (size_t)tile * RS_TILE;
+    const size_t tbase = (size_t)tile * OS_TILE;
+    const size_t wbase = tbase + (size_t)warp * (32 * OS_ITEMS) + lane;
     const uint64_t *kd = in.w[word];
-    uint32_t packed[RS_ROUNDS];
+
+    // ---- load the digit word (warp-striped: item i of lane l is wbase + 32 i) and rank per warp
+    uint64_t key[OS_ITEMS];
+    uint32_t slot[OS_ITEMS];  // (digit << 16) | rank within this warp's run of the digit; ~0 = past n
 #pragma unroll
-    for (int r = 0; r < RS_ROUNDS; ++r) {
+    for (int i = 0; i < OS_ITEMS; ++i) {
+        const size_t pos = wbase + 32 * i;
+        key[i] = pos < n ? kd[pos] : 0;
+    }
+    const uint32_t lt = lanemask_lt();
 #pragma unroll
-        for (int w = 0; w < RS_THREADS / 32; ++w) wcnt[w][t] = 0;
-        __syncthreads();
-        const size_t pos = tbase + (size_t)r * RS_THREADS + t;
-        const bool valid = pos < n;
-        const uint32_t d = valid ? (uint32_t)(kd[pos] >> shift) & 255u : 256u;
+    for (int i = 0; i < OS_ITEMS; ++i) {
+        const bool valid = wbase + 32 * i < n;
+        const uint32_t d = valid ? (uint32_t)(key[i] >> shift) & 255u : 256u;
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t wrank = __popc(peers & lanemask_lt());
-        if (valid && lane == __ffs(peers) - 1) wcnt[warp][d] = __popc(peers);
-        __syncthreads();
-        uint32_t run = running[t];
-#pragma unroll
-        for (int w = 0; w < RS_THREADS / 32; ++w) {
-            const uint32_t c = wcnt[w][t];
-            wcnt[w][t] = run;
-            run += c;
-        }
-        running[t] = run;
-        __syncthreads();
-        packed[r] = valid ? ((d << 16) | (wcnt[warp][d] + wrank)) : 0xFFFFFFFFu;
-        __syncthreads();  // wcnt is re-zeroed by the next round
+        const uint32_t before = valid ? wcnt[warp][d] : 0u;
+        __syncwarp();
+        if (valid && lane == 31 - __clz(peers)) wcnt[warp][d] = before + __popc(peers);
+        __syncwarp();
+        slot[i] = valid ? ((d << 16) | (before + __popc(peers & lt))) : 0xFFFFFFFFu;
     }
     __syncthreads();
-    // decoupled look-back for digit t
-    const uint32_t cnt = running[t];
+    // ---- digit t: counts per warp -> exclusive offsets across warps; tile total
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int w = 0; w < OS_WARPS; ++w) {
+        const uint32_t c = wcnt[w][t];
+        wcnt[w][t] = cnt;
+        cnt += c;
+    }
     volatile uint32_t *st = status;
+    if (tile != 0) st[(size_t)tile * 256 + t] = LB_AGG | cnt;  // publish the aggregate early
+    uint32_t tot;
+    const uint32_t tstart = block256_excl(cnt, wsum[0], tot);  // tile position of digit t's run
+    const uint32_t h = hist[t];
+    const uint32_t dbase = block256_excl(h, wsum[1], tot) ;    // global start of digit t
+    // ---- decoupled look-back for digit t
     uint32_t excl = 0;
     if (tile == 0) {
         st[t] = LB_INC | cnt;
     } else {
-        st[(size_t)tile * 256 + t] = LB_AGG | cnt;
         for (int64_t j = (int64_t)tile - 1; j >= 0; --j) {
             uint32_t v;
             do {
@@ -459,16 +488,52 @@ __global__ void __launch_bounds__(RS_THREADS) k_onesweep(KeyCols<KW> in, const u
         }
         st[(size_t)tile * 256 + t] = LB_INC | (excl + cnt);
     }
-    base_s[t] = my_base + excl;
+    gofs[t] = dbase + excl - tstart;
+#pragma unroll
+    for (int w = 0; w < OS_WARPS; ++w) wcnt[w][t] += tstart;
     __syncthreads();
+    // ---- tile positions; digit of each position
 #pragma unroll
-    for (int r = 0; r < RS_ROUNDS; ++r) {
-        if (packed[r] == 0xFFFFFFFFu) continue;
-        const size_t pos = tbase + (size_t)r * RS_THREADS + t;
-        const uint32_t dst = base_s[packed[r] >> 16] + (packed[r] & 0xFFFFu);
+    for (int i = 0; i < OS_ITEMS; ++i) {
+        if (slot[i] == 0xFFFFFFFFu) continue;
+        const uint32_t d = slot[i] >> 16;
+        const uint32_t p = wcnt[warp][d] + (slot[i] & 0xFFFFu);
+        slot[i] = p;
+        sdig[p] = (uint8_t)d;
+        stage[p] = key[i];
+    }
+    __syncthreads();
+    const uint32_t tn = (uint32_t)(n - tbase < (size_t)OS_TILE ? n - tbase : (size_t)OS_TILE);
+    {
+        uint64_t *o = out.w[word];
+        for (uint32_t j = t; j < tn; j += OS_THREADS) o[gofs[sdig[j]] + j] = stage[j];
+    }
+    // ---- the other key words and the value, through the same staging buffer
 #pragma unroll
-        for (int w = 0; w < KW; ++w) out.w[w][dst] = in.w[w][pos];
-        vout[dst] = vin[pos];
+    for (int w = 0; w < KW; ++w) {
+        if (w == word) continue;
+        const uint64_t *src = in.w[w];
+#pragma unroll
+        for (int i = 0; i < OS_ITEMS; ++i) key[i] = slot[i] != 0xFFFFFFFFu ? src[wbase + 32 * i] : 0;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < OS_ITEMS; ++i)
+            if (slot[i] != 0xFFFFFFFFu) stage[slot[i]] = key[i];
+        __syncthreads();
+        uint64_t *o = out.w[w];
+        for (uint32_t j = t; j < tn; j += OS_THREADS) o[gofs[sdig[j]] + j] = stage[j];
+    }
+    {
+        uint32_t vv[OS_ITEMS];
+#pragma unroll
+        for (int i = 0; i < OS_ITEMS; ++i) vv[i] = slot[i] != 0xFFFFFFFFu ? vin[wbase + 32 * i] : 0u;
+        uint32_t *st32 = reinterpret_cast<uint32_t *>(stage);
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < OS_ITEMS; ++i)
+            if (slot[i] != 0xFFFFFFFFu) st32[slot[i]] = vv[i];
+        __syncthreads();
+        for (uint32_t j = t; j < tn; j += OS_THREADS) vout[gofs[sdig[j]] + j] = st32[j];
     }
 }
 
@@ -495,7 +560,7 @@ void radix_sort(SortBufs<KW> &b, size_t n, LiveBytes<KW> live, cudaStream_t s) {
     hist.zero();
     k_radix_hist_all<KW><<<grid_for(n, RS_THREADS, 148 * 4), RS_THREADS, 0, s>>>(b.k[b.cur], n, live, hist.p);
     CK_LAUNCH("k_radix_hist_all");
-    const unsigned ntiles = (unsigned)((n + RS_TILE - 1) / RS_TILE);
+    const unsigned ntiles = (unsigned)((n + OS_TILE - 1) / OS_TILE);
     const size_t stride = (size_t)ntiles * 256 + 32;  // status words + tile counter per pass
     DBuf<uint32_t> status(stride * npass, s);
     status.zero();
@@ -504,7 +569,7 @@ void radix_sort(SortBufs<KW> &b, size_t n, LiveBytes<KW> live, cudaStream_t s) {
         for (int byte = 0; byte < 8; ++byte) {
             if (!((live.m[w] >> byte) & 1)) continue;
             uint32_t *stp = status.p + stride * p++;
-            k_onesweep<KW><<<ntiles, RS_THREADS, 0, s>>>(b.k[b.cur], b.v[b.cur], b.k[b.cur ^ 1], b.v[b.cur ^ 1], n, w,
+            k_onesweep<KW><<<ntiles, OS_THREADS, 0, s>>>(b.k[b.cur], b.v[b.cur], b.k[b.cur ^ 1], b.v[b.cur ^ 1], n, w,
                                                          8 * byte, hist.p + (size_t)(w * 8 + byte) * 256, stp,
                                                          stp + (size_t)ntiles * 256);
             CK_LAUNCH("k_onesweep");
