@@ -86,36 +86,51 @@ struct ColsUpload {
 };
 
 // ============================================================ validation (model.py:125-200)
-__device__ __forceinline__ uint32_t event_rules(const DevCols &c, size_t i) {
+// One event's fields, loaded with plain coalesced loads (the 64-B/event algorithmic read).
+struct Row {
+    uint64_t seq, start, end, nb, h, da;
+    int32_t src, dst;
+    uint8_t kind;
+    uint32_t loc;
+};
+__device__ __forceinline__ Row load_row(const DevCols &c, size_t i) {
+    Row r;
+    r.seq = c.seq[i], r.start = c.start[i], r.end = c.end[i], r.nb = c.nb[i], r.h = c.h[i], r.da = c.da[i];
+    r.src = c.src[i], r.dst = c.dst[i], r.kind = c.kind[i], r.loc = c.loc[i];
+    return r;
+}
+// Rule bits of one event given the previous event's (start, seq) (has_prev false for event 0).
+__device__ __forceinline__ uint32_t row_rules(const DevCols &c, const Row &r, bool has_prev, uint64_t ps, uint64_t pq) {
     uint32_t m = 0;
-    const uint64_t t0 = c.start[i], t1 = c.end[i];
-    const int32_t src = c.src[i], dst = c.dst[i];
-    if (t0 > t1) m |= B2L_RULE_INTERVAL;
-    if (src < 0 || src >= c.ndev) m |= B2L_RULE_SRC_DEVICE;
-    if (dst < 0 || dst >= c.ndev) m |= B2L_RULE_DST_DEVICE;
-    switch (c.kind[i]) {
+    if (r.start > r.end) m |= B2L_RULE_INTERVAL;
+    if (r.src < 0 || r.src >= c.ndev) m |= B2L_RULE_SRC_DEVICE;
+    if (r.dst < 0 || r.dst >= c.ndev) m |= B2L_RULE_DST_DEVICE;
+    switch (r.kind) {
         case B2L_KIND_TRANSFER:
-            if (c.nb[i] > 0 && c.h[i] == 0) m |= B2L_RULE_TRANSFER_HASH;
+            if (r.nb > 0 && r.h == 0) m |= B2L_RULE_TRANSFER_HASH;
             break;
         case B2L_KIND_ALLOC:
-            if (c.nb[i] == 0) m |= B2L_RULE_ALLOC_BYTES;
-            if (c.da[i] == 0) m |= B2L_RULE_ALLOC_ADDR;
+            if (r.nb == 0) m |= B2L_RULE_ALLOC_BYTES;
+            if (r.da == 0) m |= B2L_RULE_ALLOC_ADDR;
             break;
         case B2L_KIND_DELETE:
-            if (c.da[i] == 0) m |= B2L_RULE_DELETE_ADDR;
+            if (r.da == 0) m |= B2L_RULE_DELETE_ADDR;
             break;
         default:
-            if (src != dst) m |= B2L_RULE_KERNEL_DEVICE;
+            if (r.src != r.dst) m |= B2L_RULE_KERNEL_DEVICE;
     }
-    const uint8_t lf = c.loc_flags[c.loc[i]];
+    const uint8_t lf = c.loc_flags[r.loc];
     if (lf & B2L_LOC_FILE_NO_LINE) m |= B2L_RULE_LOC_FILE;
     if (lf & B2L_LOC_LINE_NONPOS) m |= B2L_RULE_LOC_LINE;
-    if (i > 0) {
-        const uint64_t ps = c.start[i - 1], pq = c.seq[i - 1], q = c.seq[i];
-        if (t0 < ps || (t0 == ps && q < pq)) m |= B2L_RULE_ORDER_SORT;
-        if (q <= pq) m |= B2L_RULE_ORDER_SEQ;
+    if (has_prev) {
+        if (r.start < ps || (r.start == ps && r.seq < pq)) m |= B2L_RULE_ORDER_SORT;
+        if (r.seq <= pq) m |= B2L_RULE_ORDER_SEQ;
     }
     return m;
+}
+__device__ __forceinline__ uint32_t event_rules(const DevCols &c, size_t i) {
+    const Row r = load_row(c, i);
+    return row_rules(c, r, i > 0, i > 0 ? c.start[i - 1] : 0, i > 0 ? c.seq[i - 1] : 0);
 }
 struct BadPred {
     DevCols c;
@@ -152,62 +167,229 @@ struct IsTargetKernel {
     __device__ bool operator()(size_t i) const { return c.kind[i] == B2L_KIND_KERNEL && c.dst[i] != c.host; }
 };
 
-__global__ void k_max_data_end(DevCols c, unsigned long long *out) {
-    unsigned long long m = 0;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += (size_t)gridDim.x * blockDim.x)
-        if (c.kind[i] != B2L_KIND_KERNEL && c.end[i] > m) m = c.end[i];
-    for (int o = 16; o; o >>= 1) {
-        unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
-        m = v > m ? v : m;
+// ============================================================ fused front pass
+// validate + partition + max data-op end + key-bit variation + start ranks in one
+// reduce -> partials-scan -> apply sequence (3 launches, two reads of the columns):
+//   reduce: per 4096-event tile, counts of {bad, H, TT, AD, A, TK} and the last start
+//           change; block-reduced atomics for max end and the OR/AND masks;
+//   apply:  order-preserving warp-ballot compaction of the five index lists (or of the
+//           bad list when validation failed) and srank[i] = last start change <= i.
+constexpr int FR_THREADS = 256, FR_ITEMS = 16, FR_TILE = FR_THREADS * FR_ITEMS, FR_NCAT = 6;
+enum : uint32_t { F_BAD = 1, F_H = 2, F_TT = 4, F_AD = 8, F_A = 16, F_TK = 32 };
+struct FrontAcc {
+    uint32_t c[FR_NCAT];
+    uint32_t lastchg;  // max index j <= i with j == 0 or start[j] != start[j-1]
+};
+struct FrontOp {
+    using T = FrontAcc;
+    static __device__ __forceinline__ T identity() { return T{{0, 0, 0, 0, 0, 0}, 0}; }
+    static __device__ __forceinline__ T combine(T a, T b) {
+        T r;
+#pragma unroll
+        for (int k = 0; k < FR_NCAT; ++k) r.c[k] = a.c[k] + b.c[k];
+        r.lastchg = a.lastchg > b.lastchg ? a.lastchg : b.lastchg;
+        return r;
     }
-    __shared__ unsigned long long wm[32];
-    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+};
+__device__ __forceinline__ uint32_t part_flags(const DevCols &c, uint8_t k, int32_t dst, uint64_t nb, uint64_t h,
+                                               bool raw) {
+    uint32_t f = 0;
+    if (k == B2L_KIND_TRANSFER && (raw || (nb > 0 && h != 0))) f |= F_H;
+    if (k == B2L_KIND_TRANSFER && dst != c.host) f |= F_TT;
+    if (k == B2L_KIND_ALLOC || k == B2L_KIND_DELETE) f |= F_AD;
+    if (k == B2L_KIND_ALLOC) f |= F_A;
+    if (k == B2L_KIND_KERNEL && dst != c.host) f |= F_TK;
+    return f;
+}
+constexpr int FR_BATCH = 4;  // items whose loads are issued together (memory-level parallelism)
+
+__global__ void __launch_bounds__(FR_THREADS, 2) k_front_reduce(DevCols c, bool validate, bool raw, FrontAcc *partials,
+                                                             unsigned long long *agg /*[0] max end, [1..5] OR, [6..10] AND*/) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const size_t wb = (size_t)blockIdx.x * FR_TILE + (size_t)warp * (32 * FR_ITEMS) + lane;
+    const size_t last = c.n - 1;
+    uint32_t cnt[FR_NCAT] = {0, 0, 0, 0, 0, 0}, lastchg = 0;
+    unsigned long long me = 0, o[5] = {0, 0, 0, 0, 0}, a[5] = {~0ull, ~0ull, ~0ull, ~0ull, ~0ull};
+#pragma unroll 1
+    for (int k0 = 0; k0 < FR_ITEMS; k0 += FR_BATCH) {
+        if (wb - lane + 32 * k0 > last) break;  // warp-uniform
+        Row r[FR_BATCH];
+        uint64_t sa[FR_BATCH], p0s = 0, p0q = 0;
+#pragma unroll
+        for (int b = 0; b < FR_BATCH; ++b) {
+            const size_t i = wb + 32 * (k0 + b), ic = i < last ? i : last;
+            r[b] = load_row(c, ic);
+            sa[b] = c.sa[ic];
+        }
+        {
+            const size_t i0 = wb + 32 * k0;  // lane 0's predecessor lives in the previous 32-run
+            if (lane == 0 && i0 > 0 && i0 <= last) p0s = c.start[i0 - 1], p0q = c.seq[i0 - 1];
+        }
+#pragma unroll
+        for (int b = 0; b < FR_BATCH; ++b) {
+            const size_t i = wb + 32 * (k0 + b);
+            uint64_t ps = __shfl_up_sync(0xffffffffu, r[b].start, 1), pq = __shfl_up_sync(0xffffffffu, r[b].seq, 1);
+            if (lane == 0) {
+                if (b == 0) ps = p0s, pq = p0q;
+                else ps = c.start[i - 1 < last ? i - 1 : last], pq = c.seq[i - 1 < last ? i - 1 : last];
+            }
+            if (i > last) continue;
+            uint32_t f = part_flags(c, r[b].kind, r[b].dst, r[b].nb, r[b].h, raw);
+            if (validate && row_rules(c, r[b], i > 0, ps, pq)) f |= F_BAD;
+#pragma unroll
+            for (int q = 0; q < FR_NCAT; ++q) cnt[q] += (f >> q) & 1u;
+            if (i == 0 || r[b].start != ps) lastchg = (uint32_t)i;  // i increases along the loop
+            if (r[b].kind != B2L_KIND_KERNEL) me = r[b].end > me ? r[b].end : me;
+            if (r[b].kind == B2L_KIND_TRANSFER) {
+                o[0] |= r[b].h, a[0] &= r[b].h;  // superset of the hashed subset
+                if (f & F_TT) o[4] |= sa[b], a[4] &= sa[b];
+            } else if (f & F_AD) {
+                o[1] |= r[b].da, a[1] &= r[b].da;
+                if (f & F_A) o[2] |= sa[b], a[2] &= sa[b], o[3] |= r[b].nb, a[3] &= r[b].nb;
+            }
+        }
+    }
+    // warp reductions
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+#pragma unroll
+        for (int q = 0; q < FR_NCAT; ++q) cnt[q] += __shfl_xor_sync(0xffffffffu, cnt[q], off);
+        const uint32_t lc = __shfl_xor_sync(0xffffffffu, lastchg, off);
+        lastchg = lc > lastchg ? lc : lastchg;
+        const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, me, off);
+        me = m2 > me ? m2 : me;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            o[q] |= __shfl_xor_sync(0xffffffffu, o[q], off);
+            a[q] &= __shfl_xor_sync(0xffffffffu, a[q], off);
+        }
+    }
+    __shared__ uint32_t sc[FR_THREADS / 32][FR_NCAT + 1];
+    __shared__ unsigned long long sm[FR_THREADS / 32][11];
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < FR_NCAT; ++q) sc[warp][q] = cnt[q];
+        sc[warp][FR_NCAT] = lastchg;
+        sm[warp][0] = me;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) sm[warp][1 + q] = o[q], sm[warp][6 + q] = a[q];
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = wm[w] > m ? wm[w] : m;
-        if (m) atomicMax(out, m);
+    if (t < FR_NCAT + 1) {
+        uint32_t v = 0;
+        for (int w = 0; w < FR_THREADS / 32; ++w) v = t < FR_NCAT ? v + sc[w][t] : (sc[w][t] > v ? sc[w][t] : v);
+        if (t < FR_NCAT) partials[blockIdx.x].c[t] = v;
+        else partials[blockIdx.x].lastchg = v;
+    } else if (t >= 32 && t < 32 + 11) {
+        const int q = t - 32;
+        unsigned long long v = q < 6 ? 0ull : ~0ull;
+        for (int w = 0; w < FR_THREADS / 32; ++w) {
+            const unsigned long long x = sm[w][q];
+            v = q == 0 ? (x > v ? x : v) : q < 6 ? (v | x) : (v & x);
+        }
+        if (q == 0) {
+            if (v) atomicMax(agg, v);
+        } else if (q < 6) {
+            if (v) atomicOr(agg + q, v);
+        } else if (~v) {
+            atomicAnd(agg + q, v);
+        }
     }
 }
 
-// Bits that vary inside each key subset (OR ^ AND over the subset): hash over hashed transfers,
-// dst_addr over allocs/deletes, src_addr and bytes over allocs, src_addr over target transfers.
-__global__ void k_col_vary(DevCols c, unsigned long long *out /*[5] OR, [5] AND*/) {
-    unsigned long long o[5] = {0, 0, 0, 0, 0}, a[5] = {~0ull, ~0ull, ~0ull, ~0ull, ~0ull};
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += (size_t)gridDim.x * blockDim.x) {
-        const uint8_t k = c.kind[i];
-        if (k == B2L_KIND_TRANSFER) o[0] |= c.h[i], a[0] &= c.h[i];  // superset of the hashed subset
-        if (k == B2L_KIND_ALLOC || k == B2L_KIND_DELETE) o[1] |= c.da[i], a[1] &= c.da[i];
-        if (k == B2L_KIND_ALLOC) o[2] |= c.sa[i], a[2] &= c.sa[i], o[3] |= c.nb[i], a[3] &= c.nb[i];
-        if (k == B2L_KIND_TRANSFER && c.dst[i] != c.host) o[4] |= c.sa[i], a[4] &= c.sa[i];
-    }
-    // warp, then block reduction: one pair of atomics per block and column
-    __shared__ unsigned long long so[32][5], sa[32][5];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+struct FrontOut {
+    uint32_t *list[FR_NCAT];  // bad, H, TT, AD, A, TK (nullptr: not written)
+    uint32_t *srank;          // nullptr: not written
+};
+// Warp-striped tiles (item k of lane l in warp w is base + w*32*ITEMS + 32k + l) keep index
+// order under ballot ranking: a warp's items precede the next warp's, items precede items.
+// bad_mode: only the bad list (validation failed); else the five partition lists + srank.
+__global__ void __launch_bounds__(FR_THREADS, 2) k_front_apply(DevCols c, bool bad_mode, bool raw,
+                                                            const FrontAcc *__restrict__ prefix, FrontOut out) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const size_t wb = (size_t)blockIdx.x * FR_TILE + (size_t)warp * (32 * FR_ITEMS) + lane;
+    const size_t last = c.n - 1;
+    const uint32_t lt = lanemask_lt();
+    uint32_t fl[FR_ITEMS];  // bits 0..5 category flags, bit 6 start change
+    uint32_t wc[FR_NCAT] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
-    for (int q = 0; q < 5; ++q) {
-        unsigned long long vo = o[q], va = a[q];
-        for (int off = 16; off; off >>= 1) {
-            vo |= __shfl_xor_sync(0xffffffffu, vo, off);
-            va &= __shfl_xor_sync(0xffffffffu, va, off);
+    for (int k0 = 0; k0 < FR_ITEMS; k0 += FR_BATCH) {
+        uint8_t kd[FR_BATCH];
+        int32_t dst[FR_BATCH];
+        uint64_t nb[FR_BATCH], h[FR_BATCH], st[FR_BATCH];
+#pragma unroll
+        for (int b = 0; b < FR_BATCH; ++b) {
+            const size_t i = wb + 32 * (k0 + b), ic = i < last ? i : last;
+            kd[b] = c.kind[ic], dst[b] = c.dst[ic], nb[b] = c.nb[ic], h[b] = c.h[ic], st[b] = c.start[ic];
         }
-        if (lane == 0) so[wid][q] = vo, sa[wid][q] = va;
+#pragma unroll
+        for (int b = 0; b < FR_BATCH; ++b) {
+            const size_t i = wb + 32 * (k0 + b);
+            uint64_t ps = __shfl_up_sync(0xffffffffu, st[b], 1);
+            if (lane == 0 && i > 0 && i <= last) ps = c.start[i - 1];
+            uint32_t f = 0;
+            if (i <= last) {
+                if (bad_mode) {
+                    f = event_rules(c, i) ? F_BAD : 0u;
+                } else {
+                    f = part_flags(c, kd[b], dst[b], nb[b], h[b], raw);
+                    if (i == 0 || st[b] != ps) f |= 64u;
+                }
+            }
+            fl[k0 + b] = f;
+#pragma unroll
+            for (int q = 0; q < FR_NCAT; ++q) wc[q] += __popc(__ballot_sync(0xffffffffu, (f >> q) & 1u));
+        }
+    }
+    // srank: the last start change at or before each index (max scan of change positions)
+    uint32_t chmax = 0;
+#pragma unroll
+    for (int k = 0; k < FR_ITEMS; ++k)
+        if (fl[k] & 64u) chmax = (uint32_t)(wb + 32 * k);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        const uint32_t v = __shfl_xor_sync(0xffffffffu, chmax, off);
+        chmax = v > chmax ? v : chmax;
+    }
+    __shared__ uint32_t swc[FR_THREADS / 32][FR_NCAT + 1];
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < FR_NCAT; ++q) swc[warp][q] = wc[q];
+        swc[warp][FR_NCAT] = chmax;
     }
     __syncthreads();
-    if (threadIdx.x < 5) {
-        unsigned long long vo = 0, va = ~0ull;
-        for (int w = 0; w < nw; ++w) vo |= so[w][threadIdx.x], va &= sa[w][threadIdx.x];
-        if (vo) atomicOr(out + threadIdx.x, vo);
-        if (~va) atomicAnd(out + 5 + threadIdx.x, va);
+    const FrontAcc pre = prefix[blockIdx.x];
+    uint32_t run[FR_NCAT];
+#pragma unroll
+    for (int q = 0; q < FR_NCAT; ++q) {
+        uint32_t b = pre.c[q];
+        for (int w = 0; w < warp; ++w) b += swc[w][q];
+        run[q] = b;
+    }
+    uint32_t carry = pre.lastchg;
+    for (int w = 0; w < warp; ++w) carry = swc[w][FR_NCAT] > carry ? swc[w][FR_NCAT] : carry;
+#pragma unroll
+    for (int k = 0; k < FR_ITEMS; ++k) {
+        const size_t i = wb + 32 * k;
+#pragma unroll
+        for (int q = 0; q < FR_NCAT; ++q) {
+            const uint32_t m = __ballot_sync(0xffffffffu, (fl[k] >> q) & 1u);
+            if (out.list[q] && ((fl[k] >> q) & 1u)) out.list[q][run[q] + __popc(m & lt)] = (uint32_t)i;
+            run[q] += __popc(m);
+        }
+        if (out.srank) {
+            uint32_t v = (fl[k] & 64u) ? (uint32_t)i : 0u;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, v, off);
+                if (lane >= off) v = y > v ? y : v;
+            }
+            v = v > carry ? v : carry;
+            if (i <= last) out.srank[i] = v;
+            carry = __shfl_sync(0xffffffffu, v, 31);
+        }
     }
 }
-struct SrankLoad {
-    const uint64_t *start;
-    __device__ uint64_t operator()(size_t i) const { return (i == 0 || start[i] != start[i - 1]) ? i : 0; }
-};
-struct SrankStore {
-    uint32_t *srank;
-    __device__ void operator()(size_t i, uint64_t ex, uint64_t it) const { srank[i] = (uint32_t)(ex > it ? ex : it); }
-};
 
 // ============================================================ helpers
 template <class F>
@@ -367,15 +549,20 @@ struct PhaseClock {
 // ============================================================ DD + RT (detectors.py:85-167)
 struct RtRecordInit {  // record r = 2k + role over hashed transfer k: role 0 = reception, 1 = send
     DevCols c;
-    const uint32_t *H;
-    uint64_t *k0, *k1;
+    const uint32_t *H, *hid;  // hid[k]: dense rank of transfer k's hash (hash order)
+    int db;                   // device bits: key = hid << db | device
+    uint64_t *k0;
     uint32_t *val;
     __device__ void operator()(size_t r) const {
-        const uint32_t e = H[r >> 1];
-        k0[r] = c.h[e];
-        k1[r] = (uint64_t)(uint32_t)((r & 1) ? c.src[e] : c.dst[e]);
+        const uint32_t k = (uint32_t)(r >> 1), e = H[k];
+        k0[r] = ((uint64_t)hid[k] << db) | (uint64_t)(uint32_t)((r & 1) ? c.src[e] : c.dst[e]);
         val[r] = (uint32_t)r;
     }
+};
+struct StoreHid {  // hash rank of every hashed transfer from the hash-sorted order
+    const uint32_t *sval;
+    uint32_t *hid;
+    __device__ void operator()(size_t p, uint32_t ex, uint32_t it) const { hid[sval[p]] = ex + it - 1; }
 };
 
 // Per sorted record: segment head, reception/send counts (segmented + global).
@@ -391,10 +578,10 @@ struct QOp {
     }
 };
 struct QLoad {
-    KeyCols<2> k;
+    const uint64_t *k;
     const uint32_t *val;
     __device__ QState operator()(size_t p) const {
-        const bool head = p == 0 || k.w[0][p] != k.w[0][p - 1] || k.w[1][p] != k.w[1][p - 1];
+        const bool head = p == 0 || k[p] != k[p - 1];
         const uint32_t rx = (val[p] & 1u) == 0;
         return QState{head, head, rx, 1u - rx, rx};
     }
@@ -417,10 +604,10 @@ struct QStore {
 };
 // r_j = j + max_{i<=j}(f_i - i) over the sends of one queue
 struct RtMaxLoad {
-    KeyCols<2> k;
+    const uint64_t *k;
     const uint32_t *val, *f_of, *j_of;
     __device__ Seg<MaxI64>::T operator()(size_t p) const {
-        const bool head = p == 0 || k.w[0][p] != k.w[0][p - 1] || k.w[1][p] != k.w[1][p - 1];
+        const bool head = p == 0 || k[p] != k[p - 1];
         const bool tx = val[p] & 1u;
         return Seg<MaxI64>::T{head ? 1u : 0u, tx ? (long long)f_of[p] - (long long)j_of[p] : MaxI64::identity()};
     }
@@ -441,34 +628,33 @@ struct RtMatchStore {
 // Strict pseudocode (detectors.py:139-160): per hash, sends in trace order peek the
 // (hash, src) queue and pop the (hash, dst) queue.  Queues of one hash interact, so one
 // thread walks each hash's events; different hashes run in parallel.
-__device__ __forceinline__ int find_seg(const uint64_t *sk0, const uint64_t *sk1, uint32_t nseg, uint64_t h,
-                                        uint64_t d) {
+__device__ __forceinline__ int find_seg(const uint64_t *sk, uint32_t nseg, uint64_t key) {
     uint32_t lo = 0, hi = nseg;
     while (lo < hi) {
         uint32_t mid = (lo + hi) >> 1;
-        if (sk0[mid] < h || (sk0[mid] == h && sk1[mid] < d))
+        if (sk[mid] < key)
             lo = mid + 1;
         else
             hi = mid;
     }
-    return (lo < nseg && sk0[lo] == h && sk1[lo] == d) ? (int)lo : -1;
+    return (lo < nseg && sk[lo] == key) ? (int)lo : -1;
 }
 __global__ void k_rt_strict(DevCols c, const uint32_t *H, const uint32_t *hsorted /*hashed-k sorted by hash*/,
-                            const uint32_t *hseg_start, uint32_t nhseg, uint32_t nH, const uint64_t *sk0,
-                            const uint64_t *sk1, uint32_t nseg, const uint32_t *seg_rxbase, const uint32_t *rxpos,
+                            const uint32_t *hseg_start, uint32_t nhseg, uint32_t nH, const uint32_t *hid, int db,
+                            const uint64_t *segk, uint32_t nseg, const uint32_t *seg_rxbase, const uint32_t *rxpos,
                             const uint32_t *sval, uint32_t *qhead, uint32_t *match) {
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < nhseg; g += gridDim.x * blockDim.x) {
         const uint32_t b = hseg_start[g], e = (g + 1 < nhseg) ? hseg_start[g + 1] : nH;
         for (uint32_t q = b; q < e; ++q) {
             const uint32_t k = hsorted[q];
             const uint32_t ev = H[k];
-            const uint64_t h = c.h[ev];
-            const int sq = find_seg(sk0, sk1, nseg, h, (uint64_t)(uint32_t)c.src[ev]);
+            const uint64_t hk = (uint64_t)hid[k] << db;
+            const int sq = find_seg(segk, nseg, hk | (uint64_t)(uint32_t)c.src[ev]);
             if (sq < 0) continue;
             const uint32_t nrx = seg_rxbase[sq + 1] - seg_rxbase[sq];
             if (qhead[sq] >= nrx) continue;  // `if not q: continue`
             match[k] = H[sval[rxpos[seg_rxbase[sq] + qhead[sq]]] >> 1];
-            const int so = find_seg(sk0, sk1, nseg, h, (uint64_t)(uint32_t)c.dst[ev]);
+            const int so = find_seg(segk, nseg, hk | (uint64_t)(uint32_t)c.dst[ev]);
             if (so >= 0 && qhead[so] < seg_rxbase[so + 1] - seg_rxbase[so]) qhead[so] += 1;
         }
     }
@@ -487,12 +673,28 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
         return r;
     }
     PhaseClock pc(s);
-    SortStore<2> st(R, s);
-    for_each(R, RtRecordInit{c, H, st.in_key(0), st.in_key(1), st.in_val()}, s);
+    // ---- hashed transfers in hash order (stable) -> dense hash rank per transfer, so the
+    // (hash, device) record sort runs on one narrow key: rank << db | device
+    SortStore<1> hsort(nH, s);
+    {
+        uint64_t *k0 = hsort.in_key(0);
+        uint32_t *v = hsort.in_val();
+        const uint64_t *hh = c.h;
+        for_each(nH, [=] __device__(size_t k) { k0[k] = hh[H[k]], v[k] = (uint32_t)k; }, s);
+    }
+    radix_sort<1>(hsort.b, nH, LiveBytes<1>{{g_masks.hash}}, s);
+    KeyCols<1> hk = hsort.b.k[hsort.b.cur];
+    DBuf<uint32_t> hid(nH, s);
+    scan<SumU32>(nH, HeadLoad<1>{hk}, StoreHid{hsort.val(), hid.p}, s);
+    int db = 0;
+    while (db < 32 && (1ull << db) < (uint64_t)(c.ndev > 0 ? c.ndev : 1)) ++db;
+    pc.mark(" hash-rank");
+    SortStore<1> st(R, s);
+    for_each(R, RtRecordInit{c, H, hid.p, db, st.in_key(0), st.in_val()}, s);
     pc.mark(" rt-init");
-    radix_sort<2>(st.b, R, LiveBytes<2>{{g_masks.hash, g_masks.dev}}, s);
+    radix_sort<1>(st.b, R, LiveBytes<1>{{live_range((uint64_t)nH << db)}}, s);
     pc.mark(" rt-sort");
-    KeyCols<2> sk = st.b.k[st.b.cur];
+    const uint64_t *sk = st.key(0);
     const uint32_t *sval = st.val();
 
     DBuf<uint32_t> seg_of(R, s), f_of(R, s), j_of(R, s), rxpos(R, s), seg_start(R + 1, s), seg_rxbase(R + 1, s);
@@ -512,29 +714,19 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
         scan<Seg<MaxI64>>(R, RtMaxLoad{sk, sval, f_of.p, j_of.p},
                           RtMatchStore{sval, j_of.p, seg_of.p, seg_rxbase.p, rxpos.p, H, match.p}, s);
     } else {
-        DBuf<uint64_t> segk0(nseg, s), segk1(nseg, s);
+        DBuf<uint64_t> segk(nseg, s);
         {
             const uint32_t *ss = seg_start.p;
-            uint64_t *a = segk0.p, *b = segk1.p;
-            const uint64_t *x0 = sk.w[0], *x1 = sk.w[1];
-            for_each(nseg, [=] __device__(size_t g) { a[g] = x0[ss[g]], b[g] = x1[ss[g]]; }, s);
+            uint64_t *a = segk.p;
+            for_each(nseg, [=] __device__(size_t g) { a[g] = sk[ss[g]]; }, s);
         }
-        // hashed transfers grouped by hash, trace order within a hash
-        SortStore<1> hsort(nH, s);
-        {
-            uint64_t *k0 = hsort.in_key(0);
-            uint32_t *v = hsort.in_val();
-            const uint64_t *hh = c.h;
-            for_each(nH, [=] __device__(size_t k) { k0[k] = hh[H[k]], v[k] = (uint32_t)k; }, s);
-        }
-        radix_sort<1>(hsort.b, nH, LiveBytes<1>{{g_masks.hash}}, s);
+        // hashed transfers grouped by hash, trace order within a hash: the hash sort above
         DBuf<uint32_t> hstart(nH, s), hcount(1, s);
-        KeyCols<1> hk = hsort.b.k[hsort.b.cur];
         compact(nH, HeadPred<1>{hk}, hstart.p, hcount.p, s);
         const uint32_t nhseg = read_u32(hcount.p, s);
         DBuf<uint32_t> qhead(nseg, s);
         qhead.zero();
-        k_rt_strict<<<grid_for(nhseg, 128), 128, 0, s>>>(c, H, hsort.val(), hstart.p, nhseg, nH, segk0.p, segk1.p,
+        k_rt_strict<<<grid_for(nhseg, 128), 128, 0, s>>>(c, H, hsort.val(), hstart.p, nhseg, nH, hid.p, db, segk.p,
                                                          nseg, seg_rxbase.p, rxpos.p, sval, qhead.p, match.p);
         CK_LAUNCH("k_rt_strict");
     }
@@ -1095,50 +1287,59 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     const DevCols c = up.d;
     const size_t n = c.n;
     pc.mark("upload");
-    DBuf<uint32_t> cnt(8, s);
-    cnt.zero();
-    // ---- 1. validation (the standalone detector entry points take unvalidated event lists)
-    if (!(flags & B2L_ANALYZE_NO_VALIDATE)) {
-        DBuf<uint32_t> bad(n ? n : 1, s);
-        compact(n, BadPred{c}, bad.p, cnt.p + 0, s);
-        const uint32_t nbad = read_u32(cnt.p + 0, s);
-        if (nbad) {
-            DBuf<uint32_t> rules(nbad, s);
-            k_bad_rules<<<grid_for(nbad, TPB), TPB, 0, s>>>(c, bad.p, cnt.p + 0, rules.p);
-            CK_LAUNCH("k_bad_rules");
-            f->n_bad = nbad;
-            HostBatch hb;
-            hb.add(&f->bad_index, bad.p, nbad);
-            hb.add(&f->bad_rules, rules.p, nbad);
-            in->slab = new HostSlab();
-            hb.flush(*in->slab, s);
-            return fail(B2L_E_INVALID_TRACE, "trace fails validation");
+    // ---- 1+2. validation, partition, max end, key-bit masks, start ranks (fused front pass)
+    const bool validate = !(flags & B2L_ANALYZE_NO_VALIDATE), raw = (flags & B2L_ANALYZE_RAW_HASHED) != 0;
+    const unsigned ftiles = (unsigned)((n + FR_TILE - 1) / FR_TILE);
+    DBuf<FrontAcc> fpart(ftiles + 1, s);
+    DBuf<unsigned long long> agg(11, s);  // [0] max data-op end, [1..5] subset OR, [6..10] subset AND
+    agg.zero();
+    CK(cudaMemsetAsync(agg.p + 6, 0xFF, 5 * sizeof(unsigned long long), s));
+    FrontAcc ftot{};
+    unsigned long long hm[11] = {0, 0, 0, 0, 0, 0, ~0ull, ~0ull, ~0ull, ~0ull, ~0ull};
+    if (n) {
+        k_front_reduce<<<ftiles, FR_THREADS, 0, s>>>(c, validate, raw, fpart.p, agg.p);
+        CK_LAUNCH("k_front_reduce");
+        k_scan_partials<FrontOp><<<1, SCAN_THREADS, 0, s>>>(fpart.p, ftiles, fpart.p + ftiles);
+        CK_LAUNCH("k_scan_partials<FrontOp>");
+        uint8_t rb[sizeof(FrontAcc) + sizeof(hm)];
+        {
+            uint8_t *st = pinned(s).reserve(sizeof(rb));
+            CK(cudaMemcpyAsync(st, fpart.p + ftiles, sizeof(FrontAcc), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(st + sizeof(FrontAcc), agg.p, sizeof(hm), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            memcpy(rb, st, sizeof(rb));
         }
+        memcpy(&ftot, rb, sizeof(FrontAcc));
+        memcpy(hm, rb + sizeof(FrontAcc), sizeof(hm));
+    }
+    const uint32_t nbad = ftot.c[0];
+    if (nbad) {
+        DBuf<uint32_t> bad(nbad, s), rules(nbad, s), dcount(1, s);
+        FrontOut fo{{bad.p, nullptr, nullptr, nullptr, nullptr, nullptr}, nullptr};
+        k_front_apply<<<ftiles, FR_THREADS, 0, s>>>(c, true, raw, fpart.p, fo);
+        CK_LAUNCH("k_front_apply(bad)");
+        CK(cudaMemcpyAsync(dcount.p, &nbad, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        k_bad_rules<<<grid_for(nbad, TPB), TPB, 0, s>>>(c, bad.p, dcount.p, rules.p);
+        CK_LAUNCH("k_bad_rules");
+        f->n_bad = nbad;
+        HostBatch hb;
+        hb.add(&f->bad_index, bad.p, nbad);
+        hb.add(&f->bad_rules, rules.p, nbad);
+        in->slab = new HostSlab();
+        hb.flush(*in->slab, s);
+        return fail(B2L_E_INVALID_TRACE, "trace fails validation");
     }
     pc.mark("validate");
     if (flags & B2L_ANALYZE_VALIDATE_ONLY) return B2L_OK;
-    // ---- 2. partition
-    DBuf<uint32_t> H(n ? n : 1, s), TT(n ? n : 1, s), AD(n ? n : 1, s), A(n ? n : 1, s), TK(n ? n : 1, s);
-    compact(n, IsHashed{c, (flags & B2L_ANALYZE_RAW_HASHED) != 0}, H.p, cnt.p + 1, s);
-    compact(n, IsTargetTransfer{c}, TT.p, cnt.p + 2, s);
-    compact(n, IsAllocDelete{c}, AD.p, cnt.p + 3, s);
-    compact(n, IsAlloc{c}, A.p, cnt.p + 4, s);
-    compact(n, IsTargetKernel{c}, TK.p, cnt.p + 5, s);
-    DBuf<unsigned long long> maxend(11, s);  // [0] max data-op end, [1..5] subset OR, [6..10] subset AND
-    maxend.zero();
-    CK(cudaMemsetAsync(maxend.p + 6, 0xFF, 5 * sizeof(unsigned long long), s));
+    const uint32_t hc[FR_NCAT] = {0, ftot.c[1], ftot.c[2], ftot.c[3], ftot.c[4], ftot.c[5]};
+    DBuf<uint32_t> H(hc[1] ? hc[1] : 1, s), TT(hc[2] ? hc[2] : 1, s), AD(hc[3] ? hc[3] : 1, s),
+        A(hc[4] ? hc[4] : 1, s), TK(hc[5] ? hc[5] : 1, s);
     DBuf<uint32_t> srank(n ? n : 1, s);
     if (n) {
-        k_max_data_end<<<grid_for(n, TPB, 148 * 8), TPB, 0, s>>>(c, maxend.p);
-        CK_LAUNCH("k_max_data_end");
-        k_col_vary<<<grid_for(n, TPB, 148 * 8), TPB, 0, s>>>(c, maxend.p + 1);
-        CK_LAUNCH("k_col_vary");
-        scan<MaxU64>(n, SrankLoad{c.start}, SrankStore{srank.p}, s);
+        FrontOut fo{{nullptr, H.p, TT.p, AD.p, A.p, TK.p}, srank.p};
+        k_front_apply<<<ftiles, FR_THREADS, 0, s>>>(c, false, raw, fpart.p, fo);
+        CK_LAUNCH("k_front_apply");
     }
-    uint32_t hc[8];
-    unsigned long long hm[11];
-    read_back(hc, cnt.p, sizeof(hc), s);
-    read_back(hm, maxend.p, sizeof(hm), s);
     const unsigned long long me = (flags & B2L_ANALYZE_SYNTH_END) ? synth_end_override : hm[0];
     const bool ddrt = !(flags & B2L_ANALYZE_SKIP_DDRT), alloc = !(flags & B2L_ANALYZE_SKIP_ALLOC);
     const uint32_t nH = ddrt ? hc[1] : 0, nT = alloc ? hc[2] : 0, nAD = alloc ? hc[3] : 0, nA = alloc ? hc[4] : 0,
@@ -1166,6 +1367,13 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     // bandwidth bound and run the two halves back to back on one stream.
     const bool overlap = n <= (size_t(4) << 20);
     if (!overlap) s2 = s;
+    else {  // the partition lists and start ranks are produced on s
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev, s));
+        CK(cudaStreamWaitEvent(s2, ev, 0));
+        CK(cudaEventDestroy(ev));
+    }
     auto device_keyed = [&] {
         try {
             CK(cudaSetDevice(dev));

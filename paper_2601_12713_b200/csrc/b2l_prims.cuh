@@ -359,19 +359,33 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_hist_all(KeyCols<KW> k, si
     for (int i = threadIdx.x; i < KW * 8 * 256; i += RS_THREADS) (&sh[0][0])[i] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const size_t stride = (size_t)gridDim.x * RS_THREADS;
-    for (size_t base = (size_t)blockIdx.x * RS_THREADS; base < n; base += stride) {
-        const size_t i = base + threadIdx.x;
-        const bool valid = i < n;
+    constexpr int U = 4;  // keys per thread per step (loads issued together)
+    const size_t stride = (size_t)gridDim.x * RS_THREADS * U;
+    for (size_t base = (size_t)blockIdx.x * RS_THREADS * U; base < n; base += stride) {
 #pragma unroll
         for (int w = 0; w < KW; ++w) {
-            const uint64_t key = valid ? k.w[w][i] : 0;
+            if (!live.m[w]) continue;
+            uint64_t key[U];
 #pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                if (!((live.m[w] >> b) & 1)) continue;
-                const uint32_t d = valid ? (uint32_t)(key >> (8 * b)) & 255u : 256u;
-                const uint32_t peers = __match_any_sync(0xffffffffu, d);
-                if (valid && lane == __ffs(peers) - 1) atomicAdd(&sh[w * 8 + b][d], (uint32_t)__popc(peers));
+            for (int u = 0; u < U; ++u) {
+                const size_t i = base + (size_t)u * RS_THREADS + threadIdx.x;
+                key[u] = i < n ? k.w[w][i] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool valid = base + (size_t)u * RS_THREADS + threadIdx.x < n;
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    if (!((live.m[w] >> b) & 1)) continue;
+                    const uint32_t d = (uint32_t)(key[u] >> (8 * b)) & 255u;
+                    // a digit shared by the whole warp (skewed or sorted keys) is one add of 32
+                    const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+                    if (__all_sync(0xffffffffu, valid && d == d0)) {
+                        if (lane == 0) atomicAdd(&sh[w * 8 + b][d0], 32u);
+                    } else if (valid) {
+                        atomicAdd(&sh[w * 8 + b][d], 1u);
+                    }
+                }
             }
         }
     }
@@ -478,13 +492,19 @@ __global__ void __launch_bounds__(OS_THREADS) k_onesweep(KeyCols<KW> in, const u
     if (tile == 0) {
         st[t] = LB_INC | cnt;
     } else {
-        for (int64_t j = (int64_t)tile - 1; j >= 0; --j) {
-            uint32_t v;
-            do {
-                v = st[(size_t)j * 256 + t];
-            } while ((v & (LB_AGG | LB_INC)) == 0);
-            excl += v & LB_VAL;
-            if (v & LB_INC) break;
+        // walk back over predecessors 4 at a time (independent loads), in order
+        bool done = false;
+        for (int64_t j = (int64_t)tile - 1; !done; j -= 4) {
+            uint32_t v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = j - u >= 0 ? st[(size_t)(j - u) * 256 + t] : LB_INC;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (done) break;
+                while ((v[u] & (LB_AGG | LB_INC)) == 0) v[u] = st[(size_t)(j - u) * 256 + t];
+                excl += v[u] & LB_VAL;
+                done = (v[u] & LB_INC) != 0;
+            }
         }
         st[(size_t)tile * 256 + t] = LB_INC | (excl + cnt);
     }
@@ -558,7 +578,7 @@ void radix_sort(SortBufs<KW> &b, size_t n, LiveBytes<KW> live, cudaStream_t s) {
     constexpr int NPOS = KW * 8;
     DBuf<uint32_t> hist((size_t)NPOS * 256, s);
     hist.zero();
-    k_radix_hist_all<KW><<<grid_for(n, RS_THREADS, 148 * 4), RS_THREADS, 0, s>>>(b.k[b.cur], n, live, hist.p);
+    k_radix_hist_all<KW><<<grid_for(n, RS_THREADS * 4, 148 * 4), RS_THREADS, 0, s>>>(b.k[b.cur], n, live, hist.p);
     CK_LAUNCH("k_radix_hist_all");
     const unsigned ntiles = (unsigned)((n + OS_TILE - 1) / OS_TILE);
     const size_t stride = (size_t)ntiles * 256 + 32;  // status words + tile counter per pass
