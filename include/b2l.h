@@ -247,6 +247,13 @@ void b2l_savings_free(b2l_savings *s);
  * (equal keys keep their order) -- sort_by_device (prep.py:99-115). */
 int b2l_stable_sort_u32(const uint32_t *keys, uint64_t n, uint32_t *out_perm);
 
+/* Stable sort of n u64 keys (host arrays) with one of the engine's strategies -- the grouping
+ * sorts behind detectors.py:85-191 (content hashes, group orders); exposed so the tests can
+ * drive each strategy with adversarial keys.  strategy: 0 = LSD over the live bytes,
+ * 1 = wide (LSD over the top live bytes + segmented fix-up of equal-prefix runs),
+ * 16 + b = LSD over live bytes >= b, then the fix-up. */
+int b2l_stable_sort_u64(const uint64_t *keys, uint64_t n, uint32_t strategy, uint32_t *out_perm);
+
 /* Positions of `n` seq values in the trace's seq column (ascending seq, as in a
  * validated trace); UINT32_MAX when absent.  Host arrays. */
 int b2l_lookup_seqs(const b2l_trace_cols *cols, const uint64_t *seqs, uint64_t n, uint32_t *out_index);

@@ -50,7 +50,14 @@ struct DevCols {
 struct Masks {
     uint8_t hash = 0xFF, sa = 0xFF, da = 0xFF, nb = 0xFF, sa_tt = 0xFF, dev = 0xFF, idx = 0xFF;
     const uint32_t *srank = nullptr;  // srank[i] = first index with start == start[i]
+    uint64_t n = 0;                   // events
 };
+// Bits needed to hold values < v.
+inline int bit_width(uint64_t v) {
+    int b = 0;
+    while (b < 64 && v > 1 && ((v - 1) >> b)) ++b;
+    return b;
+}
 thread_local Masks g_masks;
 
 // Owns device copies of host columns.
@@ -449,18 +456,45 @@ struct FirstStartKey {
         val[g] = (uint32_t)g;
     }
 };
-// Groups arrive in key order; a stable sort by the start of their first event (as the rank of the
-// first event with that start -- equal starts, equal ranks) gives the reference's (start, key...) order.
-GroupOrder order_groups(size_t ng, const uint64_t *start, const uint32_t *first_event, cudaStream_t s) {
+// Groups in key order: a stable sort by the start of their first event (as the rank of the first
+// event with that start -- equal starts, equal ranks) gives the reference's (start, key...) order.
+// Groups produced in another order pass `tie` (per group, ascending in the reference's key order)
+// and are sorted by (start rank, tie).
+GroupOrder order_groups(size_t ng, const uint64_t *start, const uint32_t *first_event, cudaStream_t s,
+                        const uint64_t *tie = nullptr, uint64_t tie_bound = 0) {
     (void)start;
     GroupOrder go;
     go.order.alloc(ng ? ng : 1, s);
     go.rank.alloc(ng ? ng : 1, s);
     if (!ng) return go;
-    SortStore<1> st(ng, s);
-    for_each(ng, FirstStartKey{g_masks.srank, first_event, st.in_key(0), st.in_val()}, s);
-    radix_sort<1>(st.b, ng, LiveBytes<1>{{g_masks.idx}}, s);
-    CK(cudaMemcpyAsync(go.order.p, st.val(), ng * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    const uint32_t *ordp;
+    const bool narrow = !tie || bit_width(tie_bound) + bit_width(g_masks.n) <= 64;
+    SortStore<1> st(narrow ? ng : 1, s);
+    SortStore<2> st2(narrow ? 1 : ng, s);
+    if (!tie) {
+        for_each(ng, FirstStartKey{g_masks.srank, first_event, st.in_key(0), st.in_val()}, s);
+        radix_sort<1>(st.b, ng, LiveBytes<1>{{g_masks.idx}}, s);
+        ordp = st.val();
+    } else if (bit_width(tie_bound) + bit_width(g_masks.n) <= 64) {
+        // one key: start rank << tie bits | tie; LSD over the bytes holding the start rank, then
+        // the segmented fix-up of equal-start runs (usually single groups)
+        const int tb = bit_width(tie_bound);
+        uint64_t *k0 = st.in_key(0);
+        uint32_t *v = st.in_val();
+        const uint32_t *sr = g_masks.srank, *fe = first_event;
+        for_each(ng, [=] __device__(size_t g) {
+            k0[g] = ((uint64_t)sr[fe[g]] << tb) | tie[g];
+            v[g] = (uint32_t)g;
+        }, s);
+        radix_sort_prefix(st.b, ng, live_range((uint64_t)g_masks.n << tb), tb / 8, s);
+        ordp = st.val();
+    } else {
+        for_each(ng, FirstStartKey{g_masks.srank, first_event, st2.in_key(0), st2.in_val()}, s);
+        CK(cudaMemcpyAsync(st2.in_key(1), tie, ng * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+        radix_sort<2>(st2.b, ng, LiveBytes<2>{{g_masks.idx, live_range(tie_bound)}}, s);
+        ordp = st2.val();
+    }
+    CK(cudaMemcpyAsync(go.order.p, ordp, ng * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     uint32_t *ord = go.order.p, *rk = go.rank.p;
     for_each(ng, [=] __device__(size_t r) { rk[ord[r]] = (uint32_t)r; }, s);
     return go;
@@ -548,21 +582,25 @@ struct PhaseClock {
 
 // ============================================================ DD + RT (detectors.py:85-167)
 struct RtRecordInit {  // record r = 2k + role over hashed transfer k: role 0 = reception, 1 = send
-    DevCols c;
-    const uint32_t *H, *hid;  // hid[k]: dense rank of transfer k's hash (hash order)
-    int db;                   // device bits: key = hid << db | device
-    uint64_t *k0;
+    DevCols c;            // generated in hash-rank order (q = 2p + role over hash-sorted position p)
+    const uint32_t *H, *hsv, *hidp;  // hsv[p]: transfer at sorted position p; hidp[p]: its hash rank
+    uint64_t *k0;                    // key = device << 32 | rank: queues (device, hash)
     uint32_t *val;
-    __device__ void operator()(size_t r) const {
-        const uint32_t k = (uint32_t)(r >> 1), e = H[k];
-        k0[r] = ((uint64_t)hid[k] << db) | (uint64_t)(uint32_t)((r & 1) ? c.src[e] : c.dst[e]);
-        val[r] = (uint32_t)r;
+    __device__ void operator()(size_t q) const {
+        const size_t p = q >> 1;
+        const uint32_t role = (uint32_t)(q & 1), k = hsv[p], e = H[k];
+        k0[q] = ((uint64_t)(uint32_t)(role ? c.src[e] : c.dst[e]) << 32) | hidp[p];
+        val[q] = 2 * k + role;
     }
 };
-struct StoreHid {  // hash rank of every hashed transfer from the hash-sorted order
+struct StoreHid {  // hash rank per sorted position and per hashed transfer
     const uint32_t *sval;
-    uint32_t *hid;
-    __device__ void operator()(size_t p, uint32_t ex, uint32_t it) const { hid[sval[p]] = ex + it - 1; }
+    uint32_t *hidp, *hid;
+    __device__ void operator()(size_t p, uint32_t ex, uint32_t it) const {
+        const uint32_t v = ex + it - 1;
+        hidp[p] = v;
+        hid[sval[p]] = v;
+    }
 };
 
 // Per sorted record: segment head, reception/send counts (segmented + global).
@@ -640,7 +678,7 @@ __device__ __forceinline__ int find_seg(const uint64_t *sk, uint32_t nseg, uint6
     return (lo < nseg && sk[lo] == key) ? (int)lo : -1;
 }
 __global__ void k_rt_strict(DevCols c, const uint32_t *H, const uint32_t *hsorted /*hashed-k sorted by hash*/,
-                            const uint32_t *hseg_start, uint32_t nhseg, uint32_t nH, const uint32_t *hid, int db,
+                            const uint32_t *hseg_start, uint32_t nhseg, uint32_t nH, const uint32_t *hid,
                             const uint64_t *segk, uint32_t nseg, const uint32_t *seg_rxbase, const uint32_t *rxpos,
                             const uint32_t *sval, uint32_t *qhead, uint32_t *match) {
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < nhseg; g += gridDim.x * blockDim.x) {
@@ -648,13 +686,13 @@ __global__ void k_rt_strict(DevCols c, const uint32_t *H, const uint32_t *hsorte
         for (uint32_t q = b; q < e; ++q) {
             const uint32_t k = hsorted[q];
             const uint32_t ev = H[k];
-            const uint64_t hk = (uint64_t)hid[k] << db;
-            const int sq = find_seg(segk, nseg, hk | (uint64_t)(uint32_t)c.src[ev]);
+            const uint64_t hk = hid[k];
+            const int sq = find_seg(segk, nseg, hk | ((uint64_t)(uint32_t)c.src[ev] << 32));
             if (sq < 0) continue;
             const uint32_t nrx = seg_rxbase[sq + 1] - seg_rxbase[sq];
             if (qhead[sq] >= nrx) continue;  // `if not q: continue`
             match[k] = H[sval[rxpos[seg_rxbase[sq] + qhead[sq]]] >> 1];
-            const int so = find_seg(segk, nseg, hk | (uint64_t)(uint32_t)c.dst[ev]);
+            const int so = find_seg(segk, nseg, hk | ((uint64_t)(uint32_t)c.dst[ev] << 32));
             if (so >= 0 && qhead[so] < seg_rxbase[so + 1] - seg_rxbase[so]) qhead[so] += 1;
         }
     }
@@ -682,17 +720,20 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
         const uint64_t *hh = c.h;
         for_each(nH, [=] __device__(size_t k) { k0[k] = hh[H[k]], v[k] = (uint32_t)k; }, s);
     }
-    radix_sort<1>(hsort.b, nH, LiveBytes<1>{{g_masks.hash}}, s);
+    radix_sort_wide(hsort.b, nH, g_masks.hash, s);
     KeyCols<1> hk = hsort.b.k[hsort.b.cur];
-    DBuf<uint32_t> hid(nH, s);
-    scan<SumU32>(nH, HeadLoad<1>{hk}, StoreHid{hsort.val(), hid.p}, s);
+    DBuf<uint32_t> hid(nH, s), hidp(nH, s);
+    scan<SumU32>(nH, HeadLoad<1>{hk}, StoreHid{hsort.val(), hidp.p, hid.p}, s);
     int db = 0;
     while (db < 32 && (1ull << db) < (uint64_t)(c.ndev > 0 ? c.ndev : 1)) ++db;
     pc.mark(" hash-rank");
+    // records generated in hash-rank order, then one stable pass over the device byte(s): queues
+    // come out in (device, hash) order, trace order inside.  Group orders that break start ties by
+    // the reference's (hash, device...) key take explicit tie keys below.
     SortStore<1> st(R, s);
-    for_each(R, RtRecordInit{c, H, hid.p, db, st.in_key(0), st.in_val()}, s);
+    for_each(R, RtRecordInit{c, H, hsort.val(), hidp.p, st.in_key(0), st.in_val()}, s);
     pc.mark(" rt-init");
-    radix_sort<1>(st.b, R, LiveBytes<1>{{live_range((uint64_t)nH << db)}}, s);
+    radix_sort<1>(st.b, R, LiveBytes<1>{{(uint8_t)(g_masks.dev << 4)}}, s);
     pc.mark(" rt-sort");
     const uint64_t *sk = st.key(0);
     const uint32_t *sval = st.val();
@@ -726,7 +767,7 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
         const uint32_t nhseg = read_u32(hcount.p, s);
         DBuf<uint32_t> qhead(nseg, s);
         qhead.zero();
-        k_rt_strict<<<grid_for(nhseg, 128), 128, 0, s>>>(c, H, hsort.val(), hstart.p, nhseg, nH, hid.p, db, segk.p,
+        k_rt_strict<<<grid_for(nhseg, 128), 128, 0, s>>>(c, H, hsort.val(), hstart.p, nhseg, nH, hid.p, segk.p,
                                                          nseg, seg_rxbase.p, rxpos.p, sval, qhead.p, match.p);
         CK_LAUNCH("k_rt_strict");
     }
@@ -740,18 +781,23 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
         const uint32_t ng = read_u32(gcount.p, s);
         r.dd_groups = ng;
         DBuf<uint32_t> first_ev(ng ? ng : 1, s), gsize(ng ? ng : 1, s), seg_group(nseg, s);
+        DBuf<uint64_t> tie(ng ? ng : 1, s);
         CK(cudaMemsetAsync(seg_group.p, 0xFF, nseg * sizeof(uint32_t), s));
         {
-            const uint32_t *gs = gseg.p, *rp = rxpos.p;
+            const uint32_t *gs = gseg.p, *rp = rxpos.p, *ss = seg_start.p;
             uint32_t *fe = first_ev.p, *sz = gsize.p, *sgp = seg_group.p;
+            uint64_t *tk = tie.p;
+            const int dbits = db;
             for_each(ng, [=] __device__(size_t g) {
                 const uint32_t sg = gs[g];
                 fe[g] = H[sval[rp[rb[sg]]] >> 1];
                 sz[g] = rb[sg + 1] - rb[sg];
                 sgp[sg] = (uint32_t)g;
+                const uint64_t key = sk[ss[sg]];  // dst << 32 | hash rank
+                tk[g] = ((key & 0xFFFFFFFFull) << dbits) | (key >> 32);  // reference order (hash, dst)
             }, s);
         }
-        GroupOrder go = order_groups(ng, c.start, first_ev.p, s);
+        GroupOrder go = order_groups(ng, c.start, first_ev.p, s, tie.p, (uint64_t)nH << db);
         out.dd_off.alloc(ng + 1, s);
         DBuf<uint64_t> total(1, s);
         scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.dd_off.p}, s, total.p);
@@ -812,20 +858,28 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
         const uint32_t ng = read_u32(gcount.p, s);
         r.rt_groups = ng;
         DBuf<uint32_t> first_ev(ng, s), gsize(ng, s), trip_group(nt, s);
+        DBuf<uint64_t> tie(ng, s);
         {
             const uint32_t *gs = gstart.p;
             uint32_t *fe = first_ev.p, *sz = gsize.p;
+            uint64_t *tk = tie.p;
             const uint32_t ntt = nt;
+            const int dbits = db;
+            const int32_t *dst = c.dst;
             for_each(ng, [=] __device__(size_t g) {
-                fe[g] = H[sval[tv[gs[g]]] >> 1];
+                const uint32_t p = tv[gs[g]], e = H[sval[p] >> 1];
+                fe[g] = e;
                 sz[g] = ((g + 1 < ng) ? gs[g + 1] : ntt) - gs[g];
+                const uint64_t key = sk[p];  // src << 32 | hash rank
+                // reference order (hash, src, dst)
+                tk[g] = ((((key & 0xFFFFFFFFull) << dbits) | (key >> 32)) << dbits) | (uint64_t)(uint32_t)dst[e];
             }, s);
         }
         {
             uint32_t *tg = trip_group.p;
             scan<SumU32>(nt, HeadLoad<1>{tk}, StoreInclMinus1{tg}, s);  // group id of every sorted trip
         }
-        GroupOrder go = order_groups(ng, c.start, first_ev.p, s);
+        GroupOrder go = order_groups(ng, c.start, first_ev.p, s, tie.p, (uint64_t)nH << (2 * db));
         out.rt_off.alloc(ng + 1, s);
         DBuf<uint64_t> total(1, s);
         scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.rt_off.p}, s, total.p);
@@ -1349,6 +1403,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     g_masks.sa_tt = live_mask(hm[5] ^ hm[10]);
     g_masks.dev = live_range((uint64_t)(c.ndev > 0 ? c.ndev : 1));
     g_masks.idx = live_range(n);
+    g_masks.n = n;
     g_masks.srank = srank.p;
 
     pc.mark("partition");
@@ -1873,6 +1928,31 @@ int b2l_stable_sort_u32(const uint32_t *keys, uint64_t n, uint32_t *out_perm) {
         const uint32_t *kk = k32.p;
         ana::for_each(n, [=] __device__(size_t i) { k0[i] = kk[i], v[i] = (uint32_t)i; }, s);
         radix_sort<1>(st.b, n, LiveBytes<1>{{0x0F}}, s);
+        read_back(out_perm, st.val(), n * sizeof(uint32_t), s);
+        return B2L_OK;
+    } catch (const b2l::EngineErr &e) {
+        return b2l::fail(e.code, e.msg);
+    }
+}
+
+int b2l_stable_sort_u64(const uint64_t *keys, uint64_t n, uint32_t strategy, uint32_t *out_perm) {
+    if (n && (!keys || !out_perm)) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
+    if (strategy > 1 && (strategy < 16 || strategy > 23)) return b2l::fail(B2L_E_INVALID_ARG, "unknown strategy");
+    if (n == 0) return B2L_OK;
+    try {
+        using namespace b2l;
+        std::lock_guard<std::mutex> lock(ana::g_mu);
+        cudaStream_t s = ana::engine_stream();
+        SortStore<1> st(n, s);
+        CK(cudaMemcpyAsync(st.in_key(0), keys, n * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+        uint32_t *v = st.in_val();
+        ana::for_each(n, [=] __device__(size_t i) { v[i] = (uint32_t)i; }, s);
+        uint64_t o = 0, a = ~0ull;
+        for (uint64_t i = 0; i < n; ++i) o |= keys[i], a &= keys[i];
+        const uint8_t live = live_mask(o ^ a);
+        if (strategy == 0) radix_sort<1>(st.b, n, LiveBytes<1>{{live}}, s);
+        else if (strategy == 1) radix_sort_wide(st.b, n, live, s);
+        else radix_sort_prefix(st.b, n, live, (int)strategy - 16, s);
         read_back(out_perm, st.val(), n * sizeof(uint32_t), s);
         return B2L_OK;
     } catch (const b2l::EngineErr &e) {

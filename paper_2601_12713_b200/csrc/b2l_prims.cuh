@@ -432,7 +432,7 @@ __device__ __forceinline__ uint32_t block256_excl(uint32_t v, uint32_t *wsum, ui
 }
 
 template <int KW>
-__global__ void __launch_bounds__(OS_THREADS) k_onesweep(KeyCols<KW> in, const uint32_t *__restrict__ vin,
+__global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(KeyCols<KW> in, const uint32_t *__restrict__ vin,
                                                          KeyCols<KW> out, uint32_t *__restrict__ vout, size_t n,
                                                          int word, int shift, const uint32_t *__restrict__ hist,
                                                          uint32_t *status, uint32_t *tile_counter) {
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(OS_THREADS) k_onesweep(KeyCols<KW> in, const u
         for (int64_t j = (int64_t)tile - 1; !done; j -= 4) {
             uint32_t v[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = j - u >= 0 ? st[(size_t)(j - u) * 256 + t] : LB_INC;
+            for (int u = 0; u < 4; ++u) v[u] = j - u >= 0 ? st[(size_t)(j - u) * 256 + t] : (uint32_t)LB_INC;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 if (done) break;
@@ -612,6 +612,180 @@ inline uint8_t live_mask(uint64_t vary) {
     for (int b = 0; b < 8; ++b)
         if ((vary >> (8 * b)) & 255ull) m |= (uint8_t)(1u << b);
     return m;
+}
+
+static __global__ void k_gather_kv(const uint32_t *__restrict__ P, size_t m, const uint64_t *__restrict__ k,
+                            const uint32_t *__restrict__ v, uint64_t *__restrict__ ko, uint32_t *__restrict__ vo) {
+    for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (size_t)gridDim.x * blockDim.x)
+        ko[j] = k[P[j]], vo[j] = v[P[j]];
+}
+static __global__ void k_scatter_kv(const uint32_t *__restrict__ P, size_t m, const uint64_t *__restrict__ k,
+                             const uint32_t *__restrict__ v, uint64_t *__restrict__ ko, uint32_t *__restrict__ vo) {
+    for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (size_t)gridDim.x * blockDim.x)
+        ko[P[j]] = k[j], vo[P[j]] = v[j];
+}
+// ---------------------------------------------------------------- segmented fix-up sort
+// Records (u64 key, u32 value) already stably ordered by the key's prefix (key >> shift) become
+// stably ordered by the full key in one pass: every run of equal prefixes of length <= FIX_T is
+// ranked in place by each of its members (reads of the run only); longer runs are flagged and
+// sorted afterwards by a full-key LSD sort of just their records.  Used where random keys have
+// few records per prefix: the hash sort needs LSD passes over ~log2(n)+1 prefix bits instead of
+// all 64, and records generated in hash-rank order need no LSD pass at all.
+constexpr uint32_t FIX_T = 32;
+
+constexpr int FX_THREADS = 256, FX_ITEMS = 8, FX_TILE = FX_THREADS * FX_ITEMS;
+// One tile of positions plus a FIX_T halo on each side in shared memory: run bounds and ranks
+// come from shared memory (global reads only at the rare run that reaches past the halo).
+static __global__ void __launch_bounds__(FX_THREADS) k_seg_fixup(const uint64_t *__restrict__ kin,
+                                                                 const uint32_t *__restrict__ vin,
+                                                                 uint64_t *__restrict__ kout,
+                                                                 uint32_t *__restrict__ vout, size_t n, int shift,
+                                                                 uint8_t *__restrict__ big, uint32_t *big_count) {
+    __shared__ uint64_t sk[FX_TILE + 2 * FIX_T];
+    const size_t t0 = (size_t)blockIdx.x * FX_TILE;
+    const size_t lo = t0 >= FIX_T ? t0 - FIX_T : 0;
+    const size_t hi = t0 + FX_TILE + FIX_T < n ? t0 + FX_TILE + FIX_T : n;
+    for (size_t j = lo + threadIdx.x; j < hi; j += FX_THREADS) sk[j - lo] = kin[j];
+    __syncthreads();
+    auto K = [&](size_t j) -> uint64_t { return (j >= lo && j < hi) ? sk[j - lo] : kin[j]; };
+    uint32_t nbig = 0;
+#pragma unroll 1
+    for (int it = 0; it < FX_ITEMS; ++it) {
+        const size_t i = t0 + (size_t)it * FX_THREADS + threadIdx.x;
+        if (i >= n) break;
+        const uint64_t key = sk[i - lo], pre = key >> shift;
+        size_t a = i;
+        while (a > 0 && i - a < FIX_T && (K(a - 1) >> shift) == pre) --a;
+        bool isbig = a > 0 && (K(a - 1) >> shift) == pre;
+        size_t b = i + 1;
+        if (!isbig) {
+            while (b < n && b - a < FIX_T && (K(b) >> shift) == pre) ++b;
+            isbig = (b < n && (K(b) >> shift) == pre) || b - a > FIX_T;  // a run of FIX_T + 1 ends here
+        }
+        big[i] = isbig;
+        if (isbig) {  // stays in place unless its run holds distinct keys (fixed up afterwards)
+            ++nbig;
+            kout[i] = key;
+            vout[i] = vin[i];
+            continue;
+        }
+        uint32_t rank = 0;
+        for (size_t j = a; j < b; ++j) {
+            const uint64_t kj = K(j);
+            rank += (kj < key || (kj == key && j < i)) ? 1u : 0u;
+        }
+        kout[a + rank] = key;
+        vout[a + rank] = vin[i];
+    }
+    if (nbig) atomicAdd(big_count, nbig);
+}
+static __global__ void k_compose_idx(const uint32_t *__restrict__ P, const uint32_t *__restrict__ S, size_t m,
+                                     uint32_t *__restrict__ out) {
+    for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (size_t)gridDim.x * blockDim.x)
+        out[j] = P[S[j]];
+}
+// Over the long-run positions P (ascending): a run starts where positions jump or the prefix changes.
+struct RunHeadLoad {
+    const uint32_t *P;
+    const uint64_t *k;
+    int shift;
+    __device__ uint32_t operator()(size_t j) const {
+        return (j == 0 || P[j - 1] + 1 != P[j] || (k[P[j - 1]] >> shift) != (k[P[j]] >> shift)) ? 1u : 0u;
+    }
+};
+struct RunIdStore {  // run id per long-run record; flag runs whose neighbours differ in the full key
+    const uint32_t *P;
+    const uint64_t *k;
+    uint32_t *rid, *rflag;
+    __device__ void operator()(size_t j, uint32_t ex, uint32_t it) const {
+        const uint32_t r = ex + it - 1;
+        rid[j] = r;
+        if (!it && k[P[j - 1]] != k[P[j]]) rflag[r] = 1;
+    }
+};
+struct RunFlagged {
+    const uint32_t *rid, *rflag;
+    __device__ bool operator()(size_t j) const { return rflag[rid[j]] != 0; }
+};
+struct BigPred {
+    const uint8_t *big;
+    __device__ bool operator()(size_t i) const { return big[i] != 0; }
+};
+
+// b.cur holds records ordered by key >> shift; on return b.cur holds them ordered by the full key.
+// `live` = the key bytes that may vary (for the long-run fallback).
+inline void seg_fixup(SortBufs<1> &b, size_t n, int shift, uint8_t live, cudaStream_t s) {
+    if (n <= 1) return;
+    DBuf<uint8_t> big(n, s);
+    DBuf<uint32_t> cnt(1, s);
+    cnt.zero();
+    const uint64_t *kin = b.k[b.cur].w[0];
+    const uint32_t *vin = b.v[b.cur];
+    uint64_t *kout = b.k[b.cur ^ 1].w[0];
+    uint32_t *vout = b.v[b.cur ^ 1];
+    k_seg_fixup<<<(unsigned)((n + FX_TILE - 1) / FX_TILE), FX_THREADS, 0, s>>>(kin, vin, kout, vout, n, shift, big.p,
+                                                                            cnt.p);
+    CK_LAUNCH("k_seg_fixup");
+    b.cur ^= 1;
+    uint32_t nbig = 0;
+    read_back(&nbig, cnt.p, sizeof(nbig), s);
+    if (!nbig) return;
+    // long runs: those holding one key repeated are already in order; the others (a "break": equal
+    // prefix, different key, between neighbours) are gathered, full-key sorted, scattered back
+    DBuf<uint32_t> pos(nbig, s), pc(1, s);
+    compact(n, BigPred{big.p}, pos.p, pc.p, s);
+    DBuf<uint32_t> rid(nbig, s), rflag(nbig, s), sel(nbig, s), nsel(1, s);
+    rflag.zero();
+    const uint32_t *P = pos.p;
+    scan<SumU32>(nbig, RunHeadLoad{P, kin, shift}, RunIdStore{P, kin, rid.p, rflag.p}, s);
+    compact(nbig, RunFlagged{rid.p, rflag.p}, sel.p, nsel.p, s);
+    const uint32_t m = [&] {
+        uint32_t v = 0;
+        read_back(&v, nsel.p, sizeof(v), s);
+        return v;
+    }();
+    if (!m) return;
+    DBuf<uint64_t> k2[2] = {DBuf<uint64_t>(m, s), DBuf<uint64_t>(m, s)};
+    DBuf<uint32_t> v2[2] = {DBuf<uint32_t>(m, s), DBuf<uint32_t>(m, s)}, P2(m, s);
+    {
+        const uint32_t *S = sel.p;
+        uint32_t *p2 = P2.p;
+        k_compose_idx<<<grid_for(m, 256), 256, 0, s>>>(P, S, m, p2);
+        CK_LAUNCH("k_compose_idx");
+    }
+    SortBufs<1> sb;
+    sb.k[0].w[0] = k2[0].p, sb.k[1].w[0] = k2[1].p, sb.v[0] = v2[0].p, sb.v[1] = v2[1].p, sb.cur = 0;
+    k_gather_kv<<<grid_for(m, 256), 256, 0, s>>>(P2.p, m, kin, vin, k2[0].p, v2[0].p);
+    CK_LAUNCH("k_gather_kv");
+    radix_sort<1>(sb, m, LiveBytes<1>{{live}}, s);
+    k_scatter_kv<<<grid_for(m, 256), 256, 0, s>>>(P2.p, m, sb.k[sb.cur].w[0], sb.v[sb.cur], kout, vout);
+    CK_LAUNCH("k_scatter_kv");
+}
+
+// Stable sort by a u64 key: LSD passes over the live bytes at and above `lowbyte` only, then the
+// segmented fix-up orders runs of equal high parts by the full key.
+inline void radix_sort_prefix(SortBufs<1> &b, size_t n, uint8_t live, int lowbyte, cudaStream_t s) {
+    if (n <= 1 || !live) return;
+    const uint8_t top = (uint8_t)(live & (0xFFu << lowbyte));
+    if (top == live || !top) {  // nothing below the prefix, or no prefix: plain LSD
+        radix_sort<1>(b, n, LiveBytes<1>{{live}}, s);
+        return;
+    }
+    radix_sort<1>(b, n, LiveBytes<1>{{top}}, s);
+    seg_fixup(b, n, 8 * lowbyte, live, s);
+}
+
+// Random, well-spread keys (content hashes): LSD over just enough of the most significant live
+// bytes for ~1 bit of slack over log2(n), then the fix-up (most runs have one record).
+inline void radix_sort_wide(SortBufs<1> &b, size_t n, uint8_t live, cudaStream_t s) {
+    if (n <= 1 || !live) return;
+    int need = 2;
+    while (need < 64 && (1ull << need) < (uint64_t)n) ++need;
+    const int nbytes = (need + 1 + 7) / 8;
+    int got = 0, low = 0;
+    for (int byte = 7; byte >= 0 && got < nbytes; --byte)
+        if ((live >> byte) & 1) ++got, low = byte;
+    radix_sort_prefix(b, n, live, low, s);
 }
 
 // Owning storage for a sort of n records.
