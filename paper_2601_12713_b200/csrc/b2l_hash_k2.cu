@@ -3,16 +3,21 @@
 //
 // f_w(h) = (h ^ w) * P is a T-function: bits [k, k+4) of the output depend only on bits < k+4
 // of the inputs.  Processing the 64-bit state in 16 groups of 4 bits, once bits < k of every
-// intermediate state are known (kept as R_i = (x_i mod 2^k) * P per word, x_i = h_i ^ w_i),
+// intermediate state are known (x_i = h_i ^ w_i known mod 2^k, R_i = (x_i mod 2^k) * P),
 // the 4-bit group of the chain obeys
 //     h4_{i+1} = ((R_i >> k) + 3 * (h4_i ^ w4_i)) mod 16        (P = 2^40 + 435 = 3 mod 16)
-// so every run of words is a map {0..15} -> {0..15}: a 16-nibble table, built for all 16
-// inputs at once with SWAR nibble arithmetic in one u64.  Tables compose associatively, so a
-// group resolves by a prefix composition across threads (warp shuffles), warps and CTAs
-// (decoupled look-back); a second pass with the actual input state advances R_i by
-// (x4_i << k) * P.  The buffer is read from HBM once: each CTA keeps its 32 KiB chunk in
-// registers for all 16 groups; chunks beyond the co-resident grid are processed in rounds
-// chained through a per-group carry.  Verified bit-exact against the serial fold (tests).
+// so every run of words is a map {0..15} -> {0..15}: a 16-byte table, built for all 16 inputs
+// at once with byte-parallel arithmetic.  Tables compose associatively, so a group resolves by
+// a prefix composition across threads (warp shuffles), warps, and CTAs; a second pass with the
+// actual input state writes the resolved bits back.
+//
+// v5 layout: each word lives in shared memory as ONE u64 y_i whose bits < k already hold x_i
+// (resolved) and bits >= k still hold w_i, so R_i's nibble is recomputed from y_i (one or two
+// IMADs) instead of being kept in registers -- 24 Ki words per CTA per round (192 KiB of smem,
+// 512 threads), fewer rounds.  Across CTAs every CTA publishes its aggregate map and composes
+// all predecessors' aggregates itself (a warp reads them in parallel): no serial look-back
+// chain through the grid.  Chunks beyond the co-resident grid are processed in rounds chained
+// through a per-group carry.  Verified bit-exact against the serial fold (tests).
 #include <cooperative_groups.h>
 
 #include "b2l_common.cuh"
@@ -20,17 +25,14 @@
 namespace b2l {
 namespace k2 {
 
-constexpr int THREADS = 256;
-constexpr int WPT = 64;                   // words per thread: payload words in smem, R_i in registers
-constexpr int CHUNK = THREADS * WPT;      // words per CTA per round (128 KiB)
+constexpr int THREADS = 512;
+constexpr int WARPS = THREADS / 32;
+constexpr int WPT = 48;                   // words per thread, resident in shared memory
+constexpr int CHUNK = THREADS * WPT;      // words per CTA per round (192 KiB)
 constexpr size_t SMEM = (size_t)THREADS * (WPT + 1) * sizeof(uint64_t);
 
-// Look-back slots: a map is 16 bytes whose entries use only the low nibble, so the high
+// Aggregate slots: a map is 16 bytes whose entries use only the low nibble, so the high
 // nibble of byte 0 marks a published slot and map + mark travel in one 16-byte access.
-struct Status {
-    uint4 agg;   // this CTA's map, marked 0x10 once published
-    uint4 incl;  // maps of CTAs 0..c of the round, marked 0x10 once published
-};
 constexpr uint32_t MARK = 0x10u;
 __device__ __forceinline__ uint4 ld_slot(const uint4 *p) {
     uint4 v;
@@ -109,47 +111,67 @@ __device__ __forceinline__ uint64_t load_word(const uint8_t *buf, uint64_t n, ui
     return w;
 }
 
+// Bits [k, k+4) of R = (y mod 2^k) * P, P = 2^40 + 435 (k a multiple of 4, warp-uniform).
+__device__ __forceinline__ uint32_t r_nib(uint64_t y, int k) {
+    if (k == 0) return 0;
+    if (k <= 28) {  // the nibble lies in the low word: (y mod 2^k) * 435, 32-bit
+        const uint32_t lo = (uint32_t)y & ((1u << k) - 1u);
+        return ((lo * 435u) >> k) & 15u;
+    }
+    const uint64_t low = y & ((1ull << k) - 1ull);
+    return (uint32_t)((low * FNV_PRIME) >> k) & 15u;
+}
+
 __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__restrict__ buf, uint64_t nbytes,
-                                                            Status *status, unsigned long long *carry,
+                                                            uint4 *aggs, unsigned long long *carry,
                                                             uint64_t *digest) {
     extern __shared__ uint64_t stage[];  // THREADS x (WPT + 1) words, padded: conflict-free row reads
-    __shared__ uint4 warp_tab[THREADS / 32];
-    __shared__ uint32_t warp_in[THREADS / 32];
+    __shared__ uint4 warp_tab[WARPS];
+    __shared__ uint32_t warp_in[WARPS];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint32_t G = gridDim.x, c = blockIdx.x;
     const uint64_t nw = (nbytes + 7) >> 3;
     const uint64_t nchunks = (nw + CHUNK - 1) / CHUNK;
     const uint64_t rounds = (nchunks + G - 1) / G;
     volatile unsigned long long *vcarry = carry;
+    constexpr int Q = WPT / 4;
 
     for (uint64_t r = 0; r < rounds; ++r) {
         const uint64_t q = r * G + c;
         if (q >= nchunks) break;  // only the last round has idle CTAs, and nobody waits on them
         const uint64_t last_in_round = (nchunks - r * G < G ? nchunks - r * G : G) - 1;
-        uint64_t R[WPT];
+        const uint32_t nc = (uint32_t)(last_in_round + 1);  // CTAs active in this round
         const uint64_t base = q * CHUNK;
         for (int idx = t; idx < CHUNK; idx += THREADS) {
             const uint64_t i = base + idx;
             stage[(idx / WPT) * (WPT + 1) + idx % WPT] = i < nw ? load_word(buf, nbytes, i) : 0ull;
         }
         __syncthreads();
-#pragma unroll
-        for (int j = 0; j < WPT; ++j) R[j] = 0;
-        const uint64_t *w = stage + t * (WPT + 1);  // this thread's words, resident for the round
+        uint64_t *w = stage + t * (WPT + 1);  // this thread's words, resident for the round
         const int64_t left = (int64_t)nw - (int64_t)(base + (uint64_t)t * WPT);
         const int nv = left <= 0 ? 0 : (left >= WPT ? WPT : (int)left);
+#pragma unroll 1
         for (int g = 0; g < 16; ++g) {
             const int k = 4 * g;
             const uint64_t slot = r * 16 + g;
-            // ---- pass A: this thread's map over its words, as four independent quarter chains (ILP)
-            constexpr int Q = WPT / 4;
+            // ---- pass A: this thread's map over its words (four independent quarter chains);
+            // the (w, R) nibbles are kept for pass B, 8 per register
+            uint32_t wn[WPT / 8], rn[WPT / 8];
+#pragma unroll
+            for (int m = 0; m < WPT / 8; ++m) wn[m] = 0, rn[m] = 0;
             Tab Tq[4] = {tab_id(), tab_id(), tab_id(), tab_id()};
 #pragma unroll
             for (int j = 0; j < Q; ++j) {
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
                     const int jj = h * Q + j;
-                    if (jj < nv) tab_step(Tq[h], (uint32_t)(w[jj] >> k) & 15u, (uint32_t)(R[jj] >> k) & 15u);
+                    if (jj < nv) {
+                        const uint64_t y = w[jj];
+                        const uint32_t w4 = (uint32_t)(y >> k) & 15u, r4 = r_nib(y, k);
+                        wn[jj / 8] |= w4 << (4 * (jj % 8));
+                        rn[jj / 8] |= r4 << (4 * (jj % 8));
+                        tab_step(Tq[h], w4, r4);
+                    }
                 }
             }
             const Tab T01 = tab_compose(Tq[0], Tq[1]);
@@ -165,39 +187,37 @@ __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__res
             if (lane == 31) warp_tab[warp] = tab_pack(T);
             __syncthreads();
             if (warp == 0) {
-                // prefix over the 8 warps (lanes 0..7), CTA aggregate in lane 7
-                Tab W = lane < THREADS / 32 ? tab_unpack(warp_tab[lane]) : tab_id();
+                // prefix over the warps (lanes 0..WARPS-1), CTA aggregate in lane WARPS-1
+                Tab W = lane < WARPS ? tab_unpack(warp_tab[lane]) : tab_id();
 #pragma unroll
-                for (int d = 1; d < THREADS / 32; d <<= 1) {
+                for (int d = 1; d < WARPS; d <<= 1) {
                     const Tab o = tab_shfl_up(W, d);
                     if (lane >= d) W = tab_compose(o, W);
                 }
                 const Tab wexcl = tab_shfl_up(W, 1);
                 Tab agg;
 #pragma unroll
-                for (int m = 0; m < 4; ++m) agg.r[m] = __shfl_sync(0xffffffffu, W.r[m], THREADS / 32 - 1);
-                // decoupled look-back (lane 0): publish the aggregate, walk back to the nearest
-                // published inclusive prefix, publish our inclusive prefix
+                for (int m = 0; m < 4; ++m) agg.r[m] = __shfl_sync(0xffffffffu, W.r[m], WARPS - 1);
+                uint4 *row = aggs + slot * G;
+                if (lane == 0 && c + 1 < nc) st_slot(&row[c], tab_pack(agg));  // the last CTA's is never read
+                // prefix of the predecessors' aggregates: lane l composes a contiguous block of
+                // them (in order), then a warp scan composes the blocks
+                const uint32_t per = (c + 31) / 32, b0 = lane * per, b1 = b0 + per < c ? b0 + per : c;
                 Tab P = tab_id();
-                if (lane == 0) {
-                    Status *me = status + slot * G + c;
-                    if (c > 0) {
-                        st_slot(&me->agg, tab_pack(agg));
-                        for (int64_t j = (int64_t)c - 1; j >= 0;) {
-                            const uint4 inc = ld_slot(&status[slot * G + j].incl);
-                            if (inc.x & MARK) {
-                                P = tab_compose(tab_unpack(unmark(inc)), P);
-                                break;
-                            }
-                            const uint4 ag = ld_slot(&status[slot * G + j].agg);
-                            if (ag.x & MARK) {
-                                P = tab_compose(tab_unpack(unmark(ag)), P);
-                                --j;
-                            }
-                        }
-                    }
-                    st_slot(&me->incl, tab_pack(tab_compose(P, agg)));
+                for (uint32_t j = b0; j < b1; ++j) {
+                    uint4 v;
+                    do {
+                        v = ld_slot(&row[j]);
+                    } while (!(v.x & MARK));
+                    P = tab_compose(P, tab_unpack(unmark(v)));
                 }
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const Tab o = tab_shfl_up(P, d);
+                    if (lane >= d) P = tab_compose(o, P);
+                }
+#pragma unroll
+                for (int m = 0; m < 4; ++m) P.r[m] = __shfl_sync(0xffffffffu, P.r[m], 31);
                 uint32_t s_cta = 0;
                 if (lane == 0) {
                     uint32_t s_round;  // the group's state entering this round
@@ -211,17 +231,18 @@ __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__res
                         s_round = (uint32_t)v & 15u;
                     }
                     s_cta = tab_apply(P, s_round);
-                    if (q == r * G + last_in_round) {  // last chunk of the round: carry its output state
+                    if (c == last_in_round) {  // last chunk of the round: carry its output state
                         __threadfence();
                         atomicExch(&carry[slot], 0x100ull | tab_apply(agg, s_cta));
                     }
                 }
                 s_cta = __shfl_sync(0xffffffffu, s_cta, 0);
-                if (lane < THREADS / 32) warp_in[lane] = lane == 0 ? s_cta : tab_apply(wexcl, s_cta);
+                if (lane < WARPS) warp_in[lane] = lane == 0 ? s_cta : tab_apply(wexcl, s_cta);
             }
             __syncthreads();
             // ---- pass B with the actual input state, the four quarters at once (quarter h's
-            // input is the composed map of the quarters before it applied to the thread's input)
+            // input is the composed map of the quarters before it applied to the thread's input);
+            // the resolved nibble x4 = h4 ^ w4 replaces w4 in y: y ^= h4 << k
             const uint32_t sin = lane == 0 ? warp_in[warp] : tab_apply(excl_lane, warp_in[warp]);
             uint32_t sq[4] = {sin, tab_apply(Tq[0], sin), tab_apply(T01, sin), tab_apply(T012, sin)};
 #pragma unroll
@@ -230,9 +251,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__res
                 for (int h = 0; h < 4; ++h) {
                     const int jj = h * Q + j;
                     if (jj < nv) {
-                        const uint32_t x4 = sq[h] ^ ((uint32_t)(w[jj] >> k) & 15u);
-                        sq[h] = (((uint32_t)(R[jj] >> k) & 15u) + 3u * x4) & 15u;
-                        R[jj] += ((uint64_t)x4 << k) * FNV_PRIME;
+                        const uint32_t w4 = (wn[jj / 8] >> (4 * (jj % 8))) & 15u;
+                        const uint32_t r4 = (rn[jj / 8] >> (4 * (jj % 8))) & 15u;
+                        w[jj] ^= (uint64_t)sq[h] << k;
+                        sq[h] = (r4 + 3u * (sq[h] ^ w4)) & 15u;
                     }
                 }
             }
@@ -256,7 +278,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__res
 
 struct Ctx {
     int grid = 0;
-    Status *status = nullptr;
+    uint4 *status = nullptr;
     unsigned long long *carry = nullptr;
     size_t status_cap = 0, carry_cap = 0;
 };
@@ -299,7 +321,7 @@ int hash_planes_launch(const void *d_buf, uint64_t nbytes, uint64_t *d_digest, c
         if (C.status) cudaFree(C.status);
         C.status = nullptr;
         C.status_cap = 0;
-        B2L_CUDA(cudaMalloc(&C.status, need_st * sizeof(k2::Status)));
+        B2L_CUDA(cudaMalloc(&C.status, need_st * sizeof(uint4)));
         C.status_cap = need_st;
     }
     if (C.carry_cap < need_c) {
@@ -309,7 +331,7 @@ int hash_planes_launch(const void *d_buf, uint64_t nbytes, uint64_t *d_digest, c
         B2L_CUDA(cudaMalloc(&C.carry, need_c * sizeof(unsigned long long)));
         C.carry_cap = need_c;
     }
-    B2L_CUDA(cudaMemsetAsync(C.status, 0, need_st * sizeof(k2::Status), stream));
+    B2L_CUDA(cudaMemsetAsync(C.status, 0, need_st * sizeof(uint4), stream));
     B2L_CUDA(cudaMemsetAsync(C.carry, 0, need_c * sizeof(unsigned long long), stream));
     const uint8_t *b = (const uint8_t *)d_buf;
     void *args[] = {(void *)&b, (void *)&nbytes, (void *)&C.status, (void *)&C.carry, (void *)&d_digest};

@@ -634,35 +634,64 @@ static __global__ void k_scatter_kv(const uint32_t *__restrict__ P, size_t m, co
 constexpr uint32_t FIX_T = 32;
 
 constexpr int FX_THREADS = 256, FX_ITEMS = 8, FX_TILE = FX_THREADS * FX_ITEMS;
-// One tile of positions plus a FIX_T halo on each side in shared memory: run bounds and ranks
-// come from shared memory (global reads only at the rare run that reaches past the halo).
+constexpr int FX_WIN = FX_TILE + 2 * FIX_T;   // tile plus halo, positions relative to lo
+constexpr int FX_HW = FX_WIN / 32 + 2;        // head-bit words (+ end sentinel)
+// One tile of positions plus a FIX_T halo on each side in shared memory, with a bitmask of run
+// heads: each record finds its run [a, b) with two bit scans (no walking); runs longer than FIX_T
+// are left in place and flagged, shorter ones are ranked from shared memory.
 static __global__ void __launch_bounds__(FX_THREADS) k_seg_fixup(const uint64_t *__restrict__ kin,
                                                                  const uint32_t *__restrict__ vin,
                                                                  uint64_t *__restrict__ kout,
                                                                  uint32_t *__restrict__ vout, size_t n, int shift,
                                                                  uint8_t *__restrict__ big, uint32_t *big_count) {
-    __shared__ uint64_t sk[FX_TILE + 2 * FIX_T];
+    __shared__ uint64_t sk[FX_WIN];
+    __shared__ uint32_t hb[FX_HW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t t0 = (size_t)blockIdx.x * FX_TILE;
     const size_t lo = t0 >= FIX_T ? t0 - FIX_T : 0;
     const size_t hi = t0 + FX_TILE + FIX_T < n ? t0 + FX_TILE + FIX_T : n;
-    for (size_t j = lo + threadIdx.x; j < hi; j += FX_THREADS) sk[j - lo] = kin[j];
+    const int wn = (int)(hi - lo);
+    for (int j = threadIdx.x; j < wn; j += FX_THREADS) sk[j] = kin[lo + j];
+    for (int j = threadIdx.x; j < FX_HW; j += FX_THREADS) hb[j] = 0;
     __syncthreads();
-    auto K = [&](size_t j) -> uint64_t { return (j >= lo && j < hi) ? sk[j - lo] : kin[j]; };
+    // head bits: position lo + j starts a run (global position 0 always does; n is a sentinel)
+    for (int w0 = warp * 32; w0 < wn + 1; w0 += FX_THREADS) {
+        const int j = w0 + lane;
+        bool h = false;
+        if (j < wn) h = (lo + j == 0) || (j > 0 && (sk[j] >> shift) != (sk[j - 1] >> shift));
+        else if (j == wn) h = hi == n;  // end of the keys: a run boundary
+        const uint32_t m = __ballot_sync(0xffffffffu, h);
+        if (lane == 0) hb[w0 >> 5] |= m;
+    }
+    __syncthreads();
+    // position lo + j, j = 0, is a head when j == 0 would need the key before lo: compare it
+    if (threadIdx.x == 0 && lo > 0 && (kin[lo - 1] >> shift) != (sk[0] >> shift)) hb[0] |= 1u;
+    __syncthreads();
     uint32_t nbig = 0;
 #pragma unroll 1
     for (int it = 0; it < FX_ITEMS; ++it) {
         const size_t i = t0 + (size_t)it * FX_THREADS + threadIdx.x;
         if (i >= n) break;
-        const uint64_t key = sk[i - lo], pre = key >> shift;
-        size_t a = i;
-        while (a > 0 && i - a < FIX_T && (K(a - 1) >> shift) == pre) --a;
-        bool isbig = a > 0 && (K(a - 1) >> shift) == pre;
-        size_t b = i + 1;
-        if (!isbig) {
-            while (b < n && b - a < FIX_T && (K(b) >> shift) == pre) ++b;
-            isbig = (b < n && (K(b) >> shift) == pre) || b - a > FIX_T;  // a run of FIX_T + 1 ends here
+        const int rel = (int)(i - lo);
+        // a = last head <= rel, searched in the word of rel and the one before
+        int a = -1;
+        {
+            const int wi = rel >> 5, bi = rel & 31;
+            const uint32_t m0 = hb[wi] & (bi == 31 ? 0xffffffffu : ((2u << bi) - 1u));
+            if (m0) a = wi * 32 + 31 - __clz(m0);
+            else if (wi > 0 && hb[wi - 1]) a = (wi - 1) * 32 + 31 - __clz(hb[wi - 1]);
         }
+        // b = first head > rel, searched in the word of rel and the one after
+        int b = -1;
+        {
+            const int wi = rel >> 5, bi = rel & 31;
+            const uint32_t m0 = bi == 31 ? 0u : (hb[wi] & ~((2u << bi) - 1u));
+            if (m0) b = wi * 32 + __ffs(m0) - 1;
+            else if (wi + 1 < FX_HW && hb[wi + 1]) b = (wi + 1) * 32 + __ffs(hb[wi + 1]) - 1;
+        }
+        const bool isbig = a < 0 || b < 0 || b - a > (int)FIX_T;
         big[i] = isbig;
+        const uint64_t key = sk[rel];
         if (isbig) {  // stays in place unless its run holds distinct keys (fixed up afterwards)
             ++nbig;
             kout[i] = key;
@@ -670,12 +699,12 @@ static __global__ void __launch_bounds__(FX_THREADS) k_seg_fixup(const uint64_t 
             continue;
         }
         uint32_t rank = 0;
-        for (size_t j = a; j < b; ++j) {
-            const uint64_t kj = K(j);
-            rank += (kj < key || (kj == key && j < i)) ? 1u : 0u;
+        for (int j = a; j < b; ++j) {
+            const uint64_t kj = sk[j];
+            rank += (kj < key || (kj == key && j < rel)) ? 1u : 0u;
         }
-        kout[a + rank] = key;
-        vout[a + rank] = vin[i];
+        kout[lo + a + rank] = key;
+        vout[lo + a + rank] = vin[i];
     }
     if (nbig) atomicAdd(big_count, nbig);
 }
