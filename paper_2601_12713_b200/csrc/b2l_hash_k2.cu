@@ -25,11 +25,12 @@
 namespace b2l {
 namespace k2 {
 
-constexpr int THREADS = 512;
+constexpr int THREADS = 256;
 constexpr int WARPS = THREADS / 32;
 constexpr int WPT = 48;                   // words per thread, resident in shared memory
-constexpr int CHUNK = THREADS * WPT;      // words per CTA per round (192 KiB)
-constexpr size_t SMEM = (size_t)THREADS * (WPT + 1) * sizeof(uint64_t);
+constexpr int CHUNK = THREADS * WPT;      // words per CTA per round (96 KiB; two CTAs per SM)
+constexpr int ROW = WPT + 1;              // padded row (u32 units): conflict-free column access
+constexpr size_t SMEM = (size_t)2 * THREADS * ROW * sizeof(uint32_t);  // lo and hi planes
 
 // Aggregate slots: a map is 16 bytes whose entries use only the low nibble, so the high
 // nibble of byte 0 marks a published slot and map + mark travel in one 16-byte access.
@@ -62,6 +63,16 @@ __device__ __forceinline__ void tab_step(Tab &T, uint32_t w4, uint32_t r4) {
     const uint32_t wb = w4 * 0x01010101u, rb = r4 * 0x01010101u;
 #pragma unroll
     for (int m = 0; m < 4; ++m) T.r[m] = ((T.r[m] ^ wb) * 3u + rb) & 0x0F0F0F0Fu;
+}
+// The same step on an unmasked table (entries < 64): the mask folds into the XOR (one LOP3),
+// so a step is LOP3 + IMAD per register; tab_mask() once after the run.
+__device__ __forceinline__ void tab_step_lazy(Tab &T, uint32_t wb, uint32_t rb) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) T.r[m] = ((T.r[m] & 0x0F0F0F0Fu) ^ wb) * 3u + rb;
+}
+__device__ __forceinline__ void tab_mask(Tab &T) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) T.r[m] &= 0x0F0F0F0Fu;
 }
 // (first A, then B): out[j] = B[A[j]]
 __device__ __forceinline__ Tab tab_compose(const Tab &A, const Tab &B) {
@@ -111,158 +122,177 @@ __device__ __forceinline__ uint64_t load_word(const uint8_t *buf, uint64_t n, ui
     return w;
 }
 
-// Bits [k, k+4) of R = (y mod 2^k) * P, P = 2^40 + 435 (k a multiple of 4, warp-uniform).
-__device__ __forceinline__ uint32_t r_nib(uint64_t y, int k) {
-    if (k == 0) return 0;
-    if (k <= 28) {  // the nibble lies in the low word: (y mod 2^k) * 435, 32-bit
-        const uint32_t lo = (uint32_t)y & ((1u << k) - 1u);
-        return ((lo * 435u) >> k) & 15u;
+// Bits [k, k+4) of R = (y mod 2^k) * P, P = 2^40 + 435, from the low / high 32-bit halves of y.
+// k < 32 (HI false): the nibble lies in the low word, (y mod 2^k) * 435 mod 2^32.
+// k >= 32 (HI true): the high word of the product: hi32(lo * 435) + (hi mod 2^(k-32)) * 435 + (lo << 8).
+template <bool HI>
+__device__ __forceinline__ uint32_t r_nib(uint32_t lo, uint32_t hi, int k) {
+    if (!HI) {
+        if (k == 0) return 0;
+        return (((lo & ((1u << k) - 1u)) * 435u) >> k) & 15u;
     }
-    const uint64_t low = y & ((1ull << k) - 1ull);
-    return (uint32_t)((low * FNV_PRIME) >> k) & 15u;
+    const int kh = k - 32;
+    const uint32_t hm = kh ? (hi & ((1u << kh) - 1u)) : 0u;
+    const uint32_t hw = __umulhi(lo, 435u) + hm * 435u + (lo << 8);
+    return (hw >> kh) & 15u;
 }
 
-__global__ void __launch_bounds__(THREADS, 1) k_hash_planes(const uint8_t *__restrict__ buf, uint64_t nbytes,
+struct Shared {
+    uint4 warp_tab[WARPS];
+    uint32_t warp_in[WARPS];
+};
+
+// One 4-bit group of one round: pass A (maps), the prefix across warps and CTAs, pass B
+// (resolved nibbles written back into y).  HI: the group lies in the high 32 bits.
+template <bool HI>
+__device__ __forceinline__ void group_step(uint32_t *ylo, uint32_t *yhi, int nv, int k, uint64_t r, uint64_t slot,
+                                           uint32_t c, uint32_t nc, uint32_t G, uint4 *aggs,
+                                           unsigned long long *carry, Shared &sh) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    constexpr int Q = WPT / 4;
+    const int ks = HI ? k - 32 : k;
+    uint32_t *ymine = HI ? yhi : ylo;
+    // ---- pass A: this thread's map over its words, four independent quarter chains
+    Tab Tq[4] = {tab_id(), tab_id(), tab_id(), tab_id()};
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const int jj = h * Q + j;
+            if (jj < nv) {
+                const uint32_t lo = ylo[jj], hi = HI ? yhi[jj] : 0u;
+                const uint32_t w4 = ((HI ? hi : lo) >> ks) & 15u, r4 = r_nib<HI>(lo, hi, k);
+                tab_step_lazy(Tq[h], w4 * 0x01010101u, r4 * 0x01010101u);
+            }
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < 4; ++h) tab_mask(Tq[h]);
+    const Tab T01 = tab_compose(Tq[0], Tq[1]);
+    const Tab T012 = tab_compose(T01, Tq[2]);
+    Tab T = tab_compose(T012, Tq[3]);
+    // ---- inclusive prefix composition across the warp (lane order)
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const Tab o = tab_shfl_up(T, d);
+        if (lane >= d) T = tab_compose(o, T);
+    }
+    const Tab excl_lane = tab_shfl_up(T, 1);
+    if (lane == 31) sh.warp_tab[warp] = tab_pack(T);
+    __syncthreads();
+    if (warp == 0) {
+        // prefix over the warps (lanes 0..WARPS-1), CTA aggregate in lane WARPS-1
+        Tab W = lane < WARPS ? tab_unpack(sh.warp_tab[lane]) : tab_id();
+#pragma unroll
+        for (int d = 1; d < WARPS; d <<= 1) {
+            const Tab o = tab_shfl_up(W, d);
+            if (lane >= d) W = tab_compose(o, W);
+        }
+        const Tab wexcl = tab_shfl_up(W, 1);
+        Tab agg;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) agg.r[m] = __shfl_sync(0xffffffffu, W.r[m], WARPS - 1);
+        uint4 *row = aggs + slot * G;
+        if (lane == 0 && c + 1 < nc) st_slot(&row[c], tab_pack(agg));  // the last CTA's is never read
+        // prefix of the predecessors' aggregates: lane l composes a contiguous block of them
+        // (in order), then a warp scan composes the blocks
+        const uint32_t per = (c + 31) / 32, b0 = lane * per, b1 = b0 + per < c ? b0 + per : c;
+        Tab P = tab_id();
+        for (uint32_t j = b0; j < b1; ++j) {
+            uint4 v;
+            do {
+                v = ld_slot(&row[j]);
+            } while (!(v.x & MARK));
+            P = tab_compose(P, tab_unpack(unmark(v)));
+        }
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const Tab o = tab_shfl_up(P, d);
+            if (lane >= d) P = tab_compose(o, P);
+        }
+#pragma unroll
+        for (int m = 0; m < 4; ++m) P.r[m] = __shfl_sync(0xffffffffu, P.r[m], 31);
+        uint32_t s_cta = 0;
+        if (lane == 0) {
+            uint32_t s_round;  // the group's state entering this round
+            if (r == 0) {
+                s_round = (uint32_t)(FNV_OFFSET >> k) & 15u;
+            } else {
+                volatile unsigned long long *vcarry = carry;
+                unsigned long long v;
+                do {
+                    v = vcarry[slot - 16];
+                } while (v == 0);
+                s_round = (uint32_t)v & 15u;
+            }
+            s_cta = tab_apply(P, s_round);
+            if (c + 1 == nc) {  // last chunk of the round: carry its output state
+                __threadfence();
+                atomicExch(&carry[slot], 0x100ull | tab_apply(agg, s_cta));
+            }
+        }
+        s_cta = __shfl_sync(0xffffffffu, s_cta, 0);
+        if (lane < WARPS) sh.warp_in[lane] = lane == 0 ? s_cta : tab_apply(wexcl, s_cta);
+    }
+    __syncthreads();
+    // ---- pass B with the actual input state, the four quarters at once (quarter h's input is
+    // the composed map of the quarters before it applied to the thread's input); the resolved
+    // nibble x4 = h4 ^ w4 replaces w4 in y: y ^= h4 << k
+    const uint32_t sin = lane == 0 ? sh.warp_in[warp] : tab_apply(excl_lane, sh.warp_in[warp]);
+    uint32_t sq[4] = {sin, tab_apply(Tq[0], sin), tab_apply(T01, sin), tab_apply(T012, sin)};
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const int jj = h * Q + j;
+            if (jj < nv) {
+                const uint32_t lo = ylo[jj], hi = HI ? yhi[jj] : 0u;
+                const uint32_t mine = HI ? hi : lo;
+                const uint32_t w4 = (mine >> ks) & 15u, r4 = r_nib<HI>(lo, hi, k);
+                ymine[jj] = mine ^ (sq[h] << ks);
+                sq[h] = (r4 + 3u * (sq[h] ^ w4)) & 15u;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(THREADS, 2) k_hash_planes(const uint8_t *__restrict__ buf, uint64_t nbytes,
                                                             uint4 *aggs, unsigned long long *carry,
                                                             uint64_t *digest) {
-    extern __shared__ uint64_t stage[];  // THREADS x (WPT + 1) words, padded: conflict-free row reads
-    __shared__ uint4 warp_tab[WARPS];
-    __shared__ uint32_t warp_in[WARPS];
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    extern __shared__ uint32_t planes[];  // lo plane then hi plane, THREADS x ROW each
+    __shared__ Shared sh;
+    const int t = threadIdx.x;
     const uint32_t G = gridDim.x, c = blockIdx.x;
     const uint64_t nw = (nbytes + 7) >> 3;
     const uint64_t nchunks = (nw + CHUNK - 1) / CHUNK;
     const uint64_t rounds = (nchunks + G - 1) / G;
-    volatile unsigned long long *vcarry = carry;
-    constexpr int Q = WPT / 4;
+    uint32_t *plo = planes, *phi = planes + THREADS * ROW;
 
     for (uint64_t r = 0; r < rounds; ++r) {
         const uint64_t q = r * G + c;
         if (q >= nchunks) break;  // only the last round has idle CTAs, and nobody waits on them
-        const uint64_t last_in_round = (nchunks - r * G < G ? nchunks - r * G : G) - 1;
-        const uint32_t nc = (uint32_t)(last_in_round + 1);  // CTAs active in this round
+        const uint32_t nc = (uint32_t)(nchunks - r * G < G ? nchunks - r * G : G);  // CTAs in this round
         const uint64_t base = q * CHUNK;
         for (int idx = t; idx < CHUNK; idx += THREADS) {
             const uint64_t i = base + idx;
-            stage[(idx / WPT) * (WPT + 1) + idx % WPT] = i < nw ? load_word(buf, nbytes, i) : 0ull;
+            const uint64_t v = i < nw ? load_word(buf, nbytes, i) : 0ull;
+            const int o = (idx / WPT) * ROW + idx % WPT;
+            plo[o] = (uint32_t)v;
+            phi[o] = (uint32_t)(v >> 32);
         }
         __syncthreads();
-        uint64_t *w = stage + t * (WPT + 1);  // this thread's words, resident for the round
+        uint32_t *ylo = plo + t * ROW, *yhi = phi + t * ROW;  // this thread's words, resident for the round
         const int64_t left = (int64_t)nw - (int64_t)(base + (uint64_t)t * WPT);
         const int nv = left <= 0 ? 0 : (left >= WPT ? WPT : (int)left);
 #pragma unroll 1
-        for (int g = 0; g < 16; ++g) {
-            const int k = 4 * g;
-            const uint64_t slot = r * 16 + g;
-            // ---- pass A: this thread's map over its words (four independent quarter chains);
-            // the (w, R) nibbles are kept for pass B, 8 per register
-            uint32_t wn[WPT / 8], rn[WPT / 8];
-#pragma unroll
-            for (int m = 0; m < WPT / 8; ++m) wn[m] = 0, rn[m] = 0;
-            Tab Tq[4] = {tab_id(), tab_id(), tab_id(), tab_id()};
-#pragma unroll
-            for (int j = 0; j < Q; ++j) {
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    const int jj = h * Q + j;
-                    if (jj < nv) {
-                        const uint64_t y = w[jj];
-                        const uint32_t w4 = (uint32_t)(y >> k) & 15u, r4 = r_nib(y, k);
-                        wn[jj / 8] |= w4 << (4 * (jj % 8));
-                        rn[jj / 8] |= r4 << (4 * (jj % 8));
-                        tab_step(Tq[h], w4, r4);
-                    }
-                }
-            }
-            const Tab T01 = tab_compose(Tq[0], Tq[1]);
-            const Tab T012 = tab_compose(T01, Tq[2]);
-            Tab T = tab_compose(T012, Tq[3]);
-            // ---- inclusive prefix composition across the warp (lane order)
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const Tab o = tab_shfl_up(T, d);
-                if (lane >= d) T = tab_compose(o, T);
-            }
-            const Tab excl_lane = tab_shfl_up(T, 1);
-            if (lane == 31) warp_tab[warp] = tab_pack(T);
-            __syncthreads();
-            if (warp == 0) {
-                // prefix over the warps (lanes 0..WARPS-1), CTA aggregate in lane WARPS-1
-                Tab W = lane < WARPS ? tab_unpack(warp_tab[lane]) : tab_id();
-#pragma unroll
-                for (int d = 1; d < WARPS; d <<= 1) {
-                    const Tab o = tab_shfl_up(W, d);
-                    if (lane >= d) W = tab_compose(o, W);
-                }
-                const Tab wexcl = tab_shfl_up(W, 1);
-                Tab agg;
-#pragma unroll
-                for (int m = 0; m < 4; ++m) agg.r[m] = __shfl_sync(0xffffffffu, W.r[m], WARPS - 1);
-                uint4 *row = aggs + slot * G;
-                if (lane == 0 && c + 1 < nc) st_slot(&row[c], tab_pack(agg));  // the last CTA's is never read
-                // prefix of the predecessors' aggregates: lane l composes a contiguous block of
-                // them (in order), then a warp scan composes the blocks
-                const uint32_t per = (c + 31) / 32, b0 = lane * per, b1 = b0 + per < c ? b0 + per : c;
-                Tab P = tab_id();
-                for (uint32_t j = b0; j < b1; ++j) {
-                    uint4 v;
-                    do {
-                        v = ld_slot(&row[j]);
-                    } while (!(v.x & MARK));
-                    P = tab_compose(P, tab_unpack(unmark(v)));
-                }
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const Tab o = tab_shfl_up(P, d);
-                    if (lane >= d) P = tab_compose(o, P);
-                }
-#pragma unroll
-                for (int m = 0; m < 4; ++m) P.r[m] = __shfl_sync(0xffffffffu, P.r[m], 31);
-                uint32_t s_cta = 0;
-                if (lane == 0) {
-                    uint32_t s_round;  // the group's state entering this round
-                    if (r == 0) {
-                        s_round = (uint32_t)(FNV_OFFSET >> k) & 15u;
-                    } else {
-                        unsigned long long v;
-                        do {
-                            v = vcarry[slot - 16];
-                        } while (v == 0);
-                        s_round = (uint32_t)v & 15u;
-                    }
-                    s_cta = tab_apply(P, s_round);
-                    if (c == last_in_round) {  // last chunk of the round: carry its output state
-                        __threadfence();
-                        atomicExch(&carry[slot], 0x100ull | tab_apply(agg, s_cta));
-                    }
-                }
-                s_cta = __shfl_sync(0xffffffffu, s_cta, 0);
-                if (lane < WARPS) warp_in[lane] = lane == 0 ? s_cta : tab_apply(wexcl, s_cta);
-            }
-            __syncthreads();
-            // ---- pass B with the actual input state, the four quarters at once (quarter h's
-            // input is the composed map of the quarters before it applied to the thread's input);
-            // the resolved nibble x4 = h4 ^ w4 replaces w4 in y: y ^= h4 << k
-            const uint32_t sin = lane == 0 ? warp_in[warp] : tab_apply(excl_lane, warp_in[warp]);
-            uint32_t sq[4] = {sin, tab_apply(Tq[0], sin), tab_apply(T01, sin), tab_apply(T012, sin)};
-#pragma unroll
-            for (int j = 0; j < Q; ++j) {
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    const int jj = h * Q + j;
-                    if (jj < nv) {
-                        const uint32_t w4 = (wn[jj / 8] >> (4 * (jj % 8))) & 15u;
-                        const uint32_t r4 = (rn[jj / 8] >> (4 * (jj % 8))) & 15u;
-                        w[jj] ^= (uint64_t)sq[h] << k;
-                        sq[h] = (r4 + 3u * (sq[h] ^ w4)) & 15u;
-                    }
-                }
-            }
-        }
+        for (int g = 0; g < 8; ++g) group_step<false>(ylo, yhi, nv, 4 * g, r, r * 16 + g, c, nc, G, aggs, carry, sh);
+#pragma unroll 1
+        for (int g = 8; g < 16; ++g) group_step<true>(ylo, yhi, nv, 4 * g, r, r * 16 + g, c, nc, G, aggs, carry, sh);
         __syncthreads();
     }
     // the final state is the carry of the last round; CTA 0 finishes the digest
     if (c == 0 && threadIdx.x == 0) {
+        volatile unsigned long long *vcarry = carry;
         uint64_t h = 0;
         const uint64_t last = rounds - 1;
         for (int g = 0; g < 16; ++g) {
