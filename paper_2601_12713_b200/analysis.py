@@ -106,6 +106,22 @@ def _cols_struct(c: Columns):
     return s, keep
 
 
+def pinned_columns(cols: Columns) -> Columns:
+    """A copy of host columns in page-locked memory, so the engine's host->device upload runs
+    at full DMA rate (the caller keeps host buffers; the engine still copies them per call)."""
+    import dataclasses
+
+    import torch
+    rep = {}
+    for f in DeviceColumns.FIELDS:
+        a = np.ascontiguousarray(getattr(cols, f))
+        buf = torch.empty(max(a.nbytes, 1), dtype=torch.uint8, pin_memory=True)
+        v = buf.numpy()[:a.nbytes].view(a.dtype)
+        v[...] = a
+        rep[f] = v
+    return dataclasses.replace(cols, **rep)
+
+
 class DeviceColumns:
     """Columns resident in device memory (torch tensors used only as buffers);
     b2l_analyze reads them in place (device_resident = 1)."""

@@ -210,6 +210,107 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(size_t n, Load ld, 
     }
 }
 
+// ---------------------------------------------------------------- single-pass scan
+// One launch per scan: tiles take ids in launch order, publish their aggregate, and a warp
+// looks back over 32 predecessors per step (flags then values; values are written before
+// their flag with a fence in between, read after it through L2), so inputs are read once.
+constexpr uint32_t SP_AGG = 1, SP_INC = 2;
+
+template <class T>
+__device__ __forceinline__ T ld_l2(const T *p) {
+    static_assert(sizeof(T) % 4 == 0, "scan values are whole words");
+    T v;
+    const unsigned *q = reinterpret_cast<const unsigned *>(p);
+    unsigned *d = reinterpret_cast<unsigned *>(&v);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(T) / 4); ++i) d[i] = __ldcg(q + i);
+    return v;
+}
+template <class T>
+__device__ __forceinline__ T shfl_down_t(T v, int off) {
+    unsigned *d = reinterpret_cast<unsigned *>(&v);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(T) / 4); ++i) d[i] = __shfl_down_sync(0xffffffffu, d[i], off);
+    return v;
+}
+
+template <class Op, class Load, class Store>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_1p(size_t n, Load ld, Store st, typename Op::T *agg,
+                                                          typename Op::T *inc, uint32_t *flag, uint32_t *counter,
+                                                          typename Op::T *d_total) {
+    using T = typename Op::T;
+    __shared__ T sm[SCAN_THREADS];
+    __shared__ uint32_t tile_s;
+    __shared__ T prefix_s;
+    if (threadIdx.x == 0) tile_s = atomicAdd(counter, 1u);
+    __syncthreads();
+    const uint32_t tile = tile_s;
+    const size_t base = (size_t)tile * SCAN_TILE + (size_t)threadIdx.x * SCAN_ITEMS;
+    T items[SCAN_ITEMS];
+    T acc = Op::identity();
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+        items[k] = base + k < n ? ld(base + k) : Op::identity();
+        acc = Op::combine(acc, items[k]);
+    }
+    T total;
+    T ex = block_excl_scan<Op>(acc, sm, total);
+    volatile uint32_t *vf = flag;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        if (tile == 0) {
+            if (lane == 0) {
+                inc[0] = total;
+                __threadfence();
+                vf[0] = SP_INC;
+                prefix_s = Op::identity();
+            }
+        } else {
+            if (lane == 0) {
+                agg[tile] = total;
+                __threadfence();
+                vf[tile] = SP_AGG;
+            }
+            T prefix = Op::identity();
+            for (int64_t j = (int64_t)tile - 1;; j -= 32) {
+                const int64_t jj = j - lane;
+                uint32_t f = SP_INC;
+                if (jj >= 0)
+                    do {
+                        f = vf[jj];
+                    } while (f == 0);
+                __threadfence();
+                T v = jj < 0 ? Op::identity() : (f == SP_INC ? ld_l2(inc + jj) : ld_l2(agg + jj));
+                const uint32_t incm = __ballot_sync(0xffffffffu, f == SP_INC);
+                const int first = incm ? __ffs(incm) - 1 : 31;  // newest predecessor with an inclusive
+                if (lane > first) v = Op::identity();
+                // ordered reduction: lane l holds tile j - l (older for higher lanes)
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const T o = shfl_down_t(v, off);
+                    if (lane + off < 32) v = Op::combine(o, v);
+                }
+                prefix = Op::combine(v, prefix);  // lane 0 holds the window, oldest first
+                if (incm) break;
+            }
+            if (lane == 0) {
+                inc[tile] = Op::combine(prefix, total);
+                __threadfence();
+                vf[tile] = SP_INC;
+                prefix_s = prefix;
+            }
+        }
+    }
+    __syncthreads();
+    if (d_total && threadIdx.x == 0 && (size_t)(tile + 1) * SCAN_TILE >= n) *d_total = Op::combine(prefix_s, total);
+    ex = Op::combine(prefix_s, ex);
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+        if (base + k < n) st(base + k, ex, items[k]);
+        ex = Op::combine(ex, items[k]);
+    }
+}
+
 // scan over n items: st(i, exclusive_prefix, item) for every i; optional device total.
 template <class Op, class Load, class Store>
 void scan(size_t n, Load ld, Store st, cudaStream_t s, typename Op::T *d_total = nullptr) {
@@ -219,13 +320,16 @@ void scan(size_t n, Load ld, Store st, cudaStream_t s, typename Op::T *d_total =
         return;
     }
     const size_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    DBuf<T> part(tiles, s);
-    k_scan_reduce<Op, Load><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(n, ld, part.p);
-    CK_LAUNCH("k_scan_reduce");
-    k_scan_partials<Op><<<1, SCAN_THREADS, 0, s>>>(part.p, tiles, d_total);
-    CK_LAUNCH("k_scan_partials");
-    k_scan_apply<Op, Load, Store><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(n, ld, st, part.p);
-    CK_LAUNCH("k_scan_apply");
+    // flags + tile counter in one zeroed block; aggregates / inclusive prefixes beside them
+    const size_t fwords = (tiles + 1 + 3) & ~size_t(3);
+    const size_t tv = (tiles * sizeof(T) + 15) & ~size_t(15);
+    DBuf<uint8_t> ws(fwords * 4 + 2 * tv, s);
+    uint32_t *flag = reinterpret_cast<uint32_t *>(ws.p);
+    CK(cudaMemsetAsync(flag, 0, fwords * 4, s));
+    T *agg = reinterpret_cast<T *>(ws.p + fwords * 4), *inc = reinterpret_cast<T *>(ws.p + fwords * 4 + tv);
+    k_scan_1p<Op, Load, Store><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(n, ld, st, agg, inc, flag, flag + tiles,
+                                                                        d_total);
+    CK_LAUNCH("k_scan_1p");
 }
 
 // ---------------------------------------------------------------- pinned readback staging
