@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <mutex>
 #include <thread>
 #include <type_traits>
@@ -850,7 +851,9 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
                 v[t] = p;
             }, s);
         }
-        radix_sort<1>(ts.b, nt, LiveBytes<1>{{(uint8_t)(g_masks.dev | (live_range(nseg) << 4))}}, s);
+        // trips come in record order, i.e. already ordered by queue: only runs of one queue need
+        // ordering by dst (stable) -- the segmented fix-up, no digit passes
+        seg_fixup(ts.b, nt, 32, (uint8_t)(g_masks.dev | (live_range(nseg) << 4)), s);
         KeyCols<1> tk = ts.b.k[ts.b.cur];
         const uint32_t *tv = ts.val();
         DBuf<uint32_t> gstart(nt, s), gcount(1, s);
@@ -1170,39 +1173,51 @@ struct RunStore {
     }
 };
 
-void ua_ut_step(const DevCols &c, const uint32_t *TK, uint32_t nK, const uint32_t *TT, uint32_t nT, Internal &out,
-                cudaStream_t s) {
-    // ---- kernels grouped by device
-    SortStore<1> ks(nK ? nK : 1, s);
-    DBuf<uint64_t> pm(nK ? nK : 1, s);
-    DBuf<uint32_t> kev(nK ? nK : 1, s);
-    if (nK) {
-        uint64_t *k0 = ks.in_key(0);
-        uint32_t *v = ks.in_val();
-        const int32_t *dst = c.dst;
-        for_each(nK, [=] __device__(size_t r) { k0[r] = (uint64_t)(uint32_t)dst[TK[r]], v[r] = (uint32_t)r; }, s);
-        radix_sort<1>(ks.b, nK, LiveBytes<1>{{g_masks.dev}}, s);
-        uint32_t *ke = kev.p;
-        const uint32_t *kv = ks.val();
-        for_each(nK, [=] __device__(size_t p) { ke[p] = TK[kv[p]]; }, s);
-        scan<Seg<MaxU64>>(nK, PmLoad{ks.key(0), kev.p, c.end}, PmStore{pm.p}, s);
+// Target kernels grouped by device with the per-device prefix max of their ends: the cursor index
+// shared by UA and UT (detectors.py:194-271).
+struct KernelIndexStore {
+    SortStore<1> ks;
+    DBuf<uint64_t> pm;
+    DBuf<uint32_t> kev, dlo, dhi;
+    KernelIndex KI{};
+    KernelIndexStore(uint32_t nK, cudaStream_t s) : ks(nK ? nK : 1, s), pm(nK ? nK : 1, s), kev(nK ? nK : 1, s) {}
+};
+void build_kernel_index(KernelIndexStore &X, const DevCols &c, const uint32_t *TK, uint32_t nK, cudaStream_t s) {
+    SortStore<1> &ks = X.ks;
+    DBuf<uint64_t> &pm = X.pm;
+    DBuf<uint32_t> &kev = X.kev, &dlo = X.dlo, &dhi = X.dhi;
+    {
+        // ---- kernels grouped by device
+        if (nK) {
+            uint64_t *k0 = ks.in_key(0);
+            uint32_t *v = ks.in_val();
+            const int32_t *dst = c.dst;
+            for_each(nK, [=] __device__(size_t r) { k0[r] = (uint64_t)(uint32_t)dst[TK[r]], v[r] = (uint32_t)r; }, s);
+            radix_sort<1>(ks.b, nK, LiveBytes<1>{{g_masks.dev}}, s);
+            uint32_t *ke = kev.p;
+            const uint32_t *kv = ks.val();
+            for_each(nK, [=] __device__(size_t p) { ke[p] = TK[kv[p]]; }, s);
+            scan<Seg<MaxU64>>(nK, PmLoad{ks.key(0), kev.p, c.end}, PmStore{pm.p}, s);
+        }
+        // per-device kernel ranges (one lookup instead of two binary searches per query)
+        const bool small_ndev = c.ndev > 0 && c.ndev <= (1 << 16);
+        dlo.alloc(small_ndev ? c.ndev : 1, s), dhi.alloc(small_ndev ? c.ndev : 1, s);
+        if (small_ndev) {
+            dlo.zero(), dhi.zero();
+            uint32_t *lo = dlo.p, *hi = dhi.p;
+            const uint64_t *kd = ks.key(0);
+            const uint32_t nk = nK;
+            for_each(nK, [=] __device__(size_t p) {
+                if (p == 0 || kd[p] != kd[p - 1]) lo[kd[p]] = (uint32_t)p;
+                if (p + 1 == nk || kd[p + 1] != kd[p]) hi[kd[p]] = (uint32_t)p + 1;
+            }, s);
+        }
+        X.KI = KernelIndex{ks.key(0), kev.p, pm.p, nK, small_ndev ? dlo.p : nullptr, small_ndev ? dhi.p : nullptr};
     }
-    // per-device kernel ranges (one lookup instead of two binary searches per query)
-    const bool small_ndev = c.ndev > 0 && c.ndev <= (1 << 16);
-    DBuf<uint32_t> dlo(small_ndev ? c.ndev : 1, s), dhi(small_ndev ? c.ndev : 1, s);
-    if (small_ndev) {
-        dlo.zero(), dhi.zero();
-        uint32_t *lo = dlo.p, *hi = dhi.p;
-        const uint64_t *kd = ks.key(0);
-        const uint32_t nk = nK;
-        for_each(nK, [=] __device__(size_t p) {
-            if (p == 0 || kd[p] != kd[p - 1]) lo[kd[p]] = (uint32_t)p;
-            if (p + 1 == nk || kd[p + 1] != kd[p]) hi[kd[p]] = (uint32_t)p + 1;
-        }, s);
-    }
-    const KernelIndex KI{ks.key(0), kev.p, pm.p, nK, small_ndev ? dlo.p : nullptr, small_ndev ? dhi.p : nullptr};
+}
 
-    // ---- UA: target pairs whose [alloc start, delete end] meets no kernel
+// UA: target pairs whose [alloc start, delete end] meets no kernel (detectors.py:194-229).
+void ua_step(const DevCols &c, const KernelIndex &KI, Internal &out, cudaStream_t s) {
     {
         const uint32_t nP = (uint32_t)out.n_pairs;
         DBuf<uint32_t> ua(nP ? nP : 1, s), uc(1, s);
@@ -1230,7 +1245,11 @@ void ua_ut_step(const DevCols &c, const uint32_t *TK, uint32_t nK, const uint32_
         out.ua = std::move(ua);
     }
 
-    // ---- UT
+}
+
+// UT (detectors.py:232-271).
+void ut_step(const DevCols &c, const KernelIndex &KI, const uint32_t *TT, uint32_t nT, Internal &out,
+             cudaStream_t s) {
     DBuf<uint8_t> flag(c.n ? c.n : 1, s);
     flag.zero();
     if (nT) {
@@ -1313,12 +1332,13 @@ cudaStream_t engine_stream() {
     }
     return g_stream[dev & 63];
 }
-cudaStream_t g_stream2[64] = {nullptr};
-cudaStream_t engine_stream2() {  // second stream: the device-keyed steps run beside DD/RT
+cudaStream_t g_streamx[2][64] = {{nullptr}};
+cudaStream_t engine_stream_n(int k) {  // side streams 1, 2: the chains that run beside DD/RT
     int dev = 0;
     CK(cudaGetDevice(&dev));
-    if (!g_stream2[dev & 63]) CK(cudaStreamCreateWithFlags(&g_stream2[dev & 63], cudaStreamNonBlocking));
-    return g_stream2[dev & 63];
+    cudaStream_t &st = g_streamx[k - 1][dev & 63];
+    if (!st) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    return st;
 }
 
 int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_override, b2l_findings **outp) {
@@ -1409,56 +1429,94 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     pc.mark("partition");
     in->synth_end = me;
     in->n_pairs = nA;
-    // ---- 3-6.  Hash-keyed (DD, RT) and device-keyed (pairs, RA, UA, UT) work are independent:
-    // run them on two streams from two host threads (each keeps its own syncs and staging).
+    // ---- 3-6.  Three independent chains: hash-keyed (DD, RT), pairs -> RA, and the kernel index
+    // -> UT (-> UA once the pairs exist).  Small traces run them on three streams from three host
+    // threads (each keeps its own syncs and staging); large traces are bandwidth bound and run
+    // them back to back on one stream.
     int dev = 0;
     CK(cudaGetDevice(&dev));
-    cudaStream_t s2 = engine_stream2();
     const Masks masks = g_masks;
     PairOut po;
-    EngineErr err2{0, ""};
-    bool failed2 = false;
-    // Overlap pays while the steps are latency/launch bound (small traces); large traces are
-    // bandwidth bound and run the two halves back to back on one stream.
     const bool overlap = n <= (size_t(4) << 20);
-    if (!overlap) s2 = s;
-    else {  // the partition lists and start ranks are produced on s
+    cudaStream_t s2 = overlap ? engine_stream_n(1) : s, s3 = overlap ? engine_stream_n(2) : s;
+    if (overlap) {  // the partition lists and start ranks are produced on s
         cudaEvent_t ev;
         CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         CK(cudaEventRecord(ev, s));
         CK(cudaStreamWaitEvent(s2, ev, 0));
+        CK(cudaStreamWaitEvent(s3, ev, 0));
         CK(cudaEventDestroy(ev));
     }
-    auto device_keyed = [&] {
+    std::promise<cudaEvent_t> pairs_done;  // recorded on s2 after pairing (UA needs the pairs)
+    std::shared_future<cudaEvent_t> pairs_ready = pairs_done.get_future().share();
+    EngineErr err2{0, ""}, err3{0, ""};
+    bool failed2 = false, failed3 = false, promised = false;
+    auto pairs_chain = [&] {
         try {
             CK(cudaSetDevice(dev));
             g_masks = masks;
             PhaseClock pc2(s2);
             po = pairs_step(c, AD.p, nAD, A.p, nA, me, *in, s2);
+            cudaEvent_t ev;
+            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            CK(cudaEventRecord(ev, s2));
+            pairs_done.set_value(ev);
+            promised = true;
             pc2.mark("pairs");
             ra_step(c, nA, *in, s2);
             pc2.mark("ra");
-            ua_ut_step(c, TK.p, nK, TT.p, nT, *in, s2);
-            pc2.mark("ua_ut");
-            CK(cudaStreamSynchronize(s2));
+            if (overlap) CK(cudaStreamSynchronize(s2));
         } catch (const EngineErr &e) {
             err2 = e;
             failed2 = true;
+            if (!promised) pairs_done.set_value(nullptr);
         }
     };
-    std::thread side;
-    if (overlap) side = std::thread(device_keyed);
-    else device_keyed();
+    auto kernel_chain = [&] {
+        try {
+            CK(cudaSetDevice(dev));
+            g_masks = masks;
+            PhaseClock pc3(s3);
+            KernelIndexStore kis(nK, s3);
+            build_kernel_index(kis, c, TK.p, nK, s3);
+            ut_step(c, kis.KI, TT.p, nT, *in, s3);
+            pc3.mark("ut");
+            cudaEvent_t ev = pairs_ready.get();
+            if (!ev) return;  // pairing failed (reported by its chain)
+            CK(cudaStreamWaitEvent(s3, ev, 0));
+            ua_step(c, kis.KI, *in, s3);
+            pc3.mark("ua");
+            if (overlap) CK(cudaStreamSynchronize(s3));
+        } catch (const EngineErr &e) {
+            err3 = e;
+            failed3 = true;
+        }
+    };
+    std::thread t2, t3;
+    if (overlap) {
+        t2 = std::thread(pairs_chain);
+        t3 = std::thread(kernel_chain);
+    } else {
+        pairs_chain();
+        kernel_chain();
+    }
+    auto join = [&] {
+        if (t2.joinable()) t2.join();
+        if (t3.joinable()) t3.join();
+        cudaEvent_t ev = pairs_ready.get();
+        if (ev) cudaEventDestroy(ev);
+    };
     try {
         DdRt dr = dd_rt_step(c, H.p, nH, (flags & B2L_ANALYZE_STRICT_RT) != 0, *in, s);
         in->dd_groups = dr.dd_groups, in->dd_members = dr.dd_members, in->rt_groups = dr.rt_groups,
         in->rt_trips = dr.rt_trips;
     } catch (...) {
-        if (side.joinable()) side.join();
+        join();
         throw;
     }
-    if (side.joinable()) side.join();
+    join();
     if (failed2) throw err2;
+    if (failed3) throw err3;
     pc.mark("detectors");
 
     // ---- results to the host (one pinned slab, one synchronisation)
@@ -1809,9 +1867,16 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     // ---- to host
     unsigned long long h[15];
     uint32_t hov = 0, hun = 0;
-    read_back(h, acc.p, sizeof(h), s);
-    read_back(&hov, ovl.p, sizeof(hov), s);
-    read_back(&hun, unic.p, sizeof(hun), s);
+    {  // one synchronisation for the three small results
+        uint8_t *st = pinned(s).reserve(sizeof(h) + 8);
+        CK(cudaMemcpyAsync(st, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(st + sizeof(h), ovl.p, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(st + sizeof(h) + 4, unic.p, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        memcpy(h, st, sizeof(h));
+        memcpy(&hov, st + sizeof(h), 4);
+        memcpy(&hun, st + sizeof(h) + 4, 4);
+    }
     for (int k = 0; k < 5; ++k) o->per_category_ns[k] = b2l_u128{h[2 * k], h[2 * k + 1]};
     o->union_ns = b2l_u128{h[10], h[11]};
     o->n_union = hun;
