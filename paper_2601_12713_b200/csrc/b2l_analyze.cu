@@ -703,6 +703,8 @@ struct DdRt {
     uint64_t dd_groups = 0, rt_groups = 0, dd_members = 0, rt_trips = 0;
 };
 
+cudaStream_t engine_stream_n(int k);
+
 DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, Internal &out, cudaStream_t s) {
     DdRt r;
     const size_t R = 2ull * nH;
@@ -749,155 +751,193 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
     CK(cudaMemcpyAsync(seg_rxbase.p + nseg, &tot.p->rx_glob, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
 
     pc.mark(" q-scan");
-    // ---- round trips: per send, the matched reception (or NONE)
-    DBuf<uint32_t> match(nH, s);
-    CK(cudaMemsetAsync(match.p, 0xFF, nH * sizeof(uint32_t), s));
-    if (!strict) {
-        scan<Seg<MaxI64>>(R, RtMaxLoad{sk, sval, f_of.p, j_of.p},
-                          RtMatchStore{sval, j_of.p, seg_of.p, seg_rxbase.p, rxpos.p, H, match.p}, s);
-    } else {
-        DBuf<uint64_t> segk(nseg, s);
-        {
-            const uint32_t *ss = seg_start.p;
-            uint64_t *a = segk.p;
-            for_each(nseg, [=] __device__(size_t g) { a[g] = sk[ss[g]]; }, s);
-        }
-        // hashed transfers grouped by hash, trace order within a hash: the hash sort above
-        DBuf<uint32_t> hstart(nH, s), hcount(1, s);
-        compact(nH, HeadPred<1>{hk}, hstart.p, hcount.p, s);
-        const uint32_t nhseg = read_u32(hcount.p, s);
-        DBuf<uint32_t> qhead(nseg, s);
-        qhead.zero();
-        k_rt_strict<<<grid_for(nhseg, 128), 128, 0, s>>>(c, H, hsort.val(), hstart.p, nhseg, nH, hid.p, segk.p,
-                                                         nseg, seg_rxbase.p, rxpos.p, sval, qhead.p, match.p);
-        CK_LAUNCH("k_rt_strict");
+    // ---- DD groups need only the queue scan: on small traces they run on their own stream (and
+    // host thread) beside the RT matching and grouping, which are latency bound there
+    const bool dd_side = R <= (size_t(8) << 20);
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const Masks masks = g_masks;
+    cudaStream_t sd = dd_side ? engine_stream_n(3) : s;
+    if (dd_side) {
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev, s));
+        CK(cudaStreamWaitEvent(sd, ev, 0));
+        CK(cudaEventDestroy(ev));
     }
+    EngineErr errd{0, ""};
+    bool faild = false;
+    auto dd_groups = [&](cudaStream_t s) {
+        try {
+            CK(cudaSetDevice(dev));
+            g_masks = masks;
+            // ---- DD groups: queue segments with >= 2 receptions (members = the receptions, trace order)
+            {
+                DBuf<uint32_t> gseg(nseg, s), gcount(1, s);
+                const uint32_t *rb = seg_rxbase.p;
+                compact(nseg, [=] __device__(size_t g) { return rb[g + 1] - rb[g] >= 2; }, gseg.p, gcount.p, s);
+                const uint32_t ng = read_u32(gcount.p, s);
+                r.dd_groups = ng;
+                DBuf<uint32_t> first_ev(ng ? ng : 1, s), gsize(ng ? ng : 1, s), seg_group(nseg, s);
+                DBuf<uint64_t> tie(ng ? ng : 1, s);
+                CK(cudaMemsetAsync(seg_group.p, 0xFF, nseg * sizeof(uint32_t), s));
+                {
+                    const uint32_t *gs = gseg.p, *rp = rxpos.p, *ss = seg_start.p;
+                    uint32_t *fe = first_ev.p, *sz = gsize.p, *sgp = seg_group.p;
+                    uint64_t *tk = tie.p;
+                    const int dbits = db;
+                    for_each(ng, [=] __device__(size_t g) {
+                        const uint32_t sg = gs[g];
+                        fe[g] = H[sval[rp[rb[sg]]] >> 1];
+                        sz[g] = rb[sg + 1] - rb[sg];
+                        sgp[sg] = (uint32_t)g;
+                        const uint64_t key = sk[ss[sg]];  // dst << 32 | hash rank
+                        tk[g] = ((key & 0xFFFFFFFFull) << dbits) | (key >> 32);  // reference order (hash, dst)
+                    }, s);
+                }
+                GroupOrder go = order_groups(ng, c.start, first_ev.p, s, tie.p, (uint64_t)nH << db);
+                out.dd_off.alloc(ng + 1, s);
+                DBuf<uint64_t> total(1, s);
+                scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.dd_off.p}, s, total.p);
+                if (ng) CK(cudaMemcpyAsync(out.dd_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+                else CK(cudaMemsetAsync(out.dd_off.p, 0, sizeof(uint64_t), s));
+                uint64_t nm = 0;
+                if (ng) {
+                    read_back(&nm, total.p, sizeof(nm), s);
+                }
+                r.dd_members = nm;
+                out.dd_mem.alloc(nm ? nm : 1, s);
+                // every reception of a grouped segment lands at off[rank] + (its rank within the segment)
+                const uint32_t *sgp = seg_group.p, *rk = go.rank.p, *so = seg_of.p, *rp = rxpos.p;
+                const uint64_t *off = out.dd_off.p;
+                uint32_t *mem = out.dd_mem.p;
+                for_each(nrx, [=] __device__(size_t q) {
+                    const uint32_t p = rp[q];
+                    const uint32_t sg = so[p];
+                    const uint32_t g = sgp[sg];
+                    if (g == NONE) return;
+                    mem[off[rk[g]] + (q - rb[sg])] = H[sval[p] >> 1];
+                }, s);
+            }
+            if (dd_side) CK(cudaStreamSynchronize(s));
+        } catch (const EngineErr &e) {
+            errd = e;
+            faild = true;
+        }
+    };
+    std::thread td;
+    if (dd_side) td = std::thread(dd_groups, sd);
+    else dd_groups(s);
+    auto rt_groups = [&] {
+        // ---- round trips: per send, the matched reception (or NONE)
+        DBuf<uint32_t> match(nH, s);
+        CK(cudaMemsetAsync(match.p, 0xFF, nH * sizeof(uint32_t), s));
+        if (!strict) {
+            scan<Seg<MaxI64>>(R, RtMaxLoad{sk, sval, f_of.p, j_of.p},
+                              RtMatchStore{sval, j_of.p, seg_of.p, seg_rxbase.p, rxpos.p, H, match.p}, s);
+        } else {
+            DBuf<uint64_t> segk(nseg, s);
+            {
+                const uint32_t *ss = seg_start.p;
+                uint64_t *a = segk.p;
+                for_each(nseg, [=] __device__(size_t g) { a[g] = sk[ss[g]]; }, s);
+            }
+            // hashed transfers grouped by hash, trace order within a hash: the hash sort above
+            DBuf<uint32_t> hstart(nH, s), hcount(1, s);
+            compact(nH, HeadPred<1>{hk}, hstart.p, hcount.p, s);
+            const uint32_t nhseg = read_u32(hcount.p, s);
+            DBuf<uint32_t> qhead(nseg, s);
+            qhead.zero();
+            k_rt_strict<<<grid_for(nhseg, 128), 128, 0, s>>>(c, H, hsort.val(), hstart.p, nhseg, nH, hid.p, segk.p,
+                                                             nseg, seg_rxbase.p, rxpos.p, sval, qhead.p, match.p);
+            CK_LAUNCH("k_rt_strict");
+        }
 
-    pc.mark(" rt-match");
-    // ---- DD groups: queue segments with >= 2 receptions (members = the receptions, trace order)
-    {
-        DBuf<uint32_t> gseg(nseg, s), gcount(1, s);
-        const uint32_t *rb = seg_rxbase.p;
-        compact(nseg, [=] __device__(size_t g) { return rb[g + 1] - rb[g] >= 2; }, gseg.p, gcount.p, s);
-        const uint32_t ng = read_u32(gcount.p, s);
-        r.dd_groups = ng;
-        DBuf<uint32_t> first_ev(ng ? ng : 1, s), gsize(ng ? ng : 1, s), seg_group(nseg, s);
-        DBuf<uint64_t> tie(ng ? ng : 1, s);
-        CK(cudaMemsetAsync(seg_group.p, 0xFF, nseg * sizeof(uint32_t), s));
+        pc.mark(" rt-match");
+        // ---- RT groups: matched sends keyed (hash, src, dst); sends of one (hash, src) queue are
+        // already in trace order in the record sort, so a stable sort by (queue segment, dst) groups them
         {
-            const uint32_t *gs = gseg.p, *rp = rxpos.p, *ss = seg_start.p;
-            uint32_t *fe = first_ev.p, *sz = gsize.p, *sgp = seg_group.p;
-            uint64_t *tk = tie.p;
-            const int dbits = db;
-            for_each(ng, [=] __device__(size_t g) {
-                const uint32_t sg = gs[g];
-                fe[g] = H[sval[rp[rb[sg]]] >> 1];
-                sz[g] = rb[sg + 1] - rb[sg];
-                sgp[sg] = (uint32_t)g;
-                const uint64_t key = sk[ss[sg]];  // dst << 32 | hash rank
-                tk[g] = ((key & 0xFFFFFFFFull) << dbits) | (key >> 32);  // reference order (hash, dst)
-            }, s);
-        }
-        GroupOrder go = order_groups(ng, c.start, first_ev.p, s, tie.p, (uint64_t)nH << db);
-        out.dd_off.alloc(ng + 1, s);
-        DBuf<uint64_t> total(1, s);
-        scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.dd_off.p}, s, total.p);
-        if (ng) CK(cudaMemcpyAsync(out.dd_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-        else CK(cudaMemsetAsync(out.dd_off.p, 0, sizeof(uint64_t), s));
-        uint64_t nm = 0;
-        if (ng) {
-            read_back(&nm, total.p, sizeof(nm), s);
-        }
-        r.dd_members = nm;
-        out.dd_mem.alloc(nm ? nm : 1, s);
-        // every reception of a grouped segment lands at off[rank] + (its rank within the segment)
-        const uint32_t *sgp = seg_group.p, *rk = go.rank.p, *so = seg_of.p, *rp = rxpos.p;
-        const uint64_t *off = out.dd_off.p;
-        uint32_t *mem = out.dd_mem.p;
-        for_each(nrx, [=] __device__(size_t q) {
-            const uint32_t p = rp[q];
-            const uint32_t sg = so[p];
-            const uint32_t g = sgp[sg];
-            if (g == NONE) return;
-            mem[off[rk[g]] + (q - rb[sg])] = H[sval[p] >> 1];
-        }, s);
-    }
-
-    pc.mark(" dd-groups");
-    // ---- RT groups: matched sends keyed (hash, src, dst); sends of one (hash, src) queue are
-    // already in trace order in the record sort, so a stable sort by (queue segment, dst) groups them
-    {
-        DBuf<uint32_t> mpos(R, s), mcount(1, s);
-        uint32_t *mt = match.p;
-        compact(R, [=] __device__(size_t p) { return (sval[p] & 1u) && mt[sval[p] >> 1] != NONE; }, mpos.p,
-                mcount.p, s);
-        const uint32_t nt = read_u32(mcount.p, s);
-        r.rt_trips = nt;
-        out.rt_tx.alloc(nt ? nt : 1, s);
-        out.rt_rx.alloc(nt ? nt : 1, s);
-        if (nt == 0) {
-            out.rt_off.alloc(1, s), out.rt_off.zero();
-            return r;
-        }
-        SortStore<1> ts(nt, s);
-        {
-            uint64_t *k0 = ts.in_key(0);
-            uint32_t *v = ts.in_val();
-            const uint32_t *mp = mpos.p, *so = seg_of.p;
-            const int32_t *dst = c.dst;
+            DBuf<uint32_t> mpos(R, s), mcount(1, s);
+            uint32_t *mt = match.p;
+            compact(R, [=] __device__(size_t p) { return (sval[p] & 1u) && mt[sval[p] >> 1] != NONE; }, mpos.p,
+                    mcount.p, s);
+            const uint32_t nt = read_u32(mcount.p, s);
+            r.rt_trips = nt;
+            out.rt_tx.alloc(nt ? nt : 1, s);
+            out.rt_rx.alloc(nt ? nt : 1, s);
+            if (nt == 0) {
+                out.rt_off.alloc(1, s), out.rt_off.zero();
+                return;
+            }
+            SortStore<1> ts(nt, s);
+            {
+                uint64_t *k0 = ts.in_key(0);
+                uint32_t *v = ts.in_val();
+                const uint32_t *mp = mpos.p, *so = seg_of.p;
+                const int32_t *dst = c.dst;
+                for_each(nt, [=] __device__(size_t t) {
+                    const uint32_t p = mp[t];
+                    k0[t] = ((uint64_t)so[p] << 32) | (uint32_t)dst[H[sval[p] >> 1]];
+                    v[t] = p;
+                }, s);
+            }
+            // trips come in record order, i.e. already ordered by queue: only runs of one queue need
+            // ordering by dst (stable) -- the segmented fix-up, no digit passes
+            seg_fixup(ts.b, nt, 32, (uint8_t)(g_masks.dev | (live_range(nseg) << 4)), s);
+            KeyCols<1> tk = ts.b.k[ts.b.cur];
+            const uint32_t *tv = ts.val();
+            DBuf<uint32_t> gstart(nt, s), gcount(1, s);
+            compact(nt, HeadPred<1>{tk}, gstart.p, gcount.p, s);
+            const uint32_t ng = read_u32(gcount.p, s);
+            r.rt_groups = ng;
+            DBuf<uint32_t> first_ev(ng, s), gsize(ng, s), trip_group(nt, s);
+            DBuf<uint64_t> tie(ng, s);
+            {
+                const uint32_t *gs = gstart.p;
+                uint32_t *fe = first_ev.p, *sz = gsize.p;
+                uint64_t *tk = tie.p;
+                const uint32_t ntt = nt;
+                const int dbits = db;
+                const int32_t *dst = c.dst;
+                for_each(ng, [=] __device__(size_t g) {
+                    const uint32_t p = tv[gs[g]], e = H[sval[p] >> 1];
+                    fe[g] = e;
+                    sz[g] = ((g + 1 < ng) ? gs[g + 1] : ntt) - gs[g];
+                    const uint64_t key = sk[p];  // src << 32 | hash rank
+                    // reference order (hash, src, dst)
+                    tk[g] = ((((key & 0xFFFFFFFFull) << dbits) | (key >> 32)) << dbits) | (uint64_t)(uint32_t)dst[e];
+                }, s);
+            }
+            {
+                uint32_t *tg = trip_group.p;
+                scan<SumU32>(nt, HeadLoad<1>{tk}, StoreInclMinus1{tg}, s);  // group id of every sorted trip
+            }
+            GroupOrder go = order_groups(ng, c.start, first_ev.p, s, tie.p, (uint64_t)nH << (2 * db));
+            out.rt_off.alloc(ng + 1, s);
+            DBuf<uint64_t> total(1, s);
+            scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.rt_off.p}, s, total.p);
+            CK(cudaMemcpyAsync(out.rt_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+            const uint32_t *tg = trip_group.p, *rk = go.rank.p, *gs = gstart.p;
+            const uint64_t *off = out.rt_off.p;
+            uint32_t *otx = out.rt_tx.p, *orx = out.rt_rx.p;
             for_each(nt, [=] __device__(size_t t) {
-                const uint32_t p = mp[t];
-                k0[t] = ((uint64_t)so[p] << 32) | (uint32_t)dst[H[sval[p] >> 1]];
-                v[t] = p;
+                const uint32_t g = tg[t];
+                const uint64_t o = off[rk[g]] + (t - gs[g]);
+                const uint32_t k = sval[tv[t]] >> 1;
+                otx[o] = H[k];
+                orx[o] = mt[k];
             }, s);
         }
-        // trips come in record order, i.e. already ordered by queue: only runs of one queue need
-        // ordering by dst (stable) -- the segmented fix-up, no digit passes
-        seg_fixup(ts.b, nt, 32, (uint8_t)(g_masks.dev | (live_range(nseg) << 4)), s);
-        KeyCols<1> tk = ts.b.k[ts.b.cur];
-        const uint32_t *tv = ts.val();
-        DBuf<uint32_t> gstart(nt, s), gcount(1, s);
-        compact(nt, HeadPred<1>{tk}, gstart.p, gcount.p, s);
-        const uint32_t ng = read_u32(gcount.p, s);
-        r.rt_groups = ng;
-        DBuf<uint32_t> first_ev(ng, s), gsize(ng, s), trip_group(nt, s);
-        DBuf<uint64_t> tie(ng, s);
-        {
-            const uint32_t *gs = gstart.p;
-            uint32_t *fe = first_ev.p, *sz = gsize.p;
-            uint64_t *tk = tie.p;
-            const uint32_t ntt = nt;
-            const int dbits = db;
-            const int32_t *dst = c.dst;
-            for_each(ng, [=] __device__(size_t g) {
-                const uint32_t p = tv[gs[g]], e = H[sval[p] >> 1];
-                fe[g] = e;
-                sz[g] = ((g + 1 < ng) ? gs[g + 1] : ntt) - gs[g];
-                const uint64_t key = sk[p];  // src << 32 | hash rank
-                // reference order (hash, src, dst)
-                tk[g] = ((((key & 0xFFFFFFFFull) << dbits) | (key >> 32)) << dbits) | (uint64_t)(uint32_t)dst[e];
-            }, s);
-        }
-        {
-            uint32_t *tg = trip_group.p;
-            scan<SumU32>(nt, HeadLoad<1>{tk}, StoreInclMinus1{tg}, s);  // group id of every sorted trip
-        }
-        GroupOrder go = order_groups(ng, c.start, first_ev.p, s, tie.p, (uint64_t)nH << (2 * db));
-        out.rt_off.alloc(ng + 1, s);
-        DBuf<uint64_t> total(1, s);
-        scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.rt_off.p}, s, total.p);
-        CK(cudaMemcpyAsync(out.rt_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-        const uint32_t *tg = trip_group.p, *rk = go.rank.p, *gs = gstart.p;
-        const uint64_t *off = out.rt_off.p;
-        uint32_t *otx = out.rt_tx.p, *orx = out.rt_rx.p;
-        for_each(nt, [=] __device__(size_t t) {
-            const uint32_t g = tg[t];
-            const uint64_t o = off[rk[g]] + (t - gs[g]);
-            const uint32_t k = sval[tv[t]] >> 1;
-            otx[o] = H[k];
-            orx[o] = mt[k];
-        }, s);
+    };
+    try {
+        rt_groups();
+    } catch (...) {
+        if (td.joinable()) td.join();
+        throw;
     }
+    if (td.joinable()) td.join();
+    if (faild) throw errd;
+    pc.mark(" dd-rt-groups");
     return r;
 }
 
@@ -1332,8 +1372,8 @@ cudaStream_t engine_stream() {
     }
     return g_stream[dev & 63];
 }
-cudaStream_t g_streamx[2][64] = {{nullptr}};
-cudaStream_t engine_stream_n(int k) {  // side streams 1, 2: the chains that run beside DD/RT
+cudaStream_t g_streamx[3][64] = {{nullptr}};
+cudaStream_t engine_stream_n(int k) {  // side streams 1..3: the chains that run beside DD/RT
     int dev = 0;
     CK(cudaGetDevice(&dev));
     cudaStream_t &st = g_streamx[k - 1][dev & 63];
