@@ -436,6 +436,16 @@ struct HeadLoad {
     KeyCols<KW> k;
     __device__ uint32_t operator()(size_t p) const { return HeadPred<KW>{k}(p) ? 1u : 0u; }
 };
+struct SegStartStore {  // over head flags: segment id per position, start position per segment
+    uint32_t *seg_of, *seg_start;
+    uint32_t n;  // seg_start[#segments] = n is written by the last position
+    __device__ void operator()(size_t i, uint32_t ex, uint32_t it) const {
+        const uint32_t sg = ex + it - 1;
+        seg_of[i] = sg;
+        if (it) seg_start[sg] = (uint32_t)i;
+        if (i + 1 == n) seg_start[sg + 1] = n;
+    }
+};
 struct StoreInclMinus1 {
     uint32_t *o;
     __device__ void operator()(size_t i, uint32_t ex, uint32_t it) const { o[i] = ex + it - 1; }
@@ -801,12 +811,7 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
                 scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.dd_off.p}, s, total.p);
                 if (ng) CK(cudaMemcpyAsync(out.dd_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
                 else CK(cudaMemsetAsync(out.dd_off.p, 0, sizeof(uint64_t), s));
-                uint64_t nm = 0;
-                if (ng) {
-                    read_back(&nm, total.p, sizeof(nm), s);
-                }
-                r.dd_members = nm;
-                out.dd_mem.alloc(nm ? nm : 1, s);
+                out.dd_mem.alloc(nrx ? nrx : 1, s);  // members are receptions; count read after the scatter
                 // every reception of a grouped segment lands at off[rank] + (its rank within the segment)
                 const uint32_t *sgp = seg_group.p, *rk = go.rank.p, *so = seg_of.p, *rp = rxpos.p;
                 const uint64_t *off = out.dd_off.p;
@@ -818,6 +823,9 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
                     if (g == NONE) return;
                     mem[off[rk[g]] + (q - rb[sg])] = H[sval[p] >> 1];
                 }, s);
+                uint64_t nm = 0;
+                if (ng) read_back(&nm, total.p, sizeof(nm), s);
+                r.dd_members = nm;
             }
             if (dd_side) CK(cudaStreamSynchronize(s));
         } catch (const EngineErr &e) {
@@ -943,8 +951,22 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
 
 
 // ============================================================ LIFO pairing (prep.py:45-96)
+struct UmPred {
+    const uint8_t *um;
+    __device__ bool operator()(size_t r) const { return um[r] != 0; }
+};
+template <class Pred>
+struct MapCompactStore {  // compaction that stores map[i] instead of i
+    Pred p;
+    const uint32_t *map;
+    uint32_t *out;
+    __device__ __forceinline__ void operator()(size_t i, uint32_t ex, uint32_t item) const {
+        if (item) out[ex] = map[i];
+    }
+};
 struct PairOut {
     uint32_t n_pairs = 0, n_warn = 0;
+    DBuf<uint32_t> wcount;  // device count of warnings (read at the end of the chain)
     DBuf<uint32_t> warn;  // unmatched deletes, trace order
 };
 // inclusive depth after an element from its (exclusive prefix, item) of the max-plus scan
@@ -1017,12 +1039,10 @@ PairOut pairs_step(const DevCols &c, const uint32_t *AD, uint32_t nAD, const uin
         for_each(nAD, [=] __device__(size_t p) {
             if (kind[AD[sv[p]]] == B2L_KIND_DELETE && lv[p] == 0) um[sv[p]] = 1;
         }, s);
-        DBuf<uint32_t> wr(nAD, s), wc(1, s);
-        compact(nAD, [=] __device__(size_t r) { return um[r] != 0; }, wr.p, wc.p, s);
-        po.n_warn = read_u32(wc.p, s);
-        uint32_t *w = po.warn.p;
-        const uint32_t *wrp = wr.p;
-        for_each(po.n_warn, [=] __device__(size_t k) { w[k] = AD[wrp[k]]; }, s);
+        // compacted straight to event indices; the count is read at the end of the chain
+        po.wcount.alloc(1, s);
+        scan<SumU32>(nAD, FlagLoad<UmPred>{UmPred{um}}, MapCompactStore<UmPred>{UmPred{um}, AD, po.warn.p}, s,
+                     po.wcount.p);
     }
     // (segment, level) sort of allocs and matched deletes: within one level of one address the
     // sequence alternates alloc, delete, alloc, ... and each alloc pairs with the delete after it
@@ -1031,14 +1051,21 @@ PairOut pairs_step(const DevCols &c, const uint32_t *AD, uint32_t nAD, const uin
         const uint32_t *lv = level.p;
         compact(nAD, [=] __device__(size_t p) { return lv[p] != 0; }, lp.p, lc.p, s);
     }
-    const uint32_t nl = read_u32(lc.p, s);
-    if (nl == 0) return po;
+    // sorted over nAD slots without reading the count back: slots past it get the sentinel key
+    // (segment nAD, level 0), which sorts after every real record
+    const uint32_t nl = nAD;
     SortStore<1> ls(nl, s);
     {
         uint64_t *k0 = ls.in_key(0);
         uint32_t *v = ls.in_val();
-        const uint32_t *lpp = lp.p, *lv = level.p, *sg = seg.p;
+        const uint32_t *lpp = lp.p, *lv = level.p, *sg = seg.p, *cnt = lc.p;
+        const uint64_t sentinel = (uint64_t)nAD << 32;
         for_each(nl, [=] __device__(size_t q) {
+            if (q >= *cnt) {
+                k0[q] = sentinel;
+                v[q] = NONE;
+                return;
+            }
             const uint32_t p = lpp[q];
             k0[q] = ((uint64_t)sg[p] << 32) | lv[p];
             v[q] = p;
@@ -1053,9 +1080,10 @@ PairOut pairs_step(const DevCols &c, const uint32_t *AD, uint32_t nAD, const uin
         uint32_t *pd = out.pair_delete.p;
         const uint32_t nll = nl;
         for_each(nl, [=] __device__(size_t q) {
+            if (lvv[q] == NONE) return;
             const uint32_t e = AD[sv[lvv[q]]];
             if (kind[e] != B2L_KIND_ALLOC) return;
-            if (q + 1 < nll && lk[q + 1] == lk[q]) {
+            if (q + 1 < nll && lk[q + 1] == lk[q] && lvv[q + 1] != NONE) {
                 const uint32_t e2 = AD[sv[lvv[q + 1]]];
                 if (kind[e2] == B2L_KIND_DELETE) pd[ar[e]] = e2;
             }
@@ -1087,19 +1115,22 @@ void ra_step(const DevCols &c, uint32_t nP, Internal &out, cudaStream_t s) {
     radix_sort<3>(st.b, nP, LiveBytes<3>{{g_masks.sa, g_masks.dev, g_masks.nb}}, s);
     KeyCols<3> sk = st.b.k[st.b.cur];
     const uint32_t *sv = st.val();
+    // one scan: segment id of every sorted pair and the start of every segment; the segment count
+    // stays on the device (the group compaction reads it), one synchronisation for the group count
     DBuf<uint32_t> sstart(nP + 1, s), scount(1, s), seg_of(nP, s);
-    compact(nP, HeadPred<3>{sk}, sstart.p, scount.p, s);
-    scan<SumU32>(nP, HeadLoad<3>{sk}, StoreInclMinus1{seg_of.p}, s);
-    const uint32_t nseg = read_u32(scount.p, s);
+    scan<SumU32>(nP, HeadLoad<3>{sk}, SegStartStore{seg_of.p, sstart.p, (uint32_t)nP}, s, scount.p);
+    DBuf<uint32_t> gseg(nP, s), gc(1, s);
+    const uint32_t *ss = sstart.p, *nsp = scount.p;
+    compact(nP, [=] __device__(size_t g) { return g < *nsp && ss[g + 1] - ss[g] >= 2; }, gseg.p, gc.p, s);
+    uint32_t cnts[2];
     {
-        uint32_t *ss = sstart.p;
-        const uint32_t np = nP;
-        for_each(1, [=] __device__(size_t) { ss[nseg] = np; }, s);
+        uint8_t *st = pinned(s).reserve(8);
+        CK(cudaMemcpyAsync(st, scount.p, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(st + 4, gc.p, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        memcpy(cnts, st, 8);
     }
-    DBuf<uint32_t> gseg(nseg, s), gc(1, s);
-    const uint32_t *ss = sstart.p;
-    compact(nseg, [=] __device__(size_t g) { return ss[g + 1] - ss[g] >= 2; }, gseg.p, gc.p, s);
-    const uint32_t ng = read_u32(gc.p, s);
+    const uint32_t nseg = cnts[0], ng = cnts[1];
     out.ra_groups = ng;
     if (ng == 0) {
         out.ra_off.alloc(1, s), out.ra_off.zero(), out.ra_mem.alloc(1, s);
@@ -1122,10 +1153,7 @@ void ra_step(const DevCols &c, uint32_t nP, Internal &out, cudaStream_t s) {
     DBuf<uint64_t> total(1, s);
     scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.ra_off.p}, s, total.p);
     CK(cudaMemcpyAsync(out.ra_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-    uint64_t nm = 0;
-    read_back(&nm, total.p, sizeof(nm), s);
-    out.ra_members = nm;
-    out.ra_mem.alloc(nm, s);
+    out.ra_mem.alloc(nP, s);  // members <= pairs; the count is read once the scatter is queued
     const uint32_t *sgp = seg_group.p, *rk = go.rank.p, *so = seg_of.p;
     const uint64_t *off = out.ra_off.p;
     uint32_t *mem = out.ra_mem.p;
@@ -1135,6 +1163,9 @@ void ra_step(const DevCols &c, uint32_t nP, Internal &out, cudaStream_t s) {
         if (g == NONE) return;
         mem[off[rk[g]] + (p - ss[sg])] = sv[p];
     }, s);
+    uint64_t nm = 0;
+    read_back(&nm, total.p, sizeof(nm), s);
+    out.ra_members = nm;
 }
 
 // ============================================================ UA / UT (detectors.py:194-271)
@@ -1504,6 +1535,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
             promised = true;
             pc2.mark("pairs");
             ra_step(c, nA, *in, s2);
+            if (po.wcount.p) po.n_warn = read_u32(po.wcount.p, s2);
             pc2.mark("ra");
             if (overlap) CK(cudaStreamSynchronize(s2));
         } catch (const EngineErr &e) {
