@@ -1632,6 +1632,34 @@ void findings_free(b2l_findings *f) {
 
 
 // ============================================================ savings (estimator.py:61-130, report.py:44-95)
+// Byte-granular atomic OR (the category bits of one event can come from several lists at once).
+__device__ __forceinline__ void atomicOr_u8(uint8_t *p, uint32_t bits) {
+    const uintptr_t a = (uintptr_t)p;
+    atomicOr(reinterpret_cast<unsigned int *>(a & ~uintptr_t(3)), bits << (8 * (a & 3)));
+}
+// Overlap flag and union list in one scan: (max end so far, count of events in any category).
+struct OvUn {
+    using T = struct {
+        unsigned long long mx;
+        uint32_t cnt, pad;
+    };
+    static __device__ __forceinline__ T identity() { return T{0ull, 0u, 0u}; }
+    static __device__ __forceinline__ T combine(T a, T b) { return T{a.mx > b.mx ? a.mx : b.mx, a.cnt + b.cnt, 0u}; }
+};
+struct OvUnLoad {
+    const uint64_t *end;
+    const uint8_t *cat;
+    __device__ OvUn::T operator()(size_t i) const { return OvUn::T{end[i], cat[i] ? 1u : 0u, 0u}; }
+};
+struct OvUnStore {
+    const uint64_t *start;
+    const uint8_t *cat;
+    uint32_t *flag, *uni;
+    __device__ void operator()(size_t i, OvUn::T ex, OvUn::T) const {
+        if (i > 0 && start[i] < ex.mx) *flag = 1;
+        if (cat[i]) uni[ex.cnt] = (uint32_t)i;
+    }
+};
 struct LoadEnd {
     const uint64_t *e;
     __device__ uint64_t operator()(size_t i) const { return e[i]; }
@@ -1849,46 +1877,47 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     PhaseClock pc(s);
     pc.mark("sv-setup");
     // ---- category bits per event
-    DBuf<uint8_t> cat(n ? n : 1, s);
+    DBuf<uint8_t> cat(((n ? n : 1) + 3) & ~size_t(3), s);  // whole words: byte atomics touch the word
     cat.zero();
     uint8_t *ct = cat.p;
     {
-        // DD: every member but the first of its group
-        const uint64_t *off = F.dd_off;
-        const uint32_t *mem = F.dd_mem;
-        const uint64_t ng = F.dd_groups;
-        for_each(F.dd_members, [=] __device__(size_t q) {
-            uint64_t lo = 0, hi = ng;  // group g with off[g] <= q < off[g+1]
-            while (hi - lo > 1) {
-                uint64_t m = (lo + hi) >> 1;
-                if (off[m] <= q) lo = m; else hi = m;
+        // one launch over the five finding lists laid end to end: DD members but the first of each
+        // group, RT receptions, RA pairs but the first of each group, UA pairs, UT events
+        const uint64_t *off = F.dd_off, *roff = F.ra_off;
+        const uint32_t *mem = F.dd_mem, *rx = F.rt_rx, *rm = F.ra_mem, *pa = F.pa, *pd = F.pd, *ua = F.ua,
+                       *ut = F.ut;
+        const uint64_t ng = F.dd_groups, rng = F.ra_groups;
+        const uint64_t e0 = F.dd_members, e1 = e0 + F.rt_trips, e2 = e1 + F.ra_members, e3 = e2 + F.n_ua,
+                       e4 = e3 + F.n_ut;
+        for_each(e4, [=] __device__(size_t q) {
+            if (q < e0) {
+                uint64_t lo = 0, hi = ng;  // group g with off[g] <= q < off[g+1]
+                while (hi - lo > 1) {
+                    uint64_t m = (lo + hi) >> 1;
+                    if (off[m] <= q) lo = m; else hi = m;
+                }
+                if (off[lo] != q) atomicOr_u8(ct + mem[q], 1);
+            } else if (q < e1) {
+                atomicOr_u8(ct + rx[q - e0], 2);
+            } else if (q < e2) {
+                const uint64_t k = q - e1;
+                uint64_t lo = 0, hi = rng;
+                while (hi - lo > 1) {
+                    uint64_t m = (lo + hi) >> 1;
+                    if (roff[m] <= k) lo = m; else hi = m;
+                }
+                if (roff[lo] == k) return;  // first pair of a group is necessary
+                const uint32_t r = rm[k];
+                atomicOr_u8(ct + pa[r], 4);
+                if (pd[r] != NONE) atomicOr_u8(ct + pd[r], 4);
+            } else if (q < e3) {
+                const uint32_t r = ua[q - e2];
+                atomicOr_u8(ct + pa[r], 8);
+                if (pd[r] != NONE) atomicOr_u8(ct + pd[r], 8);
+            } else {
+                atomicOr_u8(ct + ut[q - e3], 16);
             }
-            if (off[lo] != q) ct[mem[q]] |= 1;
         }, s);
-        const uint32_t *rx = F.rt_rx;
-        for_each(F.rt_trips, [=] __device__(size_t t) { ct[rx[t]] |= 2; }, s);
-        const uint64_t *roff = F.ra_off;
-        const uint32_t *rm = F.ra_mem, *pa = F.pa, *pd = F.pd;
-        const uint64_t rng = F.ra_groups;
-        for_each(F.ra_members, [=] __device__(size_t q) {
-            uint64_t lo = 0, hi = rng;
-            while (hi - lo > 1) {
-                uint64_t m = (lo + hi) >> 1;
-                if (roff[m] <= q) lo = m; else hi = m;
-            }
-            if (roff[lo] == q) return;  // first pair of a group is necessary
-            const uint32_t r = rm[q];
-            ct[pa[r]] |= 4;
-            if (pd[r] != NONE) ct[pd[r]] |= 4;
-        }, s);
-        const uint32_t *ua = F.ua;
-        for_each(F.n_ua, [=] __device__(size_t q) {
-            const uint32_t r = ua[q];
-            ct[pa[r]] |= 8;
-            if (pd[r] != NONE) ct[pd[r]] |= 8;
-        }, s);
-        const uint32_t *ut = F.ut;
-        for_each(F.n_ut, [=] __device__(size_t q) { ct[ut[q]] |= 16; }, s);
     }
     pc.mark("sv-catbits");
     // ---- sums, union, span
@@ -1903,16 +1932,14 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
         CK_LAUNCH("k_sums");
     }
     // overlap: exists i >= 1 with start[i] < max(end[0..i-1])  (estimator.py:51-58)
+    // ... and the union list, in the same scan
     DBuf<uint32_t> ovl(1, s);
     ovl.zero();
-    {
-        uint32_t *ov = ovl.p;
-        const uint64_t *st = c.start, *en = c.end;
-        scan<MaxU64>(n, LoadEnd{en}, StoreOverlap{st, ov}, s);
-    }
-    // union list
     DBuf<uint32_t> uni(n ? n : 1, s), unic(1, s);
-    compact(n, [=] __device__(size_t i) { return ct[i] != 0; }, uni.p, unic.p, s);
+    DBuf<OvUn::T> ovt(1, s);
+    scan<OvUn>(n, OvUnLoad{c.end, ct}, OvUnStore{c.start, ct, ovl.p, uni.p}, s, ovt.p);
+    if (n) CK(cudaMemcpyAsync(unic.p, &ovt.p->cnt, 4, cudaMemcpyDeviceToDevice, s));
+    else unic.zero();
     pc.mark("sv-sums");
     // ---- attribution
     const uint32_t nb = c.nbuckets;
