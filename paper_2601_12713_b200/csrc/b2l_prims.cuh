@@ -127,23 +127,40 @@ constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
+template <class T>
+__device__ __forceinline__ T shfl_up_t(T v, int off) {
+    static_assert(sizeof(T) % 4 == 0, "scan values are whole words");
+    unsigned *d = reinterpret_cast<unsigned *>(&v);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(T) / 4); ++i) d[i] = __shfl_up_sync(0xffffffffu, d[i], off);
+    return v;
+}
+// Exclusive block scan (256 threads): warp shuffle scans, then the 8 warp totals scanned by every
+// thread from shared memory -- two barriers.  `sm` needs SCAN_THREADS / 32 + 1 entries.
 template <class Op>
 __device__ __forceinline__ typename Op::T block_excl_scan(typename Op::T v, typename Op::T *sm,
                                                           typename Op::T &total) {
     using T = typename Op::T;
-    const int t = threadIdx.x;
-    sm[t] = v;
-    __syncthreads();
-#pragma unroll 1
-    for (int off = 1; off < SCAN_THREADS; off <<= 1) {
-        T x = t >= off ? sm[t - off] : Op::identity();
-        __syncthreads();
-        if (t >= off) sm[t] = Op::combine(x, sm[t]);
-        __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const T y = shfl_up_t(x, off);
+        if (lane >= off) x = Op::combine(y, x);
     }
-    total = sm[SCAN_THREADS - 1];
-    T ex = t ? sm[t - 1] : Op::identity();
+    if (lane == 31) sm[warp] = x;
     __syncthreads();
+    T before = Op::identity(), tot = Op::identity();
+#pragma unroll
+    for (int w = 0; w < SCAN_THREADS / 32; ++w) {
+        const T c = sm[w];
+        if (w < warp) before = Op::combine(before, c);
+        tot = Op::combine(tot, c);
+    }
+    total = tot;
+    T ex = shfl_up_t(x, 1);
+    ex = lane == 0 ? before : Op::combine(before, ex);
+    __syncthreads();  // sm is reused by the caller
     return ex;
 }
 
