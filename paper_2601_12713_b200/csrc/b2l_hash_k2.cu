@@ -262,13 +262,17 @@ __global__ void __launch_bounds__(THREADS, 2) k_hash_planes(const uint8_t *__res
     extern __shared__ uint32_t planes[];  // lo plane then hi plane, THREADS x ROW each
     __shared__ Shared sh;
     const int t = threadIdx.x;
-    const uint32_t G = gridDim.x, c = blockIdx.x;
+    // Two teams of CTAs take alternate rounds (team 0 the even ones): a round's CTAs wait on each
+    // other once per group, and with the two teams' CTAs sharing the SMs, one team's table
+    // passes fill the other's waits (team 1 runs about one group behind, on team 0's carries).
+    const uint32_t teams = gridDim.x >= 2 ? 2u : 1u;
+    const uint32_t G = gridDim.x / teams, team = blockIdx.x / G, c = blockIdx.x % G;
     const uint64_t nw = (nbytes + 7) >> 3;
     const uint64_t nchunks = (nw + CHUNK - 1) / CHUNK;
     const uint64_t rounds = (nchunks + G - 1) / G;
     uint32_t *plo = planes, *phi = planes + THREADS * ROW;
 
-    for (uint64_t r = 0; r < rounds; ++r) {
+    for (uint64_t r = team; r < rounds; r += teams) {
         const uint64_t q = r * G + c;
         if (q >= nchunks) break;  // only the last round has idle CTAs, and nobody waits on them
         const uint32_t nc = (uint32_t)(nchunks - r * G < G ? nchunks - r * G : G);  // CTAs in this round
@@ -291,7 +295,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_hash_planes(const uint8_t *__res
         __syncthreads();
     }
     // the final state is the carry of the last round; CTA 0 finishes the digest
-    if (c == 0 && threadIdx.x == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
         volatile unsigned long long *vcarry = carry;
         uint64_t h = 0;
         const uint64_t last = rounds - 1;
@@ -344,9 +348,12 @@ int hash_planes_launch(const void *d_buf, uint64_t nbytes, uint64_t *d_digest, c
     if (grid < 1) return fail(B2L_E_CUDA, "k_hash_planes: no occupancy");
     const uint64_t nw = (nbytes + 7) >> 3;
     const uint64_t nchunks = (nw + k2::CHUNK - 1) / k2::CHUNK;
-    const uint64_t g = nchunks < (uint64_t)grid ? nchunks : (uint64_t)grid;
-    const uint64_t rounds = (nchunks + g - 1) / g;
-    const size_t need_st = rounds * 16 * g, need_c = rounds * 16;
+    // two teams of g/2 CTAs (alternate rounds) when there are at least two rounds' worth of chunks
+    const uint64_t full = (uint64_t)grid & ~1ull;
+    const uint64_t g = nchunks >= full ? full : (nchunks >= 2 ? (nchunks + 1) / 2 * 2 : 1);
+    const uint64_t team = g >= 2 ? g / 2 : 1;
+    const uint64_t rounds = (nchunks + team - 1) / team;
+    const size_t need_st = rounds * 16 * team, need_c = rounds * 16;
     if (C.status_cap < need_st) {
         if (C.status) cudaFree(C.status);
         C.status = nullptr;
