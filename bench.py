@@ -522,7 +522,10 @@ def main():
         args._clock = clk
         rec = run_ours(args, rank, world, local)
         if not args.no_analysis:
-            rec["analysis"] = run_analysis_ours(args, rank, world, local)
+            try:
+                rec["analysis"] = run_analysis_ours(args, rank, world, local)
+            except Exception as exc:  # the hash line above stands on its own
+                rec["analysis"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     rec["clocks"] = clk.summary()
     rec["clocks"]["window"] = "sampled every 100 ms across both legs (warm-up + timed regions)"
     if rank == 0:
