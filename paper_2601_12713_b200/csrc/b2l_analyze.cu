@@ -636,6 +636,7 @@ struct QLoad {
     }
 };
 struct QStore {
+    static constexpr bool kStriped = true;  // six output arrays: coalesced stores pay
     const uint32_t *val;
     uint32_t *seg_of, *f_of, *j_of, *rxpos, *seg_start, *seg_rxbase;
     __device__ void operator()(size_t p, QState ex, QState it) const {

@@ -17,6 +17,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <utility>
 
 #include "b2l_common.cuh"
@@ -251,8 +252,10 @@ __device__ __forceinline__ T shfl_down_t(T v, int off) {
     return v;
 }
 
+// Blocked variant: thread t holds SCAN_ITEMS consecutive items in registers (one read of the
+// inputs); used unless the store functor asks for striped stores.
 template <class Op, class Load, class Store>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_1p(size_t n, Load ld, Store st, typename Op::T *agg,
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_1p_blocked(size_t n, Load ld, Store st, typename Op::T *agg,
                                                           typename Op::T *inc, uint32_t *flag, uint32_t *counter,
                                                           typename Op::T *d_total) {
     using T = typename Op::T;
@@ -328,6 +331,125 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_1p(size_t n, Load ld, Sto
     }
 }
 
+// Single-pass scan tiles: 256 threads x I items, I = 32 for values of up to 8 bytes, else 16.
+// Item j of a tile lives at shared slot (j / I) * (I + 1) + j % I: thread t's I consecutive
+// items form a padded row.
+template <class T>
+__host__ __device__ constexpr int scan_items() {
+    return sizeof(T) <= 8 ? 32 : 16;
+}
+template <class T>
+constexpr size_t scan_smem() {
+    return (size_t)SCAN_THREADS * (scan_items<T>() + 1) * sizeof(T);
+}
+
+// Loads and stores run in block-striped order (item k*256 + t for thread t: every warp access is
+// contiguous); the items sit in shared memory, where each thread reduces its row, and after the
+// look-back rewrites the row as exclusive prefixes, so the stores are striped again (the item
+// itself is re-read by the store pass, from L1).  Large tiles keep the look-back chain short.
+template <class Op, class Load, class Store>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_1p(size_t n, Load ld, Store st, typename Op::T *agg,
+                                                          typename Op::T *inc, uint32_t *flag, uint32_t *counter,
+                                                          typename Op::T *d_total) {
+    using T = typename Op::T;
+    constexpr int I = scan_items<T>();
+    constexpr int TILE = SCAN_THREADS * I;
+    extern __shared__ __align__(16) uint8_t scan_sm_raw[];
+    T *tr = reinterpret_cast<T *>(scan_sm_raw);  // SCAN_THREADS * (I + 1) slots
+    __shared__ T sm[SCAN_THREADS / 32 + 1];
+    __shared__ uint32_t tile_s;
+    __shared__ T prefix_s;
+    if (threadIdx.x == 0) tile_s = atomicAdd(counter, 1u);
+    __syncthreads();
+    const uint32_t tile = tile_s;
+    const size_t tb = (size_t)tile * TILE;
+    const int t = threadIdx.x;
+#pragma unroll 4
+    for (int k = 0; k < I; ++k) {
+        const int j = k * SCAN_THREADS + t;
+        tr[(j / I) * (I + 1) + j % I] = tb + j < n ? ld(tb + j) : Op::identity();
+    }
+    __syncthreads();
+    T *row = tr + t * (I + 1);
+    T acc = Op::identity();
+#pragma unroll 4
+    for (int k = 0; k < I; ++k) acc = Op::combine(acc, row[k]);
+    T total;
+    T ex = block_excl_scan<Op>(acc, sm, total);
+    volatile uint32_t *vf = flag;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        if (tile == 0) {
+            if (lane == 0) {
+                inc[0] = total;
+                __threadfence();
+                vf[0] = SP_INC;
+                prefix_s = Op::identity();
+            }
+        } else {
+            if (lane == 0) {
+                agg[tile] = total;
+                __threadfence();
+                vf[tile] = SP_AGG;
+            }
+            T prefix = Op::identity();
+            for (int64_t j = (int64_t)tile - 1;; j -= 32) {
+                const int64_t jj = j - lane;
+                uint32_t f = SP_INC;
+                if (jj >= 0)
+                    do {
+                        f = vf[jj];
+                    } while (f == 0);
+                __threadfence();
+                T v = jj < 0 ? Op::identity() : (f == SP_INC ? ld_l2(inc + jj) : ld_l2(agg + jj));
+                const uint32_t incm = __ballot_sync(0xffffffffu, f == SP_INC);
+                const int first = incm ? __ffs(incm) - 1 : 31;  // newest predecessor with an inclusive
+                if (lane > first) v = Op::identity();
+                // ordered reduction: lane l holds tile j - l (older for higher lanes)
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const T o = shfl_down_t(v, off);
+                    if (lane + off < 32) v = Op::combine(o, v);
+                }
+                prefix = Op::combine(v, prefix);  // lane 0 holds the window, oldest first
+                if (incm) break;
+            }
+            if (lane == 0) {
+                inc[tile] = Op::combine(prefix, total);
+                __threadfence();
+                vf[tile] = SP_INC;
+                prefix_s = prefix;
+            }
+        }
+    }
+    __syncthreads();
+    if (d_total && threadIdx.x == 0 && tb + TILE >= n) *d_total = Op::combine(prefix_s, total);
+    ex = Op::combine(prefix_s, ex);
+#pragma unroll 4
+    for (int k = 0; k < I; ++k) {  // exclusive prefixes over the own row, in place
+        const T it = row[k];
+        row[k] = ex;
+        ex = Op::combine(ex, it);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int k = 0; k < I; ++k) {
+        const int j = k * SCAN_THREADS + t;
+        if (tb + j < n) st(tb + j, tr[(j / I) * (I + 1) + j % I], ld(tb + j));
+    }
+}
+
+// Store functors that write several output arrays per item set `static constexpr bool kStriped
+// = true` and get the striped (coalesced-store) scan; the rest use the blocked one.
+template <class S, class = void>
+struct scan_striped {
+    static constexpr bool value = false;
+};
+template <class S>
+struct scan_striped<S, std::void_t<decltype(S::kStriped)>> {
+    static constexpr bool value = S::kStriped;
+};
+
 // scan over n items: st(i, exclusive_prefix, item) for every i; optional device total.
 template <class Op, class Load, class Store>
 void scan(size_t n, Load ld, Store st, cudaStream_t s, typename Op::T *d_total = nullptr) {
@@ -336,7 +458,9 @@ void scan(size_t n, Load ld, Store st, cudaStream_t s, typename Op::T *d_total =
         if (d_total) CK(cudaMemsetAsync(d_total, 0, sizeof(T), s));
         return;
     }
-    const size_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    constexpr bool striped = scan_striped<Store>::value;
+    constexpr size_t TILE = striped ? (size_t)SCAN_THREADS * scan_items<T>() : (size_t)SCAN_TILE;
+    const size_t tiles = (n + TILE - 1) / TILE;
     // flags + tile counter in one zeroed block; aggregates / inclusive prefixes beside them
     const size_t fwords = (tiles + 1 + 3) & ~size_t(3);
     const size_t tv = (tiles * sizeof(T) + 15) & ~size_t(15);
@@ -344,8 +468,22 @@ void scan(size_t n, Load ld, Store st, cudaStream_t s, typename Op::T *d_total =
     uint32_t *flag = reinterpret_cast<uint32_t *>(ws.p);
     CK(cudaMemsetAsync(flag, 0, fwords * 4, s));
     T *agg = reinterpret_cast<T *>(ws.p + fwords * 4), *inc = reinterpret_cast<T *>(ws.p + fwords * 4 + tv);
-    k_scan_1p<Op, Load, Store><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(n, ld, st, agg, inc, flag, flag + tiles,
-                                                                        d_total);
+    if constexpr (striped) {
+        constexpr size_t smem = scan_smem<T>();
+        if (smem > 48 * 1024) {
+            static bool opted = false;  // per instantiation
+            if (!opted) {
+                CK(cudaFuncSetAttribute(k_scan_1p<Op, Load, Store>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+                opted = true;
+            }
+        }
+        k_scan_1p<Op, Load, Store><<<(unsigned)tiles, SCAN_THREADS, smem, s>>>(n, ld, st, agg, inc, flag,
+                                                                               flag + tiles, d_total);
+    } else {
+        k_scan_1p_blocked<Op, Load, Store><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(n, ld, st, agg, inc, flag,
+                                                                                   flag + tiles, d_total);
+    }
     CK_LAUNCH("k_scan_1p");
 }
 
