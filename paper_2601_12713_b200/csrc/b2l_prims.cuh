@@ -690,7 +690,7 @@ __device__ __forceinline__ uint32_t block256_excl(uint32_t v, uint32_t *wsum, ui
     return before + x - v;
 }
 
-template <int KW>
+template <int KW, int ITEMS>
 __global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(KeyCols<KW> in, const uint32_t *__restrict__ vin,
                                                          KeyCols<KW> out, uint32_t *__restrict__ vout, size_t n,
                                                          int word, int shift, const uint32_t *__restrict__ hist,
@@ -699,29 +699,29 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(KeyCols<KW> in, cons
     __shared__ uint32_t wsum[2][OS_WARPS];
     __shared__ uint32_t wcnt[OS_WARPS][256];  // per-warp digit counts -> tile positions of each warp's run
     __shared__ uint32_t gofs[256];            // output index of tile position j of digit d = gofs[d] + j
-    __shared__ uint8_t sdig[OS_TILE];         // digit of tile position j
-    __shared__ uint64_t stage[OS_TILE];
+    __shared__ uint8_t sdig[(OS_THREADS * ITEMS)];         // digit of tile position j
+    __shared__ uint64_t stage[(OS_THREADS * ITEMS)];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     if (t == 0) tile_s = atomicAdd(tile_counter, 1u);
 #pragma unroll
     for (int w = 0; w < OS_WARPS; ++w) wcnt[w][t] = 0;
     __syncthreads();
     const uint32_t tile = tile_s;
-    const size_t tbase = (size_t)tile * OS_TILE;
-    const size_t wbase = tbase + (size_t)warp * (32 * OS_ITEMS) + lane;
+    const size_t tbase = (size_t)tile * (OS_THREADS * ITEMS);
+    const size_t wbase = tbase + (size_t)warp * (32 * ITEMS) + lane;
     const uint64_t *kd = in.w[word];
 
     // ---- load the digit word (warp-striped: item i of lane l is wbase + 32 i) and rank per warp
-    uint64_t key[OS_ITEMS];
-    uint32_t slot[OS_ITEMS];  // (digit << 16) | rank within this warp's run of the digit; ~0 = past n
+    uint64_t key[ITEMS];
+    uint32_t slot[ITEMS];  // (digit << 16) | rank within this warp's run of the digit; ~0 = past n
 #pragma unroll
-    for (int i = 0; i < OS_ITEMS; ++i) {
+    for (int i = 0; i < ITEMS; ++i) {
         const size_t pos = wbase + 32 * i;
         key[i] = pos < n ? kd[pos] : 0;
     }
     const uint32_t lt = lanemask_lt();
 #pragma unroll
-    for (int i = 0; i < OS_ITEMS; ++i) {
+    for (int i = 0; i < ITEMS; ++i) {
         const bool valid = wbase + 32 * i < n;
         const uint32_t d = valid ? (uint32_t)(key[i] >> shift) & 255u : 256u;
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(KeyCols<KW> in, cons
     __syncthreads();
     // ---- tile positions; digit of each position
 #pragma unroll
-    for (int i = 0; i < OS_ITEMS; ++i) {
+    for (int i = 0; i < ITEMS; ++i) {
         if (slot[i] == 0xFFFFFFFFu) continue;
         const uint32_t d = slot[i] >> 16;
         const uint32_t p = wcnt[warp][d] + (slot[i] & 0xFFFFu);
@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(KeyCols<KW> in, cons
         stage[p] = key[i];
     }
     __syncthreads();
-    const uint32_t tn = (uint32_t)(n - tbase < (size_t)OS_TILE ? n - tbase : (size_t)OS_TILE);
+    const uint32_t tn = (uint32_t)(n - tbase < (size_t)(OS_THREADS * ITEMS) ? n - tbase : (size_t)(OS_THREADS * ITEMS));
     {
         uint64_t *o = out.w[word];
         for (uint32_t j = t; j < tn; j += OS_THREADS) o[gofs[sdig[j]] + j] = stage[j];
@@ -793,23 +793,23 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(KeyCols<KW> in, cons
         if (w == word) continue;
         const uint64_t *src = in.w[w];
 #pragma unroll
-        for (int i = 0; i < OS_ITEMS; ++i) key[i] = slot[i] != 0xFFFFFFFFu ? src[wbase + 32 * i] : 0;
+        for (int i = 0; i < ITEMS; ++i) key[i] = slot[i] != 0xFFFFFFFFu ? src[wbase + 32 * i] : 0;
         __syncthreads();
 #pragma unroll
-        for (int i = 0; i < OS_ITEMS; ++i)
+        for (int i = 0; i < ITEMS; ++i)
             if (slot[i] != 0xFFFFFFFFu) stage[slot[i]] = key[i];
         __syncthreads();
         uint64_t *o = out.w[w];
         for (uint32_t j = t; j < tn; j += OS_THREADS) o[gofs[sdig[j]] + j] = stage[j];
     }
     {
-        uint32_t vv[OS_ITEMS];
+        uint32_t vv[ITEMS];
 #pragma unroll
-        for (int i = 0; i < OS_ITEMS; ++i) vv[i] = slot[i] != 0xFFFFFFFFu ? vin[wbase + 32 * i] : 0u;
+        for (int i = 0; i < ITEMS; ++i) vv[i] = slot[i] != 0xFFFFFFFFu ? vin[wbase + 32 * i] : 0u;
         uint32_t *st32 = reinterpret_cast<uint32_t *>(stage);
         __syncthreads();
 #pragma unroll
-        for (int i = 0; i < OS_ITEMS; ++i)
+        for (int i = 0; i < ITEMS; ++i)
             if (slot[i] != 0xFFFFFFFFu) st32[slot[i]] = vv[i];
         __syncthreads();
         for (uint32_t j = t; j < tn; j += OS_THREADS) vout[gofs[sdig[j]] + j] = st32[j];
@@ -839,7 +839,10 @@ void radix_sort(SortBufs<KW> &b, size_t n, LiveBytes<KW> live, cudaStream_t s) {
     hist.zero();
     k_radix_hist_all<KW><<<grid_for(n, RS_THREADS * 4, 148 * 4), RS_THREADS, 0, s>>>(b.k[b.cur], n, live, hist.p);
     CK_LAUNCH("k_radix_hist_all");
-    const unsigned ntiles = (unsigned)((n + OS_TILE - 1) / OS_TILE);
+    // small sorts use 1024-record tiles: four times the CTAs, so a pass is not a few long tiles
+    const bool small = n < (size_t)OS_TILE * 64;
+    const size_t tile = small ? (size_t)OS_THREADS * 4 : (size_t)OS_TILE;
+    const unsigned ntiles = (unsigned)((n + tile - 1) / tile);
     const size_t stride = (size_t)ntiles * 256 + 32;  // status words + tile counter per pass
     DBuf<uint32_t> status(stride * npass, s);
     status.zero();
@@ -848,9 +851,14 @@ void radix_sort(SortBufs<KW> &b, size_t n, LiveBytes<KW> live, cudaStream_t s) {
         for (int byte = 0; byte < 8; ++byte) {
             if (!((live.m[w] >> byte) & 1)) continue;
             uint32_t *stp = status.p + stride * p++;
-            k_onesweep<KW><<<ntiles, OS_THREADS, 0, s>>>(b.k[b.cur], b.v[b.cur], b.k[b.cur ^ 1], b.v[b.cur ^ 1], n, w,
-                                                         8 * byte, hist.p + (size_t)(w * 8 + byte) * 256, stp,
-                                                         stp + (size_t)ntiles * 256);
+            if (small)
+                k_onesweep<KW, 4><<<ntiles, OS_THREADS, 0, s>>>(b.k[b.cur], b.v[b.cur], b.k[b.cur ^ 1], b.v[b.cur ^ 1],
+                                                                n, w, 8 * byte, hist.p + (size_t)(w * 8 + byte) * 256,
+                                                                stp, stp + (size_t)ntiles * 256);
+            else
+                k_onesweep<KW, OS_ITEMS><<<ntiles, OS_THREADS, 0, s>>>(
+                    b.k[b.cur], b.v[b.cur], b.k[b.cur ^ 1], b.v[b.cur ^ 1], n, w, 8 * byte,
+                    hist.p + (size_t)(w * 8 + byte) * 256, stp, stp + (size_t)ntiles * 256);
             CK_LAUNCH("k_onesweep");
             b.cur ^= 1;
         }
