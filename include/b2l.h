@@ -258,6 +258,23 @@ int b2l_stable_sort_u64(const uint64_t *keys, uint64_t n, uint32_t strategy, uin
  * validated trace); UINT32_MAX when absent.  Host arrays. */
 int b2l_lookup_seqs(const b2l_trace_cols *cols, const uint64_t *seqs, uint64_t n, uint32_t *out_index);
 
+/* Key-range sharding (the reference has no multi-process analysis -- these route
+ * the events detectors.py:85-271 relate so that each rank's sub-traces are exact):
+ * b2l_shard_route: for a device-resident seq-range shard whose first event has global index
+ * `base`, writes one 12 x i64 row per record into d_rows (capacity 2 * n_events rows), grouped
+ * by destination rank in event order -- hashed transfers to the owner of their hash range
+ * ((hash * n_ranks) >> 64, space 0) and allocs, deletes, target kernels and target transfers
+ * to dst_device % n_ranks (space 1).  Row: [global index | space << 63, seq, start_ns, end_ns,
+ * src_addr, dst_addr, bytes, hash, src_device, dst_device, kind, loc].  counts[r] = rows for
+ * rank r; data_end_ns = max end over non-kernel events (prep.py:61-62's synthetic delete time).
+ * b2l_shard_unpack: received rows of one space -> device columns d_cols[0..11] (global index,
+ * seq, start, end, src_addr, dst_addr, bytes, hash as i64; src, dst as i32; kind u8; loc u32),
+ * capacity n_rows each; *n_out = rows of that space. */
+int b2l_shard_route(const b2l_trace_cols *cols, uint32_t n_ranks, uint64_t base, uint32_t flags, int64_t *d_rows,
+                    uint64_t *counts, uint64_t *n_rows, uint64_t *data_end_ns);
+int b2l_shard_unpack(const int64_t *d_rows, uint64_t n_rows, uint32_t space, int64_t *const *d_cols,
+                     uint64_t *n_out);
+
 #ifdef __cplusplus
 }
 #endif

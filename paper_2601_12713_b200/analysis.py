@@ -152,6 +152,27 @@ class DeviceColumns:
     def n(self):
         return self.host.n
 
+    @classmethod
+    def from_device(cls, t: dict, n: int, like: "DeviceColumns"):
+        """Columns already on the device (``t``: field -> tensor, u64 fields as int64, u32 as
+        int32), with the location table and trace metadata of ``like``."""
+        import dataclasses
+        self = cls.__new__(cls)
+        meta = like.host
+        self.host = dataclasses.replace(meta, n=n)  # metadata only: field arrays belong to `like`
+        self.t = dict(t)
+        self.t["loc_flags"], self.t["loc_bucket"] = like.t["loc_flags"], like.t["loc_bucket"]
+        ptr = lambda f: self.t[f].data_ptr() if self.t[f].numel() and n else None  # noqa: E731
+        self.struct = _Cols(n_events=n, num_devices_total=meta.num_devices_total, host_device=meta.host_device,
+                            seq=ptr("seq"), start_ns=ptr("start_ns"), end_ns=ptr("end_ns"), src_addr=ptr("src_addr"),
+                            dst_addr=ptr("dst_addr"), bytes=ptr("bytes"), hash=ptr("hash"),
+                            src_device=ptr("src_device"), dst_device=ptr("dst_device"), kind=ptr("kind"),
+                            loc=ptr("loc"), n_locs=int(meta.loc_flags.size),
+                            loc_flags=like.t["loc_flags"].data_ptr() if like.t["loc_flags"].numel() else None,
+                            loc_bucket=like.t["loc_bucket"].data_ptr() if like.t["loc_bucket"].numel() else None,
+                            n_buckets=meta.n_buckets, device_resident=1)
+        return self
+
 
 def _view(ptr, n, dtype, owner):
     """Zero-copy numpy view of engine-owned (pinned) memory; the view keeps `owner` alive."""

@@ -2038,6 +2038,161 @@ int lookup_impl(const b2l_trace_cols *cols, const uint64_t *seqs, uint64_t nq, u
 }  // namespace ana
 }  // namespace b2l
 
+namespace b2l {
+namespace ana {
+// ============================================================ key-range sharding
+// Rows exchanged between ranks: one i64 per field, ROW = 12:
+//   [0] global event index | key space << 63, then seq, start, end, src_addr, dst_addr, bytes, hash,
+//   src_device, dst_device, kind, loc (sharded.py FIELDS).
+constexpr int SH_ROW = 12;
+struct RouteCount {  // records per event: hash-keyed (space 0) and device-keyed (space 1)
+    DevCols c;
+    bool raw;
+    __device__ uint32_t operator()(size_t i) const {
+        const uint8_t k = c.kind[i];
+        const bool h = k == B2L_KIND_TRANSFER && (raw || (c.nb[i] > 0 && c.h[i] != 0));
+        const bool d = k == B2L_KIND_ALLOC || k == B2L_KIND_DELETE ||
+                       ((k == B2L_KIND_KERNEL || k == B2L_KIND_TRANSFER) && c.dst[i] != c.host);
+        return (h ? 1u : 0u) + (d ? 1u : 0u);
+    }
+};
+struct RouteStore {  // record keys (destination rank) and record ids (event << 1 | space)
+    DevCols c;
+    bool raw;
+    uint32_t G;
+    uint64_t *key;
+    uint32_t *rec;
+    __device__ void operator()(size_t i, uint32_t ex, uint32_t) const {
+        const uint8_t k = c.kind[i];
+        const bool h = k == B2L_KIND_TRANSFER && (raw || (c.nb[i] > 0 && c.h[i] != 0));
+        const bool d = k == B2L_KIND_ALLOC || k == B2L_KIND_DELETE ||
+                       ((k == B2L_KIND_KERNEL || k == B2L_KIND_TRANSFER) && c.dst[i] != c.host);
+        uint32_t o = ex;
+        if (h) {  // owner of the hash range: (hash * G) >> 64 on the top 32 bits
+            key[o] = ((c.h[i] >> 32) * (uint64_t)G) >> 32;
+            rec[o++] = (uint32_t)(i << 1);
+        }
+        if (d) {
+            key[o] = (uint64_t)((uint32_t)c.dst[i] % G);
+            rec[o] = (uint32_t)(i << 1) | 1u;
+        }
+    }
+};
+__global__ void k_route_rows(DevCols c, uint64_t base, const uint32_t *__restrict__ rec, uint64_t nrec,
+                             int64_t *__restrict__ rows) {
+    for (size_t r = (size_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrec; r += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t x = rec[r], e = x >> 1;
+        int64_t *o = rows + r * SH_ROW;
+        o[0] = (int64_t)((base + e) | ((uint64_t)(x & 1u) << 63));
+        o[1] = (int64_t)c.seq[e], o[2] = (int64_t)c.start[e], o[3] = (int64_t)c.end[e];
+        o[4] = (int64_t)c.sa[e], o[5] = (int64_t)c.da[e], o[6] = (int64_t)c.nb[e], o[7] = (int64_t)c.h[e];
+        o[8] = c.src[e], o[9] = c.dst[e], o[10] = c.kind[e], o[11] = c.loc[e];
+    }
+}
+__global__ void k_max_data_end(DevCols c, unsigned long long *out) {  // max end over non-kernel events
+    unsigned long long m = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += (size_t)gridDim.x * blockDim.x)
+        if (c.kind[i] != B2L_KIND_KERNEL && c.end[i] > m) m = c.end[i];
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+        m = v > m ? v : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+__global__ void k_route_counts(const uint64_t *__restrict__ key, uint64_t n, uint32_t G, unsigned long long *cnt) {
+    __shared__ unsigned long long sc[256];
+    for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) sc[g] = 0;
+    __syncthreads();
+    for (size_t r = (size_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (size_t)gridDim.x * blockDim.x)
+        atomicAdd(&sc[key[r]], 1ull);
+    __syncthreads();
+    for (uint32_t g = threadIdx.x; g < G; g += blockDim.x)
+        if (sc[g]) atomicAdd(cnt + g, sc[g]);
+}
+
+int shard_route_impl(const b2l_trace_cols *cols, uint32_t G, uint64_t base, uint32_t flags, int64_t *d_rows,
+                     uint64_t *h_counts, uint64_t *h_nrec, uint64_t *h_data_end) {
+    if (!cols->device_resident) return fail(B2L_E_INVALID_ARG, "b2l_shard_route: columns must be device-resident");
+    if (G == 0 || G > 256) return fail(B2L_E_INVALID_ARG, "b2l_shard_route: 1..256 ranks");
+    std::lock_guard<std::mutex> lock(g_mu);
+    cudaStream_t s = engine_stream();
+    ColsUpload up;
+    up.load(cols, s);
+    const DevCols c = up.d;
+    const size_t n = c.n;
+    const bool raw = (flags & B2L_ANALYZE_RAW_HASHED) != 0;
+    DBuf<uint64_t> key(2 * n + 1, s);
+    DBuf<uint32_t> rec(2 * n + 1, s), tot(1, s);
+    DBuf<unsigned long long> cnt(G + 1, s);  // [G] = max data-op end
+    cnt.zero();
+    scan<SumU32>(n, RouteCount{c, raw}, RouteStore{c, raw, G, key.p, rec.p}, s, tot.p);
+    if (n) {
+        k_max_data_end<<<grid_for(n, TPB, 148 * 8), TPB, 0, s>>>(c, cnt.p + G);
+        CK_LAUNCH("k_max_data_end");
+    }
+    uint32_t nrec = 0;
+    read_back(&nrec, tot.p, sizeof(nrec), s);
+    if (nrec) {
+        SortBufs<1> sb;  // stable grouping by destination rank, event order inside
+        DBuf<uint64_t> k2(nrec, s);
+        DBuf<uint32_t> v2(nrec, s);
+        sb.k[0].w[0] = key.p, sb.k[1].w[0] = k2.p, sb.v[0] = rec.p, sb.v[1] = v2.p, sb.cur = 0;
+        radix_sort<1>(sb, nrec, LiveBytes<1>{{live_range(G)}}, s);
+        k_route_counts<<<grid_for(nrec, 256, 148 * 4), 256, 0, s>>>(sb.k[sb.cur].w[0], nrec, G, cnt.p);
+        CK_LAUNCH("k_route_counts");
+        k_route_rows<<<grid_for(nrec, 256), 256, 0, s>>>(c, base, sb.v[sb.cur], nrec, d_rows);
+        CK_LAUNCH("k_route_rows");
+        std::vector<unsigned long long> hc(G + 1);
+        read_back(hc.data(), cnt.p, (G + 1) * sizeof(unsigned long long), s);
+        for (uint32_t g = 0; g < G; ++g) h_counts[g] = hc[g];
+        *h_data_end = hc[G];
+    } else {
+        unsigned long long me = 0;
+        read_back(&me, cnt.p + G, sizeof(me), s);
+        for (uint32_t g = 0; g < G; ++g) h_counts[g] = 0;
+        *h_data_end = me;
+    }
+    *h_nrec = nrec;
+    return B2L_OK;
+}
+
+// Received rows of one key space -> SoA device columns (rows arrive ordered by global index: each
+// source rank sends its records in event order, ranks hold increasing seq ranges).
+struct SpacePred {
+    const int64_t *rows;
+    uint32_t space;
+    __device__ bool operator()(size_t r) const { return ((uint64_t)rows[r * SH_ROW] >> 63) == space; }
+};
+struct UnpackOut {
+    int64_t *gid, *seq, *start, *end, *sa, *da, *nb, *h;
+    int32_t *src, *dst;
+    uint8_t *kind;
+    int32_t *loc;
+};
+int shard_unpack_impl(const int64_t *d_rows, uint64_t nrows, uint32_t space, const UnpackOut &o, uint64_t *h_n) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    cudaStream_t s = engine_stream();
+    DBuf<uint32_t> pos(nrows ? nrows : 1, s), cnt(1, s);
+    compact(nrows, SpacePred{d_rows, space}, pos.p, cnt.p, s);
+    uint32_t m = 0;
+    read_back(&m, cnt.p, sizeof(m), s);
+    const uint32_t *P = pos.p;
+    const UnpackOut O = o;
+    for_each(m, [=] __device__(size_t q) {
+        const int64_t *r = d_rows + (size_t)P[q] * SH_ROW;
+        O.gid[q] = r[0] & 0x7FFFFFFFFFFFFFFFll;
+        O.seq[q] = r[1], O.start[q] = r[2], O.end[q] = r[3], O.sa[q] = r[4], O.da[q] = r[5], O.nb[q] = r[6];
+        O.h[q] = r[7], O.src[q] = (int32_t)r[8], O.dst[q] = (int32_t)r[9], O.kind[q] = (uint8_t)r[10];
+        O.loc[q] = (int32_t)r[11];
+    }, s);
+    CK(cudaStreamSynchronize(s));
+    *h_n = m;
+    return B2L_OK;
+}
+
+}  // namespace ana
+}  // namespace b2l
+
 extern "C" {
 
 int b2l_analyze(const b2l_trace_cols *cols, uint32_t flags, b2l_findings **out) {
@@ -2143,6 +2298,29 @@ int b2l_sort_u64_pairs(const uint64_t *k0, const uint64_t *k1, uint64_t n, uint3
         radix_sort<2>(st.b, n, LiveBytes<2>{{live_mask(o0 ^ a0), live_mask(o1 ^ a1)}}, s);
         read_back(out_perm, st.val(), n * sizeof(uint32_t), s);
         return B2L_OK;
+    } catch (const b2l::EngineErr &e) {
+        return b2l::fail(e.code, e.msg);
+    }
+}
+
+int b2l_shard_route(const b2l_trace_cols *cols, uint32_t n_ranks, uint64_t base, uint32_t flags, int64_t *d_rows,
+                    uint64_t *counts, uint64_t *n_rows, uint64_t *data_end_ns) {
+    if (!cols || !d_rows || !counts || !n_rows || !data_end_ns) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
+    try {
+        return b2l::ana::shard_route_impl(cols, n_ranks, base, flags, d_rows, counts, n_rows, data_end_ns);
+    } catch (const b2l::EngineErr &e) {
+        return b2l::fail(e.code, e.msg);
+    }
+}
+
+int b2l_shard_unpack(const int64_t *d_rows, uint64_t n_rows, uint32_t space, int64_t *const *d_cols,
+                     uint64_t *n_out) {
+    if ((n_rows && !d_rows) || !d_cols || !n_out || space > 1) return b2l::fail(B2L_E_INVALID_ARG, "bad argument");
+    try {
+        b2l::ana::UnpackOut o{d_cols[0], d_cols[1], d_cols[2], d_cols[3], d_cols[4], d_cols[5], d_cols[6],
+                              d_cols[7], (int32_t *)d_cols[8], (int32_t *)d_cols[9], (uint8_t *)d_cols[10],
+                              (int32_t *)d_cols[11]};
+        return b2l::ana::shard_unpack_impl(d_rows, n_rows, space, o, n_out);
     } catch (const b2l::EngineErr &e) {
         return b2l::fail(e.code, e.msg);
     }

@@ -72,6 +72,17 @@ class LocalComm:
     def allreduce_max(self, v: int) -> int:
         return max(self._exchange(int(v)))
 
+    def alltoall_rows(self, rows, counts):
+        """Device rows grouped by destination rank (counts[r] rows for rank r) -> the rows every
+        rank sent to this one, in rank order (torch tensors stay on the device)."""
+        import torch
+        allp = self._exchange((rows, [int(x) for x in counts]))
+        got = []
+        for src_rows, src_counts in allp:
+            o = sum(src_counts[:self.rank])
+            got.append(src_rows[o:o + src_counts[self.rank]])
+        return torch.cat(got) if got else rows[:0]
+
     def allgather(self, obj):
         return self._exchange(obj)
 
@@ -107,6 +118,22 @@ class TorchComm:
             out.append(flat[o:o + r])
             o += r
         return out
+
+    def alltoall_rows(self, rows, counts):
+        """Device rows grouped by destination rank -> rows received from every rank, in rank order:
+        one all_to_all_single of the sizes, one of the rows (NCCL moves device memory over
+        NVLink; gloo stages through host memory)."""
+        torch, dist = self.torch, self.dist
+        width = rows.shape[1]
+        sizes = torch.tensor([int(x) for x in counts], dtype=torch.int64, device=self.device)
+        rsizes = torch.empty_like(sizes)
+        dist.all_to_all_single(rsizes, sizes)
+        rs = rsizes.cpu().tolist()
+        send = rows if self.device.type == rows.device.type else rows.to(self.device)
+        recv = torch.empty((sum(rs), width), dtype=rows.dtype, device=self.device)
+        dist.all_to_all_single(recv.view(-1), send.reshape(-1), [r * width for r in rs],
+                               [int(c) * width for c in counts])
+        return recv if recv.device == rows.device else recv.to(rows.device)
 
     def allreduce_max(self, v: int) -> int:
         """Max of a u64 over ranks, as (hi, lo) 32-bit halves (exact for any u64)."""
@@ -264,12 +291,229 @@ def analyze_sharded(shard: Columns, base: int, comm, strict: bool = False,
     return _merge(parts, synth_end, total_events=None)
 
 
+# ------------------------------------------------------------------------ device-resident pipeline
+_SHARD_FIELDS = ("gid", "seq", "start_ns", "end_ns", "src_addr", "dst_addr", "bytes", "hash", "src_device",
+                 "dst_device", "kind", "loc")
+
+
+def _shard_lib():
+    import ctypes
+
+    from . import _lib
+    L = _lib.lib()
+    L.b2l_shard_route.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32,
+                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    L.b2l_shard_unpack.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p,
+                                   ctypes.c_void_p]
+    return L, _lib
+
+
+def _route(shard, base: int, G: int):
+    """b2l_shard_route: device rows grouped by destination rank, counts, max data-op end."""
+    import ctypes
+
+    import torch
+    L, _lib = _shard_lib()
+    dev = shard.t["seq"].device
+    rows = torch.empty((max(2 * shard.n, 1), ROW), dtype=torch.int64, device=dev)
+    counts = np.zeros(G, np.uint64)
+    nrec, dend = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    _lib.check(L.b2l_shard_route(ctypes.addressof(shard.struct), G, base, 0, rows.data_ptr(), counts.ctypes.data,
+                                 ctypes.addressof(nrec), ctypes.addressof(dend)), "b2l_shard_route")
+    return rows[:nrec.value], counts, int(dend.value)
+
+
+def _unpack(recv, space: int, like):
+    """Rows of one key space -> (DeviceColumns sub-trace, global indices as a device tensor)."""
+    import ctypes
+
+    import torch
+
+    from .analysis import DeviceColumns
+    L, _lib = _shard_lib()
+    m, dev = recv.shape[0], recv.device
+    dt = {"src_device": torch.int32, "dst_device": torch.int32, "kind": torch.uint8, "loc": torch.int32}
+    t = {f: torch.empty(max(m, 1), dtype=dt.get(f, torch.int64), device=dev) for f in _SHARD_FIELDS}
+    ptrs = (ctypes.c_void_p * len(_SHARD_FIELDS))(*[t[f].data_ptr() for f in _SHARD_FIELDS])
+    n = ctypes.c_uint64(0)
+    _lib.check(L.b2l_shard_unpack(recv.data_ptr() if m else None, m, space, ptrs, ctypes.addressof(n)),
+               "b2l_shard_unpack")
+    k = n.value
+    gid = t.pop("gid")[:k]
+    return DeviceColumns.from_device({f: v[:k] for f, v in t.items()}, k, like), gid
+
+
+def _host(tensor, idx: np.ndarray, dtype):
+    """Device column values at host indices (small gathers for group sort keys)."""
+    import torch
+    if idx.size == 0:
+        return np.zeros(0, dtype)
+    ii = torch.from_numpy(np.ascontiguousarray(idx.astype(np.int64))).to(tensor.device)
+    v = tensor[ii].cpu().numpy()
+    return v.view(dtype) if v.dtype.itemsize == np.dtype(dtype).itemsize else v.astype(dtype)
+
+
+class _Phases:
+    """B2L_SHARD_TRACE=1: wall time of each phase on rank 0 (diagnostics only)."""
+
+    def __init__(self, rank):
+        import os
+        import time
+        self.on = rank == 0 and os.environ.get("B2L_SHARD_TRACE") is not None
+        self.time = time
+        self.t = time.perf_counter()
+
+    def mark(self, name):
+        if self.on:
+            now = self.time.perf_counter()
+            print(f"[shard] {name:10s} {1e3 * (now - self.t):8.3f} ms", flush=True)
+            self.t = now
+
+
+def analyze_sharded_device(shard, base: int, comm, strict: bool = False) -> Optional[ColumnarFindings]:
+    """The sharded pipeline with every event-sized step on the device: ``shard`` is a
+    DeviceColumns seq-range shard; validation, routing (b2l_shard_route), the all-to-all of
+    the rows (NCCL on device memory), unpacking (b2l_shard_unpack) and both engine runs stay in
+    HBM.  Only the findings (global indices and group sort keys) travel to rank 0 for the merge.
+    Same results and exceptions as ``analyze_sharded``."""
+    from .analysis import analyze_columns
+    G = comm.size
+    host = shard.host
+    ph = _Phases(comm.rank)
+    # ---- 1. validation (engine on the device shard) + the order rule across shard boundaries
+    bad_i, bad_r = np.zeros(0, np.int64), np.zeros(0, np.uint32)
+    try:
+        analyze_columns(shard, flags=FLAG_VALIDATE_ONLY)
+    except EngineInvalid as exc:
+        bad_i, bad_r = exc.bad_index.astype(np.int64), exc.bad_rules.astype(np.uint32)
+    edge = (int(host.start_ns[0]), int(host.seq[0]), int(host.start_ns[-1]), int(host.seq[-1])) if host.n else None
+    edges = comm.allgather(edge)
+    prev = None
+    for r in range(comm.rank):
+        if edges[r] is not None:
+            prev = edges[r]
+    if prev is not None and host.n:
+        s0, q0 = int(host.start_ns[0]), int(host.seq[0])
+        m = 0
+        if s0 < prev[2] or (s0 == prev[2] and q0 < prev[3]):
+            m |= 1 << 10
+        if q0 <= prev[3]:
+            m |= 1 << 11
+        if m:
+            k = np.nonzero(bad_i == 0)[0]
+            if k.size:
+                bad_r[k[0]] |= m
+            else:
+                bad_i, bad_r = np.concatenate([[0], bad_i]), np.concatenate([[m], bad_r]).astype(np.uint32)
+    all_bad = comm.allgather((bad_i + base, bad_r))
+    gi = np.concatenate([b[0] for b in all_bad])
+    if gi.size:
+        raise EngineInvalid(gi.astype(np.uint32), np.concatenate([b[1] for b in all_bad]).astype(np.uint32))
+    ph.mark("validate")
+    # ---- 2. route + one all-to-all of device rows
+    rows, counts, dmax = _route(shard, base, G) if host.n else (None, np.zeros(G, np.uint64), 0)
+    if rows is None:
+        import torch
+        rows = torch.empty((0, ROW), dtype=torch.int64, device=shard.t["seq"].device)
+    ph.mark("route")
+    recv = comm.alltoall_rows(rows, counts)
+    synth_end = comm.allreduce_max(dmax)
+    ph.mark("exchange")
+    sub_h, gid_h = _unpack(recv, 0, shard)
+    sub_d, gid_d = _unpack(recv, 1, shard)
+    ph.mark("unpack")
+    # ---- 3. per-rank engine runs on the two device sub-traces
+    out = {}
+    if sub_h.n:
+        f = analyzer_dev(sub_h, flags=FLAG_SKIP_ALLOC, strict=strict)
+        G_ = gid_h.cpu().numpy()
+        off = f.dd_offsets.astype(np.int64)
+        mem_l = f.dd_members.astype(np.int64)
+        fl = mem_l[off[:-1]] if off.size > 1 else np.zeros(0, np.int64)
+        t = sub_h.t
+        out["dd"] = (off, G_[mem_l], _host(t["start_ns"], fl, np.uint64), _host(t["hash"], fl, np.uint64),
+                     _host(t["dst_device"], fl, np.int32), G_[fl])
+        off = f.rt_offsets.astype(np.int64)
+        tx, rx = f.rt_tx.astype(np.int64), f.rt_rx.astype(np.int64)
+        ft = tx[off[:-1]] if off.size > 1 else np.zeros(0, np.int64)
+        out["rt"] = (off, G_[tx], G_[rx], _host(t["start_ns"], ft, np.uint64), _host(t["hash"], ft, np.uint64),
+                     _host(t["src_device"], ft, np.int32), _host(t["dst_device"], ft, np.int32))
+    if sub_d.n:
+        f = analyzer_dev(sub_d, flags=FLAG_SKIP_DDRT, synthetic_end_ns=synth_end)
+        G_ = gid_d.cpu().numpy()
+        pa = f.pair_alloc.astype(np.int64)
+        pd = f.pair_delete
+        out["pairs"] = (G_[pa], np.where(pd == SYN, -1, G_[np.where(pd == SYN, 0, pd).astype(np.int64)]))
+        out["warn"] = G_[f.warn_index.astype(np.int64)]
+        off = f.ra_offsets.astype(np.int64)
+        ra_alloc = G_[pa[f.ra_pairs.astype(np.int64)]]
+        fa = pa[f.ra_pairs[off[:-1]].astype(np.int64)] if off.size > 1 else np.zeros(0, np.int64)
+        t = sub_d.t
+        out["ra"] = (off, ra_alloc, _host(t["start_ns"], fa, np.uint64), _host(t["src_addr"], fa, np.uint64),
+                     _host(t["dst_device"], fa, np.int32), _host(t["bytes"], fa, np.uint64))
+        out["ua"] = G_[pa[f.ua_pairs.astype(np.int64)]]
+        out["ut"] = G_[f.ut_events.astype(np.int64)]
+    ph.mark("engine")
+    parts = comm.gather0(out)
+    ph.mark("gather")
+    if comm.rank != 0:
+        return None
+    res = _merge(parts, synth_end, total_events=None, lexsort=runs_lexsort)
+    ph.mark("merge")
+    return res
+
+
+def analyzer_dev(cols, flags=0, synthetic_end_ns=None, strict=False):
+    from .analysis import analyze_columns
+    return analyze_columns(cols, strict=strict, flags=flags, synthetic_end_ns=synthetic_end_ns)
+
+
 def _cat(parts, key, k, dtype):
     arrs = [p[key][k] for p in parts if key in p]
     return np.concatenate(arrs).astype(dtype) if arrs else np.zeros(0, dtype)
 
 
-def _merge_groups(parts, key, member_cols, sort_cols):
+def _np_lexsort(kcols):
+    return np.lexsort(tuple(reversed(kcols)))  # first column is the primary key
+
+
+def runs_lexsort(kcols):
+    """Lexicographic order of key columns (first = primary) for a concatenation of per-rank runs
+    that are each already sorted: a stable sort of the primary key alone (timsort merges the
+    runs in O(n log G)), then a full lexsort only when the primary key has ties."""
+    k0 = kcols[0]
+    order = np.argsort(k0, kind="stable")
+    s0 = k0[order]
+    if s0.size > 1 and np.any(s0[1:] == s0[:-1]):
+        return np.lexsort(tuple(reversed(kcols)))
+    return order
+
+
+def gpu_lexsort(kcols):
+    """Lexicographic order of u64 key columns (first = primary) with the engine's stable radix
+    sort, as LSD passes over (k[-2], k[-1]), (k[-4], k[-3]), ... (b2l_sort_u64_pairs)."""
+    import ctypes
+
+    from . import _lib
+    L = _lib.lib()
+    L.b2l_sort_u64_pairs.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
+    n = kcols[0].size
+    order = np.arange(n, dtype=np.int64)
+    if n < 2:
+        return order
+    cols = list(kcols)
+    if len(cols) % 2:
+        cols = [np.zeros(n, np.uint64)] + cols
+    perm = np.zeros(n, dtype=np.uint32)
+    for j in range(len(cols) - 2, -1, -2):
+        a = np.ascontiguousarray(cols[j][order], dtype=np.uint64)
+        b = np.ascontiguousarray(cols[j + 1][order], dtype=np.uint64)
+        _lib.check(L.b2l_sort_u64_pairs(a.ctypes.data, b.ctypes.data, n, perm.ctypes.data), "b2l_sort_u64_pairs")
+        order = order[perm]
+    return order
+
+
+def _merge_groups(parts, key, member_cols, sort_cols, lexsort=_np_lexsort):
     """Concatenate per-rank groups and order them by the given key columns (lexicographic)."""
     offs, mems, keys = [], [[] for _ in member_cols], [[] for _ in sort_cols]
     for p in parts:
@@ -288,26 +532,36 @@ def _merge_groups(parts, key, member_cols, sort_cols):
     size = np.concatenate(sizes)
     starts = np.concatenate([o[:-1] + sum(len(m) for m in mems[0][:i]) for i, o in enumerate(offs)])
     kcols = [np.concatenate(k) for k in keys]
-    order = np.lexsort(tuple(reversed(kcols)))  # first sort column is the primary key
+    order = lexsort(kcols)
     flat = [np.concatenate(m) for m in mems]
     new_off = np.zeros(size.size + 1, np.uint64)
     new_off[1:] = np.cumsum(size[order])
-    idx = np.concatenate([np.arange(starts[g], starts[g] + size[g]) for g in order]) if order.size else \
-        np.zeros(0, np.int64)
+    if order.size:  # members of the groups in their new order (vectorised ranges)
+        sz, st = size[order].astype(np.int64), starts[order].astype(np.int64)
+        first = np.zeros(sz.size, np.int64)
+        first[1:] = np.cumsum(sz)[:-1]
+        idx = np.repeat(st - first, sz) + np.arange(int(sz.sum()), dtype=np.int64)
+    else:
+        idx = np.zeros(0, np.int64)
     return new_off, [f[idx] for f in flat]
 
 
-def _merge(parts, synth_end, total_events=None) -> ColumnarFindings:
-    dd_off, (dd_mem,) = _merge_groups(parts, "dd", [1], [2, 3, 4])
-    rt_off, (rt_tx, rt_rx) = _merge_groups(parts, "rt", [1, 2], [3, 4, 5, 6])
+def _merge(parts, synth_end, total_events=None, lexsort=_np_lexsort) -> ColumnarFindings:
+    dd_off, (dd_mem,) = _merge_groups(parts, "dd", [1], [2, 3, 4], lexsort)
+    rt_off, (rt_tx, rt_rx) = _merge_groups(parts, "rt", [1, 2], [3, 4, 5, 6], lexsort)
     pa = _cat(parts, "pairs", 0, np.int64)
     pdl = _cat(parts, "pairs", 1, np.int64)
     o = np.argsort(pa, kind="stable")
     pa, pdl = pa[o], pdl[o]
-    ra_off, (ra_alloc,) = _merge_groups(parts, "ra", [1], [2, 3, 4, 5])
-    ra_pairs = np.searchsorted(pa, ra_alloc)
-    ua = np.sort(np.searchsorted(pa, np.concatenate([p["ua"] for p in parts if "ua" in p]) if any(
-        "ua" in p for p in parts) else np.zeros(0, np.int64)))
+    ra_off, (ra_alloc,) = _merge_groups(parts, "ra", [1], [2, 3, 4, 5], lexsort)
+    # pair rank of an alloc event: a direct lookup table over event ids (random queries into a
+    # sorted array would be one cache miss per binary-search step)
+    pos = np.zeros(int(pa[-1]) + 1 if pa.size else 1, np.int64)
+    pos[pa] = np.arange(pa.size, dtype=np.int64)
+    ra_pairs = pos[np.asarray(ra_alloc, dtype=np.int64)]
+    ua_ev = np.concatenate([p["ua"] for p in parts if "ua" in p]).astype(np.int64) if any(
+        "ua" in p for p in parts) else np.zeros(0, np.int64)
+    ua = np.sort(pos[ua_ev])
     ut = np.sort(np.concatenate([p["ut"] for p in parts if "ut" in p])) if any("ut" in p for p in parts) else \
         np.zeros(0, np.int64)
     warn = np.sort(np.concatenate([p["warn"] for p in parts if "warn" in p])) if any(
@@ -347,6 +601,30 @@ def run_local(cols: Columns, g: int, strict: bool = False, analyzer: Callable = 
     def work(r):
         try:
             res[r] = analyze_sharded(shards[r][0], shards[r][1], comms[r], strict=strict, analyzer=analyzer)
+        except BaseException as exc:  # surfaced below
+            errs[r] = exc
+            comms[r].s.barrier.abort()
+    th = [threading.Thread(target=work, args=(r,)) for r in range(g)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in errs:
+        if e is not None and not isinstance(e, threading.BrokenBarrierError):
+            raise e
+    return res[0]
+
+
+def run_local_device(cols: Columns, g: int, strict: bool = False, device="cuda"):
+    """G ranks as threads sharing one device, each with a device-resident shard."""
+    from .analysis import DeviceColumns
+    comms = LocalComm.group(g)
+    shards = [(DeviceColumns(sc, device), b) for sc, b in split(cols, g)]
+    res, errs = [None] * g, [None] * g
+
+    def work(r):
+        try:
+            res[r] = analyze_sharded_device(shards[r][0], shards[r][1], comms[r], strict=strict)
         except BaseException as exc:  # surfaced below
             errs[r] = exc
             comms[r].s.barrier.abort()

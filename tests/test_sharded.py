@@ -93,6 +93,39 @@ def test_local_ranks_engine_on_gpu(cuda, g):
             assert got.warn_index.tolist() == want.warn_index.tolist()
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("g", [2, 3, 4])
+def test_device_resident_ranks_on_gpu(cuda, g):
+    """The device-resident pipeline (b2l_shard_route / all-to-all of device rows /
+    b2l_shard_unpack / engine on device sub-traces) equals the single-GPU engine."""
+    from paper_2601_12713_b200 import analyze_columns
+    from paper_2601_12713_b200.synth import c2_trace, c4_trace
+    cases = _valid_traces(40, seed0=7000 + g) + [c2_trace(100_000, seed=3), c4_trace(100_000, seed=5)]
+    for c in cases:
+        for strict in (False, True):
+            got = sharded.run_local_device(c, g, strict=strict)
+            want = analyze_columns(c, strict=strict)
+            assert canon_columnar(got, c) == canon_columnar(want, c)
+            assert got.warn_index.tolist() == want.warn_index.tolist()
+            assert got.synthetic_end_ns == want.synthetic_end_ns
+
+
+@pytest.mark.gpu
+def test_device_resident_invalid_shard_reports_global_indices(cuda):
+    from paper_2601_12713_b200.analysis import EngineInvalid
+    c = _valid_traces(1, seed0=77)[0]
+    c.start_ns = c.start_ns.copy()
+    c.start_ns[c.n // 2] = 0 if c.start_ns[c.n // 2 - 1] > 0 else c.start_ns[c.n // 2]
+    if not R.validate_cols(c):
+        pytest.skip("mutation kept the trace valid")
+    with pytest.raises(EngineInvalid) as ei:
+        sharded.run_local_device(c, 2)
+    with pytest.raises(EngineInvalid) as ej:
+        sharded.run_local(c, 2)
+    assert ei.value.bad_index.tolist() == ej.value.bad_index.tolist()
+    assert ei.value.bad_rules.tolist() == ej.value.bad_rules.tolist()
+
+
 def _gloo_engine_worker(rank, world, port, result_path):
     """Two processes on one GPU: TorchComm over gloo for the exchange, the CUDA engine per shard."""
     import torch.distributed as dist
@@ -104,11 +137,15 @@ def _gloo_engine_worker(rank, world, port, result_path):
         from paper_2601_12713_b200.synth import c2_trace, c4_trace
         comm = sharded.TorchComm()
         ok = True
+        from paper_2601_12713_b200.analysis import DeviceColumns
         for c in _valid_traces(10, seed0=700) + [c2_trace(50_000, seed=7), c4_trace(50_000, seed=8)]:
             shard, base = sharded.split(c, world)[rank]
             got = sharded.analyze_sharded(shard, base, comm)
+            got_dev = sharded.analyze_sharded_device(DeviceColumns(shard), base, comm)
             if rank == 0:
-                ok &= canon_columnar(got, c) == canon_columnar(analyze_columns(c), c)
+                want = canon_columnar(analyze_columns(c), c)
+                ok &= canon_columnar(got, c) == want
+                ok &= canon_columnar(got_dev, c) == want
         if rank == 0:
             with open(result_path, "w") as f:
                 f.write("ok" if ok else "mismatch")
