@@ -27,8 +27,8 @@ namespace k2 {
 
 constexpr int THREADS = 256;
 constexpr int WARPS = THREADS / 32;
-constexpr int WPT = 48;                   // words per thread, resident in shared memory
-constexpr int CHUNK = THREADS * WPT;      // words per CTA per round (96 KiB; two CTAs per SM)
+constexpr int WPT = 24;                   // words per thread, resident in shared memory
+constexpr int CHUNK = THREADS * WPT;      // words per CTA per round (48 KiB; four CTAs per SM)
 constexpr int ROW = WPT + 1;              // padded row (u32 units): conflict-free column access
 constexpr size_t SMEM = (size_t)2 * THREADS * ROW * sizeof(uint32_t);  // lo and hi planes
 
@@ -256,16 +256,16 @@ __device__ __forceinline__ void group_step(uint32_t *ylo, uint32_t *yhi, int nv,
     }
 }
 
-__global__ void __launch_bounds__(THREADS, 2) k_hash_planes(const uint8_t *__restrict__ buf, uint64_t nbytes,
+__global__ void __launch_bounds__(THREADS, 4) k_hash_planes(const uint8_t *__restrict__ buf, uint64_t nbytes,
                                                             uint4 *aggs, unsigned long long *carry,
-                                                            uint64_t *digest) {
+                                                            uint64_t *digest, uint32_t teams) {
     extern __shared__ uint32_t planes[];  // lo plane then hi plane, THREADS x ROW each
     __shared__ Shared sh;
     const int t = threadIdx.x;
-    // Two teams of CTAs take alternate rounds (team 0 the even ones): a round's CTAs wait on each
-    // other once per group, and with the two teams' CTAs sharing the SMs, one team's table
-    // passes fill the other's waits (team 1 runs about one group behind, on team 0's carries).
-    const uint32_t teams = gridDim.x >= 2 ? 2u : 1u;
+    // `teams` teams of CTAs take rounds in turn (team t the rounds r = t mod teams): a round's
+    // CTAs wait on each other once per group, and with one CTA of every team on each SM, the
+    // other teams' table passes fill a team's waits (each team runs about one group behind the
+    // previous one, on its carries).
     const uint32_t G = gridDim.x / teams, team = blockIdx.x / G, c = blockIdx.x % G;
     const uint64_t nw = (nbytes + 7) >> 3;
     const uint64_t nchunks = (nw + CHUNK - 1) / CHUNK;
@@ -348,10 +348,12 @@ int hash_planes_launch(const void *d_buf, uint64_t nbytes, uint64_t *d_digest, c
     if (grid < 1) return fail(B2L_E_CUDA, "k_hash_planes: no occupancy");
     const uint64_t nw = (nbytes + 7) >> 3;
     const uint64_t nchunks = (nw + k2::CHUNK - 1) / k2::CHUNK;
-    // two teams of g/2 CTAs (alternate rounds) when there are at least two rounds' worth of chunks
-    const uint64_t full = (uint64_t)grid & ~1ull;
-    const uint64_t g = nchunks >= full ? full : (nchunks >= 2 ? (nchunks + 1) / 2 * 2 : 1);
-    const uint64_t team = g >= 2 ? g / 2 : 1;
+    // one team per co-resident CTA per SM when there is a full grid of chunks, else one team
+    const uint32_t per_sm = (uint32_t)(grid / sm_count());
+    uint32_t teams = per_sm >= 1 ? per_sm : 1;
+    uint64_t g = (uint64_t)sm_count() * teams;
+    if (nchunks < g) teams = 1, g = nchunks;
+    const uint64_t team = g / teams;
     const uint64_t rounds = (nchunks + team - 1) / team;
     const size_t need_st = rounds * 16 * team, need_c = rounds * 16;
     if (C.status_cap < need_st) {
@@ -371,7 +373,8 @@ int hash_planes_launch(const void *d_buf, uint64_t nbytes, uint64_t *d_digest, c
     B2L_CUDA(cudaMemsetAsync(C.status, 0, need_st * sizeof(uint4), stream));
     B2L_CUDA(cudaMemsetAsync(C.carry, 0, need_c * sizeof(unsigned long long), stream));
     const uint8_t *b = (const uint8_t *)d_buf;
-    void *args[] = {(void *)&b, (void *)&nbytes, (void *)&C.status, (void *)&C.carry, (void *)&d_digest};
+    void *args[] = {(void *)&b, (void *)&nbytes, (void *)&C.status, (void *)&C.carry, (void *)&d_digest,
+                    (void *)&teams};
     B2L_CUDA(cudaLaunchCooperativeKernel((const void *)k2::k_hash_planes, dim3((unsigned)g), dim3(k2::THREADS), args,
                                          k2::SMEM, stream));
     return B2L_OK;
