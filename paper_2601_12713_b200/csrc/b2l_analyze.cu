@@ -140,10 +140,6 @@ __device__ __forceinline__ uint32_t event_rules(const DevCols &c, size_t i) {
     const Row r = load_row(c, i);
     return row_rules(c, r, i > 0, i > 0 ? c.start[i - 1] : 0, i > 0 ? c.seq[i - 1] : 0);
 }
-struct BadPred {
-    DevCols c;
-    __device__ bool operator()(size_t i) const { return event_rules(c, i) != 0; }
-};
 __global__ void k_bad_rules(DevCols c, const uint32_t *bad, const uint32_t *count, uint32_t *rules) {
     const uint32_t nb = *count;
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nb; k += gridDim.x * blockDim.x)
@@ -151,29 +147,6 @@ __global__ void k_bad_rules(DevCols c, const uint32_t *bad, const uint32_t *coun
 }
 
 // ============================================================ partition (detectors.py:296-312)
-struct IsHashed {  // transfers with bytes > 0 and a content hash (raw: every transfer row)
-    DevCols c;
-    bool raw;
-    __device__ bool operator()(size_t i) const {
-        return c.kind[i] == B2L_KIND_TRANSFER && (raw || (c.nb[i] > 0 && c.h[i] != 0));
-    }
-};
-struct IsTargetTransfer {
-    DevCols c;
-    __device__ bool operator()(size_t i) const { return c.kind[i] == B2L_KIND_TRANSFER && c.dst[i] != c.host; }
-};
-struct IsAllocDelete {
-    DevCols c;
-    __device__ bool operator()(size_t i) const { return c.kind[i] == B2L_KIND_ALLOC || c.kind[i] == B2L_KIND_DELETE; }
-};
-struct IsAlloc {
-    DevCols c;
-    __device__ bool operator()(size_t i) const { return c.kind[i] == B2L_KIND_ALLOC; }
-};
-struct IsTargetKernel {
-    DevCols c;
-    __device__ bool operator()(size_t i) const { return c.kind[i] == B2L_KIND_KERNEL && c.dst[i] != c.host; }
-};
 
 // ============================================================ fused front pass
 // validate + partition + max data-op end + key-bit variation + start ranks in one
@@ -1659,17 +1632,6 @@ struct OvUnStore {
     __device__ void operator()(size_t i, OvUn::T ex, OvUn::T) const {
         if (i > 0 && start[i] < ex.mx) *flag = 1;
         if (cat[i]) uni[ex.cnt] = (uint32_t)i;
-    }
-};
-struct LoadEnd {
-    const uint64_t *e;
-    __device__ uint64_t operator()(size_t i) const { return e[i]; }
-};
-struct StoreOverlap {
-    const uint64_t *start;
-    uint32_t *flag;
-    __device__ void operator()(size_t i, uint64_t ex, uint64_t) const {
-        if (i > 0 && start[i] < ex) *flag = 1;
     }
 };
 struct U128 {

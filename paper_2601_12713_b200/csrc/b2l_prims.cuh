@@ -1,13 +1,16 @@
 // Device-wide primitives for the trace-analysis pipeline (sm_100a, hand-written):
 //   * stream-ordered scratch buffers (cudaMallocAsync pool)
-//   * generic tile scan (reduce-then-scan, 3 launches) over functor inputs/outputs,
+//   * generic single-pass scan (decoupled look-back, one launch) over functor inputs/outputs,
 //     with a segmented wrapper -- used for counts, prefix maxima, the max-plus
 //     depth scan of alloc/delete pairing, run ids, compaction
 //   * stable LSD radix sort of (multi-word u64 key, u32 value) records: 8-bit
-//     digits, per-tile histograms + scanned digit offsets, stable tile ranking with
-//     warp __match_any_sync multisplit; digit passes whose byte never varies are
-//     skipped (planned from an OR-of-XOR reduction), so wide composite keys cost
-//     only their live bytes.
+//     digits, one histogram read for all digits, one Onesweep launch per digit
+//     (warp __match_any_sync multisplit ranking, decoupled look-back, coalesced
+//     digit-ordered scatter through shared memory); digit passes whose byte never
+//     varies are skipped (planned from an OR-of-XOR reduction), so wide composite
+//     keys cost only their live bytes
+//   * segmented fix-up: records ordered by a key prefix become ordered by the full
+//     key in one pass (runs found by head-bit scans), and the wide sort built on it
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -165,20 +168,8 @@ __device__ __forceinline__ typename Op::T block_excl_scan(typename Op::T v, type
     return ex;
 }
 
-template <class Op, class Load>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(size_t n, Load ld, typename Op::T *partials) {
-    using T = typename Op::T;
-    __shared__ T sm[SCAN_THREADS];
-    const size_t base = (size_t)blockIdx.x * SCAN_TILE + (size_t)threadIdx.x * SCAN_ITEMS;
-    T acc = Op::identity();
-#pragma unroll
-    for (int k = 0; k < SCAN_ITEMS; ++k)
-        if (base + k < n) acc = Op::combine(acc, ld(base + k));
-    T total;
-    block_excl_scan<Op>(acc, sm, total);
-    if (threadIdx.x == 0) partials[blockIdx.x] = total;
-}
 
+// In-place exclusive scan of per-tile partials by one CTA (the fused front pass).
 template <class Op>
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_partials(typename Op::T *partials, size_t np,
                                                                  typename Op::T *d_total) {
@@ -204,28 +195,6 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_partials(typename Op::T *
         carry = Op::combine(carry, total);
     }
     if (threadIdx.x == 0 && d_total) *d_total = carry;
-}
-
-template <class Op, class Load, class Store>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(size_t n, Load ld, Store st,
-                                                             const typename Op::T *partials) {
-    using T = typename Op::T;
-    __shared__ T sm[SCAN_THREADS];
-    const size_t base = (size_t)blockIdx.x * SCAN_TILE + (size_t)threadIdx.x * SCAN_ITEMS;
-    T items[SCAN_ITEMS];
-    T acc = Op::identity();
-#pragma unroll
-    for (int k = 0; k < SCAN_ITEMS; ++k) {
-        items[k] = base + k < n ? ld(base + k) : Op::identity();
-        acc = Op::combine(acc, items[k]);
-    }
-    T total;
-    T ex = Op::combine(partials[blockIdx.x], block_excl_scan<Op>(acc, sm, total));
-#pragma unroll
-    for (int k = 0; k < SCAN_ITEMS; ++k) {
-        if (base + k < n) st(base + k, ex, items[k]);
-        ex = Op::combine(ex, items[k]);
-    }
 }
 
 // ---------------------------------------------------------------- single-pass scan

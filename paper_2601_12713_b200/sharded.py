@@ -489,30 +489,6 @@ def runs_lexsort(kcols):
     return order
 
 
-def gpu_lexsort(kcols):
-    """Lexicographic order of u64 key columns (first = primary) with the engine's stable radix
-    sort, as LSD passes over (k[-2], k[-1]), (k[-4], k[-3]), ... (b2l_sort_u64_pairs)."""
-    import ctypes
-
-    from . import _lib
-    L = _lib.lib()
-    L.b2l_sort_u64_pairs.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
-    n = kcols[0].size
-    order = np.arange(n, dtype=np.int64)
-    if n < 2:
-        return order
-    cols = list(kcols)
-    if len(cols) % 2:
-        cols = [np.zeros(n, np.uint64)] + cols
-    perm = np.zeros(n, dtype=np.uint32)
-    for j in range(len(cols) - 2, -1, -2):
-        a = np.ascontiguousarray(cols[j][order], dtype=np.uint64)
-        b = np.ascontiguousarray(cols[j + 1][order], dtype=np.uint64)
-        _lib.check(L.b2l_sort_u64_pairs(a.ctypes.data, b.ctypes.data, n, perm.ctypes.data), "b2l_sort_u64_pairs")
-        order = order[perm]
-    return order
-
-
 def _merge_groups(parts, key, member_cols, sort_cols, lexsort=_np_lexsort):
     """Concatenate per-rank groups and order them by the given key columns (lexicographic)."""
     offs, mems, keys = [], [[] for _ in member_cols], [[] for _ in sort_cols]
