@@ -85,13 +85,21 @@ def ncu_traffic():
     return None
 
 
-def analysis_traffic(n_events):
-    """DRAM bytes per analyze+savings step from the committed ncu capture of the same workload."""
+def analysis_traffic(n_events, peak=None):
+    """DRAM bytes per analyze+savings step from the committed ncu capture of the same workload,
+    and the top kernels' own DRAM rates (bytes each moved / its cold ncu duration)."""
     p = os.path.join(ROOT, "profiles", f"analysis_traffic_c2_{n_events}.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get("dram_bytes_per_step"), d.get("launches_per_step")
-    return None, None
+        top = []
+        for k in d.get("kernels", [])[:6]:
+            gbs = k["dram_bytes"] / (k["time_us"] * 1e-6) / 1e9 if k["time_us"] else 0.0
+            l2 = k.get("l2_bytes", 0.0) / (k["time_us"] * 1e-6) / 1e9 if k["time_us"] else 0.0
+            top.append({"kernel": k["kernel"].replace("void ", "")[:60], "launches": k["launches"],
+                        "us": round(k["time_us"], 1), "dram_gbs": round(gbs, 1), "l2_gbs": round(l2, 1),
+                        "dram_frac": round(gbs / peak, 3) if peak else None})
+        return d.get("dram_bytes_per_step"), d.get("launches_per_step"), top
+    return None, None, []
 
 
 class ClockSampler:
@@ -350,7 +358,7 @@ def run_analysis_ours(args, rank, world, local):
                                  cfh.ua_pairs, cfh.ut_events))
     peak, peak_src = peaks()
     achieved = cols.n * EVENT_BYTES / step_s / 1e9
-    traffic, launches = analysis_traffic(cols.n)
+    traffic, launches, top = analysis_traffic(cols.n, peak)
     out = {
         "metric": "M trace events/s analysed", "value": round(value, 3), "unit": "M events/s",
         "ms_per_step": round(step_s * 1e3, 3), "steps": args.steps,
@@ -367,7 +375,8 @@ def run_analysis_ours(args, rank, world, local):
                                      "(profiles/analysis_traffic_c2_<n>.json); the pipeline moves traffic/64 B "
                                      "per event across its sort/scan passes",
                      "traffic_gbs_over_step": round(traffic / step_s / 1e9, 1) if traffic else None,
-                     "kernel_launches_per_step": launches},
+                     "kernel_launches_per_step": launches,
+                     "top_kernels_ncu": top},
         "e2e": {"value": round(world * cols.n * e2e_steps / float(de.item()) / 1e6, 3), "unit": "M events/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "b2l_analyze + b2l_savings_compute on host numpy columns in page-locked memory"},
