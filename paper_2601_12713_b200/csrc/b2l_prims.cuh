@@ -808,8 +808,9 @@ void radix_sort(SortBufs<KW> &b, size_t n, LiveBytes<KW> live, cudaStream_t s) {
     hist.zero();
     k_radix_hist_all<KW><<<grid_for(n, RS_THREADS * 4, 148 * 4), RS_THREADS, 0, s>>>(b.k[b.cur], n, live, hist.p);
     CK_LAUNCH("k_radix_hist_all");
-    // small sorts use 1024-record tiles: four times the CTAs, so a pass is not a few long tiles
-    const bool small = n < (size_t)OS_TILE * 64;
+    // sorts under ~1.2M records use 1024-record tiles: four times the CTAs, so a pass is not a few
+    // long tiles on part of the GPU
+    const bool small = n < (size_t)OS_TILE * 296;  // fewer than two big tiles per SM
     const size_t tile = small ? (size_t)OS_THREADS * 4 : (size_t)OS_TILE;
     const unsigned ntiles = (unsigned)((n + tile - 1) / tile);
     const size_t stride = (size_t)ntiles * 256 + 32;  // status words + tile counter per pass
