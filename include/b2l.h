@@ -275,6 +275,41 @@ int b2l_shard_route(const b2l_trace_cols *cols, uint32_t n_ranks, uint64_t base,
 int b2l_shard_unpack(const int64_t *d_rows, uint64_t n_rows, uint32_t space, int64_t *const *d_cols,
                      uint64_t *n_out);
 
+/* ---------------------------------------------------------------- capture agent
+ * Native model of the reference's OMPT capture shim (SPEC.md "ompt-shim",
+ * pkg/shim/src/capture.ts:93-327): paired begin/end callbacks -> trace events, per-thread
+ * buffers merged by (t0, arrival), runtime device ids -> dense slots (host at slot 0).
+ * Transfer payloads are hashed on the GPU where they live: `device_buffer` (the landed
+ * destination of a host-to-device copy at end, the source of a device-to-host copy) with K1/K2
+ * synchronously in the callback; `host_buffer` only when the runtime offers nothing else
+ * (host-to-device at begin, device-to-host at end, capture.ts:210,262).  time_ns = UINT64_MAX:
+ * the agent's monotonic clock (origin at create).  Data-op types are OMPT's
+ * ompt_target_data_op_t values. */
+typedef struct b2l_capture b2l_capture;
+enum { B2L_CAPTURE_BEGIN = 1, B2L_CAPTURE_END = 2 };  /* ompt_scope_begin / ompt_scope_end */
+enum { B2L_OP_ALLOC = 1, B2L_OP_TO_DEVICE = 2, B2L_OP_FROM_DEVICE = 3, B2L_OP_DELETE = 4 };
+b2l_capture *b2l_capture_create(int32_t host_runtime_id);
+void b2l_capture_destroy(b2l_capture *c);
+/* audit mode (payload sidecars "<seq>.bin"); the default comes from $DMLENS_AUDIT_DIR */
+int b2l_capture_set_audit_dir(b2l_capture *c, const char *dir);
+/* CaptureShim.deviceSlot (capture.ts:126-134) */
+int32_t b2l_capture_device_slot(b2l_capture *c, int32_t runtime_id);
+/* onTargetBegin / onTargetEnd (capture.ts:164-189) */
+int b2l_capture_target(b2l_capture *c, int endpoint, uint64_t target_id, int32_t device_id, uint64_t codeptr,
+                       uint64_t thread_id, uint64_t time_ns);
+/* onDataOpBegin / onDataOpEnd (capture.ts:193-275) */
+int b2l_capture_data_op(b2l_capture *c, int endpoint, uint64_t host_op_id, int optype, int32_t src_device,
+                        int32_t dst_device, uint64_t src_addr, uint64_t dst_addr, uint64_t bytes, uint64_t codeptr,
+                        uint64_t thread_id, uint64_t time_ns, const void *device_buffer, const void *host_buffer);
+/* finalize (capture.ts:279-303): NDJSON text (free with b2l_capture_free_text); wall_time_ns =
+ * UINT64_MAX derives it from the last event end.  Capture state is left untouched. */
+int b2l_capture_finalize(b2l_capture *c, uint64_t wall_time_ns, char **text, uint64_t *len);
+void b2l_capture_free_text(char *text);
+/* writeTrace (capture.ts:305-321): out_path NULL -> $DMLENS_OUT (error if unset) */
+int b2l_capture_write(b2l_capture *c, const char *out_path, uint64_t wall_time_ns);
+/* ShimWarnings: [unmatched_ends, unfinished_at_exit, hash_skipped, dropped_malformed] */
+int b2l_capture_warnings(b2l_capture *c, uint64_t *out4);
+
 #ifdef __cplusplus
 }
 #endif

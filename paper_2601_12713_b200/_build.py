@@ -10,7 +10,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libb2l.so")
-SOURCES = ["b2l_api.cu", "b2l_hash.cu", "b2l_hash_k2.cu", "b2l_analyze.cu", "b2l_audit.cu", "b2l_ingest.cpp"]
+SOURCES = ["b2l_api.cu", "b2l_hash.cu", "b2l_hash_k2.cu", "b2l_analyze.cu", "b2l_audit.cu", "b2l_ingest.cpp",
+           "b2l_capture.cu"]
+OMPT_LIB = os.path.join(PKG, "libb2l_ompt.so")  # OMPT tool glue over libb2l's capture ABI
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -26,10 +28,11 @@ def _headers():
 
 
 def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(OMPT_LIB):
         return False
     t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(p) <= t for p in _sources() + _headers() + [__file__])
+    deps = _sources() + _headers() + [__file__, os.path.join(CSRC, "b2l_ompt.cpp")]
+    return all(os.path.getmtime(p) <= t for p in deps) and os.path.getmtime(OMPT_LIB) >= t
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -46,7 +49,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         sys.stderr.write(r.stderr)
     os.replace(LIB + ".tmp", LIB)
+    build_ompt()
     return LIB
+
+
+def build_ompt() -> str:
+    """libb2l_ompt.so: ompt_start_tool + the two EMI callbacks, linked against libb2l.so."""
+    src = os.path.join(CSRC, "b2l_ompt.cpp")
+    cuda = os.path.dirname(os.path.dirname(NVCC))
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-I", os.path.join(ROOT, "include"),
+           "-I", os.path.join(cuda, "include"), "-o", OMPT_LIB + ".tmp", src, "-L", PKG, "-lb2l",
+           "-L", os.path.join(cuda, "lib64"), "-lcudart", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("g++ failed building libb2l_ompt.so")
+    os.replace(OMPT_LIB + ".tmp", OMPT_LIB)
+    return OMPT_LIB
 
 
 if __name__ == "__main__":

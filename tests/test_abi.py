@@ -10,7 +10,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "b2l.h")).read()
     # function declarations: "<type> [*]b2l_name(" at the start of a line
-    return sorted(set(re.findall(r"^(?:int|void|const char \*)\s*\*?(b2l_[a-z0-9_]+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^(?:int|int32_t|void|const char \*|b2l_capture \*)\s*\*?(b2l_[a-z0-9_]+)\(", src, re.M)))
 
 
 def test_library_exports_header_symbols():
