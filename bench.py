@@ -415,6 +415,17 @@ def run_analysis_sharded(args, rank, world, local):
     dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=torch.device("cuda", local))
     dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     step_s = float(dt.item()) / steps
+    # the same pipeline up to per-rank findings (global indices, key-range distributed), i.e.
+    # without the gather + rank-0 merge into the reference's global orders
+    dist.barrier()
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    for _ in range(steps):
+        sharded.analyze_sharded_device(dshard, base, comm, gather=False)
+    torch.cuda.synchronize()
+    dl = torch.tensor([time.perf_counter() - t1], dtype=torch.float64, device=torch.device("cuda", local))
+    dist.all_reduce(dl, op=dist.ReduceOp.MAX)
+    dist_s = float(dl.item()) / steps
     out = {"metric": "M trace events/s analysed", "value": round(cols.n / step_s / 1e6, 3), "unit": "M events/s",
            "ms_per_step": round(step_s * 1e3, 3), "steps": steps,
            "config": {"workload": f"C2 trace of {cols.n} events ({args.n_events} per GPU), seq-range shards, "
@@ -422,7 +433,10 @@ def run_analysis_sharded(args, rank, world, local):
                                   f"routing, one NCCL all-to-all of event rows, engine per sub-trace, findings "
                                   f"gathered and merged on rank 0",
                       "events_total": cols.n},
-           "timing": "wall clock around analyze_sharded, max over ranks"}
+           "timing": "wall clock around analyze_sharded_device, max over ranks",
+           "distributed": {"value": round(cols.n / dist_s / 1e6, 3), "unit": "M events/s",
+                           "ms_per_step": round(dist_s * 1e3, 3),
+                           "note": "same pipeline, findings left on their key-range ranks (no gather / merge)"}}
     if rank == 0 and res is not None:
         out["counts"] = res.counts()
     return out

@@ -370,12 +370,13 @@ class _Phases:
             self.t = now
 
 
-def analyze_sharded_device(shard, base: int, comm, strict: bool = False) -> Optional[ColumnarFindings]:
+def analyze_sharded_device(shard, base: int, comm, strict: bool = False, gather: bool = True):
     """The sharded pipeline with every event-sized step on the device: ``shard`` is a
     DeviceColumns seq-range shard; validation, routing (b2l_shard_route), the all-to-all of
     the rows (NCCL on device memory), unpacking (b2l_shard_unpack) and both engine runs stay in
     HBM.  Only the findings (global indices and group sort keys) travel to rank 0 for the merge.
-    Same results and exceptions as ``analyze_sharded``."""
+    Same results and exceptions as ``analyze_sharded``.  ``gather=False`` stops before the gather:
+    every rank returns its own key range's findings (the per-rank parts, global indices)."""
     from .analysis import analyze_columns
     G = comm.size
     host = shard.host
@@ -454,6 +455,8 @@ def analyze_sharded_device(shard, base: int, comm, strict: bool = False) -> Opti
         out["ua"] = G_[pa[f.ua_pairs.astype(np.int64)]]
         out["ut"] = G_[f.ut_events.astype(np.int64)]
     ph.mark("engine")
+    if not gather:
+        return out
     parts = comm.gather0(out)
     ph.mark("gather")
     if comm.rank != 0:
