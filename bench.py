@@ -53,6 +53,9 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("B2L_BENCH_BACKEND") == "gloo":  # path check with ranks sharing GPUs (not a measurement)
+        import torch
+        local %= max(1, torch.cuda.device_count())
     return rank, world, local
 
 
@@ -269,15 +272,16 @@ def run_ours(args, rank, world, local):
     peak, peak_src = peaks()
     kern_ms = statistics.mean(launch_ms)
     achieved = total / (kern_ms / 1e3) / 1e9
-    traffic = ncu_traffic()
+    traffic = ncu_traffic() if n == N_BUFS else None  # the committed capture is of the default batch
     rec = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": "C2: 400,000 x 40,000 B buffers per GPU (16.0 GB), 25% duplicates, hashed with "
-                               "the reference FNV-1a/fmix64 fold",
+        "config": {"workload": f"C2: {n:,} x {BUF_BYTES:,} B buffers per GPU ({total / 1e9:.1f} GB), 25% "
+                               "duplicates, hashed with the reference FNV-1a/fmix64 fold",
                    "n_buffers_per_gpu": n, "buffer_bytes": BUF_BYTES, "bytes_per_gpu": total,
-                   "l2": "inputs (16 GB) larger than the 126 MB L2, no flush", "parallelism": f"shard{world}"},
+                   "l2": f"inputs ({total / 1e9:.1f} GB) larger than the 126 MB L2, no flush",
+                   "parallelism": f"shard{world}"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                      "kernel": "k_hash_coop<2,512,2> (b2l_hash_batch default variant)", "algorithmic_bytes_per_launch": total},
@@ -544,7 +548,10 @@ def main():
     import torch.distributed as dist
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("B2L_BENCH_BACKEND") == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     with ClockSampler(local) as clk:
         args._clock = clk
         rec = run_ours(args, rank, world, local)
