@@ -868,11 +868,12 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
             seg_fixup(ts.b, nt, 32, (uint8_t)(g_masks.dev | (live_range(nseg) << 4)), s);
             KeyCols<1> tk = ts.b.k[ts.b.cur];
             const uint32_t *tv = ts.val();
-            DBuf<uint32_t> gstart(nt, s), gcount(1, s);
-            compact(nt, HeadPred<1>{tk}, gstart.p, gcount.p, s);
+            // one scan: group id of every sorted trip and the first trip of every group
+            DBuf<uint32_t> gstart(nt + 1, s), gcount(1, s), trip_group(nt, s);
+            scan<SumU32>(nt, HeadLoad<1>{tk}, SegStartStore{trip_group.p, gstart.p, nt}, s, gcount.p);
             const uint32_t ng = read_u32(gcount.p, s);
             r.rt_groups = ng;
-            DBuf<uint32_t> first_ev(ng, s), gsize(ng, s), trip_group(nt, s);
+            DBuf<uint32_t> first_ev(ng, s), gsize(ng, s);
             DBuf<uint64_t> tie(ng, s);
             {
                 const uint32_t *gs = gstart.p;
@@ -889,10 +890,6 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
                     // reference order (hash, src, dst)
                     tk[g] = ((((key & 0xFFFFFFFFull) << dbits) | (key >> 32)) << dbits) | (uint64_t)(uint32_t)dst[e];
                 }, s);
-            }
-            {
-                uint32_t *tg = trip_group.p;
-                scan<SumU32>(nt, HeadLoad<1>{tk}, StoreInclMinus1{tg}, s);  // group id of every sorted trip
             }
             GroupOrder go = order_groups(ng, c.start, first_ev.p, s, tie.p, (uint64_t)nH << (2 * db));
             out.rt_off.alloc(ng + 1, s);

@@ -323,34 +323,128 @@ bool parse_event(const char *b, const char *e, uint64_t v[9], uint8_t &kind, Loc
 
 inline bool is_ws(char c) { return c == ' ' || c == '\t' || c == '\r' || c == '\v' || c == '\f'; }
 
+// ------------------------------------------------------------------ canonical-line fast path
+// The capture agents write one shape (model.ts:38-48 serializeEvent, b2l_capture.cu): the eleven
+// fields in wire order, no whitespace, plain integers, optionally ,"file":"...","line":N.  Such
+// a line is decoded with fixed literals and digit loops (no allocation); anything else -- other
+// key orders, whitespace, escapes, leading zeros, u64 overflow, unknown fields -- returns false
+// and the general scanner decides, so accepted lines give exactly the general parser's result.
+struct Fast {
+    const char *p, *e;
+    bool lit(const char *s, size_t n) {
+        if ((size_t)(e - p) < n || memcmp(p, s, n) != 0) return false;
+        p += n;
+        return true;
+    }
+    bool uint(uint64_t &v) {  // JSON non-negative integer without leading zeros, no overflow
+        if (p >= e || *p < '0' || *p > '9') return false;
+        if (*p == '0') {
+            ++p;
+            v = 0;
+            return p >= e || *p < '0' || *p > '9';
+        }
+        uint64_t x = 0;
+        int nd = 0;
+        while (p < e && *p >= '0' && *p <= '9') {
+            if (++nd > 19) return false;  // 20 digits may overflow: the general path checks
+            x = x * 10 + (uint64_t)(*p++ - '0');
+        }
+        if (p < e && (*p == '.' || *p == 'e' || *p == 'E')) return false;
+        v = x;
+        return true;
+    }
+};
+#define FLIT(s) f.lit(s, sizeof(s) - 1)
+bool parse_event_fast(const char *b, const char *e, uint64_t v[9], uint8_t &kind, uint64_t &codeptr,
+                      const char *&file, size_t &file_len, uint64_t &line) {
+    Fast f{b, e};
+    if (!FLIT("{\"seq\":") || !f.uint(v[0]) || !FLIT(",\"kind\":\"")) return false;
+    if (FLIT("transfer\"")) kind = B2L_KIND_TRANSFER;
+    else if (FLIT("alloc\"")) kind = B2L_KIND_ALLOC;
+    else if (FLIT("delete\"")) kind = B2L_KIND_DELETE;
+    else if (FLIT("kernel\"")) kind = B2L_KIND_KERNEL;
+    else return false;
+    if (!FLIT(",\"t0\":") || !f.uint(v[1]) || !FLIT(",\"t1\":") || !f.uint(v[2])) return false;
+    if (!FLIT(",\"src_dev\":") || !f.uint(v[3]) || !FLIT(",\"dst_dev\":") || !f.uint(v[4])) return false;
+    if (!FLIT(",\"src_addr\":") || !f.uint(v[5]) || !FLIT(",\"dst_addr\":") || !f.uint(v[6])) return false;
+    if (!FLIT(",\"bytes\":") || !f.uint(v[7]) || !FLIT(",\"hash\":") || !f.uint(v[8])) return false;
+    if (!FLIT(",\"codeptr\":") || !f.uint(codeptr)) return false;
+    file = nullptr, file_len = 0, line = 0;
+    if (f.p < f.e && *f.p == ',') {
+        if (!FLIT(",\"file\":\"")) return false;
+        const char *s0 = f.p;
+        while (f.p < f.e && *f.p != '"') {
+            const unsigned char ch = (unsigned char)*f.p;
+            if (ch < 0x20 || ch == '\\' || ch >= 0x80) return false;  // escapes / control / non-ASCII: general path
+            ++f.p;
+        }
+        if (f.p >= f.e) return false;
+        file = s0, file_len = (size_t)(f.p - s0);
+        ++f.p;
+        if (!FLIT(",\"line\":") || !f.uint(line) || line == 0 || line > (uint64_t)INT64_MAX) return false;
+    }
+    if (!FLIT("}") || f.p != f.e) return false;
+    return v[2] >= v[1];  // an inverted interval is the general path's (and the reference's) error
+}
+#undef FLIT
+
 void parse_range(const char *data, size_t lo, size_t hi, uint64_t first_line, Chunk &ck) {
     uint64_t line_no = first_line;
     size_t i = lo;
     uint64_t v[9];
+    static const bool use_fast = getenv("B2L_INGEST_GENERAL_ONLY") == nullptr;  // tests compare both paths
+    const size_t guess = (hi - lo) / 128 + 16;  // capture-agent lines are ~150-180 bytes
+    for (int k = 0; k < 9; ++k) ck.c[k].reserve(guess);
+    ck.kind.reserve(guess);
+    ck.loc.reserve(guess);
+    // location ids of codeptr-only locations (the common case): a small direct-mapped cache in
+    // front of the general table
+    constexpr int LC = 64;
+    uint64_t lc_key[LC];
+    uint32_t lc_id[LC];
+    bool lc_ok[LC] = {false};
+    auto loc_id = [&](const Loc &loc) {
+        auto it = ck.loc_ids.find(loc);
+        if (it != ck.loc_ids.end()) return it->second;
+        const uint32_t id = (uint32_t)ck.locs.size();
+        ck.loc_ids.emplace(loc, id);
+        ck.locs.push_back(loc);
+        return id;
+    };
     while (i < hi) {
-        size_t j = i;
-        while (j < hi && data[j] != '\n') ++j;
+        const char *nl = (const char *)memchr(data + i, '\n', hi - i);
+        const size_t j = nl ? (size_t)(nl - data) : hi;
         const char *b = data + i, *e = data + j;
         while (b < e && is_ws(*b)) ++b;
         while (e > b && is_ws(e[-1])) --e;
         if (b < e && *b != '#') {
             uint8_t kind = 0;
-            Loc loc{0, -1, false, std::string()};
-            if (!parse_event(b, e, v, kind, loc)) {
-                ck.err_line = line_no;
-                return;
+            uint64_t codeptr = 0, line = 0;
+            const char *file = nullptr;
+            size_t flen = 0;
+            uint32_t id;
+            if (use_fast && parse_event_fast(b, e, v, kind, codeptr, file, flen, line)) {
+                if (!file) {
+                    const int h = (int)((codeptr * 0x9E3779B97F4A7C15ull) >> 58);
+                    if (lc_ok[h] && lc_key[h] == codeptr) {
+                        id = lc_id[h];
+                    } else {
+                        id = loc_id(Loc{codeptr, -1, false, std::string()});
+                        lc_ok[h] = true, lc_key[h] = codeptr, lc_id[h] = id;
+                    }
+                } else {
+                    id = loc_id(Loc{codeptr, (int64_t)line, true, std::string(file, flen)});
+                }
+            } else {
+                Loc loc{0, -1, false, std::string()};
+                if (!parse_event(b, e, v, kind, loc)) {
+                    ck.err_line = line_no;
+                    return;
+                }
+                id = loc_id(loc);
             }
             for (int k = 0; k < 9; ++k) ck.c[k].push_back(v[k]);
             ck.kind.push_back(kind);
-            auto it = ck.loc_ids.find(loc);
-            uint32_t id;
-            if (it == ck.loc_ids.end()) {
-                id = (uint32_t)ck.locs.size();
-                ck.loc_ids.emplace(loc, id);
-                ck.locs.push_back(loc);
-            } else {
-                id = it->second;
-            }
             ck.loc.push_back(id);
         }
         i = j + 1;

@@ -103,6 +103,30 @@ def _copy(ptr, n, dtype):
     return np.frombuffer(buf, dtype=dtype).copy()
 
 
+class _IngestHandle:
+    """Owns a b2l_ingest* until the last column view over its arrays is gone."""
+
+    def __init__(self, L, ptr):
+        self.L, self.ptr = L, ptr
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                self.L.b2l_ingest_free(self.ptr)
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+        self.ptr = None
+
+
+def _view(ptr, n, dtype, owner):
+    """Zero-copy numpy view of parser-owned memory that keeps `owner` alive."""
+    if not n or not ptr:
+        return np.zeros(0, dtype=dtype)
+    buf = (ctypes.c_char * (int(n) * np.dtype(dtype).itemsize)).from_address(ptr)
+    buf._owner = owner
+    return np.frombuffer(buf, dtype=dtype)
+
+
 def _native(raw: bytes, threads: int):
     L = _lib.lib()
     L.b2l_ingest_ndjson.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int,
@@ -111,15 +135,16 @@ def _native(raw: bytes, threads: int):
     L.b2l_ingest_free.argtypes = [ctypes.POINTER(_Ingest)]
     out = ctypes.POINTER(_Ingest)()
     _lib.check(L.b2l_ingest_ndjson(raw, len(raw), threads, ctypes.byref(out)), "b2l_ingest_ndjson")
-    try:
+    handle = _IngestHandle(L, out)  # the event columns below are views over the parser's arrays
+    if True:
         g = out.contents
         if g.err_line:
             return None
         n = int(g.n_events)
-        cols = {f: _copy(getattr(g, f), n, np.uint64) for f in
+        cols = {f: _view(getattr(g, f), n, np.uint64, handle) for f in
                 ("seq", "start_ns", "end_ns", "src_device", "dst_device", "src_addr", "dst_addr", "bytes", "hash")}
-        cols["kind"] = _copy(g.kind, n, np.uint8)
-        cols["loc"] = _copy(g.loc, n, np.uint32)
+        cols["kind"] = _view(g.kind, n, np.uint8, handle)
+        cols["loc"] = _view(g.loc, n, np.uint32, handle)
         nl = int(g.n_locs)
         cp = _copy(g.loc_codeptr, nl, np.uint64)
         ln = _copy(g.loc_line, nl, np.int64)
@@ -136,8 +161,6 @@ def _native(raw: bytes, threads: int):
         header = (int(g.version), int(g.num_devices), int(g.host_device),
                   int(g.wall_time_ns) if g.has_wall else None)
         return header, cols, locs
-    finally:
-        L.b2l_ingest_free(out)
 
 
 def _sort_perm(t0: np.ndarray, seq: np.ndarray) -> Optional[np.ndarray]:
@@ -213,7 +236,7 @@ def _validate_columns(c: Columns, types):
 def parse_trace_columns(data, threads: Optional[int] = None, types=None) -> Columns:
     """Parse + sort + validate into device-ready columns (no per-event Python objects)."""
     raw, text = _as_bytes(data)
-    if text is None:
+    if text is None and not raw.isascii():
         text = raw.decode("utf-8")  # the reference decodes first (UnicodeDecodeError as it does)
     threads = threads or min(32, os.cpu_count() or 1)
     got = _native(raw, threads)
@@ -221,7 +244,7 @@ def parse_trace_columns(data, threads: Optional[int] = None, types=None) -> Colu
     if not header_ok or got is None or (got[1]["src_device"].size and (
             got[1]["src_device"].max() > I32_MAX or got[1]["dst_device"].max() > I32_MAX)):
         from .columns import to_columns
-        return to_columns(_parse_exact(text, types))
+        return to_columns(_parse_exact(text if text is not None else raw.decode("utf-8"), types))
     c = _to_columns(*got)
     viol = _validate_columns(c, types)
     if viol:

@@ -81,3 +81,51 @@ def test_parse_trace_drop_in_matches_reference(cuda):
             assert (got.num_devices_total, got.host_device) == (want.num_devices_total, want.host_device)
             cols = ingest.parse_trace_columns(c["text"])
             assert [int(x) for x in cols.seq] == [e.seq for e in want.events], c["name"]
+
+
+def test_canonical_fast_path_equals_general_scanner():
+    """Lines in the capture agents' canonical shape take the allocation-free fast path; every
+    edge around it (20-digit / leading-zero numbers, escapes, non-ASCII files, reordered keys,
+    whitespace, inverted intervals) must give exactly what the general scanner gives."""
+    import subprocess
+    import sys
+    head = '{"dmlens":1,"num_devices":3,"host_device":0}'
+    ev = ('{"seq":%s,"kind":"%s","t0":%s,"t1":%s,"src_dev":1,"dst_dev":2,"src_addr":0,"dst_addr":%s,'
+          '"bytes":%s,"hash":%s,"codeptr":%s%s}')
+    rows = [ev % (i, k, t0, t1, da, nb, h, cp, extra) for i, (k, t0, t1, da, nb, h, cp, extra) in enumerate([
+        ("kernel", 0, 0, 0, 0, 0, 0, ""),
+        ("transfer", 5, 9, 7, 12, 18446744073709551615, 1, ""),          # 20-digit hash: general path
+        ("alloc", 10, 10, 4096, 8, 0, 99999999999999999, ',"file":"a.c","line":3'),
+        ("delete", 11, 12, 4096, 0, 0, 7, ',"file":"dir/x y.c","line":9223372036854775807'),
+        ("transfer", 13, 14, 1, 2, 3, 4, ',"file":"\\u00e9.c","line":1'),  # escape: general path
+        ("transfer", 15, 16, 1, 2, 3, 4, ',"file":"café.c","line":2'),  # non-ASCII: general path
+        ("kernel", 17, 18, 0, 0, 0, 10, ""),
+    ])]
+    rows.append('{"kind":"kernel","seq":7,"t0":19,"t1":20,"src_dev":1,"dst_dev":1,"src_addr":0,"dst_addr":0,'
+                '"bytes":0,"hash":0,"codeptr":1}')                       # reordered keys
+    rows.append('{"seq":8, "kind":"kernel","t0":21,"t1":22,"src_dev":1,"dst_dev":1,"src_addr":0,"dst_addr":0,'
+                '"bytes":0,"hash":0,"codeptr":1}')                       # whitespace
+    good = "\n".join([head] + rows) + "\n"
+    bad_variants = [
+        good.replace('"seq":0,', '"seq":00,'),                           # leading zero: invalid JSON
+        good.replace('"t0":17,"t1":18', '"t0":18,"t1":17'),               # inverted interval
+        good.replace('"codeptr":10}', '"codeptr":10,"line":0}'),          # line 0
+        good.replace('"hash":3,', '"hash":3.0,'),                          # float
+    ]
+    code = ("import sys, json, pickle; sys.path.insert(0, %r); from paper_2601_12713_b200 import ingest; "
+            "inp = pickle.loads(sys.stdin.buffer.read()); out = []\n"
+            "for t in inp:\n"
+            "    r = ingest._native(t.encode(), threads=2)\n"
+            "    out.append(None if r is None else (r[0], {k: v.tolist() for k, v in r[1].items()}, r[2]))\n"
+            "sys.stdout.buffer.write(pickle.dumps(out))") % os.path.dirname(HERE)
+    import pickle
+    inputs = pickle.dumps([good] + bad_variants)
+    res = {}
+    for general in (False, True):
+        env = dict(os.environ)
+        if general:
+            env["B2L_INGEST_GENERAL_ONLY"] = "1"
+        p = subprocess.run([sys.executable, "-c", code], input=inputs, capture_output=True, env=env, check=True)
+        res[general] = pickle.loads(p.stdout)
+    assert res[False] == res[True]
+    assert res[False][0] is not None and all(r is None for r in res[False][1:])
