@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--n-bufs", type=int, default=N_BUFS)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-large", action="store_true", help="skip the 10M-event analysis lines")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--n-events", type=int, default=N_EVENTS)
     ap.add_argument("--no-analysis", action="store_true")
@@ -390,7 +391,38 @@ def run_analysis_ours(args, rank, world, local):
         out["cpu_baseline"] = {"value": round(cols.n / cpu_dt / 1e6, 4), "unit": "M events/s", "cores": 1,
                                "kind": "port", "sample": f"the full {cols.n}-event C2 trace through "
                                                          f"oracle/analysis_ref.analyze_cols (1 thread)"}
+    if not args.no_large:
+        out["larger_traces"] = [_analysis_at(c2_trace, n, dev) for n in (10_000_000,)] + \
+            [_analysis_at(_c4, 10_000_000, dev)]
     return out
+
+
+def _c4(n, seed=4):
+    from paper_2601_12713_b200.synth import c4_trace
+    return c4_trace(n, seed=seed)
+
+
+def _analysis_at(gen, n, dev, iters=8):
+    """The same device-resident step on a larger trace (throughput rather than launch latency)."""
+    import statistics
+
+    import torch
+
+    from paper_2601_12713_b200.analysis import DeviceColumns, analyze_columns, savings_columns
+    cols = gen(n, seed=SEED + 10)
+    d = DeviceColumns(cols, dev)
+    times = []
+    for _ in range(iters):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        savings_columns(d, analyze_columns(d))
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t)
+    step = statistics.median(times[iters // 2:])
+    name = "C4" if gen is _c4 else "C2"
+    return {"workload": f"{name} trace, {cols.n} events, columns resident in HBM", "value": round(cols.n / step / 1e6, 1),
+            "unit": "M events/s", "ms_per_step": round(step * 1e3, 3),
+            "timing": f"median of the last {iters - iters // 2} of {iters} steps"}
 
 
 def run_analysis_sharded(args, rank, world, local):
