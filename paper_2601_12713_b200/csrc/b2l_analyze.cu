@@ -1836,6 +1836,37 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     }
     PhaseClock pc(s);
     pc.mark("sv-setup");
+    // ---- attribution
+    const uint32_t nb = c.nbuckets;
+    DBuf<unsigned long long> at(5 * (size_t)nb * 6 + 1, s);
+    at.zero();
+    CK(cudaMemsetAsync(at.p + 5 * (size_t)nb * 5, 0xFF, 5 * (size_t)nb * sizeof(unsigned long long), s));
+    // the attribution kernels read only the findings: run them on a side stream beside the
+    // category bits, sums and the overlap/union scan
+    cudaStream_t sa = engine_stream_n(1);
+    {
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev, s));
+        CK(cudaStreamWaitEvent(sa, ev, 0));
+        CK(cudaEventDestroy(ev));
+    }
+    const size_t smem = nb <= 512 ? (size_t)nb * 6 * sizeof(unsigned long long) : 0;
+    auto acc_of = [&](int cat_i) {
+        unsigned long long *base = at.p;
+        return AttrAcc{base + (size_t)cat_i * nb, base + 5 * (size_t)nb + (size_t)cat_i * 2 * nb,
+                       base + 15 * (size_t)nb + (size_t)cat_i * 2 * nb, base + 25 * (size_t)nb + (size_t)cat_i * nb};
+    };
+    auto launch = [&](auto el, size_t ne, int cat_i) {
+        if (!ne || !nb) return;
+        k_attr<<<grid_for(ne, TPB, 148 * 8), TPB, smem, sa>>>(c, ne, el, acc_of(cat_i));
+        CK_LAUNCH("k_attr");
+    };
+    launch(ElemList{F.dd_mem}, F.dd_members, 0);
+    launch(ElemTrips{F.rt_tx, F.rt_rx}, F.rt_trips, 1);
+    launch(ElemPairs{F.ra_mem, F.pa, F.pd}, F.ra_members, 2);
+    launch(ElemPairs{F.ua, F.pa, F.pd}, F.n_ua, 3);
+    launch(ElemList{F.ut}, F.n_ut, 4);
     // ---- category bits per event
     DBuf<uint8_t> cat(((n ? n : 1) + 3) & ~size_t(3), s);  // whole words: byte atomics touch the word
     cat.zero();
@@ -1901,27 +1932,14 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     if (n) CK(cudaMemcpyAsync(unic.p, &ovt.p->cnt, 4, cudaMemcpyDeviceToDevice, s));
     else unic.zero();
     pc.mark("sv-sums");
-    // ---- attribution
-    const uint32_t nb = c.nbuckets;
-    DBuf<unsigned long long> at(5 * (size_t)nb * 6 + 1, s);
-    at.zero();
-    CK(cudaMemsetAsync(at.p + 5 * (size_t)nb * 5, 0xFF, 5 * (size_t)nb * sizeof(unsigned long long), s));
-    const size_t smem = nb <= 512 ? (size_t)nb * 6 * sizeof(unsigned long long) : 0;
-    auto acc_of = [&](int cat_i) {
-        unsigned long long *base = at.p;
-        return AttrAcc{base + (size_t)cat_i * nb, base + 5 * (size_t)nb + (size_t)cat_i * 2 * nb,
-                       base + 15 * (size_t)nb + (size_t)cat_i * 2 * nb, base + 25 * (size_t)nb + (size_t)cat_i * nb};
-    };
-    auto launch = [&](auto el, size_t ne, int cat_i) {
-        if (!ne || !nb) return;
-        k_attr<<<grid_for(ne, TPB, 148 * 8), TPB, smem, s>>>(c, ne, el, acc_of(cat_i));
-        CK_LAUNCH("k_attr");
-    };
-    launch(ElemList{F.dd_mem}, F.dd_members, 0);
-    launch(ElemTrips{F.rt_tx, F.rt_rx}, F.rt_trips, 1);
-    launch(ElemPairs{F.ra_mem, F.pa, F.pd}, F.ra_members, 2);
-    launch(ElemPairs{F.ua, F.pa, F.pd}, F.n_ua, 3);
-    launch(ElemList{F.ut}, F.n_ut, 4);
+    // attribution (on the side stream) has finished before anything is read back
+    {
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev, sa));
+        CK(cudaStreamWaitEvent(s, ev, 0));
+        CK(cudaEventDestroy(ev));
+    }
     pc.mark("sv-attr");
     // ---- to host
     unsigned long long h[15];
