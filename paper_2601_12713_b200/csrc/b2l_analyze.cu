@@ -1918,8 +1918,19 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
         unsigned long long init[2] = {~0ull, 0ull};
         CK(cudaMemcpyAsync(acc.p + 13, init, sizeof(init), cudaMemcpyHostToDevice, s));
     }
+    // the 128-bit sums and the overlap / union scan both only read the category bits: the sums go
+    // to a second side stream
+    cudaStream_t sb = engine_stream_n(2);
+    auto join_streams = [](cudaStream_t from, cudaStream_t to) {
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev, from));
+        CK(cudaStreamWaitEvent(to, ev, 0));
+        CK(cudaEventDestroy(ev));
+    };
+    join_streams(s, sb);
     if (n) {
-        k_sums<<<grid_for(n, TPB, 148 * 8), TPB, 0, s>>>(c, cat.p, acc.p, acc.p + 12, acc.p + 13);
+        k_sums<<<grid_for(n, TPB, 148 * 8), TPB, 0, sb>>>(c, cat.p, acc.p, acc.p + 12, acc.p + 13);
         CK_LAUNCH("k_sums");
     }
     // overlap: exists i >= 1 with start[i] < max(end[0..i-1])  (estimator.py:51-58)
@@ -1931,6 +1942,7 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     scan<OvUn>(n, OvUnLoad{c.end, ct}, OvUnStore{c.start, ct, ovl.p, uni.p}, s, ovt.p);
     if (n) CK(cudaMemcpyAsync(unic.p, &ovt.p->cnt, 4, cudaMemcpyDeviceToDevice, s));
     else unic.zero();
+    join_streams(sb, s);
     pc.mark("sv-sums");
     // attribution (on the side stream) has finished before anything is read back
     {
