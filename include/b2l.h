@@ -118,6 +118,8 @@ void b2l_ingest_free(b2l_ingest *p);
 /* Stable sort of n (k0, k1) u64 key pairs (host arrays): out_perm = sorting permutation
  * (parse_trace's events.sort(key=(start_ns, seq)), traceio.py:183). */
 int b2l_sort_u64_pairs(const uint64_t *k0, const uint64_t *k1, uint64_t n, uint32_t *out_perm);
+/* The same with DEVICE arrays (synchronous): the group orders of the multi-GPU merge on rank 0. */
+int b2l_sort_u64_pairs_device(const uint64_t *d_k0, const uint64_t *d_k1, uint64_t n, uint32_t *d_perm);
 
 /* Kernel variant selection (tuning / tests): variant -1 only reports the
  * number of variants in *count, -2 restores the default (the tuned variant,

@@ -2088,6 +2088,18 @@ __global__ void k_max_data_end(DevCols c, unsigned long long *out) {  // max end
     }
     if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
+// OR and AND of two u64 columns (warp-reduced, one atomic per warp and value).
+__global__ void k_or_and2(const uint64_t *__restrict__ a, const uint64_t *__restrict__ b, size_t n,
+                          unsigned long long *m /*[or a, or b, and a, and b]*/) {
+    unsigned long long oa = 0, ob = 0, aa = ~0ull, ab = ~0ull;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        oa |= a[i], ob |= b[i], aa &= a[i], ab &= b[i];
+    for (int o = 16; o; o >>= 1) {
+        oa |= __shfl_xor_sync(0xffffffffu, oa, o), ob |= __shfl_xor_sync(0xffffffffu, ob, o);
+        aa &= __shfl_xor_sync(0xffffffffu, aa, o), ab &= __shfl_xor_sync(0xffffffffu, ab, o);
+    }
+    if ((threadIdx.x & 31) == 0) atomicOr(m, oa), atomicOr(m + 1, ob), atomicAnd(m + 2, aa), atomicAnd(m + 3, ab);
+}
 __global__ void k_route_counts(const uint64_t *__restrict__ key, uint64_t n, uint32_t G, unsigned long long *cnt) {
     __shared__ unsigned long long sc[256];
     for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) sc[g] = 0;
@@ -2263,6 +2275,35 @@ int b2l_stable_sort_u64(const uint64_t *keys, uint64_t n, uint32_t strategy, uin
         else if (strategy == 1) radix_sort_wide(st.b, n, live, s);
         else radix_sort_prefix(st.b, n, live, (int)strategy - 16, s);
         read_back(out_perm, st.val(), n * sizeof(uint32_t), s);
+        return B2L_OK;
+    } catch (const b2l::EngineErr &e) {
+        return b2l::fail(e.code, e.msg);
+    }
+}
+
+int b2l_sort_u64_pairs_device(const uint64_t *d_k0, const uint64_t *d_k1, uint64_t n, uint32_t *d_perm) {
+    if (n && (!d_k0 || !d_k1 || !d_perm)) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
+    if (n == 0) return B2L_OK;
+    try {
+        using namespace b2l;
+        std::lock_guard<std::mutex> lock(ana::g_mu);
+        cudaStream_t s = ana::engine_stream();
+        CK(cudaStreamSynchronize(cudaStreamLegacy));  // inputs written on the caller's stream
+        SortStore<2> st(n, s);
+        CK(cudaMemcpyAsync(st.in_key(0), d_k0, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(st.in_key(1), d_k1, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+        uint32_t *v = st.in_val();
+        ana::for_each(n, [=] __device__(size_t i) { v[i] = (uint32_t)i; }, s);
+        DBuf<unsigned long long> m(4, s);
+        CK(cudaMemsetAsync(m.p, 0, 2 * sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(m.p + 2, 0xFF, 2 * sizeof(unsigned long long), s));
+        b2l::ana::k_or_and2<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(d_k0, d_k1, n, m.p);  // live digit bytes
+        CK_LAUNCH("k_or_and2");
+        unsigned long long hm[4];
+        read_back(hm, m.p, sizeof(hm), s);
+        radix_sort<2>(st.b, n, LiveBytes<2>{{live_mask(hm[0] ^ hm[2]), live_mask(hm[1] ^ hm[3])}}, s);
+        CK(cudaMemcpyAsync(d_perm, st.val(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        CK(cudaStreamSynchronize(s));
         return B2L_OK;
     } catch (const b2l::EngineErr &e) {
         return b2l::fail(e.code, e.msg);

@@ -461,7 +461,7 @@ def analyze_sharded_device(shard, base: int, comm, strict: bool = False, gather:
     ph.mark("gather")
     if comm.rank != 0:
         return None
-    res = _merge(parts, synth_end, total_events=None, lexsort=runs_lexsort)
+    res = _merge_dev(parts, synth_end, shard.t["seq"].device)
     ph.mark("merge")
     return res
 
@@ -550,6 +550,98 @@ def _merge(parts, synth_end, total_events=None, lexsort=_np_lexsort) -> Columnar
         n_events=total_events or 0, dd_offsets=dd_off.astype(np.uint64), dd_members=u32(dd_mem),
         rt_offsets=rt_off.astype(np.uint64), rt_tx=u32(rt_tx), rt_rx=u32(rt_rx), pair_alloc=u32(pa),
         pair_delete=np.where(pdl < 0, SYN, pdl).astype(np.uint32), synthetic_end_ns=int(synth_end),
+        warn_index=u32(warn), ra_offsets=ra_off.astype(np.uint64), ra_pairs=u32(ra_pairs), ua_pairs=u32(ua),
+        ut_events=u32(ut))
+
+
+# ------------------------------------------------------------------------ merge on the device
+def _dev_lexsort(kcols, dev):
+    """Order of u64 key columns (first = primary) as LSD passes of the engine's stable pair
+    sort on device arrays (b2l_sort_u64_pairs_device): (k[-2], k[-1]) first, then (k[-4], k[-3])."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    L = _lib.lib()
+    L.b2l_sort_u64_pairs_device.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
+    n = kcols[0].numel()
+    order = torch.arange(n, dtype=torch.int64, device=dev)
+    if n < 2:
+        return order
+    cols = list(kcols)
+    if len(cols) % 2:
+        cols = [torch.zeros(n, dtype=torch.int64, device=dev)] + cols
+    perm = torch.empty(n, dtype=torch.int32, device=dev)
+    for j in range(len(cols) - 2, -1, -2):
+        a = cols[j][order].contiguous()
+        b = cols[j + 1][order].contiguous()
+        torch.cuda.synchronize(dev)
+        _lib.check(L.b2l_sort_u64_pairs_device(a.data_ptr(), b.data_ptr(), n, perm.data_ptr()),
+                   "b2l_sort_u64_pairs_device")
+        order = order[perm.long()]
+    return order
+
+
+def _dev(a, dev):
+    import torch
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint64:
+        a = a.view(np.int64)
+    return torch.from_numpy(a.astype(np.int64, copy=False)).to(dev, non_blocking=False)
+
+
+def _merge_groups_dev(parts, key, member_cols, sort_cols, dev):
+    """_merge_groups with the concatenated groups on the device: one engine sort for the order,
+    the member ranges gathered with a repeat/arange index."""
+    import torch
+    offs = [np.asarray(p[key][0], np.int64) for p in parts if key in p]
+    if not offs or sum(o.size - 1 for o in offs) == 0:
+        return np.zeros(1, np.uint64), [np.zeros(0, np.int64) for _ in member_cols]
+    sizes = np.concatenate([np.diff(o) for o in offs])
+    base = np.cumsum([0] + [int(o[-1]) for o in offs[:-1]])
+    starts = np.concatenate([o[:-1] + b for o, b in zip(offs, base)])
+    keys = [_dev(np.concatenate([np.asarray(p[key][c]).astype(np.int64) for p in parts if key in p]), dev)
+            for c in sort_cols]
+    order = _dev_lexsort(keys, dev)
+    sz, st = _dev(sizes, dev)[order], _dev(starts, dev)[order]
+    first = torch.cumsum(sz, 0) - sz
+    total = int(sizes.sum())
+    idx = torch.repeat_interleave(st - first, sz, output_size=total) + torch.arange(total, device=dev)
+    new_off = np.zeros(sizes.size + 1, np.uint64)
+    new_off[1:] = np.cumsum(sz.cpu().numpy())
+    flat = [_dev(np.concatenate([np.asarray(p[key][c]) for p in parts if key in p]), dev)[idx].cpu().numpy()
+            for c in member_cols]
+    return new_off, flat
+
+
+def _merge_dev(parts, synth_end, dev) -> ColumnarFindings:
+    """_merge on rank 0's GPU: group orders by the engine's radix sort, index work as device
+    gathers; same results as the host merge."""
+    import torch
+    dd_off, (dd_mem,) = _merge_groups_dev(parts, "dd", [1], [2, 3, 4], dev)
+    rt_off, (rt_tx, rt_rx) = _merge_groups_dev(parts, "rt", [1, 2], [3, 4, 5, 6], dev)
+    pa_h = _cat(parts, "pairs", 0, np.int64)
+    pa = _dev(pa_h, dev)
+    pdl = _dev(_cat(parts, "pairs", 1, np.int64), dev)
+    o = _dev_lexsort([pa], dev)
+    pa, pdl = pa[o], pdl[o]
+    ra_off, (ra_alloc,) = _merge_groups_dev(parts, "ra", [1], [2, 3, 4, 5], dev)
+    pos = torch.zeros(int(pa_h.max()) + 1 if pa_h.size else 1, dtype=torch.int64, device=dev)
+    pos[pa] = torch.arange(pa.numel(), dtype=torch.int64, device=dev)
+    ra_pairs = pos[_dev(ra_alloc, dev)].cpu().numpy()
+    ua_l = [p["ua"] for p in parts if "ua" in p]
+    ua = np.sort(pos[_dev(np.concatenate(ua_l), dev)].cpu().numpy()) if ua_l else np.zeros(0, np.int64)
+    ut_l = [p["ut"] for p in parts if "ut" in p]
+    ut = np.sort(np.concatenate(ut_l)) if ut_l else np.zeros(0, np.int64)
+    w_l = [p["warn"] for p in parts if "warn" in p]
+    warn = np.sort(np.concatenate(w_l)) if w_l else np.zeros(0, np.int64)
+    pa_n, pdl_n = pa.cpu().numpy(), pdl.cpu().numpy()
+    u32 = lambda a: np.asarray(a).astype(np.uint32)  # noqa: E731
+    return ColumnarFindings(
+        n_events=0, dd_offsets=dd_off.astype(np.uint64), dd_members=u32(dd_mem),
+        rt_offsets=rt_off.astype(np.uint64), rt_tx=u32(rt_tx), rt_rx=u32(rt_rx), pair_alloc=u32(pa_n),
+        pair_delete=np.where(pdl_n < 0, SYN, pdl_n).astype(np.uint32), synthetic_end_ns=int(synth_end),
         warn_index=u32(warn), ra_offsets=ra_off.astype(np.uint64), ra_pairs=u32(ra_pairs), ua_pairs=u32(ua),
         ut_events=u32(ut))
 
