@@ -291,6 +291,61 @@ __global__ void __launch_bounds__(WARPS * 32) k_hash_coop(const uint64_t *__rest
 
 // Launch configurations (lanes per CTA, chunk bytes, ring depth).  Selected at
 // first use; B2L_HASH_CFG=<i> overrides (used by the tuning sweep).
+// ============================================================================ variant W
+// One WARP per buffer, for batches too small to fill the GPU with lanes (C1): all 32 lanes
+// stream the buffer's next 512-B chunk with one coalesced 16-B cp.async each (one instruction
+// per chunk instead of 32 shuffled ones), an S-deep ring per warp, and lane 0 runs the serial
+// chain out of shared memory.  A lone chain is then bound by its own dependency latency, not by
+// the cooperative ring's per-round issue cost (the longest C1 buffer sets the batch time).
+template <int WARPS, int S>
+__global__ void __launch_bounds__(WARPS * 32) k_hash_warp(const uint64_t *__restrict__ ptrs,
+                                                          const uint64_t *__restrict__ lens,
+                                                          const uint32_t *__restrict__ order, uint64_t n_bufs,
+                                                          uint64_t *__restrict__ digests) {
+    constexpr int CH = 512;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t *ring = smem + (size_t)warp * S * CH;
+    const uint32_t ring_s = smem_u32(ring);
+    const uint64_t stride = (uint64_t)gridDim.x * WARPS;
+    for (uint64_t k = (uint64_t)blockIdx.x * WARPS + warp; k < n_bufs; k += stride) {
+        BufCursor ld, cs;
+        cursor_load(ld, ptrs, lens, order, k, n_bufs);
+        cs = ld;
+        if (cs.L == 0) {
+            if (lane == 0) digests[cs.idx] = 0;
+            continue;
+        }
+        auto issue = [&](int st) {
+            if (ld.pos < ld.L) {
+                const uint32_t b = chunk_bytes(ld, CH);
+                if ((uint32_t)(16 * lane) < b) cp_async16(ring_s + (uint32_t)(st * CH + 16 * lane), ld.a0 + ld.pos + 16 * lane);
+                ld.pos += b;
+            }
+            cp_async_commit();
+        };
+#pragma unroll
+        for (int st = 0; st < S - 1; ++st) issue(st);
+        uint64_t h = FNV_OFFSET, prev = 0;
+        int st = 0;
+        while (cs.pos < cs.L) {
+            cp_async_wait<S - 2>();
+            __syncwarp();
+            issue(st == 0 ? S - 1 : st - 1);
+            const uint32_t bytes = chunk_bytes(cs, CH);
+            if (lane == 0) consume_chunk<CH>(cs, bytes, reinterpret_cast<const uint4 *>(ring + st * CH), h, prev);
+            cs.pos += bytes;
+            st = st + 1 == S ? 0 : st + 1;
+            __syncwarp();  // the slot is re-filled only after lane 0 has read it
+        }
+        cp_async_wait<0>();
+        __syncwarp();
+        if (lane == 0) digests[cs.idx] = finish_digest(h, cs.n);
+    }
+}
+constexpr int WARP_K_WARPS = 4, WARP_K_STAGES = 8;
+constexpr size_t WARP_K_SMEM = (size_t)WARP_K_WARPS * WARP_K_STAGES * 512;
+
 struct HashCfg {
     int nt, ch, s;
     size_t smem;
@@ -318,6 +373,7 @@ const HashCfg *cfg_table(int &count) {
 constexpr int DEFAULT_CFG = 6;  // coop<2 warps, 512 B, 2 stages>: 96.5% of measured HBM on C2 (r01 sweep)
 constexpr int LATENCY_CFG = 11;   // coop<1 warp, 512 B, 6 stages>: batches too small to fill the GPU
 constexpr uint64_t LATENCY_MAX_BUFS = 148ull * 2 * 32;  // one lane per buffer fits the deep variant
+constexpr uint64_t WARP_MAX_BUFS = 148ull * 32;          // one warp per buffer, all resident at once
 
 struct HashLaunch {
     int cfg = -1;
@@ -404,6 +460,14 @@ int hash_batch_launch(const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n
     int per_sm = 0;
     const HashCfg *c = active_cfg(per_sm);
     if (!c) return fail(B2L_E_CUDA, "b2l_hash_batch: cannot configure hash kernel");
+    if (setenv_variant < 0 && !getenv("B2L_HASH_CFG") && n <= WARP_MAX_BUFS) {
+        // few buffers: one warp each (every buffer's chain runs at its own latency)
+        auto fn = k_hash_warp<WARP_K_WARPS, WARP_K_STAGES>;
+        const unsigned grid = (unsigned)((n + WARP_K_WARPS - 1) / WARP_K_WARPS);
+        fn<<<grid, WARP_K_WARPS * 32, WARP_K_SMEM, stream>>>(d_ptrs, d_lens, d_order, n, d_digests);
+        B2L_CHECK_LAUNCH("k_hash_warp");
+        return B2L_OK;
+    }
     if (setenv_variant < 0 && !getenv("B2L_HASH_CFG") && n <= LATENCY_MAX_BUFS) {
         // few buffers: every chain runs alone, so what matters is bytes in flight per lane
         int count;
