@@ -91,47 +91,66 @@ def loc_key(codeptr, file, line):
     return (1, "", codeptr)
 
 
+_KIND_CODE = {"transfer": 0, "alloc": 1, "delete": 2, "kernel": 3}
+_EV_FIELDS = U64_FIELDS + ("src_device", "dst_device", "kind", "loc")
+
+
 def to_columns(trace) -> Columns:
-    """Convert a Trace (ours or dmlens's) into device-ready columns."""
+    """Convert a Trace (ours or dmlens's) into device-ready columns: one C-level attribute
+    sweep per field (operator.attrgetter), locations deduplicated per distinct location object
+    first (events usually share them)."""
+    from operator import attrgetter
     ev = trace.events
     n = len(ev)
+    cols_t = [list(map(attrgetter(f), ev)) for f in _EV_FIELDS]
     cols = {}
     try:
-        for f in U64_FIELDS:
-            cols[f] = _u64([getattr(e, f) for e in ev], n)
-        src = _i32([e.src_device for e in ev], n)
-        dst = _i32([e.dst_device for e in ev], n)
+        for k, f in enumerate(U64_FIELDS):
+            cols[f] = _u64(cols_t[k], n)
+        src = _i32(cols_t[len(U64_FIELDS)], n)
+        dst = _i32(cols_t[len(U64_FIELDS) + 1], n)
     except OverflowError as exc:
         raise Unrepresentable(str(exc)) from exc
-    kind = np.fromiter((_kind_code(e.kind) for e in ev), dtype=np.uint8, count=n)
-    # location table: dedupe on (codeptr, file, line)
+    kind_of = {}
+    for kd in set(cols_t[len(U64_FIELDS) + 2]):
+        kind_of[kd] = _KIND_CODE[getattr(kd, "value", kd)]
+    kind = np.fromiter(map(kind_of.__getitem__, cols_t[len(U64_FIELDS) + 2]), dtype=np.uint8, count=n)
+    # location table: dedupe on (codeptr, file, line); distinct location objects first
     loc_ids: dict = {}
-    loc_arr = np.empty(n, dtype=np.uint32)
+    obj_ids: dict = {}
     flags, bucket_of, locs = [], [], []
     bucket_ids: dict = {}
     bucket_keys = []
-    for i, e in enumerate(ev):
-        loc = e.loc
-        k = (loc.codeptr, loc.file, loc.line)
-        lid = loc_ids.get(k)
+    get_loc = attrgetter("codeptr", "file", "line")
+    loc_objs = cols_t[len(U64_FIELDS) + 3]
+    ids = []
+    for loc in loc_objs:
+        oid = id(loc)
+        lid = obj_ids.get(oid)
         if lid is None:
-            lid = len(flags)
-            loc_ids[k] = lid
-            locs.append(k)
-            fl = 0
-            if loc.file is not None and loc.line is None:
-                fl |= LOC_FILE_NO_LINE
-            if loc.line is not None and loc.line <= 0:
-                fl |= LOC_LINE_NONPOS
-            flags.append(fl)
-            bk = loc_key(loc.codeptr, loc.file, loc.line)
-            b = bucket_ids.get(bk)
-            if b is None:
-                b = len(bucket_keys)
-                bucket_ids[bk] = b
-                bucket_keys.append(bk)
-            bucket_of.append(b)
-        loc_arr[i] = lid
+            k = get_loc(loc)
+            lid = loc_ids.get(k)
+            if lid is None:
+                lid = len(flags)
+                loc_ids[k] = lid
+                locs.append(k)
+                cp, f, ln = k
+                fl = 0
+                if f is not None and ln is None:
+                    fl |= LOC_FILE_NO_LINE
+                if ln is not None and ln <= 0:
+                    fl |= LOC_LINE_NONPOS
+                flags.append(fl)
+                bk = loc_key(cp, f, ln)
+                bb = bucket_ids.get(bk)
+                if bb is None:
+                    bb = len(bucket_keys)
+                    bucket_ids[bk] = bb
+                    bucket_keys.append(bk)
+                bucket_of.append(bb)
+            obj_ids[oid] = lid
+        ids.append(lid)
+    loc_arr = np.array(ids, dtype=np.uint32) if n else np.zeros(0, np.uint32)
     return Columns(
         n=n, num_devices_total=int(trace.num_devices_total), host_device=int(trace.host_device),
         seq=cols["seq"], start_ns=cols["start_ns"], end_ns=cols["end_ns"], src_addr=cols["src_addr"],
