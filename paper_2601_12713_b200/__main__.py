@@ -40,7 +40,7 @@ def _color() -> bool:
     return mode == "always" or (mode != "never" and sys.stdout.isatty())
 
 
-def _load(path):
+def _load(path, validate=True):
     from .ingest import TraceIOError, parse_trace_columns
     try:
         with open(path, "rb") as fh:
@@ -49,7 +49,7 @@ def _load(path):
         print(f"dmlens: error: cannot read {path}: {exc}", file=sys.stderr)
         return None
     try:
-        return parse_trace_columns(data)
+        return parse_trace_columns(data, validate=validate)
     except TraceIOError as exc:
         print(f"dmlens: error: {type(exc).__name__}: {exc}", file=sys.stderr)
         return None
@@ -58,10 +58,17 @@ def _load(path):
 def cmd_analyze(args) -> int:
     from .analysis import analyze_columns
     from .reporting import build_report, filter_min_bytes, render_json, render_text
-    cols = _load(args.trace)
+    from .analysis import EngineInvalid
+    from .ingest import event_violations, invariant_error
+    cols = _load(args.trace, validate=False)  # the analysis run below validates the events
     if cols is None:
         return EXIT_INPUT
-    cf = analyze_columns(cols, strict=args.strict_pseudocode)
+    try:
+        cf = analyze_columns(cols, strict=args.strict_pseudocode)
+    except EngineInvalid as exc:  # the same error parse_trace would have raised
+        err = invariant_error(event_violations(cols, exc))
+        print(f"dmlens: error: {type(err).__name__}: {err}", file=sys.stderr)
+        return EXIT_INPUT
     if not args.quiet:
         for i in cf.warn_index.tolist():
             print(f"dmlens: warning: seq {int(cols.seq[i])}: {WARN_REASON}", file=sys.stderr)

@@ -1371,6 +1371,13 @@ cudaStream_t engine_stream() {
         CK(cudaDeviceGetDefaultMemPool(&pool, dev));
         uint64_t keep = ~0ull;
         CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        // grow the pool once up front (one mapping instead of many small growths on the first
+        // call; a one-shot CLI run pays the first call only)
+        void *warm = nullptr;
+        if (cudaMallocAsync(&warm, size_t(512) << 20, g_stream[dev & 63]) == cudaSuccess)
+            cudaFreeAsync(warm, g_stream[dev & 63]);
+        else
+            cudaGetLastError();
     }
     return g_stream[dev & 63];
 }

@@ -211,30 +211,55 @@ def _to_columns(header, cols, locs) -> Columns:
                    locs=locs or [(0, None, None)])
 
 
-def _validate_columns(c: Columns, types):
-    """GPU validation of parsed columns -> violations (model.py:125-200 messages)."""
+def _violation_type(types):
     T = family(types.root) if types is not None and getattr(types, "root", None) else family(None)
-    V = T.Violation
+    return T.Violation
+
+
+def _header_violations(c: Columns, types):
+    V = _violation_type(types)
     out = []
     if c.num_devices_total < 1:
         out.append(V("header", f"num_devices_total={c.num_devices_total} must be positive"))
     if not 0 <= c.host_device < max(c.num_devices_total, 1):
         out.append(V("header", f"host_device={c.host_device} out of range"))
-    try:
-        analyze_columns(c, flags=FLAG_VALIDATE_ONLY)
-    except EngineInvalid as exc:
-        for i, m in zip(exc.bad_index.tolist(), exc.bad_rules.tolist()):
-            loc = c.locs[int(c.loc[i])]
-            e = _Ev(int(c.seq[i]), int(c.start_ns[i]), int(c.end_ns[i]), int(c.src_device[i]),
-                    int(c.dst_device[i]), _Lc(loc[2]))
-            for bit, rule, text in _RULE_TEXT:
-                if m & bit:
-                    out.append(V(rule, text(e, c.num_devices_total), e.seq))
     return out
 
 
-def parse_trace_columns(data, threads: Optional[int] = None, types=None) -> Columns:
-    """Parse + sort + validate into device-ready columns (no per-event Python objects)."""
+def event_violations(c: Columns, exc: EngineInvalid, types=None):
+    """The reference's Violation list (model.py:133-196 messages, trace order) for the events an
+    engine run flagged -- from b2l_analyze's validation, whichever call ran it."""
+    V = _violation_type(types)
+    out = []
+    for i, m in zip(exc.bad_index.tolist(), exc.bad_rules.tolist()):
+        loc = c.locs[int(c.loc[i])]
+        e = _Ev(int(c.seq[i]), int(c.start_ns[i]), int(c.end_ns[i]), int(c.src_device[i]),
+                int(c.dst_device[i]), _Lc(loc[2]))
+        for bit, rule, text in _RULE_TEXT:
+            if m & bit:
+                out.append(V(rule, text(e, c.num_devices_total), e.seq))
+    return out
+
+
+def invariant_error(violations, types=None):
+    return _errors(types)[3](violations)
+
+
+def _validate_columns(c: Columns, types):
+    """GPU validation of parsed columns -> violations (model.py:125-200 messages)."""
+    out = _header_violations(c, types)
+    try:
+        analyze_columns(c, flags=FLAG_VALIDATE_ONLY)
+    except EngineInvalid as exc:
+        out += event_violations(c, exc, types)
+    return out
+
+
+def parse_trace_columns(data, threads: Optional[int] = None, types=None, validate: bool = True) -> Columns:
+    """Parse + sort + validate into device-ready columns (no per-event Python objects).
+    validate=False leaves the event rules to the caller's next engine run (b2l_analyze validates
+    anyway; turn its EngineInvalid into the same error with ``event_violations`` /
+    ``invariant_error``) -- header rules are always checked here."""
     raw, text = _as_bytes(data)
     if text is None and not raw.isascii():
         text = raw.decode("utf-8")  # the reference decodes first (UnicodeDecodeError as it does)
@@ -246,6 +271,8 @@ def parse_trace_columns(data, threads: Optional[int] = None, types=None) -> Colu
         from .columns import to_columns
         return to_columns(_parse_exact(text if text is not None else raw.decode("utf-8"), types))
     c = _to_columns(*got)
+    if not validate and not _header_violations(c, types):
+        return c
     viol = _validate_columns(c, types)
     if viol:
         raise _errors(types)[3](viol)
