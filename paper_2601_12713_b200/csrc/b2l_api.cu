@@ -41,6 +41,7 @@ int hash_launch_info(uint64_t, int *, int *, int *);
 int hash_select_variant(int, int *);
 int hash_planes_launch(const void *, uint64_t, uint64_t *, cudaStream_t);
 constexpr uint64_t K2_MIN_BYTES = 32ull << 20;  // serial chain >= ~20 ms: the whole-GPU fold wins
+constexpr uint64_t K2_SOLO_BYTES = 96ull << 10;  // a call hashing ONE buffer: K2 (~80 us floor) beats the 1.6 ns/B chain
 int fill_payloads_launch(uint8_t *, const uint64_t *, const uint64_t *, const uint64_t *, uint64_t, uint64_t,
                          cudaStream_t);
 
@@ -70,7 +71,14 @@ struct HostPipe {
     Slot slot[2];
     uint64_t *d_digests = nullptr;
     uint64_t dig_cap = 0;
+    uint8_t *h_small = nullptr, *d_small = nullptr;  // one-DMA staging for small calls (pinned / device)
 };
+
+// Small calls (the per-event HashFn drop-in: one payload of a few bytes to a few KiB) are
+// latency-bound: the payloads are packed behind their (ptr, len) table in one pinned block,
+// moved by ONE host->device copy, hashed, and the digests come back by one device->host copy.
+constexpr uint64_t SMALL_MAX_BUFS = 64, SMALL_BYTES = 64ull << 10;
+constexpr uint64_t SMALL_META = 16 * SMALL_MAX_BUFS, SMALL_CAP = SMALL_META + SMALL_BYTES + 8 * SMALL_MAX_BUFS;
 
 std::mutex g_pipe_mu;
 HostPipe g_pipes[64];
@@ -111,6 +119,34 @@ int ensure_slot(Slot &s, uint64_t data_bytes, uint64_t nbuf) {
 
 inline uint64_t span_bytes(uint64_t start, uint64_t len) { return len + (start & 15) + 16; }
 
+int hash_small(HostPipe &P, const void *const *h_bufs, const uint64_t *h_lens, uint64_t n, uint64_t *h_digests) {
+    if (!P.h_small) {
+        B2L_CUDA(cudaMallocHost(&P.h_small, SMALL_CAP));
+        B2L_CUDA(cudaMalloc(&P.d_small, SMALL_CAP));
+    }
+    uint64_t *hp = (uint64_t *)P.h_small, *hl = hp + n;
+    uint64_t off = SMALL_META;
+    bool any_empty = false;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (h_lens[i]) std::memcpy(P.h_small + off, h_bufs[i], h_lens[i]);
+        any_empty |= h_lens[i] == 0;
+        hp[i] = (uint64_t)(P.d_small + off);
+        hl[i] = h_lens[i];
+        off += (h_lens[i] + 15) & ~15ull;
+    }
+    const uint64_t dig_off = SMALL_META + SMALL_BYTES;
+    uint64_t *d_dig = (uint64_t *)(P.d_small + dig_off), *h_dig = (uint64_t *)(P.h_small + dig_off);
+    B2L_CUDA(cudaMemcpyAsync(P.d_small, P.h_small, off, cudaMemcpyHostToDevice, P.comp));
+    const uint64_t *d_meta = (const uint64_t *)P.d_small;
+    int rc = hash_batch_launch(d_meta, d_meta + n, n, d_dig, nullptr, P.comp);
+    if (rc) return rc;
+    B2L_CUDA(cudaMemcpyAsync(h_dig, d_dig, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, P.comp));
+    B2L_CUDA(cudaStreamSynchronize(P.comp));
+    std::memcpy(h_digests, h_dig, n * sizeof(uint64_t));
+    if (any_empty) return fail(B2L_E_EMPTY_PAYLOAD, "cannot hash a zero-byte payload");
+    return B2L_OK;
+}
+
 }  // namespace
 
 int hash_host_impl(const void *const *h_bufs, const uint64_t *h_lens, uint64_t n, uint64_t *h_digests) {
@@ -125,6 +161,11 @@ int hash_host_impl(const void *const *h_bufs, const uint64_t *h_lens, uint64_t n
         B2L_CUDA(cudaStreamCreateWithFlags(&P.copy, cudaStreamNonBlocking));
         B2L_CUDA(cudaStreamCreateWithFlags(&P.comp, cudaStreamNonBlocking));
         P.device = dev;
+    }
+    if (n <= SMALL_MAX_BUFS) {
+        uint64_t tot = 0;
+        for (uint64_t i = 0; i < n; ++i) tot += (h_lens[i] + 15) & ~15ull;
+        if (tot <= SMALL_BYTES) return hash_small(P, h_bufs, h_lens, n, h_digests);
     }
     if (P.dig_cap < n) {
         if (P.d_digests) cudaFree(P.d_digests);
@@ -188,7 +229,7 @@ int hash_host_impl(const void *const *h_bufs, const uint64_t *h_lens, uint64_t n
         B2L_CUDA(cudaMemcpyAsync(S.d_meta, S.h_meta, 2 * nb * sizeof(uint64_t), cudaMemcpyHostToDevice, P.copy));
         B2L_CUDA(cudaEventRecord(S.copied, P.copy));
         B2L_CUDA(cudaStreamWaitEvent(P.comp, S.copied, 0));
-        if (nb == 1 && h_lens[i0] >= K2_MIN_BYTES)  // one huge buffer: exact whole-GPU fold (K2)
+        if (nb == 1 && (h_lens[i0] >= K2_MIN_BYTES || (n == 1 && h_lens[i0] >= K2_SOLO_BYTES)))  // whole-GPU fold
             rc = hash_planes_launch((const void *)mp[0], h_lens[i0], P.d_digests + i0, P.comp);
         else
             rc = hash_batch_launch(S.d_meta, S.d_meta + nb, nb, P.d_digests + i0, d_order, P.comp);

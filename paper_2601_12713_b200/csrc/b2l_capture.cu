@@ -11,7 +11,7 @@
 // destination of a host-to-device copy once it has landed (end callback), the source of a
 // device-to-host copy -- with the K1 kernel on the agent's own stream, synchronously inside
 // the callback (a later kernel of the program may overwrite the buffer, so the digest must be
-// taken before the callback returns); buffers of 32 MiB and more go to K2 (whole GPU).  Host
+// taken before the callback returns); buffers of 96 KiB and more go to K2 (whole GPU).  Host
 // buffers, when that is all the runtime offers, are hashed on the GPU through b2l_hash_host.
 // Digests equal hashing.hash_bytes (the shared contract, capture.ts:21 / hash64.ts).
 #include <cuda_runtime.h>
@@ -125,7 +125,7 @@ struct Capture {
         if (!stream) B2L_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
         if (!d_args) B2L_CUDA(cudaMalloc(&d_args, 3 * sizeof(uint64_t)));
         if (!h_args) B2L_CUDA(cudaMallocHost(&h_args, 3 * sizeof(uint64_t)));
-        if (n >= (32ull << 20)) {
+        if (n >= (96ull << 10)) {  // one buffer at a time: K2's floor beats the serial chain here
             const int rc = hash_planes_launch(d_buf, n, d_args + 2, stream);
             if (rc) return rc;
         } else {

@@ -110,6 +110,7 @@ def hash_device(ptrs, lens, out, order=None, stream=None) -> None:
 
 
 K2_MIN_BYTES = 32 << 20  # buffers whose serial chain would dominate: hashed by the whole GPU (K2)
+K2_SOLO_BYTES = 96 << 10  # a lone buffer: K2's ~80 us floor beats the 1.6 ns/B serial chain above this
 
 
 def hash_large(ptr: int, nbytes: int, out_ptr: int, stream=None) -> None:
@@ -140,11 +141,12 @@ def hash_tensors(tensors: Sequence, stream=None):
         if not t.is_contiguous() or t.device != dev:
             raise ValueError("hash_tensors needs contiguous tensors on one CUDA device")
     out = torch.empty(len(tensors), dtype=torch.int64, device=dev)
-    big = [i for i, n in enumerate(lens_h) if n >= K2_MIN_BYTES]
+    big = [i for i, n in enumerate(lens_h) if n >= (K2_SOLO_BYTES if len(tensors) == 1 else K2_MIN_BYTES)]
     for i in big:  # each huge buffer with the whole GPU, then the rest as one batch
         hash_large(tensors[i].data_ptr(), lens_h[i], out.data_ptr() + 8 * i, stream)
     if big:
-        small = [i for i in range(len(tensors)) if lens_h[i] < K2_MIN_BYTES]
+        bigs = set(big)
+        small = [i for i in range(len(tensors)) if i not in bigs]
         if small:
             sub = hash_tensors([tensors[i] for i in small], stream=stream)
             out[torch.tensor(small, device=dev)] = sub

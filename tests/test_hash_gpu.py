@@ -280,3 +280,22 @@ def test_audit_random_vs_oracle(cuda):
                 p = p[:-1] if rng.random() < 0.5 else bytes([p[0] ^ 1]) + p[1:]
             obs.append((int(rng.integers(0, 8)), p))
         assert audit_payloads([h for h, _ in obs], [p for _, p in obs]) == hash_ref.audit_ref(obs), trial
+
+
+def test_single_buffer_routing_around_k2_solo_threshold(cuda):
+    """A call hashing ONE buffer goes to K2 from 96 KiB (b2l_hash_bytes, hash_tensors) and
+    small calls take the one-DMA staging path; every route equals the oracle."""
+    import torch
+    from paper_2601_12713_b200 import hash_batch, hash_bytes, hash_tensors
+    from paper_2601_12713_b200.hashing import to_u64_list
+    base = hash_ref.payload(1 << 20, 9, 2)
+    for n in (1, 15, 4096, 65536, (96 << 10) - 1, 96 << 10, (96 << 10) + 1, 200_003, 1 << 20):
+        p = base[:n]
+        want = hash_ref.fold64_c(p) or 1
+        assert hash_bytes(p) == want, n
+        t = torch.frombuffer(bytearray(p), dtype=torch.uint8).to(cuda)
+        assert to_u64_list(hash_tensors([t]))[0] == hash_ref.fold64_c(p), n
+    # small-call staging: up to 64 buffers / 64 KiB in one DMA, then the ring path beyond
+    for cnt, size in ((64, 1000), (65, 10), (3, 30000), (2, 40000)):
+        ps = [base[i * 7:i * 7 + size] for i in range(cnt)]
+        assert hash_batch(ps) == [hash_ref.fold64_c(q) for q in ps], (cnt, size)
