@@ -1681,10 +1681,14 @@ __global__ void k_sums(DevCols c, const uint8_t *cat, unsigned long long *acc /*
         add128(a[5], d);
         ++cnt;
     }
+    // warp -> block (shared memory) -> one set of atomics per block: every warp hitting the same
+    // nine L2 addresses serialises (~85k same-address atomics at 1M events otherwise)
+    __shared__ unsigned long long part[32][15];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
         U128 w = warp_sum128(a[k]);
-        if ((threadIdx.x & 31) == 0) atomic_add128(acc + 2 * k, w);
+        if (lane == 0) part[warp][2 * k] = w.lo, part[warp][2 * k + 1] = w.hi;
     }
     for (int o = 16; o; o >>= 1) {
         cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
@@ -1692,10 +1696,33 @@ __global__ void k_sums(DevCols c, const uint8_t *cat, unsigned long long *acc /*
         mn = x < mn ? x : mn;
         mx = y > mx ? y : mx;
     }
-    if ((threadIdx.x & 31) == 0) {
-        if (cnt) atomicAdd(nunion, cnt);
-        atomicMin(minmax, mn);
-        atomicMax(minmax + 1, mx);
+    if (lane == 0) part[warp][12] = cnt, part[warp][13] = mn, part[warp][14] = mx;
+    __syncthreads();
+    if (warp != 0) return;
+    U128 b[6];
+    unsigned long long bc = 0, bmn = ~0ull, bmx = 0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) b[k] = U128{0, 0};
+    if (lane < nwarps) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) b[k] = U128{part[lane][2 * k], part[lane][2 * k + 1]};
+        bc = part[lane][12], bmn = part[lane][13], bmx = part[lane][14];
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        U128 w = warp_sum128(b[k]);
+        if (lane == 0) atomic_add128(acc + 2 * k, w);
+    }
+    for (int o = 16; o; o >>= 1) {
+        bc += __shfl_xor_sync(0xffffffffu, bc, o);
+        unsigned long long x = __shfl_xor_sync(0xffffffffu, bmn, o), y = __shfl_xor_sync(0xffffffffu, bmx, o);
+        bmn = x < bmn ? x : bmn;
+        bmx = y > bmx ? y : bmx;
+    }
+    if (lane == 0) {
+        if (bc) atomicAdd(nunion, bc);
+        atomicMin(minmax, bmn);
+        atomicMax(minmax + 1, bmx);
     }
 }
 
@@ -1937,7 +1964,7 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     };
     join_streams(s, sb);
     if (n) {
-        k_sums<<<grid_for(n, TPB, 148 * 8), TPB, 0, sb>>>(c, cat.p, acc.p, acc.p + 12, acc.p + 13);
+        k_sums<<<grid_for(n, TPB, 148 * 4), TPB, 0, sb>>>(c, cat.p, acc.p, acc.p + 12, acc.p + 13);
         CK_LAUNCH("k_sums");
     }
     // overlap: exists i >= 1 with start[i] < max(end[0..i-1])  (estimator.py:51-58)

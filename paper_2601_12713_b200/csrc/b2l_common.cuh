@@ -90,6 +90,17 @@ __device__ __forceinline__ void fnv_step32(uint32_t &hl, uint32_t &hh, uint32_t 
     // keep the hi recurrence a single IMAD on the critical path (stop re-association)
     asm("mad.lo.u32 %0, %1, 435, %2;" : "=r"(hh) : "r"(xh), "r"(c));
 }
+// Latency form for a lone chain: the lo recurrence is a plain IMAD (no IMAD.WIDE on the
+// critical path); hi32(xl*435) comes from a separate IMAD.HI off the chain.
+// (the IMAD.HI multiplier is read from constant memory so ptxas cannot re-fuse the pair into
+// one IMAD.WIDE)
+__constant__ static uint32_t c_fnv_prime_lo = 435u;
+__device__ __forceinline__ void fnv_step32_lat(uint32_t &hl, uint32_t &hh, uint32_t wl, uint32_t wh) {
+    const uint32_t xl = hl ^ wl, xh = hh ^ wh;
+    const uint32_t c = __umulhi(xl, c_fnv_prime_lo) + (xl << 8);
+    asm("mul.lo.u32 %0, %1, 435;" : "=r"(hl) : "r"(xl));
+    asm("mad.lo.u32 %0, %1, 435, %2;" : "=r"(hh) : "r"(xh), "r"(c));
+}
 __host__ __device__ __forceinline__ uint64_t finish_digest(uint64_t h, uint64_t n) {
     h = fmix64(h ^ n);
     return h ? h : 1ull;

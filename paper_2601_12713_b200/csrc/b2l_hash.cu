@@ -54,7 +54,9 @@ __device__ __forceinline__ void cursor_load(BufCursor &c, const uint64_t *__rest
 // Hash one staged chunk (`bytes` stream bytes starting at stream offset cs.pos) into (h, prev).
 // Word j of the payload is stream u64 q = q0 + j, or -- when start % 8 != 0 -- the funnel of
 // stream u64s (q0+j, q0+j+1), emitted at q0+j+1.
-template <int CH>
+// PF (one chain per warp, registers to spare): the whole chunk is loaded into registers before
+// the chain starts, so no LDS latency lands on the chain's critical path.
+template <int CH, bool PF = false>
 __device__ __forceinline__ void consume_chunk(const BufCursor &cs, uint32_t bytes, const uint4 *__restrict__ src,
                                               uint64_t &h, uint64_t &prev) {
     const uint32_t r = cs.m & 7u;
@@ -64,7 +66,18 @@ __device__ __forceinline__ void consume_chunk(const BufCursor &cs, uint32_t byte
     const uint64_t qc = cs.pos >> 3;
     const uint32_t nu = bytes >> 3;
     const bool interior = qc >= qb && qc + nu < qe && cs.pos + bytes < cs.L;  // full, not the last chunk
-    if (r == 0 && interior) {
+    if (PF && r == 0 && interior) {
+        uint4 v[CH / 16];
+#pragma unroll
+        for (int i = 0; i < CH / 16; ++i) v[i] = src[i];
+        uint32_t hl = (uint32_t)h, hh = (uint32_t)(h >> 32);
+#pragma unroll
+        for (int i = 0; i < CH / 16; ++i) {
+            fnv_step32_lat(hl, hh, v[i].x, v[i].y);
+            fnv_step32_lat(hl, hh, v[i].z, v[i].w);
+        }
+        h = ((uint64_t)hh << 32) | hl;
+    } else if (r == 0 && interior) {
         uint32_t hl = (uint32_t)h, hh = (uint32_t)(h >> 32);
 #pragma unroll 8
         for (uint32_t i = 0; i < (uint32_t)CH / 16; ++i) {
@@ -82,8 +95,13 @@ __device__ __forceinline__ void consume_chunk(const BufCursor &cs, uint32_t byte
             uint64_t u0 = ((uint64_t)v.y << 32) | v.x, u1 = ((uint64_t)v.w << 32) | v.z;
             uint64_t w0 = (prev >> sh) | (u0 << (64 - sh));
             uint64_t w1 = (u0 >> sh) | (u1 << (64 - sh));
-            fnv_step32(hl, hh, (uint32_t)w0, (uint32_t)(w0 >> 32));
-            fnv_step32(hl, hh, (uint32_t)w1, (uint32_t)(w1 >> 32));
+            if (PF) {
+                fnv_step32_lat(hl, hh, (uint32_t)w0, (uint32_t)(w0 >> 32));
+                fnv_step32_lat(hl, hh, (uint32_t)w1, (uint32_t)(w1 >> 32));
+            } else {
+                fnv_step32(hl, hh, (uint32_t)w0, (uint32_t)(w0 >> 32));
+                fnv_step32(hl, hh, (uint32_t)w1, (uint32_t)(w1 >> 32));
+            }
             prev = u1;
         }
         h = ((uint64_t)hh << 32) | hl;
@@ -333,7 +351,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_hash_warp(const uint64_t *__rest
             __syncwarp();
             issue(st == 0 ? S - 1 : st - 1);
             const uint32_t bytes = chunk_bytes(cs, CH);
-            if (lane == 0) consume_chunk<CH>(cs, bytes, reinterpret_cast<const uint4 *>(ring + st * CH), h, prev);
+            if (lane == 0) consume_chunk<CH, true>(cs, bytes, reinterpret_cast<const uint4 *>(ring + st * CH), h, prev);
             cs.pos += bytes;
             st = st + 1 == S ? 0 : st + 1;
             __syncwarp();  // the slot is re-filled only after lane 0 has read it
