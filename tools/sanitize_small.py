@@ -27,6 +27,8 @@ for strategy in (0, 1, 16 + 5):
     _lib.check(L.b2l_stable_sort_u64(keys.ctypes.data, keys.size, strategy, perm.ctypes.data), "sort")
     assert np.array_equal(perm, np.argsort(keys, kind="stable")), strategy
 print("ok sorts")
+if "--no-sharded" in sys.argv:  # (racecheck on the threaded sharded run alone takes > 10 min)
+    sys.exit(0)
 c = c2_trace(n)
 got = sharded.run_local_device(c, 2)
 assert got.counts() == analyze_columns(c).counts()
