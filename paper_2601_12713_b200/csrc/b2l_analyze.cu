@@ -498,6 +498,7 @@ struct StoreOffset {
 // ============================================================ output container
 struct HostSlab;
 struct Internal {
+    Arena arena;  // the call's scratch (first member: released after every buffer carved from it)
     HostSlab *slab = nullptr;  // pinned host memory behind the b2l_findings arrays
     // device copies of the trace columns (when they were uploaded from host) and their identity
     ColsUpload cols;
@@ -751,7 +752,9 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
     }
     EngineErr errd{0, ""};
     bool faild = false;
+    Arena *const arena = t_arena;
     auto dd_groups = [&](cudaStream_t s) {
+        ArenaUse au(arena);
         try {
             CK(cudaSetDevice(dev));
             g_masks = masks;
@@ -1360,6 +1363,10 @@ void ut_step(const DevCols &c, const KernelIndex &KI, const uint32_t *TT, uint32
 // ============================================================ analyze (detectors.py:274-326)
 std::mutex g_mu;
 cudaStream_t g_stream[64] = {nullptr};
+// arena sizing: bytes of scratch per event as measured with B2L_TRACE (analyze 164-183 B/event on
+// C2/C4 at 10k-4M events), plus slack; beyond 64M events buffers come from the pool (reused)
+constexpr size_t ARENA_MAX_EVENTS = size_t(64) << 20, ARENA_BASE = size_t(4) << 20;
+constexpr size_t ARENA_ANALYZE_PER_EVENT = 256, ARENA_SAVINGS_PER_EVENT = 96;  // savings: 5 B/event + a 69 B/event column upload
 
 cudaStream_t engine_stream() {
     int dev = 0;
@@ -1410,6 +1417,9 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     const DevCols c = up.d;
     const size_t n = c.n;
     pc.mark("upload");
+    // scratch and device findings of this call come from one arena held by the findings
+    in->arena.open(n <= ARENA_MAX_EVENTS ? ARENA_BASE + n * ARENA_ANALYZE_PER_EVENT : 0, s);
+    ArenaUse arena_use(&in->arena);
     // ---- 1+2. validation, partition, max end, key-bit masks, start ranks (fused front pass)
     const bool validate = !(flags & B2L_ANALYZE_NO_VALIDATE), raw = (flags & B2L_ANALYZE_RAW_HASHED) != 0;
     const unsigned ftiles = (unsigned)((n + FR_TILE - 1) / FR_TILE);
@@ -1501,6 +1511,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     EngineErr err2{0, ""}, err3{0, ""};
     bool failed2 = false, failed3 = false, promised = false;
     auto pairs_chain = [&] {
+        ArenaUse au(&in->arena);
         try {
             CK(cudaSetDevice(dev));
             g_masks = masks;
@@ -1523,6 +1534,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
         }
     };
     auto kernel_chain = [&] {
+        ArenaUse au(&in->arena);
         try {
             CK(cudaSetDevice(dev));
             g_masks = masks;
@@ -1594,6 +1606,12 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     in->slab = new HostSlab();
     hb.flush(*in->slab, s);
     pc.mark("d2h");
+    if (alloc_stats().on) {
+        fprintf(stderr, "[b2l] pool alloc/free calls %llu, host %.3f ms; arena %.1f of %.1f MB (%.0f B/event)\n",
+                (unsigned long long)alloc_stats().n.load(), alloc_stats().ns.load() * 1e-6,
+                in->arena.off.load() / 1048576.0, in->arena.cap / 1048576.0, n ? (double)in->arena.off.load() / n : 0.0);
+        alloc_stats().n = 0, alloc_stats().ns = 0;
+    }
     if (in->dd_groups == 0) f->dd_offsets[0] = 0;
     if (in->rt_groups == 0) f->rt_offsets[0] = 0;
     if (in->ra_groups == 0) f->ra_offsets[0] = 0;
@@ -1830,6 +1848,9 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     *outp = o;
     std::lock_guard<std::mutex> lock(g_mu);
     cudaStream_t s = engine_stream();
+    Arena arena;  // this call's scratch (declared first: released last)
+    arena.open(cols->n_events <= ARENA_MAX_EVENTS ? ARENA_BASE + cols->n_events * ARENA_SAVINGS_PER_EVENT : 0, s);
+    ArenaUse arena_use(&arena);
     ColsUpload up;
     const Internal *fin = (const Internal *)f->internal;
     DevCols c;
@@ -2018,6 +2039,9 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     o->internal = slab;
     hb.flush(*slab, s);
     pc.mark("sv-d2h");
+    if (alloc_stats().on)
+        fprintf(stderr, "[b2l] savings arena %.1f of %.1f MB (%.0f B/event)\n", arena.off.load() / 1048576.0,
+                arena.cap / 1048576.0, n ? (double)arena.off.load() / n : 0.0);
     return B2L_OK;
 }
 
