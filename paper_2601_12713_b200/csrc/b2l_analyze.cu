@@ -17,9 +17,12 @@
 // Proofs of the reformulations: SURVEY.md Appendix A; the GPU tests check every step
 // against oracle/analysis_ref.py and the reference's golden outputs.
 #include <chrono>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
+#include <functional>
 #include <future>
 #include <mutex>
 #include <thread>
@@ -684,6 +687,46 @@ __global__ void k_rt_strict(DevCols c, const uint32_t *H, const uint32_t *hsorte
     }
 }
 
+// Persistent host workers for the side chains (spawning three threads per call cost tens of µs).
+// Calls are serialised by g_mu, so at most three tasks are in flight; the pool is never torn down.
+class Workers {
+   public:
+    explicit Workers(int n) {
+        for (int i = 0; i < n; ++i) std::thread([this] { loop(); }).detach();
+    }
+    std::future<void> submit(std::function<void()> f) {
+        auto task = std::make_shared<std::packaged_task<void()>>(std::move(f));
+        std::future<void> fu = task->get_future();
+        {
+            std::lock_guard<std::mutex> l(m_);
+            q_.emplace_back([task] { (*task)(); });
+        }
+        cv_.notify_one();
+        return fu;
+    }
+
+   private:
+    void loop() {
+        for (;;) {
+            std::function<void()> f;
+            {
+                std::unique_lock<std::mutex> l(m_);
+                cv_.wait(l, [&] { return !q_.empty(); });
+                f = std::move(q_.front());
+                q_.pop_front();
+            }
+            f();
+        }
+    }
+    std::mutex m_;
+    std::condition_variable cv_;
+    std::deque<std::function<void()>> q_;
+};
+inline Workers &workers() {
+    static Workers *w = new Workers(4);
+    return *w;
+}
+
 struct DdRt {
     uint64_t dd_groups = 0, rt_groups = 0, dd_members = 0, rt_trips = 0;
 };
@@ -810,8 +853,8 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
             faild = true;
         }
     };
-    std::thread td;
-    if (dd_side) td = std::thread(dd_groups, sd);
+    std::future<void> td;
+    if (dd_side) td = workers().submit([&] { dd_groups(sd); });
     else dd_groups(s);
     auto rt_groups = [&] {
         // ---- round trips: per send, the matched reception (or NONE)
@@ -914,10 +957,10 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
     try {
         rt_groups();
     } catch (...) {
-        if (td.joinable()) td.join();
+        if (td.valid()) td.wait();
         throw;
     }
-    if (td.joinable()) td.join();
+    if (td.valid()) td.wait();
     if (faild) throw errd;
     pc.mark(" dd-rt-groups");
     return r;
@@ -1554,17 +1597,17 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
             failed3 = true;
         }
     };
-    std::thread t2, t3;
+    std::future<void> t2, t3;
     if (overlap) {
-        t2 = std::thread(pairs_chain);
-        t3 = std::thread(kernel_chain);
+        t2 = workers().submit(pairs_chain);
+        t3 = workers().submit(kernel_chain);
     } else {
         pairs_chain();
         kernel_chain();
     }
     auto join = [&] {
-        if (t2.joinable()) t2.join();
-        if (t3.joinable()) t3.join();
+        if (t2.valid()) t2.wait();
+        if (t3.valid()) t3.wait();
         cudaEvent_t ev = pairs_ready.get();
         if (ev) cudaEventDestroy(ev);
     };
