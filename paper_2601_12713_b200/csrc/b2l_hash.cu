@@ -15,6 +15,7 @@
 // shift when start % 8 != 0.  Reads never leave the 16-B aligned segments
 // that contain buffer bytes, so they never cross a page the buffer does not
 // touch.
+#include <algorithm>
 #include <cstdlib>
 
 #include "b2l_common.cuh"
@@ -325,8 +326,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_hash_warp(const uint64_t *__rest
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint8_t *ring = smem + (size_t)warp * S * CH;
     const uint32_t ring_s = smem_u32(ring);
-    const uint64_t stride = (uint64_t)gridDim.x * WARPS;
-    for (uint64_t k = (uint64_t)blockIdx.x * WARPS + warp; k < n_bufs; k += stride) {
+    // Round r of warp w takes list position r*W + w, or r*W + (W-1-w) on odd rounds (boustrophedon
+    // over a longest-first order: the warp holding the longest buffer gets the shortest of the next
+    // round, so per-warp totals stay close and no other long chain shares its scheduler).
+    const uint64_t W = (uint64_t)gridDim.x * WARPS, wg = (uint64_t)blockIdx.x * WARPS + warp;
+    for (uint64_t r = 0; r * W < n_bufs; ++r) {
+        const uint64_t k = r * W + ((r & 1) ? W - 1 - wg : wg);
+        if (k >= n_bufs) continue;
         BufCursor ld, cs;
         cursor_load(ld, ptrs, lens, order, k, n_bufs);
         cs = ld;
@@ -392,6 +398,7 @@ constexpr int DEFAULT_CFG = 6;  // coop<2 warps, 512 B, 2 stages>: 96.5% of meas
 constexpr int LATENCY_CFG = 11;   // coop<1 warp, 512 B, 6 stages>: batches too small to fill the GPU
 constexpr uint64_t LATENCY_MAX_BUFS = 148ull * 2 * 32;  // one lane per buffer fits the deep variant
 constexpr uint64_t WARP_MAX_BUFS = 148ull * 32;          // one warp per buffer, all resident at once
+constexpr uint64_t RAGGED_WARPS_PER_SMSP = 2;
 
 struct HashLaunch {
     int cfg = -1;
@@ -481,7 +488,11 @@ int hash_batch_launch(const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n
     if (setenv_variant < 0 && !getenv("B2L_HASH_CFG") && n <= WARP_MAX_BUFS) {
         // few buffers: one warp each (every buffer's chain runs at its own latency)
         auto fn = k_hash_warp<WARP_K_WARPS, WARP_K_STAGES>;
-        const unsigned grid = (unsigned)((n + WARP_K_WARPS - 1) / WARP_K_WARPS);
+        // ragged (longest-first order given): two warps per scheduler, buffers dealt out
+        // boustrophedon; uniform: one warp per buffer, all in flight at once
+        uint64_t warps = n;
+        if (d_order) warps = std::min<uint64_t>(n, (uint64_t)sm_count() * 4 * RAGGED_WARPS_PER_SMSP);
+        const unsigned grid = (unsigned)((warps + WARP_K_WARPS - 1) / WARP_K_WARPS);
         fn<<<grid, WARP_K_WARPS * 32, WARP_K_SMEM, stream>>>(d_ptrs, d_lens, d_order, n, d_digests);
         B2L_CHECK_LAUNCH("k_hash_warp");
         return B2L_OK;
