@@ -491,7 +491,11 @@ int hash_batch_launch(const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n
         // ragged (longest-first order given): two warps per scheduler, buffers dealt out
         // boustrophedon; uniform: one warp per buffer, all in flight at once
         uint64_t warps = n;
-        if (d_order) warps = std::min<uint64_t>(n, (uint64_t)sm_count() * 4 * RAGGED_WARPS_PER_SMSP);
+        static const uint64_t wps = [] {  // B2L_RAGGED_WPS: tuning override
+            const char *e = getenv("B2L_RAGGED_WPS");
+            return e && atoi(e) > 0 ? (uint64_t)atoi(e) : RAGGED_WARPS_PER_SMSP;
+        }();
+        if (d_order) warps = std::min<uint64_t>(n, (uint64_t)sm_count() * 4 * wps);
         const unsigned grid = (unsigned)((warps + WARP_K_WARPS - 1) / WARP_K_WARPS);
         fn<<<grid, WARP_K_WARPS * 32, WARP_K_SMEM, stream>>>(d_ptrs, d_lens, d_order, n, d_digests);
         B2L_CHECK_LAUNCH("k_hash_warp");
