@@ -63,14 +63,16 @@ int b2l_hash_batch(const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n,
 
 /* Host buffers (pinned for full speed; pageable works) -> host digests.
  * Copies run on a side stream through a double-buffered device ring and
- * overlap with hashing.  Synchronous.  Returns B2L_E_EMPTY_PAYLOAD if any
+ * overlap with hashing; small calls (<= 64 buffers, <= 64 KiB) are packed into
+ * one pinned block and moved by a single copy each way.  Synchronous.  Returns B2L_E_EMPTY_PAYLOAD if any
  * length is zero (digests of the others are still written). */
 int b2l_hash_host(const void *const *h_bufs, const uint64_t *h_lens, uint64_t n,
                   uint64_t *h_digests);
 
 /* One DEVICE buffer hashed by the whole GPU (K2: exact 4-bit-group decomposition of the
  * serial fold, cooperative launch).  For buffers whose serial chain would dominate a batch
- * (b2l_hash_host routes buffers >= 32 MiB here automatically).  Asynchronous. */
+ * (b2l_hash_host routes buffers >= 32 MiB here automatically, and a call holding a single
+ * buffer from 96 KiB).  Asynchronous. */
 int b2l_hash_large(const void *d_buf, uint64_t len, uint64_t *d_digest, void *stream);
 
 /* One host payload (the HashFn drop-in). */
