@@ -732,6 +732,7 @@ struct DdRt {
 };
 
 cudaStream_t engine_stream_n(int k);
+void stream_after(cudaStream_t to, cudaStream_t from);
 
 DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, Internal &out, cudaStream_t s) {
     DdRt r;
@@ -786,13 +787,7 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
     CK(cudaGetDevice(&dev));
     const Masks masks = g_masks;
     cudaStream_t sd = dd_side ? engine_stream_n(3) : s;
-    if (dd_side) {
-        cudaEvent_t ev;
-        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        CK(cudaEventRecord(ev, s));
-        CK(cudaStreamWaitEvent(sd, ev, 0));
-        CK(cudaEventDestroy(ev));
-    }
+    if (dd_side) stream_after(sd, s);
     EngineErr errd{0, ""};
     bool faild = false;
     Arena *const arena = t_arena;
@@ -1440,6 +1435,18 @@ cudaStream_t engine_stream_n(int k) {  // side streams 1..3: the chains that run
     return st;
 }
 
+// `to` waits for everything queued on `from` so far.  One cached event per host thread and device
+// (an event may be re-recorded as soon as the wait is queued).
+void stream_after(cudaStream_t to, cudaStream_t from) {
+    thread_local cudaEvent_t ev[64] = {nullptr};
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaEvent_t &e = ev[dev & 63];
+    if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventRecord(e, from));
+    CK(cudaStreamWaitEvent(to, e, 0));
+}
+
 int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_override, b2l_findings **outp) {
     b2l_findings *f = (b2l_findings *)calloc(1, sizeof(b2l_findings));
     if (!f) return fail(B2L_E_OOM, "host allocation failed");
@@ -1542,12 +1549,8 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     const bool overlap = n <= (size_t(4) << 20);
     cudaStream_t s2 = overlap ? engine_stream_n(1) : s, s3 = overlap ? engine_stream_n(2) : s;
     if (overlap) {  // the partition lists and start ranks are produced on s
-        cudaEvent_t ev;
-        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        CK(cudaEventRecord(ev, s));
-        CK(cudaStreamWaitEvent(s2, ev, 0));
-        CK(cudaStreamWaitEvent(s3, ev, 0));
-        CK(cudaEventDestroy(ev));
+        stream_after(s2, s);
+        stream_after(s3, s);
     }
     std::promise<cudaEvent_t> pairs_done;  // recorded on s2 after pairing (UA needs the pairs)
     std::shared_future<cudaEvent_t> pairs_ready = pairs_done.get_future().share();
@@ -1942,13 +1945,7 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     // the attribution kernels read only the findings: run them on a side stream beside the
     // category bits, sums and the overlap/union scan
     cudaStream_t sa = engine_stream_n(1);
-    {
-        cudaEvent_t ev;
-        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        CK(cudaEventRecord(ev, s));
-        CK(cudaStreamWaitEvent(sa, ev, 0));
-        CK(cudaEventDestroy(ev));
-    }
+    stream_after(sa, s);
     const size_t smem = nb <= 512 ? (size_t)nb * 6 * sizeof(unsigned long long) : 0;
     auto acc_of = [&](int cat_i) {
         unsigned long long *base = at.p;
@@ -2019,13 +2016,7 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     // the 128-bit sums and the overlap / union scan both only read the category bits: the sums go
     // to a second side stream
     cudaStream_t sb = engine_stream_n(2);
-    auto join_streams = [](cudaStream_t from, cudaStream_t to) {
-        cudaEvent_t ev;
-        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        CK(cudaEventRecord(ev, from));
-        CK(cudaStreamWaitEvent(to, ev, 0));
-        CK(cudaEventDestroy(ev));
-    };
+    auto join_streams = [](cudaStream_t from, cudaStream_t to) { stream_after(to, from); };
     join_streams(s, sb);
     if (n) {
         k_sums<<<grid_for(n, TPB, 148 * 4), TPB, 0, sb>>>(c, cat.p, acc.p, acc.p + 12, acc.p + 13);
@@ -2043,13 +2034,7 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     join_streams(sb, s);
     pc.mark("sv-sums");
     // attribution (on the side stream) has finished before anything is read back
-    {
-        cudaEvent_t ev;
-        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        CK(cudaEventRecord(ev, sa));
-        CK(cudaStreamWaitEvent(s, ev, 0));
-        CK(cudaEventDestroy(ev));
-    }
+    stream_after(s, sa);
     pc.mark("sv-attr");
     // ---- to host
     unsigned long long h[15];
