@@ -980,7 +980,7 @@ static __global__ void __launch_bounds__(FX_THREADS) k_seg_fixup(const uint64_t 
     // position lo + j, j = 0, is a head when j == 0 would need the key before lo: compare it
     if (threadIdx.x == 0 && lo > 0 && (kin[lo - 1] >> shift) != (sk[0] >> shift)) hb[0] |= 1u;
     __syncthreads();
-    uint32_t nbig = 0;
+    uint32_t nbig = 0, nbreak = 0;
 #pragma unroll 1
     for (int it = 0; it < FX_ITEMS; ++it) {
         const size_t i = t0 + (size_t)it * FX_THREADS + threadIdx.x;
@@ -1007,6 +1007,8 @@ static __global__ void __launch_bounds__(FX_THREADS) k_seg_fixup(const uint64_t 
         const uint64_t key = sk[rel];
         if (isbig) {  // stays in place unless its run holds distinct keys (fixed up afterwards)
             ++nbig;
+            // a break: same run as its predecessor (not a head), different full key
+            if (i > 0 && !((hb[rel >> 5] >> (rel & 31)) & 1u) && (rel > 0 ? sk[rel - 1] : kin[i - 1]) != key) ++nbreak;
             kout[i] = key;
             vout[i] = vin[i];
             continue;
@@ -1020,6 +1022,7 @@ static __global__ void __launch_bounds__(FX_THREADS) k_seg_fixup(const uint64_t 
         vout[lo + a + rank] = vin[i];
     }
     if (nbig) atomicAdd(big_count, nbig);
+    if (nbreak) atomicAdd(big_count + 1, nbreak);
 }
 static __global__ void k_compose_idx(const uint32_t *__restrict__ P, const uint32_t *__restrict__ S, size_t m,
                                      uint32_t *__restrict__ out) {
@@ -1059,7 +1062,7 @@ struct BigPred {
 inline void seg_fixup(SortBufs<1> &b, size_t n, int shift, uint8_t live, cudaStream_t s) {
     if (n <= 1) return;
     DBuf<uint8_t> big(n, s);
-    DBuf<uint32_t> cnt(1, s);
+    DBuf<uint32_t> cnt(2, s);  // [records in long runs, breaks inside long runs]
     cnt.zero();
     const uint64_t *kin = b.k[b.cur].w[0];
     const uint32_t *vin = b.v[b.cur];
@@ -1069,9 +1072,10 @@ inline void seg_fixup(SortBufs<1> &b, size_t n, int shift, uint8_t live, cudaStr
                                                                             cnt.p);
     CK_LAUNCH("k_seg_fixup");
     b.cur ^= 1;
-    uint32_t nbig = 0;
-    read_back(&nbig, cnt.p, sizeof(nbig), s);
-    if (!nbig) return;
+    uint32_t nc[2] = {0, 0};
+    read_back(nc, cnt.p, sizeof(nc), s);
+    const uint32_t nbig = nc[0];
+    if (!nbig || !nc[1]) return;  // no long run holds two distinct keys: all in order already
     // long runs: those holding one key repeated are already in order; the others (a "break": equal
     // prefix, different key, between neighbours) are gathered, full-key sorted, scattered back
     DBuf<uint32_t> pos(nbig, s), pc(1, s);
