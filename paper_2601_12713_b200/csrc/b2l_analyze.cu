@@ -2203,6 +2203,9 @@ int shard_route_impl(const b2l_trace_cols *cols, uint32_t G, uint64_t base, uint
     if (G == 0 || G > 256) return fail(B2L_E_INVALID_ARG, "b2l_shard_route: 1..256 ranks");
     std::lock_guard<std::mutex> lock(g_mu);
     cudaStream_t s = engine_stream();
+    Arena arena;  // call-scoped scratch (outputs go to the caller's buffers)
+    arena.open(cols->n_events <= ARENA_MAX_EVENTS ? ARENA_BASE + cols->n_events * 128 : 0, s);
+    ArenaUse arena_use(&arena);
     ColsUpload up;
     up.load(cols, s);
     const DevCols c = up.d;
@@ -2259,6 +2262,9 @@ struct UnpackOut {
 int shard_unpack_impl(const int64_t *d_rows, uint64_t nrows, uint32_t space, const UnpackOut &o, uint64_t *h_n) {
     std::lock_guard<std::mutex> lock(g_mu);
     cudaStream_t s = engine_stream();
+    Arena arena;
+    arena.open(nrows <= ARENA_MAX_EVENTS ? ARENA_BASE + nrows * 32 : 0, s);
+    ArenaUse arena_use(&arena);
     DBuf<uint32_t> pos(nrows ? nrows : 1, s), cnt(1, s);
     compact(nrows, SpacePred{d_rows, space}, pos.p, cnt.p, s);
     uint32_t m = 0;
@@ -2375,6 +2381,9 @@ int b2l_sort_u64_pairs_device(const uint64_t *d_k0, const uint64_t *d_k1, uint64
         std::lock_guard<std::mutex> lock(ana::g_mu);
         cudaStream_t s = ana::engine_stream();
         CK(cudaStreamSynchronize(cudaStreamLegacy));  // inputs written on the caller's stream
+        Arena arena;
+        arena.open(n <= ana::ARENA_MAX_EVENTS ? ana::ARENA_BASE + n * 64 : 0, s);
+        ArenaUse arena_use(&arena);
         SortStore<2> st(n, s);
         CK(cudaMemcpyAsync(st.in_key(0), d_k0, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(st.in_key(1), d_k1, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
