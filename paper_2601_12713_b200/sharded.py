@@ -90,6 +90,9 @@ class LocalComm:
         out = self._exchange(obj)
         return out if self.rank == 0 else None
 
+    def gather0_findings(self, out: dict):
+        return self.gather0(out)
+
 
 class TorchComm:
     """torch.distributed communicator (NCCL for CUDA tensors, gloo on CPU)."""
@@ -154,6 +157,68 @@ class TorchComm:
         out = [None] * self.size if self.rank == 0 else None
         self.dist.gather_object(obj, out, dst=0)
         return out
+
+    def gather0_findings(self, out: dict):
+        """Per-rank findings (dict of numpy arrays / tuples of arrays) to rank 0 as ONE flat int64
+        tensor per rank (a size all-gather, then one all-gather of padded buffers; NCCL moves
+        device memory) instead of pickled objects."""
+        torch, dist = self.torch, self.dist
+        flat = _pack_findings(out)
+        n = torch.tensor([flat.size], dtype=torch.int64, device=self.device)
+        ns = [torch.empty_like(n) for _ in range(self.size)]
+        dist.all_gather(ns, n)
+        sizes = [int(x.item()) for x in ns]
+        buf = torch.zeros(max(sizes), dtype=torch.int64, device=self.device)
+        buf[:flat.size] = torch.from_numpy(flat).to(self.device)
+        bufs = [torch.empty_like(buf) for _ in range(self.size)]
+        dist.all_gather(bufs, buf)
+        if self.rank != 0:
+            return None
+        return [_unpack_findings(b[:sz].cpu().numpy()) for b, sz in zip(bufs, sizes)]
+
+
+# ------------------------------------------------------------------------ findings wire format
+# Per-rank findings as one int64 array: [n_fields, (key id, slot, dtype id, length) * n_fields,
+# payloads (each widened to 64-bit lanes)].  Keys are the detector names of analyze_sharded_device.
+_FKEYS = ("dd", "rt", "pairs", "warn", "ra", "ua", "ut")
+_FDTYPES = (np.int64, np.uint64, np.int32, np.uint32)
+
+
+def _pack_findings(out: dict) -> np.ndarray:
+    fields = []
+    for ki, key in enumerate(_FKEYS):
+        if key not in out:
+            continue
+        val = out[key]
+        arrs = val if isinstance(val, tuple) else (val,)
+        for slot, a in enumerate(arrs):
+            a = np.ascontiguousarray(a)
+            di = next(i for i, d in enumerate(_FDTYPES) if a.dtype == d)
+            slot_id = slot if isinstance(val, tuple) else -1
+            fields.append((ki, slot_id, di, a))
+    head = [len(fields)]
+    for ki, slot, di, a in fields:
+        head += [ki, slot, di, a.size]
+    body = [a.astype(np.int64) if a.dtype != np.uint64 else a.view(np.int64) for _, _, _, a in fields]
+    return np.concatenate([np.asarray(head, dtype=np.int64)] + body) if body else np.asarray(head, np.int64)
+
+
+def _unpack_findings(flat: np.ndarray) -> dict:
+    nf = int(flat[0])
+    head = flat[1:1 + 4 * nf].reshape(nf, 4)
+    o = 1 + 4 * nf
+    out: dict = {}
+    for ki, slot, di, ln in head.tolist():
+        seg = flat[o:o + ln]
+        o += ln
+        d = _FDTYPES[di]
+        a = seg.view(np.uint64).copy() if d == np.uint64 else seg.astype(d)
+        key = _FKEYS[ki]
+        if slot < 0:
+            out[key] = a
+        else:
+            out.setdefault(key, []).append(a)
+    return {k: (tuple(v) if isinstance(v, list) else v) for k, v in out.items()}
 
 
 # ------------------------------------------------------------------------ packing
@@ -457,7 +522,7 @@ def analyze_sharded_device(shard, base: int, comm, strict: bool = False, gather:
     ph.mark("engine")
     if not gather:
         return out
-    parts = comm.gather0(out)
+    parts = comm.gather0_findings(out) if hasattr(comm, "gather0_findings") else comm.gather0(out)
     ph.mark("gather")
     if comm.rank != 0:
         return None

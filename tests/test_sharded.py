@@ -165,3 +165,63 @@ def test_gloo_two_processes_engine_on_gpu(cuda, tmp_path):
     out = tmp_path / "result.txt"
     mp.spawn(_gloo_engine_worker, args=(2, port, str(out)), nprocs=2, join=True)
     assert out.read_text() == "ok"
+
+
+def _findings_sample(rank):
+    rng = np.random.default_rng(rank)
+    out = {"dd": (np.arange(4, dtype=np.int64), rng.integers(0, 99, 3), rng.integers(0, 2**63, 3, dtype=np.uint64)
+                  | np.uint64(2**63), rng.integers(0, 2**63, 3, dtype=np.uint64), np.array([-1, 2, 7], np.int32),
+                  np.zeros(0, np.int64)),
+           "warn": np.array([rank, 5], np.int64), "ut": np.zeros(0, np.int64)}
+    if rank:
+        out["pairs"] = (np.arange(3, dtype=np.int64), np.array([-1, 2, 3], np.int64))
+    return out
+
+
+def _same_findings(a, b):
+    if sorted(a) != sorted(b):
+        return False
+    for k in a:
+        x, y = (a[k], b[k]) if isinstance(a[k], tuple) else ((a[k],), (b[k],))
+        if not isinstance(b[k], type(a[k])) or len(x) != len(y):
+            return False
+        if any(p.dtype != q.dtype or not np.array_equal(p, q) for p, q in zip(x, y)):
+            return False
+    return True
+
+
+def test_findings_wire_format_roundtrip():
+    for r in (0, 1):
+        f = _findings_sample(r)
+        assert _same_findings(f, sharded._unpack_findings(sharded._pack_findings(f)))
+    assert sharded._unpack_findings(sharded._pack_findings({})) == {}
+
+
+def _gloo_gather_worker(rank, world, port, result_path):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        got = sharded.TorchComm().gather0_findings(_findings_sample(rank))
+        if rank == 0:
+            ok = len(got) == world and all(_same_findings(_findings_sample(r), got[r]) for r in range(world))
+            with open(result_path, "w") as f:
+                f.write("ok" if ok else "mismatch")
+        else:
+            assert got is None
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_findings_gather_world_size_2(tmp_path):
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = tmp_path / "result.txt"
+    mp.spawn(_gloo_gather_worker, args=(2, port, str(out)), nprocs=2, join=True)
+    assert out.read_text() == "ok"
