@@ -320,7 +320,7 @@ template <int WARPS, int S>
 __global__ void __launch_bounds__(WARPS * 32) k_hash_warp(const uint64_t *__restrict__ ptrs,
                                                           const uint64_t *__restrict__ lens,
                                                           const uint32_t *__restrict__ order, uint64_t n_bufs,
-                                                          uint64_t *__restrict__ digests) {
+                                                          uint64_t *__restrict__ digests, uint64_t primary) {
     constexpr int CH = 512;
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -328,10 +328,16 @@ __global__ void __launch_bounds__(WARPS * 32) k_hash_warp(const uint64_t *__rest
     const uint32_t ring_s = smem_u32(ring);
     // Round r of warp w takes list position r*W + w, or r*W + (W-1-w) on odd rounds (boustrophedon
     // over a longest-first order: the warp holding the longest buffer gets the shortest of the next
-    // round, so per-warp totals stay close and no other long chain shares its scheduler).
-    const uint64_t W = (uint64_t)gridDim.x * WARPS, wg = (uint64_t)blockIdx.x * WARPS + warp;
-    for (uint64_t r = 0; r * W < n_bufs; ++r) {
-        const uint64_t k = r * W + ((r & 1) ? W - 1 - wg : wg);
+    // round, so per-warp totals stay close).  With `primary` = P > 0, warps 0..P-1 (the first CTA
+    // of every SM) take the P longest buffers alone and the other warps deal out the rest, so the
+    // longest chains share their schedulers only with short work.
+    const uint64_t wg0 = (uint64_t)blockIdx.x * WARPS + warp;
+    const bool prim = wg0 < primary;
+    const uint64_t W = prim ? 1 : (uint64_t)gridDim.x * WARPS - primary;
+    const uint64_t wg = prim ? 0 : wg0 - primary, base = prim ? wg0 : primary;
+    const uint64_t rounds = prim ? 1 : ~0ull;
+    for (uint64_t r = 0; r < rounds && base + r * W < n_bufs; ++r) {
+        const uint64_t k = base + r * W + ((r & 1) ? W - 1 - wg : wg);
         if (k >= n_bufs) continue;
         BufCursor ld, cs;
         cursor_load(ld, ptrs, lens, order, k, n_bufs);
@@ -497,7 +503,11 @@ int hash_batch_launch(const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n
         }();
         if (d_order) warps = std::min<uint64_t>(n, (uint64_t)sm_count() * 4 * wps);
         const unsigned grid = (unsigned)((warps + WARP_K_WARPS - 1) / WARP_K_WARPS);
-        fn<<<grid, WARP_K_WARPS * 32, WARP_K_SMEM, stream>>>(d_ptrs, d_lens, d_order, n, d_digests);
+        // ragged and two warps per scheduler: the first CTA of every SM holds the longest buffers
+        static const bool prim_on = !getenv("B2L_HASH_NO_PRIMARY");
+        const uint64_t primary =
+            (d_order && prim_on && wps == 2 && warps == (uint64_t)sm_count() * 8) ? (uint64_t)sm_count() * 4 : 0;
+        fn<<<grid, WARP_K_WARPS * 32, WARP_K_SMEM, stream>>>(d_ptrs, d_lens, d_order, n, d_digests, primary);
         B2L_CHECK_LAUNCH("k_hash_warp");
         return B2L_OK;
     }
