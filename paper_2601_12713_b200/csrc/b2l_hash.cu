@@ -506,7 +506,7 @@ int hash_batch_launch(const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n
         // ragged and two warps per scheduler: the first CTA of every SM holds the longest buffers
         static const bool prim_on = !getenv("B2L_HASH_NO_PRIMARY");
         const uint64_t primary =
-            (d_order && prim_on && wps == 2 && warps == (uint64_t)sm_count() * 8) ? (uint64_t)sm_count() * 4 : 0;
+            (d_order && prim_on && wps >= 2 && warps == (uint64_t)sm_count() * 4 * wps) ? (uint64_t)sm_count() * 4 : 0;
         fn<<<grid, WARP_K_WARPS * 32, WARP_K_SMEM, stream>>>(d_ptrs, d_lens, d_order, n, d_digests, primary);
         B2L_CHECK_LAUNCH("k_hash_warp");
         return B2L_OK;
