@@ -77,7 +77,7 @@ struct HostPipe {
 // Small calls (the per-event HashFn drop-in: one payload of a few bytes to a few KiB) are
 // latency-bound: the payloads are packed behind their (ptr, len) table in one pinned block,
 // moved by ONE host->device copy, hashed, and the digests come back by one device->host copy.
-constexpr uint64_t SMALL_MAX_BUFS = 64, SMALL_BYTES = 64ull << 10;
+constexpr uint64_t SMALL_MAX_BUFS = 64, SMALL_BYTES = 64ull << 10, ZERO_COPY_BYTES = 4096;
 constexpr uint64_t SMALL_META = 16 * SMALL_MAX_BUFS, SMALL_CAP = SMALL_META + SMALL_BYTES + 8 * SMALL_MAX_BUFS;
 
 std::mutex g_pipe_mu;
@@ -124,23 +124,29 @@ int hash_small(HostPipe &P, const void *const *h_bufs, const uint64_t *h_lens, u
         B2L_CUDA(cudaMallocHost(&P.h_small, SMALL_CAP));
         B2L_CUDA(cudaMalloc(&P.d_small, SMALL_CAP));
     }
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < n; ++i) total += (h_lens[i] + 15) & ~15ull;
+    // a few KiB: the kernel reads the pinned block in place and writes the digests back to it
+    // (host-mapped memory through unified addressing): no copy launches at all
+    const bool zero_copy = total <= ZERO_COPY_BYTES;
+    uint8_t *const dev_view = zero_copy ? P.h_small : P.d_small;
     uint64_t *hp = (uint64_t *)P.h_small, *hl = hp + n;
     uint64_t off = SMALL_META;
     bool any_empty = false;
     for (uint64_t i = 0; i < n; ++i) {
         if (h_lens[i]) std::memcpy(P.h_small + off, h_bufs[i], h_lens[i]);
         any_empty |= h_lens[i] == 0;
-        hp[i] = (uint64_t)(P.d_small + off);
+        hp[i] = (uint64_t)(dev_view + off);
         hl[i] = h_lens[i];
         off += (h_lens[i] + 15) & ~15ull;
     }
     const uint64_t dig_off = SMALL_META + SMALL_BYTES;
-    uint64_t *d_dig = (uint64_t *)(P.d_small + dig_off), *h_dig = (uint64_t *)(P.h_small + dig_off);
-    B2L_CUDA(cudaMemcpyAsync(P.d_small, P.h_small, off, cudaMemcpyHostToDevice, P.comp));
-    const uint64_t *d_meta = (const uint64_t *)P.d_small;
+    uint64_t *d_dig = (uint64_t *)(dev_view + dig_off), *h_dig = (uint64_t *)(P.h_small + dig_off);
+    if (!zero_copy) B2L_CUDA(cudaMemcpyAsync(P.d_small, P.h_small, off, cudaMemcpyHostToDevice, P.comp));
+    const uint64_t *d_meta = (const uint64_t *)dev_view;
     int rc = hash_batch_launch(d_meta, d_meta + n, n, d_dig, nullptr, P.comp);
     if (rc) return rc;
-    B2L_CUDA(cudaMemcpyAsync(h_dig, d_dig, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, P.comp));
+    if (!zero_copy) B2L_CUDA(cudaMemcpyAsync(h_dig, d_dig, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, P.comp));
     B2L_CUDA(cudaStreamSynchronize(P.comp));
     std::memcpy(h_digests, h_dig, n * sizeof(uint64_t));
     if (any_empty) return fail(B2L_E_EMPTY_PAYLOAD, "cannot hash a zero-byte payload");
