@@ -74,8 +74,7 @@ struct Capture {
     std::string audit_dir;  // empty: no payload snapshots
     // device hashing scratch (the agent's own stream)
     cudaStream_t stream = nullptr;
-    uint64_t *d_args = nullptr;  // [ptr, len, digest]
-    uint64_t *h_args = nullptr;  // pinned
+    uint64_t *h_args = nullptr;  // pinned [ptr, len, digest], addressed by the kernels in place
     std::mutex hash_mu;
 
     explicit Capture(int32_t host_id) : host_runtime_id(host_id) {
@@ -84,7 +83,6 @@ struct Capture {
     }
     ~Capture() {
         for (auto *b : owned) delete b;
-        if (d_args) cudaFree(d_args);
         if (h_args) cudaFreeHost(h_args);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -123,18 +121,17 @@ struct Capture {
     int hash_device(const void *d_buf, uint64_t n, uint64_t &digest, std::vector<uint8_t> *snap) {
         std::lock_guard<std::mutex> l(hash_mu);
         if (!stream) B2L_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-        if (!d_args) B2L_CUDA(cudaMalloc(&d_args, 3 * sizeof(uint64_t)));
         if (!h_args) B2L_CUDA(cudaMallocHost(&h_args, 3 * sizeof(uint64_t)));
+        // (ptr, len) and the digest live in pinned host memory the kernels address directly
+        // (unified addressing): no copy launches around the hash
         if (n >= (96ull << 10)) {  // one buffer at a time: K2's floor beats the serial chain here
-            const int rc = hash_planes_launch(d_buf, n, d_args + 2, stream);
+            const int rc = hash_planes_launch(d_buf, n, h_args + 2, stream);
             if (rc) return rc;
         } else {
             h_args[0] = (uint64_t)d_buf, h_args[1] = n;
-            B2L_CUDA(cudaMemcpyAsync(d_args, h_args, 2 * sizeof(uint64_t), cudaMemcpyHostToDevice, stream));
-            const int rc = hash_batch_launch(d_args, d_args + 1, 1, d_args + 2, nullptr, stream);
+            const int rc = hash_batch_launch(h_args, h_args + 1, 1, h_args + 2, nullptr, stream);
             if (rc) return rc;
         }
-        B2L_CUDA(cudaMemcpyAsync(h_args + 2, d_args + 2, sizeof(uint64_t), cudaMemcpyDeviceToHost, stream));
         if (snap) {
             snap->resize(n);
             B2L_CUDA(cudaMemcpyAsync(snap->data(), d_buf, n, cudaMemcpyDeviceToHost, stream));
