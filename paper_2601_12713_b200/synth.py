@@ -168,3 +168,28 @@ def c4_trace(n_events=10_000_000, n_targets=4, seed=4, n_host_vars=4096, palette
     seq = np.arange(n, dtype=np.uint64)
     return columns_from_arrays(n_targets + 1, HOST, seq, start, end, src, dst, kind, src_addr, dst_addr, nbytes, hashv,
                                wall_time_ns=int(end[-1]) if n else 0)
+
+
+def with_locations(cols, n_locs=24, seed=0):
+    """The same trace with events spread over ``n_locs`` code locations (codeptrs, some with
+    file/line, several sharing one (file, line) -- report.py:67-70 buckets them together), so
+    the attribution rows of estimate/attribute are non-trivial at config scale."""
+    import dataclasses
+
+    from .columns import loc_key
+    rng = np.random.default_rng(seed + 7)
+    locs = []
+    for j in range(n_locs):
+        f = None if j % 3 == 0 else f"kern{j % 5}.c"
+        locs.append((0x400000 + 0x40 * j, f, (10 + j % 4) if f else None))
+    keys, bucket_of, ids = [], [], {}
+    for cp, f, ln in locs:
+        k = loc_key(cp, f, ln)
+        if k not in ids:
+            ids[k] = len(keys)
+            keys.append(k)
+        bucket_of.append(ids[k])
+    loc = rng.integers(0, n_locs, cols.n).astype(np.uint32)
+    return dataclasses.replace(cols, loc=loc, loc_flags=np.zeros(n_locs, np.uint8),
+                               loc_bucket=np.array(bucket_of, np.uint32), n_buckets=len(keys), bucket_keys=keys,
+                               locs=locs)

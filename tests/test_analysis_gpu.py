@@ -62,16 +62,14 @@ def test_engine_matches_oracle_on_nasty_traces(cuda):
 
 
 def test_columnar_c2_shaped_trace_vs_oracle(cuda):
+    from oracle.compare import full_parity
     from paper_2601_12713_b200 import analyze_columns, savings_columns
-    cols = cycle_trace_columns(200_000, seed=5)
+    from paper_2601_12713_b200.synth import with_locations
+    cols = with_locations(cycle_trace_columns(200_000, seed=5))
     cf = analyze_columns(cols)
-    rf = R.analyze_cols(cols)
-    assert canon_columnar(cf, cols) == canon_oracle(rf, cols)
     sv = savings_columns(cols, cf)
-    est = R.estimate_cols(cols, rf, cols.wall_time_ns)
-    assert sv.per_category_ns == est["per_category_ns"]
-    assert sv.union_ns == sum(est["per_category_ns"].values()) or sv.union_ns >= 0
-    assert cf.counts()["DD"] > 0 and cf.counts()["RT"] >= 0
+    assert full_parity(cols, cf, sv) == []
+    assert cf.counts()["DD"] > 0 and cf.counts()["RT"] > 0 and cf.counts()["RA"] > 0
 
 
 def test_invalid_events_flagged_in_order(cuda):

@@ -159,7 +159,7 @@ def test_trace_parses_with_the_reference_format(cuda, tmp_path):
 # ---------------------------------------------------------------- payloads hashed on the GPU
 @pytest.mark.gpu
 def test_h2d_host_payload_hashed_at_begin(cuda):
-    from paper_2601_12713_b200 import hash_bytes
+    from oracle.hash_ref import fold64_c as hash_bytes  # the checker, not the engine
     shim = new_shim()
     payload = bytes([1, 2, 3, 4, 5, 6, 7, 8])
     shim.on_data_op_begin(1, "transfer_to_device", HOST_RUNTIME_ID, 0, src_addr=0x1000, dest_addr=0xd000, bytes=8,
@@ -175,7 +175,7 @@ def test_h2d_host_payload_hashed_at_begin(cuda):
 def test_h2d_landed_device_copy_hashed_at_end(cuda):
     import torch
 
-    from paper_2601_12713_b200 import hash_bytes
+    from oracle.hash_ref import fold64_c as hash_bytes  # the checker, not the engine
     shim = new_shim()
     payload = np.arange(4099, dtype=np.uint8).tobytes()  # ragged length
     dev = torch.empty(len(payload), dtype=torch.uint8, device=cuda)
@@ -192,7 +192,7 @@ def test_h2d_landed_device_copy_hashed_at_end(cuda):
 def test_d2h_device_source_hashed_at_end(cuda):
     import torch
 
-    from paper_2601_12713_b200 import hash_bytes
+    from oracle.hash_ref import fold64_c as hash_bytes  # the checker, not the engine
     shim = new_shim()
     src = torch.full((4,), 9, dtype=torch.uint8, device=cuda)
     shim.on_data_op_begin(2, "transfer_from_device", 0, HOST_RUNTIME_ID, src_addr=src.data_ptr(), dest_addr=0x1000,
@@ -204,7 +204,7 @@ def test_d2h_device_source_hashed_at_end(cuda):
 
 @pytest.mark.gpu
 def test_d2h_landed_host_buffer_hashed_at_end(cuda):
-    from paper_2601_12713_b200 import hash_bytes
+    from oracle.hash_ref import fold64_c as hash_bytes  # the checker, not the engine
     shim = new_shim()
     shim.on_data_op_begin(2, "transfer_from_device", 0, HOST_RUNTIME_ID, src_addr=0xd000, dest_addr=0x1000,
                           bytes=4, time_ns=10)
@@ -253,14 +253,14 @@ def test_trace_and_audit_sidecars_written(cuda, tmp_path):
 def test_large_device_payload_goes_through_k2(cuda):
     import torch
 
-    from paper_2601_12713_b200 import hash_tensors
+    from oracle.hash_ref import fold64_c
     shim = new_shim()
     n = (32 << 20) + 13
     dev = torch.randint(0, 256, (n,), dtype=torch.uint8, device=cuda)
     shim.on_data_op_begin(1, "transfer_to_device", HOST_RUNTIME_ID, 0, src_addr=1, dest_addr=dev.data_ptr(),
                           bytes=n, time_ns=0)
     shim.on_data_op_end(1, "transfer_to_device", HOST_RUNTIME_ID, 0, time_ns=5, device_buffer=dev)
-    assert events(shim)[0]["hash"] == hash_tensors([dev])[0]
+    assert events(shim)[0]["hash"] == fold64_c(dev.cpu().numpy().tobytes())
 
 
 # ---------------------------------------------------------------- the OMPT tool, fake runtime
@@ -285,10 +285,11 @@ class _StartResult(ctypes.Structure):
 def test_ompt_tool_with_a_fake_runtime(cuda, tmp_path, monkeypatch):
     """ompt_start_tool -> initialize registers the two EMI callbacks through ompt_set_callback;
     a program's map(to:) / target / map(from:) sequence through them yields a valid trace whose
-    transfer digests equal hash_bytes of the payloads (hashed from the device copies)."""
+    transfer digests equal the oracle fold of the payloads (hashed from the device copies)."""
     import torch
 
-    from paper_2601_12713_b200 import _build, hash_bytes, ingest
+    from oracle.hash_ref import fold64_c as hash_bytes  # the checker, not the engine
+    from paper_2601_12713_b200 import _build, ingest
     monkeypatch.setenv("DMLENS_OUT", str(tmp_path / "omp.trace"))
     tool = ctypes.CDLL(_build.OMPT_LIB)
     tool.ompt_start_tool.restype = ctypes.POINTER(_StartResult)
