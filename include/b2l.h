@@ -288,7 +288,10 @@ int b2l_shard_unpack(const int64_t *d_rows, uint64_t n_rows, uint32_t space, int
  * synchronously in the callback; `host_buffer` only when the runtime offers nothing else
  * (host-to-device at begin, device-to-host at end, capture.ts:210,262).  time_ns = UINT64_MAX:
  * the agent's monotonic clock (origin at create).  Data-op types are OMPT's
- * ompt_target_data_op_t values. */
+ * ompt_target_data_op_t values.  A device buffer is hashed on its own GPU (found with
+ * cudaPointerGetAttributes; one agent stream per device; the caller's current device is kept).
+ * A payload that cannot be hashed never drops the event: it is emitted opaque (bytes 0, hash 0,
+ * counted in hash_skipped), exactly as capture.ts:212-217 records an unreadable one. */
 typedef struct b2l_capture b2l_capture;
 enum { B2L_CAPTURE_BEGIN = 1, B2L_CAPTURE_END = 2 };  /* ompt_scope_begin / ompt_scope_end */
 enum { B2L_OP_ALLOC = 1, B2L_OP_TO_DEVICE = 2, B2L_OP_FROM_DEVICE = 3, B2L_OP_DELETE = 4 };

@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <exception>
 #include <functional>
 #include <future>
 #include <mutex>
@@ -501,7 +502,15 @@ struct StoreOffset {
 // ============================================================ output container
 struct HostSlab;
 struct Internal {
-    Arena arena;  // the call's scratch (first member: released after every buffer carved from it)
+    // the device findings of the call (first member: released after every buffer carved from it).
+    // Sized from the partition counts' upper bounds (~30 B/event at most), so a live findings
+    // object keeps only its results; the call's scratch arena is released when analyze returns.
+    Arena keep;
+    template <class T>
+    void own(DBuf<T> &b, size_t n, cudaStream_t s) {
+        ArenaUse au(&keep);
+        b.alloc(n, s);
+    }
     HostSlab *slab = nullptr;  // pinned host memory behind the b2l_findings arrays
     // device copies of the trace columns (when they were uploaded from host) and their identity
     ColsUpload cols;
@@ -738,8 +747,8 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
     DdRt r;
     const size_t R = 2ull * nH;
     if (nH == 0) {
-        out.dd_off.alloc(1, s), out.dd_off.zero(), out.dd_mem.alloc(1, s);
-        out.rt_off.alloc(1, s), out.rt_off.zero(), out.rt_tx.alloc(1, s), out.rt_rx.alloc(1, s);
+        out.own(out.dd_off, 1, s), out.dd_off.zero(), out.own(out.dd_mem, 1, s);
+        out.own(out.rt_off, 1, s), out.rt_off.zero(), out.own(out.rt_tx, 1, s), out.own(out.rt_rx, 1, s);
         return r;
     }
     PhaseClock pc(s);
@@ -821,12 +830,12 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
                     }, s);
                 }
                 GroupOrder go = order_groups(ng, c.start, first_ev.p, s, tie.p, (uint64_t)nH << db);
-                out.dd_off.alloc(ng + 1, s);
+                out.own(out.dd_off, ng + 1, s);
                 DBuf<uint64_t> total(1, s);
                 scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.dd_off.p}, s, total.p);
                 if (ng) CK(cudaMemcpyAsync(out.dd_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
                 else CK(cudaMemsetAsync(out.dd_off.p, 0, sizeof(uint64_t), s));
-                out.dd_mem.alloc(nrx ? nrx : 1, s);  // members are receptions; count read after the scatter
+                out.own(out.dd_mem, nrx ? nrx : 1, s);  // members are receptions; count read after the scatter
                 // every reception of a grouped segment lands at off[rank] + (its rank within the segment)
                 const uint32_t *sgp = seg_group.p, *rk = go.rank.p, *so = seg_of.p, *rp = rxpos.p;
                 const uint64_t *off = out.dd_off.p;
@@ -886,10 +895,10 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
                     mcount.p, s);
             const uint32_t nt = read_u32(mcount.p, s);
             r.rt_trips = nt;
-            out.rt_tx.alloc(nt ? nt : 1, s);
-            out.rt_rx.alloc(nt ? nt : 1, s);
+            out.own(out.rt_tx, nt ? nt : 1, s);
+            out.own(out.rt_rx, nt ? nt : 1, s);
             if (nt == 0) {
-                out.rt_off.alloc(1, s), out.rt_off.zero();
+                out.own(out.rt_off, 1, s), out.rt_off.zero();
                 return;
             }
             SortStore<1> ts(nt, s);
@@ -933,7 +942,7 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
                 }, s);
             }
             GroupOrder go = order_groups(ng, c.start, first_ev.p, s, tie.p, (uint64_t)nH << (2 * db));
-            out.rt_off.alloc(ng + 1, s);
+            out.own(out.rt_off, ng + 1, s);
             DBuf<uint64_t> total(1, s);
             scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.rt_off.p}, s, total.p);
             CK(cudaMemcpyAsync(out.rt_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
@@ -1010,8 +1019,8 @@ PairOut pairs_step(const DevCols &c, const uint32_t *AD, uint32_t nAD, const uin
                    uint64_t synth_end, Internal &out, cudaStream_t s) {
     PairOut po;
     po.n_pairs = nA;
-    out.pair_alloc.alloc(nA ? nA : 1, s);
-    out.pair_delete.alloc(nA ? nA : 1, s);
+    out.own(out.pair_alloc, nA ? nA : 1, s);
+    out.own(out.pair_delete, nA ? nA : 1, s);
     if (nA) CK(cudaMemcpyAsync(out.pair_alloc.p, A, nA * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     if (nA) CK(cudaMemsetAsync(out.pair_delete.p, 0xFF, nA * sizeof(uint32_t), s));  // synthetic unless matched
     po.warn.alloc(nAD ? nAD : 1, s);
@@ -1109,7 +1118,7 @@ PairOut pairs_step(const DevCols &c, const uint32_t *AD, uint32_t nAD, const uin
 void ra_step(const DevCols &c, uint32_t nP, Internal &out, cudaStream_t s) {
     out.ra_groups = out.ra_members = 0;
     if (nP < 2) {
-        out.ra_off.alloc(1, s), out.ra_off.zero(), out.ra_mem.alloc(1, s);
+        out.own(out.ra_off, 1, s), out.ra_off.zero(), out.own(out.ra_mem, 1, s);
         return;
     }
     const uint32_t *PA = out.pair_alloc.p;
@@ -1145,7 +1154,7 @@ void ra_step(const DevCols &c, uint32_t nP, Internal &out, cudaStream_t s) {
     const uint32_t nseg = cnts[0], ng = cnts[1];
     out.ra_groups = ng;
     if (ng == 0) {
-        out.ra_off.alloc(1, s), out.ra_off.zero(), out.ra_mem.alloc(1, s);
+        out.own(out.ra_off, 1, s), out.ra_off.zero(), out.own(out.ra_mem, 1, s);
         return;
     }
     DBuf<uint32_t> first_ev(ng, s), gsize(ng, s), seg_group(nseg, s);
@@ -1161,11 +1170,11 @@ void ra_step(const DevCols &c, uint32_t nP, Internal &out, cudaStream_t s) {
         }, s);
     }
     GroupOrder go = order_groups(ng, c.start, first_ev.p, s);
-    out.ra_off.alloc(ng + 1, s);
+    out.own(out.ra_off, ng + 1, s);
     DBuf<uint64_t> total(1, s);
     scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.ra_off.p}, s, total.p);
     CK(cudaMemcpyAsync(out.ra_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-    out.ra_mem.alloc(nP, s);  // members <= pairs; the count is read once the scatter is queued
+    out.own(out.ra_mem, nP, s);  // members <= pairs; the count is read once the scatter is queued
     const uint32_t *sgp = seg_group.p, *rk = go.rank.p, *so = seg_of.p;
     const uint64_t *off = out.ra_off.p;
     uint32_t *mem = out.ra_mem.p;
@@ -1303,7 +1312,8 @@ void build_kernel_index(KernelIndexStore &X, const DevCols &c, const uint32_t *T
 void ua_step(const DevCols &c, const KernelIndex &KI, Internal &out, cudaStream_t s) {
     {
         const uint32_t nP = (uint32_t)out.n_pairs;
-        DBuf<uint32_t> ua(nP ? nP : 1, s), uc(1, s);
+        DBuf<uint32_t> ua, uc(1, s);
+        out.own(ua, nP ? nP : 1, s);
         const uint32_t *PA = out.pair_alloc.p, *PD = out.pair_delete.p;
         const int32_t *dst = c.dst;
         const int host = c.host;
@@ -1391,7 +1401,8 @@ void ut_step(const DevCols &c, const KernelIndex &KI, const uint32_t *TT, uint32
             }, s);
         }
     }
-    DBuf<uint32_t> ut(c.n ? c.n : 1, s), utc(1, s);
+    DBuf<uint32_t> ut, utc(1, s);
+    out.own(ut, c.n ? c.n : 1, s);
     const uint8_t *fl = flag.p;
     compact(c.n, [=] __device__(size_t i) { return fl[i] != 0; }, ut.p, utc.p, s);
     out.n_ut = read_u32(utc.p, s);
@@ -1447,6 +1458,21 @@ void stream_after(cudaStream_t to, cudaStream_t from) {
     CK(cudaStreamWaitEvent(to, e, 0));
 }
 
+// Declared right after a call's scratch arena: if the call unwinds with an exception, wait for
+// the side streams before the arena goes back to the pool (kernels queued on them may still read
+// or write scratch carved from it).  On success every chain has already been joined.
+struct SideJoin {
+    int unc = std::uncaught_exceptions();
+    ~SideJoin() {
+        if (std::uncaught_exceptions() <= unc) return;
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return;
+        for (int k = 0; k < 3; ++k)
+            if (cudaStream_t st = g_streamx[k][dev & 63]) cudaStreamSynchronize(st);
+        cudaGetLastError();
+    }
+};
+
 int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_override, b2l_findings **outp) {
     b2l_findings *f = (b2l_findings *)calloc(1, sizeof(b2l_findings));
     if (!f) return fail(B2L_E_OOM, "host allocation failed");
@@ -1467,9 +1493,12 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     const DevCols c = up.d;
     const size_t n = c.n;
     pc.mark("upload");
-    // scratch and device findings of this call come from one arena held by the findings
-    in->arena.open(n <= ARENA_MAX_EVENTS ? ARENA_BASE + n * ARENA_ANALYZE_PER_EVENT : 0, s);
-    ArenaUse arena_use(&in->arena);
+    // this call's scratch: one arena, released when the call returns (the device findings get
+    // their own, smaller arena once the partition counts bound them)
+    Arena arena;
+    SideJoin side_join;
+    arena.open(n <= ARENA_MAX_EVENTS ? ARENA_BASE + n * ARENA_ANALYZE_PER_EVENT : 0, s);
+    ArenaUse arena_use(&arena);
     // ---- 1+2. validation, partition, max end, key-bit masks, start ranks (fused front pass)
     const bool validate = !(flags & B2L_ANALYZE_NO_VALIDATE), raw = (flags & B2L_ANALYZE_RAW_HASHED) != 0;
     const unsigned ftiles = (unsigned)((n + FR_TILE - 1) / FR_TILE);
@@ -1536,6 +1565,10 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     g_masks.srank = srank.p;
 
     pc.mark("partition");
+    {  // upper bounds of the device findings: DD/RT offsets and members <= nH, pairs/RA/UA <= nA, UT <= n
+        const size_t fb = 16 * (nH + 2) + 12 * (size_t)nH + 8 * (nA + 2) + 16 * (size_t)nA + 4 * n + 32 * 256;
+        in->keep.open(n <= ARENA_MAX_EVENTS ? fb : 0, s);
+    }
     in->synth_end = me;
     in->n_pairs = nA;
     // ---- 3-6.  Three independent chains: hash-keyed (DD, RT), pairs -> RA, and the kernel index
@@ -1557,7 +1590,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     EngineErr err2{0, ""}, err3{0, ""};
     bool failed2 = false, failed3 = false, promised = false;
     auto pairs_chain = [&] {
-        ArenaUse au(&in->arena);
+        ArenaUse au(&arena);
         try {
             CK(cudaSetDevice(dev));
             g_masks = masks;
@@ -1580,7 +1613,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
         }
     };
     auto kernel_chain = [&] {
-        ArenaUse au(&in->arena);
+        ArenaUse au(&arena);
         try {
             CK(cudaSetDevice(dev));
             g_masks = masks;
@@ -1655,7 +1688,9 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     if (alloc_stats().on) {
         fprintf(stderr, "[b2l] pool alloc/free calls %llu, host %.3f ms; arena %.1f of %.1f MB (%.0f B/event)\n",
                 (unsigned long long)alloc_stats().n.load(), alloc_stats().ns.load() * 1e-6,
-                in->arena.off.load() / 1048576.0, in->arena.cap / 1048576.0, n ? (double)in->arena.off.load() / n : 0.0);
+                arena.off.load() / 1048576.0, arena.cap / 1048576.0, n ? (double)arena.off.load() / n : 0.0);
+        fprintf(stderr, "[b2l] findings arena %.1f of %.1f MB\n", in->keep.off.load() / 1048576.0,
+                in->keep.cap / 1048576.0);
         alloc_stats().n = 0, alloc_stats().ns = 0;
     }
     if (in->dd_groups == 0) f->dd_offsets[0] = 0;
@@ -1895,6 +1930,7 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     std::lock_guard<std::mutex> lock(g_mu);
     cudaStream_t s = engine_stream();
     Arena arena;  // this call's scratch (declared first: released last)
+    SideJoin side_join;
     arena.open(cols->n_events <= ARENA_MAX_EVENTS ? ARENA_BASE + cols->n_events * ARENA_SAVINGS_PER_EVENT : 0, s);
     ArenaUse arena_use(&arena);
     ColsUpload up;

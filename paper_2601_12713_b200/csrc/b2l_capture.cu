@@ -72,9 +72,13 @@ struct Capture {
     std::vector<Buf *> owned;
     uint64_t unmatched_ends = 0, unfinished_at_exit = 0, hash_skipped = 0, dropped_malformed = 0;
     std::string audit_dir;  // empty: no payload snapshots
-    // device hashing scratch (the agent's own stream)
-    cudaStream_t stream = nullptr;
-    uint64_t *h_args = nullptr;  // pinned [ptr, len, digest], addressed by the kernels in place
+    // device hashing scratch: one stream + pinned argument block per device the agent has seen
+    // (offload programs may map buffers on several GPUs; each buffer is hashed on its own GPU)
+    struct DevScratch {
+        cudaStream_t stream = nullptr;
+        uint64_t *h_args = nullptr;  // pinned [ptr, len, digest], addressed by the kernels in place
+    };
+    std::unordered_map<int, DevScratch> dev_scratch;
     std::mutex hash_mu;
 
     explicit Capture(int32_t host_id) : host_runtime_id(host_id) {
@@ -83,8 +87,10 @@ struct Capture {
     }
     ~Capture() {
         for (auto *b : owned) delete b;
-        if (h_args) cudaFreeHost(h_args);
-        if (stream) cudaStreamDestroy(stream);
+        for (auto &d : dev_scratch) {
+            if (d.second.h_args) cudaFreeHost(d.second.h_args);
+            if (d.second.stream) cudaStreamDestroy(d.second.stream);
+        }
     }
     uint64_t now() const {
         return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() -
@@ -117,27 +123,40 @@ struct Capture {
         b.v.push_back(std::move(e));
     }
 
-    // One device buffer -> digest, on the agent's stream, before returning.
+    // One device buffer -> digest, on the agent's stream of the buffer's own GPU, before returning.
+    // The calling thread's current device is restored on every path.
     int hash_device(const void *d_buf, uint64_t n, uint64_t &digest, std::vector<uint8_t> *snap) {
         std::lock_guard<std::mutex> l(hash_mu);
-        if (!stream) B2L_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-        if (!h_args) B2L_CUDA(cudaMallocHost(&h_args, 3 * sizeof(uint64_t)));
+        cudaPointerAttributes pa{};
+        B2L_CUDA(cudaPointerGetAttributes(&pa, d_buf));
+        if (pa.type != cudaMemoryTypeDevice && pa.type != cudaMemoryTypeManaged)
+            return fail(B2L_E_INVALID_ARG, "capture: device_buffer is not device memory");
+        int prev = 0;
+        B2L_CUDA(cudaGetDevice(&prev));
+        struct Restore {
+            int d;
+            ~Restore() { cudaSetDevice(d); }
+        } restore{prev};
+        B2L_CUDA(cudaSetDevice(pa.device));
+        DevScratch &D = dev_scratch[pa.device];
+        if (!D.stream) B2L_CUDA(cudaStreamCreateWithFlags(&D.stream, cudaStreamNonBlocking));
+        if (!D.h_args) B2L_CUDA(cudaMallocHost(&D.h_args, 3 * sizeof(uint64_t)));
         // (ptr, len) and the digest live in pinned host memory the kernels address directly
         // (unified addressing): no copy launches around the hash
         if (n >= (96ull << 10)) {  // one buffer at a time: K2's floor beats the serial chain here
-            const int rc = hash_planes_launch(d_buf, n, h_args + 2, stream);
+            const int rc = hash_planes_launch(d_buf, n, D.h_args + 2, D.stream);
             if (rc) return rc;
         } else {
-            h_args[0] = (uint64_t)d_buf, h_args[1] = n;
-            const int rc = hash_batch_launch(h_args, h_args + 1, 1, h_args + 2, nullptr, stream);
+            D.h_args[0] = (uint64_t)d_buf, D.h_args[1] = n;
+            const int rc = hash_batch_launch(D.h_args, D.h_args + 1, 1, D.h_args + 2, nullptr, D.stream);
             if (rc) return rc;
         }
         if (snap) {
             snap->resize(n);
-            B2L_CUDA(cudaMemcpyAsync(snap->data(), d_buf, n, cudaMemcpyDeviceToHost, stream));
+            B2L_CUDA(cudaMemcpyAsync(snap->data(), d_buf, n, cudaMemcpyDeviceToHost, D.stream));
         }
-        B2L_CUDA(cudaStreamSynchronize(stream));
-        digest = h_args[2];
+        B2L_CUDA(cudaStreamSynchronize(D.stream));
+        digest = D.h_args[2];
         return B2L_OK;
     }
     int hash_host(const void *h_buf, uint64_t n, uint64_t &digest, std::vector<uint8_t> *snap) {
@@ -152,7 +171,13 @@ struct Capture {
         if (device_buf) rc = hash_device(device_buf, e.bytes, e.hash, snap);
         else if (host_buf) rc = hash_host(host_buf, e.bytes, e.hash, snap);
         else return B2L_OK;
-        if (rc == B2L_OK) e.has_payload = snap != nullptr;
+        if (rc == B2L_OK) {
+            e.has_payload = snap != nullptr;
+        } else {  // no digest: the event is still emitted, opaque (capture.ts:212-217)
+            e.hash = 0;
+            e.payload.clear();
+            e.has_payload = false;
+        }
         return rc;
     }
 };
@@ -287,10 +312,8 @@ int b2l_capture_data_op(b2l_capture *cp, int endpoint, uint64_t host_op_id, int 
         } else if (optype == B2L_OP_TO_DEVICE || optype == B2L_OP_FROM_DEVICE) {
             e.kind = b2l::cap::TRANSFER, e.src_addr = src_addr, e.dst_addr = dst_addr, e.bytes = bytes;
             // host-to-device bytes are complete at begin in host memory; the device copy only at end
-            if (bytes > 0 && host_buffer && optype == B2L_OP_TO_DEVICE && !device_buffer) {
-                const int rc = C.hash_payload(e, nullptr, host_buffer);
-                if (rc) return rc;
-            }
+            if (bytes > 0 && host_buffer && optype == B2L_OP_TO_DEVICE && !device_buffer)
+                C.hash_payload(e, nullptr, host_buffer);  // on failure: opaque at end, never dropped
         } else {
             return b2l::fail(B2L_E_INVALID_ARG, "unknown data-op type");
         }
@@ -312,10 +335,8 @@ int b2l_capture_data_op(b2l_capture *cp, int endpoint, uint64_t host_op_id, int 
         C.pending_ops.erase(it);
     }
     if (e.kind == b2l::cap::TRANSFER) {  // capture.ts:198-219
-        if (e.bytes > 0 && (device_buffer || host_buffer)) {
-            const int rc = C.hash_payload(e, device_buffer, host_buffer);
-            if (rc) return rc;
-        }
+        if (e.bytes > 0 && (device_buffer || host_buffer))
+            C.hash_payload(e, device_buffer, host_buffer);  // on failure: opaque below, never dropped
         if (e.bytes > 0 && e.hash == 0) {  // no content identity: recorded as opaque
             std::lock_guard<std::mutex> l(C.mu);
             ++C.hash_skipped;

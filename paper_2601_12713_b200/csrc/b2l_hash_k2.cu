@@ -18,6 +18,7 @@
 // all predecessors' aggregates itself (a warp reads them in parallel): no serial look-back
 // chain through the grid.  Chunks beyond the co-resident grid are processed in rounds chained
 // through a per-group carry.  Verified bit-exact against the serial fold (tests).
+#include <mutex>
 #include <cooperative_groups.h>
 
 #include "b2l_common.cuh"
@@ -310,11 +311,18 @@ __global__ void __launch_bounds__(THREADS, 4) k_hash_planes(const uint8_t *__res
     }
 }
 
+// Per-device K2 state.  The status/carry scratch is shared by every K2 launch on the device,
+// whatever stream it is queued on (hash_tensors on the caller's stream, b2l_hash_host's
+// pipeline, the capture agent), so launches are chained: each new call's stream first waits
+// on the event recorded after the previous launch, then resets the scratch.  This also keeps
+// two whole-GPU cooperative grids from ever being resident at once.
 struct Ctx {
     int grid = 0;
     uint4 *status = nullptr;
     unsigned long long *carry = nullptr;
     size_t status_cap = 0, carry_cap = 0;
+    std::mutex mu;
+    cudaEvent_t done = nullptr;  // recorded after the last K2 launch on this device
 };
 Ctx g_ctx[64];
 
@@ -346,6 +354,9 @@ int hash_planes_launch(const void *d_buf, uint64_t nbytes, uint64_t *d_digest, c
     k2::Ctx &C = k2::g_ctx[dev & 63];
     const int grid = k2_grid();
     if (grid < 1) return fail(B2L_E_CUDA, "k_hash_planes: no occupancy");
+    std::lock_guard<std::mutex> lock(C.mu);
+    if (!C.done) B2L_CUDA(cudaEventCreateWithFlags(&C.done, cudaEventDisableTiming));
+    B2L_CUDA(cudaStreamWaitEvent(stream, C.done, 0));  // the previous K2 is done with the scratch
     const uint64_t nw = (nbytes + 7) >> 3;
     const uint64_t nchunks = (nw + k2::CHUNK - 1) / k2::CHUNK;
     // one team per co-resident CTA per SM when there is a full grid of chunks, else one team
@@ -357,14 +368,20 @@ int hash_planes_launch(const void *d_buf, uint64_t nbytes, uint64_t *d_digest, c
     const uint64_t rounds = (nchunks + team - 1) / team;
     const size_t need_st = rounds * 16 * team, need_c = rounds * 16;
     if (C.status_cap < need_st) {
-        if (C.status) cudaFree(C.status);
+        if (C.status) {
+            B2L_CUDA(cudaEventSynchronize(C.done));
+            cudaFree(C.status);
+        }
         C.status = nullptr;
         C.status_cap = 0;
         B2L_CUDA(cudaMalloc(&C.status, need_st * sizeof(uint4)));
         C.status_cap = need_st;
     }
     if (C.carry_cap < need_c) {
-        if (C.carry) cudaFree(C.carry);
+        if (C.carry) {
+            B2L_CUDA(cudaEventSynchronize(C.done));
+            cudaFree(C.carry);
+        }
         C.carry = nullptr;
         C.carry_cap = 0;
         B2L_CUDA(cudaMalloc(&C.carry, need_c * sizeof(unsigned long long)));
@@ -377,6 +394,7 @@ int hash_planes_launch(const void *d_buf, uint64_t nbytes, uint64_t *d_digest, c
                     (void *)&teams};
     B2L_CUDA(cudaLaunchCooperativeKernel((const void *)k2::k_hash_planes, dim3((unsigned)g), dim3(k2::THREADS), args,
                                          k2::SMEM, stream));
+    B2L_CUDA(cudaEventRecord(C.done, stream));
     return B2L_OK;
 }
 

@@ -250,6 +250,22 @@ def test_trace_and_audit_sidecars_written(cuda, tmp_path):
 
 
 @pytest.mark.gpu
+def test_unhashable_device_buffer_still_emitted_opaque(cuda):
+    """A hashing failure (here: a 'device' pointer that is plain host memory) never drops the
+    transfer: it is emitted opaque and counted, as capture.ts:212-217 records an unreadable one."""
+    shim = new_shim()
+    host = np.full(64, 3, dtype=np.uint8)
+    shim.on_data_op_begin(1, "transfer_to_device", HOST_RUNTIME_ID, 0, src_addr=1, dest_addr=0xd000, bytes=64,
+                          time_ns=0)
+    shim.on_data_op_end(1, "transfer_to_device", HOST_RUNTIME_ID, 0, time_ns=5,
+                        device_buffer=int(host.ctypes.data))
+    evs = events(shim)
+    assert len(evs) == 1 and evs[0]["kind"] == "transfer"
+    assert evs[0]["bytes"] == 0 and evs[0]["hash"] == 0
+    assert shim.warnings.hash_skipped == 1
+
+
+@pytest.mark.gpu
 def test_large_device_payload_goes_through_k2(cuda):
     import torch
 
