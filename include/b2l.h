@@ -95,9 +95,13 @@ int b2l_audit_batch(const uint64_t *d_hashes, const uint64_t *d_ptrs, const uint
 
 /* Native NDJSON ingest (traceio.py:153-191 wire format).  Parses the header and every
  * event record into columns (input order, not yet sorted or validated) over `threads`
- * host threads.  If any line is not a record the reference accepts without error,
- * err_line names the first such line (1-based) and no columns are returned: the caller
- * reproduces the reference's exception for it.  Free with b2l_ingest_free. */
+ * host threads.  If any line is not a record the parser can vouch the reference accepts
+ * without error, no columns are returned: err_line names the first such line (1-based) and
+ * err_lines[0..n_err_lines) lists them (ascending; a header it cannot vouch for is listed
+ * alone, body lines up to 64k per thread chunk).  The caller checks those lines the
+ * reference's way (traceio.py:153-181): the first bad one raises the reference's exception,
+ * unusual-but-valid ones are rewritten canonically and the input is parsed again.
+ * Free with b2l_ingest_free. */
 typedef struct b2l_ingest {
     uint64_t err_line;            /* 0 = every line accepted */
     uint64_t header_line;         /* 0 = no header line found */
@@ -112,10 +116,26 @@ typedef struct b2l_ingest {
     const int64_t *loc_line;      /* -1 = None */
     const uint64_t *loc_file_off; /* into strings; UINT64_MAX = None */
     const uint32_t *loc_file_len;
-    const char *strings;          /* UTF-8 file names */
+    const char *strings;          /* UTF-8 file names (lone surrogates in their 3-byte form) */
+    uint64_t n_err_lines;
+    const uint64_t *err_lines;
 } b2l_ingest;
 int b2l_ingest_ndjson(const char *data, uint64_t len, int threads, b2l_ingest **out);
 void b2l_ingest_free(b2l_ingest *p);
+
+/* serialize_trace (traceio.py:193-237) over HOST columns: `header` is the caller's rendered
+ * header line (with its '\n'); every event then becomes
+ *   {"seq":..,"kind":"..","t0":..,"t1":..,"src_dev":..,"dst_dev":..,"src_addr":..,"dst_addr":..,
+ *    "bytes":..,"hash":..<suffix of its location>\n
+ * where suffix_data[suffix_off[l] .. suffix_off[l+1]) is location l's pre-rendered tail
+ * ',"codeptr":N[,"file":"<json-escaped>","line":L]}' (the only string data; escaped once per
+ * location by the caller).  Events are written in column order over `threads` host threads.
+ * The caller validates first (the reference refuses invalid traces).  *text is malloc'ed:
+ * free with b2l_serialize_free. */
+int b2l_serialize_ndjson(const struct b2l_trace_cols *cols, const char *header, uint64_t header_len,
+                         const char *suffix_data, const uint64_t *suffix_off, int threads, char **text,
+                         uint64_t *len);
+void b2l_serialize_free(char *text);
 
 /* Stable sort of n (k0, k1) u64 key pairs (host arrays): out_perm = sorting permutation
  * (parse_trace's events.sort(key=(start_ns, seq)), traceio.py:183). */

@@ -1,7 +1,11 @@
 """Columnar command line (mirrors `dmlens analyze` / `dmlens audit`, cli.py:41-93, 126-236):
 
   python -m paper_2601_12713_b200 analyze TRACE [--json] [--min-bytes N] [--strict-pseudocode] [-q] [-v]
-  python -m paper_2601_12713_b200 audit TRACE PAYLOAD_DIR [-q] [-v]
+  python -m paper_2601_12713_b200 audit TRACE --payload-dir DIR [-q] [-v]
+  python -m paper_2601_12713_b200 version
+
+`analyze --oracle` (the reference's brute-force cross-check, cli.py:57-58,145-152) is
+rejected with an explicit message: the brute-force oracles are test infrastructure here.
 
 NDJSON is parsed natively (ingest.py), analysed on the GPU, filtered / summed /
 rendered from columns (reporting.py) -- no per-event Python objects.  Exit codes
@@ -23,15 +27,18 @@ def _parser():
     a = sub.add_parser("analyze")
     a.add_argument("trace")
     a.add_argument("--json", action="store_true")
-    a.add_argument("--min-bytes", type=int, default=0)
+    a.add_argument("--min-bytes", type=int, default=1)  # cli.py:61-63 (1 keeps everything)
+    a.add_argument("--oracle", action="store_true")
     a.add_argument("--strict-pseudocode", action="store_true")
     a.add_argument("-q", "--quiet", action="store_true")
     a.add_argument("-v", "--verbose", action="store_true")
     u = sub.add_parser("audit")
     u.add_argument("trace")
-    u.add_argument("payload_dir")
+    u.add_argument("payload_dir_pos", nargs="?", default=None, help=argparse.SUPPRESS)  # r01 positional form
+    u.add_argument("--payload-dir", dest="payload_dir", default=None)  # cli.py:84-87
     u.add_argument("-q", "--quiet", action="store_true")
     u.add_argument("-v", "--verbose", action="store_true")
+    sub.add_parser("version")
     return ap
 
 
@@ -56,6 +63,10 @@ def _load(path, validate=True):
 
 
 def cmd_analyze(args) -> int:
+    if args.oracle:
+        print("dmlens: error: --oracle is not supported by the B200 engine CLI (run `dmlens analyze --oracle`)",
+              file=sys.stderr)
+        return EXIT_INTERNAL
     from .analysis import analyze_columns
     from .reporting import build_report, filter_min_bytes, render_json, render_text
     from .analysis import EngineInvalid
@@ -84,6 +95,10 @@ def cmd_analyze(args) -> int:
 
 def cmd_audit(args) -> int:
     from pathlib import Path
+    args.payload_dir = args.payload_dir or args.payload_dir_pos
+    if args.payload_dir is None:
+        print("dmlens audit: error: the following arguments are required: --payload-dir", file=sys.stderr)
+        return EXIT_INTERNAL
 
     from .hashing import audit_payloads
     cols = _load(args.trace)
@@ -109,10 +124,16 @@ def cmd_audit(args) -> int:
     return EXIT_OK
 
 
+def cmd_version(args) -> int:
+    from . import __version__
+    print(f"dmlens {__version__}")
+    return EXIT_OK
+
+
 def main(argv=None) -> int:
     args = _parser().parse_args(argv)
     try:
-        return {"analyze": cmd_analyze, "audit": cmd_audit}[args.cmd](args)
+        return {"analyze": cmd_analyze, "audit": cmd_audit, "version": cmd_version}[args.cmd](args)
     except Exception as exc:  # noqa: BLE001 - the reference maps every internal failure to exit 2
         print(f"dmlens: internal error: {type(exc).__name__}: {exc}", file=sys.stderr)
         return EXIT_INTERNAL

@@ -2,12 +2,14 @@
 // (traceio.py:153-191, wire format traceio.py:1-23) reads ~0.07 M events/s in Python.
 // This parser splits the input at line boundaries over host threads and turns every
 // well-formed record straight into SoA columns plus a deduplicated location table.
-// It accepts exactly the records the reference accepts without error and stops at the
-// first line it cannot vouch for (any JSON or field-rule irregularity); the Python layer
-// then reproduces the reference's exact exception for that line (or parses the input
-// the slow way when the line turns out fine).  Sorting by (t0, seq) and validation run
-// on the GPU afterwards.
+// It accepts exactly the records the reference accepts without error and lists every line
+// it cannot vouch for (any JSON or field-rule irregularity, up to 64k per chunk) without
+// returning columns; the Python layer checks just those lines the reference's way --
+// raising its exact exception for the first bad one, or rewriting an unusual-but-valid
+// line in canonical form -- and calls the parser again on the patched input.  Sorting by
+// (t0, seq) and validation run on the GPU afterwards.
 #include <algorithm>
+#include <charconv>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -46,8 +48,9 @@ struct Chunk {
     std::vector<uint32_t> loc;   // chunk-local loc ids
     std::vector<Loc> locs;
     std::unordered_map<Loc, uint32_t, LocHash> loc_ids;
-    uint64_t err_line = 0;       // first rejected line (1-based), 0 = none
+    std::vector<uint64_t> err_lines;  // lines the parser cannot vouch for (1-based, ascending)
 };
+constexpr size_t MAX_ERR_LINES = size_t(1) << 16;  // per chunk and call; the caller re-parses after patching
 
 // ------------------------------------------------------------------ a strict JSON scanner
 struct Scan {
@@ -113,16 +116,17 @@ struct Scan {
                 case 'u': {
                     uint32_t v;
                     if (!hex4(v)) return false;
-                    if (v >= 0xD800 && v < 0xDC00) {  // surrogate pair, or a lone surrogate: let Python decide
+                    if (v >= 0xD800 && v < 0xDC00 && e - p >= 6 && p[0] == '\\' && p[1] == 'u') {
+                        // a surrogate pair combines as Python's json does; anything else after a
+                        // high surrogate leaves it lone (and is read as its own escape next)
+                        const char *save = p;
                         uint32_t lo;
-                        if (e - p < 6 || p[0] != '\\' || p[1] != 'u') return false;
                         p += 2;
-                        if (!hex4(lo) || lo < 0xDC00 || lo >= 0xE000) return false;
-                        v = 0x10000 + ((v - 0xD800) << 10) + (lo - 0xDC00);
-                    } else if (v >= 0xDC00 && v < 0xE000) {
-                        return false;
+                        if (hex4(lo) && lo >= 0xDC00 && lo < 0xE000) v = 0x10000 + ((v - 0xD800) << 10) + (lo - 0xDC00);
+                        else p = save;
                     }
-                    if (v == 0) return false;  // keep NULs out of names (Python path handles them)
+                    // lone surrogates are kept as their 3-byte form (Python decodes the names
+                    // with "surrogatepass"), NULs as a 0 byte: names carry explicit lengths
                     put_utf8(o, v);
                     break;
                 }
@@ -438,8 +442,11 @@ void parse_range(const char *data, size_t lo, size_t hi, uint64_t first_line, Ch
             } else {
                 Loc loc{0, -1, false, std::string()};
                 if (!parse_event(b, e, v, kind, loc)) {
-                    ck.err_line = line_no;
-                    return;
+                    ck.err_lines.push_back(line_no);
+                    if (ck.err_lines.size() >= MAX_ERR_LINES) return;
+                    i = j + 1;
+                    ++line_no;
+                    continue;
                 }
                 id = loc_id(loc);
             }
@@ -466,6 +473,7 @@ struct b2l_ingest_impl {
     std::vector<uint64_t> loc_file_off;
     std::vector<uint32_t> loc_file_len;
     std::string strings;
+    std::vector<uint64_t> err_lines;
 };
 
 extern "C" {
@@ -526,6 +534,9 @@ int b2l_ingest_ndjson(const char *data, uint64_t len, int threads, b2l_ingest **
             if (sc.p != sc.e) ok = false;
             if (!ok || !have_v || R->pub.version != 1 || !have_nd || !have_h) {
                 R->pub.err_line = line_no;
+                R->err_lines.push_back(line_no);
+                R->pub.n_err_lines = 1;
+                R->pub.err_lines = R->err_lines.data();
                 return B2L_OK;
             }
             body = j + 1 <= len ? j + 1 : len;
@@ -568,11 +579,16 @@ int b2l_ingest_ndjson(const char *data, uint64_t len, int threads, b2l_ingest **
         for (int t = 0; t < T; ++t) th.emplace_back([&, t] { parse_range(data, cut[t], cut[t + 1], first[t], ck[t]); });
         for (auto &x : th) x.join();
     }
-    for (int t = 0; t < T; ++t)
-        if (ck[t].err_line) {
-            R->pub.err_line = ck[t].err_line;
-            return B2L_OK;
-        }
+    for (int t = 0; t < T; ++t) {  // a chunk that stopped at the cap ends the list: nothing after it was read
+        R->err_lines.insert(R->err_lines.end(), ck[t].err_lines.begin(), ck[t].err_lines.end());
+        if (ck[t].err_lines.size() >= MAX_ERR_LINES) break;
+    }
+    if (!R->err_lines.empty()) {
+        R->pub.err_line = R->err_lines[0];
+        R->pub.n_err_lines = R->err_lines.size();
+        R->pub.err_lines = R->err_lines.data();
+        return B2L_OK;
+    }
     // ---- merge chunks; global location ids
     size_t n = 0;
     for (auto &c : ck) n += c.kind.size();
@@ -623,5 +639,77 @@ void b2l_ingest_free(b2l_ingest *p) {
     if (!p) return;
     delete reinterpret_cast<b2l_ingest_impl *>(p);  // pub is the first member
 }
+
+// serialize_trace's body (traceio.py:193-237): every event as one canonical line, in the given
+// order, over host threads: lengths per chunk first, then each chunk writes its own slice.
+int b2l_serialize_ndjson(const b2l_trace_cols *c, const char *header, uint64_t header_len, const char *suffix_data,
+                         const uint64_t *suffix_off, int threads, char **text, uint64_t *len) {
+    if (!c || !text || !len || (header_len && !header) || (c->n_locs && (!suffix_data || !suffix_off)))
+        return b2l::fail(B2L_E_INVALID_ARG, "null argument");
+    if (c->device_resident) return b2l::fail(B2L_E_INVALID_ARG, "b2l_serialize_ndjson needs host columns");
+    const uint64_t n = c->n_events;
+    for (uint64_t i = 0; i < n; ++i)
+        if (c->loc[i] >= c->n_locs || c->kind[i] > 3) return b2l::fail(B2L_E_INVALID_ARG, "bad kind or location id");
+    static const char *kname[4] = {"transfer", "alloc", "delete", "kernel"};
+    // one event line; writes at most 11 keys + 9 u64 + 2 i32 + the suffix
+    auto line = [&](uint64_t i, char *o) -> size_t {
+        char *p = o;
+        auto lit = [&](const char *s, size_t k) { memcpy(p, s, k), p += k; };
+        auto u = [&](uint64_t v) { p = std::to_chars(p, p + 20, v).ptr; };
+        auto d = [&](int32_t v) { p = std::to_chars(p, p + 11, v).ptr; };
+        lit("{\"seq\":", 7), u(c->seq[i]);
+        lit(",\"kind\":\"", 9);
+        const char *k = kname[c->kind[i]];
+        lit(k, strlen(k));
+        lit("\",\"t0\":", 7), u(c->start_ns[i]);
+        lit(",\"t1\":", 6), u(c->end_ns[i]);
+        lit(",\"src_dev\":", 11), d(c->src_device[i]);
+        lit(",\"dst_dev\":", 11), d(c->dst_device[i]);
+        lit(",\"src_addr\":", 12), u(c->src_addr[i]);
+        lit(",\"dst_addr\":", 12), u(c->dst_addr[i]);
+        lit(",\"bytes\":", 9), u(c->bytes[i]);
+        lit(",\"hash\":", 8), u(c->hash[i]);
+        const uint32_t l = c->loc[i];
+        lit(suffix_data + suffix_off[l], suffix_off[l + 1] - suffix_off[l]);  // ,"codeptr":..[,"file":..,"line":..]}
+        *p++ = '\n';
+        return (size_t)(p - o);
+    };
+    uint64_t max_suffix = 0;
+    for (uint32_t l = 0; l < c->n_locs; ++l) max_suffix = std::max(max_suffix, suffix_off[l + 1] - suffix_off[l]);
+    const size_t bound = 256 + max_suffix;  // per line
+    if (threads < 1) threads = 1;
+    const int T = (int)std::min<uint64_t>((uint64_t)threads, std::max<uint64_t>(1, n / 65536));
+    std::vector<uint64_t> lo(T + 1);
+    for (int t = 0; t <= T; ++t) lo[t] = n * (uint64_t)t / (uint64_t)T;
+    std::vector<std::string> part(T);
+    {
+        std::vector<std::thread> th;
+        for (int t = 0; t < T; ++t)
+            th.emplace_back([&, t] {
+                std::string &o = part[t];
+                o.resize((size_t)(lo[t + 1] - lo[t]) * 160 + bound);
+                size_t w = 0;
+                for (uint64_t i = lo[t]; i < lo[t + 1]; ++i) {
+                    if (o.size() - w < bound) o.resize(o.size() * 2 + bound);
+                    w += line(i, &o[w]);
+                }
+                o.resize(w);
+            });
+        for (auto &x : th) x.join();
+    }
+    size_t total = header_len;
+    for (auto &p : part) total += p.size();
+    char *out = (char *)malloc(total + 1);
+    if (!out) return b2l::fail(B2L_E_OOM, "host allocation failed");
+    memcpy(out, header, header_len);
+    size_t w = header_len;
+    for (auto &p : part) memcpy(out + w, p.data(), p.size()), w += p.size();
+    out[total] = 0;
+    *text = out;
+    *len = total;
+    return B2L_OK;
+}
+
+void b2l_serialize_free(char *text) { free(text); }
 
 }  // extern "C"

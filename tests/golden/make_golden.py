@@ -50,7 +50,7 @@ def hash_fixture():
     return out
 
 
-if __name__ == "__main__" and not set(sys.argv) & {"--analysis", "--standalone", "--ingest", "--reports"}:
+if __name__ == "__main__" and not set(sys.argv) & {"--analysis", "--standalone", "--ingest", "--reports", "--serialize"}:
     with open(os.path.join(HERE, "hash_vectors.json"), "w") as f:
         json.dump(hash_fixture(), f, indent=0)
     print("wrote hash_vectors.json")
@@ -322,3 +322,55 @@ if __name__ == "__main__" and "--reports" in sys.argv:
     with gzip.open(os.path.join(HERE, "report_cases.json.gz"), "wt") as f:
         json.dump(report_fixture(), f)
     print("wrote report_cases.json.gz")
+
+
+# ----------------------------------------------------------------------------- serialize_trace
+def serialize_fixture():
+    """traceio.serialize_trace (traceio.py:193-237) outputs of the unmodified reference: random
+    traces, synth patterns, location edge cases (non-ASCII / escaped / surrogate file names,
+    line without file), and the invalid traces it refuses."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("ref_conftest", os.path.join(os.path.dirname(REF), "tests",
+                                                                               "conftest.py"))
+    conf = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(conf)
+    from dmlens.model import EventKind, Trace
+    from dmlens.synth import PATTERNS, PatternSpec, generate
+    from dmlens.traceio import InvalidTrace, serialize_trace
+    cases = []
+
+    def add(name, tr):
+        c = {"name": name, "trace": _trace_json(tr)}
+        try:
+            c["text"] = serialize_trace(tr).decode("utf-8")
+        except InvalidTrace as exc:
+            c["error"] = [type(exc).__name__, str(exc), [[v.rule, v.message, v.seq] for v in exc.violations]]
+        cases.append(c)
+    for seed in range(40):
+        tr = conf.random_trace(seed)
+        if seed % 2 == 0 and tr.wall_time_ns is None:
+            tr.wall_time_ns = tr.wall_time()
+        add(f"random_trace({seed})", tr)
+    for pat in PATTERNS:
+        tr, _ = generate(PatternSpec(pattern=pat, n_iterations=3, n_devices=3, seed=5))
+        add(f"synth({pat})", tr)
+    mk = conf.make_event
+    evs = [mk(0, EventKind.KERNEL, 0, 1, src=1, dst=1, codeptr=7, file="café.c", line=3),
+           mk(1, EventKind.KERNEL, 1, 2, src=1, dst=1, codeptr=8, file='q"uo\\te\n\t.c', line=4),
+           mk(2, EventKind.KERNEL, 2, 3, src=1, dst=1, codeptr=9, file="\U0001F600\ud800x\x00y", line=5),
+           mk(3, EventKind.KERNEL, 3, 4, src=1, dst=1, codeptr=2**64 - 1, line=6),
+           mk(4, EventKind.TRANSFER, 4, 9, src=0, dst=1, nbytes=2**64 - 1, hash=2**64 - 1, src_addr=2**64 - 1,
+              dst_addr=1)]
+    add("locations", Trace(1, 2, 0, 2**64 - 1, evs))
+    add("empty", Trace(1, 3, 0, None, []))
+    add("invalid:host", Trace(1, 2, 9, None, []))
+    add("invalid:version", Trace(2, 2, 0, None, []))
+    add("invalid:inverted", Trace(1, 2, 0, None, [mk(0, EventKind.TRANSFER, 10, 5, hash=1, nbytes=8)]))
+    return cases
+
+
+if __name__ == "__main__" and "--serialize" in sys.argv:
+    import gzip
+    with gzip.open(os.path.join(HERE, "serialize_cases.json.gz"), "wt") as f:
+        json.dump(serialize_fixture(), f)
+    print("wrote serialize_cases.json.gz")
