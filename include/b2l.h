@@ -299,6 +299,23 @@ int b2l_shard_route(const b2l_trace_cols *cols, uint32_t n_ranks, uint64_t base,
 int b2l_shard_unpack(const int64_t *d_rows, uint64_t n_rows, uint32_t space, int64_t *const *d_cols,
                      uint64_t *n_out);
 
+/* ---------------------------------------------------------------- multi-GPU (one process)
+ * SURVEY 8(b)/8(e).  b2l_init(ngpus, devs): the devices this process drives (devs NULL:
+ * 0..ngpus-1; a device may repeat, e.g. for tests on one GPU); b2l_shutdown drains them.  The
+ * single-device entry points keep using the calling thread's current device. */
+int b2l_init(int ngpus, const int *devs);
+int b2l_shutdown(void);
+/* number of initialised devices (*n) and up to `cap` of their ordinals */
+int b2l_ngpus(int *n, int *devs, int cap);
+/* Placement of n buffers on `parts` devices by LPT (longest first, each to the least-loaded
+ * part; ties to the lowest part, equal lengths in index order): owner[i] in [0, parts),
+ * load[p] = bytes placed on part p (optional).  Host arrays. */
+int b2l_lpt_partition(const uint64_t *lens, uint64_t n, uint32_t parts, uint32_t *owner, uint64_t *load);
+/* b2l_hash_host over every initialised device: contiguous byte-balanced ranges of the batch, one
+ * host thread per device (its own pipeline and PCIe link), digests written in place into
+ * h_digests.  Same contract as b2l_hash_host (hashing.py:34-67 per buffer). */
+int b2l_hash_host_multi(const void *const *h_bufs, const uint64_t *h_lens, uint64_t n, uint64_t *h_digests);
+
 /* ---------------------------------------------------------------- capture agent
  * Native model of the reference's OMPT capture shim (SPEC.md "ompt-shim",
  * pkg/shim/src/capture.ts:93-327): paired begin/end callbacks -> trace events, per-thread

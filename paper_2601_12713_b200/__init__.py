@@ -12,7 +12,7 @@ from .hashing import (CollisionAuditStore, HashFn, audit_observe, hash_batch, ha
 from .analysis import (ColumnarFindings, ColumnarSavings, analyze, analyze_columns, attribute, estimate,
                        savings_columns)
 from .columns import Columns, columns_from_arrays, to_columns
-from . import ingest, reporting, sharded, synth  # noqa: F401  (submodules of the public API)
+from . import ingest, multigpu, reporting, sharded, synth  # noqa: F401  (submodules of the public API)
 from .standalone import (find_duplicate_transfers, find_repeated_allocs, find_round_trips, find_unused_allocs,
                          find_unused_transfers, get_alloc_delete_pairs, sort_by_device, validate)
 

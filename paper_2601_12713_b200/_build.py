@@ -11,7 +11,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libb2l.so")
 SOURCES = ["b2l_api.cu", "b2l_hash.cu", "b2l_hash_k2.cu", "b2l_analyze.cu", "b2l_audit.cu", "b2l_ingest.cpp",
-           "b2l_capture.cu"]
+           "b2l_capture.cu", "b2l_multi.cu"]
 OMPT_LIB = os.path.join(PKG, "libb2l_ompt.so")  # OMPT tool glue over libb2l's capture ABI
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

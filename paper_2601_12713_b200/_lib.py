@@ -34,6 +34,8 @@ EXPORTED = (
     "b2l_capture_create", "b2l_capture_destroy", "b2l_capture_set_audit_dir", "b2l_capture_device_slot",
     "b2l_capture_target", "b2l_capture_data_op", "b2l_capture_finalize", "b2l_capture_free_text",
     "b2l_capture_write", "b2l_capture_warnings",
+    "b2l_init", "b2l_shutdown", "b2l_ngpus", "b2l_lpt_partition", "b2l_hash_host_multi",
+    "b2l_serialize_ndjson", "b2l_serialize_free", "b2l_ingest_ndjson", "b2l_ingest_free",
 )
 
 _u64 = ctypes.c_uint64
@@ -57,6 +59,11 @@ def _declare(lib):
         "b2l_hash_select_variant": ([_int, ctypes.POINTER(_int)], _int),
         "b2l_hash_large": ([_p, _u64, _p, _p], _int),
         "b2l_hash_launch_info": ([_u64, ctypes.POINTER(_int), ctypes.POINTER(_int), ctypes.POINTER(_int)], _int),
+        "b2l_init": ([_int, ctypes.POINTER(_int)], _int),
+        "b2l_shutdown": ([], _int),
+        "b2l_ngpus": ([ctypes.POINTER(_int), ctypes.POINTER(_int), _int], _int),
+        "b2l_lpt_partition": ([_p, _u64, ctypes.c_uint32, _p, _p], _int),
+        "b2l_hash_host_multi": ([_p, _p, _u64, _p], _int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

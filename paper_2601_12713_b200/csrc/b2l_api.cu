@@ -48,7 +48,7 @@ int fill_payloads_launch(uint8_t *, const uint64_t *, const uint64_t *, const ui
 // ------------------------------------------------------------------ host pipeline
 // Double-buffered device ring: batch b's host->device copy (side stream) overlaps
 // batch b-1's hashing (compute stream).  Contiguous host buffers are merged into
-// one DMA.  One pipeline per device, serialized by a mutex.
+// one DMA.  One pipeline per device, serialized by that device's mutex.
 namespace {
 
 constexpr uint64_t RING_SLOT_BYTES = 512ull << 20;
@@ -80,7 +80,7 @@ struct HostPipe {
 constexpr uint64_t SMALL_MAX_BUFS = 64, SMALL_BYTES = 64ull << 10, ZERO_COPY_BYTES = 4096;
 constexpr uint64_t SMALL_META = 16 * SMALL_MAX_BUFS, SMALL_CAP = SMALL_META + SMALL_BYTES + 8 * SMALL_MAX_BUFS;
 
-std::mutex g_pipe_mu;
+std::mutex g_pipe_mu[64];  // one per device: pipelines of different GPUs run concurrently
 HostPipe g_pipes[64];
 
 int ensure_slot(Slot &s, uint64_t data_bytes, uint64_t nbuf) {
@@ -161,7 +161,7 @@ int hash_host_impl(const void *const *h_bufs, const uint64_t *h_lens, uint64_t n
     int dev = 0;
     B2L_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64) return fail(B2L_E_INVALID_ARG, "device ordinal out of range");
-    std::lock_guard<std::mutex> lock(g_pipe_mu);
+    std::lock_guard<std::mutex> lock(g_pipe_mu[dev]);
     HostPipe &P = g_pipes[dev];
     if (!P.copy) {
         B2L_CUDA(cudaStreamCreateWithFlags(&P.copy, cudaStreamNonBlocking));

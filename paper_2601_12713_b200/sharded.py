@@ -93,6 +93,15 @@ class LocalComm:
     def gather0_findings(self, out: dict):
         return self.gather0(out)
 
+    def gatherv(self, t, dst: int = 0):
+        """Tensors of any length (same trailing shape) -> their concatenation in rank order on
+        `dst` (None elsewhere); stays on the tensors' device."""
+        import torch
+        if t.is_cuda:  # another thread's stream reads it next
+            torch.cuda.current_stream(t.device).synchronize()
+        allp = self._exchange(t)
+        return torch.cat(allp) if self.rank == dst else None
+
 
 class TorchComm:
     """torch.distributed communicator (NCCL for CUDA tensors, gloo on CPU)."""
@@ -157,6 +166,28 @@ class TorchComm:
         out = [None] * self.size if self.rank == 0 else None
         self.dist.gather_object(obj, out, dst=0)
         return out
+
+    def gatherv(self, t, dst: int = 0):
+        """Exact-size gather: tensors of any length (same trailing shape) -> their concatenation in
+        rank order on `dst` (None elsewhere).  One size all-gather, then one all_to_all_single in
+        which only `dst` receives (NCCL moves device memory; no padding)."""
+        torch, dist = self.torch, self.dist
+        width = int(np.prod(t.shape[1:])) if t.dim() > 1 else 1
+        n = torch.tensor([t.shape[0]], dtype=torch.int64, device=self.device)
+        ns = [torch.empty_like(n) for _ in range(self.size)]
+        dist.all_gather(ns, n)
+        sizes = [int(x.item()) for x in ns]
+        send = t if t.device.type == self.device.type else t.to(self.device)
+        send = send.contiguous().view(-1)
+        rows = sum(sizes) if self.rank == dst else 0
+        recv = torch.empty(rows * width, dtype=t.dtype, device=self.device)
+        in_split = [t.shape[0] * width if r == dst else 0 for r in range(self.size)]
+        out_split = [sz * width if self.rank == dst else 0 for sz in sizes]
+        dist.all_to_all_single(recv, send, out_split, in_split)
+        if self.rank != dst:
+            return None
+        recv = recv.view(rows, *t.shape[1:]) if t.dim() > 1 else recv
+        return recv if recv.device == t.device else recv.to(t.device)
 
     def gather0_findings(self, out: dict):
         """Per-rank findings (dict of numpy arrays / tuples of arrays) to rank 0 as ONE flat int64
