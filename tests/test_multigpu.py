@@ -102,7 +102,7 @@ def _payload_slab(lens, seed, dev):
     from oracle import hash_ref  # the checker: payload bytes and digests
     offs = np.zeros(len(lens), np.int64)
     if len(lens) > 1:
-        offs[1:] = np.cumsum((np.asarray(lens, np.int64) + 255) // 256 * 256)[:-1] + np.arange(1, len(lens)) % 16
+        offs[1:] = np.cumsum((np.asarray(lens, np.int64) + 16 + 255) // 256 * 256)[:-1] + np.arange(1, len(lens)) % 16
     host = np.zeros(int(offs[-1] + lens[-1]) + 16, np.uint8)
     pays = [hash_ref.payload(int(n), seed, i) for i, n in enumerate(lens)]
     for o, p in zip(offs, pays):
