@@ -445,7 +445,7 @@ def _analysis_e2e(cols, steps):
     from paper_2601_12713_b200.analysis import DeviceColumns, analyze_columns, pinned_columns, savings_columns
     cols = pinned_columns(cols)
     for _ in range(3):  # warm-up with the timed loop's object lifetimes (previous findings alive)
-        cfh = analyze_columns(cols)
+        cfh = analyze_columns(cols, with_savings=True)
         savings_columns(cols, cfh)
     gc.collect()
     gc.disable()
@@ -454,7 +454,7 @@ def _analysis_e2e(cols, steps):
         t0 = time.perf_counter()
         marks = []
         for _ in range(steps):
-            cfh = analyze_columns(cols)
+            cfh = analyze_columns(cols, with_savings=True)
             savings_columns(cols, cfh)
             marks.append(time.perf_counter())
         torch.cuda.synchronize()
@@ -483,7 +483,7 @@ def _analysis_device(cols, dev, iters, warm=3):
     hold = {}
 
     def step():
-        hold["cf"] = analyze_columns(d)
+        hold["cf"] = analyze_columns(d, with_savings=True)
         hold["sv"] = savings_columns(d, hold["cf"])
     for _ in range(warm):
         step()
@@ -511,13 +511,13 @@ def run_analysis_ours(args, rank, world, local):
     dcols = DeviceColumns(cols, dev)
     torch.cuda.synchronize()
     for _ in range(args.warmup):
-        cf = analyze_columns(dcols)
+        cf = analyze_columns(dcols, with_savings=True)
         sv = savings_columns(dcols, cf)
     verified, why = _verify(cols, cf, sv)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        cf = analyze_columns(dcols)
+        cf = analyze_columns(dcols, with_savings=True)
         savings_columns(dcols, cf)
     torch.cuda.synchronize()
     dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)

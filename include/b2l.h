@@ -179,8 +179,11 @@ enum {
     B2L_ANALYZE_SKIP_DDRT = 8,      /* shard holds no hash-keyed work: skip DD / RT */
     B2L_ANALYZE_SKIP_ALLOC = 16,    /* shard holds no device-keyed work: skip pairs / RA / UA / UT */
     B2L_ANALYZE_NO_VALIDATE = 32,   /* standalone detectors (find_*) take event lists as given */
-    B2L_ANALYZE_RAW_HASHED = 64     /* DD/RT over every transfer row (find_duplicate_transfers /
+    B2L_ANALYZE_RAW_HASHED = 64,    /* DD/RT over every transfer row (find_duplicate_transfers /
                                        find_round_trips group whatever they are given) */
+    B2L_ANALYZE_WITH_SAVINGS = 128  /* also compute b2l_savings_compute's results (estimate + attribute
+                                       aggregates), category by category as the detector chains finish;
+                                       the next b2l_savings_compute of the same columns returns them */
 };
 #define B2L_SYNTHETIC 0xFFFFFFFFu   /* pair_delete of a synthetic trace-end delete (prep.py:78-93) */
 

@@ -75,7 +75,7 @@ def cmd_analyze(args) -> int:
     if cols is None:
         return EXIT_INPUT
     try:
-        cf = analyze_columns(cols, strict=args.strict_pseudocode)
+        cf = analyze_columns(cols, strict=args.strict_pseudocode, with_savings=args.min_bytes <= 1)
     except EngineInvalid as exc:  # the same error parse_trace would have raised
         err = invariant_error(event_violations(cols, exc))
         print(f"dmlens: error: {type(err).__name__}: {err}", file=sys.stderr)

@@ -239,13 +239,19 @@ class EngineInvalid(Exception):
 
 
 FLAG_STRICT_RT, FLAG_VALIDATE_ONLY, FLAG_SYNTH_END, FLAG_SKIP_DDRT, FLAG_SKIP_ALLOC = 1, 2, 4, 8, 16
+FLAG_WITH_SAVINGS = 128
 
 
 def analyze_columns(cols: Columns, strict: bool = False, flags: int = 0,
-                    synthetic_end_ns: Optional[int] = None) -> ColumnarFindings:
+                    synthetic_end_ns: Optional[int] = None, with_savings: bool = False) -> ColumnarFindings:
     """Run the whole detection pipeline on the device.  Raises EngineInvalid with
     the flagged events / rule bits when the trace fails validation.  ``flags`` /
-    ``synthetic_end_ns`` are the shard controls of b2l_analyze_ex (sharded.py)."""
+    ``synthetic_end_ns`` are the shard controls of b2l_analyze_ex (sharded.py).
+    ``with_savings``: the same call also computes the estimate/attribute aggregates, feeding
+    each category in as its detector chain finishes; the next ``savings_columns`` of the same
+    columns returns them without another pass."""
+    if with_savings:
+        flags |= FLAG_WITH_SAVINGS
     L = _L()
     if isinstance(cols, DeviceColumns):
         cs, keep = cols.struct, None
@@ -498,7 +504,7 @@ def analyze(trace, warn: Optional[Callable] = None, strict_pseudocode: bool = Fa
         raise Invalid(_boundary_violations(trace, T.Violation))
     head = _header_violations(trace, T.Violation)
     try:
-        cf = analyze_columns(cols, strict=strict_pseudocode)
+        cf = analyze_columns(cols, strict=strict_pseudocode, with_savings=True)
     except EngineInvalid as exc:
         raise Invalid(head + _event_violations(trace, exc.bad_index, exc.bad_rules, T.Violation))
     if head:

@@ -500,6 +500,8 @@ struct StoreOffset {
 };
 
 // ============================================================ output container
+void stream_after(cudaStream_t to, cudaStream_t from);
+cudaStream_t engine_stream_n(int k);
 struct HostSlab;
 struct Internal {
     // the device findings of the call (first member: released after every buffer carved from it).
@@ -512,6 +514,7 @@ struct Internal {
         b.alloc(n, s);
     }
     HostSlab *slab = nullptr;  // pinned host memory behind the b2l_findings arrays
+    HostSlab *slab_pairs = nullptr, *slab_kern = nullptr;  // ... of the pairs/RA and UT/UA chains
     // device copies of the trace columns (when they were uploaded from host) and their identity
     ColsUpload cols;
     const void *cols_key[3] = {nullptr, nullptr, nullptr};
@@ -521,6 +524,11 @@ struct Internal {
     DBuf<uint32_t> dd_mem, rt_tx, rt_rx, pair_alloc, pair_delete, ra_mem, ua, ut;
     uint64_t dd_groups = 0, dd_members = 0, rt_groups = 0, rt_trips = 0, ra_groups = 0, ra_members = 0;
     uint64_t n_pairs = 0, n_ua = 0, n_ut = 0, synth_end = 0;
+    // savings computed by a fused analyze (B2L_ANALYZE_WITH_SAVINGS), handed to the first
+    // b2l_savings_compute of the same columns
+    b2l_savings *fused = nullptr;
+    const void *fused_key[3] = {nullptr, nullptr, nullptr};
+    uint64_t fused_n = 0;
 };
 
 template <class T>
@@ -546,6 +554,21 @@ struct HostBatch {
     template <class T>
     void add(T **dst, const T *d, size_t n) {
         items.push_back(Item{(void **)dst, d, n * sizeof(T)});
+    }
+    // Queue the copies on `copy` once everything queued so far on `after` is done, into a fresh
+    // slab; no synchronisation (the caller synchronises `copy` before reading).
+    void flush_async(HostSlab &slab, cudaStream_t after, cudaStream_t copy) {
+        size_t total = 0;
+        for (auto &it : items) total += (it.bytes + 63) & ~size_t(63);
+        slab.p = slab_pool().acquire(total, slab.cap);
+        stream_after(copy, after);
+        size_t off = 0;
+        for (auto &it : items) {
+            if (it.bytes) CK(cudaMemcpyAsync(slab.p + off, it.src, it.bytes, cudaMemcpyDeviceToHost, copy));
+            *it.dst = slab.p + off;
+            off += (it.bytes + 63) & ~size_t(63);
+        }
+        items.clear();
     }
     void flush(HostSlab &slab, cudaStream_t s) {
         size_t total = 0;
@@ -1415,7 +1438,7 @@ cudaStream_t g_stream[64] = {nullptr};
 // arena sizing: bytes of scratch per event as measured with B2L_TRACE (analyze 164-183 B/event on
 // C2/C4 at 10k-4M events), plus slack; beyond 64M events buffers come from the pool (reused)
 constexpr size_t ARENA_MAX_EVENTS = size_t(64) << 20, ARENA_BASE = size_t(4) << 20;
-constexpr size_t ARENA_ANALYZE_PER_EVENT = 256, ARENA_SAVINGS_PER_EVENT = 96;  // savings: 5 B/event + a 69 B/event column upload
+constexpr size_t ARENA_ANALYZE_PER_EVENT = 272, ARENA_SAVINGS_PER_EVENT = 96;  // savings: 5 B/event + a 69 B/event column upload
 
 cudaStream_t engine_stream() {
     int dev = 0;
@@ -1437,8 +1460,8 @@ cudaStream_t engine_stream() {
     }
     return g_stream[dev & 63];
 }
-cudaStream_t g_streamx[3][64] = {{nullptr}};
-cudaStream_t engine_stream_n(int k) {  // side streams 1..3: the chains that run beside DD/RT
+cudaStream_t g_streamx[4][64] = {{nullptr}};
+cudaStream_t engine_stream_n(int k) {  // side streams 1..3: the chains that run beside DD/RT; 4: result copies
     int dev = 0;
     CK(cudaGetDevice(&dev));
     cudaStream_t &st = g_streamx[k - 1][dev & 63];
@@ -1467,245 +1490,12 @@ struct SideJoin {
         if (std::uncaught_exceptions() <= unc) return;
         int dev = 0;
         if (cudaGetDevice(&dev) != cudaSuccess) return;
-        for (int k = 0; k < 3; ++k)
+        for (int k = 0; k < 4; ++k)
             if (cudaStream_t st = g_streamx[k][dev & 63]) cudaStreamSynchronize(st);
         cudaGetLastError();
     }
 };
 
-int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_override, b2l_findings **outp) {
-    b2l_findings *f = (b2l_findings *)calloc(1, sizeof(b2l_findings));
-    if (!f) return fail(B2L_E_OOM, "host allocation failed");
-    *outp = f;
-    f->n_events = cols->n_events;
-    if (cols->n_events >= 0xFFFFFFFFull) return fail(B2L_E_INVALID_ARG, "trace too large for 32-bit event indices");
-    std::lock_guard<std::mutex> lock(g_mu);
-    cudaStream_t s = engine_stream();
-    PhaseClock pc(s);
-    Internal *in = new Internal();
-    f->internal = in;
-    ColsUpload &up = in->cols;
-    up.load(cols, s);
-    if (!cols->device_resident) {
-        in->cols_key[0] = cols->seq, in->cols_key[1] = cols->start_ns, in->cols_key[2] = cols->hash;
-        in->cols_n = cols->n_events;
-    }
-    const DevCols c = up.d;
-    const size_t n = c.n;
-    pc.mark("upload");
-    // this call's scratch: one arena, released when the call returns (the device findings get
-    // their own, smaller arena once the partition counts bound them)
-    Arena arena;
-    SideJoin side_join;
-    arena.open(n <= ARENA_MAX_EVENTS ? ARENA_BASE + n * ARENA_ANALYZE_PER_EVENT : 0, s);
-    ArenaUse arena_use(&arena);
-    // ---- 1+2. validation, partition, max end, key-bit masks, start ranks (fused front pass)
-    const bool validate = !(flags & B2L_ANALYZE_NO_VALIDATE), raw = (flags & B2L_ANALYZE_RAW_HASHED) != 0;
-    const unsigned ftiles = (unsigned)((n + FR_TILE - 1) / FR_TILE);
-    DBuf<FrontAcc> fpart(ftiles + 1, s);
-    DBuf<unsigned long long> agg(11, s);  // [0] max data-op end, [1..5] subset OR, [6..10] subset AND
-    agg.zero();
-    CK(cudaMemsetAsync(agg.p + 6, 0xFF, 5 * sizeof(unsigned long long), s));
-    FrontAcc ftot{};
-    unsigned long long hm[11] = {0, 0, 0, 0, 0, 0, ~0ull, ~0ull, ~0ull, ~0ull, ~0ull};
-    if (n) {
-        k_front_reduce<<<ftiles, FR_THREADS, 0, s>>>(c, validate, raw, fpart.p, agg.p);
-        CK_LAUNCH("k_front_reduce");
-        k_scan_partials<FrontOp><<<1, SCAN_THREADS, 0, s>>>(fpart.p, ftiles, fpart.p + ftiles);
-        CK_LAUNCH("k_scan_partials<FrontOp>");
-        uint8_t rb[sizeof(FrontAcc) + sizeof(hm)];
-        {
-            uint8_t *st = pinned(s).reserve(sizeof(rb));
-            CK(cudaMemcpyAsync(st, fpart.p + ftiles, sizeof(FrontAcc), cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(st + sizeof(FrontAcc), agg.p, sizeof(hm), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            memcpy(rb, st, sizeof(rb));
-        }
-        memcpy(&ftot, rb, sizeof(FrontAcc));
-        memcpy(hm, rb + sizeof(FrontAcc), sizeof(hm));
-    }
-    const uint32_t nbad = ftot.c[0];
-    if (nbad) {
-        DBuf<uint32_t> bad(nbad, s), rules(nbad, s), dcount(1, s);
-        FrontOut fo{{bad.p, nullptr, nullptr, nullptr, nullptr, nullptr}, nullptr};
-        k_front_apply<<<ftiles, FR_THREADS, 0, s>>>(c, true, raw, fpart.p, fo);
-        CK_LAUNCH("k_front_apply(bad)");
-        CK(cudaMemcpyAsync(dcount.p, &nbad, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-        k_bad_rules<<<grid_for(nbad, TPB), TPB, 0, s>>>(c, bad.p, dcount.p, rules.p);
-        CK_LAUNCH("k_bad_rules");
-        f->n_bad = nbad;
-        HostBatch hb;
-        hb.add(&f->bad_index, bad.p, nbad);
-        hb.add(&f->bad_rules, rules.p, nbad);
-        in->slab = new HostSlab();
-        hb.flush(*in->slab, s);
-        return fail(B2L_E_INVALID_TRACE, "trace fails validation");
-    }
-    pc.mark("validate");
-    if (flags & B2L_ANALYZE_VALIDATE_ONLY) return B2L_OK;
-    const uint32_t hc[FR_NCAT] = {0, ftot.c[1], ftot.c[2], ftot.c[3], ftot.c[4], ftot.c[5]};
-    DBuf<uint32_t> H(hc[1] ? hc[1] : 1, s), TT(hc[2] ? hc[2] : 1, s), AD(hc[3] ? hc[3] : 1, s),
-        A(hc[4] ? hc[4] : 1, s), TK(hc[5] ? hc[5] : 1, s);
-    DBuf<uint32_t> srank(n ? n : 1, s);
-    if (n) {
-        FrontOut fo{{nullptr, H.p, TT.p, AD.p, A.p, TK.p}, srank.p};
-        k_front_apply<<<ftiles, FR_THREADS, 0, s>>>(c, false, raw, fpart.p, fo);
-        CK_LAUNCH("k_front_apply");
-    }
-    const unsigned long long me = (flags & B2L_ANALYZE_SYNTH_END) ? synth_end_override : hm[0];
-    const bool ddrt = !(flags & B2L_ANALYZE_SKIP_DDRT), alloc = !(flags & B2L_ANALYZE_SKIP_ALLOC);
-    const uint32_t nH = ddrt ? hc[1] : 0, nT = alloc ? hc[2] : 0, nAD = alloc ? hc[3] : 0, nA = alloc ? hc[4] : 0,
-                   nK = alloc ? hc[5] : 0;
-    g_masks.hash = live_mask(hm[1] ^ hm[6]), g_masks.da = live_mask(hm[2] ^ hm[7]);
-    g_masks.sa = live_mask(hm[3] ^ hm[8]), g_masks.nb = live_mask(hm[4] ^ hm[9]);
-    g_masks.sa_tt = live_mask(hm[5] ^ hm[10]);
-    g_masks.dev = live_range((uint64_t)(c.ndev > 0 ? c.ndev : 1));
-    g_masks.idx = live_range(n);
-    g_masks.n = n;
-    g_masks.srank = srank.p;
-
-    pc.mark("partition");
-    {  // upper bounds of the device findings: DD/RT offsets and members <= nH, pairs/RA/UA <= nA, UT <= n
-        const size_t fb = 16 * (nH + 2) + 12 * (size_t)nH + 8 * (nA + 2) + 16 * (size_t)nA + 4 * n + 32 * 256;
-        in->keep.open(n <= ARENA_MAX_EVENTS ? fb : 0, s);
-    }
-    in->synth_end = me;
-    in->n_pairs = nA;
-    // ---- 3-6.  Three independent chains: hash-keyed (DD, RT), pairs -> RA, and the kernel index
-    // -> UT (-> UA once the pairs exist).  Small traces run them on three streams from three host
-    // threads (each keeps its own syncs and staging); large traces are bandwidth bound and run
-    // them back to back on one stream.
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    const Masks masks = g_masks;
-    PairOut po;
-    const bool overlap = n <= (size_t(4) << 20);
-    cudaStream_t s2 = overlap ? engine_stream_n(1) : s, s3 = overlap ? engine_stream_n(2) : s;
-    if (overlap) {  // the partition lists and start ranks are produced on s
-        stream_after(s2, s);
-        stream_after(s3, s);
-    }
-    std::promise<cudaEvent_t> pairs_done;  // recorded on s2 after pairing (UA needs the pairs)
-    std::shared_future<cudaEvent_t> pairs_ready = pairs_done.get_future().share();
-    EngineErr err2{0, ""}, err3{0, ""};
-    bool failed2 = false, failed3 = false, promised = false;
-    auto pairs_chain = [&] {
-        ArenaUse au(&arena);
-        try {
-            CK(cudaSetDevice(dev));
-            g_masks = masks;
-            PhaseClock pc2(s2);
-            po = pairs_step(c, AD.p, nAD, A.p, nA, me, *in, s2);
-            cudaEvent_t ev;
-            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-            CK(cudaEventRecord(ev, s2));
-            pairs_done.set_value(ev);
-            promised = true;
-            pc2.mark("pairs");
-            ra_step(c, nA, *in, s2);
-            if (po.wcount.p) po.n_warn = read_u32(po.wcount.p, s2);
-            pc2.mark("ra");
-            if (overlap) CK(cudaStreamSynchronize(s2));
-        } catch (const EngineErr &e) {
-            err2 = e;
-            failed2 = true;
-            if (!promised) pairs_done.set_value(nullptr);
-        }
-    };
-    auto kernel_chain = [&] {
-        ArenaUse au(&arena);
-        try {
-            CK(cudaSetDevice(dev));
-            g_masks = masks;
-            PhaseClock pc3(s3);
-            KernelIndexStore kis(nK, s3);
-            build_kernel_index(kis, c, TK.p, nK, s3);
-            ut_step(c, kis.KI, TT.p, nT, *in, s3);
-            pc3.mark("ut");
-            cudaEvent_t ev = pairs_ready.get();
-            if (!ev) return;  // pairing failed (reported by its chain)
-            CK(cudaStreamWaitEvent(s3, ev, 0));
-            ua_step(c, kis.KI, *in, s3);
-            pc3.mark("ua");
-            if (overlap) CK(cudaStreamSynchronize(s3));
-        } catch (const EngineErr &e) {
-            err3 = e;
-            failed3 = true;
-        }
-    };
-    std::future<void> t2, t3;
-    if (overlap) {
-        t2 = workers().submit(pairs_chain);
-        t3 = workers().submit(kernel_chain);
-    } else {
-        pairs_chain();
-        kernel_chain();
-    }
-    auto join = [&] {
-        if (t2.valid()) t2.wait();
-        if (t3.valid()) t3.wait();
-        cudaEvent_t ev = pairs_ready.get();
-        if (ev) cudaEventDestroy(ev);
-    };
-    try {
-        DdRt dr = dd_rt_step(c, H.p, nH, (flags & B2L_ANALYZE_STRICT_RT) != 0, *in, s);
-        in->dd_groups = dr.dd_groups, in->dd_members = dr.dd_members, in->rt_groups = dr.rt_groups,
-        in->rt_trips = dr.rt_trips;
-    } catch (...) {
-        join();
-        throw;
-    }
-    join();
-    if (failed2) throw err2;
-    if (failed3) throw err3;
-    pc.mark("detectors");
-
-    // ---- results to the host (one pinned slab, one synchronisation)
-    HostBatch hb;
-    f->dd_groups = in->dd_groups;
-    hb.add(&f->dd_offsets, in->dd_off.p, in->dd_groups + 1);
-    hb.add(&f->dd_members, in->dd_mem.p, in->dd_members);
-    f->rt_groups = in->rt_groups;
-    hb.add(&f->rt_offsets, in->rt_off.p, in->rt_groups + 1);
-    hb.add(&f->rt_tx, in->rt_tx.p, in->rt_trips);
-    hb.add(&f->rt_rx, in->rt_rx.p, in->rt_trips);
-    f->n_pairs = nA;
-    hb.add(&f->pair_alloc, in->pair_alloc.p, nA);
-    hb.add(&f->pair_delete, in->pair_delete.p, nA);
-    f->synthetic_end_ns = me;
-    f->n_warnings = po.n_warn;
-    hb.add(&f->warn_index, po.warn.p, po.n_warn);
-    f->ra_groups = in->ra_groups;
-    hb.add(&f->ra_offsets, in->ra_off.p, in->ra_groups + 1);
-    hb.add(&f->ra_pairs, in->ra_mem.p, in->ra_members);
-    f->n_ua = in->n_ua;
-    hb.add(&f->ua_pairs, in->ua.p, in->n_ua);
-    f->n_ut = in->n_ut;
-    hb.add(&f->ut_events, in->ut.p, in->n_ut);
-    in->slab = new HostSlab();
-    hb.flush(*in->slab, s);
-    pc.mark("d2h");
-    if (alloc_stats().on) {
-        fprintf(stderr, "[b2l] pool alloc/free calls %llu, host %.3f ms; arena %.1f of %.1f MB (%.0f B/event)\n",
-                (unsigned long long)alloc_stats().n.load(), alloc_stats().ns.load() * 1e-6,
-                arena.off.load() / 1048576.0, arena.cap / 1048576.0, n ? (double)arena.off.load() / n : 0.0);
-        fprintf(stderr, "[b2l] findings arena %.1f of %.1f MB\n", in->keep.off.load() / 1048576.0,
-                in->keep.cap / 1048576.0);
-        alloc_stats().n = 0, alloc_stats().ns = 0;
-    }
-    if (in->dd_groups == 0) f->dd_offsets[0] = 0;
-    if (in->rt_groups == 0) f->rt_offsets[0] = 0;
-    if (in->ra_groups == 0) f->ra_offsets[0] = 0;
-    return B2L_OK;
-}
-
-void findings_free(b2l_findings *f) {
-    if (!f) return;
-    Internal *in = (Internal *)f->internal;
-    if (in) delete in->slab;  // arrays live in the slab
-    delete in;
-    free(f);
-}
 
 
 // ============================================================ savings (estimator.py:61-130, report.py:44-95)
@@ -1923,7 +1713,173 @@ struct FindingsDev {  // device views of a findings set
     uint64_t dd_groups, dd_members, rt_trips, n_pairs, ra_groups, ra_members, n_ua, n_ut;
 };
 
+// One savings computation (estimator.py:61-130 integer part, report.py:44-95 aggregation),
+// split so a fused analyze can feed it category by category as its chains finish: attribution
+// and category bits of a category only need that category's findings; the sums and the
+// overlap / union scan need all five.
+struct SvRun {
+    DevCols c{};
+    size_t n = 0;
+    uint32_t nb = 0;
+    size_t smem = 0;
+    DBuf<unsigned long long> at, acc;
+    DBuf<uint8_t> cat;
+    DBuf<uint32_t> ovl, uni, unic;
+    DBuf<OvUn::T> ovt;
+    AttrAcc acc_of(int cat_i) const {
+        unsigned long long *base = at.p;
+        return AttrAcc{base + (size_t)cat_i * nb, base + 5 * (size_t)nb + (size_t)cat_i * 2 * nb,
+                       base + 15 * (size_t)nb + (size_t)cat_i * 2 * nb, base + 25 * (size_t)nb + (size_t)cat_i * nb};
+    }
+};
+
+void sv_begin(SvRun &R, const DevCols &c, cudaStream_t s) {
+    R.c = c;
+    R.n = c.n;
+    R.nb = c.nbuckets;
+    R.at.alloc(5 * (size_t)R.nb * 6 + 1, s);
+    R.at.zero();
+    CK(cudaMemsetAsync(R.at.p + 5 * (size_t)R.nb * 5, 0xFF, 5 * (size_t)R.nb * sizeof(unsigned long long), s));
+    R.smem = R.nb <= 512 ? (size_t)R.nb * 6 * sizeof(unsigned long long) : 0;
+    R.cat.alloc(((R.n ? R.n : 1) + 3) & ~size_t(3), s);  // whole words: byte atomics touch the word
+    R.cat.zero();
+}
+
+// Attribution + category bits of category k (DD 0, RT 1, RA 2, UA 3, UT 4) on stream st.
+void sv_add(SvRun &R, int k, const FindingsDev &F, cudaStream_t st) {
+    const DevCols c = R.c;
+    uint8_t *ct = R.cat.p;
+    auto launch = [&](auto el, size_t ne) {
+        if (!ne || !R.nb) return;
+        k_attr<<<grid_for(ne, TPB, 148 * 8), TPB, R.smem, st>>>(c, ne, el, R.acc_of(k));
+        CK_LAUNCH("k_attr");
+    };
+    if (k == 0) {  // DD: every member counts for attribution; all but the first of a group are eliminable
+        launch(ElemList{F.dd_mem}, F.dd_members);
+        const uint64_t *off = F.dd_off;
+        const uint32_t *mem = F.dd_mem;
+        const uint64_t ng = F.dd_groups;
+        for_each(F.dd_members, [=] __device__(size_t q) {
+            uint64_t lo = 0, hi = ng;  // group g with off[g] <= q < off[g+1]
+            while (hi - lo > 1) {
+                uint64_t m = (lo + hi) >> 1;
+                if (off[m] <= q) lo = m; else hi = m;
+            }
+            if (off[lo] != q) atomicOr_u8(ct + mem[q], 1);
+        }, st);
+    } else if (k == 1) {  // RT: tx and rx attributed, the receptions eliminable
+        launch(ElemTrips{F.rt_tx, F.rt_rx}, F.rt_trips);
+        const uint32_t *rx = F.rt_rx;
+        for_each(F.rt_trips, [=] __device__(size_t q) { atomicOr_u8(ct + rx[q], 2); }, st);
+    } else if (k == 2) {  // RA: pairs after the first of a group (alloc + non-synthetic delete)
+        launch(ElemPairs{F.ra_mem, F.pa, F.pd}, F.ra_members);
+        const uint64_t *roff = F.ra_off;
+        const uint32_t *rm = F.ra_mem, *pa = F.pa, *pd = F.pd;
+        const uint64_t rng = F.ra_groups;
+        for_each(F.ra_members, [=] __device__(size_t q) {
+            uint64_t lo = 0, hi = rng;
+            while (hi - lo > 1) {
+                uint64_t m = (lo + hi) >> 1;
+                if (roff[m] <= q) lo = m; else hi = m;
+            }
+            if (roff[lo] == q) return;  // first pair of a group is necessary
+            const uint32_t r = rm[q];
+            atomicOr_u8(ct + pa[r], 4);
+            if (pd[r] != NONE) atomicOr_u8(ct + pd[r], 4);
+        }, st);
+    } else if (k == 3) {  // UA
+        launch(ElemPairs{F.ua, F.pa, F.pd}, F.n_ua);
+        const uint32_t *ua = F.ua, *pa = F.pa, *pd = F.pd;
+        for_each(F.n_ua, [=] __device__(size_t q) {
+            const uint32_t r = ua[q];
+            atomicOr_u8(ct + pa[r], 8);
+            if (pd[r] != NONE) atomicOr_u8(ct + pd[r], 8);
+        }, st);
+    } else {  // UT
+        launch(ElemList{F.ut}, F.n_ut);
+        const uint32_t *ut = F.ut;
+        for_each(F.n_ut, [=] __device__(size_t q) { atomicOr_u8(ct + ut[q], 16); }, st);
+    }
+}
+
+// Sums, overlap flag and union list once every category is in (all on s), then the results to
+// the host: the small ones with one synchronisation of s, the arrays on `copy` (not synchronised).
+void sv_finish(SvRun &R, b2l_savings *o, cudaStream_t s, cudaStream_t copy) {
+    const size_t n = R.n;
+    const DevCols c = R.c;
+    R.acc.alloc(12 + 1 + 2, s);
+    R.acc.zero();
+    {
+        unsigned long long init[2] = {~0ull, 0ull};
+        CK(cudaMemcpyAsync(R.acc.p + 13, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    }
+    if (n) {
+        k_sums<<<grid_for(n, TPB, 148 * 4), TPB, 0, s>>>(c, R.cat.p, R.acc.p, R.acc.p + 12, R.acc.p + 13);
+        CK_LAUNCH("k_sums");
+    }
+    // overlap: exists i >= 1 with start[i] < max(end[0..i-1])  (estimator.py:51-58)
+    // ... and the union list, in the same scan
+    R.ovl.alloc(1, s);
+    R.ovl.zero();
+    R.uni.alloc(n ? n : 1, s);
+    R.unic.alloc(1, s);
+    R.ovt.alloc(1, s);
+    scan<OvUn>(n, OvUnLoad{c.end, R.cat.p}, OvUnStore{c.start, R.cat.p, R.ovl.p, R.uni.p}, s, R.ovt.p);
+    if (n) CK(cudaMemcpyAsync(R.unic.p, &R.ovt.p->cnt, 4, cudaMemcpyDeviceToDevice, s));
+    else R.unic.zero();
+    unsigned long long h[15];
+    uint32_t hov = 0, hun = 0;
+    {  // one synchronisation for the three small results
+        uint8_t *st = pinned(s).reserve(sizeof(h) + 8);
+        CK(cudaMemcpyAsync(st, R.acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(st + sizeof(h), R.ovl.p, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(st + sizeof(h) + 4, R.unic.p, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        memcpy(h, st, sizeof(h));
+        memcpy(&hov, st + sizeof(h), 4);
+        memcpy(&hun, st + sizeof(h) + 4, 4);
+    }
+    for (int k = 0; k < 5; ++k) o->per_category_ns[k] = b2l_u128{h[2 * k], h[2 * k + 1]};
+    o->union_ns = b2l_u128{h[10], h[11]};
+    o->n_union = hun;
+    o->has_overlaps = hov ? 1 : 0;
+    o->min_start_ns = n ? h[13] : 0;
+    o->max_end_ns = h[14];
+    HostBatch hb;
+    hb.add(&o->union_index, R.uni.p, hun);
+    o->n_buckets = R.nb;
+    const size_t nb5 = 5 * (size_t)R.nb;
+    hb.add((unsigned long long **)&o->attr_count, R.at.p, nb5);
+    hb.add((unsigned long long **)&o->attr_ns, R.at.p + nb5, 2 * nb5);
+    hb.add((unsigned long long **)&o->attr_bytes, R.at.p + 3 * nb5, 2 * nb5);
+    hb.add((unsigned long long **)&o->attr_first, R.at.p + 5 * nb5, nb5);
+    HostSlab *slab = new HostSlab();
+    o->internal = slab;
+    hb.flush_async(*slab, s, copy);
+}
+
+FindingsDev findings_dev(const Internal &in) {
+    FindingsDev F{};
+    F.dd_off = in.dd_off.p, F.ra_off = in.ra_off.p, F.dd_mem = in.dd_mem.p, F.rt_tx = in.rt_tx.p;
+    F.rt_rx = in.rt_rx.p, F.pa = in.pair_alloc.p, F.pd = in.pair_delete.p, F.ra_mem = in.ra_mem.p;
+    F.ua = in.ua.p, F.ut = in.ut.p;
+    F.dd_groups = in.dd_groups, F.dd_members = in.dd_members, F.rt_trips = in.rt_trips, F.n_pairs = in.n_pairs;
+    F.ra_groups = in.ra_groups, F.ra_members = in.ra_members, F.n_ua = in.n_ua, F.n_ut = in.n_ut;
+    return F;
+}
+
 int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings **outp) {
+    // a fused analyze (B2L_ANALYZE_WITH_SAVINGS) of these very columns already computed them
+    if (f && f->internal) {
+        Internal *in = (Internal *)f->internal;
+        if (in->fused && in->fused_n == cols->n_events && in->fused_key[0] == (const void *)cols->seq &&
+            in->fused_key[1] == (const void *)cols->start_ns && in->fused_key[2] == (const void *)cols->hash &&
+            in->fused->n_buckets == cols->n_buckets) {
+            *outp = in->fused;
+            in->fused = nullptr;
+            return B2L_OK;
+        }
+    }
     b2l_savings *o = (b2l_savings *)calloc(1, sizeof(b2l_savings));
     if (!o) return fail(B2L_E_OOM, "host allocation failed");
     *outp = o;
@@ -1944,7 +1900,6 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
         up.load(cols, s);
         c = up.d;
     }
-    const size_t n = c.n;
     // findings on the device: reuse the engine's copies, or upload caller arrays
     FindingsDev F{};
     std::vector<DBuf<uint8_t>> keep;
@@ -1958,154 +1913,34 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     const uint64_t nm_dd = f->dd_groups ? f->dd_offsets[f->dd_groups] : 0;
     const uint64_t nt_rt = f->rt_groups ? f->rt_offsets[f->rt_groups] : 0;
     const uint64_t nm_ra = f->ra_groups ? f->ra_offsets[f->ra_groups] : 0;
-    F.dd_groups = f->dd_groups, F.dd_members = nm_dd, F.rt_trips = nt_rt, F.n_pairs = f->n_pairs;
-    F.ra_groups = f->ra_groups, F.ra_members = nm_ra, F.n_ua = f->n_ua, F.n_ut = f->n_ut;
     if (f->internal) {
-        const Internal *in = (const Internal *)f->internal;
-        F.dd_off = in->dd_off.p, F.ra_off = in->ra_off.p, F.dd_mem = in->dd_mem.p, F.rt_tx = in->rt_tx.p;
-        F.rt_rx = in->rt_rx.p, F.pa = in->pair_alloc.p, F.pd = in->pair_delete.p, F.ra_mem = in->ra_mem.p;
-        F.ua = in->ua.p, F.ut = in->ut.p;
+        F = findings_dev(*(const Internal *)f->internal);
     } else {
         F.dd_off = upl(f->dd_offsets, f->dd_groups + 1), F.ra_off = upl(f->ra_offsets, f->ra_groups + 1);
         F.dd_mem = upl(f->dd_members, nm_dd), F.rt_tx = upl(f->rt_tx, nt_rt), F.rt_rx = upl(f->rt_rx, nt_rt);
         F.pa = upl(f->pair_alloc, f->n_pairs), F.pd = upl(f->pair_delete, f->n_pairs);
         F.ra_mem = upl(f->ra_pairs, nm_ra), F.ua = upl(f->ua_pairs, f->n_ua), F.ut = upl(f->ut_events, f->n_ut);
     }
+    F.dd_groups = f->dd_groups, F.dd_members = nm_dd, F.rt_trips = nt_rt, F.n_pairs = f->n_pairs;
+    F.ra_groups = f->ra_groups, F.ra_members = nm_ra, F.n_ua = f->n_ua, F.n_ut = f->n_ut;
     PhaseClock pc(s);
     pc.mark("sv-setup");
-    // ---- attribution
-    const uint32_t nb = c.nbuckets;
-    DBuf<unsigned long long> at(5 * (size_t)nb * 6 + 1, s);
-    at.zero();
-    CK(cudaMemsetAsync(at.p + 5 * (size_t)nb * 5, 0xFF, 5 * (size_t)nb * sizeof(unsigned long long), s));
-    // the attribution kernels read only the findings: run them on a side stream beside the
-    // category bits, sums and the overlap/union scan
+    SvRun R;
+    sv_begin(R, c, s);
+    // attribution and category bits: DD, RT, RA on a side stream, UA, UT on s
     cudaStream_t sa = engine_stream_n(1);
     stream_after(sa, s);
-    const size_t smem = nb <= 512 ? (size_t)nb * 6 * sizeof(unsigned long long) : 0;
-    auto acc_of = [&](int cat_i) {
-        unsigned long long *base = at.p;
-        return AttrAcc{base + (size_t)cat_i * nb, base + 5 * (size_t)nb + (size_t)cat_i * 2 * nb,
-                       base + 15 * (size_t)nb + (size_t)cat_i * 2 * nb, base + 25 * (size_t)nb + (size_t)cat_i * nb};
-    };
-    auto launch = [&](auto el, size_t ne, int cat_i) {
-        if (!ne || !nb) return;
-        k_attr<<<grid_for(ne, TPB, 148 * 8), TPB, smem, sa>>>(c, ne, el, acc_of(cat_i));
-        CK_LAUNCH("k_attr");
-    };
-    launch(ElemList{F.dd_mem}, F.dd_members, 0);
-    launch(ElemTrips{F.rt_tx, F.rt_rx}, F.rt_trips, 1);
-    launch(ElemPairs{F.ra_mem, F.pa, F.pd}, F.ra_members, 2);
-    launch(ElemPairs{F.ua, F.pa, F.pd}, F.n_ua, 3);
-    launch(ElemList{F.ut}, F.n_ut, 4);
-    // ---- category bits per event
-    DBuf<uint8_t> cat(((n ? n : 1) + 3) & ~size_t(3), s);  // whole words: byte atomics touch the word
-    cat.zero();
-    uint8_t *ct = cat.p;
-    {
-        // one launch over the five finding lists laid end to end: DD members but the first of each
-        // group, RT receptions, RA pairs but the first of each group, UA pairs, UT events
-        const uint64_t *off = F.dd_off, *roff = F.ra_off;
-        const uint32_t *mem = F.dd_mem, *rx = F.rt_rx, *rm = F.ra_mem, *pa = F.pa, *pd = F.pd, *ua = F.ua,
-                       *ut = F.ut;
-        const uint64_t ng = F.dd_groups, rng = F.ra_groups;
-        const uint64_t e0 = F.dd_members, e1 = e0 + F.rt_trips, e2 = e1 + F.ra_members, e3 = e2 + F.n_ua,
-                       e4 = e3 + F.n_ut;
-        for_each(e4, [=] __device__(size_t q) {
-            if (q < e0) {
-                uint64_t lo = 0, hi = ng;  // group g with off[g] <= q < off[g+1]
-                while (hi - lo > 1) {
-                    uint64_t m = (lo + hi) >> 1;
-                    if (off[m] <= q) lo = m; else hi = m;
-                }
-                if (off[lo] != q) atomicOr_u8(ct + mem[q], 1);
-            } else if (q < e1) {
-                atomicOr_u8(ct + rx[q - e0], 2);
-            } else if (q < e2) {
-                const uint64_t k = q - e1;
-                uint64_t lo = 0, hi = rng;
-                while (hi - lo > 1) {
-                    uint64_t m = (lo + hi) >> 1;
-                    if (roff[m] <= k) lo = m; else hi = m;
-                }
-                if (roff[lo] == k) return;  // first pair of a group is necessary
-                const uint32_t r = rm[k];
-                atomicOr_u8(ct + pa[r], 4);
-                if (pd[r] != NONE) atomicOr_u8(ct + pd[r], 4);
-            } else if (q < e3) {
-                const uint32_t r = ua[q - e2];
-                atomicOr_u8(ct + pa[r], 8);
-                if (pd[r] != NONE) atomicOr_u8(ct + pd[r], 8);
-            } else {
-                atomicOr_u8(ct + ut[q - e3], 16);
-            }
-        }, s);
-    }
-    pc.mark("sv-catbits");
-    // ---- sums, union, span
-    DBuf<unsigned long long> acc(12 + 1 + 2, s);
-    acc.zero();
-    {
-        unsigned long long init[2] = {~0ull, 0ull};
-        CK(cudaMemcpyAsync(acc.p + 13, init, sizeof(init), cudaMemcpyHostToDevice, s));
-    }
-    // the 128-bit sums and the overlap / union scan both only read the category bits: the sums go
-    // to a second side stream
-    cudaStream_t sb = engine_stream_n(2);
-    auto join_streams = [](cudaStream_t from, cudaStream_t to) { stream_after(to, from); };
-    join_streams(s, sb);
-    if (n) {
-        k_sums<<<grid_for(n, TPB, 148 * 4), TPB, 0, sb>>>(c, cat.p, acc.p, acc.p + 12, acc.p + 13);
-        CK_LAUNCH("k_sums");
-    }
-    // overlap: exists i >= 1 with start[i] < max(end[0..i-1])  (estimator.py:51-58)
-    // ... and the union list, in the same scan
-    DBuf<uint32_t> ovl(1, s);
-    ovl.zero();
-    DBuf<uint32_t> uni(n ? n : 1, s), unic(1, s);
-    DBuf<OvUn::T> ovt(1, s);
-    scan<OvUn>(n, OvUnLoad{c.end, ct}, OvUnStore{c.start, ct, ovl.p, uni.p}, s, ovt.p);
-    if (n) CK(cudaMemcpyAsync(unic.p, &ovt.p->cnt, 4, cudaMemcpyDeviceToDevice, s));
-    else unic.zero();
-    join_streams(sb, s);
-    pc.mark("sv-sums");
-    // attribution (on the side stream) has finished before anything is read back
+    for (int k = 0; k < 3; ++k) sv_add(R, k, F, sa);
+    for (int k = 3; k < 5; ++k) sv_add(R, k, F, s);
     stream_after(s, sa);
     pc.mark("sv-attr");
-    // ---- to host
-    unsigned long long h[15];
-    uint32_t hov = 0, hun = 0;
-    {  // one synchronisation for the three small results
-        uint8_t *st = pinned(s).reserve(sizeof(h) + 8);
-        CK(cudaMemcpyAsync(st, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(st + sizeof(h), ovl.p, 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(st + sizeof(h) + 4, unic.p, 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        memcpy(h, st, sizeof(h));
-        memcpy(&hov, st + sizeof(h), 4);
-        memcpy(&hun, st + sizeof(h) + 4, 4);
-    }
-    for (int k = 0; k < 5; ++k) o->per_category_ns[k] = b2l_u128{h[2 * k], h[2 * k + 1]};
-    o->union_ns = b2l_u128{h[10], h[11]};
-    o->n_union = hun;
-    o->has_overlaps = hov ? 1 : 0;
-    o->min_start_ns = n ? h[13] : 0;
-    o->max_end_ns = h[14];
-    HostBatch hb;
-    hb.add(&o->union_index, uni.p, hun);
-    o->n_buckets = nb;
-    const size_t nb5 = 5 * (size_t)nb;
-    hb.add((unsigned long long **)&o->attr_count, at.p, nb5);
-    hb.add((unsigned long long **)&o->attr_ns, at.p + nb5, 2 * nb5);
-    hb.add((unsigned long long **)&o->attr_bytes, at.p + 3 * nb5, 2 * nb5);
-    hb.add((unsigned long long **)&o->attr_first, at.p + 5 * nb5, nb5);
-    HostSlab *slab = new HostSlab();
-    o->internal = slab;
-    hb.flush(*slab, s);
+    cudaStream_t sc = engine_stream_n(4);
+    sv_finish(R, o, s, sc);
+    CK(cudaStreamSynchronize(sc));
     pc.mark("sv-d2h");
     if (alloc_stats().on)
         fprintf(stderr, "[b2l] savings arena %.1f of %.1f MB (%.0f B/event)\n", arena.off.load() / 1048576.0,
-                arena.cap / 1048576.0, n ? (double)arena.off.load() / n : 0.0);
+                arena.cap / 1048576.0, c.n ? (double)arena.off.load() / c.n : 0.0);
     return B2L_OK;
 }
 
@@ -2113,6 +1948,284 @@ void savings_free(b2l_savings *o) {
     if (!o) return;
     delete (HostSlab *)o->internal;
     free(o);
+}
+
+int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_override, b2l_findings **outp) {
+    b2l_findings *f = (b2l_findings *)calloc(1, sizeof(b2l_findings));
+    if (!f) return fail(B2L_E_OOM, "host allocation failed");
+    *outp = f;
+    f->n_events = cols->n_events;
+    if (cols->n_events >= 0xFFFFFFFFull) return fail(B2L_E_INVALID_ARG, "trace too large for 32-bit event indices");
+    std::lock_guard<std::mutex> lock(g_mu);
+    cudaStream_t s = engine_stream();
+    PhaseClock pc(s);
+    Internal *in = new Internal();
+    f->internal = in;
+    ColsUpload &up = in->cols;
+    up.load(cols, s);
+    if (!cols->device_resident) {
+        in->cols_key[0] = cols->seq, in->cols_key[1] = cols->start_ns, in->cols_key[2] = cols->hash;
+        in->cols_n = cols->n_events;
+    }
+    const DevCols c = up.d;
+    const size_t n = c.n;
+    pc.mark("upload");
+    // this call's scratch: one arena, released when the call returns (the device findings get
+    // their own, smaller arena once the partition counts bound them)
+    Arena arena;
+    SideJoin side_join;
+    arena.open(n <= ARENA_MAX_EVENTS ? ARENA_BASE + n * ARENA_ANALYZE_PER_EVENT : 0, s);
+    ArenaUse arena_use(&arena);
+    // ---- 1+2. validation, partition, max end, key-bit masks, start ranks (fused front pass)
+    const bool validate = !(flags & B2L_ANALYZE_NO_VALIDATE), raw = (flags & B2L_ANALYZE_RAW_HASHED) != 0;
+    const unsigned ftiles = (unsigned)((n + FR_TILE - 1) / FR_TILE);
+    DBuf<FrontAcc> fpart(ftiles + 1, s);
+    DBuf<unsigned long long> agg(11, s);  // [0] max data-op end, [1..5] subset OR, [6..10] subset AND
+    agg.zero();
+    CK(cudaMemsetAsync(agg.p + 6, 0xFF, 5 * sizeof(unsigned long long), s));
+    FrontAcc ftot{};
+    unsigned long long hm[11] = {0, 0, 0, 0, 0, 0, ~0ull, ~0ull, ~0ull, ~0ull, ~0ull};
+    // the five partition lists are sized n (an upper bound) so the apply pass is queued right
+    // behind the reduce, before the one read-back of the counts and masks
+    const bool only_validate = (flags & B2L_ANALYZE_VALIDATE_ONLY) != 0;
+    const size_t nl = only_validate || !n ? 1 : n;
+    DBuf<uint32_t> H(nl, s), TT(nl, s), AD(nl, s), A(nl, s), TK(nl, s);
+    DBuf<uint32_t> srank(nl, s);
+    if (n) {
+        k_front_reduce<<<ftiles, FR_THREADS, 0, s>>>(c, validate, raw, fpart.p, agg.p);
+        CK_LAUNCH("k_front_reduce");
+        k_scan_partials<FrontOp><<<1, SCAN_THREADS, 0, s>>>(fpart.p, ftiles, fpart.p + ftiles);
+        CK_LAUNCH("k_scan_partials<FrontOp>");
+        if (!only_validate) {  // lists of an invalid trace are never read
+            FrontOut fo{{nullptr, H.p, TT.p, AD.p, A.p, TK.p}, srank.p};
+            k_front_apply<<<ftiles, FR_THREADS, 0, s>>>(c, false, raw, fpart.p, fo);
+            CK_LAUNCH("k_front_apply");
+        }
+        uint8_t rb[sizeof(FrontAcc) + sizeof(hm)];
+        {
+            uint8_t *st = pinned(s).reserve(sizeof(rb));
+            CK(cudaMemcpyAsync(st, fpart.p + ftiles, sizeof(FrontAcc), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(st + sizeof(FrontAcc), agg.p, sizeof(hm), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            memcpy(rb, st, sizeof(rb));
+        }
+        memcpy(&ftot, rb, sizeof(FrontAcc));
+        memcpy(hm, rb + sizeof(FrontAcc), sizeof(hm));
+    }
+    const uint32_t nbad = ftot.c[0];
+    if (nbad) {
+        DBuf<uint32_t> bad(nbad, s), rules(nbad, s), dcount(1, s);
+        FrontOut fo{{bad.p, nullptr, nullptr, nullptr, nullptr, nullptr}, nullptr};
+        k_front_apply<<<ftiles, FR_THREADS, 0, s>>>(c, true, raw, fpart.p, fo);
+        CK_LAUNCH("k_front_apply(bad)");
+        CK(cudaMemcpyAsync(dcount.p, &nbad, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        k_bad_rules<<<grid_for(nbad, TPB), TPB, 0, s>>>(c, bad.p, dcount.p, rules.p);
+        CK_LAUNCH("k_bad_rules");
+        f->n_bad = nbad;
+        HostBatch hb;
+        hb.add(&f->bad_index, bad.p, nbad);
+        hb.add(&f->bad_rules, rules.p, nbad);
+        in->slab = new HostSlab();
+        hb.flush(*in->slab, s);
+        return fail(B2L_E_INVALID_TRACE, "trace fails validation");
+    }
+    pc.mark("validate");
+    if (flags & B2L_ANALYZE_VALIDATE_ONLY) return B2L_OK;
+    const uint32_t hc[FR_NCAT] = {0, ftot.c[1], ftot.c[2], ftot.c[3], ftot.c[4], ftot.c[5]};
+    const unsigned long long me = (flags & B2L_ANALYZE_SYNTH_END) ? synth_end_override : hm[0];
+    const bool ddrt = !(flags & B2L_ANALYZE_SKIP_DDRT), alloc = !(flags & B2L_ANALYZE_SKIP_ALLOC);
+    const uint32_t nH = ddrt ? hc[1] : 0, nT = alloc ? hc[2] : 0, nAD = alloc ? hc[3] : 0, nA = alloc ? hc[4] : 0,
+                   nK = alloc ? hc[5] : 0;
+    g_masks.hash = live_mask(hm[1] ^ hm[6]), g_masks.da = live_mask(hm[2] ^ hm[7]);
+    g_masks.sa = live_mask(hm[3] ^ hm[8]), g_masks.nb = live_mask(hm[4] ^ hm[9]);
+    g_masks.sa_tt = live_mask(hm[5] ^ hm[10]);
+    g_masks.dev = live_range((uint64_t)(c.ndev > 0 ? c.ndev : 1));
+    g_masks.idx = live_range(n);
+    g_masks.n = n;
+    g_masks.srank = srank.p;
+
+    pc.mark("partition");
+    // fused savings: attribution / category bits of each category queued as its chain finishes
+    const bool with_sv = (flags & B2L_ANALYZE_WITH_SAVINGS) != 0;
+    SvRun R;
+    if (with_sv) sv_begin(R, c, s);
+    {  // upper bounds of the device findings: DD/RT offsets and members <= nH, pairs/RA/UA <= nA, UT <= n
+        const size_t fb = 16 * (nH + 2) + 12 * (size_t)nH + 8 * (nA + 2) + 16 * (size_t)nA + 4 * n + 32 * 256;
+        in->keep.open(n <= ARENA_MAX_EVENTS ? fb : 0, s);
+    }
+    in->synth_end = me;
+    in->n_pairs = nA;
+    // ---- 3-6.  Three independent chains: hash-keyed (DD, RT), pairs -> RA, and the kernel index
+    // -> UT (-> UA once the pairs exist).  Small traces run them on three streams from three host
+    // threads (each keeps its own syncs and staging); large traces are bandwidth bound and run
+    // them back to back on one stream.
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const Masks masks = g_masks;
+    PairOut po;
+    const bool overlap = n <= (size_t(4) << 20);
+    cudaStream_t s2 = overlap ? engine_stream_n(1) : s, s3 = overlap ? engine_stream_n(2) : s;
+    cudaStream_t sc = engine_stream_n(4);  // device -> host result copies, chain by chain
+    if (overlap) {  // the partition lists and start ranks are produced on s
+        stream_after(s2, s);
+        stream_after(s3, s);
+    }
+    std::promise<cudaEvent_t> pairs_done;  // recorded on s2 after pairing (UA needs the pairs)
+    std::shared_future<cudaEvent_t> pairs_ready = pairs_done.get_future().share();
+    EngineErr err2{0, ""}, err3{0, ""};
+    bool failed2 = false, failed3 = false, promised = false;
+    auto pairs_chain = [&] {
+        ArenaUse au(&arena);
+        try {
+            CK(cudaSetDevice(dev));
+            g_masks = masks;
+            PhaseClock pc2(s2);
+            po = pairs_step(c, AD.p, nAD, A.p, nA, me, *in, s2);
+            cudaEvent_t ev;
+            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            CK(cudaEventRecord(ev, s2));
+            pairs_done.set_value(ev);
+            promised = true;
+            pc2.mark("pairs");
+            ra_step(c, nA, *in, s2);
+            if (po.wcount.p) po.n_warn = read_u32(po.wcount.p, s2);
+            pc2.mark("ra");
+            if (with_sv) sv_add(R, 2, findings_dev(*in), s2);
+            {  // this chain's results go to the host while the other chains still run
+                HostBatch hb;
+                hb.add(&f->pair_alloc, in->pair_alloc.p, nA);
+                hb.add(&f->pair_delete, in->pair_delete.p, nA);
+                hb.add(&f->warn_index, po.warn.p, po.n_warn);
+                hb.add(&f->ra_offsets, in->ra_off.p, in->ra_groups + 1);
+                hb.add(&f->ra_pairs, in->ra_mem.p, in->ra_members);
+                in->slab_pairs = new HostSlab();
+                hb.flush_async(*in->slab_pairs, s2, sc);
+            }
+            if (overlap) CK(cudaStreamSynchronize(s2));
+        } catch (const EngineErr &e) {
+            err2 = e;
+            failed2 = true;
+            if (!promised) pairs_done.set_value(nullptr);
+        }
+    };
+    auto kernel_chain = [&] {
+        ArenaUse au(&arena);
+        try {
+            CK(cudaSetDevice(dev));
+            g_masks = masks;
+            PhaseClock pc3(s3);
+            KernelIndexStore kis(nK, s3);
+            build_kernel_index(kis, c, TK.p, nK, s3);
+            ut_step(c, kis.KI, TT.p, nT, *in, s3);
+            pc3.mark("ut");
+            cudaEvent_t ev = pairs_ready.get();
+            if (!ev) return;  // pairing failed (reported by its chain)
+            CK(cudaStreamWaitEvent(s3, ev, 0));
+            ua_step(c, kis.KI, *in, s3);
+            pc3.mark("ua");
+            if (with_sv) {
+                const FindingsDev F = findings_dev(*in);
+                sv_add(R, 3, F, s3);
+                sv_add(R, 4, F, s3);
+            }
+            {
+                HostBatch hb;
+                hb.add(&f->ua_pairs, in->ua.p, in->n_ua);
+                hb.add(&f->ut_events, in->ut.p, in->n_ut);
+                in->slab_kern = new HostSlab();
+                hb.flush_async(*in->slab_kern, s3, sc);
+            }
+            if (overlap) CK(cudaStreamSynchronize(s3));
+        } catch (const EngineErr &e) {
+            err3 = e;
+            failed3 = true;
+        }
+    };
+    std::future<void> t2, t3;
+    if (overlap) {
+        t2 = workers().submit(pairs_chain);
+        t3 = workers().submit(kernel_chain);
+    } else {
+        pairs_chain();
+        kernel_chain();
+    }
+    auto join = [&] {
+        if (t2.valid()) t2.wait();
+        if (t3.valid()) t3.wait();
+        cudaEvent_t ev = pairs_ready.get();
+        if (ev) cudaEventDestroy(ev);
+    };
+    try {
+        DdRt dr = dd_rt_step(c, H.p, nH, (flags & B2L_ANALYZE_STRICT_RT) != 0, *in, s);
+        in->dd_groups = dr.dd_groups, in->dd_members = dr.dd_members, in->rt_groups = dr.rt_groups,
+        in->rt_trips = dr.rt_trips;
+        if (with_sv) {
+            const FindingsDev F = findings_dev(*in);
+            sv_add(R, 0, F, s);
+            sv_add(R, 1, F, s);
+        }
+    } catch (...) {
+        join();
+        throw;
+    }
+    join();
+    if (failed2) throw err2;
+    if (failed3) throw err3;
+    pc.mark("detectors");
+
+    // ---- results to the host: DD/RT now (the other chains queued theirs when they ended), then
+    // one synchronisation of the copy stream
+    HostBatch hb;
+    f->dd_groups = in->dd_groups;
+    hb.add(&f->dd_offsets, in->dd_off.p, in->dd_groups + 1);
+    hb.add(&f->dd_members, in->dd_mem.p, in->dd_members);
+    f->rt_groups = in->rt_groups;
+    hb.add(&f->rt_offsets, in->rt_off.p, in->rt_groups + 1);
+    hb.add(&f->rt_tx, in->rt_tx.p, in->rt_trips);
+    hb.add(&f->rt_rx, in->rt_rx.p, in->rt_trips);
+    in->slab = new HostSlab();
+    hb.flush_async(*in->slab, s, sc);
+    f->n_pairs = nA;
+    f->synthetic_end_ns = me;
+    f->n_warnings = po.n_warn;
+    f->ra_groups = in->ra_groups;
+    f->n_ua = in->n_ua;
+    f->n_ut = in->n_ut;
+    if (with_sv) {  // every category is in: sums, overlap / union scan, results on the copy stream
+        b2l_savings *o = (b2l_savings *)calloc(1, sizeof(b2l_savings));
+        if (!o) throw EngineErr{B2L_E_OOM, "host allocation failed"};
+        in->fused = o;
+        in->fused_key[0] = cols->seq, in->fused_key[1] = cols->start_ns, in->fused_key[2] = cols->hash;
+        in->fused_n = cols->n_events;
+        sv_finish(R, o, s, sc);
+    }
+    CK(cudaStreamSynchronize(sc));
+    pc.mark("d2h");
+    if (alloc_stats().on) {
+        fprintf(stderr, "[b2l] pool alloc/free calls %llu, host %.3f ms; arena %.1f of %.1f MB (%.0f B/event)\n",
+                (unsigned long long)alloc_stats().n.load(), alloc_stats().ns.load() * 1e-6,
+                arena.off.load() / 1048576.0, arena.cap / 1048576.0, n ? (double)arena.off.load() / n : 0.0);
+        fprintf(stderr, "[b2l] findings arena %.1f of %.1f MB\n", in->keep.off.load() / 1048576.0,
+                in->keep.cap / 1048576.0);
+        alloc_stats().n = 0, alloc_stats().ns = 0;
+    }
+    if (in->dd_groups == 0) f->dd_offsets[0] = 0;
+    if (in->rt_groups == 0) f->rt_offsets[0] = 0;
+    if (in->ra_groups == 0) f->ra_offsets[0] = 0;
+    return B2L_OK;
+}
+
+void findings_free(b2l_findings *f) {
+    if (!f) return;
+    Internal *in = (Internal *)f->internal;
+    if (in) {  // arrays live in the slabs
+        if (in->fused) savings_free(in->fused);
+        delete in->slab;
+        delete in->slab_pairs;
+        delete in->slab_kern;
+    }
+    delete in;
+    free(f);
 }
 
 // seq -> trace position (binary search over the ascending seq column)

@@ -18,11 +18,17 @@ pytestmark = pytest.mark.gpu
 
 
 def _check(cols, strict):
+    """Both savings paths: separate (b2l_savings_compute) and fused into the analyze call
+    (B2L_ANALYZE_WITH_SAVINGS, categories fed in as the detector chains finish)."""
     from paper_2601_12713_b200 import analyze_columns, savings_columns
     cf = analyze_columns(cols, strict=strict)
     sv = savings_columns(cols, cf)
     rf = R.analyze_cols(cols, strict=strict)
     assert full_parity(cols, cf, sv, rf=rf) == []
+    cf2 = analyze_columns(cols, strict=strict, with_savings=True)
+    assert cf2._handle.ptr.contents.internal  # the fused results ride on the findings
+    sv2 = savings_columns(cols, cf2)
+    assert full_parity(cols, cf2, sv2, rf=rf) == []
     return cf, rf
 
 
@@ -65,3 +71,6 @@ def test_c4_device_resident_matches_host(cuda):
     cf = analyze_columns(d)
     sv = savings_columns(d, cf)
     assert full_parity(cols, cf, sv) == []
+    cf = analyze_columns(d, with_savings=True)
+    assert full_parity(cols, cf, savings_columns(d, cf)) == []
+    assert full_parity(cols, cf, savings_columns(d, cf)) == []  # second call: computed again

@@ -22,7 +22,7 @@ cols = DeviceColumns(c) if a.device else c
 an, sv_t = [], []
 for i in range(a.iters):
     t = time.perf_counter()
-    cf = analyze_columns(cols)
+    cf = analyze_columns(cols, with_savings=True)
     t1 = time.perf_counter()
     sv = savings_columns(cols, cf)
     t2 = time.perf_counter()
