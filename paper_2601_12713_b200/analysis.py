@@ -6,6 +6,7 @@ Same signatures, results, ordering and errors as the reference:
   attribute(trace, findings) -> list[AttributedIssue]              report.py:73-95
 plus columnar entry points that skip Python objects entirely:
   analyze_columns(cols, strict=False) -> ColumnarFindings
+  analyze_many(traces) -> iterator of (ColumnarFindings, ColumnarSavings), uploads overlapped
   savings_columns(cols, cf) -> ColumnarSavings
 
 All detection and all integer sums run in CUDA (b2l_analyze / b2l_savings_compute);
@@ -129,17 +130,27 @@ class DeviceColumns:
     FIELDS = ("seq", "start_ns", "end_ns", "src_addr", "dst_addr", "bytes", "hash", "src_device", "dst_device",
               "kind", "loc", "loc_flags", "loc_bucket")
 
-    def __init__(self, cols: Columns, device="cuda"):
+    def __init__(self, cols: Columns, device="cuda", stream=None):
+        """Upload host columns; with ``stream`` the copies are queued on it (asynchronous from
+        page-locked memory) and ``ready`` is an event recorded after them."""
+        import contextlib
+
         import torch
         self.host = cols
         self.t = {}
-        for f in self.FIELDS:
-            a = getattr(cols, f)
-            if a.dtype == np.uint64:
-                a = a.view(np.int64)
-            elif a.dtype == np.uint32:
-                a = a.view(np.int32)
-            self.t[f] = torch.from_numpy(np.ascontiguousarray(a)).to(device)
+        self.ready = None
+        ctx = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+        with ctx:
+            for f in self.FIELDS:
+                a = getattr(cols, f)
+                if a.dtype == np.uint64:
+                    a = a.view(np.int64)
+                elif a.dtype == np.uint32:
+                    a = a.view(np.int32)
+                self.t[f] = torch.from_numpy(np.ascontiguousarray(a)).to(device, non_blocking=stream is not None)
+            if stream is not None:
+                self.ready = torch.cuda.Event()
+                self.ready.record(stream)
         ptr = lambda f: self.t[f].data_ptr() if self.t[f].numel() else None  # noqa: E731
         self.struct = _Cols(n_events=cols.n, num_devices_total=cols.num_devices_total, host_device=cols.host_device,
                             seq=ptr("seq"), start_ns=ptr("start_ns"), end_ns=ptr("end_ns"), src_addr=ptr("src_addr"),
@@ -172,6 +183,34 @@ class DeviceColumns:
                             loc_bucket=like.t["loc_bucket"].data_ptr() if like.t["loc_bucket"].numel() else None,
                             n_buckets=meta.n_buckets, device_resident=1)
         return self
+
+
+def analyze_many(traces, strict: bool = False, device=None, with_savings: bool = True):
+    """Analyse a sequence of host traces (Columns), yielding ``(ColumnarFindings,
+    ColumnarSavings | None)`` per trace, in order.  Trace k+1's columns are queued for upload on
+    a copy stream before trace k is analysed, so from page-locked host memory (``pinned_columns``)
+    the host->device traffic hides behind the analysis: the per-trace cost becomes
+    max(upload, analysis) instead of their sum.  Every trace's columns are still copied to the
+    device and its results back to the host (pageable columns upload synchronously: correct,
+    just not overlapped)."""
+    import torch
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    copy = torch.cuda.Stream(dev)
+    it = iter(traces)
+    nxt = None
+    for cols in it:
+        nxt = DeviceColumns(cols, dev, stream=copy)
+        break
+    while nxt is not None:
+        cur, nxt = nxt, None
+        for cols in it:  # queue the next upload before this trace's analysis
+            nxt = DeviceColumns(cols, dev, stream=copy)
+            break
+        cur.ready.synchronize()  # this trace's columns are on the device
+        cf = analyze_columns(cur, strict=strict, with_savings=with_savings)
+        sv = savings_columns(cur, cf) if with_savings else None
+        del cur  # analysed (the engine call is synchronous): its buffers may be reused
+        yield cf, sv
 
 
 def _view(ptr, n, dtype, owner):

@@ -478,11 +478,11 @@ GroupOrder order_groups(size_t ng, const uint64_t *start, const uint32_t *first_
         ordp = st.val();
     } else {
         for_each(ng, FirstStartKey{g_masks.srank, first_event, st2.in_key(0), st2.in_val()}, s);
-        CK(cudaMemcpyAsync(st2.in_key(1), tie, ng * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+        dev_copy(st2.in_key(1), tie, ng * sizeof(uint64_t), s);
         radix_sort<2>(st2.b, ng, LiveBytes<2>{{g_masks.idx, live_range(tie_bound)}}, s);
         ordp = st2.val();
     }
-    CK(cudaMemcpyAsync(go.order.p, ordp, ng * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    dev_copy(go.order.p, ordp, ng * sizeof(uint32_t), s);
     uint32_t *ord = go.order.p, *rk = go.rank.p;
     for_each(ng, [=] __device__(size_t r) { rk[ord[r]] = (uint32_t)r; }, s);
     return go;
@@ -564,7 +564,7 @@ struct HostBatch {
         stream_after(copy, after);
         size_t off = 0;
         for (auto &it : items) {
-            if (it.bytes) CK(cudaMemcpyAsync(slab.p + off, it.src, it.bytes, cudaMemcpyDeviceToHost, copy));
+            to_host_async(slab.p + off, it.src, it.bytes, copy);
             *it.dst = slab.p + off;
             off += (it.bytes + 63) & ~size_t(63);
         }
@@ -576,7 +576,7 @@ struct HostBatch {
         slab.p = slab_pool().acquire(total, slab.cap);
         size_t off = 0;
         for (auto &it : items) {
-            if (it.bytes) CK(cudaMemcpyAsync(slab.p + off, it.src, it.bytes, cudaMemcpyDeviceToHost, s));
+            to_host_async(slab.p + off, it.src, it.bytes, s);
             *it.dst = slab.p + off;
             off += (it.bytes + 63) & ~size_t(63);
         }
@@ -809,7 +809,7 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
     QState qt{};
     read_back(&qt, tot.p, sizeof(qt), s);
     const uint32_t nseg = qt.seg, nrx = qt.rx_glob;
-    CK(cudaMemcpyAsync(seg_rxbase.p + nseg, &tot.p->rx_glob, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    dev_copy(seg_rxbase.p + nseg, &tot.p->rx_glob, sizeof(uint32_t), s);
 
     pc.mark(" q-scan");
     // ---- DD groups need only the queue scan: on small traces they run on their own stream (and
@@ -837,7 +837,7 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
                 r.dd_groups = ng;
                 DBuf<uint32_t> first_ev(ng ? ng : 1, s), gsize(ng ? ng : 1, s), seg_group(nseg, s);
                 DBuf<uint64_t> tie(ng ? ng : 1, s);
-                CK(cudaMemsetAsync(seg_group.p, 0xFF, nseg * sizeof(uint32_t), s));
+                dev_memset(seg_group.p, 0xFF, nseg * sizeof(uint32_t), s);
                 {
                     const uint32_t *gs = gseg.p, *rp = rxpos.p, *ss = seg_start.p;
                     uint32_t *fe = first_ev.p, *sz = gsize.p, *sgp = seg_group.p;
@@ -856,8 +856,8 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
                 out.own(out.dd_off, ng + 1, s);
                 DBuf<uint64_t> total(1, s);
                 scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.dd_off.p}, s, total.p);
-                if (ng) CK(cudaMemcpyAsync(out.dd_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-                else CK(cudaMemsetAsync(out.dd_off.p, 0, sizeof(uint64_t), s));
+                if (ng) dev_copy(out.dd_off.p + ng, total.p, sizeof(uint64_t), s);
+                else dev_memset(out.dd_off.p, 0, sizeof(uint64_t), s);
                 out.own(out.dd_mem, nrx ? nrx : 1, s);  // members are receptions; count read after the scatter
                 // every reception of a grouped segment lands at off[rank] + (its rank within the segment)
                 const uint32_t *sgp = seg_group.p, *rk = go.rank.p, *so = seg_of.p, *rp = rxpos.p;
@@ -886,7 +886,7 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
     auto rt_groups = [&] {
         // ---- round trips: per send, the matched reception (or NONE)
         DBuf<uint32_t> match(nH, s);
-        CK(cudaMemsetAsync(match.p, 0xFF, nH * sizeof(uint32_t), s));
+        dev_memset(match.p, 0xFF, nH * sizeof(uint32_t), s);
         if (!strict) {
             scan<Seg<MaxI64>>(R, RtMaxLoad{sk, sval, f_of.p, j_of.p},
                               RtMatchStore{sval, j_of.p, seg_of.p, seg_rxbase.p, rxpos.p, H, match.p}, s);
@@ -968,7 +968,7 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
             out.own(out.rt_off, ng + 1, s);
             DBuf<uint64_t> total(1, s);
             scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.rt_off.p}, s, total.p);
-            CK(cudaMemcpyAsync(out.rt_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+            dev_copy(out.rt_off.p + ng, total.p, sizeof(uint64_t), s);
             const uint32_t *tg = trip_group.p, *rk = go.rank.p, *gs = gstart.p;
             const uint64_t *off = out.rt_off.p;
             uint32_t *otx = out.rt_tx.p, *orx = out.rt_rx.p;
@@ -1044,8 +1044,8 @@ PairOut pairs_step(const DevCols &c, const uint32_t *AD, uint32_t nAD, const uin
     po.n_pairs = nA;
     out.own(out.pair_alloc, nA ? nA : 1, s);
     out.own(out.pair_delete, nA ? nA : 1, s);
-    if (nA) CK(cudaMemcpyAsync(out.pair_alloc.p, A, nA * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-    if (nA) CK(cudaMemsetAsync(out.pair_delete.p, 0xFF, nA * sizeof(uint32_t), s));  // synthetic unless matched
+    if (nA) dev_copy(out.pair_alloc.p, A, nA * sizeof(uint32_t), s);
+    if (nA) dev_memset(out.pair_delete.p, 0xFF, nA * sizeof(uint32_t), s);  // synthetic unless matched
     po.warn.alloc(nAD ? nAD : 1, s);
     if (nAD == 0) return po;
     // event -> allocation rank (pairs are in allocation order, prep.py:95)
@@ -1169,8 +1169,8 @@ void ra_step(const DevCols &c, uint32_t nP, Internal &out, cudaStream_t s) {
     uint32_t cnts[2];
     {
         uint8_t *st = pinned(s).reserve(8);
-        CK(cudaMemcpyAsync(st, scount.p, 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(st + 4, gc.p, 4, cudaMemcpyDeviceToHost, s));
+        to_host_async(st, scount.p, 4, s);
+        to_host_async(st + 4, gc.p, 4, s);
         CK(cudaStreamSynchronize(s));
         memcpy(cnts, st, 8);
     }
@@ -1181,7 +1181,7 @@ void ra_step(const DevCols &c, uint32_t nP, Internal &out, cudaStream_t s) {
         return;
     }
     DBuf<uint32_t> first_ev(ng, s), gsize(ng, s), seg_group(nseg, s);
-    CK(cudaMemsetAsync(seg_group.p, 0xFF, nseg * sizeof(uint32_t), s));
+    dev_memset(seg_group.p, 0xFF, nseg * sizeof(uint32_t), s);
     {
         const uint32_t *gs = gseg.p;
         uint32_t *fe = first_ev.p, *sz = gsize.p, *sgp = seg_group.p;
@@ -1196,7 +1196,7 @@ void ra_step(const DevCols &c, uint32_t nP, Internal &out, cudaStream_t s) {
     out.own(out.ra_off, ng + 1, s);
     DBuf<uint64_t> total(1, s);
     scan<SumU64>(ng, SizeByRank{go.order.p, gsize.p}, StoreOffset{out.ra_off.p}, s, total.p);
-    CK(cudaMemcpyAsync(out.ra_off.p + ng, total.p, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    dev_copy(out.ra_off.p + ng, total.p, sizeof(uint64_t), s);
     out.own(out.ra_mem, nP, s);  // members <= pairs; the count is read once the scatter is queued
     const uint32_t *sgp = seg_group.p, *rk = go.rank.p, *so = seg_of.p;
     const uint64_t *off = out.ra_off.p;
@@ -1739,7 +1739,7 @@ void sv_begin(SvRun &R, const DevCols &c, cudaStream_t s) {
     R.nb = c.nbuckets;
     R.at.alloc(5 * (size_t)R.nb * 6 + 1, s);
     R.at.zero();
-    CK(cudaMemsetAsync(R.at.p + 5 * (size_t)R.nb * 5, 0xFF, 5 * (size_t)R.nb * sizeof(unsigned long long), s));
+    dev_memset(R.at.p + 5 * (size_t)R.nb * 5, 0xFF, 5 * (size_t)R.nb * sizeof(unsigned long long), s);
     R.smem = R.nb <= 512 ? (size_t)R.nb * 6 * sizeof(unsigned long long) : 0;
     R.cat.alloc(((R.n ? R.n : 1) + 3) & ~size_t(3), s);  // whole words: byte atomics touch the word
     R.cat.zero();
@@ -1809,10 +1809,7 @@ void sv_finish(SvRun &R, b2l_savings *o, cudaStream_t s, cudaStream_t copy) {
     const DevCols c = R.c;
     R.acc.alloc(12 + 1 + 2, s);
     R.acc.zero();
-    {
-        unsigned long long init[2] = {~0ull, 0ull};
-        CK(cudaMemcpyAsync(R.acc.p + 13, init, sizeof(init), cudaMemcpyHostToDevice, s));
-    }
+    dev_memset(R.acc.p + 13, 0xFF, sizeof(unsigned long long), s);  // min start := ~0 (max end stays 0)
     if (n) {
         k_sums<<<grid_for(n, TPB, 148 * 4), TPB, 0, s>>>(c, R.cat.p, R.acc.p, R.acc.p + 12, R.acc.p + 13);
         CK_LAUNCH("k_sums");
@@ -1825,15 +1822,15 @@ void sv_finish(SvRun &R, b2l_savings *o, cudaStream_t s, cudaStream_t copy) {
     R.unic.alloc(1, s);
     R.ovt.alloc(1, s);
     scan<OvUn>(n, OvUnLoad{c.end, R.cat.p}, OvUnStore{c.start, R.cat.p, R.ovl.p, R.uni.p}, s, R.ovt.p);
-    if (n) CK(cudaMemcpyAsync(R.unic.p, &R.ovt.p->cnt, 4, cudaMemcpyDeviceToDevice, s));
+    if (n) dev_copy(R.unic.p, &R.ovt.p->cnt, 4, s);
     else R.unic.zero();
     unsigned long long h[15];
     uint32_t hov = 0, hun = 0;
     {  // one synchronisation for the three small results
         uint8_t *st = pinned(s).reserve(sizeof(h) + 8);
-        CK(cudaMemcpyAsync(st, R.acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(st + sizeof(h), R.ovl.p, 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(st + sizeof(h) + 4, R.unic.p, 4, cudaMemcpyDeviceToHost, s));
+        to_host_async(st, R.acc.p, sizeof(h), s);
+        to_host_async(st + sizeof(h), R.ovl.p, 4, s);
+        to_host_async(st + sizeof(h) + 4, R.unic.p, 4, s);
         CK(cudaStreamSynchronize(s));
         memcpy(h, st, sizeof(h));
         memcpy(&hov, st + sizeof(h), 4);
@@ -1982,7 +1979,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     DBuf<FrontAcc> fpart(ftiles + 1, s);
     DBuf<unsigned long long> agg(11, s);  // [0] max data-op end, [1..5] subset OR, [6..10] subset AND
     agg.zero();
-    CK(cudaMemsetAsync(agg.p + 6, 0xFF, 5 * sizeof(unsigned long long), s));
+    dev_memset(agg.p + 6, 0xFF, 5 * sizeof(unsigned long long), s);
     FrontAcc ftot{};
     unsigned long long hm[11] = {0, 0, 0, 0, 0, 0, ~0ull, ~0ull, ~0ull, ~0ull, ~0ull};
     // the five partition lists are sized n (an upper bound) so the apply pass is queued right
@@ -2004,8 +2001,8 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
         uint8_t rb[sizeof(FrontAcc) + sizeof(hm)];
         {
             uint8_t *st = pinned(s).reserve(sizeof(rb));
-            CK(cudaMemcpyAsync(st, fpart.p + ftiles, sizeof(FrontAcc), cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(st + sizeof(FrontAcc), agg.p, sizeof(hm), cudaMemcpyDeviceToHost, s));
+            to_host_async(st, fpart.p + ftiles, sizeof(FrontAcc), s);
+            to_host_async(st + sizeof(FrontAcc), agg.p, sizeof(hm), s);
             CK(cudaStreamSynchronize(s));
             memcpy(rb, st, sizeof(rb));
         }
@@ -2534,19 +2531,19 @@ int b2l_sort_u64_pairs_device(const uint64_t *d_k0, const uint64_t *d_k1, uint64
         arena.open(n <= ana::ARENA_MAX_EVENTS ? ana::ARENA_BASE + n * 64 : 0, s);
         ArenaUse arena_use(&arena);
         SortStore<2> st(n, s);
-        CK(cudaMemcpyAsync(st.in_key(0), d_k0, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-        CK(cudaMemcpyAsync(st.in_key(1), d_k1, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+        dev_copy(st.in_key(0), d_k0, n * sizeof(uint64_t), s);
+        dev_copy(st.in_key(1), d_k1, n * sizeof(uint64_t), s);
         uint32_t *v = st.in_val();
         ana::for_each(n, [=] __device__(size_t i) { v[i] = (uint32_t)i; }, s);
         DBuf<unsigned long long> m(4, s);
-        CK(cudaMemsetAsync(m.p, 0, 2 * sizeof(unsigned long long), s));
-        CK(cudaMemsetAsync(m.p + 2, 0xFF, 2 * sizeof(unsigned long long), s));
+        dev_memset(m.p, 0, 2 * sizeof(unsigned long long), s);
+        dev_memset(m.p + 2, 0xFF, 2 * sizeof(unsigned long long), s);
         b2l::ana::k_or_and2<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(d_k0, d_k1, n, m.p);  // live digit bytes
         CK_LAUNCH("k_or_and2");
         unsigned long long hm[4];
         read_back(hm, m.p, sizeof(hm), s);
         radix_sort<2>(st.b, n, LiveBytes<2>{{live_mask(hm[0] ^ hm[2]), live_mask(hm[1] ^ hm[3])}}, s);
-        CK(cudaMemcpyAsync(d_perm, st.val(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        dev_copy(d_perm, st.val(), n * sizeof(uint32_t), s);
         CK(cudaStreamSynchronize(s));
         return B2L_OK;
     } catch (const b2l::EngineErr &e) {

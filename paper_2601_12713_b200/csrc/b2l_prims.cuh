@@ -102,6 +102,45 @@ struct ArenaUse {
     ~ArenaUse() { t_arena = prev; }
 };
 
+// Device-side fill / copy as kernels, never through a copy engine: the engines may be busy with a
+// large host->device upload (analyze_many queues the next trace's upload beside this analysis), and
+// a memset or device-to-device copy queued behind it would stall the whole dependent chain.
+static __global__ void k_fill_bytes(uint8_t *__restrict__ p, size_t n, uint32_t v4) {
+    const size_t head = (16 - ((uintptr_t)p & 15)) & 15;
+    const size_t h = head < n ? head : n;
+    const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = tid; i < h; i += stride) p[i] = (uint8_t)v4;
+    const size_t nv = (n - h) / 16;
+    uint4 *q = reinterpret_cast<uint4 *>(p + h);
+    for (size_t i = tid; i < nv; i += stride) q[i] = make_uint4(v4, v4, v4, v4);
+    for (size_t i = h + nv * 16 + tid; i < n; i += stride) p[i] = (uint8_t)v4;
+}
+static __global__ void k_copy_bytes(uint8_t *__restrict__ d, const uint8_t *__restrict__ s, size_t n) {
+    const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+    if ((((uintptr_t)d | (uintptr_t)s) & 15) == 0) {
+        const size_t nv = n / 16;
+        for (size_t i = tid; i < nv; i += stride) reinterpret_cast<uint4 *>(d)[i] = reinterpret_cast<const uint4 *>(s)[i];
+        for (size_t i = nv * 16 + tid; i < n; i += stride) d[i] = s[i];
+    } else {
+        for (size_t i = tid; i < n; i += stride) d[i] = s[i];
+    }
+}
+inline unsigned fill_grid(size_t bytes) {
+    const size_t b = (bytes / 16 + 255) / 256;
+    return (unsigned)(b < 1 ? 1 : (b > 148 * 8 ? 148 * 8 : b));
+}
+inline void dev_memset(void *p, int v, size_t bytes, cudaStream_t s) {
+    if (!bytes) return;
+    const uint32_t b = (uint32_t)(v & 0xFF);
+    k_fill_bytes<<<fill_grid(bytes), 256, 0, s>>>((uint8_t *)p, bytes, b | (b << 8) | (b << 16) | (b << 24));
+    CK(cudaGetLastError());
+}
+inline void dev_copy(void *d, const void *src, size_t bytes, cudaStream_t s) {
+    if (!bytes) return;
+    k_copy_bytes<<<fill_grid(bytes), 256, 0, s>>>((uint8_t *)d, (const uint8_t *)src, bytes);
+    CK(cudaGetLastError());
+}
+
 template <class T>
 struct DBuf {
     T *p = nullptr;
@@ -126,7 +165,7 @@ struct DBuf {
         CK(cudaMallocAsync((void **)&p, n_ * sizeof(T), st));
     }
     void zero() {
-        if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+        if (n) dev_memset(p, 0, n * sizeof(T), s);
     }
     void release() {
         if (p && !arena) {
@@ -500,7 +539,7 @@ template <class Op, class Load, class Store>
 void scan(size_t n, Load ld, Store st, cudaStream_t s, typename Op::T *d_total = nullptr) {
     using T = typename Op::T;
     if (n == 0) {  // only sums are scanned with a device total over possibly-empty ranges
-        if (d_total) CK(cudaMemsetAsync(d_total, 0, sizeof(T), s));
+        if (d_total) dev_memset(d_total, 0, sizeof(T), s);
         return;
     }
     constexpr bool striped = scan_striped<Store>::value;
@@ -511,7 +550,7 @@ void scan(size_t n, Load ld, Store st, cudaStream_t s, typename Op::T *d_total =
     const size_t tv = (tiles * sizeof(T) + 15) & ~size_t(15);
     DBuf<uint8_t> ws(fwords * 4 + 2 * tv, s);
     uint32_t *flag = reinterpret_cast<uint32_t *>(ws.p);
-    CK(cudaMemsetAsync(flag, 0, fwords * 4, s));
+    dev_memset(flag, 0, fwords * 4, s);
     T *agg = reinterpret_cast<T *>(ws.p + fwords * 4), *inc = reinterpret_cast<T *>(ws.p + fwords * 4 + tv);
     if constexpr (striped) {
         constexpr size_t smem = scan_smem<T>();
@@ -593,10 +632,16 @@ inline SlabPool &slab_pool() {
     return pool;
 }
 
+// Device->host reads go through the copy engine of that direction (it stays free while the
+// other direction carries analyze_many's next upload; a kernel storing into mapped host memory
+// would instead wait on the busy PCIe link for its write acknowledgements).
+inline void to_host_async(void *h_pinned, const void *d_src, size_t bytes, cudaStream_t s) {
+    if (bytes) CK(cudaMemcpyAsync(h_pinned, d_src, bytes, cudaMemcpyDeviceToHost, s));
+}
 // Read `bytes` from device memory into host `dst` (synchronous).
 inline void read_back(void *dst, const void *d_src, size_t bytes, cudaStream_t s) {
     uint8_t *st = pinned(s).reserve(bytes);
-    CK(cudaMemcpyAsync(st, d_src, bytes, cudaMemcpyDeviceToHost, s));
+    to_host_async(st, d_src, bytes, s);
     CK(cudaStreamSynchronize(s));
     memcpy(dst, st, bytes);
 }
@@ -619,7 +664,7 @@ struct CompactStore {
 template <class Pred>
 void compact(size_t n, Pred pred, uint32_t *out, uint32_t *d_count, cudaStream_t s) {
     if (n == 0) {
-        CK(cudaMemsetAsync(d_count, 0, sizeof(uint32_t), s));
+        dev_memset(d_count, 0, sizeof(uint32_t), s);
         return;
     }
     scan<SumU32>(n, FlagLoad<Pred>{pred}, CompactStore<Pred>{pred, out}, s, d_count);

@@ -106,3 +106,18 @@ def test_foreign_findings_mismatch(cuda):
     if f.unused_transfers or f.duplicates:
         with pytest.raises(FindingsTraceMismatch):
             estimate(other, f)
+
+
+def test_analyze_many_pipelined_matches_single_calls(cuda):
+    """analyze_many (upload of trace k+1 overlapped with the analysis of trace k) gives, per
+    trace and in order, exactly the single-call results."""
+    from oracle.compare import full_parity
+    from paper_2601_12713_b200 import analyze_many
+    from paper_2601_12713_b200.analysis import pinned_columns
+    from paper_2601_12713_b200.synth import c2_trace, c3_trace, c4_trace
+    traces = [pinned_columns(c2_trace(20_000, seed=5)), c4_trace(30_000, seed=6), c3_trace(500),
+              pinned_columns(c2_trace(5, seed=1))]
+    got = list(analyze_many(traces))
+    assert len(got) == len(traces)
+    for cols, (cf, sv) in zip(traces, got):
+        assert full_parity(cols, cf, sv) == []

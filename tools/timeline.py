@@ -21,6 +21,8 @@ ap.add_argument("--n", type=int, default=1_000_000)
 ap.add_argument("--json", default=None)
 ap.add_argument("--host", action="store_true", help="host columns (e2e) instead of device-resident")
 ap.add_argument("--streams", action="store_true", help="print every op per stream")
+ap.add_argument("--many", type=int, default=0, help="profile analyze_many over this many copies of the trace")
+ap.add_argument("--bg-h2d", action="store_true", help="a 400 MB host->device copy runs beside the analysis")
 a = ap.parse_args()
 gen = {"c2": lambda: c2_trace(a.n), "c3": lambda: c3_trace(max(1, a.n // 3)), "c4": lambda: c4_trace(a.n)}[a.config]
 c = gen()
@@ -31,11 +33,30 @@ if a.host:
 for _ in range(5):
     savings_columns(cols, analyze_columns(cols, with_savings=True))
 torch.cuda.synchronize()
+if a.many:
+    from paper_2601_12713_b200.analysis import analyze_many, pinned_columns
+    pc = pinned_columns(c)
+    for _ in analyze_many([pc] * 3):
+        pass
+if a.bg_h2d:
+    big = torch.empty(400 << 20, dtype=torch.uint8, pin_memory=True)
+    dbig = torch.empty(400 << 20, dtype=torch.uint8, device="cuda")
+    bgs = torch.cuda.Stream()
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+    if a.bg_h2d:
+        with torch.cuda.stream(bgs):
+            dbig.copy_(big, non_blocking=True)
     t0 = time.perf_counter()
-    cf = analyze_columns(cols, with_savings=True)
-    t1 = time.perf_counter()
-    savings_columns(cols, cf)
+    if a.many:
+        marks = [time.perf_counter()]
+        for _ in analyze_many([pc] * a.many):
+            marks.append(time.perf_counter())
+        print("analyze_many step ms:", [round(1e3 * (y - x), 3) for x, y in zip(marks, marks[1:])])
+        t1 = time.perf_counter()
+    else:
+        cf = analyze_columns(cols, with_savings=True)
+        t1 = time.perf_counter()
+        savings_columns(cols, cf)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
 evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
