@@ -52,6 +52,9 @@ __device__ __forceinline__ void cursor_load(BufCursor &c, const uint64_t *__rest
     c.pos = 0;
 }
 
+#ifndef PF_STEP
+#define PF_STEP fnv_step32_lat
+#endif
 // Hash one staged chunk (`bytes` stream bytes starting at stream offset cs.pos) into (h, prev).
 // Word j of the payload is stream u64 q = q0 + j, or -- when start % 8 != 0 -- the funnel of
 // stream u64s (q0+j, q0+j+1), emitted at q0+j+1.
@@ -74,8 +77,8 @@ __device__ __forceinline__ void consume_chunk(const BufCursor &cs, uint32_t byte
         uint32_t hl = (uint32_t)h, hh = (uint32_t)(h >> 32);
 #pragma unroll
         for (int i = 0; i < CH / 16; ++i) {
-            fnv_step32_lat(hl, hh, v[i].x, v[i].y);
-            fnv_step32_lat(hl, hh, v[i].z, v[i].w);
+            PF_STEP(hl, hh, v[i].x, v[i].y);
+            PF_STEP(hl, hh, v[i].z, v[i].w);
         }
         h = ((uint64_t)hh << 32) | hl;
     } else if (r == 0 && interior) {
@@ -97,8 +100,8 @@ __device__ __forceinline__ void consume_chunk(const BufCursor &cs, uint32_t byte
             uint64_t w0 = (prev >> sh) | (u0 << (64 - sh));
             uint64_t w1 = (u0 >> sh) | (u1 << (64 - sh));
             if (PF) {
-                fnv_step32_lat(hl, hh, (uint32_t)w0, (uint32_t)(w0 >> 32));
-                fnv_step32_lat(hl, hh, (uint32_t)w1, (uint32_t)(w1 >> 32));
+                PF_STEP(hl, hh, (uint32_t)w0, (uint32_t)(w0 >> 32));
+                PF_STEP(hl, hh, (uint32_t)w1, (uint32_t)(w1 >> 32));
             } else {
                 fnv_step32(hl, hh, (uint32_t)w0, (uint32_t)(w0 >> 32));
                 fnv_step32(hl, hh, (uint32_t)w1, (uint32_t)(w1 >> 32));
@@ -308,6 +311,247 @@ __global__ void __launch_bounds__(WARPS * 32) k_hash_coop(const uint64_t *__rest
     cp_async_wait<0>();
 }
 
+// ============================================================================ split pair
+// Two warps fold ONE long buffer.  h = (h ^ w) * P mod 2^64 with P = 2^40 + 435 splits into two
+// 32-bit recurrences (hashing.py:38-40):
+//   lo' = lo32(xl * 435)                                  xl = lo ^ wl  (needs only the low halves)
+//   hi' = xh * 435 + c,   c = hi32(xl * 435) + (xl << 8)   xh = hi ^ wh
+// Each is one LOP3 -> IMAD dependency (~10 cycles/word), but one thread running both, plus the
+// IMAD.HI behind c (a quarter-rate op), needs ~16-20 cycles per word (tools/chain_bench.cu).
+// So warp A runs the low chain and publishes every xl; warp B computes the c values of a whole
+// chunk with 32 lanes at once (off its chain, interleaved with the previous chunk's fold) and
+// runs the high chain one chunk behind.  Warp A streams the buffer through an S-slot smem ring
+// (coalesced 16-B cp.async, D chunks in flight); per-slot mbarriers hand a chunk (payload + xl)
+// from A to B ("full", 32 arrivals) and the slot back from B to A ("empty", 32 arrivals).  B
+// finishes the digest.  Chunks are 2 KiB: a chunk's synchronisation (cp.async wait, mbarrier
+// try_wait ~90 cycles even when complete, arrive) costs ~300 cycles, ~1 cycle/word at 256 words.
+// Only 16-B aligned buffers take this path (the halves are then plain 32-bit words).
+//
+// Both roles run warp-uniform code (every lane computes the chain; lane 0's copy is the one
+// stored), so side work sits in the chain's basic block and fills its dependency stalls.  A
+// chunk is folded in 32-word blocks held in registers; the next block's shared-memory loads are
+// issued before the current block is folded (program order: ptxas keeps loads behind earlier
+// stores to the same array), and a block's xl values are stored after it is folded (stores
+// interleaved with the chain stall it on register reuse).  The block loop stays rolled (two
+// blocks per iteration): fully unrolled chunks made the warps stall on instruction fetch once
+// more than ~40 SMs ran them (ncu: "no_instructions" 5% -> 31% of samples).
+constexpr int SPLIT_S = 4, SPLIT_D = 1, SPLIT_CH = 4096;
+#ifndef B2L_SPLIT_UNROLL
+#define B2L_SPLIT_UNROLL 4
+#endif
+constexpr int SPLIT_UNROLL = B2L_SPLIT_UNROLL;  // block pairs per loop iteration
+constexpr int SPLIT_BW = 32;                            // words per register block
+constexpr int SPLIT_NB = SPLIT_CH / 8 / SPLIT_BW;        // blocks per chunk
+constexpr int SPLIT_CW = SPLIT_CH / 8;                   // words per chunk
+constexpr uint64_t SPLIT_MIN_BYTES = 64 << 10;
+struct SplitBars {
+    uint64_t full[SPLIT_S], empty[SPLIT_S];
+};
+// per-pair shared memory: payload ring, published xl per slot, c values (two chunks), lo states
+constexpr size_t SPLIT_RING = (size_t)SPLIT_S * SPLIT_CH;
+constexpr size_t SPLIT_XB = (size_t)SPLIT_S * SPLIT_CW * 4, SPLIT_CB = 2ull * SPLIT_CW * 4, SPLIT_HLB = 16 * 4;
+constexpr size_t SPLIT_PAIR = SPLIT_RING + SPLIT_XB + SPLIT_CB + SPLIT_HLB;
+#ifdef B2L_SPLIT_PROF  // tools/split_bench.cu: cycles each role spends waiting
+__device__ long long g_split_wait[2];
+#define SPLIT_WAIT(role, bar, par)                       \
+    do {                                                 \
+        long long t0_ = clock64();                       \
+        mbar_wait(bar, par);                             \
+        if (threadIdx.x % 32 == 0) atomicAdd((unsigned long long *)&g_split_wait[role], clock64() - t0_); \
+    } while (0)
+#else
+#define SPLIT_WAIT(role, bar, par) mbar_wait(bar, par)
+#endif
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ uint32_t split_words(uint64_t nwf, uint64_t k) {
+    const uint64_t w0 = k * SPLIT_CW;
+    return nwf > w0 ? (uint32_t)(nwf - w0 < (uint64_t)SPLIT_CW ? nwf - w0 : (uint64_t)SPLIT_CW) : 0u;
+}
+// 128-bit shared loads in program order (ptxas otherwise splits the strided halves into 32-bit
+// LDS, one per word -- more in-flight loads than a warp's scoreboards cover, ~3.5 cycles/word)
+__device__ __forceinline__ uint4 lds128(const void *p) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(smem_u32(p)));
+    return v;
+}
+// the low (HI = 0) or high (HI = 1) halves of block `blk` of chunk k
+template <int HI>
+__device__ __forceinline__ void split_load(uint32_t (&w)[SPLIT_BW], const uint8_t *ring, uint64_t k, int blk) {
+    const uint8_t *src = ring + (k % SPLIT_S) * SPLIT_CH + blk * SPLIT_BW * 8;
+#pragma unroll
+    for (int j = 0; j < SPLIT_BW / 2; ++j) {
+        const uint4 v = lds128(src + 16 * j);
+        w[2 * j] = HI ? v.y : v.x;
+        w[2 * j + 1] = HI ? v.w : v.z;
+    }
+}
+__device__ __forceinline__ void split_lo_block(uint32_t &hl, const uint32_t (&w)[SPLIT_BW], uint32_t *xdst, bool st) {
+    uint32_t x[SPLIT_BW];
+#pragma unroll
+    for (int j = 0; j < SPLIT_BW; ++j) {
+        x[j] = hl ^ w[j];
+        asm("mul.lo.u32 %0, %1, 435;" : "=r"(hl) : "r"(x[j]));
+    }
+    if (st) {
+        uint4 *d4 = reinterpret_cast<uint4 *>(xdst);
+#pragma unroll
+        for (int j = 0; j < SPLIT_BW; j += 4) d4[j / 4] = make_uint4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+    }
+}
+__device__ __forceinline__ void split_c_load(uint32_t (&c)[SPLIT_BW], const uint32_t *cc, int blk) {
+#pragma unroll
+    for (int j = 0; j < SPLIT_BW / 4; ++j) {
+        const uint4 v = lds128(cc + blk * SPLIT_BW + 4 * j);
+        c[4 * j] = v.x, c[4 * j + 1] = v.y, c[4 * j + 2] = v.z, c[4 * j + 3] = v.w;
+    }
+}
+__device__ __forceinline__ void split_hi_block(uint32_t &hh, const uint32_t (&w)[SPLIT_BW], const uint32_t (&c)[SPLIT_BW]) {
+#pragma unroll
+    for (int j = 0; j < SPLIT_BW; ++j) asm("mad.lo.u32 %0, %1, 435, %2;" : "=r"(hh) : "r"(hh ^ w[j]), "r"(c[j]));
+}
+
+// role 0 (warp A)
+__device__ __forceinline__ void split_lo(const BufCursor &cur, int lane, uint8_t *pair_smem, SplitBars *b, uint64_t base) {
+    uint8_t *ring = pair_smem;
+    uint32_t *xb = reinterpret_cast<uint32_t *>(pair_smem + SPLIT_RING);
+    uint32_t *hlb = reinterpret_cast<uint32_t *>(pair_smem + SPLIT_RING + SPLIT_XB + SPLIT_CB);
+    const uint32_t ring_s = smem_u32(ring);
+    const uint64_t nch = (cur.L + SPLIT_CH - 1) / SPLIT_CH, nwf = cur.n >> 3;
+    auto issue = [&](uint64_t k) {
+        if (k < nch) {
+            const uint64_t g = base + k;  // pair-lifetime chunk number: slot and barrier phase
+            if (g >= SPLIT_S) SPLIT_WAIT(0, &b->empty[g % SPLIT_S], (uint32_t)((g / SPLIT_S - 1) & 1));
+            const uint64_t off = k * SPLIT_CH;
+            const uint64_t rem = cur.L - off;
+            const uint32_t bytes = rem < SPLIT_CH ? (uint32_t)rem : SPLIT_CH;
+            const uint32_t dst = ring_s + (uint32_t)((g % SPLIT_S) * SPLIT_CH);
+#pragma unroll
+            for (int i = 0; i < SPLIT_CH / 512; ++i) {
+                const uint32_t o = (uint32_t)(512 * i + 16 * lane);
+                if (o < bytes) cp_async16(dst + o, cur.a0 + off + o);
+            }
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int k = 0; k < SPLIT_D; ++k) issue(k);
+    uint32_t hl = (uint32_t)FNV_OFFSET;
+    uint32_t wa[SPLIT_BW], wb[SPLIT_BW];
+    cp_async_wait<SPLIT_D - 1>();  // chunk 0 landed (this lane's pieces) ...
+    __syncwarp();                  // ... and every lane's
+    split_load<0>(wa, ring, base, 0);
+    for (uint64_t k = 0; k < nch; ++k) {
+        const int s = (int)((base + k) % SPLIT_S);
+        const uint32_t words = split_words(nwf, k);
+        uint32_t *xs = xb + s * SPLIT_CW;
+        issue(k + SPLIT_D);
+        if (words == SPLIT_CW) {
+#pragma unroll(SPLIT_UNROLL)
+            for (int blk = 0; blk < SPLIT_NB; blk += 2) {  // rolled: the whole GPU runs this code, so
+                                                           // it must stay in the instruction caches
+                split_load<0>(wb, ring, base + k, blk + 1);
+                split_lo_block(hl, wa, xs + blk * SPLIT_BW, lane == 0);
+                if (blk + 2 < SPLIT_NB) {
+                    split_load<0>(wa, ring, base + k, blk + 2);
+                } else if (k + 1 < nch) {
+                    cp_async_wait<SPLIT_D - 1>();  // chunk k+1 landed (this lane's pieces) ...
+                    __syncwarp();                  // ... and every lane's
+                    split_load<0>(wa, ring, base + k + 1, 0);
+                }
+                split_lo_block(hl, wb, xs + (blk + 1) * SPLIT_BW, lane == 0);
+            }
+        } else {  // the last, partial chunk
+            const uint32_t *s32 = reinterpret_cast<const uint32_t *>(ring + s * SPLIT_CH);
+            for (uint32_t j = 0; j < words; ++j) {
+                const uint32_t x = hl ^ s32[2 * j];
+                if (lane == 0) xs[j] = x;
+                hl = x * 435u;
+            }
+        }
+        if (lane == 0) hlb[s] = hl;
+        __syncwarp();
+        mbar_arrive(&b->full[s]);
+    }
+    cp_async_wait<0>();
+}
+
+// role 1 (warp B)
+__device__ __forceinline__ void split_hi(const BufCursor &cur, int lane, uint8_t *pair_smem, SplitBars *b,
+                                         uint64_t *__restrict__ digests, uint64_t base) {
+    const uint8_t *ring = pair_smem;
+    const uint32_t *xb = reinterpret_cast<const uint32_t *>(pair_smem + SPLIT_RING);
+    uint32_t *cb = reinterpret_cast<uint32_t *>(pair_smem + SPLIT_RING + SPLIT_XB);
+    const uint32_t *hlb = reinterpret_cast<const uint32_t *>(pair_smem + SPLIT_RING + SPLIT_XB + SPLIT_CB);
+    const uint64_t nch = (cur.L + SPLIT_CH - 1) / SPLIT_CH, nwf = cur.n >> 3;
+    // c of chunk k into cb[k & 1] (chunk k's "full" already waited)
+    auto make_c = [&](uint64_t k) {
+        const uint32_t words = split_words(nwf, k);
+        const uint32_t *x32 = xb + ((base + k) % SPLIT_S) * SPLIT_CW;
+        uint32_t *c = cb + (k & 1) * SPLIT_CW;
+#pragma unroll
+        for (int h = 0; h < SPLIT_CW / 32; ++h) {
+            const uint32_t j = (uint32_t)lane + 32u * h;
+            if (j < words) {
+                const uint32_t x = x32[j];
+                c[j] = __umulhi(x, 435u) + (x << 8);
+            }
+        }
+    };
+    SPLIT_WAIT(1, &b->full[base % SPLIT_S], (uint32_t)((base / SPLIT_S) & 1));
+    make_c(0);
+    __syncwarp();
+    uint32_t hh = (uint32_t)(FNV_OFFSET >> 32);
+    uint32_t wa[SPLIT_BW], wb[SPLIT_BW], ca[SPLIT_BW], cr[SPLIT_BW];
+    split_load<1>(wa, ring, base, 0);
+    split_c_load(ca, cb, 0);
+    for (uint64_t k = 0; k < nch; ++k) {
+        const int s = (int)((base + k) % SPLIT_S);
+        const uint32_t words = split_words(nwf, k);
+        const uint32_t *cc = cb + (k & 1) * SPLIT_CW;
+        if (k + 1 < nch) {  // the next chunk's c values, computed beside this chunk's chain
+            SPLIT_WAIT(1, &b->full[(base + k + 1) % SPLIT_S], (uint32_t)(((base + k + 1) / SPLIT_S) & 1));
+            make_c(k + 1);
+        }
+        if (words == SPLIT_CW) {
+#pragma unroll(SPLIT_UNROLL)
+            for (int blk = 0; blk < SPLIT_NB; blk += 2) {  // rolled: the whole GPU runs this code, so
+                                                           // it must stay in the instruction caches
+                split_load<1>(wb, ring, base + k, blk + 1);
+                split_c_load(cr, cc, blk + 1);
+                split_hi_block(hh, wa, ca);
+                if (blk + 2 < SPLIT_NB) {
+                    split_load<1>(wa, ring, base + k, blk + 2);
+                    split_c_load(ca, cc, blk + 2);
+                } else if (k + 1 < nch) {
+                    __syncwarp();  // the next chunk's c values are in
+                    split_load<1>(wa, ring, base + k + 1, 0);
+                    split_c_load(ca, cb + ((k + 1) & 1) * SPLIT_CW, 0);
+                }
+                split_hi_block(hh, wb, cr);
+            }
+        } else {  // the last, partial chunk
+            const uint32_t *s32 = reinterpret_cast<const uint32_t *>(ring + s * SPLIT_CH);
+            for (uint32_t j = 0; j < words; ++j) hh = (hh ^ s32[2 * j + 1]) * 435u + cc[j];
+        }
+        if (k + 1 == nch && lane == 0) {  // both halves of the last full word are in: tail word + finish
+            uint64_t h = ((uint64_t)hh << 32) | hlb[s];
+            const uint32_t tailb = (uint32_t)(cur.n & 7);
+            if (tailb) {
+                const uint64_t *s64 = reinterpret_cast<const uint64_t *>(ring + s * SPLIT_CH);
+                const uint64_t w = s64[(uint32_t)(nwf - k * SPLIT_CW)] & ((1ull << (8 * tailb)) - 1);
+                h = fnv_step(h, w);
+            }
+            digests[cur.idx] = finish_digest(h, cur.n);
+        }
+        __syncwarp();  // this slot fully read
+        mbar_arrive(&b->empty[s]);
+    }
+}
+
 // Launch configurations (lanes per CTA, chunk bytes, ring depth).  Selected at
 // first use; B2L_HASH_CFG=<i> overrides (used by the tuning sweep).
 // ============================================================================ variant W
@@ -316,65 +560,131 @@ __global__ void __launch_bounds__(WARPS * 32) k_hash_coop(const uint64_t *__rest
 // per chunk instead of 32 shuffled ones), an S-deep ring per warp, and lane 0 runs the serial
 // chain out of shared memory.  A lone chain is then bound by its own dependency latency, not by
 // the cooperative ring's per-round issue cost (the longest C1 buffer sets the batch time).
+template <int S>
+__device__ __forceinline__ void warp_fold(BufCursor ld, int lane, uint8_t *ring, uint64_t *__restrict__ digests) {
+    constexpr int CH = 512;
+    const uint32_t ring_s = smem_u32(ring);
+    BufCursor cs = ld;
+    if (cs.L == 0) {
+        if (lane == 0) digests[cs.idx] = 0;
+        return;
+    }
+    auto issue = [&](int st) {
+        if (ld.pos < ld.L) {
+            const uint32_t b = chunk_bytes(ld, CH);
+            if ((uint32_t)(16 * lane) < b) cp_async16(ring_s + (uint32_t)(st * CH + 16 * lane), ld.a0 + ld.pos + 16 * lane);
+            ld.pos += b;
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int st = 0; st < S - 1; ++st) issue(st);
+    uint64_t h = FNV_OFFSET, prev = 0;
+    int st = 0;
+    while (cs.pos < cs.L) {
+        cp_async_wait<S - 2>();
+        __syncwarp();
+        issue(st == 0 ? S - 1 : st - 1);
+        const uint32_t bytes = chunk_bytes(cs, CH);
+        if (lane == 0) consume_chunk<CH, true>(cs, bytes, reinterpret_cast<const uint4 *>(ring + st * CH), h, prev);
+        cs.pos += bytes;
+        st = st + 1 == S ? 0 : st + 1;
+        __syncwarp();  // the slot is re-filled only after lane 0 has read it
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+    if (lane == 0) digests[cs.idx] = finish_digest(h, cs.n);
+}
+
+// Work is claimed dynamically from per-launch counters (`WarpSched`, zeroed before the launch):
+// the first CTA to start on each SM (a per-SM ticket) is a LEAD CTA -- with `split` = P > 0 its
+// two warp pairs claim list positions 0..P-1 (the longest buffers) one at a time and fold each
+// as a split pair (lo chain on warp 2p, hi chain on warp 2p+1: different schedulers), or with
+// warp A alone when a buffer is short or unaligned; every other warp, and the lead warps once
+// those positions are gone, claims the next position of [P, n) and folds it alone.  Claiming a
+// longest-first list in order is greedy LPT, whatever the CTA placement or residency.
+struct WarpSched {
+    unsigned int lead[256];        // per-SM tickets
+    unsigned int pair_next;        // next position of [0, P)
+    unsigned int pad;
+    unsigned long long deal_next;  // next position of [P, n), minus P
+};
+__device__ __forceinline__ void named_bar(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 template <int WARPS, int S>
 __global__ void __launch_bounds__(WARPS * 32) k_hash_warp(const uint64_t *__restrict__ ptrs,
                                                           const uint64_t *__restrict__ lens,
                                                           const uint32_t *__restrict__ order, uint64_t n_bufs,
-                                                          uint64_t *__restrict__ digests, uint64_t primary) {
+                                                          uint64_t *__restrict__ digests, WarpSched *sch,
+                                                          uint32_t split) {
     constexpr int CH = 512;
     extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint32_t s_lead, s_item[2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint8_t *ring = smem + (size_t)warp * S * CH;
-    const uint32_t ring_s = smem_u32(ring);
-    // Round r of warp w takes list position r*W + w, or r*W + (W-1-w) on odd rounds (boustrophedon
-    // over a longest-first order: the warp holding the longest buffer gets the shortest of the next
-    // round, so per-warp totals stay close).  With `primary` = P > 0, warps 0..P-1 (the first CTA
-    // of every SM) take the P longest buffers alone and the other warps deal out the rest, so the
-    // longest chains share their schedulers only with short work.
-    const uint64_t wg0 = (uint64_t)blockIdx.x * WARPS + warp;
-    const bool prim = wg0 < primary;
-    const uint64_t W = prim ? 1 : (uint64_t)gridDim.x * WARPS - primary;
-    const uint64_t wg = prim ? 0 : wg0 - primary, base = prim ? wg0 : primary;
-    const uint64_t rounds = prim ? 1 : ~0ull;
-    for (uint64_t r = 0; r < rounds && base + r * W < n_bufs; ++r) {
-        const uint64_t k = base + r * W + ((r & 1) ? W - 1 - wg : wg);
-        if (k >= n_bufs) continue;
-        BufCursor ld, cs;
-        cursor_load(ld, ptrs, lens, order, k, n_bufs);
-        cs = ld;
-        if (cs.L == 0) {
-            if (lane == 0) digests[cs.idx] = 0;
-            continue;
+    if (split) {
+        static_assert(WARPS == 4, "a lead CTA holds two split pairs");
+        if (threadIdx.x == 0) {
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            s_lead = atomicAdd(&sch->lead[smid & 255], 1u) == 0;  // every SM that runs a CTA has a lead
         }
-        auto issue = [&](int st) {
-            if (ld.pos < ld.L) {
-                const uint32_t b = chunk_bytes(ld, CH);
-                if ((uint32_t)(16 * lane) < b) cp_async16(ring_s + (uint32_t)(st * CH + 16 * lane), ld.a0 + ld.pos + 16 * lane);
-                ld.pos += b;
+        __syncthreads();
+        if (s_lead) {
+            SplitBars *bars = reinterpret_cast<SplitBars *>(smem + 2 * SPLIT_PAIR);
+            const int pair = warp >> 1, role = warp & 1;
+            if (lane == 0 && role == 0) {
+                for (int i = 0; i < SPLIT_S; ++i) mbar_init(&bars[pair].full[i], 32), mbar_init(&bars[pair].empty[i], 32);
+                fence_mbar_init();
             }
-            cp_async_commit();
-        };
-#pragma unroll
-        for (int st = 0; st < S - 1; ++st) issue(st);
-        uint64_t h = FNV_OFFSET, prev = 0;
-        int st = 0;
-        while (cs.pos < cs.L) {
-            cp_async_wait<S - 2>();
-            __syncwarp();
-            issue(st == 0 ? S - 1 : st - 1);
-            const uint32_t bytes = chunk_bytes(cs, CH);
-            if (lane == 0) consume_chunk<CH, true>(cs, bytes, reinterpret_cast<const uint4 *>(ring + st * CH), h, prev);
-            cs.pos += bytes;
-            st = st + 1 == S ? 0 : st + 1;
-            __syncwarp();  // the slot is re-filled only after lane 0 has read it
+            __syncthreads();
+            uint8_t *pr = smem + (size_t)pair * SPLIT_PAIR;
+            uint64_t base = 0;  // chunks this pair has moved so far (ring slot / barrier phase)
+            for (;;) {
+                if (lane == 0 && role == 0) s_item[pair] = atomicAdd(&sch->pair_next, 1u);
+                named_bar(1 + pair, 64);
+                const uint64_t k = s_item[pair];
+                named_bar(1 + pair, 64);  // both warps have read the item
+                if (k >= split || k >= n_bufs) break;
+                BufCursor cur;
+                cursor_load(cur, ptrs, lens, order, k, n_bufs);
+                if (cur.m == 0 && cur.n >= SPLIT_MIN_BYTES) {
+                    if (role == 0) split_lo(cur, lane, pr, &bars[pair], base);
+                    else split_hi(cur, lane, pr, &bars[pair], digests, base);
+                    base += (cur.L + SPLIT_CH - 1) / SPLIT_CH;
+                } else if (role == 0) {  // short or unaligned: warp A folds it alone
+                    warp_fold<S>(cur, lane, pr, digests);
+                }
+                named_bar(1 + pair, 64);  // the pair's shared memory is free again
+            }
+            ring = pr + (size_t)role * S * CH;  // this pair's area, split between its two warps
         }
-        cp_async_wait<0>();
-        __syncwarp();
-        if (lane == 0) digests[cs.idx] = finish_digest(h, cs.n);
+    }
+    if (!sch) {  // uniform batch: one warp per buffer, all in flight at once
+        const uint64_t k = (uint64_t)blockIdx.x * WARPS + warp;
+        if (k < n_bufs) {
+            BufCursor cur;
+            cursor_load(cur, ptrs, lens, order, k, n_bufs);
+            warp_fold<S>(cur, lane, ring, digests);
+        }
+        return;
+    }
+    // claim the next position of [split, n) and fold it with this warp alone
+    for (;;) {
+        unsigned long long k = 0;
+        if (lane == 0) k = atomicAdd(&sch->deal_next, 1ull);
+        k = __shfl_sync(0xffffffffu, k, 0) + split;
+        if (k >= n_bufs) break;
+        BufCursor cur;
+        cursor_load(cur, ptrs, lens, order, k, n_bufs);
+        warp_fold<S>(cur, lane, ring, digests);
     }
 }
 constexpr int WARP_K_WARPS = 4, WARP_K_STAGES = 8;
-constexpr size_t WARP_K_SMEM = (size_t)WARP_K_WARPS * WARP_K_STAGES * 512;
+constexpr size_t WARP_K_SMEM_DEAL = (size_t)WARP_K_WARPS * WARP_K_STAGES * 512;
+constexpr size_t WARP_K_SMEM_SPLIT = 2 * SPLIT_PAIR + 2 * sizeof(SplitBars);
+constexpr size_t WARP_K_SMEM = WARP_K_SMEM_DEAL > WARP_K_SMEM_SPLIT ? WARP_K_SMEM_DEAL : WARP_K_SMEM_SPLIT;
 
 struct HashCfg {
     int nt, ch, s;
@@ -494,8 +804,15 @@ int hash_batch_launch(const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n
     if (setenv_variant < 0 && !getenv("B2L_HASH_CFG") && n <= WARP_MAX_BUFS) {
         // few buffers: one warp each (every buffer's chain runs at its own latency)
         auto fn = k_hash_warp<WARP_K_WARPS, WARP_K_STAGES>;
-        // ragged (longest-first order given): two warps per scheduler, buffers dealt out
-        // boustrophedon; uniform: one warp per buffer, all in flight at once
+        static bool smem_set[64] = {false};
+        int cur_dev = 0;
+        B2L_CUDA(cudaGetDevice(&cur_dev));
+        if (!smem_set[cur_dev & 63]) {  // the split pairs' rings exceed the 48 KiB default
+            B2L_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WARP_K_SMEM));
+            smem_set[cur_dev & 63] = true;
+        }
+        // ragged (longest-first order given): three warps per scheduler claiming the list (the
+        // lead CTAs' split pairs first); uniform: one warp per buffer, all in flight at once
         uint64_t warps = n;
         static const uint64_t wps = [] {  // B2L_RAGGED_WPS: tuning override
             const char *e = getenv("B2L_RAGGED_WPS");
@@ -503,12 +820,20 @@ int hash_batch_launch(const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n
         }();
         if (d_order) warps = std::min<uint64_t>(n, (uint64_t)sm_count() * 4 * wps);
         const unsigned grid = (unsigned)((warps + WARP_K_WARPS - 1) / WARP_K_WARPS);
-        // ragged and two warps per scheduler: the first CTA of every SM holds the longest buffers
-        static const bool prim_on = !getenv("B2L_HASH_NO_PRIMARY");
-        const uint64_t primary =
-            (d_order && prim_on && wps >= 2 && warps == (uint64_t)sm_count() * 4 * wps) ? (uint64_t)sm_count() * 4 : 0;
-        fn<<<grid, WARP_K_WARPS * 32, WARP_K_SMEM, stream>>>(d_ptrs, d_lens, d_order, n, d_digests, primary);
-        B2L_CHECK_LAUNCH("k_hash_warp");
+        // ragged: the first CTA on every SM folds the longest buffers as split pairs
+        // (B2L_HASH_NO_SPLIT: one warp each); the list is claimed dynamically (WarpSched)
+        static const bool split_on = !getenv("B2L_HASH_NO_SPLIT");
+        const uint32_t split = d_order && split_on ? 2u * (uint32_t)sm_count() : 0u;
+        WarpSched *sch = nullptr;
+        if (d_order) {
+            B2L_CUDA(cudaMallocAsync((void **)&sch, sizeof(WarpSched), stream));
+            B2L_CUDA(cudaMemsetAsync(sch, 0, sizeof(WarpSched), stream));
+        }
+        fn<<<grid, WARP_K_WARPS * 32, split ? WARP_K_SMEM : WARP_K_SMEM_DEAL, stream>>>(d_ptrs, d_lens, d_order, n,
+                                                                                      d_digests, sch, split);
+        const cudaError_t le = cudaGetLastError();
+        if (sch) B2L_CUDA(cudaFreeAsync(sch, stream));
+        if (le != cudaSuccess) return cuda_fail(le, "k_hash_warp");
         return B2L_OK;
     }
     if (setenv_variant < 0 && !getenv("B2L_HASH_CFG") && n <= LATENCY_MAX_BUFS) {

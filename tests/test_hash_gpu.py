@@ -130,6 +130,27 @@ def test_ragged_longest_first_order(cuda):
     assert _device_digests(cuda, payloads) == want
 
 
+def test_split_pairs_chunk_edges_and_reuse(cuda):
+    """Ragged batches fold their longest buffers with warp pairs (lo / hi 32-bit chains,
+    b2l_hash.cu "split pair"): lengths at the 64 KiB eligibility edge and around the 4 KiB
+    chunks (tails of 1..7 bytes, a last chunk with no full word), unaligned long buffers (warp A
+    alone), zero-length entries, and more long buffers than pairs so every pair folds several
+    (its ring slots and barrier phases carry over)."""
+    rng = np.random.default_rng(31)
+    edge = [64 << 10, (64 << 10) - 1, (64 << 10) + 1, (64 << 10) + 7, 4096 * 17, 4096 * 17 + 1, 4096 * 17 + 8,
+            4096 * 17 + 9, 4096 * 33 - 1, 4096 * 40 + 3, (1 << 20) + 5, 1 << 20, 0, 0]
+    lens = edge + [int(x) for x in rng.integers(64 << 10, 300 << 10, size=420)] + \
+        [int(x) for x in rng.integers(1, 5000, size=200)]
+    offs = [0] * len(lens)
+    for i in range(0, len(lens), 7):
+        offs[i] = int(rng.integers(1, 16))  # unaligned: not split-eligible
+    payloads = [hash_ref.payload(n, 23, i) for i, n in enumerate(lens)]
+    want = [hash_ref.fold64_c(p) if p else 0 for p in payloads]
+    order = list(np.argsort(-np.array(lens), kind="stable"))
+    assert _device_digests(cuda, payloads, offsets=offs, order=order) == want
+    assert _device_digests(cuda, payloads, order=order) == want
+
+
 def test_zero_length_gets_reserved_digest_and_host_raises(cuda):
     from paper_2601_12713_b200 import EmptyPayload, hash_batch, hash_bytes
     payloads = [b"abc", b"", b"x" * 100]
