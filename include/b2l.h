@@ -287,18 +287,37 @@ int b2l_lookup_seqs(const b2l_trace_cols *cols, const uint64_t *seqs, uint64_t n
 
 /* Key-range sharding (the reference has no multi-process analysis -- these route
  * the events detectors.py:85-271 relate so that each rank's sub-traces are exact):
+ * b2l_shard_kernel_summary: per target device (num_devices_total entries) of a device-resident
+ * shard: has_kernels (0/1) and the max end of its target kernels.  All-gathered, these give
+ * every rank the carry of the shards before it.
  * b2l_shard_route: for a device-resident seq-range shard whose first event has global index
- * `base`, writes one 12 x i64 row per record into d_rows (capacity 2 * n_events rows), grouped
- * by destination rank in event order -- hashed transfers to the owner of their hash range
- * ((hash * n_ranks) >> 64, space 0) and allocs, deletes, target kernels and target transfers
- * to dst_device % n_ranks (space 1).  Row: [global index | space << 63, seq, start_ns, end_ns,
- * src_addr, dst_addr, bytes, hash, src_device, dst_device, kind, loc].  counts[r] = rows for
- * rank r; data_end_ns = max end over non-kernel events (prep.py:61-62's synthetic delete time).
+ * `base`, writes one 12 x i64 row per record into d_rows, grouped by destination rank in event
+ * order: space 0 -- hashed transfers to the owner of their hash range ((hash * n_ranks) >> 64);
+ * space 1 -- allocs and deletes to the pairing owner of (dst_device, dst_addr) ((dst_device +
+ * owner(mix(dst_addr))) % n_ranks), target transfers to the owner of (dst_device, src_addr),
+ * and the target kernels those ranks need for exact UA/UT cursors: each target transfer's /
+ * target alloc's cursor kernel (to that query's rank), the shard's first kernel of every device
+ * (to every rank), and at the head of every rank's block one carry kernel per device whose
+ * carry_max_end (the max kernel end on earlier shards; carry_has[d] = any) reaches the shard's
+ * first start (owner(key) = top 32 bits of a splitmix64 mix of the key, times n_ranks, >> 32).
+ * Row: [global index | space << 63, seq, start_ns, end_ns, src_addr, dst_addr, bytes, hash,
+ * src_device, dst_device, kind, loc].  d_rows NULL: sizing call (*n_rows = an upper bound, and
+ * data_end_ns); else capacity >= that bound, *n_rows is not updated and counts[r] = rows for
+ * rank r.  data_end_ns = max end over non-kernel events (prep.py:61-62's synthetic delete time).
+ * b2l_shard_route_pairs: the second exchange.  For a device sub-trace (global indices d_gid) and
+ * its alloc/delete pairs (indices, delete 0xFFFFFFFF = synthetic), every pair's alloc and real
+ * delete go to the owner of the RA key (alloc src_addr, dst_device, bytes; detectors.py:170-176)
+ * as space-1 rows, sub-trace order per destination.  d_rows NULL: sizing call.
  * b2l_shard_unpack: received rows of one space -> device columns d_cols[0..11] (global index,
  * seq, start, end, src_addr, dst_addr, bytes, hash as i64; src, dst as i32; kind u8; loc u32),
  * capacity n_rows each; *n_out = rows of that space. */
-int b2l_shard_route(const b2l_trace_cols *cols, uint32_t n_ranks, uint64_t base, uint32_t flags, int64_t *d_rows,
-                    uint64_t *counts, uint64_t *n_rows, uint64_t *data_end_ns);
+int b2l_shard_kernel_summary(const b2l_trace_cols *cols, uint64_t *has_kernels, uint64_t *max_kernel_end);
+int b2l_shard_route(const b2l_trace_cols *cols, uint32_t n_ranks, uint64_t base, uint32_t flags,
+                    const uint8_t *carry_has, const uint64_t *carry_max_end, int64_t *d_rows, uint64_t *counts,
+                    uint64_t *n_rows, uint64_t *data_end_ns);
+int b2l_shard_route_pairs(const b2l_trace_cols *cols, const int64_t *d_gid, const uint32_t *d_pair_alloc,
+                          const uint32_t *d_pair_delete, uint64_t n_pairs, uint32_t n_ranks, int64_t *d_rows,
+                          uint64_t *counts, uint64_t *n_rows);
 int b2l_shard_unpack(const int64_t *d_rows, uint64_t n_rows, uint32_t space, int64_t *const *d_cols,
                      uint64_t *n_out);
 

@@ -31,6 +31,7 @@ EXPORTED = (
     "b2l_hash_launch_info", "b2l_hash_select_variant", "b2l_hash_large",
     "b2l_analyze", "b2l_analyze_ex", "b2l_findings_free", "b2l_savings_compute", "b2l_savings_free",
     "b2l_lookup_seqs", "b2l_audit_batch", "b2l_stable_sort_u32", "b2l_stable_sort_u64", "b2l_shard_route", "b2l_shard_unpack", "b2l_sort_u64_pairs_device",
+    "b2l_shard_kernel_summary", "b2l_shard_route_pairs",
     "b2l_capture_create", "b2l_capture_destroy", "b2l_capture_set_audit_dir", "b2l_capture_device_slot",
     "b2l_capture_target", "b2l_capture_data_op", "b2l_capture_finalize", "b2l_capture_free_text",
     "b2l_capture_write", "b2l_capture_warnings",

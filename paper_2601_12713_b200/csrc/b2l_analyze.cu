@@ -2266,48 +2266,166 @@ namespace ana {
 //   [0] global event index | key space << 63, then seq, start, end, src_addr, dst_addr, bytes, hash,
 //   src_device, dst_device, kind, loc (sharded.py FIELDS).
 constexpr int SH_ROW = 12;
-struct RouteCount {  // records per event: hash-keyed (space 0) and device-keyed (space 1)
-    DevCols c;
-    bool raw;
-    __device__ uint32_t operator()(size_t i) const {
+// Owner rank of a device-keyed record: ((mix * G) >> 64) on the top 32 bits of a splitmix64 mix
+// of the key (sharded.py route_mix -- the host path routes identically).
+__host__ __device__ __forceinline__ uint64_t route_splitmix(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t route_mix(uint64_t a, uint64_t b) { return route_splitmix(a ^ route_splitmix(b)); }
+__host__ __device__ __forceinline__ uint32_t route_owner(uint64_t key, uint32_t G) {
+    return (uint32_t)(((key >> 32) * (uint64_t)G) >> 32);
+}
+// Records of one event (the exchange of the key-range sharded analysis):
+//  space 0: a hashed transfer -> the owner of its hash range (DD / RT: detectors.py:85-167);
+//  space 1: an alloc or delete -> the pairing owner of (dst_device, dst_addr) (prep.py:58-70);
+//           a target transfer -> the owner of (dst_device, src_addr) (UT's next-same-address
+//           key, detectors.py:250-264); a target kernel -> every rank that needs it for exact
+//           UA / UT cursors (detectors.py:208-212,251-253): the rank of each query (target
+//           transfer or target alloc) whose cursor lands on it, and every rank for the first
+//           kernel of each device in the shard (queries whose cursor lands on a later shard).
+//           Cursors that land on an earlier shard are covered by a per-device carry kernel at
+//           the head of every rank's block (sharded.py device_parts).
+struct RouteKind {
+    bool h, ad, tt, tk;
+    __device__ RouteKind(const DevCols &c, size_t i, bool raw) {
         const uint8_t k = c.kind[i];
-        const bool h = k == B2L_KIND_TRANSFER && (raw || (c.nb[i] > 0 && c.h[i] != 0));
-        const bool d = k == B2L_KIND_ALLOC || k == B2L_KIND_DELETE ||
-                       ((k == B2L_KIND_KERNEL || k == B2L_KIND_TRANSFER) && c.dst[i] != c.host);
-        return (h ? 1u : 0u) + (d ? 1u : 0u);
+        h = k == B2L_KIND_TRANSFER && (raw || (c.nb[i] > 0 && c.h[i] != 0));
+        ad = k == B2L_KIND_ALLOC || k == B2L_KIND_DELETE;
+        tt = k == B2L_KIND_TRANSFER && c.dst[i] != c.host;
+        tk = k == B2L_KIND_KERNEL && c.dst[i] != c.host;
     }
 };
-struct RouteStore {  // record keys (destination rank) and record ids (event << 1 | space)
+struct RouteKeys {
+    DevCols c;
+    uint32_t G;
+    __device__ uint32_t pair_owner(size_t i) const {  // (dst + owner(mix(dst_addr))) % G
+        return (uint32_t)(((uint64_t)(uint32_t)c.dst[i] + route_owner(route_splitmix(c.da[i]), G)) % G);
+    }
+    __device__ uint32_t ut_owner(size_t i) const {
+        return route_owner(route_mix((uint64_t)(uint32_t)c.dst[i] ^ (1ull << 40), c.sa[i]), G);
+    }
+};
+constexpr int NEED_W = 4;  // 64-bit words of the per-kernel rank mask (G <= 256)
+struct RouteCtx {
     DevCols c;
     bool raw;
-    uint32_t G;
+    uint32_t G, W;
+    const uint32_t *kpos;   // event -> kernel position (target kernels), else NONE
+    const uint64_t *need;   // [position][W] ranks that need the kernel
+    __device__ uint32_t count(size_t i) const {
+        const RouteKind r(c, i, raw);
+        uint32_t n = (r.h ? 1u : 0u) + (r.ad || r.tt ? 1u : 0u);
+        if (r.tk) {
+            const uint64_t *m = need + (size_t)kpos[i] * W;
+            for (uint32_t w = 0; w < W; ++w) n += __popcll(m[w]);
+        }
+        return n;
+    }
+};
+struct RouteCount {
+    RouteCtx x;
+    __device__ uint32_t operator()(size_t i) const { return x.count(i); }
+};
+struct RouteStore {  // record keys (destination rank) and record ids (event << 1 | space)
+    RouteCtx x;
     uint64_t *key;
     uint32_t *rec;
     __device__ void operator()(size_t i, uint32_t ex, uint32_t) const {
-        const uint8_t k = c.kind[i];
-        const bool h = k == B2L_KIND_TRANSFER && (raw || (c.nb[i] > 0 && c.h[i] != 0));
-        const bool d = k == B2L_KIND_ALLOC || k == B2L_KIND_DELETE ||
-                       ((k == B2L_KIND_KERNEL || k == B2L_KIND_TRANSFER) && c.dst[i] != c.host);
+        const DevCols &c = x.c;
+        const RouteKind r(c, i, x.raw);
+        const RouteKeys K{c, x.G};
         uint32_t o = ex;
-        if (h) {  // owner of the hash range: (hash * G) >> 64 on the top 32 bits
-            key[o] = ((c.h[i] >> 32) * (uint64_t)G) >> 32;
+        if (r.h) {  // owner of the hash range: (hash * G) >> 64 on the top 32 bits
+            key[o] = ((c.h[i] >> 32) * (uint64_t)x.G) >> 32;
             rec[o++] = (uint32_t)(i << 1);
         }
-        if (d) {
-            key[o] = (uint64_t)((uint32_t)c.dst[i] % G);
-            rec[o] = (uint32_t)(i << 1) | 1u;
+        const uint32_t id = (uint32_t)(i << 1) | 1u;
+        if (r.ad) key[o] = K.pair_owner(i), rec[o++] = id;
+        if (r.tt) key[o] = K.ut_owner(i), rec[o++] = id;
+        if (r.tk) {
+            const uint64_t *m = x.need + (size_t)x.kpos[i] * x.W;
+            for (uint32_t w = 0; w < x.W; ++w)
+                for (uint64_t b = m[w]; b; b &= b - 1) key[o] = 64 * w + __ffsll((long long)b) - 1, rec[o++] = id;
         }
     }
 };
-__global__ void k_route_rows(DevCols c, uint64_t base, const uint32_t *__restrict__ rec, uint64_t nrec,
-                             int64_t *__restrict__ rows) {
+__global__ void k_route_total(RouteCtx x, unsigned long long *out) {
+    unsigned long long t = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < x.c.n; i += (size_t)gridDim.x * blockDim.x)
+        t += x.count(i);
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if ((threadIdx.x & 31) == 0 && t) atomicAdd(out, t);
+}
+// kernel position of every event (target kernels; NONE elsewhere)
+__global__ void k_kernel_pos(const uint32_t *__restrict__ kev, uint32_t nk, uint32_t *__restrict__ kpos) {
+    for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < nk; p += (size_t)gridDim.x * blockDim.x)
+        kpos[kev[p]] = (uint32_t)p;
+}
+// first kernel of each device: every rank; each query's cursor kernel: the query's rank
+struct NeedFirst {
+    KernelIndex KI;
+    uint32_t G, W;
+    uint64_t *need;
+    __device__ void operator()(size_t p) const {
+        if (p == 0 || KI.kdev[p] != KI.kdev[p - 1])
+            for (uint32_t g = 0; g < G; ++g) need[p * W + g / 64] |= 1ull << (g % 64);
+    }
+};
+struct NeedCursor {
+    DevCols c;
+    KernelIndex KI;
+    RouteKeys K;
+    uint32_t W;
+    const uint8_t *carry_has;
+    const uint64_t *carry_max;
+    uint64_t *need;
+    __device__ void operator()(size_t i) const {
+        const uint8_t k = c.kind[i];
+        const bool tt = k == B2L_KIND_TRANSFER && c.dst[i] != c.host;
+        const bool ta = k == B2L_KIND_ALLOC && c.dst[i] != c.host;
+        if (!tt && !ta) return;
+        const uint32_t dev = (uint32_t)c.dst[i];
+        const uint64_t t = c.start[i];
+        if (carry_has[dev] && carry_max[dev] >= t) return;  // the cursor lands on an earlier shard
+        uint32_t lo, hi;
+        KI.range(dev, lo, hi);
+        const uint32_t p = KI.cursor(lo, hi, t);
+        if (p >= hi) return;  // on a later shard (its first kernel goes to every rank)
+        const uint32_t r = tt ? K.ut_owner(i) : K.pair_owner(i);
+        atomicOr((unsigned long long *)&need[(size_t)p * W + r / 64], 1ull << (r % 64));
+    }
+};
+// rows: rank r's block = its carry kernels, then its records (sorted by rank, event order inside)
+__global__ void k_route_rows(DevCols c, uint64_t base, const int64_t *__restrict__ gid,
+                             const uint64_t *__restrict__ key, const uint32_t *__restrict__ rec, uint64_t nrec,
+                             uint32_t npseudo, int64_t *__restrict__ rows) {
     for (size_t r = (size_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrec; r += (size_t)gridDim.x * blockDim.x) {
         const uint32_t x = rec[r], e = x >> 1;
-        int64_t *o = rows + r * SH_ROW;
-        o[0] = (int64_t)((base + e) | ((uint64_t)(x & 1u) << 63));
+        int64_t *o = rows + (r + (key[r] + 1) * npseudo) * SH_ROW;
+        const uint64_t g = gid ? (uint64_t)gid[e] : base + e;
+        o[0] = (int64_t)(g | ((uint64_t)(x & 1u) << 63));
         o[1] = (int64_t)c.seq[e], o[2] = (int64_t)c.start[e], o[3] = (int64_t)c.end[e];
         o[4] = (int64_t)c.sa[e], o[5] = (int64_t)c.da[e], o[6] = (int64_t)c.nb[e], o[7] = (int64_t)c.h[e];
         o[8] = c.src[e], o[9] = c.dst[e], o[10] = c.kind[e], o[11] = c.loc[e];
+    }
+}
+// carry kernel rows (space 1) at the head of every rank's block: start = the shard's first start,
+// end = the device's max kernel end on earlier shards
+__global__ void k_route_carry_rows(DevCols c, uint64_t base, const unsigned long long *__restrict__ cnt,
+                                   const uint32_t *__restrict__ pdev, const uint64_t *__restrict__ carry_max,
+                                   uint32_t npseudo, uint32_t G, int64_t *__restrict__ rows) {
+    const uint32_t r = blockIdx.x;
+    uint64_t off = 0;
+    for (uint32_t q = 0; q < r; ++q) off += cnt[q] + npseudo;
+    for (uint32_t j = threadIdx.x; j < npseudo; j += blockDim.x) {
+        const uint32_t d = pdev[j];
+        int64_t *o = rows + (off + j) * SH_ROW;
+        o[0] = (int64_t)(base | (1ull << 63));
+        o[1] = (int64_t)c.seq[0], o[2] = (int64_t)c.start[0], o[3] = (int64_t)carry_max[d];
+        o[4] = 0, o[5] = 0, o[6] = 0, o[7] = 0, o[8] = d, o[9] = d, o[10] = B2L_KIND_KERNEL, o[11] = c.loc[0];
     }
 }
 __global__ void k_max_data_end(DevCols c, unsigned long long *out) {  // max end over non-kernel events
@@ -2319,6 +2437,15 @@ __global__ void k_max_data_end(DevCols c, unsigned long long *out) {  // max end
         m = v > m ? v : m;
     }
     if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+// per target device: has kernels, max kernel end (the carry other shards need)
+__global__ void k_kernel_summary(DevCols c, unsigned long long *has, unsigned long long *mx) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n; i += (size_t)gridDim.x * blockDim.x)
+        if (c.kind[i] == B2L_KIND_KERNEL && c.dst[i] != c.host) {
+            const uint32_t d = (uint32_t)c.dst[i];
+            if (!has[d]) atomicOr(&has[d], 1ull);
+            atomicMax(&mx[d], (unsigned long long)c.end[i]);
+        }
 }
 // OR and AND of two u64 columns (warp-reduced, one atomic per warp and value).
 __global__ void k_or_and2(const uint64_t *__restrict__ a, const uint64_t *__restrict__ b, size_t n,
@@ -2342,53 +2469,188 @@ __global__ void k_route_counts(const uint64_t *__restrict__ key, uint64_t n, uin
     for (uint32_t g = threadIdx.x; g < G; g += blockDim.x)
         if (sc[g]) atomicAdd(cnt + g, sc[g]);
 }
+// records (key = destination rank, rec = event << 1 | space) -> rows grouped by destination, event
+// order inside (one stable radix pass over the rank), npseudo carry rows ahead of every block;
+// per-rank row counts to the host
+void route_emit(const DevCols &c, uint64_t base, const int64_t *gid, uint64_t *key, uint32_t *rec, uint32_t nrec,
+                uint32_t G, uint32_t npseudo, const uint32_t *pdev, const uint64_t *carry_max, int64_t *d_rows,
+                unsigned long long *cnt, uint64_t *h_counts, cudaStream_t s) {
+    SortBufs<1> sb;
+    DBuf<uint64_t> k2(nrec ? nrec : 1, s);
+    DBuf<uint32_t> v2(nrec ? nrec : 1, s);
+    if (nrec) {
+        sb.k[0].w[0] = key, sb.k[1].w[0] = k2.p, sb.v[0] = rec, sb.v[1] = v2.p, sb.cur = 0;
+        radix_sort<1>(sb, nrec, LiveBytes<1>{{live_range(G)}}, s);
+        k_route_counts<<<grid_for(nrec, 256, 148 * 4), 256, 0, s>>>(sb.k[sb.cur].w[0], nrec, G, cnt);
+        CK_LAUNCH("k_route_counts");
+        k_route_rows<<<grid_for(nrec, 256), 256, 0, s>>>(c, base, gid, sb.k[sb.cur].w[0], sb.v[sb.cur], nrec, npseudo,
+                                                          d_rows);
+        CK_LAUNCH("k_route_rows");
+    }
+    if (npseudo) {
+        k_route_carry_rows<<<G, 64, 0, s>>>(c, base, cnt, pdev, carry_max, npseudo, G, d_rows);
+        CK_LAUNCH("k_route_carry_rows");
+    }
+    std::vector<unsigned long long> hc(G);
+    read_back(hc.data(), cnt, G * sizeof(unsigned long long), s);
+    for (uint32_t g = 0; g < G; ++g) h_counts[g] = hc[g] + npseudo;
+}
 
-int shard_route_impl(const b2l_trace_cols *cols, uint32_t G, uint64_t base, uint32_t flags, int64_t *d_rows,
-                     uint64_t *h_counts, uint64_t *h_nrec, uint64_t *h_data_end) {
+int shard_kernel_summary_impl(const b2l_trace_cols *cols, uint64_t *h_has, uint64_t *h_max) {
+    if (!cols->device_resident) return fail(B2L_E_INVALID_ARG, "b2l_shard_kernel_summary: device columns only");
+    std::lock_guard<std::mutex> lock(g_mu);
+    cudaStream_t s = engine_stream();
+    ColsUpload up;
+    up.load(cols, s);
+    const DevCols c = up.d;
+    const uint32_t nd = c.ndev > 0 ? (uint32_t)c.ndev : 1;
+    DBuf<unsigned long long> hm(2 * nd, s);
+    hm.zero();
+    if (c.n) {
+        k_kernel_summary<<<grid_for(c.n, TPB, 148 * 8), TPB, 0, s>>>(c, hm.p, hm.p + nd);
+        CK_LAUNCH("k_kernel_summary");
+    }
+    std::vector<unsigned long long> h(2 * nd);
+    read_back(h.data(), hm.p, 2 * nd * sizeof(unsigned long long), s);
+    for (uint32_t d = 0; d < (uint32_t)c.ndev; ++d) h_has[d] = h[d], h_max[d] = h[nd + d];
+    return B2L_OK;
+}
+
+int shard_route_impl(const b2l_trace_cols *cols, uint32_t G, uint64_t base, uint32_t flags, const uint8_t *h_carry_has,
+                     const uint64_t *h_carry_max, int64_t *d_rows, uint64_t *h_counts, uint64_t *h_nrec,
+                     uint64_t *h_data_end) {
     if (!cols->device_resident) return fail(B2L_E_INVALID_ARG, "b2l_shard_route: columns must be device-resident");
-    if (G == 0 || G > 256) return fail(B2L_E_INVALID_ARG, "b2l_shard_route: 1..256 ranks");
+    if (G == 0 || G > 64 * NEED_W) return fail(B2L_E_INVALID_ARG, "b2l_shard_route: 1..256 ranks");
     std::lock_guard<std::mutex> lock(g_mu);
     cudaStream_t s = engine_stream();
     Arena arena;  // call-scoped scratch (outputs go to the caller's buffers)
-    arena.open(cols->n_events <= ARENA_MAX_EVENTS ? ARENA_BASE + cols->n_events * 128 : 0, s);
+    arena.open(cols->n_events <= ARENA_MAX_EVENTS ? ARENA_BASE + cols->n_events * 96 : 0, s);
     ArenaUse arena_use(&arena);
     ColsUpload up;
     up.load(cols, s);
     const DevCols c = up.d;
     const size_t n = c.n;
     const bool raw = (flags & B2L_ANALYZE_RAW_HASHED) != 0;
-    DBuf<uint64_t> key(2 * n + 1, s);
-    DBuf<uint32_t> rec(2 * n + 1, s), tot(1, s);
-    DBuf<unsigned long long> cnt(G + 1, s);  // [G] = max data-op end
+    const uint32_t nd = c.ndev > 0 ? (uint32_t)c.ndev : 1, W = (G + 63) / 64;
+    g_masks = Masks{};
+    g_masks.dev = live_range(nd);
+    g_masks.idx = live_range(n);
+    g_masks.n = n;
+    // carry per device (host arrays, NULL = none) and the devices that get a carry kernel
+    std::vector<uint8_t> ch(nd, 0);
+    std::vector<uint64_t> cm(nd, 0);
+    std::vector<uint32_t> pd;
+    uint64_t first_start = 0;
+    if (n) read_back(&first_start, c.start, sizeof(uint64_t), s);
+    for (uint32_t d = 0; d < (uint32_t)c.ndev; ++d) {
+        ch[d] = h_carry_has ? h_carry_has[d] : 0, cm[d] = h_carry_max ? h_carry_max[d] : 0;
+        if (ch[d] && cm[d] >= first_start && n) pd.push_back(d);
+    }
+    const uint32_t npseudo = (uint32_t)pd.size();
+    DBuf<uint8_t> d_ch(nd, s);
+    DBuf<uint64_t> d_cm(nd, s);
+    DBuf<uint32_t> d_pd(npseudo ? npseudo : 1, s);
+    // pageable sources: the copies are staged before cudaMemcpyAsync returns
+    CK(cudaMemcpyAsync(d_ch.p, ch.data(), nd, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_cm.p, cm.data(), nd * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    if (npseudo) CK(cudaMemcpyAsync(d_pd.p, pd.data(), npseudo * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    DBuf<unsigned long long> cnt(G + 2, s);  // [G] = max data-op end, [G + 1] = records
     cnt.zero();
-    scan<SumU32>(n, RouteCount{c, raw}, RouteStore{c, raw, G, key.p, rec.p}, s, tot.p);
+    // target kernels, grouped by device with their prefix-max ends; which ranks need which kernel
+    DBuf<uint32_t> TK(n ? n : 1, s), nk_d(1, s), kpos(n ? n : 1, s);
+    const int32_t *dst = c.dst;
+    const uint8_t *kind = c.kind;
+    const int32_t host = c.host;
+    compact(n, [=] __device__(size_t i) { return kind[i] == B2L_KIND_KERNEL && dst[i] != host; }, TK.p, nk_d.p, s);
+    const uint32_t nK = n ? read_u32(nk_d.p, s) : 0;
+    KernelIndexStore kis(nK, s);
+    build_kernel_index(kis, c, TK.p, nK, s);
+    DBuf<uint64_t> need((size_t)(nK ? nK : 1) * W, s);
+    need.zero();
+    if (nK) {
+        k_kernel_pos<<<grid_for(nK, TPB), TPB, 0, s>>>(kis.kev.p, nK, kpos.p);
+        CK_LAUNCH("k_kernel_pos");
+        for_each(nK, NeedFirst{kis.KI, G, W, need.p}, s);
+        for_each(n, NeedCursor{c, kis.KI, RouteKeys{c, G}, W, d_ch.p, d_cm.p, need.p}, s);
+    }
+    const RouteCtx x{c, raw, G, W, kpos.p, need.p};
     if (n) {
         k_max_data_end<<<grid_for(n, TPB, 148 * 8), TPB, 0, s>>>(c, cnt.p + G);
         CK_LAUNCH("k_max_data_end");
+        k_route_total<<<grid_for(n, TPB, 148 * 8), TPB, 0, s>>>(x, cnt.p + G + 1);
+        CK_LAUNCH("k_route_total");
     }
-    uint32_t nrec = 0;
-    read_back(&nrec, tot.p, sizeof(nrec), s);
-    if (nrec) {
-        SortBufs<1> sb;  // stable grouping by destination rank, event order inside
-        DBuf<uint64_t> k2(nrec, s);
-        DBuf<uint32_t> v2(nrec, s);
-        sb.k[0].w[0] = key.p, sb.k[1].w[0] = k2.p, sb.v[0] = rec.p, sb.v[1] = v2.p, sb.cur = 0;
-        radix_sort<1>(sb, nrec, LiveBytes<1>{{live_range(G)}}, s);
-        k_route_counts<<<grid_for(nrec, 256, 148 * 4), 256, 0, s>>>(sb.k[sb.cur].w[0], nrec, G, cnt.p);
-        CK_LAUNCH("k_route_counts");
-        k_route_rows<<<grid_for(nrec, 256), 256, 0, s>>>(c, base, sb.v[sb.cur], nrec, d_rows);
-        CK_LAUNCH("k_route_rows");
-        std::vector<unsigned long long> hc(G + 1);
-        read_back(hc.data(), cnt.p, (G + 1) * sizeof(unsigned long long), s);
-        for (uint32_t g = 0; g < G; ++g) h_counts[g] = hc[g];
-        *h_data_end = hc[G];
-    } else {
-        unsigned long long me = 0;
-        read_back(&me, cnt.p + G, sizeof(me), s);
-        for (uint32_t g = 0; g < G; ++g) h_counts[g] = 0;
-        *h_data_end = me;
+    unsigned long long hv[2] = {0, 0};
+    read_back(hv, cnt.p + G, sizeof(hv), s);
+    *h_data_end = hv[0];
+    if (hv[1] >= 0xFFFFFFFFull) return fail(B2L_E_INVALID_ARG, "b2l_shard_route: too many records for one call");
+    const uint32_t nrec = (uint32_t)hv[1];
+    *h_nrec = nrec + (uint64_t)G * npseudo;
+    for (uint32_t g = 0; g < G; ++g) h_counts[g] = 0;
+    if (!d_rows) return B2L_OK;  // sizing call
+    DBuf<uint64_t> key(nrec ? nrec : 1, s);
+    DBuf<uint32_t> rec(nrec ? nrec : 1, s);
+    if (nrec) scan<SumU32>(n, RouteCount{x}, RouteStore{x, key.p, rec.p}, s);
+    route_emit(c, base, nullptr, key.p, rec.p, nrec, G, npseudo, d_pd.p, d_cm.p, d_rows, cnt.p, h_counts, s);
+    return B2L_OK;
+}
+
+// The second exchange: every event of a pair (the alloc, and its delete unless synthetic) of a
+// device sub-trace goes to the owner of the pair's RA key (alloc src_addr, dst_device, bytes:
+// detectors.py:170-176), as space-1 rows; global indices from gid[].
+struct PairDestOp {
+    DevCols c;
+    const uint32_t *pa, *pd;
+    uint32_t G;
+    uint32_t *dest;
+    __device__ void operator()(size_t p) const {
+        const uint32_t a = pa[p];
+        const uint32_t o = route_owner(route_mix(c.sa[a], route_mix((uint64_t)(uint32_t)c.dst[a], c.nb[a])), G);
+        dest[a] = o;
+        if (pd[p] != NONE) dest[pd[p]] = o;
     }
+};
+struct DestPred {
+    const uint32_t *dest;
+    __device__ bool operator()(size_t i) const { return dest[i] != NONE; }
+};
+int shard_route_pairs_impl(const b2l_trace_cols *cols, const int64_t *gid, const uint32_t *pa, const uint32_t *pd,
+                           uint64_t np, uint32_t G, int64_t *d_rows, uint64_t *h_counts, uint64_t *h_nrec) {
+    if (!cols->device_resident) return fail(B2L_E_INVALID_ARG, "b2l_shard_route_pairs: columns must be device-resident");
+    if (G == 0 || G > 256) return fail(B2L_E_INVALID_ARG, "b2l_shard_route_pairs: 1..256 ranks");
+    std::lock_guard<std::mutex> lock(g_mu);
+    cudaStream_t s = engine_stream();
+    ColsUpload up;
+    up.load(cols, s);
+    const DevCols c = up.d;
+    const size_t n = c.n;
+    for (uint32_t g = 0; g < G; ++g) h_counts[g] = 0;
+    *h_nrec = 0;
+    if (!n || !np) return B2L_OK;
+    Arena arena;
+    arena.open(n <= ARENA_MAX_EVENTS ? ARENA_BASE + n * 64 : 0, s);
+    ArenaUse arena_use(&arena);
+    DBuf<uint32_t> dest(n, s), rec(n, s), tot(1, s);
+    dev_memset(dest.p, 0xFF, n * sizeof(uint32_t), s);
+    for_each(np, PairDestOp{c, pa, pd, G, dest.p}, s);
+    compact(n, DestPred{dest.p}, rec.p, tot.p, s);
+    const uint32_t nrec = read_u32(tot.p, s);
     *h_nrec = nrec;
+    if (!d_rows || !nrec) return B2L_OK;
+    DBuf<uint64_t> key(nrec, s);
+    {
+        uint64_t *k = key.p;
+        uint32_t *r = rec.p;
+        const uint32_t *d = dest.p;
+        for_each(nrec, [=] __device__(size_t q) {
+            const uint32_t e = r[q];
+            k[q] = d[e];
+            r[q] = (e << 1) | 1u;
+        }, s);
+    }
+    DBuf<unsigned long long> cnt(G, s);
+    cnt.zero();
+    route_emit(c, 0, gid, key.p, rec.p, nrec, G, 0, nullptr, nullptr, d_rows, cnt.p, h_counts, s);
     return B2L_OK;
 }
 
@@ -2574,11 +2836,35 @@ int b2l_sort_u64_pairs(const uint64_t *k0, const uint64_t *k1, uint64_t n, uint3
     }
 }
 
-int b2l_shard_route(const b2l_trace_cols *cols, uint32_t n_ranks, uint64_t base, uint32_t flags, int64_t *d_rows,
-                    uint64_t *counts, uint64_t *n_rows, uint64_t *data_end_ns) {
-    if (!cols || !d_rows || !counts || !n_rows || !data_end_ns) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
+int b2l_shard_kernel_summary(const b2l_trace_cols *cols, uint64_t *has_kernels, uint64_t *max_kernel_end) {
+    if (!cols || !has_kernels || !max_kernel_end) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
     try {
-        return b2l::ana::shard_route_impl(cols, n_ranks, base, flags, d_rows, counts, n_rows, data_end_ns);
+        return b2l::ana::shard_kernel_summary_impl(cols, has_kernels, max_kernel_end);
+    } catch (const b2l::EngineErr &e) {
+        return b2l::fail(e.code, e.msg);
+    }
+}
+
+int b2l_shard_route(const b2l_trace_cols *cols, uint32_t n_ranks, uint64_t base, uint32_t flags,
+                    const uint8_t *carry_has, const uint64_t *carry_max_end, int64_t *d_rows, uint64_t *counts,
+                    uint64_t *n_rows, uint64_t *data_end_ns) {
+    if (!cols || !counts || !n_rows || !data_end_ns) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
+    try {
+        return b2l::ana::shard_route_impl(cols, n_ranks, base, flags, carry_has, carry_max_end, d_rows, counts,
+                                          n_rows, data_end_ns);
+    } catch (const b2l::EngineErr &e) {
+        return b2l::fail(e.code, e.msg);
+    }
+}
+
+int b2l_shard_route_pairs(const b2l_trace_cols *cols, const int64_t *d_gid, const uint32_t *d_pair_alloc,
+                          const uint32_t *d_pair_delete, uint64_t n_pairs, uint32_t n_ranks, int64_t *d_rows,
+                          uint64_t *counts, uint64_t *n_rows) {
+    if (!cols || !d_gid || (n_pairs && (!d_pair_alloc || !d_pair_delete)) || !counts || !n_rows)
+        return b2l::fail(B2L_E_INVALID_ARG, "null argument");
+    try {
+        return b2l::ana::shard_route_pairs_impl(cols, d_gid, d_pair_alloc, d_pair_delete, n_pairs, n_ranks, d_rows,
+                                                counts, n_rows);
     } catch (const b2l::EngineErr &e) {
         return b2l::fail(e.code, e.msg);
     }

@@ -36,6 +36,49 @@ def test_local_ranks_with_oracle_match_single(g):
             assert got.synthetic_end_ns == want.synthetic_end
 
 
+def _spread(cols, g):
+    """(pairing records, UT records) per rank."""
+    (ad, o_ad), (tt, o_tt) = sharded.device_owners(cols, g)
+    return np.bincount(o_ad[ad], minlength=g), np.bincount(o_tt[tt], minlength=g)
+
+
+@pytest.mark.parametrize("g", [2, 3, 4])
+def test_one_and_four_device_traces_spread_over_ranks(g):
+    """Traces with ONE target device (C2 cycles on one device; C3) and four (C4): the G-way
+    findings equal the single-shard ones, and device-keyed work spreads over the ranks by
+    (device, address) key rather than by device.  A key is indivisible: C2 cycles reuse one
+    device address per device (one pairing key per device) and C3 has one host array in flight
+    (one UT key), so only the keys that exist spread."""
+    from paper_2601_12713_b200.synth import c2_trace, c3_trace, c4_trace
+    balanced = lambda x: x.min() > 0.5 * x.mean()  # noqa: E731
+    every = lambda x: x.min() > 0  # noqa: E731
+    none = lambda x: True  # noqa: E731
+    for c, ok_pairs, ok_ut in ((c2_trace(3000, n_targets=1, seed=8, n_host_vars=256), none, balanced),
+                               (c4_trace(3000, seed=5, n_host_vars=64, palette=128), balanced, balanced),
+                               (c2_trace(3000, n_targets=2 * g, seed=9), every, balanced),
+                               (c3_trace(400, array_bytes=1 << 16), none, none)):
+        pairs, ut = _spread(c, g)
+        assert ok_pairs(pairs), pairs
+        assert ok_ut(ut), ut
+        for strict in (False, True):
+            got = sharded.run_local(c, g, strict=strict, analyzer=oracle_analyzer)
+            want = R.analyze_cols(c, strict=strict)
+            assert canon_columnar(got, c) == canon_oracle(want, c)
+            assert got.warn_index.tolist() == want.warnings
+
+
+def test_routing_keys_match_the_kernels():
+    """route_mix / route_owner restate b2l_analyze.cu's routing (fixed vectors)."""
+    a = np.array([0, 1, 0xFFFFFFFFFFFFFFFF, 0xD000], np.uint64)
+    b = np.array([0, 7, 3, 0x1234], np.uint64)
+    key = sharded.route_mix(a, b)
+    assert key.dtype == np.uint64
+    # splitmix64(0) is the well-known first output of the generator seeded with 0
+    assert int(sharded.route_splitmix(np.array([0], np.uint64))[0]) == 0xE220A8397B1DCDAF
+    assert sharded.route_owner(key, 1).tolist() == [0, 0, 0, 0]
+    assert all(0 <= o < 8 for o in sharded.route_owner(key, 8).tolist())
+
+
 def test_local_ranks_report_invalid_shard():
     c = _valid_traces(1, seed0=77)[0]
     c.start_ns = c.start_ns.copy()
@@ -99,8 +142,10 @@ def test_device_resident_ranks_on_gpu(cuda, g):
     """The device-resident pipeline (b2l_shard_route / all-to-all of device rows /
     b2l_shard_unpack / engine on device sub-traces) equals the single-GPU engine."""
     from paper_2601_12713_b200 import analyze_columns
-    from paper_2601_12713_b200.synth import c2_trace, c4_trace
-    cases = _valid_traces(40, seed0=7000 + g) + [c2_trace(100_000, seed=3), c4_trace(100_000, seed=5)]
+    from paper_2601_12713_b200.synth import c2_trace, c3_trace, c4_trace
+    cases = _valid_traces(40, seed0=7000 + g) + [c2_trace(100_000, seed=3), c4_trace(100_000, seed=5),
+                                                 c2_trace(30_000, n_targets=1, seed=6, n_host_vars=512),
+                                                 c3_trace(2000, array_bytes=1 << 16)]
     for c in cases:
         for strict in (False, True):
             got = sharded.run_local_device(c, g, strict=strict)
