@@ -580,7 +580,7 @@ struct HostBatch {
             *it.dst = slab.p + off;
             off += (it.bytes + 63) & ~size_t(63);
         }
-        CK(cudaStreamSynchronize(s));
+        stream_wait(s);
         items.clear();
     }
 };
@@ -874,7 +874,7 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
                 if (ng) read_back(&nm, total.p, sizeof(nm), s);
                 r.dd_members = nm;
             }
-            if (dd_side) CK(cudaStreamSynchronize(s));
+            if (dd_side) stream_wait(s);
         } catch (const EngineErr &e) {
             errd = e;
             faild = true;
@@ -1168,11 +1168,7 @@ void ra_step(const DevCols &c, uint32_t nP, Internal &out, cudaStream_t s) {
     compact(nP, [=] __device__(size_t g) { return g < *nsp && ss[g + 1] - ss[g] >= 2; }, gseg.p, gc.p, s);
     uint32_t cnts[2];
     {
-        uint8_t *st = pinned(s).reserve(8);
-        to_host_async(st, scount.p, 4, s);
-        to_host_async(st + 4, gc.p, 4, s);
-        CK(cudaStreamSynchronize(s));
-        memcpy(cnts, st, 8);
+        read_back_multi({{&cnts[0], scount.p, 4}, {&cnts[1], gc.p, 4}}, s);
     }
     const uint32_t nseg = cnts[0], ng = cnts[1];
     out.ra_groups = ng;
@@ -1827,14 +1823,7 @@ void sv_finish(SvRun &R, b2l_savings *o, cudaStream_t s, cudaStream_t copy) {
     unsigned long long h[15];
     uint32_t hov = 0, hun = 0;
     {  // one synchronisation for the three small results
-        uint8_t *st = pinned(s).reserve(sizeof(h) + 8);
-        to_host_async(st, R.acc.p, sizeof(h), s);
-        to_host_async(st + sizeof(h), R.ovl.p, 4, s);
-        to_host_async(st + sizeof(h) + 4, R.unic.p, 4, s);
-        CK(cudaStreamSynchronize(s));
-        memcpy(h, st, sizeof(h));
-        memcpy(&hov, st + sizeof(h), 4);
-        memcpy(&hun, st + sizeof(h) + 4, 4);
+        read_back_multi({{h, R.acc.p, sizeof(h)}, {&hov, R.ovl.p, 4}, {&hun, R.unic.p, 4}}, s);
     }
     for (int k = 0; k < 5; ++k) o->per_category_ns[k] = b2l_u128{h[2 * k], h[2 * k + 1]};
     o->union_ns = b2l_u128{h[10], h[11]};
@@ -1933,7 +1922,7 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     pc.mark("sv-attr");
     cudaStream_t sc = engine_stream_n(4);
     sv_finish(R, o, s, sc);
-    CK(cudaStreamSynchronize(sc));
+    stream_wait(sc);
     pc.mark("sv-d2h");
     if (alloc_stats().on)
         fprintf(stderr, "[b2l] savings arena %.1f of %.1f MB (%.0f B/event)\n", arena.off.load() / 1048576.0,
@@ -1998,16 +1987,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
             k_front_apply<<<ftiles, FR_THREADS, 0, s>>>(c, false, raw, fpart.p, fo);
             CK_LAUNCH("k_front_apply");
         }
-        uint8_t rb[sizeof(FrontAcc) + sizeof(hm)];
-        {
-            uint8_t *st = pinned(s).reserve(sizeof(rb));
-            to_host_async(st, fpart.p + ftiles, sizeof(FrontAcc), s);
-            to_host_async(st + sizeof(FrontAcc), agg.p, sizeof(hm), s);
-            CK(cudaStreamSynchronize(s));
-            memcpy(rb, st, sizeof(rb));
-        }
-        memcpy(&ftot, rb, sizeof(FrontAcc));
-        memcpy(hm, rb + sizeof(FrontAcc), sizeof(hm));
+        read_back_multi({{&ftot, fpart.p + ftiles, sizeof(FrontAcc)}, {hm, agg.p, sizeof(hm)}}, s);
     }
     const uint32_t nbad = ftot.c[0];
     if (nbad) {
@@ -2098,7 +2078,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
                 in->slab_pairs = new HostSlab();
                 hb.flush_async(*in->slab_pairs, s2, sc);
             }
-            if (overlap) CK(cudaStreamSynchronize(s2));
+            if (overlap) stream_wait(s2);
         } catch (const EngineErr &e) {
             err2 = e;
             failed2 = true;
@@ -2132,7 +2112,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
                 in->slab_kern = new HostSlab();
                 hb.flush_async(*in->slab_kern, s3, sc);
             }
-            if (overlap) CK(cudaStreamSynchronize(s3));
+            if (overlap) stream_wait(s3);
         } catch (const EngineErr &e) {
             err3 = e;
             failed3 = true;
@@ -2196,7 +2176,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
         in->fused_n = cols->n_events;
         sv_finish(R, o, s, sc);
     }
-    CK(cudaStreamSynchronize(sc));
+    stream_wait(sc);
     pc.mark("d2h");
     if (alloc_stats().on) {
         fprintf(stderr, "[b2l] pool alloc/free calls %llu, host %.3f ms; arena %.1f of %.1f MB (%.0f B/event)\n",

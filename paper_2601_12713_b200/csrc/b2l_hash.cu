@@ -612,7 +612,9 @@ struct WarpSched {
 __device__ __forceinline__ void named_bar(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
-template <int WARPS, int S>
+// RAGGED = false compiles only the uniform path (one warp per buffer): without the split pairs'
+// registers more CTAs fit per SM, so a uniform batch keeps every buffer in flight at once.
+template <int WARPS, int S, bool RAGGED>
 __global__ void __launch_bounds__(WARPS * 32) k_hash_warp(const uint64_t *__restrict__ ptrs,
                                                           const uint64_t *__restrict__ lens,
                                                           const uint32_t *__restrict__ order, uint64_t n_bufs,
@@ -623,6 +625,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_hash_warp(const uint64_t *__rest
     __shared__ uint32_t s_lead, s_item[2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint8_t *ring = smem + (size_t)warp * S * CH;
+    if (!RAGGED || !sch) {  // uniform batch: one warp per buffer, all in flight at once
+        const uint64_t k = (uint64_t)blockIdx.x * WARPS + warp;
+        if (k < n_bufs) {
+            BufCursor cur;
+            cursor_load(cur, ptrs, lens, order, k, n_bufs);
+            warp_fold<S>(cur, lane, ring, digests);
+        }
+        return;
+    }
     if (split) {
         static_assert(WARPS == 4, "a lead CTA holds two split pairs");
         if (threadIdx.x == 0) {
@@ -660,15 +671,6 @@ __global__ void __launch_bounds__(WARPS * 32) k_hash_warp(const uint64_t *__rest
             }
             ring = pr + (size_t)role * S * CH;  // this pair's area, split between its two warps
         }
-    }
-    if (!sch) {  // uniform batch: one warp per buffer, all in flight at once
-        const uint64_t k = (uint64_t)blockIdx.x * WARPS + warp;
-        if (k < n_bufs) {
-            BufCursor cur;
-            cursor_load(cur, ptrs, lens, order, k, n_bufs);
-            warp_fold<S>(cur, lane, ring, digests);
-        }
-        return;
     }
     // claim the next position of [split, n) and fold it with this warp alone
     for (;;) {
@@ -803,12 +805,13 @@ int hash_batch_launch(const uint64_t *d_ptrs, const uint64_t *d_lens, uint64_t n
     if (!c) return fail(B2L_E_CUDA, "b2l_hash_batch: cannot configure hash kernel");
     if (setenv_variant < 0 && !getenv("B2L_HASH_CFG") && n <= WARP_MAX_BUFS) {
         // few buffers: one warp each (every buffer's chain runs at its own latency)
-        auto fn = k_hash_warp<WARP_K_WARPS, WARP_K_STAGES>;
+        auto fn = d_order ? k_hash_warp<WARP_K_WARPS, WARP_K_STAGES, true> : k_hash_warp<WARP_K_WARPS, WARP_K_STAGES, false>;
         static bool smem_set[64] = {false};
         int cur_dev = 0;
         B2L_CUDA(cudaGetDevice(&cur_dev));
         if (!smem_set[cur_dev & 63]) {  // the split pairs' rings exceed the 48 KiB default
-            B2L_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WARP_K_SMEM));
+            B2L_CUDA(cudaFuncSetAttribute(k_hash_warp<WARP_K_WARPS, WARP_K_STAGES, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WARP_K_SMEM));
             smem_set[cur_dev & 63] = true;
         }
         // ragged (longest-first order given): three warps per scheduler claiming the list (the

@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -638,12 +639,125 @@ inline SlabPool &slab_pool() {
 inline void to_host_async(void *h_pinned, const void *d_src, size_t bytes, cudaStream_t s) {
     if (bytes) CK(cudaMemcpyAsync(h_pinned, d_src, bytes, cudaMemcpyDeviceToHost, s));
 }
+// Small read-backs (the "how many?" counts that size the next step) go through a per-stream
+// MAILBOX in mapped pinned memory: one tiny kernel copies the value there and then bumps a tag
+// (__threadfence_system in between), the host spins on the tag.  A D2H copy + stream
+// synchronisation costs ~23 us per round trip and ~60 us while a host->device upload shares the
+// PCIe link (analyze_many uploads the next trace beside the current analysis); the mailbox costs
+// ~8 / ~36 us (tools/pipe_exp4.py).  The tag lands after every earlier operation of the stream,
+// so the read is also a stream barrier.  While spinning, cudaStreamQuery surfaces faults.
+constexpr size_t MAILBOX_BYTES = 256;
+struct Mailbox {
+    uint8_t *host = nullptr;  // [0, 4): tag; [64, 64 + MAILBOX_BYTES): payload (mapped, UVA)
+    uint32_t seq = 0;
+};
+inline Mailbox &mailbox(cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<cudaStream_t, Mailbox> by_stream;
+    std::lock_guard<std::mutex> lock(mu);
+    Mailbox &m = by_stream[s];
+    if (!m.host) {
+        CK(cudaHostAlloc((void **)&m.host, 64 + MAILBOX_BYTES, cudaHostAllocMapped | cudaHostAllocPortable));
+        memset(m.host, 0, 64 + MAILBOX_BYTES);
+    }
+    return m;
+}
+static __global__ void k_mailbox(const uint8_t *__restrict__ src, uint32_t bytes, uint8_t *box, uint32_t tag) {
+    for (uint32_t i = threadIdx.x; i < bytes; i += blockDim.x) box[64 + i] = src[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        *reinterpret_cast<volatile uint32_t *>(box) = tag;
+    }
+}
+inline bool mailbox_on() {
+    static const bool on = !getenv("B2L_NO_MAILBOX");
+    return on;
+}
+inline void mailbox_wait(Mailbox &m, uint32_t tag, cudaStream_t s) {
+    const volatile uint32_t *t = reinterpret_cast<volatile uint32_t *>(m.host);
+    for (uint32_t spin = 1;; ++spin) {
+        if (*t == tag) break;
+        if ((spin & 1023u) == 0) {  // a faulted stream never delivers the tag
+            const cudaError_t e = cudaStreamQuery(s);
+            if (e != cudaSuccess && e != cudaErrorNotReady) CK(e);
+            if (e == cudaSuccess && *t != tag) CK(cudaStreamSynchronize(s));  // idle: the write is in flight
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+}
 // Read `bytes` from device memory into host `dst` (synchronous).
 inline void read_back(void *dst, const void *d_src, size_t bytes, cudaStream_t s) {
+    if (bytes <= MAILBOX_BYTES && mailbox_on()) {
+        Mailbox &m = mailbox(s);
+        const uint32_t tag = ++m.seq ? m.seq : ++m.seq;
+        k_mailbox<<<1, 64, 0, s>>>(static_cast<const uint8_t *>(d_src), (uint32_t)bytes, m.host, tag);
+        CK(cudaGetLastError());
+        mailbox_wait(m, tag, s);
+        memcpy(dst, m.host + 64, bytes);
+        return;
+    }
     uint8_t *st = pinned(s).reserve(bytes);
     to_host_async(st, d_src, bytes, s);
     CK(cudaStreamSynchronize(s));
     memcpy(dst, st, bytes);
+}
+// Several small device values in one mailbox trip (up to 8 pieces, MAILBOX_BYTES in total).
+struct ReadPiece {
+    void *dst;
+    const void *src;
+    size_t bytes;
+};
+struct MailboxPieces {
+    const uint8_t *src[8];
+    uint32_t bytes[8];
+    uint32_t n;
+};
+static __global__ void k_mailbox_multi(MailboxPieces p, uint8_t *box, uint32_t tag) {
+    uint32_t off = 0;
+    for (uint32_t k = 0; k < p.n; ++k) {
+        for (uint32_t i = threadIdx.x; i < p.bytes[k]; i += blockDim.x) box[64 + off + i] = p.src[k][i];
+        off += p.bytes[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        *reinterpret_cast<volatile uint32_t *>(box) = tag;
+    }
+}
+inline void read_back_multi(std::initializer_list<ReadPiece> pieces, cudaStream_t s) {
+    size_t total = 0;
+    for (const ReadPiece &q : pieces) total += q.bytes;
+    if (!mailbox_on() || pieces.size() > 8 || total > MAILBOX_BYTES) {
+        uint8_t *st = pinned(s).reserve(total);
+        size_t off = 0;
+        for (const ReadPiece &q : pieces) to_host_async(st + off, q.src, q.bytes, s), off += q.bytes;
+        CK(cudaStreamSynchronize(s));
+        off = 0;
+        for (const ReadPiece &q : pieces) memcpy(q.dst, st + off, q.bytes), off += q.bytes;
+        return;
+    }
+    MailboxPieces mp{};
+    for (const ReadPiece &q : pieces) mp.src[mp.n] = static_cast<const uint8_t *>(q.src), mp.bytes[mp.n++] = (uint32_t)q.bytes;
+    Mailbox &m = mailbox(s);
+    const uint32_t tag = ++m.seq ? m.seq : ++m.seq;
+    k_mailbox_multi<<<1, 64, 0, s>>>(mp, m.host, tag);
+    CK(cudaGetLastError());
+    mailbox_wait(m, tag, s);
+    size_t off = 0;
+    for (const ReadPiece &q : pieces) memcpy(q.dst, m.host + 64 + off, q.bytes), off += q.bytes;
+}
+// Wait until everything queued on `s` has run (cudaStreamSynchronize through the mailbox).
+inline void stream_wait(cudaStream_t s) {
+    if (!mailbox_on()) {
+        CK(cudaStreamSynchronize(s));
+        return;
+    }
+    Mailbox &m = mailbox(s);
+    const uint32_t tag = ++m.seq ? m.seq : ++m.seq;
+    k_mailbox<<<1, 32, 0, s>>>(nullptr, 0, m.host, tag);
+    CK(cudaGetLastError());
+    mailbox_wait(m, tag, s);
 }
 
 // ---------------------------------------------------------------- compaction

@@ -34,10 +34,11 @@ ok = np.array_equal(out.cpu().numpy().view(np.uint64), want)
 print(f"{'one 1 MiB + 1999 x 1 KiB' if os.environ.get('ONE_LONG') else 'C1'} {part or ''} wps={os.environ.get('B2L_RAGGED_WPS','-')} lead={os.environ.get('B2L_LEAD_TICKET','-')} split={os.environ.get('B2L_HASH_NO_SPLIT') is None}: {dt*1e3:.3f} ms {lens.sum()/dt/1e9:.1f} GB/s digests ok={ok}")
 PY
 python /tmp/c1t.py
+B2L_HASH_NO_DUAL=1 python /tmp/c1t.py
 B2L_HASH_NO_SPLIT=1 python /tmp/c1t.py
 B2L_RAGGED_WPS=3 python /tmp/c1t.py
-B2L_RAGGED_WPS=4 python /tmp/c1t.py
 PART=top python /tmp/c1t.py
 PART=rest python /tmp/c1t.py
-PART=rest B2L_RAGGED_WPS=3 python /tmp/c1t.py
-timeout 600 python -m pytest tests/test_hash_gpu.py -q -x 2>&1 | tail -2
+PART=rest B2L_HASH_NO_DUAL=1 python /tmp/c1t.py
+bash tools/gpu/chain.sh 2>&1 | tail -1
+timeout 600 python -m pytest tests/test_hash_gpu.py tests/test_capture.py -q -x 2>&1 | tail -2
