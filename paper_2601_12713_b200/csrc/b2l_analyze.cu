@@ -1960,7 +1960,10 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     // their own, smaller arena once the partition counts bound them)
     Arena arena;
     SideJoin side_join;
-    arena.open(n <= ARENA_MAX_EVENTS ? ARENA_BASE + n * ARENA_ANALYZE_PER_EVENT : 0, s);
+    // zeroed pool: the scans' flags and the radix passes' look-back status words (1-KiB status
+    // per 1024-record tile under ~1.2M records, per 4096-record tile above)
+    arena.open(n <= ARENA_MAX_EVENTS ? ARENA_BASE + n * ARENA_ANALYZE_PER_EVENT : 0, s,
+               (size_t(64) << 10) + (n < (size_t(2) << 20) ? n * 16 : n * 2));
     ArenaUse arena_use(&arena);
     // ---- 1+2. validation, partition, max end, key-bit masks, start ranks (fused front pass)
     const bool validate = !(flags & B2L_ANALYZE_NO_VALIDATE), raw = (flags & B2L_ANALYZE_RAW_HASHED) != 0;
@@ -2028,7 +2031,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     if (with_sv) sv_begin(R, c, s);
     {  // upper bounds of the device findings: DD/RT offsets and members <= nH, pairs/RA/UA <= nA, UT <= n
         const size_t fb = 16 * (nH + 2) + 12 * (size_t)nH + 8 * (nA + 2) + 16 * (size_t)nA + 4 * n + 32 * 256;
-        in->keep.open(n <= ARENA_MAX_EVENTS ? fb : 0, s);
+        in->keep.open(n <= ARENA_MAX_EVENTS ? fb : 0, s, 0);
     }
     in->synth_end = me;
     in->n_pairs = nA;

@@ -75,23 +75,40 @@ struct Arena {
     size_t cap = 0;
     std::atomic<size_t> off{0};
     cudaStream_t s = nullptr;
-    void open(size_t bytes, cudaStream_t st) {
+    // A zeroed pool at the head of the arena (one fill when it opens) serves the small scratch
+    // that must start at zero -- look-back flags and tile tickets of the scans -- so a scan is one
+    // launch instead of a fill and a launch (~35 scans per analysis call).
+    uint8_t *zbase = nullptr;
+    size_t zcap = 0;
+    std::atomic<size_t> zoff{0};
+    void open(size_t bytes, cudaStream_t st, size_t zero_bytes = size_t(64) << 10) {
         s = st;
         if (!bytes) return;
-        if (cudaMallocAsync((void **)&base, bytes, st) != cudaSuccess) {
+        zero_bytes = (zero_bytes + 255) & ~size_t(255);
+        if (cudaMallocAsync((void **)&base, bytes + zero_bytes, st) != cudaSuccess) {
             cudaGetLastError();  // no arena: every buffer comes from the pool
             base = nullptr;
             return;
         }
+        zbase = base, zcap = zero_bytes;
+        base += zero_bytes;
         cap = bytes;
+        zero_pool();
     }
+    inline void zero_pool();
     void *take(size_t bytes) {
         bytes = (bytes + 255) & ~size_t(255);
         const size_t o = off.fetch_add(bytes, std::memory_order_relaxed);
         return o + bytes <= cap ? base + o : nullptr;
     }
+    void *take_zeroed(size_t bytes) {
+        if (!zbase) return nullptr;
+        bytes = (bytes + 15) & ~size_t(15);
+        const size_t o = zoff.fetch_add(bytes, std::memory_order_relaxed);
+        return o + bytes <= zcap ? zbase + o : nullptr;
+    }
     ~Arena() {
-        if (base) cudaFreeAsync(base, s);
+        if (zbase) cudaFreeAsync(zbase, s);
     }
 };
 // the arena the calling thread's buffers come from (set for the duration of an engine call, and in
@@ -136,6 +153,7 @@ inline void dev_memset(void *p, int v, size_t bytes, cudaStream_t s) {
     k_fill_bytes<<<fill_grid(bytes), 256, 0, s>>>((uint8_t *)p, bytes, b | (b << 8) | (b << 16) | (b << 24));
     CK(cudaGetLastError());
 }
+inline void Arena::zero_pool() { dev_memset(zbase, 0, zcap, s); }
 inline void dev_copy(void *d, const void *src, size_t bytes, cudaStream_t s) {
     if (!bytes) return;
     k_copy_bytes<<<fill_grid(bytes), 256, 0, s>>>((uint8_t *)d, (const uint8_t *)src, bytes);
@@ -550,8 +568,11 @@ void scan(size_t n, Load ld, Store st, cudaStream_t s, typename Op::T *d_total =
     const size_t fwords = (tiles + 1 + 3) & ~size_t(3);
     const size_t tv = (tiles * sizeof(T) + 15) & ~size_t(15);
     DBuf<uint8_t> ws(fwords * 4 + 2 * tv, s);
-    uint32_t *flag = reinterpret_cast<uint32_t *>(ws.p);
-    dev_memset(flag, 0, fwords * 4, s);
+    uint32_t *flag = t_arena ? static_cast<uint32_t *>(t_arena->take_zeroed(fwords * 4)) : nullptr;
+    if (!flag) {  // no zeroed pool left: this scan's own scratch, zeroed
+        flag = reinterpret_cast<uint32_t *>(ws.p);
+        dev_memset(flag, 0, fwords * 4, s);
+    }
     T *agg = reinterpret_cast<T *>(ws.p + fwords * 4), *inc = reinterpret_cast<T *>(ws.p + fwords * 4 + tv);
     if constexpr (striped) {
         constexpr size_t smem = scan_smem<T>();
@@ -1039,8 +1060,16 @@ void radix_sort(SortBufs<KW> &b, size_t n, LiveBytes<KW> live, cudaStream_t s) {
     for (int w = 0; w < KW; ++w) npass += __builtin_popcount(live.m[w]);
     if (npass == 0) return;
     constexpr int NPOS = KW * 8;
-    DBuf<uint32_t> hist((size_t)NPOS * 256, s);
-    hist.zero();
+    DBuf<uint32_t> hist_own;
+    uint32_t *hist_p = t_arena ? static_cast<uint32_t *>(t_arena->take_zeroed((size_t)NPOS * 256 * 4)) : nullptr;
+    if (!hist_p) {
+        hist_own.alloc((size_t)NPOS * 256, s);
+        hist_own.zero();
+        hist_p = hist_own.p;
+    }
+    struct {
+        uint32_t *p;
+    } hist{hist_p};
     k_radix_hist_all<KW><<<grid_for(n, RS_THREADS * 4, 148 * 4), RS_THREADS, 0, s>>>(b.k[b.cur], n, live, hist.p);
     CK_LAUNCH("k_radix_hist_all");
     // sorts under ~1.2M records use 1024-record tiles: four times the CTAs, so a pass is not a few
@@ -1049,8 +1078,16 @@ void radix_sort(SortBufs<KW> &b, size_t n, LiveBytes<KW> live, cudaStream_t s) {
     const size_t tile = small ? (size_t)OS_THREADS * 4 : (size_t)OS_TILE;
     const unsigned ntiles = (unsigned)((n + tile - 1) / tile);
     const size_t stride = (size_t)ntiles * 256 + 32;  // status words + tile counter per pass
-    DBuf<uint32_t> status(stride * npass, s);
-    status.zero();
+    DBuf<uint32_t> status_own;
+    uint32_t *status_p = t_arena ? static_cast<uint32_t *>(t_arena->take_zeroed(stride * npass * 4)) : nullptr;
+    if (!status_p) {
+        status_own.alloc(stride * npass, s);
+        status_own.zero();
+        status_p = status_own.p;
+    }
+    struct {
+        uint32_t *p;
+    } status{status_p};
     int p = 0;
     for (int w = KW - 1; w >= 0; --w) {
         for (int byte = 0; byte < 8; ++byte) {
