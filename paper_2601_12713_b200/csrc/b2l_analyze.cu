@@ -1964,6 +1964,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     // per 1024-record tile under ~1.2M records, per 4096-record tile above)
     arena.open(n <= ARENA_MAX_EVENTS ? ARENA_BASE + n * ARENA_ANALYZE_PER_EVENT : 0, s,
                (size_t(64) << 10) + (n < (size_t(2) << 20) ? n * 16 : n * 2));
+    arena.mailbox = n <= (size_t(16) << 20);
     ArenaUse arena_use(&arena);
     // ---- 1+2. validation, partition, max end, key-bit masks, start ranks (fused front pass)
     const bool validate = !(flags & B2L_ANALYZE_NO_VALIDATE), raw = (flags & B2L_ANALYZE_RAW_HASHED) != 0;

@@ -80,6 +80,7 @@ struct Arena {
     // launch instead of a fill and a launch (~35 scans per analysis call).
     uint8_t *zbase = nullptr;
     size_t zcap = 0;
+    bool mailbox = true;  // small read-backs through the mailbox (read_back); off for huge calls
     std::atomic<size_t> zoff{0};
     void open(size_t bytes, cudaStream_t st, size_t zero_bytes = size_t(64) << 10) {
         s = st;
@@ -660,7 +661,9 @@ inline SlabPool &slab_pool() {
 inline void to_host_async(void *h_pinned, const void *d_src, size_t bytes, cudaStream_t s) {
     if (bytes) CK(cudaMemcpyAsync(h_pinned, d_src, bytes, cudaMemcpyDeviceToHost, s));
 }
-// Small read-backs (the "how many?" counts that size the next step) go through a per-stream
+// Small read-backs (the "how many?" counts that size the next step) of calls up to ~16M events
+// (their arena says so; huge calls overlap many-MB result copies, behind which the mailbox
+// kernel's host writes wait) go through a per-stream
 // MAILBOX in mapped pinned memory: one tiny kernel copies the value there and then bumps a tag
 // (__threadfence_system in between), the host spins on the tag.  A D2H copy + stream
 // synchronisation costs ~23 us per round trip and ~60 us while a host->device upload shares the
@@ -695,21 +698,27 @@ inline bool mailbox_on() {
     static const bool on = !getenv("B2L_NO_MAILBOX");
     return on;
 }
+// Spin on the tag without touching the driver (a cudaStreamQuery takes the driver lock the
+// other chains' launches need); after ~200 us of waiting, fall back to a blocking stream sync,
+// which also surfaces a fault (a faulted stream never delivers the tag).
 inline void mailbox_wait(Mailbox &m, uint32_t tag, cudaStream_t s) {
     const volatile uint32_t *t = reinterpret_cast<volatile uint32_t *>(m.host);
-    for (uint32_t spin = 1;; ++spin) {
-        if (*t == tag) break;
-        if ((spin & 1023u) == 0) {  // a faulted stream never delivers the tag
-            const cudaError_t e = cudaStreamQuery(s);
-            if (e != cudaSuccess && e != cudaErrorNotReady) CK(e);
-            if (e == cudaSuccess && *t != tag) CK(cudaStreamSynchronize(s));  // idle: the write is in flight
+    if (*t != tag) {
+        const auto t0 = std::chrono::steady_clock::now();
+        for (uint32_t spin = 1; *t != tag; ++spin) {
+            if ((spin & 255u) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(200)) {
+                CK(cudaStreamSynchronize(s));  // long wait: block (the tag landed with the stream's work)
+                while (*t != tag) {
+                }
+                break;
+            }
         }
     }
     std::atomic_thread_fence(std::memory_order_acquire);
 }
 // Read `bytes` from device memory into host `dst` (synchronous).
 inline void read_back(void *dst, const void *d_src, size_t bytes, cudaStream_t s) {
-    if (bytes <= MAILBOX_BYTES && mailbox_on()) {
+    if (bytes <= MAILBOX_BYTES && mailbox_on() && t_arena && t_arena->mailbox) {
         Mailbox &m = mailbox(s);
         const uint32_t tag = ++m.seq ? m.seq : ++m.seq;
         k_mailbox<<<1, 64, 0, s>>>(static_cast<const uint8_t *>(d_src), (uint32_t)bytes, m.host, tag);
@@ -749,7 +758,7 @@ static __global__ void k_mailbox_multi(MailboxPieces p, uint8_t *box, uint32_t t
 inline void read_back_multi(std::initializer_list<ReadPiece> pieces, cudaStream_t s) {
     size_t total = 0;
     for (const ReadPiece &q : pieces) total += q.bytes;
-    if (!mailbox_on() || pieces.size() > 8 || total > MAILBOX_BYTES) {
+    if (!mailbox_on() || !t_arena || !t_arena->mailbox || pieces.size() > 8 || total > MAILBOX_BYTES) {
         uint8_t *st = pinned(s).reserve(total);
         size_t off = 0;
         for (const ReadPiece &q : pieces) to_host_async(st + off, q.src, q.bytes, s), off += q.bytes;
@@ -768,18 +777,10 @@ inline void read_back_multi(std::initializer_list<ReadPiece> pieces, cudaStream_
     size_t off = 0;
     for (const ReadPiece &q : pieces) memcpy(q.dst, m.host + 64 + off, q.bytes), off += q.bytes;
 }
-// Wait until everything queued on `s` has run (cudaStreamSynchronize through the mailbox).
-inline void stream_wait(cudaStream_t s) {
-    if (!mailbox_on()) {
-        CK(cudaStreamSynchronize(s));
-        return;
-    }
-    Mailbox &m = mailbox(s);
-    const uint32_t tag = ++m.seq ? m.seq : ++m.seq;
-    k_mailbox<<<1, 32, 0, s>>>(nullptr, 0, m.host, tag);
-    CK(cudaGetLastError());
-    mailbox_wait(m, tag, s);
-}
+// Wait until everything queued on `s` has run.  (Not through the mailbox: these waits follow
+// large result copies, and a kernel writing into mapped host memory behind a device->host copy
+// stream waits for that link -- at 100M events the chains slowed from 47 to 110 ms.)
+inline void stream_wait(cudaStream_t s) { CK(cudaStreamSynchronize(s)); }
 
 // ---------------------------------------------------------------- compaction
 template <class Pred>
