@@ -187,7 +187,8 @@ int hash_host_impl(const void *const *h_bufs, const uint64_t *h_lens, uint64_t n
         // ---- form batch [i0, i1): fits one ring slot (a single oversized buffer gets its own, grown slot)
         uint64_t i1 = i0, bytes = 0;
         while (i1 < n) {
-            uint64_t sb = span_bytes((uint64_t)h_bufs[i1], h_lens[i1]);
+            // ring bytes of buffer i1 (with the gap a merged copy run carries; see the copy plan)
+            uint64_t sb = span_bytes((uint64_t)h_bufs[i1], h_lens[i1]) + (i1 > i0 ? 4096 : 0);
             if (i1 > i0 && (bytes + sb > RING_SLOT_BYTES || h_lens[i1] >= K2_MIN_BYTES)) break;
             if (h_lens[i1] >= K2_MIN_BYTES) {  // huge buffers are hashed alone by K2
                 bytes += sb;
@@ -210,7 +211,20 @@ int hash_host_impl(const void *const *h_bufs, const uint64_t *h_lens, uint64_t n
             uint64_t run_start = (uint64_t)h_bufs[k];
             uint64_t run_end = run_start + h_lens[k];
             uint64_t e = k + 1;
-            while (e < i1 && (uint64_t)h_bufs[e] == run_end) run_end += h_lens[e++];
+            // one DMA per run of buffers that follow each other in host memory: adjacent, or
+            // separated by a gap that lies in pages the two buffers already touch (a page holding
+            // any buffer byte is mapped -- and pinned, when the buffer is -- so copying the rest of
+            // it is safe).  Thousands of separate copies of small buffers cost ~5 us each.
+            auto joins = [&](uint64_t next) {
+                if (next < run_end) return false;
+                if (next == run_end) return true;
+                const uint64_t last_page = (run_end - 1) >> 12, next_page = next >> 12;
+                return run_end > run_start && next_page <= last_page + 1 && next - run_end <= 4096;
+            };
+            while (e < i1 && h_lens[e] && joins((uint64_t)h_bufs[e])) {
+                run_end = (uint64_t)h_bufs[e] + h_lens[e];
+                ++e;
+            }
             off = ((off + 15) & ~15ull) + (run_start & 15);
             uint8_t *dst = S.d_data + off;
             if (run_end > run_start)

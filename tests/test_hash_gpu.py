@@ -151,6 +151,44 @@ def test_split_pairs_chunk_edges_and_reuse(cuda):
     assert _device_digests(cuda, payloads, order=order) == want
 
 
+def test_host_batch_merged_copy_runs(cuda):
+    """b2l_hash_host merges buffers that follow each other in host memory -- adjacent, or with a
+    gap inside pages the two buffers touch -- into one DMA (b2l_api.cu copy plan): gaps of
+    0..4096 bytes at every alignment, buffers out of address order, a buffer inside another's
+    run, and buffers in separate allocations, pinned and pageable."""
+    import torch
+    from paper_2601_12713_b200.hashing import hash_host_arrays
+    rng = np.random.default_rng(41)
+    lens = [int(x) for x in rng.integers(1, 20000, size=600)]
+    gaps = [int(rng.choice([0, 0, 1, 7, 15, 16, 100, 255, 4000, 4096, 4097, 9000])) for _ in lens]
+    total = sum(lens) + sum(gaps) + 64
+    pinned = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+    host = pinned.numpy()
+    host[:] = np.frombuffer(rng.bytes(total), np.uint8)
+    offs, pos = [], 3
+    for n, g in zip(lens, gaps):
+        offs.append(pos)
+        pos += n + g
+    payloads = [bytes(host[o:o + n]) for o, n in zip(offs, lens)]
+    base = pinned.data_ptr()
+    order = np.arange(len(lens))
+    order[100:200] = order[100:200][::-1]  # a stretch out of address order
+    ptrs = np.array([base + offs[i] for i in order], np.uint64)
+    ln = np.array([lens[i] for i in order], np.uint64)
+    extra = [np.frombuffer(rng.bytes(n), np.uint8).copy() for n in (5, 4096, 70001)]  # pageable, separate
+    inside = (offs[10] + 1, max(lens[10] - 1, 1))  # inside another buffer's run
+    ptrs = np.concatenate([ptrs[:50], np.array([e.ctypes.data for e in extra], np.uint64), ptrs[50:],
+                           np.array([base + inside[0]], np.uint64)])
+    ln = np.concatenate([ln[:50], np.array([e.size for e in extra], np.uint64), ln[50:],
+                         np.array([inside[1]], np.uint64)])
+    want = [hash_ref.fold64_c(payloads[i]) for i in order]
+    want = want[:50] + [hash_ref.fold64_c(e.tobytes()) for e in extra] + want[50:] + \
+        [hash_ref.fold64_c(bytes(host[inside[0]:inside[0] + inside[1]]))]
+    out = np.zeros(ptrs.size, np.uint64)
+    hash_host_arrays(ptrs, ln, out)
+    assert out.tolist() == want
+
+
 def test_zero_length_gets_reserved_digest_and_host_raises(cuda):
     from paper_2601_12713_b200 import EmptyPayload, hash_batch, hash_bytes
     payloads = [b"abc", b"", b"x" * 100]
