@@ -814,7 +814,8 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
     pc.mark(" q-scan");
     // ---- DD groups need only the queue scan: on small traces they run on their own stream (and
     // host thread) beside the RT matching and grouping, which are latency bound there
-    const bool dd_side = R <= (size_t(8) << 20);
+    static const uint64_t side_min = getenv("B2L_SIDE_MIN") ? strtoull(getenv("B2L_SIDE_MIN"), nullptr, 10) : 0;
+    const bool dd_side = R <= (size_t(8) << 20) && R >= side_min;
     int dev = 0;
     CK(cudaGetDevice(&dev));
     const Masks masks = g_masks;
@@ -2044,7 +2045,8 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     CK(cudaGetDevice(&dev));
     const Masks masks = g_masks;
     PairOut po;
-    const bool overlap = n <= (size_t(4) << 20);
+    static const uint64_t overlap_min = getenv("B2L_OVERLAP_MIN") ? strtoull(getenv("B2L_OVERLAP_MIN"), nullptr, 10) : 0;
+    const bool overlap = n <= (size_t(4) << 20) && n >= overlap_min;
     cudaStream_t s2 = overlap ? engine_stream_n(1) : s, s3 = overlap ? engine_stream_n(2) : s;
     cudaStream_t sc = engine_stream_n(4);  // device -> host result copies, chain by chain
     if (overlap) {  // the partition lists and start ranks are produced on s
