@@ -902,8 +902,8 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
             DBuf<uint32_t> hstart(nH, s), hcount(1, s);
             compact(nH, HeadPred<1>{hk}, hstart.p, hcount.p, s);
             const uint32_t nhseg = read_u32(hcount.p, s);
-            DBuf<uint32_t> qhead(nseg, s);
-            qhead.zero();
+            DBuf<uint32_t> qhead;
+            qhead.alloc_zeroed(nseg, s);
             k_rt_strict<<<grid_for(nhseg, 128), 128, 0, s>>>(c, H, hsort.val(), hstart.p, nhseg, nH, hid.p, segk.p,
                                                              nseg, seg_rxbase.p, rxpos.p, sval, qhead.p, match.p);
             CK_LAUNCH("k_rt_strict");
@@ -1076,8 +1076,8 @@ PairOut pairs_step(const DevCols &c, const uint32_t *AD, uint32_t nAD, const uin
     scan<SumU32>(nAD, HeadLoad<2>{sk}, StoreInclMinus1{seg.p}, s);
     // unmatched deletes -> warnings in trace order (flag by AD rank, compact in AD order)
     {
-        DBuf<uint8_t> unmatched(nAD, s);
-        unmatched.zero();
+        DBuf<uint8_t> unmatched;
+        unmatched.alloc_zeroed(nAD, s);
         uint8_t *um = unmatched.p;
         const uint32_t *lv = level.p;
         const uint8_t *kind = c.kind;
@@ -1313,9 +1313,8 @@ void build_kernel_index(KernelIndexStore &X, const DevCols &c, const uint32_t *T
         }
         // per-device kernel ranges (one lookup instead of two binary searches per query)
         const bool small_ndev = c.ndev > 0 && c.ndev <= (1 << 16);
-        dlo.alloc(small_ndev ? c.ndev : 1, s), dhi.alloc(small_ndev ? c.ndev : 1, s);
+        dlo.alloc_zeroed(small_ndev ? c.ndev : 1, s), dhi.alloc_zeroed(small_ndev ? c.ndev : 1, s);
         if (small_ndev) {
-            dlo.zero(), dhi.zero();
             uint32_t *lo = dlo.p, *hi = dhi.p;
             const uint64_t *kd = ks.key(0);
             const uint32_t nk = nK;
@@ -1363,8 +1362,8 @@ void ua_step(const DevCols &c, const KernelIndex &KI, Internal &out, cudaStream_
 // UT (detectors.py:232-271).
 void ut_step(const DevCols &c, const KernelIndex &KI, const uint32_t *TT, uint32_t nT, Internal &out,
              cudaStream_t s) {
-    DBuf<uint8_t> flag(c.n ? c.n : 1, s);
-    flag.zero();
+    DBuf<uint8_t> flag;
+    flag.alloc_zeroed(c.n ? c.n : 1, s);
     if (nT) {
         DBuf<uint32_t> cur(nT, s), run(nT, s);
         DBuf<uint8_t> cls(nT, s);
@@ -1735,11 +1734,9 @@ void sv_begin(SvRun &R, const DevCols &c, cudaStream_t s) {
     R.n = c.n;
     R.nb = c.nbuckets;
     R.at.alloc(5 * (size_t)R.nb * 6 + 1, s);
-    R.at.zero();
-    dev_memset(R.at.p + 5 * (size_t)R.nb * 5, 0xFF, 5 * (size_t)R.nb * sizeof(unsigned long long), s);
+    init_u64(R.at.p, 5 * (size_t)R.nb * 5, 5 * (size_t)R.nb, 1, s);  // the first-member slots start at ~0
     R.smem = R.nb <= 512 ? (size_t)R.nb * 6 * sizeof(unsigned long long) : 0;
-    R.cat.alloc(((R.n ? R.n : 1) + 3) & ~size_t(3), s);  // whole words: byte atomics touch the word
-    R.cat.zero();
+    R.cat.alloc_zeroed(((R.n ? R.n : 1) + 3) & ~size_t(3), s);  // whole words: byte atomics touch the word
 }
 
 // Attribution + category bits of category k (DD 0, RT 1, RA 2, UA 3, UT 4) on stream st.
@@ -1805,16 +1802,14 @@ void sv_finish(SvRun &R, b2l_savings *o, cudaStream_t s, cudaStream_t copy) {
     const size_t n = R.n;
     const DevCols c = R.c;
     R.acc.alloc(12 + 1 + 2, s);
-    R.acc.zero();
-    dev_memset(R.acc.p + 13, 0xFF, sizeof(unsigned long long), s);  // min start := ~0 (max end stays 0)
+    init_u64(R.acc.p, 13, 1, 1, s);  // min start := ~0 (max end stays 0)
     if (n) {
         k_sums<<<grid_for(n, TPB, 148 * 4), TPB, 0, s>>>(c, R.cat.p, R.acc.p, R.acc.p + 12, R.acc.p + 13);
         CK_LAUNCH("k_sums");
     }
     // overlap: exists i >= 1 with start[i] < max(end[0..i-1])  (estimator.py:51-58)
     // ... and the union list, in the same scan
-    R.ovl.alloc(1, s);
-    R.ovl.zero();
+    R.ovl.alloc_zeroed(1, s);
     R.uni.alloc(n ? n : 1, s);
     R.unic.alloc(1, s);
     R.ovt.alloc(1, s);
@@ -1874,7 +1869,8 @@ int savings_impl(const b2l_trace_cols *cols, const b2l_findings *f, b2l_savings 
     cudaStream_t s = engine_stream();
     Arena arena;  // this call's scratch (declared first: released last)
     SideJoin side_join;
-    arena.open(cols->n_events <= ARENA_MAX_EVENTS ? ARENA_BASE + cols->n_events * ARENA_SAVINGS_PER_EVENT : 0, s);
+    arena.open(cols->n_events <= ARENA_MAX_EVENTS ? ARENA_BASE + cols->n_events * ARENA_SAVINGS_PER_EVENT : 0, s,
+               (size_t(1) << 20) + cols->n_events * 2);
     ArenaUse arena_use(&arena);
     ColsUpload up;
     const Internal *fin = (const Internal *)f->internal;
@@ -1964,7 +1960,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     // zeroed pool: the scans' flags and the radix passes' look-back status words (1-KiB status
     // per 1024-record tile under ~1.2M records, per 4096-record tile above)
     arena.open(n <= ARENA_MAX_EVENTS ? ARENA_BASE + n * ARENA_ANALYZE_PER_EVENT : 0, s,
-               (size_t(64) << 10) + (n < (size_t(2) << 20) ? n * 16 : n * 2));
+               (size_t(1) << 20) + (n < (size_t(2) << 20) ? n * 20 : n * 4));
     arena.mailbox = n <= (size_t(16) << 20);
     ArenaUse arena_use(&arena);
     // ---- 1+2. validation, partition, max end, key-bit masks, start ranks (fused front pass)
@@ -1972,8 +1968,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     const unsigned ftiles = (unsigned)((n + FR_TILE - 1) / FR_TILE);
     DBuf<FrontAcc> fpart(ftiles + 1, s);
     DBuf<unsigned long long> agg(11, s);  // [0] max data-op end, [1..5] subset OR, [6..10] subset AND
-    agg.zero();
-    dev_memset(agg.p + 6, 0xFF, 5 * sizeof(unsigned long long), s);
+    init_u64(agg.p, 6, 5, 0, s);
     FrontAcc ftot{};
     unsigned long long hm[11] = {0, 0, 0, 0, 0, 0, ~0ull, ~0ull, ~0ull, ~0ull, ~0ull};
     // the five partition lists are sized n (an upper bound) so the apply pass is queued right

@@ -155,6 +155,17 @@ inline void dev_memset(void *p, int v, size_t bytes, cudaStream_t s) {
     CK(cudaGetLastError());
 }
 inline void Arena::zero_pool() { dev_memset(zbase, 0, zcap, s); }
+// u64 words [0, n0) = 0, [n0, n0 + n1) = ~0, then n2 more zeros, in one launch (accumulators
+// whose max / min slots start at the identity)
+static __global__ void k_init_u64(uint64_t *__restrict__ p, size_t n0, size_t n1, size_t n2) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n0 + n1 + n2; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = (i >= n0 && i < n0 + n1) ? ~0ull : 0ull;
+}
+inline void init_u64(void *p, size_t n0, size_t n1, size_t n2, cudaStream_t s) {
+    if (!n0 && !n1 && !n2) return;
+    k_init_u64<<<fill_grid((n0 + n1 + n2) * 8), 256, 0, s>>>((uint64_t *)p, n0, n1, n2);
+    CK(cudaGetLastError());
+}
 inline void dev_copy(void *d, const void *src, size_t bytes, cudaStream_t s) {
     if (!bytes) return;
     k_copy_bytes<<<fill_grid(bytes), 256, 0, s>>>((uint8_t *)d, (const uint8_t *)src, bytes);
@@ -186,6 +197,22 @@ struct DBuf {
     }
     void zero() {
         if (n) dev_memset(p, 0, n * sizeof(T), s);
+    }
+    // zero-initialised: from the call arena's zeroed pool when it has room (no fill launch)
+    void alloc_zeroed(size_t n_, cudaStream_t st) {
+        release();
+        s = st;
+        n = n_;
+        if (!n_) return;
+        if (t_arena) {
+            if (void *q = t_arena->take_zeroed(n_ * sizeof(T))) {
+                p = (T *)q;
+                arena = true;
+                return;
+            }
+        }
+        alloc(n_, st);
+        zero();
     }
     void release() {
         if (p && !arena) {
@@ -1259,8 +1286,8 @@ struct BigPred {
 inline void seg_fixup(SortBufs<1> &b, size_t n, int shift, uint8_t live, cudaStream_t s) {
     if (n <= 1) return;
     DBuf<uint8_t> big(n, s);
-    DBuf<uint32_t> cnt(2, s);  // [records in long runs, breaks inside long runs]
-    cnt.zero();
+    DBuf<uint32_t> cnt;  // [records in long runs, breaks inside long runs]
+    cnt.alloc_zeroed(2, s);
     const uint64_t *kin = b.k[b.cur].w[0];
     const uint32_t *vin = b.v[b.cur];
     uint64_t *kout = b.k[b.cur ^ 1].w[0];
@@ -1277,8 +1304,8 @@ inline void seg_fixup(SortBufs<1> &b, size_t n, int shift, uint8_t live, cudaStr
     // prefix, different key, between neighbours) are gathered, full-key sorted, scattered back
     DBuf<uint32_t> pos(nbig, s), pc(1, s);
     compact(n, BigPred{big.p}, pos.p, pc.p, s);
-    DBuf<uint32_t> rid(nbig, s), rflag(nbig, s), sel(nbig, s), nsel(1, s);
-    rflag.zero();
+    DBuf<uint32_t> rid(nbig, s), rflag, sel(nbig, s), nsel(1, s);
+    rflag.alloc_zeroed(nbig, s);
     const uint32_t *P = pos.p;
     scan<SumU32>(nbig, RunHeadLoad{P, kin, shift}, RunIdStore{P, kin, rid.p, rflag.p}, s);
     compact(nbig, RunFlagged{rid.p, rflag.p}, sel.p, nsel.p, s);
