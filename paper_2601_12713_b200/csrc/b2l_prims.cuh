@@ -1069,6 +1069,104 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(KeyCols<KW> in, cons
     }
 }
 
+// Sorts that fit one tile (<= ST_TILE records): every live digit pass in ONE CTA, the records
+// in shared memory between passes (the same warp-multisplit ranking as a Onesweep pass, without
+// the global histogram and look-back) -- one launch instead of a histogram + a pass per digit.
+// A small trace's analysis makes ~10 such sorts, each otherwise 3-5 launches.
+constexpr int ST_THREADS = 256, ST_ITEMS = 16, ST_TILE = ST_THREADS * ST_ITEMS;
+template <int KW>
+constexpr size_t sort_tile_smem() {
+    return (size_t)KW * ST_TILE * 8 + (size_t)ST_TILE * 4;
+}
+template <int KW>
+__global__ void __launch_bounds__(ST_THREADS) k_sort_tile(KeyCols<KW> in, const uint32_t *__restrict__ vin,
+                                                           KeyCols<KW> out, uint32_t *__restrict__ vout, uint32_t n,
+                                                           LiveBytes<KW> live) {
+    extern __shared__ __align__(16) uint8_t st_raw[];
+    uint64_t *sk = reinterpret_cast<uint64_t *>(st_raw);                         // [KW][ST_TILE]
+    uint32_t *sv = reinterpret_cast<uint32_t *>(st_raw + (size_t)KW * ST_TILE * 8);  // [ST_TILE]
+    __shared__ uint32_t wsum[OS_WARPS];
+    __shared__ uint32_t wcnt[OS_WARPS][256];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    for (uint32_t j = t; j < n; j += ST_THREADS) {
+#pragma unroll
+        for (int w = 0; w < KW; ++w) sk[(size_t)w * ST_TILE + j] = in.w[w][j];
+        sv[j] = vin[j];
+    }
+    __syncthreads();
+    const uint32_t wbase = (uint32_t)warp * (32 * ST_ITEMS) + lane;  // item i of lane l: wbase + 32 i
+    for (int w = KW - 1; w >= 0; --w) {
+        for (int byte = 0; byte < 8; ++byte) {
+            if (!((live.m[w] >> byte) & 1)) continue;
+            const int shift = 8 * byte;
+#pragma unroll
+            for (int ww = 0; ww < OS_WARPS; ++ww) wcnt[ww][t] = 0;
+            __syncthreads();
+            uint32_t slot[ST_ITEMS];
+            const uint32_t lt = lanemask_lt();
+#pragma unroll
+            for (int i = 0; i < ST_ITEMS; ++i) {
+                const uint32_t pos = wbase + 32 * i;
+                const bool valid = pos < n;
+                const uint32_t d = valid ? (uint32_t)(sk[(size_t)w * ST_TILE + pos] >> shift) & 255u : 256u;
+                const uint32_t peers = __match_any_sync(0xffffffffu, d);
+                const uint32_t before = valid ? wcnt[warp][d] : 0u;
+                __syncwarp();
+                if (valid && lane == 31 - __clz(peers)) wcnt[warp][d] = before + __popc(peers);
+                __syncwarp();
+                slot[i] = valid ? ((d << 16) | (before + __popc(peers & lt))) : 0xFFFFFFFFu;
+            }
+            __syncthreads();
+            uint32_t cnt = 0;  // digit t: counts per warp -> exclusive offsets across warps
+#pragma unroll
+            for (int ww = 0; ww < OS_WARPS; ++ww) {
+                const uint32_t c = wcnt[ww][t];
+                wcnt[ww][t] = cnt;
+                cnt += c;
+            }
+            uint32_t tot;
+            const uint32_t dstart = block256_excl(cnt, wsum, tot);
+#pragma unroll
+            for (int ww = 0; ww < OS_WARPS; ++ww) wcnt[ww][t] += dstart;
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < ST_ITEMS; ++i)
+                if (slot[i] != 0xFFFFFFFFu) slot[i] = wcnt[warp][slot[i] >> 16] + (slot[i] & 0xFFFFu);
+            // permute every key word and the value in place: load all, barrier, store all
+#pragma unroll
+            for (int kw = 0; kw < KW; ++kw) {
+                uint64_t v[ST_ITEMS];
+#pragma unroll
+                for (int i = 0; i < ST_ITEMS; ++i) v[i] = slot[i] != 0xFFFFFFFFu ? sk[(size_t)kw * ST_TILE + wbase + 32 * i] : 0;
+                __syncthreads();
+#pragma unroll
+                for (int i = 0; i < ST_ITEMS; ++i)
+                    if (slot[i] != 0xFFFFFFFFu) sk[(size_t)kw * ST_TILE + slot[i]] = v[i];
+                __syncthreads();
+            }
+            {
+                uint32_t v[ST_ITEMS];
+#pragma unroll
+                for (int i = 0; i < ST_ITEMS; ++i) v[i] = slot[i] != 0xFFFFFFFFu ? sv[wbase + 32 * i] : 0u;
+                __syncthreads();
+#pragma unroll
+                for (int i = 0; i < ST_ITEMS; ++i)
+                    if (slot[i] != 0xFFFFFFFFu) sv[slot[i]] = v[i];
+                __syncthreads();
+            }
+        }
+    }
+    for (uint32_t j = t; j < n; j += ST_THREADS) {
+#pragma unroll
+        for (int w = 0; w < KW; ++w) out.w[w][j] = sk[(size_t)w * ST_TILE + j];
+        vout[j] = sv[j];
+    }
+}
+
+inline bool sort_tiles_on() {
+    static const bool on = !getenv("B2L_NO_SORT_TILE");
+    return on;
+}
 template <int KW>
 struct SortBufs {
     KeyCols<KW> k[2];
@@ -1087,6 +1185,19 @@ void radix_sort(SortBufs<KW> &b, size_t n, LiveBytes<KW> live, cudaStream_t s) {
     int npass = 0;
     for (int w = 0; w < KW; ++w) npass += __builtin_popcount(live.m[w]);
     if (npass == 0) return;
+    if (n <= (size_t)ST_TILE && sort_tiles_on()) {  // one CTA, every pass in shared memory
+        constexpr size_t smem = sort_tile_smem<KW>();
+        static bool opted = false;  // per instantiation
+        if (!opted) {
+            CK(cudaFuncSetAttribute(k_sort_tile<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            opted = true;
+        }
+        k_sort_tile<KW><<<1, ST_THREADS, smem, s>>>(b.k[b.cur], b.v[b.cur], b.k[b.cur ^ 1], b.v[b.cur ^ 1],
+                                                    (uint32_t)n, live);
+        CK_LAUNCH("k_sort_tile");
+        b.cur ^= 1;
+        return;
+    }
     constexpr int NPOS = KW * 8;
     DBuf<uint32_t> hist_own;
     uint32_t *hist_p = t_arena ? static_cast<uint32_t *>(t_arena->take_zeroed((size_t)NPOS * 256 * 4)) : nullptr;
@@ -1336,6 +1447,10 @@ inline void seg_fixup(SortBufs<1> &b, size_t n, int shift, uint8_t live, cudaStr
 // segmented fix-up orders runs of equal high parts by the full key.
 inline void radix_sort_prefix(SortBufs<1> &b, size_t n, uint8_t live, int lowbyte, cudaStream_t s) {
     if (n <= 1 || !live) return;
+    if (n <= (size_t)ST_TILE && sort_tiles_on()) {  // small: the whole key in one tile sort, no fix-up
+        radix_sort<1>(b, n, LiveBytes<1>{{live}}, s);
+        return;
+    }
     const uint8_t top = (uint8_t)(live & (0xFFu << lowbyte));
     if (top == live || !top) {  // nothing below the prefix, or no prefix: plain LSD
         radix_sort<1>(b, n, LiveBytes<1>{{live}}, s);
@@ -1349,6 +1464,10 @@ inline void radix_sort_prefix(SortBufs<1> &b, size_t n, uint8_t live, int lowbyt
 // bytes for ~1 bit of slack over log2(n), then the fix-up (most runs have one record).
 inline void radix_sort_wide(SortBufs<1> &b, size_t n, uint8_t live, cudaStream_t s) {
     if (n <= 1 || !live) return;
+    if (n <= (size_t)ST_TILE && sort_tiles_on()) {
+        radix_sort<1>(b, n, LiveBytes<1>{{live}}, s);
+        return;
+    }
     int need = 2;
     while (need < 64 && (1ull << need) < (uint64_t)n) ++need;
     const int nbytes = (need + 1 + 7) / 8;
