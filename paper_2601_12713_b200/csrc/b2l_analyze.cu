@@ -2187,6 +2187,11 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
                 in->keep.cap / 1048576.0);
         alloc_stats().n = 0, alloc_stats().ns = 0;
     }
+    if (sync_stats().on) {
+        fprintf(stderr, "[b2l] host round trips %llu, %.3f ms waiting (all chains)\n",
+                (unsigned long long)sync_stats().n.load(), sync_stats().ns.load() * 1e-6);
+        sync_stats().n = 0, sync_stats().ns = 0;
+    }
     if (in->dd_groups == 0) f->dd_offsets[0] = 0;
     if (in->rt_groups == 0) f->rt_offsets[0] = 0;
     if (in->ra_groups == 0) f->ra_offsets[0] = 0;

@@ -49,6 +49,28 @@ struct AllocStats {
     std::atomic<uint64_t> n{0}, ns{0};
     bool on = getenv("B2L_TRACE") != nullptr;
 };
+// B2L_SYNC_STATS: host round trips per analysis call (read-backs and stream waits), per thread
+struct SyncStats {
+    std::atomic<uint64_t> n{0}, ns{0};
+    bool on = getenv("B2L_SYNC_STATS") != nullptr;
+};
+inline SyncStats &sync_stats() {
+    static SyncStats a;
+    return a;
+}
+struct SyncTimer {
+    bool on;
+    std::chrono::steady_clock::time_point t0;
+    SyncTimer() : on(sync_stats().on) {
+        if (on) t0 = std::chrono::steady_clock::now();
+    }
+    ~SyncTimer() {
+        if (!on) return;
+        sync_stats().n++;
+        sync_stats().ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                               std::chrono::steady_clock::now() - t0).count();
+    }
+};
 inline AllocStats &alloc_stats() {
     static AllocStats a;
     return a;
@@ -745,6 +767,7 @@ inline void mailbox_wait(Mailbox &m, uint32_t tag, cudaStream_t s) {
 }
 // Read `bytes` from device memory into host `dst` (synchronous).
 inline void read_back(void *dst, const void *d_src, size_t bytes, cudaStream_t s) {
+    SyncTimer st_;
     if (bytes <= MAILBOX_BYTES && mailbox_on() && t_arena && t_arena->mailbox) {
         Mailbox &m = mailbox(s);
         const uint32_t tag = ++m.seq ? m.seq : ++m.seq;
@@ -783,6 +806,7 @@ static __global__ void k_mailbox_multi(MailboxPieces p, uint8_t *box, uint32_t t
     }
 }
 inline void read_back_multi(std::initializer_list<ReadPiece> pieces, cudaStream_t s) {
+    SyncTimer st_;
     size_t total = 0;
     for (const ReadPiece &q : pieces) total += q.bytes;
     if (!mailbox_on() || !t_arena || !t_arena->mailbox || pieces.size() > 8 || total > MAILBOX_BYTES) {
@@ -807,7 +831,10 @@ inline void read_back_multi(std::initializer_list<ReadPiece> pieces, cudaStream_
 // Wait until everything queued on `s` has run.  (Not through the mailbox: these waits follow
 // large result copies, and a kernel writing into mapped host memory behind a device->host copy
 // stream waits for that link -- at 100M events the chains slowed from 47 to 110 ms.)
-inline void stream_wait(cudaStream_t s) { CK(cudaStreamSynchronize(s)); }
+inline void stream_wait(cudaStream_t s) {
+    SyncTimer st_;
+    CK(cudaStreamSynchronize(s));
+}
 
 // ---------------------------------------------------------------- compaction
 template <class Pred>
