@@ -412,7 +412,8 @@ def run_ours(args, rank, world, local):
         "impl": "ours",
     }
     if world > 1:
-        rec["step"] = "b2l_hash_batch over the rank's 16 GB + gather of every rank's digests to rank 0 (NCCL)"
+        rec["step"] = (f"b2l_hash_batch over the rank's {total / 1e9:.1f} GB + gather of every rank's digests to "
+                       f"rank 0 (NCCL)")
     del slab
     torch.cuda.empty_cache()
     return rec
