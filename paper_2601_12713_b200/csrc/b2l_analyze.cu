@@ -379,13 +379,13 @@ __global__ void __launch_bounds__(FR_THREADS, 2) k_front_apply(DevCols c, bool b
 // ============================================================ helpers
 template <class F>
 __global__ void k_for(size_t n, F f) {
+    pdl_enter();
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) f(i);
 }
 template <class F>
 void for_each(size_t n, F f, cudaStream_t s) {
     if (!n) return;
-    k_for<F><<<grid_for(n, TPB), TPB, 0, s>>>(n, f);
-    CK_LAUNCH("k_for");
+    launch_k(k_for<F>, grid_for(n, TPB), TPB, 0, s, n, f);
 }
 
 // Read a device u32 count (one sync).

@@ -143,10 +143,35 @@ struct ArenaUse {
     ~ArenaUse() { t_arena = prev; }
 };
 
+// Programmatic dependent launch: kernels of a chain are launched with programmatic stream
+// serialisation, enter with griddepcontrol.wait (every prerequisite grid complete, its memory
+// visible) and immediately allow their own dependents to be scheduled, so the next kernel's
+// launch processing overlaps this one instead of following its completion (small traces run
+// ~50 dependent kernels per chain).  Kernels launched without the attribute are unaffected.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+inline bool pdl_on() {
+    static const bool on = !getenv("B2L_NO_PDL");
+    return on;
+}
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid, cfg.blockDim = block, cfg.dynamicSmemBytes = smem, cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at, cfg.numAttrs = pdl_on() ? 1 : 0;
+    ck(cudaLaunchKernelEx(&cfg, k, args...), "cudaLaunchKernelEx");
+}
+
 // Device-side fill / copy as kernels, never through a copy engine: the engines may be busy with a
 // large host->device upload (analyze_many queues the next trace's upload beside this analysis), and
 // a memset or device-to-device copy queued behind it would stall the whole dependent chain.
 static __global__ void k_fill_bytes(uint8_t *__restrict__ p, size_t n, uint32_t v4) {
+    pdl_enter();
     const size_t head = (16 - ((uintptr_t)p & 15)) & 15;
     const size_t h = head < n ? head : n;
     const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
@@ -157,6 +182,7 @@ static __global__ void k_fill_bytes(uint8_t *__restrict__ p, size_t n, uint32_t 
     for (size_t i = h + nv * 16 + tid; i < n; i += stride) p[i] = (uint8_t)v4;
 }
 static __global__ void k_copy_bytes(uint8_t *__restrict__ d, const uint8_t *__restrict__ s, size_t n) {
+    pdl_enter();
     const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
     if ((((uintptr_t)d | (uintptr_t)s) & 15) == 0) {
         const size_t nv = n / 16;
@@ -173,24 +199,25 @@ inline unsigned fill_grid(size_t bytes) {
 inline void dev_memset(void *p, int v, size_t bytes, cudaStream_t s) {
     if (!bytes) return;
     const uint32_t b = (uint32_t)(v & 0xFF);
-    k_fill_bytes<<<fill_grid(bytes), 256, 0, s>>>((uint8_t *)p, bytes, b | (b << 8) | (b << 16) | (b << 24));
+    launch_k(k_fill_bytes, fill_grid(bytes), 256, 0, s, (uint8_t *)p, bytes, b | (b << 8) | (b << 16) | (b << 24));
     CK(cudaGetLastError());
 }
 inline void Arena::zero_pool() { dev_memset(zbase, 0, zcap, s); }
 // u64 words [0, n0) = 0, [n0, n0 + n1) = ~0, then n2 more zeros, in one launch (accumulators
 // whose max / min slots start at the identity)
 static __global__ void k_init_u64(uint64_t *__restrict__ p, size_t n0, size_t n1, size_t n2) {
+    pdl_enter();
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n0 + n1 + n2; i += (size_t)gridDim.x * blockDim.x)
         p[i] = (i >= n0 && i < n0 + n1) ? ~0ull : 0ull;
 }
 inline void init_u64(void *p, size_t n0, size_t n1, size_t n2, cudaStream_t s) {
     if (!n0 && !n1 && !n2) return;
-    k_init_u64<<<fill_grid((n0 + n1 + n2) * 8), 256, 0, s>>>((uint64_t *)p, n0, n1, n2);
+    launch_k(k_init_u64, fill_grid((n0 + n1 + n2) * 8), 256, 0, s, (uint64_t *)p, n0, n1, n2);
     CK(cudaGetLastError());
 }
 inline void dev_copy(void *d, const void *src, size_t bytes, cudaStream_t s) {
     if (!bytes) return;
-    k_copy_bytes<<<fill_grid(bytes), 256, 0, s>>>((uint8_t *)d, (const uint8_t *)src, bytes);
+    launch_k(k_copy_bytes, fill_grid(bytes), 256, 0, s, (uint8_t *)d, (const uint8_t *)src, bytes);
     CK(cudaGetLastError());
 }
 
@@ -411,6 +438,7 @@ template <class Op, class Load, class Store>
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_1p_blocked(size_t n, Load ld, Store st, typename Op::T *agg,
                                                           typename Op::T *inc, uint32_t *flag, uint32_t *counter,
                                                           typename Op::T *d_total) {
+    pdl_enter();
     using T = typename Op::T;
     __shared__ T sm[SCAN_THREADS];
     __shared__ uint32_t tile_s;
@@ -504,6 +532,7 @@ template <class Op, class Load, class Store>
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_1p(size_t n, Load ld, Store st, typename Op::T *agg,
                                                           typename Op::T *inc, uint32_t *flag, uint32_t *counter,
                                                           typename Op::T *d_total) {
+    pdl_enter();
     using T = typename Op::T;
     constexpr int I = scan_items<T>();
     constexpr int TILE = SCAN_THREADS * I;
@@ -634,10 +663,10 @@ void scan(size_t n, Load ld, Store st, cudaStream_t s, typename Op::T *d_total =
                 opted = true;
             }
         }
-        k_scan_1p<Op, Load, Store><<<(unsigned)tiles, SCAN_THREADS, smem, s>>>(n, ld, st, agg, inc, flag,
+        launch_k(k_scan_1p<Op, Load, Store>, (unsigned)tiles, SCAN_THREADS, smem, s, n, ld, st, agg, inc, flag,
                                                                                flag + tiles, d_total);
     } else {
-        k_scan_1p_blocked<Op, Load, Store><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(n, ld, st, agg, inc, flag,
+        launch_k(k_scan_1p_blocked<Op, Load, Store>, (unsigned)tiles, SCAN_THREADS, 0, s, n, ld, st, agg, inc, flag,
                                                                                    flag + tiles, d_total);
     }
     CK_LAUNCH("k_scan_1p");
@@ -736,6 +765,7 @@ inline Mailbox &mailbox(cudaStream_t s) {
     return m;
 }
 static __global__ void k_mailbox(const uint8_t *__restrict__ src, uint32_t bytes, uint8_t *box, uint32_t tag) {
+    pdl_enter();
     for (uint32_t i = threadIdx.x; i < bytes; i += blockDim.x) box[64 + i] = src[i];
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -771,7 +801,7 @@ inline void read_back(void *dst, const void *d_src, size_t bytes, cudaStream_t s
     if (bytes <= MAILBOX_BYTES && mailbox_on() && t_arena && t_arena->mailbox) {
         Mailbox &m = mailbox(s);
         const uint32_t tag = ++m.seq ? m.seq : ++m.seq;
-        k_mailbox<<<1, 64, 0, s>>>(static_cast<const uint8_t *>(d_src), (uint32_t)bytes, m.host, tag);
+        launch_k(k_mailbox, 1, 64, 0, s, static_cast<const uint8_t *>(d_src), (uint32_t)bytes, m.host, tag);
         CK(cudaGetLastError());
         mailbox_wait(m, tag, s);
         memcpy(dst, m.host + 64, bytes);
@@ -794,6 +824,7 @@ struct MailboxPieces {
     uint32_t n;
 };
 static __global__ void k_mailbox_multi(MailboxPieces p, uint8_t *box, uint32_t tag) {
+    pdl_enter();
     uint32_t off = 0;
     for (uint32_t k = 0; k < p.n; ++k) {
         for (uint32_t i = threadIdx.x; i < p.bytes[k]; i += blockDim.x) box[64 + off + i] = p.src[k][i];
@@ -822,7 +853,7 @@ inline void read_back_multi(std::initializer_list<ReadPiece> pieces, cudaStream_
     for (const ReadPiece &q : pieces) mp.src[mp.n] = static_cast<const uint8_t *>(q.src), mp.bytes[mp.n++] = (uint32_t)q.bytes;
     Mailbox &m = mailbox(s);
     const uint32_t tag = ++m.seq ? m.seq : ++m.seq;
-    k_mailbox_multi<<<1, 64, 0, s>>>(mp, m.host, tag);
+    launch_k(k_mailbox_multi, 1, 64, 0, s, mp, m.host, tag);
     CK(cudaGetLastError());
     mailbox_wait(m, tag, s);
     size_t off = 0;
@@ -894,6 +925,7 @@ struct LiveBytes {
 template <int KW>
 __global__ void __launch_bounds__(RS_THREADS) k_radix_hist_all(KeyCols<KW> k, size_t n, LiveBytes<KW> live,
                                                                uint32_t *__restrict__ hist) {
+    pdl_enter();
     __shared__ uint32_t sh[KW * 8][256];
     for (int i = threadIdx.x; i < KW * 8 * 256; i += RS_THREADS) (&sh[0][0])[i] = 0;
     __syncthreads();
@@ -975,6 +1007,7 @@ __global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(KeyCols<KW> in, cons
                                                          KeyCols<KW> out, uint32_t *__restrict__ vout, size_t n,
                                                          int word, int shift, const uint32_t *__restrict__ hist,
                                                          uint32_t *status, uint32_t *tile_counter) {
+    pdl_enter();
     __shared__ uint32_t tile_s;
     __shared__ uint32_t wsum[2][OS_WARPS];
     __shared__ uint32_t wcnt[OS_WARPS][256];  // per-warp digit counts -> tile positions of each warp's run
@@ -1109,6 +1142,7 @@ template <int KW>
 __global__ void __launch_bounds__(ST_THREADS) k_sort_tile(KeyCols<KW> in, const uint32_t *__restrict__ vin,
                                                            KeyCols<KW> out, uint32_t *__restrict__ vout, uint32_t n,
                                                            LiveBytes<KW> live) {
+    pdl_enter();
     extern __shared__ __align__(16) uint8_t st_raw[];
     uint64_t *sk = reinterpret_cast<uint64_t *>(st_raw);                         // [KW][ST_TILE]
     uint32_t *sv = reinterpret_cast<uint32_t *>(st_raw + (size_t)KW * ST_TILE * 8);  // [ST_TILE]
@@ -1219,8 +1253,8 @@ void radix_sort(SortBufs<KW> &b, size_t n, LiveBytes<KW> live, cudaStream_t s) {
             CK(cudaFuncSetAttribute(k_sort_tile<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             opted = true;
         }
-        k_sort_tile<KW><<<1, ST_THREADS, smem, s>>>(b.k[b.cur], b.v[b.cur], b.k[b.cur ^ 1], b.v[b.cur ^ 1],
-                                                    (uint32_t)n, live);
+        launch_k(k_sort_tile<KW>, 1, ST_THREADS, smem, s, b.k[b.cur], (const uint32_t *)b.v[b.cur], b.k[b.cur ^ 1],
+                 b.v[b.cur ^ 1], (uint32_t)n, live);
         CK_LAUNCH("k_sort_tile");
         b.cur ^= 1;
         return;
@@ -1236,7 +1270,7 @@ void radix_sort(SortBufs<KW> &b, size_t n, LiveBytes<KW> live, cudaStream_t s) {
     struct {
         uint32_t *p;
     } hist{hist_p};
-    k_radix_hist_all<KW><<<grid_for(n, RS_THREADS * 4, 148 * 4), RS_THREADS, 0, s>>>(b.k[b.cur], n, live, hist.p);
+    launch_k(k_radix_hist_all<KW>, grid_for(n, RS_THREADS * 4, 148 * 4), RS_THREADS, 0, s, b.k[b.cur], n, live, hist.p);
     CK_LAUNCH("k_radix_hist_all");
     // sorts under ~1.2M records use 1024-record tiles: four times the CTAs, so a pass is not a few
     // long tiles on part of the GPU
@@ -1260,13 +1294,13 @@ void radix_sort(SortBufs<KW> &b, size_t n, LiveBytes<KW> live, cudaStream_t s) {
             if (!((live.m[w] >> byte) & 1)) continue;
             uint32_t *stp = status.p + stride * p++;
             if (small)
-                k_onesweep<KW, 4><<<ntiles, OS_THREADS, 0, s>>>(b.k[b.cur], b.v[b.cur], b.k[b.cur ^ 1], b.v[b.cur ^ 1],
-                                                                n, w, 8 * byte, hist.p + (size_t)(w * 8 + byte) * 256,
-                                                                stp, stp + (size_t)ntiles * 256);
+                launch_k(k_onesweep<KW, 4>, ntiles, OS_THREADS, 0, s, b.k[b.cur], (const uint32_t *)b.v[b.cur],
+                         b.k[b.cur ^ 1], b.v[b.cur ^ 1], n, w, 8 * byte,
+                         (const uint32_t *)(hist.p + (size_t)(w * 8 + byte) * 256), stp, stp + (size_t)ntiles * 256);
             else
-                k_onesweep<KW, OS_ITEMS><<<ntiles, OS_THREADS, 0, s>>>(
-                    b.k[b.cur], b.v[b.cur], b.k[b.cur ^ 1], b.v[b.cur ^ 1], n, w, 8 * byte,
-                    hist.p + (size_t)(w * 8 + byte) * 256, stp, stp + (size_t)ntiles * 256);
+                launch_k(k_onesweep<KW, OS_ITEMS>, ntiles, OS_THREADS, 0, s, b.k[b.cur], (const uint32_t *)b.v[b.cur],
+                         b.k[b.cur ^ 1], b.v[b.cur ^ 1], n, w, 8 * byte,
+                         (const uint32_t *)(hist.p + (size_t)(w * 8 + byte) * 256), stp, stp + (size_t)ntiles * 256);
             CK_LAUNCH("k_onesweep");
             b.cur ^= 1;
         }
@@ -1291,11 +1325,13 @@ inline uint8_t live_mask(uint64_t vary) {
 
 static __global__ void k_gather_kv(const uint32_t *__restrict__ P, size_t m, const uint64_t *__restrict__ k,
                             const uint32_t *__restrict__ v, uint64_t *__restrict__ ko, uint32_t *__restrict__ vo) {
+    pdl_enter();
     for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (size_t)gridDim.x * blockDim.x)
         ko[j] = k[P[j]], vo[j] = v[P[j]];
 }
 static __global__ void k_scatter_kv(const uint32_t *__restrict__ P, size_t m, const uint64_t *__restrict__ k,
                              const uint32_t *__restrict__ v, uint64_t *__restrict__ ko, uint32_t *__restrict__ vo) {
+    pdl_enter();
     for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (size_t)gridDim.x * blockDim.x)
         ko[P[j]] = k[j], vo[P[j]] = v[j];
 }
@@ -1319,6 +1355,7 @@ static __global__ void __launch_bounds__(FX_THREADS) k_seg_fixup(const uint64_t 
                                                                  uint64_t *__restrict__ kout,
                                                                  uint32_t *__restrict__ vout, size_t n, int shift,
                                                                  uint8_t *__restrict__ big, uint32_t *big_count) {
+    pdl_enter();
     __shared__ uint64_t sk[FX_WIN];
     __shared__ uint32_t hb[FX_HW];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1388,6 +1425,7 @@ static __global__ void __launch_bounds__(FX_THREADS) k_seg_fixup(const uint64_t 
 }
 static __global__ void k_compose_idx(const uint32_t *__restrict__ P, const uint32_t *__restrict__ S, size_t m,
                                      uint32_t *__restrict__ out) {
+    pdl_enter();
     for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (size_t)gridDim.x * blockDim.x)
         out[j] = P[S[j]];
 }
