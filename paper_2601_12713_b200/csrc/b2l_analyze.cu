@@ -190,6 +190,7 @@ constexpr int FR_BATCH = 4;  // items whose loads are issued together (memory-le
 
 __global__ void __launch_bounds__(FR_THREADS, 2) k_front_reduce(DevCols c, bool validate, bool raw, FrontAcc *partials,
                                                              unsigned long long *agg /*[0] max end, [1..5] OR, [6..10] AND*/) {
+    pdl_enter();
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const size_t wb = (size_t)blockIdx.x * FR_TILE + (size_t)warp * (32 * FR_ITEMS) + lane;
     const size_t last = c.n - 1;
@@ -291,6 +292,7 @@ struct FrontOut {
 // bad_mode: only the bad list (validation failed); else the five partition lists + srank.
 __global__ void __launch_bounds__(FR_THREADS, 2) k_front_apply(DevCols c, bool bad_mode, bool raw,
                                                             const FrontAcc *__restrict__ prefix, FrontOut out) {
+    pdl_enter();
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const size_t wb = (size_t)blockIdx.x * FR_TILE + (size_t)warp * (32 * FR_ITEMS) + lane;
     const size_t last = c.n - 1;
@@ -702,6 +704,7 @@ __global__ void k_rt_strict(DevCols c, const uint32_t *H, const uint32_t *hsorte
                             const uint32_t *hseg_start, uint32_t nhseg, uint32_t nH, const uint32_t *hid,
                             const uint64_t *segk, uint32_t nseg, const uint32_t *seg_rxbase, const uint32_t *rxpos,
                             const uint32_t *sval, uint32_t *qhead, uint32_t *match) {
+    pdl_enter();
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < nhseg; g += gridDim.x * blockDim.x) {
         const uint32_t b = hseg_start[g], e = (g + 1 < nhseg) ? hseg_start[g + 1] : nH;
         for (uint32_t q = b; q < e; ++q) {
@@ -1549,6 +1552,7 @@ __device__ __forceinline__ void atomic_add128(unsigned long long *lohi, U128 v) 
 // per-event category bits: DD 1, RT 2, RA 4, UA 8, UT 16 (estimator.py:77-113)
 __global__ void k_sums(DevCols c, const uint8_t *cat, unsigned long long *acc /*[6][2]*/, unsigned long long *nunion,
                        unsigned long long *minmax /*[2]: min start, max end*/) {
+    pdl_enter();
     U128 a[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) a[k] = U128{0, 0};
@@ -1618,6 +1622,7 @@ struct AttrAcc {
 };
 template <class Elem>
 __global__ void k_attr(DevCols c, size_t n_elem, Elem el, AttrAcc g) {
+    pdl_enter();
     extern __shared__ unsigned long long sm[];
     const uint32_t nb = c.nbuckets;
     const bool local = nb <= 512;
@@ -1745,7 +1750,7 @@ void sv_add(SvRun &R, int k, const FindingsDev &F, cudaStream_t st) {
     uint8_t *ct = R.cat.p;
     auto launch = [&](auto el, size_t ne) {
         if (!ne || !R.nb) return;
-        k_attr<<<grid_for(ne, TPB, 148 * 8), TPB, R.smem, st>>>(c, ne, el, R.acc_of(k));
+        launch_k(k_attr<decltype(el)>, grid_for(ne, TPB, 148 * 8), TPB, R.smem, st, c, ne, el, R.acc_of(k));
         CK_LAUNCH("k_attr");
     };
     if (k == 0) {  // DD: every member counts for attribution; all but the first of a group are eliminable
@@ -1804,7 +1809,7 @@ void sv_finish(SvRun &R, b2l_savings *o, cudaStream_t s, cudaStream_t copy) {
     R.acc.alloc(12 + 1 + 2, s);
     init_u64(R.acc.p, 13, 1, 1, s);  // min start := ~0 (max end stays 0)
     if (n) {
-        k_sums<<<grid_for(n, TPB, 148 * 4), TPB, 0, s>>>(c, R.cat.p, R.acc.p, R.acc.p + 12, R.acc.p + 13);
+        launch_k(k_sums, grid_for(n, TPB, 148 * 4), TPB, 0, s, c, (const uint8_t *)R.cat.p, R.acc.p, R.acc.p + 12, R.acc.p + 13);
         CK_LAUNCH("k_sums");
     }
     // overlap: exists i >= 1 with start[i] < max(end[0..i-1])  (estimator.py:51-58)
@@ -1978,13 +1983,13 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     DBuf<uint32_t> H(nl, s), TT(nl, s), AD(nl, s), A(nl, s), TK(nl, s);
     DBuf<uint32_t> srank(nl, s);
     if (n) {
-        k_front_reduce<<<ftiles, FR_THREADS, 0, s>>>(c, validate, raw, fpart.p, agg.p);
+        launch_k(k_front_reduce, ftiles, FR_THREADS, 0, s, c, validate, raw, fpart.p, agg.p);
         CK_LAUNCH("k_front_reduce");
-        k_scan_partials<FrontOp><<<1, SCAN_THREADS, 0, s>>>(fpart.p, ftiles, fpart.p + ftiles);
+        launch_k(k_scan_partials<FrontOp>, 1, SCAN_THREADS, 0, s, fpart.p, (size_t)ftiles, fpart.p + ftiles);
         CK_LAUNCH("k_scan_partials<FrontOp>");
         if (!only_validate) {  // lists of an invalid trace are never read
             FrontOut fo{{nullptr, H.p, TT.p, AD.p, A.p, TK.p}, srank.p};
-            k_front_apply<<<ftiles, FR_THREADS, 0, s>>>(c, false, raw, fpart.p, fo);
+            launch_k(k_front_apply, ftiles, FR_THREADS, 0, s, c, false, raw, (const FrontAcc *)fpart.p, fo);
             CK_LAUNCH("k_front_apply");
         }
         read_back_multi({{&ftot, fpart.p + ftiles, sizeof(FrontAcc)}, {hm, agg.p, sizeof(hm)}}, s);

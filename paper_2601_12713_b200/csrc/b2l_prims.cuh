@@ -384,6 +384,7 @@ __device__ __forceinline__ typename Op::T block_excl_scan(typename Op::T v, type
 template <class Op>
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_partials(typename Op::T *partials, size_t np,
                                                                  typename Op::T *d_total) {
+    pdl_enter();
     using T = typename Op::T;
     __shared__ T sm[SCAN_THREADS];
     T carry = Op::identity();
@@ -1468,7 +1469,7 @@ inline void seg_fixup(SortBufs<1> &b, size_t n, int shift, uint8_t live, cudaStr
     const uint32_t *vin = b.v[b.cur];
     uint64_t *kout = b.k[b.cur ^ 1].w[0];
     uint32_t *vout = b.v[b.cur ^ 1];
-    k_seg_fixup<<<(unsigned)((n + FX_TILE - 1) / FX_TILE), FX_THREADS, 0, s>>>(kin, vin, kout, vout, n, shift, big.p,
+    launch_k(k_seg_fixup, (unsigned)((n + FX_TILE - 1) / FX_TILE), FX_THREADS, 0, s, kin, vin, kout, vout, n, shift, big.p,
                                                                             cnt.p);
     CK_LAUNCH("k_seg_fixup");
     b.cur ^= 1;
@@ -1496,15 +1497,16 @@ inline void seg_fixup(SortBufs<1> &b, size_t n, int shift, uint8_t live, cudaStr
     {
         const uint32_t *S = sel.p;
         uint32_t *p2 = P2.p;
-        k_compose_idx<<<grid_for(m, 256), 256, 0, s>>>(P, S, m, p2);
+        launch_k(k_compose_idx, grid_for(m, 256), 256, 0, s, P, S, (size_t)m, p2);
         CK_LAUNCH("k_compose_idx");
     }
     SortBufs<1> sb;
     sb.k[0].w[0] = k2[0].p, sb.k[1].w[0] = k2[1].p, sb.v[0] = v2[0].p, sb.v[1] = v2[1].p, sb.cur = 0;
-    k_gather_kv<<<grid_for(m, 256), 256, 0, s>>>(P2.p, m, kin, vin, k2[0].p, v2[0].p);
+    launch_k(k_gather_kv, grid_for(m, 256), 256, 0, s, (const uint32_t *)P2.p, (size_t)m, kin, vin, k2[0].p, v2[0].p);
     CK_LAUNCH("k_gather_kv");
     radix_sort<1>(sb, m, LiveBytes<1>{{live}}, s);
-    k_scatter_kv<<<grid_for(m, 256), 256, 0, s>>>(P2.p, m, sb.k[sb.cur].w[0], sb.v[sb.cur], kout, vout);
+    launch_k(k_scatter_kv, grid_for(m, 256), 256, 0, s, (const uint32_t *)P2.p, (size_t)m, (const uint64_t *)sb.k[sb.cur].w[0],
+             (const uint32_t *)sb.v[sb.cur], kout, vout);
     CK_LAUNCH("k_scatter_kv");
 }
 
