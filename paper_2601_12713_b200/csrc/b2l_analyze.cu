@@ -516,7 +516,7 @@ struct Internal {
         b.alloc(n, s);
     }
     HostSlab *slab = nullptr;  // pinned host memory behind the b2l_findings arrays
-    HostSlab *slab_pairs = nullptr, *slab_kern = nullptr;  // ... of the pairs/RA and UT/UA chains
+    HostSlab *slab_pairs = nullptr, *slab_kern = nullptr, *slab_dd = nullptr;  // ... of the other chains
     // device copies of the trace columns (when they were uploaded from host) and their identity
     ColsUpload cols;
     const void *cols_key[3] = {nullptr, nullptr, nullptr};
@@ -546,6 +546,29 @@ struct HostSlab {
     size_t cap = 0;
     ~HostSlab() { slab_pool().release(p, cap); }
 };
+// Segments packed into one staging block (HostBatch::flush_async): segment k at off[k].
+struct PackSegs {
+    static constexpr int MAX = 16;
+    const uint8_t *src[MAX];
+    size_t off[MAX], bytes[MAX];
+    int n;
+};
+__global__ void k_pack_segs(PackSegs ps, uint8_t *__restrict__ dst) {
+    pdl_enter();
+    const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+    for (int k = 0; k < ps.n; ++k) {
+        const uint8_t *src = ps.src[k];
+        uint8_t *d = dst + ps.off[k];
+        const size_t b = ps.bytes[k];
+        if ((((uintptr_t)src | (uintptr_t)d) & 15) == 0) {
+            const size_t nv = b / 16;
+            for (size_t i = tid; i < nv; i += stride) reinterpret_cast<uint4 *>(d)[i] = reinterpret_cast<const uint4 *>(src)[i];
+            for (size_t i = nv * 16 + tid; i < b; i += stride) d[i] = src[i];
+        } else {
+            for (size_t i = tid; i < b; i += stride) d[i] = src[i];
+        }
+    }
+}
 struct HostBatch {
     struct Item {
         void **dst;
@@ -558,11 +581,32 @@ struct HostBatch {
         items.push_back(Item{(void **)dst, d, n * sizeof(T)});
     }
     // Queue the copies on `copy` once everything queued so far on `after` is done, into a fresh
-    // slab; no synchronisation (the caller synchronises `copy` before reading).
+    // slab; no synchronisation (the caller synchronises `copy` before reading).  Several arrays
+    // are first packed (one kernel on `after`) into a device staging block laid out like the
+    // slab, so the batch is ONE device->host copy instead of one per array (each costs the copy
+    // engine ~5 us).  The staging block comes from the call's arena (the caller synchronises
+    // `copy` before the arena is released).
     void flush_async(HostSlab &slab, cudaStream_t after, cudaStream_t copy) {
         size_t total = 0;
         for (auto &it : items) total += (it.bytes + 63) & ~size_t(63);
         slab.p = slab_pool().acquire(total, slab.cap);
+        uint8_t *stage = items.size() > 1 && items.size() <= PackSegs::MAX && t_arena
+                             ? static_cast<uint8_t *>(t_arena->take(total))
+                             : nullptr;
+        if (stage) {
+            PackSegs ps{};
+            size_t off = 0;
+            for (auto &it : items) {
+                ps.src[ps.n] = static_cast<const uint8_t *>(it.src), ps.off[ps.n] = off, ps.bytes[ps.n++] = it.bytes;
+                *it.dst = slab.p + off;
+                off += (it.bytes + 63) & ~size_t(63);
+            }
+            launch_k(k_pack_segs, grid_for(total / 16 + 1, 256, 148 * 4), 256, 0, after, ps, stage);
+            stream_after(copy, after);
+            to_host_async(slab.p, stage, total, copy);
+            items.clear();
+            return;
+        }
         stream_after(copy, after);
         size_t off = 0;
         for (auto &it : items) {
@@ -769,7 +813,8 @@ struct DdRt {
 cudaStream_t engine_stream_n(int k);
 void stream_after(cudaStream_t to, cudaStream_t from);
 
-DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, Internal &out, cudaStream_t s) {
+DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, Internal &out, cudaStream_t s,
+                b2l_findings *f = nullptr, cudaStream_t sc = nullptr) {
     DdRt r;
     const size_t R = 2ull * nH;
     if (nH == 0) {
@@ -877,6 +922,13 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
                 uint64_t nm = 0;
                 if (ng) read_back(&nm, total.p, sizeof(nm), s);
                 r.dd_members = nm;
+                if (f && sc) {  // the DD results go to the host while RT still runs
+                    HostBatch hb;
+                    hb.add(&f->dd_offsets, (const uint64_t *)out.dd_off.p, (size_t)ng + 1);
+                    hb.add(&f->dd_members, (const uint32_t *)out.dd_mem.p, (size_t)nm);
+                    out.slab_dd = new HostSlab();
+                    hb.flush_async(*out.slab_dd, s, sc);
+                }
             }
             if (dd_side) stream_wait(s);
         } catch (const EngineErr &e) {
@@ -2139,7 +2191,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
         if (ev) cudaEventDestroy(ev);
     };
     try {
-        DdRt dr = dd_rt_step(c, H.p, nH, (flags & B2L_ANALYZE_STRICT_RT) != 0, *in, s);
+        DdRt dr = dd_rt_step(c, H.p, nH, (flags & B2L_ANALYZE_STRICT_RT) != 0, *in, s, f, sc);
         in->dd_groups = dr.dd_groups, in->dd_members = dr.dd_members, in->rt_groups = dr.rt_groups,
         in->rt_trips = dr.rt_trips;
         if (with_sv) {
@@ -2160,8 +2212,10 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     // one synchronisation of the copy stream
     HostBatch hb;
     f->dd_groups = in->dd_groups;
-    hb.add(&f->dd_offsets, in->dd_off.p, in->dd_groups + 1);
-    hb.add(&f->dd_members, in->dd_mem.p, in->dd_members);
+    if (!in->slab_dd) {  // (no hashed transfers: the DD chain queued nothing)
+        hb.add(&f->dd_offsets, in->dd_off.p, in->dd_groups + 1);
+        hb.add(&f->dd_members, in->dd_mem.p, in->dd_members);
+    }
     f->rt_groups = in->rt_groups;
     hb.add(&f->rt_offsets, in->rt_off.p, in->rt_groups + 1);
     hb.add(&f->rt_tx, in->rt_tx.p, in->rt_trips);
@@ -2211,6 +2265,7 @@ void findings_free(b2l_findings *f) {
         delete in->slab;
         delete in->slab_pairs;
         delete in->slab_kern;
+        delete in->slab_dd;
     }
     delete in;
     free(f);
