@@ -1094,6 +1094,26 @@ struct DepthStore {  // level (>= 1) of allocs and matched deletes, 0 for unmatc
     }
 };
 
+// Unmatched deletes (level 0) flagged by AD rank, and the largest level (block max, one atomic per
+// block) so the (segment, level) sort key can be packed to its exact width.
+__global__ void k_pair_unmatched(size_t n, const uint32_t *sv, const uint32_t *AD, const uint8_t *kind,
+                                 const uint32_t *lv, uint8_t *um, unsigned *maxlv) {
+    pdl_enter();
+    __shared__ unsigned bm;
+    if (threadIdx.x == 0) bm = 0;
+    __syncthreads();
+    unsigned m = 0;
+    for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t l = lv[p];
+        m = l > m ? l : m;
+        if (l == 0 && kind[AD[sv[p]]] == B2L_KIND_DELETE) um[sv[p]] = 1;
+    }
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(&bm, m);
+    __syncthreads();
+    if (threadIdx.x == 0 && bm) atomicMax(maxlv, bm);
+}
+
 PairOut pairs_step(const DevCols &c, const uint32_t *AD, uint32_t nAD, const uint32_t *A, uint32_t nA,
                    uint64_t synth_end, Internal &out, cudaStream_t s) {
     PairOut po;
@@ -1126,19 +1146,18 @@ PairOut pairs_step(const DevCols &c, const uint32_t *AD, uint32_t nAD, const uin
     radix_sort<2>(st.b, nAD, LiveBytes<2>{{g_masks.dev, g_masks.da}}, s);
     KeyCols<2> sk = st.b.k[st.b.cur];
     const uint32_t *sv = st.val();
-    DBuf<uint32_t> level(nAD, s), seg(nAD, s);
+    DBuf<uint32_t> level(nAD, s), seg(nAD, s), nseg_d(1, s), maxlv;
+    maxlv.alloc_zeroed(1, s);
     scan<Seg<MaxPlus>>(nAD, DepthLoad{sk, sv, AD, c.kind}, DepthStore{sv, AD, c.kind, level.p}, s);
-    scan<SumU32>(nAD, HeadLoad<2>{sk}, StoreInclMinus1{seg.p}, s);
+    scan<SumU32>(nAD, HeadLoad<2>{sk}, StoreInclMinus1{seg.p}, s, nseg_d.p);
     // unmatched deletes -> warnings in trace order (flag by AD rank, compact in AD order)
     {
         DBuf<uint8_t> unmatched;
         unmatched.alloc_zeroed(nAD, s);
         uint8_t *um = unmatched.p;
-        const uint32_t *lv = level.p;
-        const uint8_t *kind = c.kind;
-        for_each(nAD, [=] __device__(size_t p) {
-            if (kind[AD[sv[p]]] == B2L_KIND_DELETE && lv[p] == 0) um[sv[p]] = 1;
-        }, s);
+        launch_k(k_pair_unmatched, grid_for(nAD, TPB, 148 * 8), TPB, 0, s, (size_t)nAD, sv, AD, c.kind,
+                 (const uint32_t *)level.p, um, maxlv.p);
+        CK_LAUNCH("k_pair_unmatched");
         // compacted straight to event indices; the count is read at the end of the chain
         po.wcount.alloc(1, s);
         scan<SumU32>(nAD, FlagLoad<UmPred>{UmPred{um}}, MapCompactStore<UmPred>{UmPred{um}, AD, po.warn.p}, s,
@@ -1151,27 +1170,26 @@ PairOut pairs_step(const DevCols &c, const uint32_t *AD, uint32_t nAD, const uin
         const uint32_t *lv = level.p;
         compact(nAD, [=] __device__(size_t p) { return lv[p] != 0; }, lp.p, lc.p, s);
     }
-    // sorted over nAD slots without reading the count back: slots past it get the sentinel key
-    // (segment nAD, level 0), which sorts after every real record
-    const uint32_t nl = nAD;
+    // one read-back sizes the sort exactly: the record count, and a key (segment << lb) | level
+    // packed to the bits the segments and levels really use (typically 3 digit passes, not 6)
+    uint32_t h[3];
+    read_back_multi({{&h[0], lc.p, 4}, {&h[1], nseg_d.p, 4}, {&h[2], maxlv.p, 4}}, s);
+    const uint32_t nl = h[0], nseg = h[1], maxl = h[2];
+    if (nl == 0) return po;
+    int lb = 0;
+    while (lb < 32 && (uint64_t(1) << lb) <= maxl) ++lb;
     SortStore<1> ls(nl, s);
     {
         uint64_t *k0 = ls.in_key(0);
         uint32_t *v = ls.in_val();
-        const uint32_t *lpp = lp.p, *lv = level.p, *sg = seg.p, *cnt = lc.p;
-        const uint64_t sentinel = (uint64_t)nAD << 32;
+        const uint32_t *lpp = lp.p, *lv = level.p, *sg = seg.p;
         for_each(nl, [=] __device__(size_t q) {
-            if (q >= *cnt) {
-                k0[q] = sentinel;
-                v[q] = NONE;
-                return;
-            }
             const uint32_t p = lpp[q];
-            k0[q] = ((uint64_t)sg[p] << 32) | lv[p];
+            k0[q] = ((uint64_t)sg[p] << lb) | lv[p];
             v[q] = p;
         }, s);
     }
-    radix_sort<1>(ls.b, nl, LiveBytes<1>{{(uint8_t)(live_range(nAD + 1) | (live_range(nAD + 1) << 4))}}, s);
+    radix_sort<1>(ls.b, nl, LiveBytes<1>{{live_range((((uint64_t)(nseg ? nseg - 1 : 0)) << lb | maxl) + 1)}}, s);
     {
         const uint64_t *lk = ls.key(0);
         const uint32_t *lvv = ls.val();
@@ -1180,10 +1198,9 @@ PairOut pairs_step(const DevCols &c, const uint32_t *AD, uint32_t nAD, const uin
         uint32_t *pd = out.pair_delete.p;
         const uint32_t nll = nl;
         for_each(nl, [=] __device__(size_t q) {
-            if (lvv[q] == NONE) return;
             const uint32_t e = AD[sv[lvv[q]]];
             if (kind[e] != B2L_KIND_ALLOC) return;
-            if (q + 1 < nll && lk[q + 1] == lk[q] && lvv[q + 1] != NONE) {
+            if (q + 1 < nll && lk[q + 1] == lk[q]) {
                 const uint32_t e2 = AD[sv[lvv[q + 1]]];
                 if (kind[e2] == B2L_KIND_DELETE) pd[ar[e]] = e2;
             }
@@ -2091,14 +2108,16 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     in->n_pairs = nA;
     // ---- 3-6.  Three independent chains: hash-keyed (DD, RT), pairs -> RA, and the kernel index
     // -> UT (-> UA once the pairs exist).  Small traces run them on three streams from three host
-    // threads (each keeps its own syncs and staging); large traces are bandwidth bound and run
-    // them back to back on one stream.
+    // threads (each keeps its own syncs and staging); traces past 16M events run them back to back
+    // on one stream (measured r02: three streams win 7-8 % at 10M, tie at 30M, lose 9 % at 100M
+    // where the chains' working sets evict each other from L2).
     int dev = 0;
     CK(cudaGetDevice(&dev));
     const Masks masks = g_masks;
     PairOut po;
     static const uint64_t overlap_min = getenv("B2L_OVERLAP_MIN") ? strtoull(getenv("B2L_OVERLAP_MIN"), nullptr, 10) : 0;
-    const bool overlap = n <= (size_t(4) << 20) && n >= overlap_min;
+    static const uint64_t overlap_max = getenv("B2L_OVERLAP_MAX") ? strtoull(getenv("B2L_OVERLAP_MAX"), nullptr, 10) : (size_t(16) << 20);
+    const bool overlap = n <= overlap_max && n >= overlap_min;
     cudaStream_t s2 = overlap ? engine_stream_n(1) : s, s3 = overlap ? engine_stream_n(2) : s;
     cudaStream_t sc = engine_stream_n(4);  // device -> host result copies, chain by chain
     if (overlap) {  // the partition lists and start ranks are produced on s
