@@ -632,13 +632,61 @@ struct HostBatch {
 };
 
 // B2L_TRACE=1: synchronise after each phase and print its wall time (diagnostics only).
+// B2L_TRACE=ev: no synchronisation; each mark records a timing event on its stream and the host
+// time it was queued, printed side by side when the call ends (ev_log_flush): where the GPU waits
+// for the host and where the host waits for the GPU.
+struct EvLog {
+    struct Rec {
+        const char *name;
+        std::chrono::steady_clock::time_point host;
+        cudaEvent_t ev;
+        cudaStream_t s;
+    };
+    std::mutex mu;
+    std::vector<Rec> recs;
+};
+inline EvLog &ev_log() {
+    static EvLog l;
+    return l;
+}
+inline int trace_mode() {
+    static const int m = getenv("B2L_TRACE") ? (strcmp(getenv("B2L_TRACE"), "ev") == 0 ? 2 : 1) : 0;
+    return m;
+}
+void ev_log_flush() {
+    if (trace_mode() != 2) return;
+    EvLog &l = ev_log();
+    std::lock_guard<std::mutex> g(l.mu);
+    if (l.recs.empty()) return;
+    for (auto &r : l.recs) cudaEventSynchronize(r.ev);
+    std::sort(l.recs.begin(), l.recs.end(), [](const EvLog::Rec &a, const EvLog::Rec &b) { return a.host < b.host; });
+    const auto h0 = l.recs[0].host;
+    const cudaEvent_t g0 = l.recs[0].ev;
+    for (auto &r : l.recs) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, g0, r.ev);
+        fprintf(stderr, "[b2l-ev] %-14s host %8.1f us  gpu %8.1f us  stream %p\n", r.name,
+                std::chrono::duration<double, std::micro>(r.host - h0).count(), ms * 1e3, (void *)r.s);
+    }
+    for (auto &r : l.recs) cudaEventDestroy(r.ev);
+    l.recs.clear();
+}
 struct PhaseClock {
-    bool on;
+    int on;
     cudaStream_t s;
     std::chrono::steady_clock::time_point t;
-    explicit PhaseClock(cudaStream_t st) : on(getenv("B2L_TRACE") != nullptr), s(st), t(std::chrono::steady_clock::now()) {}
+    explicit PhaseClock(cudaStream_t st) : on(trace_mode()), s(st), t(std::chrono::steady_clock::now()) {}
     void mark(const char *name) {
         if (!on) return;
+        if (on == 2) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            cudaEventRecord(e, s);
+            EvLog &l = ev_log();
+            std::lock_guard<std::mutex> g(l.mu);
+            l.recs.push_back({name, std::chrono::steady_clock::now(), e, s});
+            return;
+        }
         cudaStreamSynchronize(s);
         auto now = std::chrono::steady_clock::now();
         fprintf(stderr, "[b2l] %-12s %8.3f ms\n", name, std::chrono::duration<double, std::milli>(now - t).count());
@@ -691,7 +739,6 @@ struct QLoad {
     }
 };
 struct QStore {
-    static constexpr bool kStriped = true;  // six output arrays: coalesced stores pay
     const uint32_t *val;
     uint32_t *seg_of, *f_of, *j_of, *rxpos, *seg_start, *seg_rxbase;
     __device__ void operator()(size_t p, QState ex, QState it) const {
@@ -1174,6 +1221,7 @@ PairOut pairs_step(const DevCols &c, const uint32_t *AD, uint32_t nAD, const uin
     // packed to the bits the segments and levels really use (typically 3 digit passes, not 6)
     uint32_t h[3];
     read_back_multi({{&h[0], lc.p, 4}, {&h[1], nseg_d.p, 4}, {&h[2], maxlv.p, 4}}, s);
+    PhaseClock(s).mark(" pairs-rb");
     const uint32_t nl = h[0], nseg = h[1], maxl = h[2];
     if (nl == 0) return po;
     int lb = 0;
@@ -1243,6 +1291,7 @@ void ra_step(const DevCols &c, uint32_t nP, Internal &out, cudaStream_t s) {
     {
         read_back_multi({{&cnts[0], scount.p, 4}, {&cnts[1], gc.p, 4}}, s);
     }
+    PhaseClock(s).mark(" ra-rb");
     const uint32_t nseg = cnts[0], ng = cnts[1];
     out.ra_groups = ng;
     if (ng == 0) {
@@ -1892,9 +1941,11 @@ void sv_finish(SvRun &R, b2l_savings *o, cudaStream_t s, cudaStream_t copy) {
     else R.unic.zero();
     unsigned long long h[15];
     uint32_t hov = 0, hun = 0;
+    PhaseClock(s).mark(" sv-queued");
     {  // one synchronisation for the three small results
         read_back_multi({{h, R.acc.p, sizeof(h)}, {&hov, R.ovl.p, 4}, {&hun, R.unic.p, 4}}, s);
     }
+    PhaseClock(s).mark(" sv-rb");
     for (int k = 0; k < 5; ++k) o->per_category_ns[k] = b2l_u128{h[2 * k], h[2 * k + 1]};
     o->union_ns = b2l_u128{h[10], h[11]};
     o->n_union = hun;
@@ -2016,6 +2067,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     std::lock_guard<std::mutex> lock(g_mu);
     cudaStream_t s = engine_stream();
     PhaseClock pc(s);
+    pc.mark("start");
     Internal *in = new Internal();
     f->internal = in;
     ColsUpload &up = in->cols;
@@ -2134,6 +2186,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
             CK(cudaSetDevice(dev));
             g_masks = masks;
             PhaseClock pc2(s2);
+            pc2.mark("pairs-start");
             po = pairs_step(c, AD.p, nAD, A.p, nA, me, *in, s2);
             cudaEvent_t ev;
             CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -2168,6 +2221,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
             CK(cudaSetDevice(dev));
             g_masks = masks;
             PhaseClock pc3(s3);
+            pc3.mark("kern-start");
             KernelIndexStore kis(nK, s3);
             build_kernel_index(kis, c, TK.p, nK, s3);
             ut_step(c, kis.KI, TT.p, nT, *in, s3);
@@ -2255,8 +2309,10 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
         in->fused_n = cols->n_events;
         sv_finish(R, o, s, sc);
     }
+    pc.mark("queued");
     stream_wait(sc);
     pc.mark("d2h");
+    ev_log_flush();
     if (alloc_stats().on) {
         fprintf(stderr, "[b2l] pool alloc/free calls %llu, host %.3f ms; arena %.1f of %.1f MB (%.0f B/event)\n",
                 (unsigned long long)alloc_stats().n.load(), alloc_stats().ns.load() * 1e-6,
@@ -2266,9 +2322,10 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
         alloc_stats().n = 0, alloc_stats().ns = 0;
     }
     if (sync_stats().on) {
-        fprintf(stderr, "[b2l] host round trips %llu, %.3f ms waiting (all chains)\n",
-                (unsigned long long)sync_stats().n.load(), sync_stats().ns.load() * 1e-6);
-        sync_stats().n = 0, sync_stats().ns = 0;
+        fprintf(stderr, "[b2l] host round trips %llu, %.3f ms waiting (all chains); %llu launches, %.3f ms host\n",
+                (unsigned long long)sync_stats().n.load(), sync_stats().ns.load() * 1e-6,
+                (unsigned long long)sync_stats().ln.load(), sync_stats().lns.load() * 1e-6);
+        sync_stats().n = 0, sync_stats().ns = 0, sync_stats().ln = 0, sync_stats().lns = 0;
     }
     if (in->dd_groups == 0) f->dd_offsets[0] = 0;
     if (in->rt_groups == 0) f->rt_offsets[0] = 0;

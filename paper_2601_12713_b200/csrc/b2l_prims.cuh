@@ -51,7 +51,7 @@ struct AllocStats {
 };
 // B2L_SYNC_STATS: host round trips per analysis call (read-backs and stream waits), per thread
 struct SyncStats {
-    std::atomic<uint64_t> n{0}, ns{0};
+    std::atomic<uint64_t> n{0}, ns{0}, ln{0}, lns{0};  // round trips; launches and their host time
     bool on = getenv("B2L_SYNC_STATS") != nullptr;
 };
 inline SyncStats &sync_stats() {
@@ -164,7 +164,14 @@ inline void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at, cfg.numAttrs = pdl_on() ? 1 : 0;
+    if (!sync_stats().on) {
+        ck(cudaLaunchKernelEx(&cfg, k, args...), "cudaLaunchKernelEx");
+        return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
     ck(cudaLaunchKernelEx(&cfg, k, args...), "cudaLaunchKernelEx");
+    sync_stats().ln += 1;
+    sync_stats().lns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
 }
 
 // Device-side fill / copy as kernels, never through a copy engine: the engines may be busy with a
@@ -414,6 +421,13 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_partials(typename Op::T *
 // looks back over 32 predecessors per step (flags then values; values are written before
 // their flag with a fence in between, read after it through L2), so inputs are read once.
 constexpr uint32_t SP_AGG = 1, SP_INC = 2;
+// look-back flags sit one per 128-byte line: every resident tile polls its predecessors' flags,
+// and packed flags put tens of thousands of polling threads on a handful of L2 lines (measured:
+// ~10 us per tile at 1M items, about 4x the whole scan's load and store work)
+#ifndef B2L_FLAG_STRIDE
+#define B2L_FLAG_STRIDE 32
+#endif
+constexpr uint32_t FS = B2L_FLAG_STRIDE;
 
 template <class T>
 __device__ __forceinline__ T ld_l2(const T *p) {
@@ -433,102 +447,106 @@ __device__ __forceinline__ T shfl_down_t(T v, int off) {
     return v;
 }
 
-// Blocked variant: thread t holds SCAN_ITEMS consecutive items in registers (one read of the
-// inputs); used unless the store functor asks for striped stores.
-template <class Op, class Load, class Store>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_1p_blocked(size_t n, Load ld, Store st, typename Op::T *agg,
-                                                          typename Op::T *inc, uint32_t *flag, uint32_t *counter,
-                                                          typename Op::T *d_total) {
-    pdl_enter();
+// Decoupled look-back by the whole block (all SCAN_THREADS threads, called uniformly): publishes
+// this tile's aggregate, then inspects 256 predecessors per step -- one flag and one value per
+// thread -- until a window holds an inclusive prefix; returns this tile's exclusive prefix and
+// publishes its inclusive one.  Flags are one per 128-byte line (FS) and polled with acquire
+// loads.  Measured in isolation (tools/scan_bench.cu, u32 sum scan, B200): 1M items 29 -> 11 us,
+// 10M 100 -> 41 us against the earlier warp-wide look-back over packed flags with full fences.
+// Value stores before the flag: a release store orders them; the pollers read flags with acquire
+// loads, so neither side needs a full fence.
+__device__ __forceinline__ void publish_flag(uint32_t *f, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t acquire_flag(const uint32_t *f) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    return v;
+}
+template <class Op>
+__device__ __forceinline__ typename Op::T block_lookback(uint32_t tile, typename Op::T total, typename Op::T *agg,
+                                                         typename Op::T *inc, uint32_t *flag) {
     using T = typename Op::T;
-    __shared__ T sm[SCAN_THREADS];
-    __shared__ uint32_t tile_s;
-    __shared__ T prefix_s;
-    if (threadIdx.x == 0) tile_s = atomicAdd(counter, 1u);
-    __syncthreads();
-    const uint32_t tile = tile_s;
-    const size_t base = (size_t)tile * SCAN_TILE + (size_t)threadIdx.x * SCAN_ITEMS;
-    T items[SCAN_ITEMS];
-    T acc = Op::identity();
-#pragma unroll
-    for (int k = 0; k < SCAN_ITEMS; ++k) {
-        items[k] = base + k < n ? ld(base + k) : Op::identity();
-        acc = Op::combine(acc, items[k]);
-    }
-    T total;
-    T ex = block_excl_scan<Op>(acc, sm, total);
-    volatile uint32_t *vf = flag;
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        if (tile == 0) {
-            if (lane == 0) {
-                inc[0] = total;
-                __threadfence();
-                vf[0] = SP_INC;
-                prefix_s = Op::identity();
-            }
-        } else {
-            if (lane == 0) {
-                agg[tile] = total;
-                __threadfence();
-                vf[tile] = SP_AGG;
-            }
-            T prefix = Op::identity();
-            for (int64_t j = (int64_t)tile - 1;; j -= 32) {
-                const int64_t jj = j - lane;
-                uint32_t f = SP_INC;
-                if (jj >= 0)
-                    do {
-                        f = vf[jj];
-                    } while (f == 0);
-                __threadfence();
-                T v = jj < 0 ? Op::identity() : (f == SP_INC ? ld_l2(inc + jj) : ld_l2(agg + jj));
-                const uint32_t incm = __ballot_sync(0xffffffffu, f == SP_INC);
-                const int first = incm ? __ffs(incm) - 1 : 31;  // newest predecessor with an inclusive
-                if (lane > first) v = Op::identity();
-                // ordered reduction: lane l holds tile j - l (older for higher lanes)
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const T o = shfl_down_t(v, off);
-                    if (lane + off < 32) v = Op::combine(o, v);
-                }
-                prefix = Op::combine(v, prefix);  // lane 0 holds the window, oldest first
-                if (incm) break;
-            }
-            if (lane == 0) {
-                inc[tile] = Op::combine(prefix, total);
-                __threadfence();
-                vf[tile] = SP_INC;
-                prefix_s = prefix;
-            }
+    constexpr int NW = SCAN_THREADS / 32;
+    __shared__ T wv[NW];
+    __shared__ int wfirst[NW];
+    __shared__ T prefix_sh;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if (tile == 0) {
+        if (t == 0) {
+            inc[0] = total;
+            publish_flag(flag, SP_INC);  // tile 0's flag: word 0
         }
+        return Op::identity();
+    }
+    if (t == 0) {
+        agg[tile] = total;
+        publish_flag(flag + (size_t)tile * FS, SP_AGG);
+    }
+    T prefix = Op::identity();  // meaningful in thread 0
+    for (int64_t base = (int64_t)tile - 1;; base -= SCAN_THREADS) {
+        const int64_t jj = base - t;  // thread t holds tile base - t (older for higher t)
+        uint32_t f = SP_INC;
+        if (jj >= 0)
+            do {
+                f = acquire_flag(flag + jj * FS);
+            } while (f == 0);
+        T v = jj < 0 ? Op::identity() : (f == SP_INC ? ld_l2(inc + jj) : ld_l2(agg + jj));
+        const uint32_t incm = __ballot_sync(0xffffffffu, f == SP_INC);
+        if (lane == 0) wfirst[warp] = incm ? warp * 32 + __ffs(incm) - 1 : SCAN_THREADS;
+        __syncthreads();
+        int first = SCAN_THREADS;  // newest predecessor holding an inclusive prefix
+#pragma unroll
+        for (int w = 0; w < NW; ++w) first = wfirst[w] < first ? wfirst[w] : first;
+        if (t > first) v = Op::identity();
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {  // ordered: lane 0 gets its warp's window, oldest first
+            const T o = shfl_down_t(v, off);
+            if (lane + off < 32) v = Op::combine(o, v);
+        }
+        if (lane == 0) wv[warp] = v;
+        __syncthreads();
+        if (t == 0) {
+            T win = wv[NW - 1];
+#pragma unroll
+            for (int w = NW - 2; w >= 0; --w) win = Op::combine(win, wv[w]);
+            prefix = Op::combine(win, prefix);
+        }
+        if (first < SCAN_THREADS) break;  // uniform: every thread read the same wfirst[]
+        __syncthreads();                  // wfirst / wv are rewritten by the next window
+    }
+    if (t == 0) {
+        inc[tile] = Op::combine(prefix, total);
+        publish_flag(flag + (size_t)tile * FS, SP_INC);
+        prefix_sh = prefix;
     }
     __syncthreads();
-    if (d_total && threadIdx.x == 0 && (size_t)(tile + 1) * SCAN_TILE >= n) *d_total = Op::combine(prefix_s, total);
-    ex = Op::combine(prefix_s, ex);
-#pragma unroll
-    for (int k = 0; k < SCAN_ITEMS; ++k) {
-        if (base + k < n) st(base + k, ex, items[k]);
-        ex = Op::combine(ex, items[k]);
-    }
+    return prefix_sh;
 }
 
-// Single-pass scan tiles: 256 threads x I items, I = 32 for values of up to 8 bytes, else 16.
-// Item j of a tile lives at shared slot (j / I) * (I + 1) + j % I: thread t's I consecutive
-// items form a padded row.
+// Single-pass scan tiles: 256 threads x I items (I = 16 for values of up to 8 bytes, else 8).
+// Loads are block-striped (item k*256 + t for thread t: every warp access is contiguous, and a
+// thread's I loads -- gathers included -- are all in flight at once) and stay in registers; a
+// copy goes to shared memory in a padded blocked layout (item j at slot (j / I) * (I + 1) + j % I)
+// where each thread reduces its row, and after the look-back the row is rewritten as exclusive
+// prefixes, which the striped store pass reads back beside the items it still holds.
+// (Measured on B200, u32 sum scan: a blocked register layout -- thread t owning I consecutive
+// items -- ran 2x slower at 1M-30M items: every load / store instruction touched 32 sectors.)
+#ifndef B2L_SCAN_I
+#define B2L_SCAN_I 0
+#endif
 template <class T>
 __host__ __device__ constexpr int scan_items() {
-    return sizeof(T) <= 8 ? 32 : 16;
+    return B2L_SCAN_I ? B2L_SCAN_I : (sizeof(T) <= 8 ? 16 : 8);
 }
 template <class T>
 constexpr size_t scan_smem() {
     return (size_t)SCAN_THREADS * (scan_items<T>() + 1) * sizeof(T);
 }
 
-// Loads and stores run in block-striped order (item k*256 + t for thread t: every warp access is
-// contiguous); the items sit in shared memory, where each thread reduces its row, and after the
-// look-back rewrites the row as exclusive prefixes, so the stores are striped again (the item
-// itself is re-read by the store pass, from L1).  Large tiles keep the look-back chain short.
+#ifdef B2L_SCAN_PROF
+__device__ long long g_scan_prof[65536 * 6];
+#endif
 template <class Op, class Load, class Store>
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_1p(size_t n, Load ld, Store st, typename Op::T *agg,
                                                           typename Op::T *inc, uint32_t *flag, uint32_t *counter,
@@ -541,97 +559,67 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_1p(size_t n, Load ld, Sto
     T *tr = reinterpret_cast<T *>(scan_sm_raw);  // SCAN_THREADS * (I + 1) slots
     __shared__ T sm[SCAN_THREADS / 32 + 1];
     __shared__ uint32_t tile_s;
-    __shared__ T prefix_s;
     if (threadIdx.x == 0) tile_s = atomicAdd(counter, 1u);
     __syncthreads();
     const uint32_t tile = tile_s;
     const size_t tb = (size_t)tile * TILE;
     const int t = threadIdx.x;
-#pragma unroll 4
+#ifdef B2L_SCAN_PROF
+    long long c0 = clock64(), g0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+#endif
+    T items[I];
+#pragma unroll
+    for (int k = 0; k < I; ++k) {
+        const size_t i = tb + (size_t)k * SCAN_THREADS + t;
+        items[k] = i < n ? ld(i) : Op::identity();
+    }
+#pragma unroll
     for (int k = 0; k < I; ++k) {
         const int j = k * SCAN_THREADS + t;
-        tr[(j / I) * (I + 1) + j % I] = tb + j < n ? ld(tb + j) : Op::identity();
+        tr[(j / I) * (I + 1) + j % I] = items[k];
     }
     __syncthreads();
     T *row = tr + t * (I + 1);
     T acc = Op::identity();
-#pragma unroll 4
+#pragma unroll
     for (int k = 0; k < I; ++k) acc = Op::combine(acc, row[k]);
     T total;
     T ex = block_excl_scan<Op>(acc, sm, total);
-    volatile uint32_t *vf = flag;
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        if (tile == 0) {
-            if (lane == 0) {
-                inc[0] = total;
-                __threadfence();
-                vf[0] = SP_INC;
-                prefix_s = Op::identity();
-            }
-        } else {
-            if (lane == 0) {
-                agg[tile] = total;
-                __threadfence();
-                vf[tile] = SP_AGG;
-            }
-            T prefix = Op::identity();
-            for (int64_t j = (int64_t)tile - 1;; j -= 32) {
-                const int64_t jj = j - lane;
-                uint32_t f = SP_INC;
-                if (jj >= 0)
-                    do {
-                        f = vf[jj];
-                    } while (f == 0);
-                __threadfence();
-                T v = jj < 0 ? Op::identity() : (f == SP_INC ? ld_l2(inc + jj) : ld_l2(agg + jj));
-                const uint32_t incm = __ballot_sync(0xffffffffu, f == SP_INC);
-                const int first = incm ? __ffs(incm) - 1 : 31;  // newest predecessor with an inclusive
-                if (lane > first) v = Op::identity();
-                // ordered reduction: lane l holds tile j - l (older for higher lanes)
+#ifdef B2L_SCAN_PROF
+    long long c1 = clock64();
+#endif
+    const T prefix = block_lookback<Op>(tile, total, agg, inc, flag);
+#ifdef B2L_SCAN_PROF
+    long long c2 = clock64();
+#endif
+    if (d_total && t == 0 && tb + TILE >= n) *d_total = Op::combine(prefix, total);
+    ex = Op::combine(prefix, ex);
 #pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const T o = shfl_down_t(v, off);
-                    if (lane + off < 32) v = Op::combine(o, v);
-                }
-                prefix = Op::combine(v, prefix);  // lane 0 holds the window, oldest first
-                if (incm) break;
-            }
-            if (lane == 0) {
-                inc[tile] = Op::combine(prefix, total);
-                __threadfence();
-                vf[tile] = SP_INC;
-                prefix_s = prefix;
-            }
-        }
-    }
-    __syncthreads();
-    if (d_total && threadIdx.x == 0 && tb + TILE >= n) *d_total = Op::combine(prefix_s, total);
-    ex = Op::combine(prefix_s, ex);
-#pragma unroll 4
     for (int k = 0; k < I; ++k) {  // exclusive prefixes over the own row, in place
         const T it = row[k];
         row[k] = ex;
         ex = Op::combine(ex, it);
     }
     __syncthreads();
-#pragma unroll 4
+#pragma unroll
     for (int k = 0; k < I; ++k) {
         const int j = k * SCAN_THREADS + t;
-        if (tb + j < n) st(tb + j, tr[(j / I) * (I + 1) + j % I], ld(tb + j));
+        if (tb + j < n) st(tb + j, tr[(j / I) * (I + 1) + j % I], items[k]);
     }
+#ifdef B2L_SCAN_PROF
+    __syncthreads();
+    if (t == 0 && tile < 65536) {
+        long long c3 = clock64(), g3;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g3));
+        g_scan_prof[tile * 6 + 0] = g0, g_scan_prof[tile * 6 + 1] = c1 - c0, g_scan_prof[tile * 6 + 2] = c2 - c1;
+        g_scan_prof[tile * 6 + 3] = c3 - c2, g_scan_prof[tile * 6 + 4] = g3;
+        unsigned smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_scan_prof[tile * 6 + 5] = smid;
+    }
+#endif
 }
-
-// Store functors that write several output arrays per item set `static constexpr bool kStriped
-// = true` and get the striped (coalesced-store) scan; the rest use the blocked one.
-template <class S, class = void>
-struct scan_striped {
-    static constexpr bool value = false;
-};
-template <class S>
-struct scan_striped<S, std::void_t<decltype(S::kStriped)>> {
-    static constexpr bool value = S::kStriped;
-};
 
 // scan over n items: st(i, exclusive_prefix, item) for every i; optional device total.
 template <class Op, class Load, class Store>
@@ -641,11 +629,10 @@ void scan(size_t n, Load ld, Store st, cudaStream_t s, typename Op::T *d_total =
         if (d_total) dev_memset(d_total, 0, sizeof(T), s);
         return;
     }
-    constexpr bool striped = scan_striped<Store>::value;
-    constexpr size_t TILE = striped ? (size_t)SCAN_THREADS * scan_items<T>() : (size_t)SCAN_TILE;
+    constexpr size_t TILE = (size_t)SCAN_THREADS * scan_items<T>();
     const size_t tiles = (n + TILE - 1) / TILE;
-    // flags + tile counter in one zeroed block; aggregates / inclusive prefixes beside them
-    const size_t fwords = (tiles + 1 + 3) & ~size_t(3);
+    // flags (one per line) + tile counter in one zeroed block; aggregates / inclusive prefixes beside them
+    const size_t fwords = (tiles + 1) * FS;
     const size_t tv = (tiles * sizeof(T) + 15) & ~size_t(15);
     DBuf<uint8_t> ws(fwords * 4 + 2 * tv, s);
     uint32_t *flag = t_arena ? static_cast<uint32_t *>(t_arena->take_zeroed(fwords * 4)) : nullptr;
@@ -654,22 +641,16 @@ void scan(size_t n, Load ld, Store st, cudaStream_t s, typename Op::T *d_total =
         dev_memset(flag, 0, fwords * 4, s);
     }
     T *agg = reinterpret_cast<T *>(ws.p + fwords * 4), *inc = reinterpret_cast<T *>(ws.p + fwords * 4 + tv);
-    if constexpr (striped) {
-        constexpr size_t smem = scan_smem<T>();
-        if (smem > 48 * 1024) {
-            static bool opted = false;  // per instantiation
-            if (!opted) {
-                CK(cudaFuncSetAttribute(k_scan_1p<Op, Load, Store>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
-                opted = true;
-            }
+    constexpr size_t smem = scan_smem<T>();
+    if (smem > 48 * 1024) {
+        static bool opted = false;  // per instantiation
+        if (!opted) {
+            CK(cudaFuncSetAttribute(k_scan_1p<Op, Load, Store>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            opted = true;
         }
-        launch_k(k_scan_1p<Op, Load, Store>, (unsigned)tiles, SCAN_THREADS, smem, s, n, ld, st, agg, inc, flag,
-                                                                               flag + tiles, d_total);
-    } else {
-        launch_k(k_scan_1p_blocked<Op, Load, Store>, (unsigned)tiles, SCAN_THREADS, 0, s, n, ld, st, agg, inc, flag,
-                                                                                   flag + tiles, d_total);
     }
+    launch_k(k_scan_1p<Op, Load, Store>, (unsigned)tiles, SCAN_THREADS, smem, s, n, ld, st, agg, inc, flag,
+             flag + tiles * FS, d_total);
     CK_LAUNCH("k_scan_1p");
 }
 
