@@ -286,6 +286,11 @@ __global__ void __launch_bounds__(FR_THREADS, 2) k_front_reduce(DevCols c, bool 
 struct FrontOut {
     uint32_t *list[FR_NCAT];  // bad, H, TT, AD, A, TK (nullptr: not written)
     uint32_t *srank;          // nullptr: not written
+    // attribution record per event (fused savings; nullptr: not written): {duration | bucket << 40,
+    // bytes} -- one 16-byte gather per finding member in k_attr instead of four column gathers
+    // (loc, start, end, bytes); `nopack` is set when some duration >= 2^40 or bucket >= 2^24
+    ulonglong2 *attr;
+    unsigned *nopack;
 };
 // Warp-striped tiles (item k of lane l in warp w is base + w*32*ITEMS + 32k + l) keep index
 // order under ballot ranking: a warp's items precede the next warp's, items precede items.
@@ -299,6 +304,7 @@ __global__ void __launch_bounds__(FR_THREADS, 2) k_front_apply(DevCols c, bool b
     const uint32_t lt = lanemask_lt();
     uint32_t fl[FR_ITEMS];  // bits 0..5 category flags, bit 6 start change
     uint32_t wc[FR_NCAT] = {0, 0, 0, 0, 0, 0};
+    bool nopack = false;
 #pragma unroll
     for (int k0 = 0; k0 < FR_ITEMS; k0 += FR_BATCH) {
         uint8_t kd[FR_BATCH];
@@ -308,6 +314,17 @@ __global__ void __launch_bounds__(FR_THREADS, 2) k_front_apply(DevCols c, bool b
         for (int b = 0; b < FR_BATCH; ++b) {
             const size_t i = wb + 32 * (k0 + b), ic = i < last ? i : last;
             kd[b] = c.kind[ic], dst[b] = c.dst[ic], nb[b] = c.nb[ic], h[b] = c.h[ic], st[b] = c.start[ic];
+        }
+        if (out.attr) {
+#pragma unroll
+            for (int b = 0; b < FR_BATCH; ++b) {
+                const size_t i = wb + 32 * (k0 + b);
+                if (i > last) continue;
+                const uint64_t d = c.end[i] - st[b];
+                const uint32_t bk = c.nbuckets ? c.loc_bucket[c.loc[i]] : 0u;
+                nopack |= (d >> 40) != 0 || (bk >> 24) != 0;
+                out.attr[i] = make_ulonglong2(d | ((unsigned long long)bk << 40), nb[b]);
+            }
         }
 #pragma unroll
         for (int b = 0; b < FR_BATCH; ++b) {
@@ -328,6 +345,7 @@ __global__ void __launch_bounds__(FR_THREADS, 2) k_front_apply(DevCols c, bool b
             for (int q = 0; q < FR_NCAT; ++q) wc[q] += __popc(__ballot_sync(0xffffffffu, (f >> q) & 1u));
         }
     }
+    if (out.attr && __any_sync(0xffffffffu, nopack) && lane == 0) atomicOr(out.nopack, 1u);
     // srank: the last start change at or before each index (max scan of change positions)
     uint32_t chmax = 0;
 #pragma unroll
@@ -1737,6 +1755,8 @@ __global__ void k_sums(DevCols c, const uint8_t *cat, unsigned long long *acc /*
 // (report.py:44-95): count, sum of durations, sum of bytes, first member (min position).
 struct AttrAcc {
     unsigned long long *cnt, *ns, *by, *first;  // [nb], [2nb], [2nb], [nb]
+    const ulonglong2 *rec;                       // packed per-event records (FrontOut::attr) or nullptr
+    const unsigned *nopack;
 };
 template <class Elem>
 __global__ void k_attr(DevCols c, size_t n_elem, Elem el, AttrAcc g) {
@@ -1751,6 +1771,7 @@ __global__ void k_attr(DevCols c, size_t n_elem, Elem el, AttrAcc g) {
         __syncthreads();
     }
     const size_t stride = (size_t)gridDim.x * blockDim.x;
+    const bool packed = g.rec && !*g.nopack;
     // warp-uniform trip count so every lane reaches the warp collectives below
     for (size_t base = (size_t)blockIdx.x * blockDim.x; base < n_elem; base += stride) {
         const size_t q = base + threadIdx.x;
@@ -1760,8 +1781,14 @@ __global__ void k_attr(DevCols c, size_t n_elem, Elem el, AttrAcc g) {
         for (int j = 0; j < 2; ++j) {
             const bool have = j < k;
             const uint32_t e = have ? ev[j] : 0;
-            const uint32_t b = have ? c.loc_bucket[c.loc[e]] : 0xFFFFFFFFu;
-            unsigned long long d = have ? c.end[e] - c.start[e] : 0, by = have ? c.nb[e] : 0;
+            uint32_t b = 0xFFFFFFFFu;
+            unsigned long long d = 0, by = 0;
+            if (have && packed) {
+                const ulonglong2 r = g.rec[e];
+                b = (uint32_t)(r.x >> 40), d = r.x & ((1ull << 40) - 1), by = r.y;
+            } else if (have) {
+                b = c.loc_bucket[c.loc[e]], d = c.end[e] - c.start[e], by = c.nb[e];
+            }
             unsigned long long fp = have ? ((pos[j] << 32) | e) : ~0ull, cnt = have ? 1 : 0;
             const uint32_t peers = __match_any_sync(0xffffffffu, b);
             U128 sd{d, 0}, sb{by, 0};
@@ -1845,10 +1872,13 @@ struct SvRun {
     DBuf<uint8_t> cat;
     DBuf<uint32_t> ovl, uni, unic;
     DBuf<OvUn::T> ovt;
+    const ulonglong2 *rec = nullptr;
+    const unsigned *nopack = nullptr;
     AttrAcc acc_of(int cat_i) const {
         unsigned long long *base = at.p;
         return AttrAcc{base + (size_t)cat_i * nb, base + 5 * (size_t)nb + (size_t)cat_i * 2 * nb,
-                       base + 15 * (size_t)nb + (size_t)cat_i * 2 * nb, base + 25 * (size_t)nb + (size_t)cat_i * nb};
+                       base + 15 * (size_t)nb + (size_t)cat_i * 2 * nb, base + 25 * (size_t)nb + (size_t)cat_i * nb,
+                       rec, nopack};
     }
 };
 
@@ -2103,13 +2133,18 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     const size_t nl = only_validate || !n ? 1 : n;
     DBuf<uint32_t> H(nl, s), TT(nl, s), AD(nl, s), A(nl, s), TK(nl, s);
     DBuf<uint32_t> srank(nl, s);
+    // fused savings: the attribution records come out of the apply pass
+    const bool want_attr = (flags & B2L_ANALYZE_WITH_SAVINGS) != 0 && !only_validate && n && c.nbuckets;
+    DBuf<ulonglong2> attr;
+    DBuf<unsigned> nopack;
+    if (want_attr) attr.alloc(n, s), nopack.alloc_zeroed(1, s);
     if (n) {
         launch_k(k_front_reduce, ftiles, FR_THREADS, 0, s, c, validate, raw, fpart.p, agg.p);
         CK_LAUNCH("k_front_reduce");
         launch_k(k_scan_partials<FrontOp>, 1, SCAN_THREADS, 0, s, fpart.p, (size_t)ftiles, fpart.p + ftiles);
         CK_LAUNCH("k_scan_partials<FrontOp>");
         if (!only_validate) {  // lists of an invalid trace are never read
-            FrontOut fo{{nullptr, H.p, TT.p, AD.p, A.p, TK.p}, srank.p};
+            FrontOut fo{{nullptr, H.p, TT.p, AD.p, A.p, TK.p}, srank.p, attr.p, nopack.p};
             launch_k(k_front_apply, ftiles, FR_THREADS, 0, s, c, false, raw, (const FrontAcc *)fpart.p, fo);
             CK_LAUNCH("k_front_apply");
         }
@@ -2118,7 +2153,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     const uint32_t nbad = ftot.c[0];
     if (nbad) {
         DBuf<uint32_t> bad(nbad, s), rules(nbad, s), dcount(1, s);
-        FrontOut fo{{bad.p, nullptr, nullptr, nullptr, nullptr, nullptr}, nullptr};
+        FrontOut fo{{bad.p, nullptr, nullptr, nullptr, nullptr, nullptr}, nullptr, nullptr, nullptr};
         k_front_apply<<<ftiles, FR_THREADS, 0, s>>>(c, true, raw, fpart.p, fo);
         CK_LAUNCH("k_front_apply(bad)");
         CK(cudaMemcpyAsync(dcount.p, &nbad, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
@@ -2151,7 +2186,10 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     // fused savings: attribution / category bits of each category queued as its chain finishes
     const bool with_sv = (flags & B2L_ANALYZE_WITH_SAVINGS) != 0;
     SvRun R;
-    if (with_sv) sv_begin(R, c, s);
+    if (with_sv) {
+        sv_begin(R, c, s);
+        R.rec = attr.p, R.nopack = nopack.p;
+    }
     {  // upper bounds of the device findings: DD/RT offsets and members <= nH, pairs/RA/UA <= nA, UT <= n
         const size_t fb = 16 * (nH + 2) + 12 * (size_t)nH + 8 * (nA + 2) + 16 * (size_t)nA + 4 * n + 32 * 256;
         in->keep.open(n <= ARENA_MAX_EVENTS ? fb : 0, s, 0);

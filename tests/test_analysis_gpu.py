@@ -121,3 +121,27 @@ def test_analyze_many_pipelined_matches_single_calls(cuda):
     assert len(got) == len(traces)
     for cols, (cf, sv) in zip(traces, got):
         assert full_parity(cols, cf, sv) == []
+
+
+def test_fused_savings_packed_records_and_fallback(cuda):
+    """Fused analyze + savings (B2L_ANALYZE_WITH_SAVINGS): attribution reads the front pass's
+    packed per-event records; a duration >= 2^40 ns cannot be packed and takes the column gathers."""
+    from oracle.compare import full_parity
+    from paper_2601_12713_b200 import analyze_columns, savings_columns
+    from paper_2601_12713_b200.columns import to_columns
+    checked = huge = 0
+    for seed in range(300):
+        cols = to_columns(nasty_trace(seed))
+        if R.validate_cols(cols):
+            continue
+        cf = analyze_columns(cols, with_savings=True)
+        assert full_parity(cols, cf, savings_columns(cols, cf)) == [], seed
+        checked += 1
+        if seed % 10 == 0 and cols.end_ns.size:
+            cols.end_ns[cols.end_ns.size // 2] += np.uint64(1 << 41)  # one very long event
+            if R.validate_cols(cols):
+                continue
+            cf = analyze_columns(cols, with_savings=True)
+            assert full_parity(cols, cf, savings_columns(cols, cf)) == [], ("huge", seed)
+            huge += 1
+    assert checked > 100 and huge > 5
