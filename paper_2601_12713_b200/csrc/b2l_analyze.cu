@@ -291,6 +291,7 @@ struct FrontOut {
     // (loc, start, end, bytes); `nopack` is set when some duration >= 2^40 or bucket >= 2^24
     ulonglong2 *attr;
     unsigned *nopack;
+    uint64_t *hd;  // per entry of the hashed-transfer list: src << 32 | dst (nullptr: not written)
 };
 // Warp-striped tiles (item k of lane l in warp w is base + w*32*ITEMS + 32k + l) keep index
 // order under ballot ranking: a warp's items precede the next warp's, items precede items.
@@ -379,7 +380,11 @@ __global__ void __launch_bounds__(FR_THREADS, 2) k_front_apply(DevCols c, bool b
 #pragma unroll
         for (int q = 0; q < FR_NCAT; ++q) {
             const uint32_t m = __ballot_sync(0xffffffffu, (fl[k] >> q) & 1u);
-            if (out.list[q] && ((fl[k] >> q) & 1u)) out.list[q][run[q] + __popc(m & lt)] = (uint32_t)i;
+            if (out.list[q] && ((fl[k] >> q) & 1u)) {
+                out.list[q][run[q] + __popc(m & lt)] = (uint32_t)i;
+                if (q == 1 && out.hd)  // (the columns were just read: cached)
+                    out.hd[run[q] + __popc(m & lt)] = ((uint64_t)(uint32_t)c.src[i] << 32) | (uint32_t)c.dst[i];
+            }
             run[q] += __popc(m);
         }
         if (out.srank) {
@@ -716,12 +721,21 @@ struct PhaseClock {
 struct RtRecordInit {  // record r = 2k + role over hashed transfer k: role 0 = reception, 1 = send
     DevCols c;            // generated in hash-rank order (q = 2p + role over hash-sorted position p)
     const uint32_t *H, *hsv, *hidp;  // hsv[p]: transfer at sorted position p; hidp[p]: its hash rank
+    const uint64_t *hd;              // (src << 32 | dst) per hashed transfer (front pass) or nullptr
     uint64_t *k0;                    // key = device << 32 | rank: queues (device, hash)
     uint32_t *val;
     __device__ void operator()(size_t q) const {
         const size_t p = q >> 1;
-        const uint32_t role = (uint32_t)(q & 1), k = hsv[p], e = H[k];
-        k0[q] = ((uint64_t)(uint32_t)(role ? c.src[e] : c.dst[e]) << 32) | hidp[p];
+        const uint32_t role = (uint32_t)(q & 1), k = hsv[p];
+        uint32_t dev;
+        if (hd) {  // one gather per record instead of three (H[k], then src or dst)
+            const uint64_t sd = hd[k];
+            dev = role ? (uint32_t)(sd >> 32) : (uint32_t)sd;
+        } else {
+            const uint32_t e = H[k];
+            dev = (uint32_t)(role ? c.src[e] : c.dst[e]);
+        }
+        k0[q] = ((uint64_t)dev << 32) | hidp[p];
         val[q] = 2 * k + role;
     }
 };
@@ -878,7 +892,8 @@ struct DdRt {
 cudaStream_t engine_stream_n(int k);
 void stream_after(cudaStream_t to, cudaStream_t from);
 
-DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, Internal &out, cudaStream_t s,
+DdRt dd_rt_step(const DevCols &c, const uint32_t *H, const uint64_t *HD, uint32_t nH, bool strict, Internal &out,
+                cudaStream_t s,
                 b2l_findings *f = nullptr, cudaStream_t sc = nullptr) {
     DdRt r;
     const size_t R = 2ull * nH;
@@ -908,7 +923,7 @@ DdRt dd_rt_step(const DevCols &c, const uint32_t *H, uint32_t nH, bool strict, I
     // come out in (device, hash) order, trace order inside.  Group orders that break start ties by
     // the reference's (hash, device...) key take explicit tie keys below.
     SortStore<1> st(R, s);
-    for_each(R, RtRecordInit{c, H, hsort.val(), hidp.p, st.in_key(0), st.in_val()}, s);
+    for_each(R, RtRecordInit{c, H, hsort.val(), hidp.p, HD, st.in_key(0), st.in_val()}, s);
     pc.mark(" rt-init");
     radix_sort<1>(st.b, R, LiveBytes<1>{{(uint8_t)(g_masks.dev << 4)}}, s);
     pc.mark(" rt-sort");
@@ -2132,6 +2147,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     const bool only_validate = (flags & B2L_ANALYZE_VALIDATE_ONLY) != 0;
     const size_t nl = only_validate || !n ? 1 : n;
     DBuf<uint32_t> H(nl, s), TT(nl, s), AD(nl, s), A(nl, s), TK(nl, s);
+    DBuf<uint64_t> HD(nl, s);
     DBuf<uint32_t> srank(nl, s);
     // fused savings: the attribution records come out of the apply pass
     const bool want_attr = (flags & B2L_ANALYZE_WITH_SAVINGS) != 0 && !only_validate && n && c.nbuckets;
@@ -2144,7 +2160,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
         launch_k(k_scan_partials<FrontOp>, 1, SCAN_THREADS, 0, s, fpart.p, (size_t)ftiles, fpart.p + ftiles);
         CK_LAUNCH("k_scan_partials<FrontOp>");
         if (!only_validate) {  // lists of an invalid trace are never read
-            FrontOut fo{{nullptr, H.p, TT.p, AD.p, A.p, TK.p}, srank.p, attr.p, nopack.p};
+            FrontOut fo{{nullptr, H.p, TT.p, AD.p, A.p, TK.p}, srank.p, attr.p, nopack.p, HD.p};
             launch_k(k_front_apply, ftiles, FR_THREADS, 0, s, c, false, raw, (const FrontAcc *)fpart.p, fo);
             CK_LAUNCH("k_front_apply");
         }
@@ -2153,7 +2169,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     const uint32_t nbad = ftot.c[0];
     if (nbad) {
         DBuf<uint32_t> bad(nbad, s), rules(nbad, s), dcount(1, s);
-        FrontOut fo{{bad.p, nullptr, nullptr, nullptr, nullptr, nullptr}, nullptr, nullptr, nullptr};
+        FrontOut fo{{bad.p, nullptr, nullptr, nullptr, nullptr, nullptr}, nullptr, nullptr, nullptr, nullptr};
         k_front_apply<<<ftiles, FR_THREADS, 0, s>>>(c, true, raw, fpart.p, fo);
         CK_LAUNCH("k_front_apply(bad)");
         CK(cudaMemcpyAsync(dcount.p, &nbad, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
@@ -2302,7 +2318,7 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
         if (ev) cudaEventDestroy(ev);
     };
     try {
-        DdRt dr = dd_rt_step(c, H.p, nH, (flags & B2L_ANALYZE_STRICT_RT) != 0, *in, s, f, sc);
+        DdRt dr = dd_rt_step(c, H.p, HD.p, nH, (flags & B2L_ANALYZE_STRICT_RT) != 0, *in, s, f, sc);
         in->dd_groups = dr.dd_groups, in->dd_members = dr.dd_members, in->rt_groups = dr.rt_groups,
         in->rt_trips = dr.rt_trips;
         if (with_sv) {
