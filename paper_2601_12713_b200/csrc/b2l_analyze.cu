@@ -414,9 +414,9 @@ void for_each(size_t n, F f, cudaStream_t s) {
 }
 
 // Read a device u32 count (one sync).
-uint32_t read_u32(const uint32_t *d, cudaStream_t s) {
+uint32_t read_u32(const uint32_t *d, cudaStream_t s, int line = __builtin_LINE()) {
     uint32_t v = 0;
-    read_back(&v, d, sizeof(v), s);
+    read_back(&v, d, sizeof(v), s, line);
     return v;
 }
 
@@ -2380,6 +2380,20 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
                 (unsigned long long)sync_stats().n.load(), sync_stats().ns.load() * 1e-6,
                 (unsigned long long)sync_stats().ln.load(), sync_stats().lns.load() * 1e-6);
         sync_stats().n = 0, sync_stats().ns = 0, sync_stats().ln = 0, sync_stats().lns = 0;
+        std::lock_guard<std::mutex> g(sync_log_mu());
+        auto &L = sync_log();
+        if (!L.empty()) {
+            std::sort(L.begin(), L.end(), [](const SyncRec &a, const SyncRec &b) { return a.t0 < b.t0; });
+            std::vector<size_t> tids;
+            for (auto &r : L) {
+                size_t k = 0;
+                while (k < tids.size() && tids[k] != r.thread) ++k;
+                if (k == tids.size()) tids.push_back(r.thread);
+                fprintf(stderr, "[b2l-rb] thread %zu line %5d at %8.1f us waited %6.1f us\n", k, r.line,
+                        std::chrono::duration<double, std::micro>(r.t0 - L[0].t0).count(), r.ns * 1e-3);
+            }
+            L.clear();
+        }
     }
     if (in->dd_groups == 0) f->dd_offsets[0] = 0;
     if (in->rt_groups == 0) f->rt_offsets[0] = 0;

@@ -26,6 +26,8 @@
 #include <string>
 #include <type_traits>
 #include <utility>
+#include <thread>
+#include <vector>
 
 #include "b2l_common.cuh"
 
@@ -58,17 +60,39 @@ inline SyncStats &sync_stats() {
     static SyncStats a;
     return a;
 }
+// B2L_SYNC_STATS=2: also every round trip's caller line, host start and wait (printed per call)
+struct SyncRec {
+    int line;
+    std::chrono::steady_clock::time_point t0;
+    uint64_t ns;
+    size_t thread;
+};
+inline std::mutex &sync_log_mu() {
+    static std::mutex m;
+    return m;
+}
+inline std::vector<SyncRec> &sync_log() {
+    static std::vector<SyncRec> v;
+    return v;
+}
 struct SyncTimer {
     bool on;
+    int line;
     std::chrono::steady_clock::time_point t0;
-    SyncTimer() : on(sync_stats().on) {
+    explicit SyncTimer(int ln = 0) : on(sync_stats().on), line(ln) {
         if (on) t0 = std::chrono::steady_clock::now();
     }
     ~SyncTimer() {
         if (!on) return;
+        const uint64_t ns = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+            std::chrono::steady_clock::now() - t0).count();
         sync_stats().n++;
-        sync_stats().ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
-                               std::chrono::steady_clock::now() - t0).count();
+        sync_stats().ns += ns;
+        static const bool detail = getenv("B2L_SYNC_STATS") && getenv("B2L_SYNC_STATS")[0] == '2';
+        if (detail) {
+            std::lock_guard<std::mutex> g(sync_log_mu());
+            sync_log().push_back({line, t0, ns, std::hash<std::thread::id>()(std::this_thread::get_id())});
+        }
     }
 };
 inline AllocStats &alloc_stats() {
@@ -778,8 +802,8 @@ inline void mailbox_wait(Mailbox &m, uint32_t tag, cudaStream_t s) {
     std::atomic_thread_fence(std::memory_order_acquire);
 }
 // Read `bytes` from device memory into host `dst` (synchronous).
-inline void read_back(void *dst, const void *d_src, size_t bytes, cudaStream_t s) {
-    SyncTimer st_;
+inline void read_back(void *dst, const void *d_src, size_t bytes, cudaStream_t s, int line = __builtin_LINE()) {
+    SyncTimer st_(line);
     if (bytes <= MAILBOX_BYTES && mailbox_on() && t_arena && t_arena->mailbox) {
         Mailbox &m = mailbox(s);
         const uint32_t tag = ++m.seq ? m.seq : ++m.seq;
@@ -818,8 +842,8 @@ static __global__ void k_mailbox_multi(MailboxPieces p, uint8_t *box, uint32_t t
         *reinterpret_cast<volatile uint32_t *>(box) = tag;
     }
 }
-inline void read_back_multi(std::initializer_list<ReadPiece> pieces, cudaStream_t s) {
-    SyncTimer st_;
+inline void read_back_multi(std::initializer_list<ReadPiece> pieces, cudaStream_t s, int line = __builtin_LINE()) {
+    SyncTimer st_(line);
     size_t total = 0;
     for (const ReadPiece &q : pieces) total += q.bytes;
     if (!mailbox_on() || !t_arena || !t_arena->mailbox || pieces.size() > 8 || total > MAILBOX_BYTES) {
@@ -844,8 +868,8 @@ inline void read_back_multi(std::initializer_list<ReadPiece> pieces, cudaStream_
 // Wait until everything queued on `s` has run.  (Not through the mailbox: these waits follow
 // large result copies, and a kernel writing into mapped host memory behind a device->host copy
 // stream waits for that link -- at 100M events the chains slowed from 47 to 110 ms.)
-inline void stream_wait(cudaStream_t s) {
-    SyncTimer st_;
+inline void stream_wait(cudaStream_t s, int line = __builtin_LINE()) {
+    SyncTimer st_(line);
     CK(cudaStreamSynchronize(s));
 }
 
