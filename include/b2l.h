@@ -75,6 +75,14 @@ int b2l_hash_host(const void *const *h_bufs, const uint64_t *h_lens, uint64_t n,
  * buffer from 96 KiB).  Asynchronous. */
 int b2l_hash_large(const void *d_buf, uint64_t len, uint64_t *d_digest, void *stream);
 
+/* n huge DEVICE buffers (host array of device addresses + host lengths) -> d_digests[0..n)
+ * (device).  K2 over several buffers per cooperative launch (up to 16, longest first), each
+ * with its own share of the CTAs, so one buffer's cross-CTA waits overlap the others'
+ * arithmetic.  Same digests as n b2l_hash_large calls (hashing.py:34-52 per buffer).
+ * Asynchronous on `stream`; B2L_E_EMPTY_PAYLOAD if any length is zero. */
+int b2l_hash_large_many(const void *const *d_bufs, const uint64_t *lens, uint64_t n,
+                        uint64_t *d_digests, void *stream);
+
 /* One host payload (the HashFn drop-in). */
 int b2l_hash_bytes(const void *h_buf, uint64_t len, uint64_t *digest);
 

@@ -28,7 +28,7 @@ B2L_E_NO_DEVICE = -8
 EXPORTED = (
     "b2l_abi_version", "b2l_last_error", "b2l_device_count",
     "b2l_hash_batch", "b2l_hash_host", "b2l_hash_bytes", "b2l_fill_payloads",
-    "b2l_hash_launch_info", "b2l_hash_select_variant", "b2l_hash_large",
+    "b2l_hash_launch_info", "b2l_hash_select_variant", "b2l_hash_large", "b2l_hash_large_many",
     "b2l_analyze", "b2l_analyze_ex", "b2l_findings_free", "b2l_savings_compute", "b2l_savings_free",
     "b2l_lookup_seqs", "b2l_audit_batch", "b2l_stable_sort_u32", "b2l_stable_sort_u64", "b2l_shard_route", "b2l_shard_unpack", "b2l_sort_u64_pairs_device",
     "b2l_shard_kernel_summary", "b2l_shard_route_pairs",
@@ -59,6 +59,7 @@ def _declare(lib):
         "b2l_fill_payloads": ([_p, _p, _p, _p, _u64, _u64, _p], _int),
         "b2l_hash_select_variant": ([_int, ctypes.POINTER(_int)], _int),
         "b2l_hash_large": ([_p, _u64, _p, _p], _int),
+        "b2l_hash_large_many": ([_p, _p, _u64, _p, _p], _int),
         "b2l_hash_launch_info": ([_u64, ctypes.POINTER(_int), ctypes.POINTER(_int), ctypes.POINTER(_int)], _int),
         "b2l_init": ([_int, ctypes.POINTER(_int)], _int),
         "b2l_shutdown": ([], _int),

@@ -40,6 +40,7 @@ int hash_batch_launch(const uint64_t *, const uint64_t *, uint64_t, uint64_t *, 
 int hash_launch_info(uint64_t, int *, int *, int *);
 int hash_select_variant(int, int *);
 int hash_planes_launch(const void *, uint64_t, uint64_t *, cudaStream_t);
+int hash_planes_launch_many(const void *const *, const uint64_t *, uint64_t, uint64_t *, cudaStream_t);
 constexpr uint64_t K2_MIN_BYTES = 32ull << 20;  // serial chain >= ~20 ms: the whole-GPU fold wins
 constexpr uint64_t K2_SOLO_BYTES = 96ull << 10;  // a call hashing ONE buffer: K2 (~80 us floor) beats the 1.6 ns/B chain
 int fill_payloads_launch(uint8_t *, const uint64_t *, const uint64_t *, const uint64_t *, uint64_t, uint64_t,
@@ -297,6 +298,16 @@ int b2l_hash_large(const void *d_buf, uint64_t len, uint64_t *d_digest, void *st
     if (!d_buf || !d_digest) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
     if (len == 0) return b2l::fail(B2L_E_EMPTY_PAYLOAD, "cannot hash a zero-byte payload");
     return b2l::hash_planes_launch(d_buf, len, d_digest, (cudaStream_t)stream);
+}
+
+int b2l_hash_large_many(const void *const *d_bufs, const uint64_t *lens, uint64_t n, uint64_t *d_digests,
+                        void *stream) {
+    if (n && (!d_bufs || !lens || !d_digests)) return b2l::fail(B2L_E_INVALID_ARG, "null argument");
+    for (uint64_t i = 0; i < n; ++i) {
+        if (lens[i] == 0) return b2l::fail(B2L_E_EMPTY_PAYLOAD, "cannot hash a zero-byte payload");
+        if (!d_bufs[i]) return b2l::fail(B2L_E_INVALID_ARG, "null buffer");
+    }
+    return b2l::hash_planes_launch_many(d_bufs, lens, n, d_digests, (cudaStream_t)stream);
 }
 
 int b2l_hash_bytes(const void *h_buf, uint64_t len, uint64_t *digest) {

@@ -18,7 +18,10 @@
 // all predecessors' aggregates itself (a warp reads them in parallel): no serial look-back
 // chain through the grid.  Chunks beyond the co-resident grid are processed in rounds chained
 // through a per-group carry.  Verified bit-exact against the serial fold (tests).
+#include <algorithm>
+#include <cstdlib>
 #include <mutex>
+#include <vector>
 #include <cooperative_groups.h>
 
 #include "b2l_common.cuh"
@@ -36,6 +39,17 @@ constexpr size_t SMEM = (size_t)2 * THREADS * ROW * sizeof(uint32_t);  // lo and
 // Aggregate slots: a map is 16 bytes whose entries use only the low nibble, so the high
 // nibble of byte 0 marks a published slot and map + mark travel in one 16-byte access.
 constexpr uint32_t MARK = 0x10u;
+// Each slot sits alone on a 128-byte line (uint4 units): up to ~600 CTAs' warps poll their
+// predecessors' slots at once, and slots packed 8 to a line queue those polls on a few lines.
+constexpr uint32_t SLOT_STRIDE = 8;
+// Predecessor slots a lane loads at once before it starts composing (the rest one by one).
+constexpr uint32_t PREFETCH = 1;
+// Optional back-off between polls of an unpublished slot (-DK2_SPIN_NS=n).  Spin loops are ~25%
+// of the kernel's instructions, but 64 or 400 ns of back-off measured no faster than none.
+#ifndef K2_SPIN_NS
+#define K2_SPIN_NS 0
+#endif
+constexpr unsigned SPIN_NS = K2_SPIN_NS;
 __device__ __forceinline__ uint4 ld_slot(const uint4 *p) {
     uint4 v;
     asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -145,7 +159,7 @@ struct Shared {
 
 // One 4-bit group of one round: pass A (maps), the prefix across warps and CTAs, pass B
 // (resolved nibbles written back into y).  HI: the group lies in the high 32 bits.
-template <bool HI>
+template <bool HI, bool FULL>
 __device__ __forceinline__ void group_step(uint32_t *ylo, uint32_t *yhi, int nv, int k, uint64_t r, uint64_t slot,
                                            uint32_t c, uint32_t nc, uint32_t G, uint4 *aggs,
                                            unsigned long long *carry, Shared &sh) {
@@ -160,7 +174,7 @@ __device__ __forceinline__ void group_step(uint32_t *ylo, uint32_t *yhi, int nv,
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
             const int jj = h * Q + j;
-            if (jj < nv) {
+            if (FULL || jj < nv) {
                 const uint32_t lo = ylo[jj], hi = HI ? yhi[jj] : 0u;
                 const uint32_t w4 = ((HI ? hi : lo) >> ks) & 15u, r4 = r_nib<HI>(lo, hi, k);
                 tab_step_lazy(Tq[h], w4 * 0x01010101u, r4 * 0x01010101u);
@@ -193,17 +207,34 @@ __device__ __forceinline__ void group_step(uint32_t *ylo, uint32_t *yhi, int nv,
         Tab agg;
 #pragma unroll
         for (int m = 0; m < 4; ++m) agg.r[m] = __shfl_sync(0xffffffffu, W.r[m], WARPS - 1);
-        uint4 *row = aggs + slot * G;
-        if (lane == 0 && c + 1 < nc) st_slot(&row[c], tab_pack(agg));  // the last CTA's is never read
+        uint4 *row = aggs + slot * G * SLOT_STRIDE;
+        if (lane == 0 && c + 1 < nc) st_slot(&row[c * SLOT_STRIDE], tab_pack(agg));  // the last CTA's is never read
+        // the carry into this round is needed only after the composition: its load goes out now
+        unsigned long long cv = 0;
+        if (lane == 0 && r != 0) cv = ((volatile unsigned long long *)carry)[slot - 16];
         // prefix of the predecessors' aggregates: lane l composes a contiguous block of them
-        // (in order), then a warp scan composes the blocks
+        // (in order), then a warp scan composes the blocks.  The block's first PREFETCH slots
+        // are loaded together (one L2 round trip, not one per slot); unpublished ones re-polled.
         const uint32_t per = (c + 31) / 32, b0 = lane * per, b1 = b0 + per < c ? b0 + per : c;
         Tab P = tab_id();
-        for (uint32_t j = b0; j < b1; ++j) {
+        uint4 pv[PREFETCH];
+#pragma unroll
+        for (uint32_t u = 0; u < PREFETCH; ++u)
+            if (b0 + u < b1) pv[u] = ld_slot(&row[(b0 + u) * SLOT_STRIDE]);
+#pragma unroll
+        for (uint32_t u = 0; u < PREFETCH; ++u) {
+            if (b0 + u < b1) {
+                while (!(pv[u].x & MARK)) {
+                    if (SPIN_NS) __nanosleep(SPIN_NS);
+                    pv[u] = ld_slot(&row[(b0 + u) * SLOT_STRIDE]);
+                }
+                P = tab_compose(P, tab_unpack(unmark(pv[u])));
+            }
+        }
+        for (uint32_t j = b0 + PREFETCH; j < b1; ++j) {
             uint4 v;
-            do {
-                v = ld_slot(&row[j]);
-            } while (!(v.x & MARK));
+            for (v = ld_slot(&row[j * SLOT_STRIDE]); !(v.x & MARK); v = ld_slot(&row[j * SLOT_STRIDE]))
+                if (SPIN_NS) __nanosleep(SPIN_NS);
             P = tab_compose(P, tab_unpack(unmark(v)));
         }
 #pragma unroll
@@ -220,11 +251,11 @@ __device__ __forceinline__ void group_step(uint32_t *ylo, uint32_t *yhi, int nv,
                 s_round = (uint32_t)(FNV_OFFSET >> k) & 15u;
             } else {
                 volatile unsigned long long *vcarry = carry;
-                unsigned long long v;
-                do {
-                    v = vcarry[slot - 16];
-                } while (v == 0);
-                s_round = (uint32_t)v & 15u;
+                while (cv == 0) {
+                    if (SPIN_NS) __nanosleep(SPIN_NS);
+                    cv = vcarry[slot - 16];
+                }
+                s_round = (uint32_t)cv & 15u;
             }
             s_cta = tab_apply(P, s_round);
             if (c + 1 == nc) {  // last chunk of the round: carry its output state
@@ -246,7 +277,7 @@ __device__ __forceinline__ void group_step(uint32_t *ylo, uint32_t *yhi, int nv,
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
             const int jj = h * Q + j;
-            if (jj < nv) {
+            if (FULL || jj < nv) {
                 const uint32_t lo = ylo[jj], hi = HI ? yhi[jj] : 0u;
                 const uint32_t mine = HI ? hi : lo;
                 const uint32_t w4 = (mine >> ks) & 15u, r4 = r_nib<HI>(lo, hi, k);
@@ -257,17 +288,40 @@ __device__ __forceinline__ void group_step(uint32_t *ylo, uint32_t *yhi, int nv,
     }
 }
 
-__global__ void __launch_bounds__(THREADS, 4) k_hash_planes(const uint8_t *__restrict__ buf, uint64_t nbytes,
-                                                            uint4 *aggs, unsigned long long *carry,
-                                                            uint64_t *digest, uint32_t teams) {
+// One buffer of a launch.  A launch hashes up to MAX_JOBS buffers at once, each by its own
+// `teams` teams of G CTAs (G = grid / (jobs * teams)), with its own slot and carry scratch.
+// Independent buffers share every SM, so one buffer's cross-CTA waits are filled by the
+// others' table passes, and a smaller G makes each (round, group) step cheaper.
+struct Job {
+    const uint8_t *buf;
+    uint64_t nbytes;
+    uint4 *aggs;
+    unsigned long long *carry;
+    uint64_t *digest;
+};
+constexpr int MAX_JOBS = 16;
+struct Jobs {
+    Job j[MAX_JOBS];
+    uint32_t njobs, teams;
+};
+
+__global__ void __launch_bounds__(THREADS, 4) k_hash_planes(const __grid_constant__ Jobs J) {
     extern __shared__ uint32_t planes[];  // lo plane then hi plane, THREADS x ROW each
     __shared__ Shared sh;
     const int t = threadIdx.x;
-    // `teams` teams of CTAs take rounds in turn (team t the rounds r = t mod teams): a round's
-    // CTAs wait on each other once per group, and with one CTA of every team on each SM, the
-    // other teams' table passes fill a team's waits (each team runs about one group behind the
-    // previous one, on its carries).
-    const uint32_t G = gridDim.x / teams, team = blockIdx.x / G, c = blockIdx.x % G;
+    // `teams` teams of CTAs take a buffer's rounds in turn (team t the rounds r = t mod teams):
+    // a round's CTAs wait on each other once per group, and with CTAs of several teams on each
+    // SM, the other teams' table passes fill a team's waits (each team runs about one group
+    // behind the previous one, on its carries).
+    const uint32_t teams = J.teams, G = gridDim.x / (J.njobs * teams);
+    const uint32_t unit = blockIdx.x / G, c = blockIdx.x % G;
+    if (unit >= J.njobs * teams) return;
+    const Job &jb = J.j[unit / teams];
+    const uint32_t team = unit % teams;
+    const uint8_t *buf = jb.buf;
+    const uint64_t nbytes = jb.nbytes;
+    uint4 *aggs = jb.aggs;
+    unsigned long long *carry = jb.carry;
     const uint64_t nw = (nbytes + 7) >> 3;
     const uint64_t nchunks = (nw + CHUNK - 1) / CHUNK;
     const uint64_t rounds = (nchunks + G - 1) / G;
@@ -289,14 +343,25 @@ __global__ void __launch_bounds__(THREADS, 4) k_hash_planes(const uint8_t *__res
         uint32_t *ylo = plo + t * ROW, *yhi = phi + t * ROW;  // this thread's words, resident for the round
         const int64_t left = (int64_t)nw - (int64_t)(base + (uint64_t)t * WPT);
         const int nv = left <= 0 ? 0 : (left >= WPT ? WPT : (int)left);
+        if (base + CHUNK <= nw) {  // a full chunk (CTA-uniform): the table passes run unpredicated
 #pragma unroll 1
-        for (int g = 0; g < 8; ++g) group_step<false>(ylo, yhi, nv, 4 * g, r, r * 16 + g, c, nc, G, aggs, carry, sh);
+            for (int g = 0; g < 8; ++g)
+                group_step<false, true>(ylo, yhi, nv, 4 * g, r, r * 16 + g, c, nc, G, aggs, carry, sh);
 #pragma unroll 1
-        for (int g = 8; g < 16; ++g) group_step<true>(ylo, yhi, nv, 4 * g, r, r * 16 + g, c, nc, G, aggs, carry, sh);
+            for (int g = 8; g < 16; ++g)
+                group_step<true, true>(ylo, yhi, nv, 4 * g, r, r * 16 + g, c, nc, G, aggs, carry, sh);
+        } else {
+#pragma unroll 1
+            for (int g = 0; g < 8; ++g)
+                group_step<false, false>(ylo, yhi, nv, 4 * g, r, r * 16 + g, c, nc, G, aggs, carry, sh);
+#pragma unroll 1
+            for (int g = 8; g < 16; ++g)
+                group_step<true, false>(ylo, yhi, nv, 4 * g, r, r * 16 + g, c, nc, G, aggs, carry, sh);
+        }
         __syncthreads();
     }
-    // the final state is the carry of the last round; CTA 0 finishes the digest
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // the final state is the carry of the last round; the buffer's first CTA finishes the digest
+    if (team == 0 && c == 0 && threadIdx.x == 0) {
         volatile unsigned long long *vcarry = carry;
         uint64_t h = 0;
         const uint64_t last = rounds - 1;
@@ -307,7 +372,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_hash_planes(const uint8_t *__res
             } while (v == 0);
             h |= (uint64_t)(v & 15ull) << (4 * g);
         }
-        *digest = finish_digest(h, nbytes);
+        *jb.digest = finish_digest(h, nbytes);
     }
 }
 
@@ -346,56 +411,99 @@ int k2_grid() {
     return C.grid;
 }
 
-// Digest of one device buffer with the whole GPU (cooperative launch: every CTA co-resident).
-int hash_planes_launch(const void *d_buf, uint64_t nbytes, uint64_t *d_digest, cudaStream_t stream) {
-    if (nbytes == 0) return B2L_OK;
+static uint32_t env_u32(const char *name, uint32_t dflt) {
+    const char *v = getenv(name);
+    return v && *v ? (uint32_t)strtoul(v, nullptr, 10) : dflt;
+}
+
+// Digests of n device buffers with the whole GPU (cooperative launches: every CTA co-resident).
+// Buffers go MAX_JOBS (or B2L_K2_JOBS) per launch, longest first; a lone buffer gets one team
+// per co-resident CTA per SM.
+int hash_planes_launch_many(const void *const *d_bufs, const uint64_t *lens, uint64_t n, uint64_t *d_digests,
+                            cudaStream_t stream) {
+    if (n == 0) return B2L_OK;
     int dev = 0;
     B2L_CUDA(cudaGetDevice(&dev));
     k2::Ctx &C = k2::g_ctx[dev & 63];
     const int grid = k2_grid();
     if (grid < 1) return fail(B2L_E_CUDA, "k_hash_planes: no occupancy");
+    std::vector<uint64_t> order(n);
+    for (uint64_t i = 0; i < n; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) { return lens[a] > lens[b]; });
+    const uint32_t per_sm = (uint32_t)(grid / sm_count()) ? (uint32_t)(grid / sm_count()) : 1u;
+    const uint32_t max_jobs = std::min<uint32_t>(std::max<uint32_t>(env_u32("B2L_K2_JOBS", k2::MAX_JOBS), 1u),
+                                                 (uint32_t)k2::MAX_JOBS);
     std::lock_guard<std::mutex> lock(C.mu);
     if (!C.done) B2L_CUDA(cudaEventCreateWithFlags(&C.done, cudaEventDisableTiming));
     B2L_CUDA(cudaStreamWaitEvent(stream, C.done, 0));  // the previous K2 is done with the scratch
-    const uint64_t nw = (nbytes + 7) >> 3;
-    const uint64_t nchunks = (nw + k2::CHUNK - 1) / k2::CHUNK;
-    // one team per co-resident CTA per SM when there is a full grid of chunks, else one team
-    const uint32_t per_sm = (uint32_t)(grid / sm_count());
-    uint32_t teams = per_sm >= 1 ? per_sm : 1;
-    uint64_t g = (uint64_t)sm_count() * teams;
-    if (nchunks < g) teams = 1, g = nchunks;
-    const uint64_t team = g / teams;
-    const uint64_t rounds = (nchunks + team - 1) / team;
-    const size_t need_st = rounds * 16 * team, need_c = rounds * 16;
-    if (C.status_cap < need_st) {
-        if (C.status) {
-            B2L_CUDA(cudaEventSynchronize(C.done));
-            cudaFree(C.status);
+    for (uint64_t i0 = 0; i0 < n;) {
+        const uint32_t nj = (uint32_t)std::min<uint64_t>(max_jobs, n - i0);
+        for (uint32_t k = 0; k < nj; ++k)
+            if (lens[order[i0 + k]] == 0) return fail(B2L_E_EMPTY_PAYLOAD, "cannot hash a zero-byte payload");
+        // teams per buffer: one per co-resident CTA per SM for a lone buffer, else B2L_K2_TEAMS (1)
+        uint32_t teams = nj == 1 ? per_sm : std::max<uint32_t>(env_u32("B2L_K2_TEAMS", 1), 1u);
+        uint64_t G = (uint64_t)grid / ((uint64_t)nj * teams);
+        if (G < 1) teams = 1, G = (uint64_t)grid / nj;
+        const uint64_t nch0 = ((lens[order[i0]] + 7) / 8 + k2::CHUNK - 1) / k2::CHUNK;  // the longest
+        if (nj == 1 && nch0 < (uint64_t)sm_count() * teams) teams = 1, G = std::min<uint64_t>(nch0, grid);
+        else if (nch0 < G) G = nch0;
+        size_t need_st = 0, need_c = 0;
+        k2::Jobs J{};
+        J.njobs = nj;
+        J.teams = teams;
+        for (uint32_t k = 0; k < nj; ++k) {
+            const uint64_t len = lens[order[i0 + k]];
+            const uint64_t nch = ((len + 7) / 8 + k2::CHUNK - 1) / k2::CHUNK;
+            const uint64_t rounds = (nch + G - 1) / G;
+            J.j[k].buf = (const uint8_t *)d_bufs[order[i0 + k]];
+            J.j[k].nbytes = len;
+            J.j[k].digest = d_digests + order[i0 + k];
+            J.j[k].aggs = (uint4 *)(uintptr_t)need_st;  // offsets until the scratch is sized
+            J.j[k].carry = (unsigned long long *)(uintptr_t)need_c;
+            need_st += rounds * 16 * G * k2::SLOT_STRIDE;
+            need_c += rounds * 16;
         }
-        C.status = nullptr;
-        C.status_cap = 0;
-        B2L_CUDA(cudaMalloc(&C.status, need_st * sizeof(uint4)));
-        C.status_cap = need_st;
-    }
-    if (C.carry_cap < need_c) {
-        if (C.carry) {
-            B2L_CUDA(cudaEventSynchronize(C.done));
-            cudaFree(C.carry);
+        if (C.status_cap < need_st) {
+            if (C.status) {
+                B2L_CUDA(cudaEventSynchronize(C.done));
+                B2L_CUDA(cudaStreamSynchronize(stream));
+                cudaFree(C.status);
+            }
+            C.status = nullptr;
+            C.status_cap = 0;
+            B2L_CUDA(cudaMalloc(&C.status, need_st * sizeof(uint4)));
+            C.status_cap = need_st;
         }
-        C.carry = nullptr;
-        C.carry_cap = 0;
-        B2L_CUDA(cudaMalloc(&C.carry, need_c * sizeof(unsigned long long)));
-        C.carry_cap = need_c;
+        if (C.carry_cap < need_c) {
+            if (C.carry) {
+                B2L_CUDA(cudaEventSynchronize(C.done));
+                B2L_CUDA(cudaStreamSynchronize(stream));
+                cudaFree(C.carry);
+            }
+            C.carry = nullptr;
+            C.carry_cap = 0;
+            B2L_CUDA(cudaMalloc(&C.carry, need_c * sizeof(unsigned long long)));
+            C.carry_cap = need_c;
+        }
+        for (uint32_t k = 0; k < nj; ++k) {
+            J.j[k].aggs = C.status + (uintptr_t)J.j[k].aggs;
+            J.j[k].carry = C.carry + (uintptr_t)J.j[k].carry;
+        }
+        B2L_CUDA(cudaMemsetAsync(C.status, 0, need_st * sizeof(uint4), stream));
+        B2L_CUDA(cudaMemsetAsync(C.carry, 0, need_c * sizeof(unsigned long long), stream));
+        void *args[] = {(void *)&J};
+        B2L_CUDA(cudaLaunchCooperativeKernel((const void *)k2::k_hash_planes, dim3((unsigned)(G * nj * teams)),
+                                             dim3(k2::THREADS), args, k2::SMEM, stream));
+        i0 += nj;
     }
-    B2L_CUDA(cudaMemsetAsync(C.status, 0, need_st * sizeof(uint4), stream));
-    B2L_CUDA(cudaMemsetAsync(C.carry, 0, need_c * sizeof(unsigned long long), stream));
-    const uint8_t *b = (const uint8_t *)d_buf;
-    void *args[] = {(void *)&b, (void *)&nbytes, (void *)&C.status, (void *)&C.carry, (void *)&d_digest,
-                    (void *)&teams};
-    B2L_CUDA(cudaLaunchCooperativeKernel((const void *)k2::k_hash_planes, dim3((unsigned)g), dim3(k2::THREADS), args,
-                                         k2::SMEM, stream));
     B2L_CUDA(cudaEventRecord(C.done, stream));
     return B2L_OK;
+}
+
+// Digest of one device buffer with the whole GPU.
+int hash_planes_launch(const void *d_buf, uint64_t nbytes, uint64_t *d_digest, cudaStream_t stream) {
+    if (nbytes == 0) return B2L_OK;
+    return hash_planes_launch_many(&d_buf, &nbytes, 1, d_digest, stream);
 }
 
 }  // namespace b2l

@@ -125,6 +125,23 @@ def hash_large(ptr: int, nbytes: int, out_ptr: int, stream=None) -> None:
     _lib.check(_lib.lib().b2l_hash_large(ptr, nbytes, out_ptr, sp), "b2l_hash_large")
 
 
+def hash_large_many(ptrs, lens, out_ptr: int, stream=None) -> None:
+    """n huge device buffers (addresses, lengths) -> n u64 digests at device address
+    ``out_ptr`` -- b2l_hash_large_many (K2, several buffers per launch).  Asynchronous."""
+    import torch
+    n = len(ptrs)
+    if n == 0:
+        return
+    if any(int(x) == 0 for x in lens):
+        raise EmptyPayload()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    p = np.ascontiguousarray(np.asarray(ptrs, dtype=np.uint64))
+    ln = np.ascontiguousarray(np.asarray(lens, dtype=np.uint64))
+    _lib.check(_lib.lib().b2l_hash_large_many(p.ctypes.data, ln.ctypes.data, n, out_ptr, sp), "b2l_hash_large_many")
+
+
 def hash_tensors(tensors: Sequence, stream=None):
     """Digests of device-resident tensors' bytes, as an int64 CUDA tensor
     holding the u64 bit patterns (``to_u64_list`` converts).  Ragged batches
@@ -142,9 +159,10 @@ def hash_tensors(tensors: Sequence, stream=None):
             raise ValueError("hash_tensors needs contiguous tensors on one CUDA device")
     out = torch.empty(len(tensors), dtype=torch.int64, device=dev)
     big = [i for i, n in enumerate(lens_h) if n >= (K2_SOLO_BYTES if len(tensors) == 1 else K2_MIN_BYTES)]
-    for i in big:  # each huge buffer with the whole GPU, then the rest as one batch
-        hash_large(tensors[i].data_ptr(), lens_h[i], out.data_ptr() + 8 * i, stream)
-    if big:
+    if big:  # the huge buffers with the whole GPU (K2, several per launch), then the rest as one batch
+        bout = torch.empty(len(big), dtype=torch.int64, device=dev)
+        hash_large_many([tensors[i].data_ptr() for i in big], [lens_h[i] for i in big], bout.data_ptr(), stream)
+        out[torch.tensor(big, device=dev)] = bout
         bigs = set(big)
         small = [i for i in range(len(tensors)) if i not in bigs]
         if small:

@@ -308,6 +308,36 @@ def test_k2_multi_round_buffer_and_routing(cuda):
     assert got == want
 
 
+def test_k2_many_ragged_vs_oracle(cuda):
+    """b2l_hash_large_many: 21 buffers (two launches of up to 16), ragged and misaligned, from
+    one word to 40 MiB + 7 (full and partial chunks, one- and multi-round buffers), vs the C oracle
+    and vs one b2l_hash_large per buffer."""
+    import torch
+    from paper_2601_12713_b200.hashing import hash_large, hash_large_many
+    rng = np.random.default_rng(21)
+    lens = [1, 7, 8, 4095, 49152, 49153, (40 << 20) + 7, 3 << 20] + [int(x) for x in rng.integers(1, 3 << 20, 13)]
+    offs, o = [], 0
+    for n in lens:
+        o += int(rng.integers(0, 8))
+        offs.append(o)
+        o += n
+    slab = torch.randint(0, 256, (o + 8,), dtype=torch.uint8, device=cuda)
+    ptrs = [slab.data_ptr() + x for x in offs]
+    out = torch.zeros(len(lens), dtype=torch.int64, device=cuda)
+    hash_large_many(ptrs, lens, out.data_ptr())
+    one = torch.zeros(len(lens), dtype=torch.int64, device=cuda)
+    for i, (p, n) in enumerate(zip(ptrs, lens)):
+        hash_large(p, n, one.data_ptr() + 8 * i)
+    torch.cuda.synchronize()
+    host = slab.cpu().numpy()
+    want = hash_ref.fold64_c_batch(np.array([host.ctypes.data + x for x in offs], dtype=np.uint64),
+                                   np.array(lens, dtype=np.uint64))
+    assert out.cpu().numpy().view(np.uint64).tolist() == want.tolist()
+    assert torch.equal(out, one)
+    with pytest.raises(Exception):
+        hash_large_many(ptrs[:2], [5, 0], out.data_ptr())
+
+
 # ----------------------------------------------------------------------------- collision audit
 def test_audit_reference_cases(cuda):
     from paper_2601_12713_b200 import CollisionAuditStore, audit_observe, hash_bytes
