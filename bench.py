@@ -688,7 +688,7 @@ def _c3_hash(args, dev):
     peak, peak_src = peaks()
     return _line("C3-hash", k * size / dt / 1e9, "GB/s", dt * 1e3, buffers=k, buffer_bytes=size,
                  ms_per_buffer=round(dt / k * 1e3, 3), verified=verified,
-                 roofline=_roofline(k * size / dt / 1e9, peak, peak_src, traffic=ncu_traffic("k2_ncu_summary.json"),
+                 roofline=_roofline(k * size / dt / 1e9, peak, peak_src, traffic=ncu_traffic("k2_many_ncu_summary.json"),
                                     algorithmic_bytes_per_launch=k * size,
                                     kernel="k_hash_planes (K2, the 16 arrays in one launch)",
                                     note="ALU/latency bound: one serial FNV chain per buffer resolved as 16 "

@@ -159,7 +159,18 @@ __global__ void k_bad_rules(DevCols c, const uint32_t *bad, const uint32_t *coun
 //           change; block-reduced atomics for max end and the OR/AND masks;
 //   apply:  order-preserving warp-ballot compaction of the five index lists (or of the
 //           bad list when validation failed) and srank[i] = last start change <= i.
-constexpr int FR_THREADS = 256, FR_ITEMS = 16, FR_TILE = FR_THREADS * FR_ITEMS, FR_NCAT = 6;
+#ifndef B2L_FR_ITEMS
+#define B2L_FR_ITEMS 16
+#endif
+#ifndef B2L_FR_MINB
+#define B2L_FR_MINB 2
+#endif
+constexpr int FR_THREADS = 256, FR_ITEMS = B2L_FR_ITEMS, FR_TILE = FR_THREADS * FR_ITEMS, FR_NCAT = 6;
+#ifndef B2L_FR_MINB_APPLY
+#define B2L_FR_MINB_APPLY B2L_FR_MINB
+#endif
+constexpr int FR_MINB = B2L_FR_MINB;  // resident CTAs per SM the front kernels are compiled for
+constexpr int FR_MINB_APPLY = B2L_FR_MINB_APPLY;
 enum : uint32_t { F_BAD = 1, F_H = 2, F_TT = 4, F_AD = 8, F_A = 16, F_TK = 32 };
 struct FrontAcc {
     uint32_t c[FR_NCAT];
@@ -188,7 +199,7 @@ __device__ __forceinline__ uint32_t part_flags(const DevCols &c, uint8_t k, int3
 }
 constexpr int FR_BATCH = 4;  // items whose loads are issued together (memory-level parallelism)
 
-__global__ void __launch_bounds__(FR_THREADS, 2) k_front_reduce(DevCols c, bool validate, bool raw, FrontAcc *partials,
+__global__ void __launch_bounds__(FR_THREADS, FR_MINB) k_front_reduce(DevCols c, bool validate, bool raw, FrontAcc *partials,
                                                              unsigned long long *agg /*[0] max end, [1..5] OR, [6..10] AND*/) {
     pdl_enter();
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -296,7 +307,7 @@ struct FrontOut {
 // Warp-striped tiles (item k of lane l in warp w is base + w*32*ITEMS + 32k + l) keep index
 // order under ballot ranking: a warp's items precede the next warp's, items precede items.
 // bad_mode: only the bad list (validation failed); else the five partition lists + srank.
-__global__ void __launch_bounds__(FR_THREADS, 2) k_front_apply(DevCols c, bool bad_mode, bool raw,
+__global__ void __launch_bounds__(FR_THREADS, FR_MINB_APPLY) k_front_apply(DevCols c, bool bad_mode, bool raw,
                                                             const FrontAcc *__restrict__ prefix, FrontOut out) {
     pdl_enter();
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;

@@ -29,7 +29,11 @@
 namespace b2l {
 namespace k2 {
 
-constexpr int THREADS = 256;
+#ifndef K2_THREADS
+#define K2_THREADS 256
+#endif
+constexpr int THREADS = K2_THREADS;
+constexpr int MIN_BLOCKS = 1024 / THREADS;  // 1024 threads' worth of CTAs per SM (64 registers)
 constexpr int WARPS = THREADS / 32;
 constexpr int WPT = 24;                   // words per thread, resident in shared memory
 constexpr int CHUNK = THREADS * WPT;      // words per CTA per round (48 KiB; four CTAs per SM)
@@ -305,7 +309,7 @@ struct Jobs {
     uint32_t njobs, teams;
 };
 
-__global__ void __launch_bounds__(THREADS, 4) k_hash_planes(const __grid_constant__ Jobs J) {
+__global__ void __launch_bounds__(THREADS, MIN_BLOCKS) k_hash_planes(const __grid_constant__ Jobs J) {
     extern __shared__ uint32_t planes[];  // lo plane then hi plane, THREADS x ROW each
     __shared__ Shared sh;
     const int t = threadIdx.x;

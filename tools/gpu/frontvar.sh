@@ -1,0 +1,17 @@
+# front-pass tile / occupancy variants (prebuilt into tools/_exp): parity subset + timings
+cp paper_2601_12713_b200/libb2l.so /tmp/libb2l_keep.so
+for v in base i8a3 i8a2 i16a3; do
+  cp tools/_exp/libb2l_$v.so paper_2601_12713_b200/libb2l.so
+  echo "== $v"
+  timeout -k 5 300 python -m pytest tests/test_analysis_gpu.py -q -x 2>&1 | tail -1
+  for cfg in "c2 1000000 24" "c2 10000000 8"; do
+    set -- $cfg
+    timeout -k 5 300 python tools/time_analysis.py --device --config $1 --n $2 --iters $3 2>&1 | tail -1
+  done
+done
+for v in base i8a3; do
+  cp tools/_exp/libb2l_$v.so paper_2601_12713_b200/libb2l.so
+  echo "== $v again"
+  timeout -k 5 300 python tools/time_analysis.py --device --config c2 --n 10000000 --iters 8 2>&1 | tail -1
+done
+cp /tmp/libb2l_keep.so paper_2601_12713_b200/libb2l.so
