@@ -157,6 +157,12 @@ def hash_tensors(tensors: Sequence, stream=None):
     for t in tensors:
         if not t.is_contiguous() or t.device != dev:
             raise ValueError("hash_tensors needs contiguous tensors on one CUDA device")
+    if stream is not None:  # torch's own copies and scatters below go on the caller's stream too
+        if not isinstance(stream, torch.cuda.Stream):
+            stream = torch.cuda.ExternalStream(int(stream), device=dev)
+        if stream != torch.cuda.current_stream(dev):
+            with torch.cuda.stream(stream):
+                return hash_tensors(tensors, stream=stream)
     out = torch.empty(len(tensors), dtype=torch.int64, device=dev)
     big = [i for i, n in enumerate(lens_h) if n >= (K2_SOLO_BYTES if len(tensors) == 1 else K2_MIN_BYTES)]
     if big:  # the huge buffers with the whole GPU (K2, several per launch), then the rest as one batch

@@ -338,6 +338,23 @@ def test_k2_many_ragged_vs_oracle(cuda):
         hash_large_many(ptrs[:2], [5, 0], out.data_ptr())
 
 
+def test_hash_tensors_on_side_stream(cuda):
+    """hash_tensors(stream=...) with K2 and K1 buffers: every torch copy/scatter of the call is
+    ordered on the caller's stream (a torch Stream or a raw handle)."""
+    import torch
+    from paper_2601_12713_b200 import hash_tensors
+    from paper_2601_12713_b200.hashing import to_u64_list
+    g = torch.Generator(device=cuda).manual_seed(5)
+    slab = torch.randint(0, 256, ((40 << 20) + (33 << 20) + 4096,), dtype=torch.uint8, device=cuda, generator=g)
+    ts = [slab[:(40 << 20) + 1], slab[(40 << 20) + 3:(40 << 20) + 1003], slab[-(33 << 20):]]
+    want = [hash_ref.fold64_c(t.cpu().numpy().tobytes()) for t in ts]
+    side = torch.cuda.Stream(device=cuda)
+    for st in (side, side.cuda_stream):
+        got = hash_tensors(ts, stream=st)
+        side.synchronize()
+        assert to_u64_list(got) == want
+
+
 # ----------------------------------------------------------------------------- collision audit
 def test_audit_reference_cases(cuda):
     from paper_2601_12713_b200 import CollisionAuditStore, audit_observe, hash_bytes
