@@ -412,6 +412,167 @@ __global__ void __launch_bounds__(FR_THREADS, FR_MINB_APPLY) k_front_apply(DevCo
     }
 }
 
+// Single-pass front (the normal path): reduce + apply in ONE read of the columns.  Tiles take
+// ids in launch order; each reads its 4096 rows once (validation rules, partition flags, start
+// changes, max data-op end, key masks, attribution records), publishes its counts by decoupled
+// look-back (block_lookback: the same protocol as the single-pass scans) and compacts its five
+// index lists + start ranks behind the exclusive prefix it gets back.  The bad list is not
+// written: a trace with violations (total.c[0] > 0) takes the reduce/apply path above, once, to
+// list them (an error path).  Columns are read once instead of twice (10M events: ~140 -> ~100
+// B/event for the front pass).
+__global__ void __launch_bounds__(FR_THREADS, FR_MINB) k_front_fused(DevCols c, bool validate, bool raw,
+                                                                     FrontOut out, FrontAcc *lb_agg,
+                                                                     FrontAcc *lb_inc, uint32_t *lb_flag,
+                                                                     uint32_t *counter, FrontAcc *d_total,
+                                                                     unsigned long long *agg) {
+    static_assert(FR_THREADS == SCAN_THREADS, "block_lookback runs on the whole block");
+    pdl_enter();
+    __shared__ uint32_t tile_s;
+    if (threadIdx.x == 0) tile_s = atomicAdd(counter, 1u);
+    __syncthreads();
+    const uint32_t tile = tile_s;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const size_t wb = (size_t)tile * FR_TILE + (size_t)warp * (32 * FR_ITEMS) + lane;
+    const size_t last = c.n - 1;
+    const uint32_t lt = lanemask_lt();
+    uint32_t fl[FR_ITEMS];  // bits 0..5 category flags, bit 6 start change
+    uint32_t wc[FR_NCAT] = {0, 0, 0, 0, 0, 0};
+    bool nopack = false;
+    unsigned long long me = 0, o[5] = {0, 0, 0, 0, 0}, a[5] = {~0ull, ~0ull, ~0ull, ~0ull, ~0ull};
+#pragma unroll
+    for (int k0 = 0; k0 < FR_ITEMS; k0 += FR_BATCH) {
+        Row r[FR_BATCH];
+        uint64_t sa[FR_BATCH], p0s = 0, p0q = 0;
+#pragma unroll
+        for (int b = 0; b < FR_BATCH; ++b) {
+            const size_t i = wb + 32 * (k0 + b), ic = i < last ? i : last;
+            r[b] = load_row(c, ic);
+            sa[b] = c.sa[ic];
+        }
+        {
+            const size_t i0 = wb + 32 * k0;  // lane 0's predecessor lives in the previous 32-run
+            if (lane == 0 && i0 > 0 && i0 <= last) p0s = c.start[i0 - 1], p0q = c.seq[i0 - 1];
+        }
+#pragma unroll
+        for (int b = 0; b < FR_BATCH; ++b) {
+            const size_t i = wb + 32 * (k0 + b);
+            uint64_t ps = __shfl_up_sync(0xffffffffu, r[b].start, 1), pq = __shfl_up_sync(0xffffffffu, r[b].seq, 1);
+            if (lane == 0) {
+                if (b == 0) ps = p0s, pq = p0q;
+                else ps = c.start[i - 1 < last ? i - 1 : last], pq = c.seq[i - 1 < last ? i - 1 : last];
+            }
+            uint32_t f = 0;
+            if (i <= last) {
+                f = part_flags(c, r[b].kind, r[b].dst, r[b].nb, r[b].h, raw);
+                if (validate && row_rules(c, r[b], i > 0, ps, pq)) f |= F_BAD;
+                if (i == 0 || r[b].start != ps) f |= 64u;
+                if (r[b].kind != B2L_KIND_KERNEL) me = r[b].end > me ? r[b].end : me;
+                if (r[b].kind == B2L_KIND_TRANSFER) {
+                    o[0] |= r[b].h, a[0] &= r[b].h;  // superset of the hashed subset
+                    if (f & F_TT) o[4] |= sa[b], a[4] &= sa[b];
+                } else if (f & F_AD) {
+                    o[1] |= r[b].da, a[1] &= r[b].da;
+                    if (f & F_A) o[2] |= sa[b], a[2] &= sa[b], o[3] |= r[b].nb, a[3] &= r[b].nb;
+                }
+                if (out.attr) {
+                    const uint64_t d = r[b].end - r[b].start;
+                    const uint32_t bk = c.nbuckets ? c.loc_bucket[r[b].loc] : 0u;
+                    nopack |= (d >> 40) != 0 || (bk >> 24) != 0;
+                    out.attr[i] = make_ulonglong2(d | ((unsigned long long)bk << 40), r[b].nb);
+                }
+            }
+            fl[k0 + b] = f;
+#pragma unroll
+            for (int q = 0; q < FR_NCAT; ++q) wc[q] += __popc(__ballot_sync(0xffffffffu, (f >> q) & 1u));
+        }
+    }
+    if (out.attr && __any_sync(0xffffffffu, nopack) && lane == 0) atomicOr(out.nopack, 1u);
+    uint32_t chmax = 0;
+#pragma unroll
+    for (int k = 0; k < FR_ITEMS; ++k)
+        if (fl[k] & 64u) chmax = (uint32_t)(wb + 32 * k);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        const uint32_t v = __shfl_xor_sync(0xffffffffu, chmax, off);
+        chmax = v > chmax ? v : chmax;
+        const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, me, off);
+        me = m2 > me ? m2 : me;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            o[q] |= __shfl_xor_sync(0xffffffffu, o[q], off);
+            a[q] &= __shfl_xor_sync(0xffffffffu, a[q], off);
+        }
+    }
+    __shared__ uint32_t swc[FR_THREADS / 32][FR_NCAT + 1];
+    __shared__ unsigned long long sm[FR_THREADS / 32][11];
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < FR_NCAT; ++q) swc[warp][q] = wc[q];
+        swc[warp][FR_NCAT] = chmax;
+        sm[warp][0] = me;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) sm[warp][1 + q] = o[q], sm[warp][6 + q] = a[q];
+    }
+    __syncthreads();
+    if (t >= 32 && t < 32 + 11) {  // key masks and max end: block-reduced atomics
+        const int q = t - 32;
+        unsigned long long v = q < 6 ? 0ull : ~0ull;
+        for (int w = 0; w < FR_THREADS / 32; ++w) {
+            const unsigned long long x = sm[w][q];
+            v = q == 0 ? (x > v ? x : v) : q < 6 ? (v | x) : (v & x);
+        }
+        if (q == 0) {
+            if (v) atomicMax(agg, v);
+        } else if (q < 6) {
+            if (v) atomicOr(agg + q, v);
+        } else if (~v) {
+            atomicAnd(agg + q, v);
+        }
+    }
+    FrontAcc total = FrontOp::identity();
+    for (int w = 0; w < FR_THREADS / 32; ++w) {
+#pragma unroll
+        for (int q = 0; q < FR_NCAT; ++q) total.c[q] += swc[w][q];
+        total.lastchg = swc[w][FR_NCAT] > total.lastchg ? swc[w][FR_NCAT] : total.lastchg;
+    }
+    const FrontAcc pre = block_lookback<FrontOp>(tile, total, lb_agg, lb_inc, lb_flag);
+    if (t == 0 && (size_t)(tile + 1) * FR_TILE > last) *d_total = FrontOp::combine(pre, total);
+    uint32_t run[FR_NCAT];
+#pragma unroll
+    for (int q = 0; q < FR_NCAT; ++q) {
+        uint32_t b = pre.c[q];
+        for (int w = 0; w < warp; ++w) b += swc[w][q];
+        run[q] = b;
+    }
+    uint32_t carry = pre.lastchg;
+    for (int w = 0; w < warp; ++w) carry = swc[w][FR_NCAT] > carry ? swc[w][FR_NCAT] : carry;
+#pragma unroll
+    for (int k = 0; k < FR_ITEMS; ++k) {
+        const size_t i = wb + 32 * k;
+#pragma unroll
+        for (int q = 1; q < FR_NCAT; ++q) {
+            const uint32_t m = __ballot_sync(0xffffffffu, (fl[k] >> q) & 1u);
+            if (out.list[q] && ((fl[k] >> q) & 1u)) {
+                out.list[q][run[q] + __popc(m & lt)] = (uint32_t)i;
+                if (q == 1 && out.hd)  // (the columns were just read: cached)
+                    out.hd[run[q] + __popc(m & lt)] = ((uint64_t)(uint32_t)c.src[i] << 32) | (uint32_t)c.dst[i];
+            }
+            run[q] += __popc(m);
+        }
+        if (out.srank) {
+            uint32_t v = (fl[k] & 64u) ? (uint32_t)i : 0u;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, v, off);
+                if (lane >= off) v = y > v ? y : v;
+            }
+            v = v > carry ? v : carry;
+            if (i <= last) out.srank[i] = v;
+            carry = __shfl_sync(0xffffffffu, v, 31);
+        }
+    }
+}
+
 // ============================================================ helpers
 template <class F>
 __global__ void k_for(size_t n, F f) {
@@ -2165,7 +2326,18 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
     DBuf<ulonglong2> attr;
     DBuf<unsigned> nopack;
     if (want_attr) attr.alloc(n, s), nopack.alloc_zeroed(1, s);
-    if (n) {
+    static const bool two_pass = getenv("B2L_FRONT_TWO_PASS") != nullptr;  // the r02 reduce/apply path
+    const bool fused_front = n && !only_validate && !two_pass;
+    if (fused_front) {  // one read of the columns (k_front_fused); the counts come back with the masks
+        DBuf<uint32_t> lbf;  // look-back flags (one per 128-byte line) + the tile ticket, zeroed
+        lbf.alloc_zeroed((ftiles + 1) * FS + 1, s);
+        DBuf<FrontAcc> lb(2 * (size_t)ftiles, s);
+        FrontOut fo{{nullptr, H.p, TT.p, AD.p, A.p, TK.p}, srank.p, attr.p, nopack.p, HD.p};
+        launch_k(k_front_fused, ftiles, FR_THREADS, 0, s, c, validate, raw, fo, lb.p, lb.p + ftiles, lbf.p,
+                 lbf.p + (ftiles + 1) * FS, fpart.p + ftiles, agg.p);
+        CK_LAUNCH("k_front_fused");
+        read_back_multi({{&ftot, fpart.p + ftiles, sizeof(FrontAcc)}, {hm, agg.p, sizeof(hm)}}, s);
+    } else if (n) {
         launch_k(k_front_reduce, ftiles, FR_THREADS, 0, s, c, validate, raw, fpart.p, agg.p);
         CK_LAUNCH("k_front_reduce");
         launch_k(k_scan_partials<FrontOp>, 1, SCAN_THREADS, 0, s, fpart.p, (size_t)ftiles, fpart.p + ftiles);
@@ -2178,6 +2350,13 @@ int analyze_impl(const b2l_trace_cols *cols, uint32_t flags, uint64_t synth_end_
         read_back_multi({{&ftot, fpart.p + ftiles, sizeof(FrontAcc)}, {hm, agg.p, sizeof(hm)}}, s);
     }
     const uint32_t nbad = ftot.c[0];
+    if (nbad && fused_front) {  // error path: per-tile bad counts for the bad list
+        init_u64(agg.p, 6, 5, 0, s);
+        launch_k(k_front_reduce, ftiles, FR_THREADS, 0, s, c, validate, raw, fpart.p, agg.p);
+        CK_LAUNCH("k_front_reduce");
+        launch_k(k_scan_partials<FrontOp>, 1, SCAN_THREADS, 0, s, fpart.p, (size_t)ftiles, fpart.p + ftiles);
+        CK_LAUNCH("k_scan_partials<FrontOp>");
+    }
     if (nbad) {
         DBuf<uint32_t> bad(nbad, s), rules(nbad, s), dcount(1, s);
         FrontOut fo{{bad.p, nullptr, nullptr, nullptr, nullptr, nullptr}, nullptr, nullptr, nullptr, nullptr};
