@@ -171,6 +171,14 @@ constexpr int FR_THREADS = 256, FR_ITEMS = B2L_FR_ITEMS, FR_TILE = FR_THREADS * 
 #endif
 constexpr int FR_MINB = B2L_FR_MINB;  // resident CTAs per SM the front kernels are compiled for
 constexpr int FR_MINB_APPLY = B2L_FR_MINB_APPLY;
+#ifndef B2L_FR_MINB_FUSED
+#define B2L_FR_MINB_FUSED B2L_FR_MINB
+#endif
+constexpr int FR_MINB_FUSED = B2L_FR_MINB_FUSED;
+#ifndef B2L_FR_BATCH_FUSED
+#define B2L_FR_BATCH_FUSED 4
+#endif
+constexpr int FR_BATCH_FUSED = B2L_FR_BATCH_FUSED;  // rows whose loads the fused pass issues together
 enum : uint32_t { F_BAD = 1, F_H = 2, F_TT = 4, F_AD = 8, F_A = 16, F_TK = 32 };
 struct FrontAcc {
     uint32_t c[FR_NCAT];
@@ -420,7 +428,7 @@ __global__ void __launch_bounds__(FR_THREADS, FR_MINB_APPLY) k_front_apply(DevCo
 // written: a trace with violations (total.c[0] > 0) takes the reduce/apply path above, once, to
 // list them (an error path).  Columns are read once instead of twice (10M events: ~140 -> ~100
 // B/event for the front pass).
-__global__ void __launch_bounds__(FR_THREADS, FR_MINB) k_front_fused(DevCols c, bool validate, bool raw,
+__global__ void __launch_bounds__(FR_THREADS, FR_MINB_FUSED) k_front_fused(DevCols c, bool validate, bool raw,
                                                                      FrontOut out, FrontAcc *lb_agg,
                                                                      FrontAcc *lb_inc, uint32_t *lb_flag,
                                                                      uint32_t *counter, FrontAcc *d_total,
@@ -440,11 +448,11 @@ __global__ void __launch_bounds__(FR_THREADS, FR_MINB) k_front_fused(DevCols c, 
     bool nopack = false;
     unsigned long long me = 0, o[5] = {0, 0, 0, 0, 0}, a[5] = {~0ull, ~0ull, ~0ull, ~0ull, ~0ull};
 #pragma unroll
-    for (int k0 = 0; k0 < FR_ITEMS; k0 += FR_BATCH) {
-        Row r[FR_BATCH];
-        uint64_t sa[FR_BATCH], p0s = 0, p0q = 0;
+    for (int k0 = 0; k0 < FR_ITEMS; k0 += FR_BATCH_FUSED) {
+        Row r[FR_BATCH_FUSED];
+        uint64_t sa[FR_BATCH_FUSED], p0s = 0, p0q = 0;
 #pragma unroll
-        for (int b = 0; b < FR_BATCH; ++b) {
+        for (int b = 0; b < FR_BATCH_FUSED; ++b) {
             const size_t i = wb + 32 * (k0 + b), ic = i < last ? i : last;
             r[b] = load_row(c, ic);
             sa[b] = c.sa[ic];
@@ -454,7 +462,7 @@ __global__ void __launch_bounds__(FR_THREADS, FR_MINB) k_front_fused(DevCols c, 
             if (lane == 0 && i0 > 0 && i0 <= last) p0s = c.start[i0 - 1], p0q = c.seq[i0 - 1];
         }
 #pragma unroll
-        for (int b = 0; b < FR_BATCH; ++b) {
+        for (int b = 0; b < FR_BATCH_FUSED; ++b) {
             const size_t i = wb + 32 * (k0 + b);
             uint64_t ps = __shfl_up_sync(0xffffffffu, r[b].start, 1), pq = __shfl_up_sync(0xffffffffu, r[b].seq, 1);
             if (lane == 0) {
