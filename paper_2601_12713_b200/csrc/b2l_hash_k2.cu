@@ -33,9 +33,15 @@ namespace k2 {
 #define K2_THREADS 256
 #endif
 constexpr int THREADS = K2_THREADS;
-constexpr int MIN_BLOCKS = 1024 / THREADS;  // 1024 threads' worth of CTAs per SM (64 registers)
+#ifndef K2_MIN_BLOCKS
+#define K2_MIN_BLOCKS (1024 / K2_THREADS)
+#endif
+constexpr int MIN_BLOCKS = K2_MIN_BLOCKS;  // 1024 threads' worth of CTAs per SM (64 registers)
 constexpr int WARPS = THREADS / 32;
-constexpr int WPT = 24;                   // words per thread, resident in shared memory
+#ifndef K2_WPT
+#define K2_WPT 24
+#endif
+constexpr int WPT = K2_WPT;                   // words per thread, resident in shared memory
 constexpr int CHUNK = THREADS * WPT;      // words per CTA per round (48 KiB; four CTAs per SM)
 constexpr int ROW = WPT + 1;              // padded row (u32 units): conflict-free column access
 constexpr size_t SMEM = (size_t)2 * THREADS * ROW * sizeof(uint32_t);  // lo and hi planes

@@ -40,3 +40,22 @@ def test_hash_fails_loudly_without_device():
     from paper_2601_12713_b200 import EngineError, hash_bytes
     with pytest.raises(EngineError):
         hash_bytes(b"abc")
+
+
+def test_hash_large_many_argument_errors():
+    """b2l_hash_large_many checks its arguments before touching a device (hashing.py:29 maps a
+    zero-length payload to EmptyPayload; null arrays are B2L_E_INVALID_ARG)."""
+    import numpy as np
+    import pytest
+    from paper_2601_12713_b200 import _lib
+    from paper_2601_12713_b200.errors import EmptyPayload
+    from paper_2601_12713_b200.hashing import hash_large_many
+    L = _lib.lib()
+    assert L.b2l_hash_large_many(None, None, 0, None, None) == 0  # nothing to hash
+    assert L.b2l_hash_large_many(None, None, 1, None, None) != 0
+    ptrs = np.array([4096, 8192], dtype=np.uint64)
+    lens = np.array([16, 0], dtype=np.uint64)
+    assert L.b2l_hash_large_many(ptrs.ctypes.data, lens.ctypes.data, 2, 64, None) != 0
+    assert b"zero-byte" in L.b2l_last_error()
+    with pytest.raises(EmptyPayload):
+        hash_large_many([4096, 8192], [16, 0], 64)
