@@ -34,15 +34,19 @@ namespace k2 {
 #endif
 constexpr int THREADS = K2_THREADS;
 #ifndef K2_MIN_BLOCKS
-#define K2_MIN_BLOCKS (1024 / K2_THREADS)
+#define K2_MIN_BLOCKS 3
 #endif
-constexpr int MIN_BLOCKS = K2_MIN_BLOCKS;  // 1024 threads' worth of CTAs per SM (64 registers)
+constexpr int MIN_BLOCKS = K2_MIN_BLOCKS;  // co-resident CTAs per SM (three: up to 85 registers, 3 x 74 KiB of words)
 constexpr int WARPS = THREADS / 32;
 #ifndef K2_WPT
-#define K2_WPT 24
+#define K2_WPT 36
 #endif
 constexpr int WPT = K2_WPT;                   // words per thread, resident in shared memory
-constexpr int CHUNK = THREADS * WPT;      // words per CTA per round (48 KiB; four CTAs per SM)
+// words per CTA per round (72 KiB; three CTAs per SM).  Measured (16 x 256 MiB / one 256 MiB):
+// 24 words x 4 CTAs 164 / 143 GB/s, 32 x 3 186 / 156, 36 x 3 196 / 163, 48 x 2 191 / 159 -- the
+// step count falls with the words resident per SM, and each step costs about the same.
+static_assert(WPT % 4 == 0, "the table passes run four quarter chains per thread");
+constexpr int CHUNK = THREADS * WPT;
 constexpr int ROW = WPT + 1;              // padded row (u32 units): conflict-free column access
 constexpr size_t SMEM = (size_t)2 * THREADS * ROW * sizeof(uint32_t);  // lo and hi planes
 
