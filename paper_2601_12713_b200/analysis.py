@@ -18,6 +18,7 @@ divisions -- is done here from exact integers, as in the reference.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 from typing import Callable, Optional
 
@@ -185,6 +186,9 @@ class DeviceColumns:
         return self
 
 
+_COPY_STREAMS: dict = {}
+
+
 def analyze_many(traces, strict: bool = False, device=None, with_savings: bool = True):
     """Analyse a sequence of host traces (Columns), yielding ``(ColumnarFindings,
     ColumnarSavings | None)`` per trace, in order.  Trace k+1's columns are queued for upload on
@@ -195,7 +199,14 @@ def analyze_many(traces, strict: bool = False, device=None, with_savings: bool =
     just not overlapped)."""
     import torch
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    copy = torch.cuda.Stream(dev)
+    # one copy stream per device for every call: the uploads' blocks come from the caching
+    # allocator's pool of that stream, so a later call reuses them instead of allocating afresh
+    if os.environ.get("B2L_MANY_FRESH_STREAM"):
+        copy = torch.cuda.Stream(dev)
+    else:
+        copy = _COPY_STREAMS.get(dev.index)
+        if copy is None:
+            copy = _COPY_STREAMS[dev.index] = torch.cuda.Stream(dev)
     it = iter(traces)
     nxt = None
     for cols in it:
