@@ -450,9 +450,8 @@ def _analysis_e2e(cols, steps):
     for _ in range(3):  # warm-up with the timed loop's object lifetimes (previous findings alive)
         cfh = analyze_columns(cols, with_savings=True)
         savings_columns(cols, cfh)
-    for _ in range(2):  # (a first timed step once stalled ~0.6 s after a 3-step warm-up)
-        for _ in analyze_many([cols] * max(3, steps // 4)):
-            pass
+    for _ in analyze_many([cols] * 3):
+        pass
     gc.collect()
     gc.disable()
     try:
