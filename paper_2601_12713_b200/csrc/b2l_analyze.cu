@@ -179,6 +179,7 @@ constexpr int FR_MINB_FUSED = B2L_FR_MINB_FUSED;
 #define B2L_FR_BATCH_FUSED 4
 #endif
 constexpr int FR_BATCH_FUSED = B2L_FR_BATCH_FUSED;  // rows whose loads the fused pass issues together
+static_assert(FR_ITEMS % FR_BATCH_FUSED == 0 && FR_ITEMS % 4 == 0, "the load batches tile a thread's items");
 enum : uint32_t { F_BAD = 1, F_H = 2, F_TT = 4, F_AD = 8, F_A = 16, F_TK = 32 };
 struct FrontAcc {
     uint32_t c[FR_NCAT];
