@@ -17,7 +17,8 @@ ap.add_argument("--n", type=int, default=1_000_000)
 ap.add_argument("--iters", type=int, default=6)
 a = ap.parse_args()
 assert os.environ.get("B2L_TRACE") == "ev"
-c = {"c2": c2_trace, "c4": c4_trace}[a.config](a.n)
+from paper_2601_12713_b200.synth import c3_trace  # noqa: E402
+c = {"c2": c2_trace, "c3": c3_trace, "c4": c4_trace}[a.config](a.n)
 cols = DeviceColumns(c)
 for i in range(a.iters):
     if i == a.iters - 1:
