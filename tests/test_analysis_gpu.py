@@ -121,6 +121,10 @@ def test_analyze_many_pipelined_matches_single_calls(cuda):
     assert len(got) == len(traces)
     for cols, (cf, sv) in zip(traces, got):
         assert full_parity(cols, cf, sv) == []
+    # later calls reuse the device's copy stream: a second call, and two generators interleaved
+    g1, g2 = analyze_many(traces[::-1]), analyze_many(traces)
+    for a, b, ca, cb in zip(g1, g2, traces[::-1], traces):
+        assert full_parity(ca, *a) == [] and full_parity(cb, *b) == []
 
 
 def test_fused_savings_packed_records_and_fallback(cuda):
